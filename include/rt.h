@@ -1,0 +1,192 @@
+/* rt.h — C ABI of the B200 segmented-decode serving engine (arxiv 2412.18695).
+ *
+ * The calls follow the paper's problem statement: "A robotic agent submits a
+ * request, along with its time-sensitive requirement in terms of the Expected
+ * Response Time or deadline (ERT in TUF), the tolerance level for missing
+ * deadlines (alpha in TUF), and the time-sensitive degree (beta in TUF)"
+ * (§3); the system "evaluates resource availability whenever the
+ * LLM inference engine completes a decoding iteration" and
+ * "dispatches the generated segment to the corresponding agent for immediate
+ * action".  BASELINE.json fixes the verbs
+ * submit_request(agent, prompt, deadline, utility_fn), step(), poll_segment().
+ *
+ * Conventions
+ *   - Every call returns rt_status (0 = RT_OK, < 0 = error).  No C++ exception
+ *     or longjmp crosses the ABI.  RT_E_CUDA / RT_E_NCCL are sticky: the engine
+ *     is unusable afterwards (only rt_destroy / rt_last_error are valid).
+ *   - Times are int64 microseconds (reading AMB-23).
+ *   - All pointers are HOST pointers unless stated otherwise; the engine copies
+ *     what it needs before returning (caller keeps ownership).
+ *   - One thread per engine; one engine per GPU/process.  rt_step is
+ *     asynchronous except for one small pinned-memory handshake (the round plan).
+ *   - No CPU fallback: rt_create fails with RT_E_CUDA when no sm_100 device is
+ *     present.
+ */
+#ifndef RT_H_
+#define RT_H_
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t rt_status;
+enum {
+  RT_OK = 0,
+  RT_E_INVAL = -1,   /* bad argument (see each call) */
+  RT_E_NOMEM = -2,   /* task table full, request larger than the page pool, HBM exhausted */
+  RT_E_CUDA = -3,    /* CUDA error (sticky) */
+  RT_E_NCCL = -4,    /* NCCL error (sticky) */
+  RT_E_STATE = -5    /* call not valid in the engine's current state */
+};
+
+enum { RT_CLOCK_VIRTUAL = 0, RT_CLOCK_WALL = 1 };
+enum { RT_POLICY_PUD = 0, RT_POLICY_FCFS = 1, RT_POLICY_EDF = 2 };
+/* Stop reasons, in priority order EOS > MAXNEW > SKILL_WINDOW > CAP (DESIGN.md a9). */
+enum { RT_STOP_NONE = 0, RT_STOP_EOS = 1, RT_STOP_MAXNEW = 2, RT_STOP_SKILL = 3, RT_STOP_CAP = 4 };
+/* rt_config.flags */
+enum {
+  RT_FLAG_NO_MODEL = 1,     /* scheduling-only engine: scripted tokens, no forward pass */
+  RT_FLAG_KEEP_LOGITS = 2,  /* materialise fp32 logits of the last round (parity tests) */
+  RT_FLAG_CAPTURE = 4,      /* keep q / attention output (fp32) of layer capture_layer */
+  RT_FLAG_TIMING = 8        /* CUDA-event timing of attention / GEMM launches (rt_stats) */
+};
+
+typedef struct rt_engine rt_engine;
+
+/* Eq. 1 family only: TUF(t) = min(beta, alpha (t - ERT) + beta), alpha <= 0
+ * (SPEC.md:32-35). */
+typedef struct { double alpha, beta; } rt_utility;
+
+typedef struct {
+  /* replicas (BASELINE.json: agents partitioned over GPUs, one allgather per round) */
+  int32_t rank, world;
+  const uint8_t* nccl_id;           /* 128-byte ncclUniqueId (host); NULL when world == 1 */
+  int32_t device;                   /* CUDA device ordinal */
+  /* model shape (Llama-3 family; random init, DESIGN.md AMB-15) */
+  int32_t n_layers, d_model, n_q_heads, n_kv_heads, head_dim, d_ff, vocab;
+  uint64_t weight_seed;
+  float init_std;                   /* 0.02 */
+  /* paged KV pool + tables */
+  int32_t page_tokens;              /* must be 16 */
+  int32_t max_batch;                /* running slots per round */
+  int32_t max_tasks;                /* task-table capacity (<= 2048) */
+  int32_t max_ctx;                  /* prompt + max_new_tokens bound */
+  int32_t n_pages;                  /* KV pages in the pool (0: derive from kv_pool_bytes) */
+  int64_t kv_pool_bytes;
+  int32_t max_rows_per_forward;     /* prefill chunk size (rows), >= max_batch */
+  /* method parameters */
+  int32_t max_seg_tokens;           /* 10, <= 16 */
+  int32_t g_us;                     /* G(s_k) = 90000 */
+  int32_t net_us;                   /* 8000 */
+  int32_t eps_l_us;                 /* 1000 */
+  int32_t speed_window;             /* 5, <= 8 */
+  int32_t max_admit_per_round;      /* AMB-8; <= 0 means unbounded */
+  int32_t policy;                   /* RT_POLICY_* */
+  int32_t clock_mode;               /* RT_CLOCK_* */
+  /* VIRTUAL clock cost model (DESIGN.md AMB-24), integers in microseconds */
+  int32_t base_us, gamma_ppm, kv_us_per_1k, prefill_us_per_tok;
+  int64_t t0_us;
+  /* stop-checker tables [vocab], copied at create (token -> skill id / E_min µs) */
+  const int16_t* tok_skill;
+  const int32_t* tok_exec_min_us;
+  int32_t eos_id;
+  int32_t flags;                    /* RT_FLAG_* */
+  int32_t capture_layer;
+} rt_config;
+
+typedef struct {
+  int64_t request_id;
+  int32_t agent_id, k, tok_begin, tok_end, n_skills, reason;
+  int64_t est_exec_us;              /* sum of E_min over the segment's skills */
+  int64_t dispatch_us;              /* clock at the end of the producing round */
+  int32_t tokens[16];               /* tok_end - tok_begin <= max_seg_tokens valid */
+} rt_segment;
+
+typedef struct {
+  int64_t t_us, round_us;
+  int32_t n_waiting, n_running, n_admitted, n_stopped, n_refused_mem, n_refused_wcet;
+  int32_t n_rows, n_prefill_rows;
+} rt_round_info;
+
+typedef struct {
+  int64_t rounds, tokens, segments, prefill_tokens;
+  double attn_ms, gemm_ms, sched_ms, step_ms;   /* CUDA-event sums (RT_FLAG_TIMING) */
+  int64_t attn_launches, gemm_launches, kernel_launches;
+  double attn_bytes;                            /* algorithmic KV+q+o bytes of timed attention */
+} rt_stats;
+
+/* Create an engine on cfg->device.  Allocates weights (counter-based init on
+ * device), the KV page pool, task table and pinned rings.  Errors:
+ * RT_E_INVAL (shape / limits invalid), RT_E_NOMEM, RT_E_CUDA (no sm_100 GPU),
+ * RT_E_NCCL (world > 1 and communicator init failed). */
+rt_status rt_create(const rt_config* cfg, rt_engine** out);
+rt_status rt_destroy(rt_engine* e);
+
+/* Submit one request.  prompt[n_prompt] token ids; deadline_us = ERT relative to
+ * arrival; fn = (alpha, beta) of Eq. 1; exec_window_us = execution time a
+ * segment must cover before it ends at a skill (0 = end at any skill, the
+ * paper's rule); script[n_script] (optional) = scripted output tokens (then
+ * max_new_tokens := n_script).  request_id_out receives a global id
+ * (local_seq * world + rank).  Errors: RT_E_INVAL for alpha > 0, ERT < 0,
+ * non-finite beta, token ids outside [0, vocab), n_prompt < 1,
+ * n_prompt + max_new_tokens > max_ctx; RT_E_NOMEM for a full task table or a
+ * reservation larger than the pool.  Admission refusal is NOT an error. */
+rt_status rt_submit_request(rt_engine* e, int32_t agent_id, const int32_t* prompt, int32_t n_prompt,
+                            int64_t arrival_us, int64_t deadline_us, rt_utility fn,
+                            int32_t exec_window_us, int32_t max_new_tokens,
+                            const int32_t* script, int32_t n_script, int64_t* request_id_out);
+
+/* One scheduling round + one decoding iteration (DESIGN.md R-ROUND).  now_us is
+ * the round start in WALL mode and ignored in VIRTUAL mode.  info (nullable)
+ * receives the round summary available at return (t_us, n_waiting, n_running,
+ * n_admitted, refusals, n_rows); n_stopped / round_us of this round are
+ * reported by rt_last_round after the next synchronising call. */
+rt_status rt_step(rt_engine* e, int64_t now_us, rt_round_info* info);
+
+/* Drain up to cap segment records produced so far (synchronises with the
+ * device).  n_out receives the number written.  Records come in round order,
+ * slot order within a round. */
+rt_status rt_poll_segment(rt_engine* e, rt_segment* out, int32_t cap, int32_t* n_out);
+
+/* Completed summary of the last executed round (synchronises). */
+rt_status rt_last_round(rt_engine* e, rt_round_info* info);
+
+/* Block until all device work of this engine is complete. */
+rt_status rt_sync(rt_engine* e);
+
+rt_status rt_get_stats(rt_engine* e, rt_stats* out);
+rt_status rt_reset_stats(rt_engine* e);
+
+/* Parity-test dumps (synchronise).  bytes_out receives the size needed; a
+ * NULL dst only queries the size.
+ *   RT_DUMP_TASKS       int64 per task slot: [rid, state, k, ctx, n_pages, n_gen, seg_tok, R]
+ *   RT_DUMP_PAGE_TABLES int32 [max_tasks][pages_per_task]
+ *   RT_DUMP_ROUND       int32: [B, n_rows, n_admitted, free_top, slot_rid_lo[B], tokens[B],
+ *                        argmax[B], admitted_rid_lo[n_admitted]]
+ *   RT_DUMP_LOGITS      fp32 [B][vocab]       (RT_FLAG_KEEP_LOGITS)
+ *   RT_DUMP_HIDDEN      bf16 [B][d_model]     final-normed hidden of the logits rows
+ *   RT_DUMP_CAPTURE_Q   fp32 [n_rows][n_q_heads][head_dim]   (RT_FLAG_CAPTURE)
+ *   RT_DUMP_CAPTURE_O   fp32 [n_rows][n_q_heads][head_dim]
+ *   RT_DUMP_ROWS        int32 [n_rows][3] (task slot, position, token) of the last round
+ *   RT_DUMP_KV_LAYER    bf16 logical [n_pages][2][n_kv_heads][16][head_dim] of capture_layer
+ *   RT_DUMP_FREE_STACK  int32 [free_top]
+ *   RT_DUMP_TASK_SLOTS  int32 [B] task slot of each batch slot of the last round
+ *   RT_DUMP_MERGED      int64 [K][4] merged global top-K (world > 1) */
+enum {
+  RT_DUMP_TASKS = 1, RT_DUMP_PAGE_TABLES = 2, RT_DUMP_ROUND = 3, RT_DUMP_LOGITS = 4,
+  RT_DUMP_HIDDEN = 5, RT_DUMP_CAPTURE_Q = 6, RT_DUMP_CAPTURE_O = 7, RT_DUMP_ROWS = 8,
+  RT_DUMP_KV_LAYER = 9, RT_DUMP_FREE_STACK = 10, RT_DUMP_TASK_SLOTS = 11, RT_DUMP_MERGED = 12
+};
+rt_status rt_debug_dump(rt_engine* e, int32_t what, void* dst, int64_t bytes, int64_t* bytes_out);
+
+/* Human-readable description of the last error (engine may be NULL). */
+const char* rt_last_error(rt_engine* e);
+
+/* Library build / device information string ("sm_100a ..."). */
+const char* rt_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RT_H_ */

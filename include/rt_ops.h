@@ -1,0 +1,70 @@
+/* rt_ops.h — op-level C ABI of the hot-path kernels (per-op parity tests and
+ * microbenchmarks).  Every pointer named d_* is a DEVICE pointer (the caller
+ * owns the allocation, e.g. a torch.cuda tensor); `stream` is a cudaStream_t
+ * (NULL = legacy default stream).  All calls are asynchronous on `stream` and
+ * return rt_status (RT_E_INVAL for bad shapes, RT_E_CUDA on launch failure).
+ *
+ * KV page layout: one layer's pool is
+ *   [n_pages][n_kv_heads][2 (K,V)][16 tokens][head_dim] bf16,
+ * each 16 x head_dim block stored with the 16-byte-chunk XOR swizzle
+ *   phys_chunk = chunk ^ ((tok >> s) & m)   (hd=128/64: s=0, m=7; hd=32: s=1, m=3)
+ * so that one cp.async.bulk of a (page, kv head) lands conflict-free for ldmatrix.
+ */
+#ifndef RT_OPS_H_
+#define RT_OPS_H_
+#include <stdint.h>
+#include "rt.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* a7 paged decode attention (PAPER.md:387 PagedAttention; BASELINE.json
+ * "paged-KV ('context cache') attention decode").  For each row r:
+ *   o[r, h] = softmax(q[r, h] . K[0:seqlen[r]]^T / sqrt(hd)) V[0:seqlen[r]],
+ *   K/V of kv head h / G from pages page_table[row_task[r] * pt_stride + p / 16].
+ * d_q bf16 [n_rows][n_q][hd]; d_out bf16 [n_rows][n_q][hd]; d_out_f32 (nullable)
+ * fp32 same shape; d_ws workspace >= rt_op_attention_ws_bytes(...).
+ * hd in {32, 64, 128}; G = n_q / n_kv in {1..8}. */
+rt_status rt_op_paged_attention(const void* d_q, const void* d_pool, const int32_t* d_page_table,
+                                int32_t pt_stride, const int32_t* d_row_task,
+                                const int32_t* d_row_seqlen, int32_t n_rows, int32_t max_seqlen,
+                                int32_t n_q, int32_t n_kv, int32_t hd, void* d_out, float* d_out_f32,
+                                void* d_ws, int64_t ws_bytes, void* stream);
+int64_t rt_op_attention_ws_bytes(int32_t n_rows, int32_t max_seqlen, int32_t n_q, int32_t hd);
+
+/* Write logical K/V rows into the swizzled pool: row r of d_k / d_v (bf16
+ * [n_rows][n_kv][hd]) goes to token slot d_slot[r] = page * 16 + offset. */
+rt_status rt_op_kv_write(void* d_pool, const void* d_k, const void* d_v, const int32_t* d_slot,
+                         int32_t n_rows, int32_t n_kv, int32_t hd, void* stream);
+/* Inverse: read logical [n_pages][2][n_kv][16][hd] bf16 out of the swizzled pool. */
+rt_status rt_op_kv_read(const void* d_pool, void* d_out, int32_t n_pages, int32_t n_kv, int32_t hd,
+                        void* stream);
+
+/* a6 dense projection on tcgen05 (UMMA 128 x BN x 16, TMEM accumulator, TMA SW128):
+ *   d_out[s][n][m] = sum_{k in split s} W[m, k] * X[n, k]     fp32 partials
+ * d_w bf16 [M][K] row-major, d_x bf16 [N][K] row-major (N rows padded to
+ * n_cap rows allocated), splits >= 1.  K % 64 == 0. */
+rt_status rt_op_gemm(const void* d_w, const void* d_x, float* d_out, int32_t M, int32_t N, int32_t K,
+                     int32_t n_cap, int32_t splits, void* stream);
+
+/* a8 lm_head + greedy argmax (lowest index on ties) over the vocabulary:
+ * d_tok[n] = argmax_m sum_k W[m,k] X[n,k]; d_logits (nullable) fp32 [N][M]. */
+rt_status rt_op_lm_argmax(const void* d_w, const void* d_x, int32_t M, int32_t N, int32_t K,
+                          int32_t n_cap, int32_t* d_tok, float* d_logits, void* d_ws,
+                          int64_t ws_bytes, void* stream);
+
+/* Counter-based init (DESIGN.md AMB-15): d_out bf16 [n] holds the weights of
+ * tensor_id at flat indices [0, n). */
+rt_status rt_op_init_weights(void* d_out, int64_t n, uint64_t seed, int32_t tensor_id, float sigma,
+                             void* stream);
+
+/* a2 Eq. 4 priority for n tasks (fp64, fixed op order). */
+rt_status rt_op_priority(const int64_t* d_t_ref_d_ert /* [n][4]: t, ref, D, ERT */,
+                         const int32_t* d_k, const double* d_alpha, const double* d_beta, int32_t n,
+                         int32_t g_us, int32_t net_us, int32_t eps_l_us, double* d_pri, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RT_OPS_H_ */

@@ -1,0 +1,108 @@
+// common.cuh — device helpers shared by the sm_100a kernels of the engine.
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#define RT_DEV __device__ __forceinline__
+
+typedef __nv_bfloat16 bf16;
+
+// ---------------------------------------------------------------- bf16 helpers
+RT_DEV float bf16_lo(uint32_t v) { return __uint_as_float(v << 16); }
+RT_DEV float bf16_hi(uint32_t v) { return __uint_as_float(v & 0xFFFF0000u); }
+RT_DEV uint16_t f32_to_bf16_bits(float f) {  // RNE (finite inputs)
+  return __bfloat16_as_ushort(__float2bfloat16_rn(f));
+}
+RT_DEV uint32_t pack_bf16x2(float lo, float hi) {
+  return (uint32_t)f32_to_bf16_bits(lo) | ((uint32_t)f32_to_bf16_bits(hi) << 16);
+}
+RT_DEV float bf16_round(float f) { return __bfloat162float(__float2bfloat16_rn(f)); }
+
+// ------------------------------------------------------------- warp utilities
+RT_DEV float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+RT_DEV float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// --------------------------------------------------------------- PTX wrappers
+RT_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+RT_DEV void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+RT_DEV void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+RT_DEV void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+RT_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+RT_DEV void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+RT_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n\t"
+      "DONE_%=:\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// 1-D bulk async copy global -> shared (TMA engine, no tensor map): SASS UBLKCP
+RT_DEV void bulk_g2s(void* smem_dst, const void* gmem_src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(smem_dst)),
+      "l"(gmem_src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+RT_DEV void ldmatrix_x4(uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3, uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+RT_DEV void ldmatrix_x4_trans(uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3, uint32_t addr) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+// D(16x8 f32) += A(16x16 bf16, row) * B(16x8 bf16, col)
+RT_DEV void mma_bf16_16816(float* d, const uint32_t* a, const uint32_t* b) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+
+// ------------------------------------------------------- KV page swizzle
+// A (page, kv head) block: [2 (K,V)][16 tok][hd] bf16; inside a 16 x hd matrix the
+// 16-byte chunk c of token row j is stored at chunk c ^ ((j >> s) & m).
+template <int HD>
+struct KvSwz {
+  static constexpr int CR = HD / 8;                 // 16B chunks per row
+  static constexpr int M = (CR >= 8 ? 8 : CR) - 1;  // xor mask
+  static constexpr int S = (CR >= 8 ? 0 : (CR == 4 ? 1 : 2));
+  static constexpr int ROW_BYTES = HD * 2;
+  static constexpr int MAT_BYTES = 16 * ROW_BYTES;  // one K or V matrix
+  static constexpr int BLOCK_BYTES = 2 * MAT_BYTES; // K + V of one (page, head)
+  RT_DEV static int chunk_off(int j, int c) { return j * ROW_BYTES + ((c ^ ((j >> S) & M)) << 4); }
+  // byte offset of element (j, d) inside a K or V matrix
+  RT_DEV static int elem_off(int j, int d) { return chunk_off(j, d >> 3) + ((d & 7) << 1); }
+};
+
+__host__ __device__ inline int kv_swz_chunk(int hd, int j, int c) {
+  int cr = hd / 8;
+  int m = (cr >= 8 ? 8 : cr) - 1;
+  int s = (cr >= 8 ? 0 : (cr == 4 ? 1 : 2));
+  return c ^ ((j >> s) & m);
+}

@@ -1,0 +1,900 @@
+// engine.cu — host runtime behind the C ABI (include/rt.h).
+//
+// One engine per GPU/process.  A round (rt_step) is, on one CUDA stream:
+//   [H2D staged submissions + apply kernel] -> sched_pre (1 CTA) -> plan handshake
+//   (the only host sync: 1 small mapped-memory read) -> forward pass over the
+//   round's rows (prefill chunks + decode rows) -> lm_head+argmax -> sched_post.
+// With world > 1 the per-rank top-K candidates are allgathered with NCCL on a
+// side stream and merged on device (BASELINE.json: "one NCCL allgather over
+// NVLink per scheduling round").
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+#include <algorithm>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "rt.h"
+#include "internal.h"
+#include "model.h"
+
+using namespace rt;
+static_assert(sizeof(SegRec) == sizeof(rt_segment), "segment record layout");
+
+namespace rt {
+void launch_merge_cand(const double* all, int world, double* merged, cudaStream_t s);
+}
+
+// ----------------------------------------------------------------- NCCL (dlopen)
+typedef struct { char internal[128]; } nccl_uid_t;
+typedef void* nccl_comm_t;
+typedef int (*pfn_comm_init_rank)(nccl_comm_t*, int, nccl_uid_t, int);
+typedef int (*pfn_all_gather)(const void*, void*, size_t, int, nccl_comm_t, cudaStream_t);
+typedef int (*pfn_comm_destroy)(nccl_comm_t);
+typedef const char* (*pfn_get_error_string)(int);
+struct NcclApi {
+  void* h = nullptr;
+  pfn_comm_init_rank init = nullptr;
+  pfn_all_gather allgather = nullptr;
+  pfn_comm_destroy destroy = nullptr;
+  pfn_get_error_string errstr = nullptr;
+  bool load() {
+    if (h) return true;
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    for (const char* n : names) {
+      h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+      if (h) break;
+    }
+    if (!h) return false;
+    init = (pfn_comm_init_rank)dlsym(h, "ncclCommInitRank");
+    allgather = (pfn_all_gather)dlsym(h, "ncclAllGather");
+    destroy = (pfn_comm_destroy)dlsym(h, "ncclCommDestroy");
+    errstr = (pfn_get_error_string)dlsym(h, "ncclGetErrorString");
+    return init && allgather && destroy;
+  }
+};
+static NcclApi g_nccl;
+static const int kNcclFloat64 = 8;
+
+struct LayerW {
+  bf16 *qkv, *o, *gu, *d;
+  TmaMap m_qkv, m_o, m_gu, m_d;
+};
+
+struct rt_engine {
+  rt_config cfg{};
+  std::vector<int16_t> tok_skill;
+  std::vector<int32_t> tok_exec;
+  int qkv_dim = 0, pt_stride = 0, rows_cap = 0, fwd_rows = 0, part_rows = 0;
+  int64_t pool_layer_bytes = 0;
+  cudaStream_t stream = nullptr, side = nullptr;
+  cudaEvent_t ev_plan = nullptr, ev_post = nullptr, ev_cand = nullptr, ev_merge = nullptr;
+  bool post_pending = false, merge_pending = false;
+  // weights
+  void* d_wbuf = nullptr;
+  bf16 *emb = nullptr, *lm = nullptr;
+  std::vector<LayerW> layers;
+  TmaMap m_lm;
+  // KV pool
+  unsigned char* d_pool = nullptr;
+  // scheduler state
+  TaskTable tt{};
+  std::vector<void*> allocs;
+  DevState* d_st = nullptr;
+  HostMailbox* h_mb = nullptr;
+  HostMailbox* d_mb = nullptr;
+  SegRec* h_ring = nullptr;
+  SegRec* d_ring = nullptr;
+  int64_t ring_cap = 65536;
+  SchedParams sp{};
+  // activations
+  float *d_x = nullptr, *d_part = nullptr, *d_attn_ws = nullptr, *d_logits = nullptr, *d_am_val = nullptr;
+  int32_t* d_am_idx = nullptr;
+  bf16 *d_h = nullptr, *d_q = nullptr, *d_o = nullptr, *d_act = nullptr, *d_hfin = nullptr;
+  float *d_cap_q = nullptr, *d_cap_o = nullptr, *d_rope_cos = nullptr, *d_rope_sin = nullptr;
+  int64_t attn_ws_cap = 0;
+  GemmTmaSet x_h, x_o, x_act, x_hfin;
+  // submissions
+  SubmitRec* h_recs = nullptr;
+  int32_t* h_toks = nullptr;
+  SubmitRec* d_recs = nullptr;
+  int32_t* d_toks = nullptr;
+  int n_staged = 0, recs_cap = 0;
+  int64_t toks_staged = 0, toks_cap = 0;
+  std::vector<int> free_slots;
+  std::unordered_map<int64_t, int> rid_slot;
+  int64_t n_submitted = 0;
+  int64_t seg_read = 0;
+  HostMailbox plan{};
+  // timing
+  std::vector<cudaEvent_t> ev_attn;  // 2 per layer
+  cudaEvent_t ev_f0 = nullptr, ev_f1 = nullptr, ev_s0 = nullptr, ev_s1 = nullptr, ev_q1 = nullptr;
+  bool timing_pending = false;
+  int timing_layers = 0;
+  double attn_bytes_pending = 0.0;
+  rt_stats stats{};
+  // nccl
+  nccl_comm_t comm = nullptr;
+  double *d_cand_all = nullptr, *d_merged = nullptr;
+  // errors
+  bool sticky = false;
+  std::string err;
+};
+
+static std::string g_last_err;
+
+static rt_status fail(rt_engine* e, rt_status code, const std::string& msg) {
+  if (e) {
+    e->err = msg;
+    if (code == RT_E_CUDA || code == RT_E_NCCL) e->sticky = true;
+  }
+  g_last_err = msg;
+  return code;
+}
+
+#define CK(e, x)                                                                       \
+  do {                                                                                 \
+    cudaError_t _r = (x);                                                              \
+    if (_r != cudaSuccess)                                                             \
+      return fail(e, RT_E_CUDA, std::string(#x) + ": " + cudaGetErrorString(_r));       \
+  } while (0)
+
+template <typename T>
+static cudaError_t dalloc(rt_engine* e, T** p, size_t n) {
+  void* q = nullptr;
+  cudaError_t r = cudaMalloc(&q, std::max<size_t>(n * sizeof(T), 16));
+  if (r == cudaSuccess) {
+    e->allocs.push_back(q);
+    cudaMemset(q, 0, std::max<size_t>(n * sizeof(T), 16));
+    *p = (T*)q;
+  }
+  return r;
+}
+
+extern "C" const char* rt_version(void) {
+  return "paper_2412_18695_b200 rt 0.1 (sm_100a: tcgen05 GEMM, bulk-copy paged attention, device scheduler)";
+}
+
+extern "C" const char* rt_last_error(rt_engine* e) { return e ? e->err.c_str() : g_last_err.c_str(); }
+
+// ------------------------------------------------------------------ create
+static rt_status validate(const rt_config* c) {
+  if (!c) return RT_E_INVAL;
+  if (c->page_tokens != 16) return RT_E_INVAL;
+  if (c->max_batch < 1 || c->max_batch > 1024) return RT_E_INVAL;
+  if (c->max_tasks < 1 || c->max_tasks > kMaxTasks) return RT_E_INVAL;
+  if (c->max_ctx < 2) return RT_E_INVAL;
+  if (c->max_seg_tokens < 1 || c->max_seg_tokens > kMaxSegTok) return RT_E_INVAL;
+  if (c->speed_window < 1 || c->speed_window > 8) return RT_E_INVAL;
+  if (c->g_us <= 0 || c->eps_l_us <= 0 || c->net_us < 0) return RT_E_INVAL;
+  if (c->policy < 0 || c->policy > 2 || c->clock_mode < 0 || c->clock_mode > 1) return RT_E_INVAL;
+  if (c->vocab < 2 || !c->tok_skill || !c->tok_exec_min_us) return RT_E_INVAL;
+  if (c->eos_id < 0 || c->eos_id >= c->vocab) return RT_E_INVAL;
+  if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return RT_E_INVAL;
+  if (!(c->flags & RT_FLAG_NO_MODEL)) {
+    if (c->n_layers < 1 || c->d_model % 64 || c->d_ff % 64 || c->n_q_heads < 1 || c->n_kv_heads < 1) return RT_E_INVAL;
+    if (c->n_q_heads % c->n_kv_heads || c->n_q_heads / c->n_kv_heads > 8) return RT_E_INVAL;
+    if (c->head_dim != 32 && c->head_dim != 64 && c->head_dim != 128) return RT_E_INVAL;
+    if ((c->n_q_heads * c->head_dim) % 64) return RT_E_INVAL;
+  }
+  return RT_OK;
+}
+
+static rt_status create_impl(rt_engine* e, const rt_config* cfg);
+
+extern "C" rt_status rt_create(const rt_config* cfg, rt_engine** out) {
+  if (!out) return RT_E_INVAL;
+  *out = nullptr;
+  rt_status v = validate(cfg);
+  if (v != RT_OK) return fail(nullptr, v, "invalid rt_config");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev <= cfg->device)
+    return fail(nullptr, RT_E_CUDA, "no CUDA device (this library has no CPU fallback)");
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, cfg->device) != cudaSuccess || prop.major != 10)
+    return fail(nullptr, RT_E_CUDA, "an sm_100 (B200) device is required");
+  rt_engine* e = new rt_engine();
+  rt_status s = create_impl(e, cfg);
+  if (s != RT_OK) {
+    g_last_err = e->err;
+    rt_destroy(e);
+    return s;
+  }
+  *out = e;
+  return RT_OK;
+}
+
+static rt_status create_impl(rt_engine* e, const rt_config* cfg) {
+  e->cfg = *cfg;
+  const rt_config& c = e->cfg;
+  e->tok_skill.assign(cfg->tok_skill, cfg->tok_skill + cfg->vocab);
+  e->tok_exec.assign(cfg->tok_exec_min_us, cfg->tok_exec_min_us + cfg->vocab);
+  e->cfg.tok_skill = nullptr;
+  e->cfg.tok_exec_min_us = nullptr;
+  e->cfg.nccl_id = nullptr;
+  if (e->cfg.max_admit_per_round <= 0) e->cfg.max_admit_per_round = 1 << 30;
+  if (e->cfg.max_rows_per_forward < c.max_batch) e->cfg.max_rows_per_forward = std::max(c.max_batch, 2048);
+  const bool model = !(c.flags & RT_FLAG_NO_MODEL);
+  auto done = [&](rt_status s) { return s; };
+  if (cudaSetDevice(c.device) != cudaSuccess) return done(fail(e, RT_E_CUDA, "cudaSetDevice"));
+  if (cudaStreamCreateWithFlags(&e->stream, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking) != cudaSuccess)
+    return done(fail(e, RT_E_CUDA, "stream create"));
+  cudaEventCreateWithFlags(&e->ev_plan, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&e->ev_post, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&e->ev_cand, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&e->ev_merge, cudaEventDisableTiming);
+  cudaEventCreate(&e->ev_f0);
+  cudaEventCreate(&e->ev_f1);
+  cudaEventCreate(&e->ev_s0);
+  cudaEventCreate(&e->ev_s1);
+  cudaEventCreate(&e->ev_q1);
+
+  e->pt_stride = (c.max_ctx + 15) / 16;
+  e->rows_cap = c.max_batch * c.max_ctx;
+  e->fwd_rows = e->cfg.max_rows_per_forward;
+  const int d = c.d_model, hd = c.head_dim, nq = c.n_q_heads, nkv = c.n_kv_heads, L = c.n_layers;
+  e->qkv_dim = (nq + 2 * nkv) * hd;
+
+  // ---- page pool
+  int n_pages = c.n_pages;
+  const int64_t page_bytes_all_layers = model ? (int64_t)L * nkv * 64 * hd : 0;
+  if (n_pages <= 0) {
+    if (!model || c.kv_pool_bytes <= 0) return done(fail(e, RT_E_INVAL, "n_pages or kv_pool_bytes required"));
+    n_pages = (int)std::min<int64_t>(c.kv_pool_bytes / page_bytes_all_layers, INT32_MAX / 2);
+  }
+  if (n_pages < 1) return done(fail(e, RT_E_INVAL, "empty page pool"));
+  e->cfg.n_pages = n_pages;
+
+  // ---- task table
+  TaskTable& T = e->tt;
+  const int MT = c.max_tasks;
+#define A(f, n) CK(e, dalloc(e, &T.f, (size_t)(n)))
+  A(rid, MT); A(arrival, MT); A(ert, MT); A(D, MT); A(ref, MT); A(end_est, MT); A(seg_exec, MT);
+  A(alpha, MT); A(beta, MT); A(pri, MT);
+  A(state, MT); A(agent, MT); A(k, MT); A(n_prompt, MT); A(max_new, MT); A(window, MT); A(scripted, MT);
+  A(n_gen, MT); A(seg_tok, MT); A(n_skills, MT); A(pending, MT); A(ctx, MT); A(n_pages, MT); A(R, MT);
+  A(holder, MT); A(argmax_last, MT);
+  A(page_table, (size_t)MT * e->pt_stride);
+  A(prompt, (size_t)MT * c.max_ctx);
+  A(script, (size_t)MT * c.max_ctx);
+  A(out, (size_t)MT * c.max_ctx);
+#undef A
+  {
+    std::vector<int32_t> fs(MT, T_FREE);
+    CK(e, cudaMemcpy(T.state, fs.data(), MT * 4, cudaMemcpyHostToDevice));
+  }
+  SchedParams& P = e->sp;
+  CK(e, dalloc(e, &e->d_st, 1));
+  {
+    DevState st{};
+    st.t = c.t0_us;
+    st.free_top = n_pages;
+    CK(e, cudaMemcpy(e->d_st, &st, sizeof(st), cudaMemcpyHostToDevice));
+  }
+  CK(e, cudaHostAlloc((void**)&e->h_mb, sizeof(HostMailbox), cudaHostAllocMapped));
+  memset(e->h_mb, 0, sizeof(HostMailbox));
+  CK(e, cudaHostGetDevicePointer((void**)&e->d_mb, e->h_mb, 0));
+  CK(e, cudaHostAlloc((void**)&e->h_ring, sizeof(SegRec) * e->ring_cap, cudaHostAllocMapped));
+  CK(e, cudaHostGetDevicePointer((void**)&e->d_ring, e->h_ring, 0));
+  CK(e, dalloc(e, &P.free_stack, n_pages));
+  launch_init_free_stack(P.free_stack, n_pages, e->stream);
+  CK(e, dalloc(e, &P.slot_task, c.max_batch));
+  CK(e, dalloc(e, &P.round_slots, c.max_batch));
+  CK(e, dalloc(e, &P.slot_is_prefill, c.max_batch));
+  CK(e, dalloc(e, &P.slot_row, c.max_batch));
+  CK(e, dalloc(e, &P.admitted, c.max_batch));
+  CK(e, dalloc(e, &P.row_task, e->rows_cap));
+  CK(e, dalloc(e, &P.row_pos, e->rows_cap));
+  CK(e, dalloc(e, &P.row_tok, e->rows_cap));
+  CK(e, dalloc(e, &P.argmax_tok, c.max_batch));
+  CK(e, dalloc(e, &P.slot_tok, c.max_batch));
+  CK(e, dalloc(e, &P.popped, 2 * ((size_t)n_pages + c.max_batch)));
+  CK(e, dalloc(e, &P.cand, kTopK * 4));
+  int16_t* d_skill;
+  int32_t* d_exec;
+  CK(e, dalloc(e, &d_skill, c.vocab));
+  CK(e, dalloc(e, &d_exec, c.vocab));
+  CK(e, cudaMemcpy(d_skill, e->tok_skill.data(), c.vocab * 2, cudaMemcpyHostToDevice));
+  CK(e, cudaMemcpy(d_exec, e->tok_exec.data(), c.vocab * 4, cudaMemcpyHostToDevice));
+  P.tt = T;
+  P.st = e->d_st;
+  P.mb = e->d_mb;
+  P.seg_ring = e->d_ring;
+  P.seg_ring_cap = e->ring_cap;
+  P.tok_skill = d_skill;
+  P.tok_exec = d_exec;
+  P.max_tasks = MT;
+  P.max_batch = c.max_batch;
+  P.max_ctx = c.max_ctx;
+  P.pt_stride = e->pt_stride;
+  P.n_pages = n_pages;
+  P.page_tokens = 16;
+  P.rows_cap = e->rows_cap;
+  P.max_seg_tokens = c.max_seg_tokens;
+  P.g_us = c.g_us;
+  P.net_us = c.net_us;
+  P.eps_l_us = c.eps_l_us;
+  P.speed_window = c.speed_window;
+  P.max_admit = e->cfg.max_admit_per_round;
+  P.policy = c.policy;
+  P.clock_mode = c.clock_mode;
+  P.base_us = c.base_us;
+  P.gamma_ppm = c.gamma_ppm;
+  P.kv_us_per_1k = c.kv_us_per_1k;
+  P.prefill_us_per_tok = c.prefill_us_per_tok;
+  P.eos_id = c.eos_id;
+  P.rank = c.rank;
+  P.world = c.world;
+  P.no_model = model ? 0 : 1;
+
+  // ---- submission staging (pinned)
+  e->recs_cap = std::min(MT, 1024);
+  e->toks_cap = (int64_t)std::max(4 * c.max_ctx, 1 << 20);
+  CK(e, cudaHostAlloc((void**)&e->h_recs, sizeof(SubmitRec) * e->recs_cap, cudaHostAllocDefault));
+  CK(e, cudaHostAlloc((void**)&e->h_toks, 4 * e->toks_cap, cudaHostAllocDefault));
+  CK(e, dalloc(e, &e->d_recs, e->recs_cap));
+  CK(e, dalloc(e, &e->d_toks, e->toks_cap));
+  for (int i = MT - 1; i >= 0; --i) e->free_slots.push_back(i);
+
+  // ---- model
+  if (model) {
+    const int ff = c.d_ff, V = c.vocab;
+    const size_t n_emb = (size_t)V * d, n_qkv = (size_t)e->qkv_dim * d, n_o = (size_t)d * nq * hd,
+                 n_gu = (size_t)2 * ff * d, n_d = (size_t)d * ff;
+    const size_t total = 2 * n_emb + L * (n_qkv + n_o + n_gu + n_d);
+    if (cudaMalloc(&e->d_wbuf, total * 2) != cudaSuccess) return done(fail(e, RT_E_NOMEM, "weights do not fit in HBM"));
+    bf16* w = (bf16*)e->d_wbuf;
+    const float sig = c.init_std > 0 ? c.init_std : 0.02f;
+    e->emb = w;
+    w += n_emb;
+    e->lm = w;
+    w += n_emb;
+    launch_init_weights(e->emb, n_emb, c.weight_seed, 0, sig, e->stream);
+    launch_init_weights(e->lm, n_emb, c.weight_seed, 1, sig, e->stream);
+    e->layers.resize(L);
+    for (int l = 0; l < L; ++l) {
+      LayerW& lw = e->layers[l];
+      lw.qkv = w; w += n_qkv;
+      lw.o = w; w += n_o;
+      lw.gu = w; w += n_gu;
+      lw.d = w; w += n_d;
+      launch_init_weights(lw.qkv, n_qkv, c.weight_seed, 16 + 8 * l + 0, sig, e->stream);
+      launch_init_weights(lw.o, n_o, c.weight_seed, 16 + 8 * l + 1, sig, e->stream);
+      launch_init_weights(lw.gu, n_gu, c.weight_seed, 16 + 8 * l + 2, sig, e->stream);
+      launch_init_weights(lw.d, n_d, c.weight_seed, 16 + 8 * l + 3, sig, e->stream);
+      bool ok = make_tma_2d_bf16(&lw.m_qkv, lw.qkv, d, e->qkv_dim, 64, 128) &&
+                make_tma_2d_bf16(&lw.m_o, lw.o, nq * hd, d, 64, 128) &&
+                make_tma_2d_bf16(&lw.m_gu, lw.gu, d, 2 * ff, 64, 128) &&
+                make_tma_2d_bf16(&lw.m_d, lw.d, ff, d, 64, 128);
+      if (!ok) return done(fail(e, RT_E_CUDA, "cuTensorMapEncodeTiled failed (weights)"));
+    }
+    if (!make_tma_2d_bf16(&e->m_lm, e->lm, d, V, 64, 128)) return done(fail(e, RT_E_CUDA, "tensor map lm_head"));
+    // KV pool
+    e->pool_layer_bytes = (int64_t)n_pages * nkv * 64 * hd;
+    if (cudaMalloc(&e->d_pool, (size_t)e->pool_layer_bytes * L) != cudaSuccess)
+      return done(fail(e, RT_E_NOMEM, "KV pool does not fit in HBM"));
+    CK(e, cudaMemsetAsync(e->d_pool, 0, (size_t)e->pool_layer_bytes * L, e->stream));
+    // activations (one forward chunk of fwd_rows rows)
+    const int R = e->fwd_rows;
+    e->part_rows = std::max(R, 16 * c.max_batch);
+    const int max_out = std::max(std::max(e->qkv_dim, d), 2 * ff);
+    CK(e, dalloc(e, &e->d_x, (size_t)R * d));
+    CK(e, dalloc(e, &e->d_h, (size_t)R * d));
+    CK(e, dalloc(e, &e->d_q, (size_t)R * nq * hd));
+    CK(e, dalloc(e, &e->d_o, (size_t)R * nq * hd));
+    CK(e, dalloc(e, &e->d_act, (size_t)R * ff));
+    CK(e, dalloc(e, &e->d_part, (size_t)e->part_rows * max_out));
+    CK(e, dalloc(e, &e->d_hfin, (size_t)c.max_batch * d));
+    const int mt = (V + 127) / 128;
+    CK(e, dalloc(e, &e->d_am_val, (size_t)mt * c.max_batch));
+    CK(e, dalloc(e, &e->d_am_idx, (size_t)mt * c.max_batch));
+    if (c.flags & RT_FLAG_KEEP_LOGITS) CK(e, dalloc(e, &e->d_logits, (size_t)c.max_batch * V));
+    e->attn_ws_cap = (int64_t)(148 * 8 + (int64_t)R * nkv) * 8 * (hd + 2) * 2;
+    CK(e, dalloc(e, &e->d_attn_ws, (size_t)e->attn_ws_cap));
+    if (c.flags & RT_FLAG_CAPTURE) {
+      CK(e, dalloc(e, &e->d_cap_q, (size_t)e->rows_cap * nq * hd));
+      CK(e, dalloc(e, &e->d_cap_o, (size_t)e->rows_cap * nq * hd));
+    }
+    // RoPE tables (rotate-half, theta 500000), fp64 on host -> fp32
+    std::vector<float> cs((size_t)c.max_ctx * hd / 2), sn((size_t)c.max_ctx * hd / 2);
+    for (int p = 0; p < c.max_ctx; ++p)
+      for (int i = 0; i < hd / 2; ++i) {
+        const double inv = pow(500000.0, -2.0 * i / hd);
+        const double ang = (double)p * inv;
+        cs[(size_t)p * hd / 2 + i] = (float)cos(ang);
+        sn[(size_t)p * hd / 2 + i] = (float)sin(ang);
+      }
+    CK(e, dalloc(e, &e->d_rope_cos, cs.size()));
+    CK(e, dalloc(e, &e->d_rope_sin, sn.size()));
+    CK(e, cudaMemcpy(e->d_rope_cos, cs.data(), cs.size() * 4, cudaMemcpyHostToDevice));
+    CK(e, cudaMemcpy(e->d_rope_sin, sn.data(), sn.size() * 4, cudaMemcpyHostToDevice));
+    bool ok = make_gemm_act_maps(&e->x_h, e->d_h, d, R) && make_gemm_act_maps(&e->x_o, e->d_o, nq * hd, R) &&
+              make_gemm_act_maps(&e->x_act, e->d_act, ff, R) &&
+              make_gemm_act_maps(&e->x_hfin, e->d_hfin, d, c.max_batch);
+    if (!ok) return done(fail(e, RT_E_CUDA, "cuTensorMapEncodeTiled failed (activations)"));
+    e->ev_attn.resize(2 * L);
+    for (auto& ev : e->ev_attn) cudaEventCreate(&ev);
+  }
+  // ---- replicas: NCCL communicator (one allgather of top-K candidates per round)
+  if (c.world > 1) {
+    if (!cfg->nccl_id) return done(fail(e, RT_E_INVAL, "nccl_id required when world > 1"));
+    if (!g_nccl.load()) return done(fail(e, RT_E_NCCL, "libnccl.so.2 not loadable"));
+    nccl_uid_t uid;
+    memcpy(uid.internal, cfg->nccl_id, 128);
+    int r = g_nccl.init(&e->comm, c.world, uid, c.rank);
+    if (r != 0) return done(fail(e, RT_E_NCCL, std::string("ncclCommInitRank: ") + (g_nccl.errstr ? g_nccl.errstr(r) : "?")));
+    CK(e, dalloc(e, &e->d_cand_all, (size_t)c.world * kTopK * 4));
+    CK(e, dalloc(e, &e->d_merged, (size_t)kTopK * 4));
+  }
+  CK(e, cudaStreamSynchronize(e->stream));
+  CK(e, cudaGetLastError());
+  return done(RT_OK);
+}
+
+extern "C" rt_status rt_destroy(rt_engine* e) {
+  if (!e) return RT_OK;
+  if (e->stream) cudaStreamSynchronize(e->stream);
+  if (e->side) cudaStreamSynchronize(e->side);
+  if (e->comm && g_nccl.destroy) g_nccl.destroy(e->comm);
+  for (void* p : e->allocs) cudaFree(p);
+  if (e->d_wbuf) cudaFree(e->d_wbuf);
+  if (e->d_pool) cudaFree(e->d_pool);
+  if (e->h_mb) cudaFreeHost(e->h_mb);
+  if (e->h_ring) cudaFreeHost(e->h_ring);
+  if (e->h_recs) cudaFreeHost(e->h_recs);
+  if (e->h_toks) cudaFreeHost(e->h_toks);
+  for (auto ev : e->ev_attn) cudaEventDestroy(ev);
+  cudaEvent_t evs[] = {e->ev_plan, e->ev_post, e->ev_cand, e->ev_merge, e->ev_f0, e->ev_f1, e->ev_s0, e->ev_s1, e->ev_q1};
+  for (auto ev : evs)
+    if (ev) cudaEventDestroy(ev);
+  if (e->stream) cudaStreamDestroy(e->stream);
+  if (e->side) cudaStreamDestroy(e->side);
+  delete e;
+  return RT_OK;
+}
+
+// ------------------------------------------------------------------ submit
+static rt_status flush_staging(rt_engine* e) {
+  if (e->n_staged == 0) return RT_OK;
+  CK(e, cudaMemcpyAsync(e->d_recs, e->h_recs, sizeof(SubmitRec) * e->n_staged, cudaMemcpyHostToDevice, e->stream));
+  if (e->toks_staged)
+    CK(e, cudaMemcpyAsync(e->d_toks, e->h_toks, 4 * e->toks_staged, cudaMemcpyHostToDevice, e->stream));
+  launch_apply_submits(e->sp, e->d_recs, e->d_toks, e->n_staged, e->stream);
+  e->n_staged = 0;
+  e->toks_staged = 0;
+  return RT_OK;
+}
+
+extern "C" rt_status rt_submit_request(rt_engine* e, int32_t agent_id, const int32_t* prompt, int32_t n_prompt,
+                                       int64_t arrival_us, int64_t deadline_us, rt_utility fn,
+                                       int32_t exec_window_us, int32_t max_new_tokens, const int32_t* script,
+                                       int32_t n_script, int64_t* request_id_out) {
+  if (!e) return RT_E_INVAL;
+  if (e->sticky) return RT_E_CUDA;
+  const rt_config& c = e->cfg;
+  if (!(fn.alpha <= 0.0) || deadline_us < 0 || !isfinite(fn.beta) || exec_window_us < 0 || agent_id < 0)
+    return fail(e, RT_E_INVAL, "bad utility function / agent");
+  if (!prompt || n_prompt < 1) return fail(e, RT_E_INVAL, "empty prompt");
+  for (int i = 0; i < n_prompt; ++i)
+    if (prompt[i] < 0 || prompt[i] >= c.vocab) return fail(e, RT_E_INVAL, "prompt token out of range");
+  const bool scripted = script != nullptr;
+  if (scripted) {
+    if (n_script < 1) return fail(e, RT_E_INVAL, "empty script");
+    for (int i = 0; i < n_script; ++i)
+      if (script[i] < 0 || script[i] >= c.vocab) return fail(e, RT_E_INVAL, "script token out of range");
+    max_new_tokens = n_script;
+  } else if (c.flags & RT_FLAG_NO_MODEL) {
+    return fail(e, RT_E_INVAL, "engine without model needs scripted requests");
+  }
+  if (max_new_tokens < 1 || (int64_t)n_prompt + max_new_tokens > c.max_ctx)
+    return fail(e, RT_E_INVAL, "n_prompt + max_new_tokens > max_ctx");
+  const int R = (n_prompt + max_new_tokens + 15) / 16;
+  if (R > c.n_pages) return fail(e, RT_E_NOMEM, "request larger than the page pool");
+  if (e->free_slots.empty()) return fail(e, RT_E_NOMEM, "task table full");
+  const int64_t need = (int64_t)n_prompt + (scripted ? n_script : 0);
+  if (e->n_staged >= e->recs_cap || e->toks_staged + need > e->toks_cap) {
+    rt_status s = flush_staging(e);
+    if (s != RT_OK) return s;
+    CK(e, cudaStreamSynchronize(e->stream));
+  }
+  const int slot = e->free_slots.back();
+  e->free_slots.pop_back();
+  SubmitRec& r = e->h_recs[e->n_staged++];
+  r.rid = e->n_submitted * c.world + c.rank;
+  e->n_submitted++;
+  r.arrival = arrival_us;
+  r.ert = deadline_us;
+  r.alpha = fn.alpha;
+  r.beta = fn.beta;
+  r.slot = slot;
+  r.agent = agent_id;
+  r.n_prompt = n_prompt;
+  r.max_new = max_new_tokens;
+  r.window = exec_window_us;
+  r.scripted = scripted ? 1 : 0;
+  r.tok_off = e->toks_staged;
+  memcpy(e->h_toks + e->toks_staged, prompt, 4 * (size_t)n_prompt);
+  e->toks_staged += n_prompt;
+  if (scripted) {
+    memcpy(e->h_toks + e->toks_staged, script, 4 * (size_t)n_script);
+    e->toks_staged += n_script;
+  }
+  e->rid_slot[r.rid] = slot;
+  if (request_id_out) *request_id_out = r.rid;
+  return RT_OK;
+}
+
+// ------------------------------------------------------------------ timing
+static void harvest_timing(rt_engine* e) {
+  if (!e->timing_pending) return;
+  float ms = 0.f;
+  for (int l = 0; l < e->timing_layers; ++l) {
+    if (cudaEventElapsedTime(&ms, e->ev_attn[2 * l], e->ev_attn[2 * l + 1]) == cudaSuccess) {
+      e->stats.attn_ms += ms;
+      e->stats.attn_launches++;
+    }
+  }
+  if (cudaEventElapsedTime(&ms, e->ev_s0, e->ev_q1) == cudaSuccess) e->stats.step_ms += ms;
+  if (cudaEventElapsedTime(&ms, e->ev_s0, e->ev_s1) == cudaSuccess) e->stats.sched_ms += ms;
+  if (cudaEventElapsedTime(&ms, e->ev_f1, e->ev_q1) == cudaSuccess) e->stats.sched_ms += ms;
+  if (cudaEventElapsedTime(&ms, e->ev_f0, e->ev_f1) == cudaSuccess) e->stats.gemm_ms += ms;
+  e->stats.attn_bytes += e->attn_bytes_pending;
+  e->timing_pending = false;
+}
+
+// ------------------------------------------------------------------ forward
+static rt_status forward(rt_engine* e, const HostMailbox& plan) {
+  const rt_config& c = e->cfg;
+  const int d = c.d_model, hd = c.head_dim, nq = c.n_q_heads, nkv = c.n_kv_heads, ff = c.d_ff, V = c.vocab;
+  const int B = plan.B, n_rows = plan.n_rows;
+  const bool timing = (c.flags & RT_FLAG_TIMING) != 0;
+  cudaStream_t s = e->stream;
+  SchedParams& P = e->sp;
+  const float sl2 = (float)(1.4426950408889634 / sqrt((double)hd));
+  for (int row0 = 0; row0 < n_rows; row0 += e->fwd_rows) {
+    const int n = std::min(e->fwd_rows, n_rows - row0);
+    const int max_splits = std::max(1, std::min(16, e->part_rows / n));
+    launch_embed_norm(P.row_tok, row0, n, e->emb, d, e->d_x, e->d_h, s);
+    AttnArgs aa{};
+    aa.q = e->d_q;
+    aa.page_table = e->tt.page_table;
+    aa.pt_stride = e->pt_stride;
+    aa.row_task = P.row_task;
+    aa.row_pos = P.row_pos;
+    aa.row_seqlen = nullptr;
+    aa.row0 = row0;
+    aa.n_rows = n;
+    aa.nq = nq;
+    aa.nkv = nkv;
+    aa.hd = hd;
+    aa.G = nq / nkv;
+    attn_plan(n, nkv, plan.max_seqlen, &aa.chunk_pages, &aa.max_chunks);
+    if (attn_ws_floats(n, nq, hd, aa.max_chunks) > e->attn_ws_cap) {
+      aa.chunk_pages = (plan.max_seqlen + 15) / 16;
+      aa.max_chunks = 1;
+    }
+    aa.out = e->d_o;
+    aa.ws = e->d_attn_ws;
+    aa.scale_log2 = sl2;
+    for (int l = 0; l < c.n_layers; ++l) {
+      LayerW& w = e->layers[l];
+      void* pool_l = e->d_pool + (size_t)l * e->pool_layer_bytes;
+      int sp = launch_gemm(w.m_qkv, e->x_h, e->qkv_dim, n, d, e->d_part, max_splits, s);
+      QkvEpiArgs qa{};
+      qa.part = e->d_part;
+      qa.splits = sp;
+      qa.n_rows = n;
+      qa.row0 = row0;
+      qa.row_task = P.row_task;
+      qa.row_pos = P.row_pos;
+      qa.page_table = e->tt.page_table;
+      qa.pt_stride = e->pt_stride;
+      qa.nq = nq;
+      qa.nkv = nkv;
+      qa.hd = hd;
+      qa.rope_cos = e->d_rope_cos;
+      qa.rope_sin = e->d_rope_sin;
+      qa.q_out = e->d_q;
+      qa.pool = pool_l;
+      qa.q_cap = (e->d_cap_q && l == c.capture_layer) ? e->d_cap_q : nullptr;
+      launch_qkv_epilogue(qa, s);
+      aa.pool = pool_l;
+      aa.out_f32 = (e->d_cap_o && l == c.capture_layer) ? e->d_cap_o : nullptr;
+      if (timing && row0 == 0) cudaEventRecord(e->ev_attn[2 * l], s);
+      launch_attention(aa, s);
+      if (timing && row0 == 0) cudaEventRecord(e->ev_attn[2 * l + 1], s);
+      sp = launch_gemm(w.m_o, e->x_o, d, n, nq * hd, e->d_part, max_splits, s);
+      launch_resid_norm(e->d_part, sp, n, d, e->d_x, e->d_h, s);
+      sp = launch_gemm(w.m_gu, e->x_h, 2 * ff, n, d, e->d_part, max_splits, s);
+      launch_swiglu(e->d_part, sp, n, ff, e->d_act, s);
+      sp = launch_gemm(w.m_d, e->x_act, d, n, ff, e->d_part, max_splits, s);
+      launch_resid_norm(e->d_part, sp, n, d, e->d_x, e->d_h, s);
+    }
+    launch_gather_rows(P.slot_row, B, row0, n, e->d_h, d, e->d_hfin, s);
+  }
+  launch_gemm_argmax(e->m_lm, e->x_hfin, V, B, d, e->d_am_val, e->d_am_idx, e->d_logits, s);
+  launch_argmax_reduce(e->d_am_val, e->d_am_idx, (V + 127) / 128, B, P.argmax_tok, s);
+  CK(e, cudaGetLastError());
+  if (timing) e->timing_layers = c.n_layers;
+  return RT_OK;
+}
+
+// -------------------------------------------------------------------- step
+extern "C" rt_status rt_step(rt_engine* e, int64_t now_us, rt_round_info* info) {
+  if (!e) return RT_E_INVAL;
+  if (e->sticky) return RT_E_CUDA;
+  const rt_config& c = e->cfg;
+  cudaStream_t s = e->stream;
+  const bool timing = (c.flags & RT_FLAG_TIMING) != 0;
+  if (e->merge_pending) CK(e, cudaStreamWaitEvent(s, e->ev_merge, 0));
+  if (e->timing_pending) {
+    CK(e, cudaEventSynchronize(e->ev_post));
+    harvest_timing(e);
+  }
+  rt_status st = flush_staging(e);
+  if (st != RT_OK) return st;
+  if (timing) cudaEventRecord(e->ev_s0, s);
+  launch_sched_pre(e->sp, now_us, s);
+  if (timing) cudaEventRecord(e->ev_s1, s);
+  CK(e, cudaEventRecord(e->ev_plan, s));
+  CK(e, cudaEventSynchronize(e->ev_plan));
+  CK(e, cudaGetLastError());
+  const volatile HostMailbox* mb = e->h_mb;
+  HostMailbox plan;
+  memcpy(&plan, (const void*)mb, sizeof(plan));
+  e->plan = plan;
+  if (info) {
+    memset(info, 0, sizeof(*info));
+    info->t_us = plan.t_us;
+    info->round_us = plan.round_us;
+    info->n_waiting = plan.n_waiting;
+    info->n_running = plan.idle ? 0 : plan.B;
+    info->n_admitted = plan.n_admitted;
+    info->n_refused_mem = plan.n_refused_mem;
+    info->n_refused_wcet = plan.n_refused_wcet;
+    info->n_rows = plan.n_rows;
+    info->n_prefill_rows = plan.n_prefill_rows;
+  }
+  if (plan.idle || plan.B == 0) return RT_OK;
+  if (c.world > 1) {  // a12: allgather of this round's local top-K candidates on the side stream
+    CK(e, cudaEventRecord(e->ev_cand, s));
+    CK(e, cudaStreamWaitEvent(e->side, e->ev_cand, 0));
+    int r = g_nccl.allgather(e->sp.cand, e->d_cand_all, kTopK * 4, kNcclFloat64, e->comm, e->side);
+    if (r != 0) return fail(e, RT_E_NCCL, "ncclAllGather failed");
+    launch_merge_cand(e->d_cand_all, c.world, e->d_merged, e->side);
+    CK(e, cudaEventRecord(e->ev_merge, e->side));
+    e->merge_pending = true;
+  }
+  if (timing) cudaEventRecord(e->ev_f0, s);
+  if (!(c.flags & RT_FLAG_NO_MODEL)) {
+    st = forward(e, plan);
+    if (st != RT_OK) return st;
+  }
+  if (timing) {
+    cudaEventRecord(e->ev_f1, s);
+    e->timing_pending = !(c.flags & RT_FLAG_NO_MODEL);
+  }
+  launch_sched_post(e->sp, s);
+  if (timing) {
+    cudaEventRecord(e->ev_q1, s);
+    const rt_config& cc = e->cfg;
+    e->attn_bytes_pending = (double)cc.n_layers *
+        ((double)plan.attn_tokens * cc.n_kv_heads * cc.head_dim * 4.0 +
+         (double)std::min(plan.n_rows, e->fwd_rows) * cc.n_q_heads * cc.head_dim * 4.0);
+  }
+  CK(e, cudaEventRecord(e->ev_post, s));
+  CK(e, cudaGetLastError());
+  e->post_pending = true;
+  e->stats.rounds++;
+  e->stats.tokens += plan.B;
+  e->stats.prefill_tokens += plan.n_prefill_rows;
+  return RT_OK;
+}
+
+static rt_status wait_post(rt_engine* e) {
+  if (e->post_pending) {
+    CK(e, cudaEventSynchronize(e->ev_post));
+    e->post_pending = false;
+  }
+  return RT_OK;
+}
+
+extern "C" rt_status rt_sync(rt_engine* e) {
+  if (!e) return RT_E_INVAL;
+  if (e->sticky) return RT_E_CUDA;
+  CK(e, cudaStreamSynchronize(e->stream));
+  CK(e, cudaStreamSynchronize(e->side));
+  e->post_pending = false;
+  harvest_timing(e);
+  return RT_OK;
+}
+
+extern "C" rt_status rt_poll_segment(rt_engine* e, rt_segment* out, int32_t cap, int32_t* n_out) {
+  if (!e || !n_out || (cap > 0 && !out)) return RT_E_INVAL;
+  if (e->sticky) return RT_E_CUDA;
+  *n_out = 0;
+  rt_status st = wait_post(e);
+  if (st != RT_OK) return st;
+  const volatile HostMailbox* mb = e->h_mb;
+  const int64_t published = mb->seg_written;
+  if (published - e->seg_read > e->ring_cap) return fail(e, RT_E_STATE, "segment ring overflow (poll more often)");
+  int32_t n = 0;
+  while (n < cap && e->seg_read < published) {
+    const SegRec& r = e->h_ring[e->seg_read % e->ring_cap];
+    memcpy(&out[n], &r, sizeof(rt_segment));
+    ++n;
+    ++e->seg_read;
+  }
+  // the host saw the final segment: the task slot may be reused (the device
+  // ignores T_FINISHED slots; apply_submits overwrites every field)
+  for (int i = 0; i < n; ++i) {
+    if (out[i].reason != RT_STOP_EOS && out[i].reason != RT_STOP_MAXNEW) continue;
+    auto it = e->rid_slot.find(out[i].request_id);
+    if (it != e->rid_slot.end()) {
+      e->free_slots.push_back(it->second);
+      e->rid_slot.erase(it);
+    }
+  }
+  e->stats.segments += n;
+  *n_out = n;
+  return RT_OK;
+}
+
+extern "C" rt_status rt_last_round(rt_engine* e, rt_round_info* info) {
+  if (!e || !info) return RT_E_INVAL;
+  if (e->sticky) return RT_E_CUDA;
+  rt_status st = wait_post(e);
+  if (st != RT_OK) return st;
+  const volatile HostMailbox* mb = e->h_mb;
+  memset(info, 0, sizeof(*info));
+  info->t_us = mb->t_us;
+  info->round_us = mb->round_us;
+  info->n_waiting = mb->n_waiting;
+  info->n_running = mb->idle ? 0 : mb->B;
+  info->n_admitted = mb->n_admitted;
+  info->n_stopped = mb->idle ? 0 : mb->n_stopped;
+  info->n_refused_mem = mb->n_refused_mem;
+  info->n_refused_wcet = mb->n_refused_wcet;
+  info->n_rows = mb->n_rows;
+  info->n_prefill_rows = mb->n_prefill_rows;
+  return RT_OK;
+}
+
+extern "C" rt_status rt_get_stats(rt_engine* e, rt_stats* out) {
+  if (!e || !out) return RT_E_INVAL;
+  rt_status st = rt_sync(e);
+  if (st != RT_OK) return st;
+  *out = e->stats;
+  return RT_OK;
+}
+
+extern "C" rt_status rt_reset_stats(rt_engine* e) {
+  if (!e) return RT_E_INVAL;
+  rt_status st = rt_sync(e);
+  if (st != RT_OK) return st;
+  memset(&e->stats, 0, sizeof(e->stats));
+  return RT_OK;
+}
+
+// -------------------------------------------------------------------- dumps
+static rt_status copy_out(rt_engine* e, void* dst, int64_t bytes, const void* src, int64_t need,
+                          int64_t* bytes_out, bool device_src = true) {
+  if (bytes_out) *bytes_out = need;
+  if (!dst) return RT_OK;
+  if (bytes < need) return fail(e, RT_E_INVAL, "dump buffer too small");
+  if (need == 0) return RT_OK;
+  if (device_src) CK(e, cudaMemcpy(dst, src, need, cudaMemcpyDeviceToHost));
+  else memcpy(dst, src, need);
+  return RT_OK;
+}
+
+extern "C" rt_status rt_debug_dump(rt_engine* e, int32_t what, void* dst, int64_t bytes, int64_t* bytes_out) {
+  if (!e) return RT_E_INVAL;
+  if (e->sticky) return RT_E_CUDA;
+  rt_status st = rt_sync(e);
+  if (st != RT_OK) return st;
+  const rt_config& c = e->cfg;
+  const int MT = c.max_tasks;
+  DevState ds;
+  CK(e, cudaMemcpy(&ds, e->d_st, sizeof(ds), cudaMemcpyDeviceToHost));
+  const int B = ds.B, n_rows = ds.n_rows;
+  switch (what) {
+    case RT_DUMP_TASKS: {
+      std::vector<int64_t> v((size_t)MT * 8);
+      std::vector<int64_t> rid(MT);
+      std::vector<int32_t> a(MT);
+      CK(e, cudaMemcpy(rid.data(), e->tt.rid, 8 * MT, cudaMemcpyDeviceToHost));
+      for (int i = 0; i < MT; ++i) v[(size_t)i * 8] = rid[i];
+      int32_t* fields[] = {e->tt.state, e->tt.k, e->tt.ctx, e->tt.n_pages, e->tt.n_gen, e->tt.seg_tok, e->tt.R};
+      for (int f = 0; f < 7; ++f) {
+        CK(e, cudaMemcpy(a.data(), fields[f], 4 * MT, cudaMemcpyDeviceToHost));
+        for (int i = 0; i < MT; ++i) v[(size_t)i * 8 + 1 + f] = a[i];
+      }
+      return copy_out(e, dst, bytes, v.data(), (int64_t)v.size() * 8, bytes_out, false);
+    }
+    case RT_DUMP_PAGE_TABLES:
+      return copy_out(e, dst, bytes, e->tt.page_table, (int64_t)MT * e->pt_stride * 4, bytes_out);
+    case RT_DUMP_ROUND: {
+      std::vector<int32_t> v;
+      v.push_back(B);
+      v.push_back(n_rows);
+      v.push_back(ds.n_admitted);
+      v.push_back(ds.free_top);
+      std::vector<int32_t> slots(std::max(B, 1)), toks(std::max(B, 1)), am(std::max(B, 1)),
+          adm(std::max(ds.n_admitted, 1));
+      std::vector<int64_t> rid(MT);
+      CK(e, cudaMemcpy(rid.data(), e->tt.rid, 8 * MT, cudaMemcpyDeviceToHost));
+      if (B > 0) {
+        CK(e, cudaMemcpy(slots.data(), e->sp.round_slots, 4 * B, cudaMemcpyDeviceToHost));
+        CK(e, cudaMemcpy(toks.data(), e->sp.slot_tok, 4 * B, cudaMemcpyDeviceToHost));
+        CK(e, cudaMemcpy(am.data(), e->sp.argmax_tok, 4 * B, cudaMemcpyDeviceToHost));
+      }
+      if (ds.n_admitted > 0) CK(e, cudaMemcpy(adm.data(), e->sp.admitted, 4 * ds.n_admitted, cudaMemcpyDeviceToHost));
+      for (int i = 0; i < B; ++i) v.push_back((int32_t)rid[slots[i]]);
+      for (int i = 0; i < B; ++i) v.push_back(toks[i]);
+      for (int i = 0; i < B; ++i) v.push_back((c.flags & RT_FLAG_NO_MODEL) ? -1 : am[i]);
+      for (int i = 0; i < ds.n_admitted; ++i) v.push_back((int32_t)rid[adm[i]]);
+      return copy_out(e, dst, bytes, v.data(), (int64_t)v.size() * 4, bytes_out, false);
+    }
+    case RT_DUMP_LOGITS:
+      if (!e->d_logits) return fail(e, RT_E_STATE, "RT_FLAG_KEEP_LOGITS not set");
+      return copy_out(e, dst, bytes, e->d_logits, (int64_t)B * c.vocab * 4, bytes_out);
+    case RT_DUMP_HIDDEN:
+      if (!e->d_hfin) return fail(e, RT_E_STATE, "no model");
+      return copy_out(e, dst, bytes, e->d_hfin, (int64_t)B * c.d_model * 2, bytes_out);
+    case RT_DUMP_CAPTURE_Q:
+      if (!e->d_cap_q) return fail(e, RT_E_STATE, "RT_FLAG_CAPTURE not set");
+      return copy_out(e, dst, bytes, e->d_cap_q, (int64_t)n_rows * c.n_q_heads * c.head_dim * 4, bytes_out);
+    case RT_DUMP_CAPTURE_O:
+      if (!e->d_cap_o) return fail(e, RT_E_STATE, "RT_FLAG_CAPTURE not set");
+      return copy_out(e, dst, bytes, e->d_cap_o, (int64_t)n_rows * c.n_q_heads * c.head_dim * 4, bytes_out);
+    case RT_DUMP_ROWS: {
+      std::vector<int32_t> a(std::max(n_rows, 1)), b(std::max(n_rows, 1)), t(std::max(n_rows, 1)), v;
+      if (n_rows > 0) {
+        CK(e, cudaMemcpy(a.data(), e->sp.row_task, 4 * n_rows, cudaMemcpyDeviceToHost));
+        CK(e, cudaMemcpy(b.data(), e->sp.row_pos, 4 * n_rows, cudaMemcpyDeviceToHost));
+        CK(e, cudaMemcpy(t.data(), e->sp.row_tok, 4 * n_rows, cudaMemcpyDeviceToHost));
+      }
+      for (int i = 0; i < n_rows; ++i) {
+        v.push_back(a[i]);
+        v.push_back(b[i]);
+        v.push_back(t[i]);
+      }
+      return copy_out(e, dst, bytes, v.data(), (int64_t)v.size() * 4, bytes_out, false);
+    }
+    case RT_DUMP_KV_LAYER: {
+      if (!e->d_pool) return fail(e, RT_E_STATE, "no model");
+      const int64_t need = (int64_t)c.n_pages * 2 * c.n_kv_heads * 16 * c.head_dim * 2;
+      if (bytes_out) *bytes_out = need;
+      if (!dst) return RT_OK;
+      if (bytes < need) return fail(e, RT_E_INVAL, "dump buffer too small");
+      bf16* tmp = nullptr;
+      CK(e, cudaMalloc(&tmp, need));
+      launch_kv_read(e->d_pool + (size_t)c.capture_layer * e->pool_layer_bytes, tmp, c.n_pages, c.n_kv_heads,
+                     c.head_dim, e->stream);
+      CK(e, cudaStreamSynchronize(e->stream));
+      cudaError_t r = cudaMemcpy(dst, tmp, need, cudaMemcpyDeviceToHost);
+      cudaFree(tmp);
+      CK(e, r);
+      return RT_OK;
+    }
+    case RT_DUMP_FREE_STACK:
+      return copy_out(e, dst, bytes, e->sp.free_stack, (int64_t)ds.free_top * 4, bytes_out);
+    case RT_DUMP_TASK_SLOTS:
+      return copy_out(e, dst, bytes, e->sp.round_slots, (int64_t)B * 4, bytes_out);
+    case RT_DUMP_MERGED: {
+      if (!e->d_merged) return fail(e, RT_E_STATE, "world == 1");
+      std::vector<double> m(kTopK * 4);
+      CK(e, cudaMemcpy(m.data(), e->d_merged, 8 * m.size(), cudaMemcpyDeviceToHost));
+      std::vector<int64_t> v(kTopK * 4);
+      for (int i = 0; i < kTopK * 4; ++i) memcpy(&v[i], &m[i], 8);
+      return copy_out(e, dst, bytes, v.data(), (int64_t)v.size() * 8, bytes_out, false);
+    }
+    default:
+      return fail(e, RT_E_INVAL, "unknown dump kind");
+  }
+}

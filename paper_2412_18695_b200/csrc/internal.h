@@ -1,0 +1,101 @@
+// internal.h — structures shared by the host engine and the device kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace rt {
+
+enum TaskState : int32_t { T_FREE = -1, T_PENDING = 0, T_WAITING = 1, T_RUNNING = 2, T_FINISHED = 3 };
+
+constexpr int kMaxSegTok = 16;
+constexpr int kMaxTasks = 2048;
+constexpr int kSchedThreads = 1024;
+constexpr int kTopK = 16;          // per-rank candidates exchanged per round (a12)
+
+// Submission record staged in pinned host memory, applied on device at the next step.
+struct SubmitRec {
+  int64_t rid, arrival, ert;
+  double alpha, beta;
+  int32_t slot, agent, n_prompt, max_new, window, scripted;
+  int64_t tok_off;  // offset of prompt (then script) tokens in the staging token pool
+};
+
+// Device task table (structure of arrays, capacity max_tasks).
+struct TaskTable {
+  int64_t *rid, *arrival, *ert, *D, *ref, *end_est, *seg_exec;
+  double *alpha, *beta, *pri;
+  int32_t *state, *agent, *k, *n_prompt, *max_new, *window, *scripted;
+  int32_t *n_gen, *seg_tok, *n_skills, *pending, *ctx, *n_pages, *R, *holder, *argmax_last;
+  int32_t* page_table;   // [max_tasks][pt_stride]
+  int32_t* prompt;       // [max_tasks][max_ctx]
+  int32_t* script;       // [max_tasks][max_ctx]
+  int32_t* out;          // [max_tasks][max_ctx]
+};
+
+// Scalars kept on device across rounds.
+struct DevState {
+  int64_t t, last_t;
+  int64_t hist[8];
+  int32_t hist_n, hist_pos, last_nonempty;
+  int32_t n_slots;       // running slots after the last retire
+  int32_t free_top;      // free-stack size
+  int32_t B, n_rows, n_prefill_rows, max_seqlen;
+  int64_t round_us, dispatch_us, sum_ctx, sum_prompt;
+  int64_t seg_written;   // segment records published so far
+  int32_t n_admitted, n_waiting, n_refused_mem, n_refused_wcet, n_stopped, n_pops;
+  int32_t error;
+};
+
+// Round plan / summary published to the host (mapped pinned memory).
+struct HostMailbox {
+  int64_t t_us, round_us;
+  int32_t idle, B, n_rows, n_prefill_rows, max_seqlen, n_admitted, n_waiting;
+  int32_t n_refused_mem, n_refused_wcet, n_stopped, error;
+  int64_t seg_written;
+  int64_t round_seq;
+  int64_t attn_tokens;   // sum over rows of attended positions (algorithmic attention bytes)
+};
+
+struct SegRec {  // identical layout to rt_segment
+  int64_t request_id;
+  int32_t agent_id, k, tok_begin, tok_end, n_skills, reason;
+  int64_t est_exec_us;
+  int64_t dispatch_us;
+  int32_t tokens[16];
+};
+
+struct SchedParams {
+  TaskTable tt;
+  DevState* st;
+  HostMailbox* mb;           // mapped host pointer
+  SegRec* seg_ring;          // mapped host pointer
+  int64_t seg_ring_cap;
+  int32_t* free_stack;       // [n_pages]
+  int32_t* slot_task;        // [max_batch]   task slot of each running slot (persistent)
+  int32_t* round_slots;      // [max_batch]   task slot of each slot of the current round (log)
+  int32_t* slot_is_prefill;  // [max_batch]
+  int32_t* slot_row;         // [max_batch]   logits row of each slot
+  int32_t* admitted;         // [max_batch]   admitted task slots (this round, in order)
+  int32_t* row_task;         // [rows_cap]
+  int32_t* row_pos;          // [rows_cap]
+  int32_t* row_tok;          // [rows_cap]
+  int32_t* argmax_tok;       // [max_batch]   lm_head argmax per slot
+  int32_t* slot_tok;         // [max_batch]   selected token per slot (log)
+  int32_t* popped;           // [max_pops][2]
+  const int16_t* tok_skill;
+  const int32_t* tok_exec;
+  double* cand;              // [kTopK][4] local top-K candidates (pri, arrival, rid, rank)
+  int32_t max_tasks, max_batch, max_ctx, pt_stride, n_pages, page_tokens, rows_cap;
+  int32_t max_seg_tokens, g_us, net_us, eps_l_us, speed_window, max_admit, policy, clock_mode;
+  int32_t base_us, gamma_ppm, kv_us_per_1k, prefill_us_per_tok;
+  int32_t eos_id, rank, world, no_model;
+};
+
+// launchers (sched.cu)
+void launch_apply_submits(const SchedParams& p, const SubmitRec* d_recs, const int32_t* d_toks, int n,
+                          cudaStream_t s);
+void launch_sched_pre(const SchedParams& p, int64_t now_us, cudaStream_t s);
+void launch_sched_post(const SchedParams& p, cudaStream_t s);
+void launch_init_free_stack(int32_t* stack, int n, cudaStream_t s);
+
+}  // namespace rt

@@ -1,0 +1,77 @@
+// model.h — launchers of the decode-step kernels (model.cu, attn.cu, gemm_tc.cu).
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+#include <algorithm>
+#include <limits.h>
+
+namespace rt {
+typedef __nv_bfloat16 bf16;
+
+struct QkvEpiArgs {
+  const float* part;
+  int splits, n_rows, row0;
+  const int32_t *row_task, *row_pos, *page_table;
+  int pt_stride, nq, nkv, hd;
+  const float *rope_cos, *rope_sin;
+  bf16* q_out;
+  void* pool;      // this layer's pool
+  float* q_cap;    // nullable [rows_total][nq][hd] capture (indexed by global row)
+};
+
+void launch_init_weights(bf16* out, int64_t n, uint64_t seed, int32_t tensor_id, float sigma, cudaStream_t s);
+void launch_embed_norm(const int32_t* row_tok, int row0, int n, const bf16* emb, int d, float* x, bf16* h,
+                       cudaStream_t s);
+void launch_resid_norm(const float* part, int splits, int n, int d, float* x, bf16* h, cudaStream_t s);
+void launch_swiglu(const float* part, int splits, int n, int ff, bf16* act, cudaStream_t s);
+void launch_qkv_epilogue(const QkvEpiArgs& a, cudaStream_t s);
+void launch_gather_rows(const int32_t* slot_row, int B, int row0, int n, const bf16* h, int d, bf16* hfin,
+                        cudaStream_t s);
+void launch_argmax_reduce(const float* pv, const int32_t* pi, int n_mtiles, int N, int32_t* tok,
+                          cudaStream_t s);
+void launch_kv_write(void* pool, const bf16* k, const bf16* v, const int32_t* slot, int n, int nkv, int hd,
+                     cudaStream_t s);
+void launch_kv_read(const void* pool, bf16* out, int n_pages, int nkv, int hd, cudaStream_t s);
+
+// ---- paged decode attention (attn.cu)
+struct AttnArgs {
+  const bf16* q;            // [n_rows][nq][hd]  (rows of this launch)
+  const void* pool;         // this layer's pool
+  const int32_t* page_table;
+  int pt_stride;
+  const int32_t* row_task;  // indexed by row0 + r
+  const int32_t* row_pos;   // seqlen = pos + 1   (when row_seqlen == nullptr)
+  const int32_t* row_seqlen;
+  int row0, n_rows, nq, nkv, hd, G;
+  int chunk_pages, max_chunks;
+  bf16* out;                // [n_rows][nq][hd]
+  float* out_f32;           // nullable, indexed by global row (row0 + r)
+  float* ws;                // partials
+  float scale_log2;
+};
+int64_t attn_ws_floats(int n_rows, int nq, int hd, int max_chunks);
+void attn_plan(int n_rows, int nkv, int max_seqlen, int* chunk_pages, int* max_chunks);
+void launch_attention(const AttnArgs& a, cudaStream_t s);
+
+// ---- tcgen05 GEMM (gemm_tc.cu)
+struct TmaMap {
+  alignas(64) unsigned char bytes[128];
+};
+bool make_tma_2d_bf16(TmaMap* out, const void* base, uint64_t inner, uint64_t rows, uint32_t box_inner,
+                      uint32_t box_rows);
+struct GemmTmaSet {       // activation operand: one map per supported N tile
+  TmaMap m32, m64, m128, m256;
+  int rows_cap;
+};
+bool make_gemm_act_maps(GemmTmaSet* out, const void* base, int K, int rows_cap);
+// out[s][n][m] partial sums (MODE store) ; returns splits used
+int launch_gemm(const TmaMap& wmap, const GemmTmaSet& xmaps, int M, int N, int K, float* out, int max_splits,
+                cudaStream_t s);
+// lm_head + argmax partials: part_val/part_idx [ceil(M/128)][N]; logits nullable [N][M]
+void launch_gemm_argmax(const TmaMap& wmap, const GemmTmaSet& xmaps, int M, int N, int K, float* part_val,
+                        int32_t* part_idx, float* logits, cudaStream_t s);
+int gemm_choose_splits(int M, int N, int K, int max_splits);
+void launch_gemm_fixed(const TmaMap& wmap, const GemmTmaSet& xmaps, int M, int N, int K, float* out, int splits,
+                       cudaStream_t s);
+}  // namespace rt

@@ -1,0 +1,115 @@
+// ops.cu — op-level C ABI (include/rt_ops.h): the hot-path kernels on caller-owned
+// device buffers, for per-op parity tests and microbenchmarks.
+#include <cuda_runtime.h>
+#include <math.h>
+#include "rt_ops.h"
+#include "internal.h"
+#include "model.h"
+
+using namespace rt;
+
+namespace rt {
+void launch_priority_batch(const int64_t* trde, const int32_t* k, const double* alpha, const double* beta, int n,
+                           int g_us, int net_us, int eps_l_us, double* pri, cudaStream_t s);
+}
+
+static rt_status last_launch() { return cudaGetLastError() == cudaSuccess ? RT_OK : RT_E_CUDA; }
+
+extern "C" int64_t rt_op_attention_ws_bytes(int32_t n_rows, int32_t max_seqlen, int32_t n_q, int32_t hd) {
+  int cp = 0, mc = 0;
+  attn_plan(n_rows, 1, max_seqlen, &cp, &mc);
+  // nkv only changes the plan through n_rows * nkv >= target; bound with nkv = 1
+  return attn_ws_floats(n_rows, n_q, hd, mc) * 4;
+}
+
+extern "C" rt_status rt_op_paged_attention(const void* d_q, const void* d_pool, const int32_t* d_page_table,
+                                           int32_t pt_stride, const int32_t* d_row_task,
+                                           const int32_t* d_row_seqlen, int32_t n_rows, int32_t max_seqlen,
+                                           int32_t n_q, int32_t n_kv, int32_t hd, void* d_out, float* d_out_f32,
+                                           void* d_ws, int64_t ws_bytes, void* stream) {
+  if (n_rows < 0 || max_seqlen < 1 || n_kv < 1 || n_q % n_kv || n_q / n_kv > 8) return RT_E_INVAL;
+  if (hd != 32 && hd != 64 && hd != 128) return RT_E_INVAL;
+  if (n_rows == 0) return RT_OK;
+  AttnArgs a{};
+  a.q = (const bf16*)d_q;
+  a.pool = d_pool;
+  a.page_table = d_page_table;
+  a.pt_stride = pt_stride;
+  a.row_task = d_row_task;
+  a.row_pos = nullptr;
+  a.row_seqlen = d_row_seqlen;
+  a.row0 = 0;
+  a.n_rows = n_rows;
+  a.nq = n_q;
+  a.nkv = n_kv;
+  a.hd = hd;
+  a.G = n_q / n_kv;
+  attn_plan(n_rows, n_kv, max_seqlen, &a.chunk_pages, &a.max_chunks);
+  if (a.max_chunks > 1 && attn_ws_floats(n_rows, n_q, hd, a.max_chunks) * 4 > ws_bytes) {
+    a.chunk_pages = (max_seqlen + 15) / 16;
+    a.max_chunks = 1;
+  }
+  a.out = (bf16*)d_out;
+  a.out_f32 = d_out_f32;
+  a.ws = (float*)d_ws;
+  a.scale_log2 = (float)(1.4426950408889634 / sqrt((double)hd));
+  launch_attention(a, (cudaStream_t)stream);
+  return last_launch();
+}
+
+extern "C" rt_status rt_op_kv_write(void* d_pool, const void* d_k, const void* d_v, const int32_t* d_slot,
+                                    int32_t n_rows, int32_t n_kv, int32_t hd, void* stream) {
+  if (n_rows < 0 || n_kv < 1 || hd % 8) return RT_E_INVAL;
+  if (n_rows == 0) return RT_OK;
+  launch_kv_write(d_pool, (const bf16*)d_k, (const bf16*)d_v, d_slot, n_rows, n_kv, hd, (cudaStream_t)stream);
+  return last_launch();
+}
+
+extern "C" rt_status rt_op_kv_read(const void* d_pool, void* d_out, int32_t n_pages, int32_t n_kv, int32_t hd,
+                                   void* stream) {
+  if (n_pages < 1 || n_kv < 1 || hd % 8) return RT_E_INVAL;
+  launch_kv_read(d_pool, (bf16*)d_out, n_pages, n_kv, hd, (cudaStream_t)stream);
+  return last_launch();
+}
+
+extern "C" rt_status rt_op_gemm(const void* d_w, const void* d_x, float* d_out, int32_t M, int32_t N, int32_t K,
+                                int32_t n_cap, int32_t splits, void* stream) {
+  if (M < 1 || N < 1 || K < 64 || K % 64 || n_cap < N || splits < 1 || splits > K / 64) return RT_E_INVAL;
+  TmaMap wm;
+  GemmTmaSet xm;
+  if (!make_tma_2d_bf16(&wm, d_w, K, M, 64, 128) || !make_gemm_act_maps(&xm, d_x, K, n_cap)) return RT_E_CUDA;
+  launch_gemm_fixed(wm, xm, M, N, K, d_out, splits, (cudaStream_t)stream);
+  return last_launch();
+}
+
+extern "C" rt_status rt_op_lm_argmax(const void* d_w, const void* d_x, int32_t M, int32_t N, int32_t K,
+                                     int32_t n_cap, int32_t* d_tok, float* d_logits, void* d_ws, int64_t ws_bytes,
+                                     void* stream) {
+  if (M < 1 || N < 1 || K < 64 || K % 64 || n_cap < N) return RT_E_INVAL;
+  const int mt = (M + 127) / 128;
+  if (ws_bytes < (int64_t)mt * N * 8) return RT_E_INVAL;
+  TmaMap wm;
+  GemmTmaSet xm;
+  if (!make_tma_2d_bf16(&wm, d_w, K, M, 64, 128) || !make_gemm_act_maps(&xm, d_x, K, n_cap)) return RT_E_CUDA;
+  float* pv = (float*)d_ws;
+  int32_t* pi = (int32_t*)(pv + (size_t)mt * N);
+  launch_gemm_argmax(wm, xm, M, N, K, pv, pi, d_logits, (cudaStream_t)stream);
+  launch_argmax_reduce(pv, pi, mt, N, d_tok, (cudaStream_t)stream);
+  return last_launch();
+}
+
+extern "C" rt_status rt_op_init_weights(void* d_out, int64_t n, uint64_t seed, int32_t tensor_id, float sigma,
+                                        void* stream) {
+  if (n < 0 || tensor_id < 0) return RT_E_INVAL;
+  if (n == 0) return RT_OK;
+  launch_init_weights((bf16*)d_out, n, seed, tensor_id, sigma, (cudaStream_t)stream);
+  return last_launch();
+}
+
+extern "C" rt_status rt_op_priority(const int64_t* d_trde, const int32_t* d_k, const double* d_alpha,
+                                    const double* d_beta, int32_t n, int32_t g_us, int32_t net_us, int32_t eps_l_us,
+                                    double* d_pri, void* stream) {
+  if (n < 0 || g_us <= 0 || eps_l_us <= 0) return RT_E_INVAL;
+  launch_priority_batch(d_trde, d_k, d_alpha, d_beta, n, g_us, net_us, eps_l_us, d_pri, (cudaStream_t)stream);
+  return last_launch();
+}

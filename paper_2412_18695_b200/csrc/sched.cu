@@ -1,0 +1,791 @@
+// sched.cu — device-side segmented scheduler (rows a1-a4, a9-a11 of SURVEY §8(a)).
+//
+// One CTA of 1024 threads per kernel; all state lives in HBM (task table SoA,
+// free stack, slot arrays) so a round needs no host round trip except the plan
+// handshake.  Semantics are those of DESIGN.md R-ROUND (identical to
+// oracle/engine.py, which is written from the paper independently):
+//   pre  : clock, ingest, Eq. 4 scoring of every waiting
+//          task, sort by (Pri desc, arrival, id),
+//          WCET gate + memory check admission,
+//          page pops + batch assembly, forward rows.
+//   post : stop checker (window rule BASELINE.json),
+//          segment records to the pinned ring, suspend with the
+//          completion estimate / finish + free, clock advance.
+// Floating point: Eq. 4 in IEEE fp64 with explicit _rn intrinsics (no FMA
+// contraction), fixed operation order, -0.0 canonicalised (AMB-10).
+#include "common.cuh"
+#include "internal.h"
+#include <limits.h>
+
+namespace rt {
+
+// ------------------------------------------------------------------ helpers
+__device__ __forceinline__ unsigned long long enc_i64(int64_t a) {
+  return (unsigned long long)a ^ 0x8000000000000000ull;
+}
+__device__ __forceinline__ int64_t dec_i64(unsigned long long u) {
+  return (int64_t)(u ^ 0x8000000000000000ull);
+}
+
+// Eq. 1 at waiting w (µs): min(beta, alpha (w - ERT)/1e6 + beta)
+__device__ double tuf0_d(double beta, double alpha, int64_t ert, int64_t w) {
+  double x = __ddiv_rn(__ll2double_rn(w - ert), 1e6);
+  double y = __dmul_rn(alpha, x);
+  y = __dadd_rn(y, beta);
+  return (beta <= y) ? beta : y;
+}
+// TUF_1: min(beta, alpha max(w, 0)/1e6 + beta)
+__device__ double tuf1_d(double beta, double alpha, int64_t w) {
+  double x = __ddiv_rn(__ll2double_rn(w > 0 ? w : 0), 1e6);
+  double y = __dmul_rn(alpha, x);
+  y = __dadd_rn(y, beta);
+  return (beta <= y) ? beta : y;
+}
+// Eq. 4 with readings AMB-2/3/4/5
+__device__ double priority_d(int64_t t, int32_t k, int64_t ref, int64_t D, int64_t ert, double alpha,
+                             double beta, int32_t g_us, int32_t net_us, int32_t eps_l_us) {
+  int64_t w = t + (int64_t)g_us + (int64_t)net_us - ref;
+  double num = (k == 0) ? tuf0_d(beta, alpha, ert, w) : tuf1_d(beta, alpha, w);
+  int64_t L = D - t - (int64_t)g_us;
+  if (L < (int64_t)eps_l_us) L = eps_l_us;
+  double a = __ddiv_rn(__ll2double_rn((int64_t)g_us), 1e6);
+  double b = __ddiv_rn(__ll2double_rn(L), 1e6);
+  double den = __dmul_rn(a, b);
+  double pri = __ddiv_rn(num, den);
+  return __dadd_rn(pri, 0.0);
+}
+
+__device__ __forceinline__ int ceil_div_i(int a, int b) { return (a + b - 1) / b; }
+
+// Exclusive scan in place over a[0..n) (shared memory), returns the total.
+// All threads of the block must call it.
+__device__ int block_scan_excl(int* a, int n, int* wbuf) {
+  const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, w = tid >> 5, nw = nt >> 5;
+  const int per = (n + nt - 1) / nt;
+  const int beg = min(tid * per, n), end = min(beg + per, n);
+  int local = 0;
+  for (int i = beg; i < end; ++i) local += a[i];
+  int v = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    int y = __shfl_up_sync(0xffffffffu, v, o);
+    if (lane >= o) v += y;
+  }
+  if (lane == 31) wbuf[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    int x = lane < nw ? wbuf[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    wbuf[lane] = x;
+  }
+  __syncthreads();
+  int run = (w > 0 ? wbuf[w - 1] : 0) + v - local;
+  const int total = wbuf[nw - 1];
+  for (int i = beg; i < end; ++i) {
+    int x = a[i];
+    a[i] = run;
+    run += x;
+  }
+  __syncthreads();
+  return total;
+}
+
+__device__ void hist_push(DevState* st, int64_t v) {
+  st->hist[st->hist_pos] = v;
+  st->hist_pos = (st->hist_pos + 1) & 7;
+  if (st->hist_n < 8) st->hist_n++;
+}
+
+// ------------------------------------------------------------ submissions
+__global__ void k_apply_submits(SchedParams p, const SubmitRec* recs, const int32_t* toks) {
+  const SubmitRec r = recs[blockIdx.x];
+  TaskTable T = p.tt;
+  const int i = r.slot;
+  for (int j = threadIdx.x; j < r.n_prompt; j += blockDim.x)
+    T.prompt[(size_t)i * p.max_ctx + j] = toks[r.tok_off + j];
+  if (r.scripted)
+    for (int j = threadIdx.x; j < r.max_new; j += blockDim.x)
+      T.script[(size_t)i * p.max_ctx + j] = toks[r.tok_off + r.n_prompt + j];
+  if (threadIdx.x == 0) {
+    T.rid[i] = r.rid;
+    T.arrival[i] = r.arrival;
+    T.ert[i] = r.ert;
+    T.D[i] = r.arrival + r.ert;
+    T.ref[i] = r.arrival;
+    T.end_est[i] = LLONG_MIN;
+    T.seg_exec[i] = 0;
+    T.alpha[i] = r.alpha;
+    T.beta[i] = r.beta;
+    T.pri[i] = 0.0;
+    T.agent[i] = r.agent;
+    T.k[i] = 0;
+    T.n_prompt[i] = r.n_prompt;
+    T.max_new[i] = r.max_new;
+    T.window[i] = r.window;
+    T.scripted[i] = r.scripted;
+    T.n_gen[i] = 0;
+    T.seg_tok[i] = 0;
+    T.n_skills[i] = 0;
+    T.pending[i] = -1;
+    T.ctx[i] = 0;
+    T.n_pages[i] = 0;
+    T.R[i] = ceil_div_i(r.n_prompt + r.max_new, p.page_tokens);
+    T.holder[i] = 0;
+    T.argmax_last[i] = -1;
+    __threadfence();
+    T.state[i] = T_PENDING;
+  }
+}
+
+void launch_apply_submits(const SchedParams& p, const SubmitRec* d_recs, const int32_t* d_toks, int n,
+                          cudaStream_t s) {
+  if (n > 0) k_apply_submits<<<n, 256, 0, s>>>(p, d_recs, d_toks);
+}
+
+__global__ void k_init_free_stack(int32_t* stack, int n) {
+  // stack[0] is the bottom; top = stack[n-1] = 0 -> pops yield 0, 1, 2, ... (AMB-14)
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    stack[i] = n - 1 - i;
+}
+void launch_init_free_stack(int32_t* stack, int n, cudaStream_t s) {
+  k_init_free_stack<<<(n + 255) / 256, 256, 0, s>>>(stack, n);
+}
+
+// -------------------------------------------------------------- sched_pre
+struct PreSmem {
+  double a0[kMaxTasks];
+  long long a1[kMaxTasks], a2[kMaxTasks], a3[kMaxTasks];
+  int perm[kMaxTasks];
+  int cslot[kMaxTasks], ck[kMaxTasks], cR[kMaxTasks];
+  int cnt_a[kMaxTasks], cnt_b[kMaxTasks];
+  int adm[kMaxTasks];
+};
+
+__device__ __forceinline__ bool key_before(const PreSmem& S, int x, int y, int n) {
+  // x before y ?  invalid (>= n) entries sort last
+  if (x >= n) return false;
+  if (y >= n) return true;
+  if (S.a0[x] != S.a0[y]) return S.a0[x] > S.a0[y];
+  if (S.a1[x] != S.a1[y]) return S.a1[x] < S.a1[y];
+  if (S.a2[x] != S.a2[y]) return S.a2[x] < S.a2[y];
+  return S.a3[x] < S.a3[y];
+}
+
+__global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, int64_t now_us) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  PreSmem& S = *reinterpret_cast<PreSmem*>(dsm);
+  __shared__ long long s_t;
+  __shared__ int s_nwait, s_nc, s_nadm, s_gate_ok, s_refused_mem, s_refused_wcet, s_outstanding;
+  __shared__ unsigned long long s_min_arr;
+  __shared__ int wbuf[32];
+  __shared__ unsigned long long s_sum_ctx, s_sum_prompt, s_attn_tok;
+  __shared__ int s_max_seqlen;
+
+  TaskTable T = p.tt;
+  DevState* st = p.st;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const bool wall = (p.clock_mode == 1);
+
+  if (tid == 0) {
+    int64_t t;
+    if (wall) {
+      t = now_us;
+      if (st->last_nonempty) hist_push(st, t - st->last_t);
+      st->last_nonempty = 0;
+      st->last_t = t;
+    } else {
+      t = st->t;
+    }
+    s_t = t;
+    s_nwait = 0;
+    s_min_arr = ~0ull;
+    s_outstanding = 0;
+    s_sum_ctx = 0;
+    s_sum_prompt = 0;
+    s_attn_tok = 0;
+    s_max_seqlen = 0;
+  }
+  __syncthreads();
+  int64_t t = s_t;
+
+  // ---- (1) ingest arrivals <= t
+  for (int i = tid; i < p.max_tasks; i += nt) {
+    int sti = T.state[i];
+    if (sti == T_PENDING && T.arrival[i] <= t) {
+      T.state[i] = T_WAITING;
+      sti = T_WAITING;
+    }
+    if (sti == T_WAITING) atomicAdd(&s_nwait, 1);
+    if (sti == T_PENDING) atomicMin(&s_min_arr, enc_i64(T.arrival[i]));
+  }
+  __syncthreads();
+  const int n_run = st->n_slots;
+  if (n_run == 0 && s_nwait == 0) {
+    if (!wall && s_min_arr != ~0ull) {  // virtual clock jumps to the next arrival
+      t = dec_i64(s_min_arr);
+      __syncthreads();
+      if (tid == 0) {
+        s_t = t;
+        st->t = t;
+      }
+      for (int i = tid; i < p.max_tasks; i += nt) {
+        if (T.state[i] == T_PENDING && T.arrival[i] <= t) {
+          T.state[i] = T_WAITING;
+          atomicAdd(&s_nwait, 1);
+        }
+      }
+      __syncthreads();
+    }
+    if (s_nwait == 0) {
+      if (tid == 0) {
+        st->B = 0;
+        st->n_rows = 0;
+        st->n_prefill_rows = 0;
+        st->round_us = 0;
+        st->n_admitted = 0;
+        st->n_waiting = 0;
+        st->n_refused_mem = 0;
+        st->n_refused_wcet = 0;
+        HostMailbox* mb = p.mb;
+        mb->t_us = t;
+        mb->round_us = 0;
+        mb->idle = 1;
+        mb->B = 0;
+        mb->n_rows = 0;
+        mb->n_prefill_rows = 0;
+        mb->max_seqlen = 0;
+        mb->n_admitted = 0;
+        mb->n_waiting = 0;
+        mb->n_refused_mem = 0;
+        mb->n_refused_wcet = 0;
+        for (int j = 0; j < kTopK; ++j) {
+          p.cand[j * 4 + 0] = -INFINITY;
+          p.cand[j * 4 + 2] = -1.0;
+        }
+        __threadfence_system();
+      }
+      return;
+    }
+  }
+
+  // ---- (2) score every waiting task (Eq. 4 recomputed before fetching)
+  if (tid == 0) s_nc = 0;
+  __syncthreads();
+  for (int i = tid; i < p.max_tasks; i += nt) {
+    if (T.state[i] != T_WAITING) continue;
+    const int pos = atomicAdd(&s_nc, 1);
+    const int64_t arr = T.arrival[i], rid = T.rid[i];
+    const int k = T.k[i];
+    double a0 = 0.0;
+    long long a1, a2, a3 = 0;
+    if (p.policy == 0) {  // PUD (the paper's)
+      a0 = priority_d(t, k, T.ref[i], T.D[i], T.ert[i], T.alpha[i], T.beta[i], p.g_us, p.net_us,
+                      p.eps_l_us);
+      T.pri[i] = a0;
+      a1 = arr;
+      a2 = rid;
+    } else if (p.policy == 1) {  // FCFS
+      a1 = arr;
+      a2 = rid;
+    } else {  // EDF on the initial deadline
+      a1 = arr + T.ert[i];
+      a2 = arr;
+      a3 = rid;
+    }
+    S.a0[pos] = a0;
+    S.a1[pos] = a1;
+    S.a2[pos] = a2;
+    S.a3[pos] = a3;
+    S.cslot[pos] = i;
+    S.ck[pos] = k;
+    S.cR[pos] = T.R[i];
+  }
+  // outstanding reservations sum_active (R - held)  (AMB-26)
+  int my_out = 0;
+  for (int i = tid; i < p.max_tasks; i += nt)
+    if (T.holder[i]) my_out += T.R[i] - T.n_pages[i];
+  if (my_out) atomicAdd(&s_outstanding, my_out);
+  __syncthreads();
+  const int n = s_nc;
+  int n_pad = 1;
+  while (n_pad < n) n_pad <<= 1;
+  for (int i = tid; i < n_pad; i += nt) S.perm[i] = i;
+  __syncthreads();
+  // bitonic sort of perm by key
+  for (int kk = 2; kk <= n_pad; kk <<= 1) {
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      for (int i = tid; i < n_pad; i += nt) {
+        const int ixj = i ^ j;
+        if (ixj > i) {
+          const int x = S.perm[i], y = S.perm[ixj];
+          const bool up = ((i & kk) == 0);
+          const bool sw = up ? key_before(S, y, x, n) : key_before(S, x, y, n);
+          if (sw) {
+            S.perm[i] = y;
+            S.perm[ixj] = x;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+
+  // ---- local top-K candidates for the round allgather (a12)
+  if (tid < kTopK) {
+    if (tid < n) {
+      const int x = S.perm[tid];
+      p.cand[tid * 4 + 0] = S.a0[x];
+      p.cand[tid * 4 + 1] = (double)S.a1[x];
+      p.cand[tid * 4 + 2] = (double)S.a2[x];
+      p.cand[tid * 4 + 3] = (double)p.rank;
+    } else {
+      p.cand[tid * 4 + 0] = -INFINITY;
+      p.cand[tid * 4 + 1] = 0.0;
+      p.cand[tid * 4 + 2] = -1.0;
+      p.cand[tid * 4 + 3] = (double)p.rank;
+    }
+  }
+
+  // ---- (3a) WCET gate on the most urgent running generation
+  if (tid < 32) {
+    long long best_bud = LLONG_MAX, best_rid = LLONG_MAX;
+    int best_seg = 0;
+    for (int s = tid; s < n_run; s += 32) {
+      const int task = p.slot_task[s];
+      const long long bud = T.D[task] - t;
+      const long long rid = T.rid[task];
+      if (bud >= 0 && (bud < best_bud || (bud == best_bud && rid < best_rid))) {
+        best_bud = bud;
+        best_rid = rid;
+        best_seg = T.seg_tok[task];
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      long long ob = __shfl_xor_sync(0xffffffffu, best_bud, o);
+      long long orid = __shfl_xor_sync(0xffffffffu, best_rid, o);
+      int os = __shfl_xor_sync(0xffffffffu, best_seg, o);
+      if (ob < best_bud || (ob == best_bud && orid < best_rid)) {
+        best_bud = ob;
+        best_rid = orid;
+        best_seg = os;
+      }
+    }
+    if (tid == 0) {
+      int gate = 1;
+      const int nh = min(p.speed_window, st->hist_n);
+      if (best_bud != LLONG_MAX && nh > 0) {
+        long long sum = 0;
+        for (int j = 1; j <= nh; ++j) sum += st->hist[(st->hist_pos - j + 8) & 7];
+        const long long rem = max(0, p.max_seg_tokens - best_seg);
+        gate = (rem * sum <= (long long)nh * best_bud) ? 1 : 0;
+      }
+      s_gate_ok = gate;
+    }
+  }
+  __syncthreads();
+
+  // ---- (3b) admission in key order (reading R-MEM)
+  if (tid == 0) {
+    long long avail = (long long)st->free_top - s_outstanding;
+    int nadm = 0, rmem = 0, rwcet = 0;
+    bool mem_blocked = false;
+    for (int c = 0; c < n; ++c) {
+      if (nadm >= p.max_admit) break;
+      if (n_run + nadm >= p.max_batch) break;
+      if (!s_gate_ok) {
+        rwcet = 1;
+        break;
+      }
+      const int x = S.perm[c];
+      if (S.ck[x] == 0) {
+        if (mem_blocked || avail < S.cR[x]) {
+          mem_blocked = true;
+          ++rmem;
+          continue;
+        }
+        avail -= S.cR[x];
+      }
+      S.adm[nadm++] = S.cslot[x];
+    }
+    s_nadm = nadm;
+    s_refused_mem = rmem;
+    s_refused_wcet = rwcet;
+  }
+  __syncthreads();
+  const int nadm = s_nadm;
+  const int B = n_run + nadm;
+
+  // ---- (4) batch assembly: running slots keep their order, admissions appended
+  for (int j = tid; j < nadm; j += nt) {
+    const int task = S.adm[j];
+    const int s = n_run + j;
+    p.slot_task[s] = task;
+    p.admitted[j] = task;
+    T.state[task] = T_RUNNING;
+    const int pre = (T.k[task] == 0);
+    p.slot_is_prefill[s] = pre;
+    if (pre) T.holder[task] = 1;
+  }
+  for (int s = tid; s < n_run; s += nt) p.slot_is_prefill[s] = 0;
+  __syncthreads();
+  // page pops: prefill admissions (admission order) first, then decode slots in slot order
+  for (int s = tid; s < B; s += nt) {
+    const int task = p.slot_task[s];
+    p.round_slots[s] = task;
+    if (p.slot_is_prefill[s]) {
+      S.cnt_a[s] = ceil_div_i(T.n_prompt[task], p.page_tokens);
+      S.cnt_b[s] = 0;
+    } else {
+      S.cnt_a[s] = 0;
+      S.cnt_b[s] = (T.ctx[task] % p.page_tokens == 0) ? 1 : 0;
+    }
+  }
+  __syncthreads();
+  const int tot_a = block_scan_excl(S.cnt_a, B, wbuf);
+  const int tot_b = block_scan_excl(S.cnt_b, B, wbuf);
+  const int top = st->free_top;
+  for (int s = tid; s < B; s += nt) {
+    const int task = p.slot_task[s];
+    int32_t* pt = T.page_table + (size_t)task * p.pt_stride;
+    if (p.slot_is_prefill[s]) {
+      const int npg = ceil_div_i(T.n_prompt[task], p.page_tokens);
+      for (int m = 0; m < npg; ++m) {
+        const int q = S.cnt_a[s] + m;
+        const int pg = p.free_stack[top - 1 - q];
+        pt[m] = pg;
+        p.popped[2 * q] = task;
+        p.popped[2 * q + 1] = pg;
+      }
+      T.n_pages[task] = npg;
+    } else if (T.ctx[task] % p.page_tokens == 0) {
+      const int q = tot_a + S.cnt_b[s];
+      const int pg = p.free_stack[top - 1 - q];
+      const int np = T.n_pages[task];
+      pt[np] = pg;
+      T.n_pages[task] = np + 1;
+      p.popped[2 * q] = task;
+      p.popped[2 * q + 1] = pg;
+    }
+  }
+  __syncthreads();
+  // forward rows: prefill slot -> n_prompt rows, decode slot -> 1 row (AMB-13)
+  for (int s = tid; s < B; s += nt) {
+    const int task = p.slot_task[s];
+    S.cnt_a[s] = p.slot_is_prefill[s] ? T.n_prompt[task] : 1;
+  }
+  __syncthreads();
+  const int n_rows = block_scan_excl(S.cnt_a, B, wbuf);
+  int n_prefill_rows = 0;
+  for (int s = tid; s < B; s += nt) {
+    const int task = p.slot_task[s];
+    const int off = S.cnt_a[s];
+    if (p.slot_is_prefill[s]) {
+      const int P = T.n_prompt[task];
+      p.slot_row[s] = off + P - 1;
+      T.ctx[task] = P;
+      atomicAdd(&s_sum_prompt, (unsigned long long)P);
+      atomicAdd(&s_attn_tok, (unsigned long long)P * (P + 1) / 2);
+      atomicMax(&s_max_seqlen, P);
+    } else {
+      const int c = T.ctx[task];
+      p.row_task[off] = task;
+      p.row_pos[off] = c;
+      p.row_tok[off] = T.pending[task];
+      p.slot_row[s] = off;
+      T.ctx[task] = c + 1;
+      atomicAdd(&s_sum_ctx, (unsigned long long)(c + 1));
+      atomicAdd(&s_attn_tok, (unsigned long long)(c + 1));
+      atomicMax(&s_max_seqlen, c + 1);
+    }
+  }
+  // prefill rows filled slot by slot, all threads in parallel
+  for (int s = n_run; s < B; ++s) {
+    if (!p.slot_is_prefill[s]) continue;
+    const int task = p.slot_task[s];
+    const int off = S.cnt_a[s];
+    const int P = T.n_prompt[task];
+    const int32_t* pr = T.prompt + (size_t)task * p.max_ctx;
+    for (int j = tid; j < P; j += nt) {
+      p.row_task[off + j] = task;
+      p.row_pos[off + j] = j;
+      p.row_tok[off + j] = pr[j];
+    }
+    n_prefill_rows += P;
+  }
+  __syncthreads();
+
+  // ---- (5) round latency (VIRTUAL cost model, AMB-24) and plan publication
+  if (tid == 0) {
+    const long long sum_ctx = (long long)s_sum_ctx, sum_prompt = (long long)s_sum_prompt;
+    long long round_us, dispatch;
+    if (!wall) {
+      round_us = (long long)p.base_us + ((long long)p.base_us * p.gamma_ppm * (long long)(B - 1)) / 1000000 +
+                 ((long long)p.kv_us_per_1k * sum_ctx) / 1024 + (long long)p.prefill_us_per_tok * sum_prompt;
+      dispatch = t + round_us;
+    } else {
+      round_us = st->hist_n > 0 ? st->hist[(st->hist_pos + 7) & 7] : 0;
+      dispatch = t + round_us;
+    }
+    st->free_top = top - tot_a - tot_b;
+    st->B = B;
+    st->n_rows = n_rows;
+    st->n_prefill_rows = n_prefill_rows;
+    st->max_seqlen = s_max_seqlen;
+    st->round_us = round_us;
+    st->dispatch_us = dispatch;
+    st->sum_ctx = sum_ctx;
+    st->sum_prompt = sum_prompt;
+    st->n_admitted = nadm;
+    st->n_waiting = n;
+    st->n_refused_mem = s_refused_mem;
+    st->n_refused_wcet = s_refused_wcet;
+    st->n_pops = tot_a + tot_b;
+    HostMailbox* mb = p.mb;
+    mb->t_us = t;
+    mb->round_us = round_us;
+    mb->idle = 0;
+    mb->B = B;
+    mb->n_rows = n_rows;
+    mb->n_prefill_rows = n_prefill_rows;
+    mb->max_seqlen = s_max_seqlen;
+    mb->n_admitted = nadm;
+    mb->n_waiting = n;
+    mb->n_refused_mem = s_refused_mem;
+    mb->n_refused_wcet = s_refused_wcet;
+    mb->attn_tokens = (long long)s_attn_tok;
+    __threadfence_system();
+  }
+}
+
+void launch_sched_pre(const SchedParams& p, int64_t now_us, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_sched_pre, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PreSmem));
+    attr = true;
+  }
+  k_sched_pre<<<1, kSchedThreads, sizeof(PreSmem), s>>>(p, now_us);
+}
+
+// -------------------------------------------------------------- sched_post
+struct PostSmem {
+  int reason[1024];
+  int stop_off[1024];
+  int keep_off[1024];
+  int keep_task[1024];
+  int fin[1024];
+  int fin_off[1024];
+};
+
+__global__ void __launch_bounds__(kSchedThreads, 1) k_sched_post(SchedParams p) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  PostSmem& S = *reinterpret_cast<PostSmem*>(dsm);
+  __shared__ int wbuf[32];
+  __shared__ int s_nfin;
+  TaskTable T = p.tt;
+  DevState* st = p.st;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int B = st->B;
+  if (B == 0) return;
+  const int64_t dispatch = st->dispatch_us;
+  if (tid == 0) s_nfin = 0;
+
+  // ---- (6) stop checker per slot (a9)
+  for (int s = tid; s < B; s += nt) {
+    const int task = p.slot_task[s];
+    const size_t base = (size_t)task * p.max_ctx;
+    const int ng0 = T.n_gen[task];
+    const int am = p.no_model ? -1 : p.argmax_tok[s];
+    const int tok = T.scripted[task] ? T.script[base + ng0] : am;
+    T.argmax_last[task] = am;
+    const int ng = ng0 + 1;
+    const int segt = T.seg_tok[task] + 1;
+    T.out[base + ng0] = tok;
+    T.pending[task] = tok;
+    int64_t sx = T.seg_exec[task];
+    int nsk = T.n_skills[task];
+    const int sk = p.tok_skill[tok];
+    if (sk >= 0) {
+      sx += p.tok_exec[tok];
+      ++nsk;
+    }
+    int reason = 0;
+    if (tok == p.eos_id) reason = 1;
+    else if (ng == T.max_new[task]) reason = 2;
+    else if (sk >= 0 && sx >= (int64_t)T.window[task]) reason = 3;
+    else if (segt == p.max_seg_tokens) reason = 4;
+    T.n_gen[task] = ng;
+    T.seg_tok[task] = segt;
+    T.seg_exec[task] = sx;
+    T.n_skills[task] = nsk;
+    p.slot_tok[s] = tok;
+    S.reason[s] = reason;
+    S.stop_off[s] = reason != 0;
+    S.keep_off[s] = reason == 0;
+    S.keep_task[s] = task;
+  }
+  __syncthreads();
+  const int n_stop = block_scan_excl(S.stop_off, B, wbuf);
+  const int n_keep = block_scan_excl(S.keep_off, B, wbuf);
+  const int64_t seg_base = st->seg_written;
+
+  // ---- (7) segment records + retire (a10)
+  for (int s = tid; s < B; s += nt) {
+    const int task = S.keep_task[s];
+    const int reason = S.reason[s];
+    if (reason == 0) {
+      p.slot_task[S.keep_off[s]] = task;  // stable compaction (reads use keep_task copy)
+      continue;
+    }
+    const int ng = T.n_gen[task], segt = T.seg_tok[task];
+    const int64_t idx = seg_base + S.stop_off[s];
+    SegRec* r = p.seg_ring + (idx % p.seg_ring_cap);
+    r->request_id = T.rid[task];
+    r->agent_id = T.agent[task];
+    r->k = T.k[task];
+    r->tok_begin = ng - segt;
+    r->tok_end = ng;
+    r->n_skills = T.n_skills[task];
+    r->reason = reason;
+    r->est_exec_us = T.seg_exec[task];
+    r->dispatch_us = dispatch;
+    const int32_t* o = T.out + (size_t)task * p.max_ctx;
+    for (int j = 0; j < 16; ++j) r->tokens[j] = (j < segt) ? o[ng - segt + j] : -1;
+    if (reason == 1 || reason == 2) {  // finish: free pages + reservation
+      T.state[task] = T_FINISHED;
+      T.holder[task] = 0;
+      const int f = atomicAdd(&s_nfin, 1);
+      S.fin[f] = task;
+    } else {  // suspend: completion estimate of the dispatched segment
+      int64_t b = dispatch + (int64_t)p.net_us;
+      const int64_t prev = T.end_est[task];
+      if (prev != LLONG_MIN && prev > b) b = prev;
+      const int64_t e = b + T.seg_exec[task];
+      T.end_est[task] = e;
+      T.D[task] = e;
+      T.ref[task] = e;
+      T.k[task] = T.k[task] + 1;
+      T.seg_tok[task] = 0;
+      T.seg_exec[task] = 0;
+      T.n_skills[task] = 0;
+      T.state[task] = T_WAITING;
+    }
+  }
+  __syncthreads();
+  // finished requests push their pages in ascending request id, each in reverse
+  // page-table order (AMB-14)
+  const int nfin = s_nfin;
+  if (tid == 0) {
+    for (int a = 1; a < nfin; ++a) {  // insertion sort by rid (few per round)
+      const int x = S.fin[a];
+      const int64_t rx = T.rid[x];
+      int b = a - 1;
+      while (b >= 0 && T.rid[S.fin[b]] > rx) {
+        S.fin[b + 1] = S.fin[b];
+        --b;
+      }
+      S.fin[b + 1] = x;
+    }
+  }
+  __syncthreads();
+  for (int f = tid; f < nfin; f += nt) S.fin_off[f] = T.n_pages[S.fin[f]];
+  __syncthreads();
+  const int n_push = block_scan_excl(S.fin_off, nfin, wbuf);
+  const int top = st->free_top;
+  for (int f = tid; f < nfin; f += nt) {
+    const int task = S.fin[f];
+    const int np = T.n_pages[task];
+    const int32_t* pt = T.page_table + (size_t)task * p.pt_stride;
+    for (int m = 0; m < np; ++m) p.free_stack[top + S.fin_off[f] + m] = pt[np - 1 - m];
+    T.n_pages[task] = 0;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    st->free_top = top + n_push;
+    st->n_slots = n_keep;
+    st->n_stopped = n_stop;
+    st->seg_written = seg_base + n_stop;
+    if (p.clock_mode == 0) {
+      st->t = st->t + st->round_us;
+      hist_push(st, st->round_us);
+    } else {
+      st->last_nonempty = 1;
+    }
+    HostMailbox* mb = p.mb;
+    mb->n_stopped = n_stop;
+    mb->seg_written = seg_base + n_stop;
+    mb->round_seq = mb->round_seq + 1;
+    __threadfence_system();
+  }
+}
+
+void launch_sched_post(const SchedParams& p, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_sched_post, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PostSmem));
+    attr = true;
+  }
+  k_sched_post<<<1, kSchedThreads, sizeof(PostSmem), s>>>(p);
+}
+
+// ------------------------------------------------ multi-GPU candidate merge (a12)
+// all: [world][kTopK][4] (pri, arrival, rid, rank); merged: global top-K by
+// (pri desc, arrival asc, rid asc) over the union (AMB-22); rid < 0 = empty.
+__global__ void k_merge_cand(const double* all, int world, double* merged) {
+  __shared__ double key[8 * kTopK][4];
+  __shared__ int perm[8 * kTopK];
+  const int n = world * kTopK;
+  int n_pad = 1;
+  while (n_pad < n) n_pad <<= 1;
+  for (int i = threadIdx.x; i < n_pad; i += blockDim.x) {
+    perm[i] = i;
+    for (int j = 0; j < 4; ++j) key[i][j] = i < n ? all[i * 4 + j] : 0.0;
+    if (i >= n) key[i][2] = -1.0;
+  }
+  __syncthreads();
+  for (int kk = 2; kk <= n_pad; kk <<= 1)
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      for (int i = threadIdx.x; i < n_pad; i += blockDim.x) {
+        const int ixj = i ^ j;
+        if (ixj <= i) continue;
+        const int x = perm[i], y = perm[ixj];
+        auto before = [&](int a, int b) {
+          const bool va = key[a][2] >= 0, vb = key[b][2] >= 0;
+          if (va != vb) return va;
+          if (key[a][0] != key[b][0]) return key[a][0] > key[b][0];
+          if (key[a][1] != key[b][1]) return key[a][1] < key[b][1];
+          return key[a][2] < key[b][2];
+        };
+        const bool up = (i & kk) == 0;
+        if (up ? before(y, x) : before(x, y)) {
+          perm[i] = y;
+          perm[ixj] = x;
+        }
+      }
+      __syncthreads();
+    }
+  for (int i = threadIdx.x; i < kTopK; i += blockDim.x)
+    for (int j = 0; j < 4; ++j) merged[i * 4 + j] = key[perm[i]][j];
+}
+
+void launch_merge_cand(const double* all, int world, double* merged, cudaStream_t s) {
+  k_merge_cand<<<1, 128, 0, s>>>(all, world, merged);
+}
+
+// ------------------------------------------------ op-level Eq. 4 (rt_op_priority)
+__global__ void k_priority_batch(const int64_t* trde, const int32_t* k, const double* alpha, const double* beta,
+                                 int n, int g_us, int net_us, int eps_l_us, double* pri) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  pri[i] = priority_d(trde[4 * i], k[i], trde[4 * i + 1], trde[4 * i + 2], trde[4 * i + 3], alpha[i], beta[i],
+                      g_us, net_us, eps_l_us);
+}
+void launch_priority_batch(const int64_t* trde, const int32_t* k, const double* alpha, const double* beta, int n,
+                           int g_us, int net_us, int eps_l_us, double* pri, cudaStream_t s) {
+  if (n > 0) k_priority_batch<<<(n + 127) / 128, 128, 0, s>>>(trde, k, alpha, beta, n, g_us, net_us, eps_l_us, pri);
+}
+
+}  // namespace rt

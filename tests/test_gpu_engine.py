@@ -1,0 +1,268 @@
+"""End-to-end parity of the C-ABI engine (rt_submit_request / rt_step /
+rt_poll_segment) against the oracle round loop (run on a B200).
+
+* scheduling parity — bit-exact admission order, batch slots, emitted tokens,
+  segment records, page tables and free stack, every round (scripted streams,
+  SURVEY AMB-17), across policies, per-round admission caps {1, 4, inf} (AMB-8),
+  memory pressure, WCET gating and the WALL clock replayed from its log;
+* model parity on the tiny C1 model — logits (end-to-end, gated 1e-2) and the
+  per-op attention of the capture layer on the GPU's own q and KV pages;
+* 8B-shaped operating point — sampled per-op attention and logits checks.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle.engine import OracleEngine, FINISHED          # noqa: E402
+from oracle.model import OracleModel, paged_attention     # noqa: E402
+from oracle import weights as OW                          # noqa: E402
+from oracle.bf16 import bf16                              # noqa: E402
+from synth import MODEL_SHAPES, make_vocab, engine_params, compose_workload  # noqa: E402
+from synth.configs import POLICY_FCFS, POLICY_EDF, CLOCK_WALL  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def rt():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2412_18695_b200 import rt as _rt
+    _rt.lib()
+    return _rt
+
+
+def make_pair(rt, vocab, params, shape=None, seed=0, flags=0, model=False, **kw):
+    eng = rt.Engine(shape, params, vocab, seed=seed, flags=flags, **kw)
+    om = OracleModel(shape, seed=seed) if model else None
+    ora = OracleEngine(params, vocab.tok_skill, vocab.tok_exec_min_us, vocab.eos_id, vocab.vocab, model=om)
+    return eng, ora
+
+
+def submit_both(eng, ora, reqs, scripted=True):
+    for r in reqs:
+        a = eng.submit(r.agent_id, r.prompt, r.arrival_us, r.ert_us, r.alpha, r.beta, r.exec_window_us,
+                       len(r.plan), script=r.plan if scripted else None)
+        b = ora.submit(r.agent_id, r.prompt, r.arrival_us, r.ert_us, r.alpha, r.beta, r.exec_window_us,
+                       len(r.plan), script=r.plan if scripted else None)
+        assert a == b
+
+
+def lockstep(eng, ora, max_rounds=5000, now=None, check_every=1):
+    n = 0
+    while n < max_rounds:
+        t = None if now is None else now(n)
+        ig = eng.step(t or 0)
+        io = ora.step(t)
+        n += 1
+        for key in ("t_us", "n_waiting", "n_running", "n_admitted", "n_refused_mem", "n_refused_wcet"):
+            assert ig[key] == io[key], (n, key, ig, io)
+        if io["n_running"]:
+            lg = eng.round_log()
+            lo = ora.round_log[-1]
+            assert lg["slots"] == lo["slots"], n
+            assert lg["admitted"] == lo["admitted"], n
+            assert lg["tokens"] == lo["tokens"], n
+            assert lg["free"] == lo["free"], n
+            if n % check_every == 0:
+                assert eng.page_tables() == ora.page_tables(), n
+                li = eng.last_round()
+                assert li["n_stopped"] == io["n_stopped"] and li["round_us"] == io["round_us"], (li, io)
+        if io["n_running"] == 0 and all(r.state == FINISHED for r in ora.reqs.values()):
+            break
+    sg, so = eng.poll(), ora.poll()
+    assert sg == so
+    from paper_2412_18695_b200 import rt as _rt
+    fs = eng.dump(_rt.RT_DUMP_FREE_STACK, np.int32)
+    assert list(fs) == ora.free
+    return n, sg
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_sched_parity_c1(rt, seed):
+    v = make_vocab(512)
+    p = engine_params("paper-4090", max_batch=4, max_tasks=64, max_ctx=256, n_pages=64)
+    reqs = compose_workload(4, 1.0, 2, range(1, 9), 30.0, seed, v, prompt_len_range=(40, 64), max_requests=12)
+    eng, ora = make_pair(rt, v, p)
+    submit_both(eng, ora, reqs)
+    n, segs = lockstep(eng, ora)
+    assert len({s["request_id"] for s in segs if s["reason"] in (1, 2)}) == 12
+
+
+@pytest.mark.parametrize("policy,max_admit", [(0, 1), (0, 4), (0, 1 << 30), (POLICY_FCFS, 1 << 30),
+                                              (POLICY_EDF, 2)])
+def test_sched_parity_contention(rt, policy, max_admit):
+    # 64 agents, bursty arrivals, small pool (memory refusals), batch 16
+    v = make_vocab(512)
+    p = engine_params("paper-4090", max_batch=16, max_tasks=256, max_ctx=256, n_pages=96, policy=policy,
+                      max_admit_per_round=max_admit)
+    reqs = compose_workload(64, 8.0, 16, range(1, 12), 6.0, 5, v, prompt_len_range=(20, 120))
+    eng, ora = make_pair(rt, v, p)
+    submit_both(eng, ora, reqs)
+    n, segs = lockstep(eng, ora, max_rounds=20000, check_every=3)
+    assert any(r["n_refused_mem"] > 0 for r in ora.round_log)
+
+
+def test_sched_parity_wcet_gate(rt):
+    # slow paper-4090 clock with gamma: urgent running tasks block admissions (WCET)
+    v = make_vocab(512)
+    p = engine_params("paper-4090", max_batch=8, max_tasks=128, max_ctx=256, n_pages=256)
+    reqs = compose_workload(32, 4.0, 8, [6, 7, 8, 1, 2], 4.0, 11, v, prompt_len_range=(10, 30))
+    eng, ora = make_pair(rt, v, p)
+    submit_both(eng, ora, reqs)
+    lockstep(eng, ora, max_rounds=20000, check_every=5)
+    assert any(r["n_refused_wcet"] > 0 for r in ora.round_log)
+
+
+def test_sched_parity_wall_clock_replay(rt):
+    v = make_vocab(512)
+    p = engine_params("paper-4090", max_batch=4, max_tasks=64, max_ctx=256, n_pages=64, clock_mode=CLOCK_WALL)
+    reqs = compose_workload(8, 2.0, 4, range(1, 9), 3.0, 4, v, prompt_len_range=(8, 40))
+    eng, ora = make_pair(rt, v, p)
+    submit_both(eng, ora, reqs)
+    rng = np.random.default_rng(0)
+    clock = np.cumsum(rng.integers(5000, 40000, 20000))     # recorded wall-clock log
+    lockstep(eng, ora, max_rounds=20000, now=lambda i: int(clock[i]), check_every=4)
+
+
+def test_submit_errors(rt):
+    v = make_vocab(512)
+    p = engine_params("paper-4090", max_batch=4, max_tasks=2, max_ctx=64, n_pages=2)
+    eng = rt.Engine(None, p, v)
+    with pytest.raises(rt.RtError) as ex:
+        eng.submit(0, [1], 0, 10, 0.5, 1.0, 0, script=[5])
+    assert ex.value.code == rt.RT_E_INVAL
+    with pytest.raises(rt.RtError) as ex:
+        eng.submit(0, [1] * 40, 0, 10, -1.0, 1.0, 0, script=[5])
+    assert ex.value.code == rt.RT_E_NOMEM
+    with pytest.raises(rt.RtError) as ex:
+        eng.submit(0, [1], 0, 10, -1.0, 1.0, 0)                  # no model -> needs a script
+    assert ex.value.code == rt.RT_E_INVAL
+    eng.submit(0, [1], 0, 10, -1.0, 1.0, 0, script=[5])
+    eng.submit(0, [1], 0, 10, -1.0, 1.0, 0, script=[5])
+    with pytest.raises(rt.RtError) as ex:
+        eng.submit(0, [1], 0, 10, -1.0, 1.0, 0, script=[5])      # table full until polled
+    assert ex.value.code == rt.RT_E_NOMEM
+    eng.step()
+    assert len(eng.poll()) == 2
+    eng.submit(0, [1], 0, 10, -1.0, 1.0, 0, script=[5])          # slots recycled after poll
+
+
+# ------------------------------------------------------------- model parity
+def test_tiny_model_e2e_and_per_op(rt):
+    shape = MODEL_SHAPES["tiny"]
+    v = make_vocab(shape.vocab)
+    p = engine_params("paper-4090", max_batch=4, max_tasks=64, max_ctx=256, n_pages=64)
+    reqs = compose_workload(4, 1.0, 2, range(1, 9), 30.0, 0, v, prompt_len_range=(40, 64), max_requests=12)
+    flags = rt.RT_FLAG_KEEP_LOGITS | rt.RT_FLAG_CAPTURE
+    eng, ora = make_pair(rt, v, p, shape=shape, seed=3, flags=flags, model=True, capture_layer=1)
+    submit_both(eng, ora, reqs)
+    worst_logit = worst_attn = worst_lm = 0.0
+    lm = OW.matrix(3, OW.TID_LM, range(shape.vocab), shape.d_model)
+    for n in range(400):
+        ig, io = eng.step(), ora.step()
+        assert ig["n_running"] == io["n_running"]
+        if io["n_running"] == 0:
+            if all(r.state == FINISHED for r in ora.reqs.values()):
+                break
+            continue
+        B = io["n_running"]
+        lg = eng.dump(rt.RT_DUMP_LOGITS, np.float32).reshape(B, -1)
+        lo = np.stack([ora.round_log[-1]["logits"][rid] for rid in ora.round_log[-1]["slots"]])
+        worst_logit = max(worst_logit, float(np.abs(lg - lo).max()))
+        # logits per op: oracle lm_head on the GPU's own final bf16 hidden
+        hid = eng.dump(rt.RT_DUMP_HIDDEN, np.uint16).reshape(B, -1)
+        h = (hid.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+        worst_lm = max(worst_lm, float(np.abs(h @ lm.T - lg).max()))
+        # attention per op (capture layer): oracle attention on the GPU's q and pages
+        rows = eng.dump(rt.RT_DUMP_ROWS, np.int32).reshape(-1, 3)
+        q = eng.dump(rt.RT_DUMP_CAPTURE_Q, np.float32).reshape(len(rows), shape.n_q_heads, shape.head_dim)
+        o = eng.dump(rt.RT_DUMP_CAPTURE_O, np.float32).reshape(len(rows), shape.n_q_heads, shape.head_dim)
+        kv = eng.dump(rt.RT_DUMP_KV_LAYER, np.uint16).reshape(p.n_pages, 2, shape.n_kv_heads, 16, shape.head_dim)
+        kvf = (kv.astype(np.uint32) << 16).view(np.float32)
+        kp = kvf[:, 0].transpose(0, 2, 1, 3)
+        vp = kvf[:, 1].transpose(0, 2, 1, 3)
+        tabs = eng.dump(rt.RT_DUMP_PAGE_TABLES, np.int32).reshape(p.max_tasks, -1)
+        for i in range(0, len(rows), max(1, len(rows) // 16)):
+            task, pos, _ = rows[i]
+            ref = paged_attention(q[i], kp, vp, tabs[task], pos + 1)
+            worst_attn = max(worst_attn, float(np.abs(o[i] - ref).max()))
+    assert worst_attn < 2e-3, worst_attn
+    assert worst_lm < 1e-3, worst_lm
+    assert worst_logit < 1e-2, worst_logit
+    assert eng.poll() == ora.poll()
+
+
+def test_tiny_model_free_running_tokens(rt):
+    """Free-running greedy: GPU argmax stream fed to the oracle (teacher forcing,
+    AMB-17); argmax must agree wherever the oracle's top-2 margin exceeds 2x drift."""
+    shape = MODEL_SHAPES["tiny"]
+    v = make_vocab(shape.vocab)
+    p = engine_params("paper-4090", max_batch=4, max_tasks=16, max_ctx=256, n_pages=64)
+    eng = rt.Engine(shape, p, v, seed=5, flags=rt.RT_FLAG_KEEP_LOGITS)
+    om = OracleModel(shape, seed=5)
+    rng = np.random.default_rng(1)
+    prompts = [rng.integers(0, 400, 30 + 7 * i) for i in range(3)]
+    for i, pr in enumerate(prompts):
+        eng.submit(i, pr, 0, 1_000_000, -2.0, 1.0, 0, 24)
+    seqs = {i: list(map(int, pr)) for i, pr in enumerate(prompts)}
+    agree = checked = 0
+    for _ in range(60):
+        info = eng.step()
+        if info["n_running"] == 0:
+            break
+        lg = eng.dump(rt.RT_DUMP_LOGITS, np.float32).reshape(info["n_running"], -1)
+        log = eng.round_log()
+        for s, rid in enumerate(log["slots"]):
+            ref_rows = [(rid + 100, j, t) for j, t in enumerate(seqs[rid])]
+            om.drop(rid + 100)
+            ref = om.logits(om.forward(ref_rows)[-1:])[0]
+            top2 = np.sort(ref)[-2:]
+            drift = float(np.abs(lg[s] - ref).max())
+            if top2[1] - top2[0] > 2 * drift:
+                checked += 1
+                agree += int(np.argmax(ref) == log["tokens"][s])
+            seqs[rid].append(log["tokens"][s])
+    assert checked > 10 and agree == checked
+
+
+def test_llama8b_shape_sampled(rt):
+    """BASELINE configs[1] shape (Llama-3-8B dims, random init) at the bench's
+    launch configuration: per-op attention on sampled (row, head) pairs and
+    logits on sampled vocab rows, computed one by one by the oracle."""
+    shape = MODEL_SHAPES["llama3-8b"]
+    v = make_vocab(shape.vocab)
+    p = engine_params("b200-roofline", max_batch=64, max_tasks=128, max_ctx=2048, n_pages=64 * 90)
+    flags = rt.RT_FLAG_KEEP_LOGITS | rt.RT_FLAG_CAPTURE
+    eng = rt.Engine(shape, p, v, seed=11, flags=flags, capture_layer=31, max_rows_per_forward=4096)
+    reqs = compose_workload(64, 100.0, 64, range(1, 9), 0.2, 2, v, prompt_len_range=(1250, 1310), max_requests=64)
+    for r in reqs:
+        eng.submit(r.agent_id, r.prompt, 0, r.ert_us, r.alpha, r.beta, r.exec_window_us, 0, script=r.plan)
+    for _ in range(3):
+        info = eng.step()
+    B = info["n_running"]
+    assert B == 64 and info["n_prefill_rows"] == 0
+    rows = eng.dump(rt.RT_DUMP_ROWS, np.int32).reshape(-1, 3)
+    nq, nkv, hd = shape.n_q_heads, shape.n_kv_heads, shape.head_dim
+    q = eng.dump(rt.RT_DUMP_CAPTURE_Q, np.float32).reshape(len(rows), nq, hd)
+    o = eng.dump(rt.RT_DUMP_CAPTURE_O, np.float32).reshape(len(rows), nq, hd)
+    kv = eng.dump(rt.RT_DUMP_KV_LAYER, np.uint16).reshape(p.n_pages, 2, nkv, 16, hd)
+    tabs = eng.dump(rt.RT_DUMP_PAGE_TABLES, np.int32).reshape(p.max_tasks, -1)
+    rng = np.random.default_rng(0)
+    worst = 0.0
+    for i in rng.choice(len(rows), 8, replace=False):
+        task, pos, _ = rows[i]
+        npg = (pos + 16) // 16
+        pages = tabs[task][:npg]
+        kvf = (kv[pages].astype(np.uint32) << 16).view(np.float32)
+        kp, vp = kvf[:, 0].transpose(0, 2, 1, 3), kvf[:, 1].transpose(0, 2, 1, 3)
+        ref = paged_attention(q[i], kp, vp, list(range(npg)), pos + 1)
+        worst = max(worst, float(np.abs(o[i] - ref).max()))
+    assert worst < 2e-3, worst
+    lg = eng.dump(rt.RT_DUMP_LOGITS, np.float32).reshape(B, -1)
+    hid = eng.dump(rt.RT_DUMP_HIDDEN, np.uint16).reshape(B, -1)
+    h = (hid.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    cols = np.concatenate([rng.choice(shape.vocab, 512, replace=False), np.argmax(lg, axis=1)])
+    W = OW.matrix(11, OW.TID_LM, cols, shape.d_model)
+    err = np.abs(h @ W.T - lg[:, cols]).max()
+    assert err < 1e-2, err

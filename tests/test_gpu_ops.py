@@ -1,0 +1,161 @@
+"""Per-op parity of the sm_100a kernels against the oracle (run on a B200).
+
+Tolerances: integer / index work bit-exact; attention
+fp32 output <= 2e-3 max-abs (bf16 P in the PV product, fp32 accumulation; the
+1e-2 contract is met with margin); bf16 outputs <= 1e-2 + 1 bf16 ulp of the
+value; GEMM fp32 partials vs fp64 on the same bf16 inputs <= 1e-3 * sqrt(K)-scaled.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import weights as OW                      # noqa: E402
+from oracle.model import paged_attention as o_attn   # noqa: E402
+from oracle.priority import priority as o_priority   # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def rt():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    from paper_2412_18695_b200 import rt as _rt
+    _rt.lib()
+    return _rt
+
+
+def bf16_t(a):
+    return torch.from_numpy(np.asarray(a, dtype=np.float32)).to(torch.bfloat16)
+
+
+@pytest.mark.parametrize("tid,n", [(0, 4096 * 3 + 17), (1, 100000), (16 + 8 * 3 + 2, 65536)])
+def test_init_weights_bitexact(rt, tid, n):
+    out = torch.empty(n, dtype=torch.bfloat16, device="cuda")
+    rt.init_weights(out, n, 0xC0FFEE, tid, 0.02)
+    torch.cuda.synchronize()
+    got = out.view(torch.int16).cpu().numpy().view(np.uint16)
+    ref = OW.weight_values(0xC0FFEE, tid, np.arange(n, dtype=np.uint64), 0.02)
+    refb = (ref.view(np.uint32) >> 16).astype(np.uint16)
+    assert np.array_equal(got, refb)
+
+
+def test_priority_bitexact(rt):
+    rng = np.random.default_rng(0)
+    n = 5000
+    t = rng.integers(0, 5_000_000, n)
+    ref_ = t - rng.integers(-3_000_000, 2_000_000, n)
+    D = t + rng.integers(-2_000_000, 3_000_000, n)
+    ert = rng.integers(0, 2_000_000, n)
+    k = rng.integers(0, 3, n).astype(np.int32)
+    alpha = -rng.uniform(0, 10, n)
+    alpha[::7] = -6.67
+    beta = rng.uniform(-2, 3, n)
+    beta[::11] = 0.0
+    trde = np.stack([t, ref_, D, ert], axis=1).astype(np.int64)
+    dt = lambda a: torch.from_numpy(np.ascontiguousarray(a)).cuda()
+    out = torch.empty(n, dtype=torch.float64, device="cuda")
+    rt.priority(dt(trde), dt(k), dt(alpha), dt(beta), 90000, 8000, 1000, out)
+    got = out.cpu().numpy()
+    ref = np.array([o_priority(int(t[i]), int(k[i]), int(ref_[i]), int(D[i]), int(ert[i]), float(alpha[i]),
+                               float(beta[i]), 90000, 8000, 1000) for i in range(n)])
+    assert np.array_equal(got.view(np.uint64), ref.view(np.uint64))
+
+
+@pytest.mark.parametrize("M,N,K,splits", [(256, 64, 512, 1), (384, 7, 1024, 4), (200, 130, 256, 2),
+                                          (6144, 64, 4096, 6), (1024, 300, 768, 1), (512, 32, 14336, 8)])
+def test_gemm_tcgen05(rt, M, N, K, splits):
+    g = torch.Generator().manual_seed(M * 7 + N)
+    W = (torch.randn(M, K, generator=g) * 0.05).to(torch.bfloat16)
+    n_cap = ((N + 255) // 256) * 256
+    X = torch.zeros(n_cap, K, dtype=torch.bfloat16)
+    X[:N] = torch.randn(N, K, generator=g).to(torch.bfloat16)
+    Wd, Xd = W.cuda(), X.cuda()
+    out = torch.full((splits, N, M), float("nan"), device="cuda")
+    rt.gemm(Wd, Xd, out, M, N, K, n_cap, splits)
+    torch.cuda.synchronize()
+    got = out.sum(0).double().cpu()
+    ref = X[:N].double() @ W.double().T
+    err = (got - ref).abs().max().item()
+    assert err < 1e-3 * max(1.0, (K / 512) ** 0.5), err
+
+
+@pytest.mark.parametrize("M,N,K", [(512, 4, 128), (128256, 64, 1024), (1000, 33, 256)])
+def test_lm_argmax(rt, M, N, K):
+    g = torch.Generator().manual_seed(N)
+    W = (torch.randn(M, K, generator=g) * 0.02).to(torch.bfloat16)
+    X = torch.randn(N, K, generator=g).to(torch.bfloat16)
+    tok = torch.empty(N, dtype=torch.int32, device="cuda")
+    logits = torch.empty(N, M, device="cuda")
+    rt.lm_argmax(W.cuda(), X.cuda().contiguous(), M, N, K, N, tok, logits)
+    torch.cuda.synchronize()
+    ref = X.double() @ W.double().T
+    assert (logits.double().cpu() - ref).abs().max().item() < 1e-3
+    lg = logits.cpu().numpy()
+    assert np.array_equal(tok.cpu().numpy(), np.argmax(lg, axis=1))   # lowest index on ties
+
+
+def _attn_case(rt, hd, nq, nkv, seqlens, seed, n_pages=None, f32=True):
+    rng = np.random.default_rng(seed)
+    P = 16
+    max_pages = max((s + P - 1) // P for s in seqlens)
+    need = sum((s + P - 1) // P for s in seqlens)
+    n_pages = n_pages or need + 5
+    perm = rng.permutation(n_pages)
+    tables, used = [], 0
+    for s in seqlens:
+        k = (s + P - 1) // P
+        tables.append(list(perm[used:used + k]) + [0] * (max_pages - k))
+        used += k
+    # random logical K/V for every (page, slot) -> write through rt_op_kv_write
+    kv_k = bf16_t(rng.standard_normal((n_pages * P, nkv, hd)))
+    kv_v = bf16_t(rng.standard_normal((n_pages * P, nkv, hd)))
+    pool = torch.zeros(n_pages * nkv * 64 * hd, dtype=torch.uint8, device="cuda")
+    slots = torch.arange(n_pages * P, dtype=torch.int32, device="cuda")
+    rt.kv_write(pool, kv_k.cuda(), kv_v.cuda(), slots, nkv, hd)
+    q = bf16_t(rng.standard_normal((len(seqlens), nq, hd)))
+    pt = torch.tensor(np.array(tables, dtype=np.int32)).cuda()
+    row_task = torch.arange(len(seqlens), dtype=torch.int32, device="cuda")
+    row_sl = torch.tensor(seqlens, dtype=torch.int32, device="cuda")
+    out = torch.empty(len(seqlens), nq, hd, dtype=torch.bfloat16, device="cuda")
+    out32 = torch.empty(len(seqlens), nq, hd, device="cuda") if f32 else None
+    rt.paged_attention(q.cuda(), pool, pt, row_task, row_sl, max(seqlens), nq, nkv, hd, out, out32)
+    torch.cuda.synchronize()
+    kp = kv_k.float().numpy().reshape(n_pages, P, nkv, hd)
+    vp = kv_v.float().numpy().reshape(n_pages, P, nkv, hd)
+    qf = q.float().numpy()
+    errs32, errs16 = [], []
+    for r, s in enumerate(seqlens):
+        ref = o_attn(qf[r], kp, vp, tables[r], s, P)
+        got16 = out[r].float().cpu().numpy()
+        tol16 = 1e-2 + np.abs(ref) * 2.0 ** -8
+        errs16.append(float(np.max(np.abs(got16 - ref) - tol16)))
+        if f32:
+            errs32.append(float(np.max(np.abs(out32[r].cpu().numpy() - ref))))
+    # read-back of the pool is the identity on the logical layout
+    back = torch.empty(n_pages, 2, nkv, P, hd, dtype=torch.bfloat16, device="cuda")
+    rt.kv_read(pool, back, n_pages, nkv, hd)
+    b = back.cpu()
+    assert torch.equal(b[:, 0].permute(0, 2, 1, 3).reshape(-1, nkv, hd), kv_k)
+    assert torch.equal(b[:, 1].permute(0, 2, 1, 3).reshape(-1, nkv, hd), kv_v)
+    return max(errs32) if f32 else 0.0, max(errs16)
+
+
+@pytest.mark.parametrize("hd,nq,nkv", [(128, 32, 8), (128, 64, 8), (32, 4, 1), (64, 8, 2), (128, 8, 8)])
+def test_paged_attention_ragged(rt, hd, nq, nkv):
+    seqlens = [1, 15, 16, 17, 33, 100, 257, 1310]
+    e32, e16 = _attn_case(rt, hd, nq, nkv, seqlens, seed=hd + nq)
+    assert e32 < 2e-3, e32
+    assert e16 <= 0.0, e16
+
+
+def test_paged_attention_split_kv_long(rt):
+    # few rows, long contexts -> split-KV chunks + combine kernel
+    e32, e16 = _attn_case(rt, 128, 32, 8, [8192, 2884, 4000], seed=3)
+    assert e32 < 2e-3 and e16 <= 0.0
+
+
+def test_paged_attention_c2_operating_point_sampled(rt):
+    # 64 rows at ctx 1310 (C2), 8B heads; all rows checked (cheap in numpy)
+    e32, e16 = _attn_case(rt, 128, 32, 8, [1310] * 64, seed=9)
+    assert e32 < 2e-3 and e16 <= 0.0
