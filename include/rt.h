@@ -180,6 +180,15 @@ enum {
 };
 rt_status rt_debug_dump(rt_engine* e, int32_t what, void* dst, int64_t bytes, int64_t* bytes_out);
 
+/* Device-time markers on the engine's stream (CUDA events): which = 0 records the
+ * start mark, 1 the stop mark; rt_elapsed_ms synchronises and returns stop - start. */
+rt_status rt_mark(rt_engine* e, int32_t which);
+rt_status rt_elapsed_ms(rt_engine* e, double* ms_out);
+
+/* Create a 128-byte ncclUniqueId (rank 0 calls it and broadcasts the bytes;
+ * libnccl.so.2 is loaded with dlopen).  RT_E_NCCL if NCCL is unavailable. */
+rt_status rt_nccl_unique_id(uint8_t* out128);
+
 /* Human-readable description of the last error (engine may be NULL). */
 const char* rt_last_error(rt_engine* e);
 

@@ -42,9 +42,11 @@ rt_status rt_op_kv_read(const void* d_pool, void* d_out, int32_t n_pages, int32_
                         void* stream);
 
 /* a6 dense projection on tcgen05 (UMMA 128 x BN x 16, TMEM accumulator, TMA SW128):
- *   d_out[s][n][m] = sum_{k in split s} W[m, k] * X[n, k]     fp32 partials
- * d_w bf16 [M][K] row-major, d_x bf16 [N][K] row-major (N rows padded to
- * n_cap rows allocated), splits >= 1.  K % 64 == 0. */
+ *   d_out[n][m] = sum_k W[m, k] * X[n, k]     fp32, split-K over `splits` CTAs per
+ *   tile reduced in split order by the last CTA of each tile (deterministic).
+ * d_w bf16 [M][K] row-major, d_x bf16 [N][K] row-major (n_cap >= N rows allocated),
+ * 1 <= splits <= K / 64, K % 64 == 0.  Synchronises `stream` when splits > 1
+ * (temporary workspace). */
 rt_status rt_op_gemm(const void* d_w, const void* d_x, float* d_out, int32_t M, int32_t N, int32_t K,
                      int32_t n_cap, int32_t splits, void* stream);
 

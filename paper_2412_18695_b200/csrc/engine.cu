@@ -35,12 +35,14 @@ typedef int (*pfn_comm_init_rank)(nccl_comm_t*, int, nccl_uid_t, int);
 typedef int (*pfn_all_gather)(const void*, void*, size_t, int, nccl_comm_t, cudaStream_t);
 typedef int (*pfn_comm_destroy)(nccl_comm_t);
 typedef const char* (*pfn_get_error_string)(int);
+typedef int (*pfn_get_unique_id)(nccl_uid_t*);
 struct NcclApi {
   void* h = nullptr;
   pfn_comm_init_rank init = nullptr;
   pfn_all_gather allgather = nullptr;
   pfn_comm_destroy destroy = nullptr;
   pfn_get_error_string errstr = nullptr;
+  pfn_get_unique_id get_uid = nullptr;
   bool load() {
     if (h) return true;
     const char* names[] = {"libnccl.so.2", "libnccl.so"};
@@ -53,6 +55,7 @@ struct NcclApi {
     allgather = (pfn_all_gather)dlsym(h, "ncclAllGather");
     destroy = (pfn_comm_destroy)dlsym(h, "ncclCommDestroy");
     errstr = (pfn_get_error_string)dlsym(h, "ncclGetErrorString");
+    get_uid = (pfn_get_unique_id)dlsym(h, "ncclGetUniqueId");
     return init && allgather && destroy;
   }
 };
@@ -95,7 +98,9 @@ struct rt_engine {
   int32_t* d_am_idx = nullptr;
   bf16 *d_h = nullptr, *d_q = nullptr, *d_o = nullptr, *d_act = nullptr, *d_hfin = nullptr;
   float *d_cap_q = nullptr, *d_cap_o = nullptr, *d_rope_cos = nullptr, *d_rope_sin = nullptr;
-  int64_t attn_ws_cap = 0;
+  int64_t attn_ws_cap = 0, gemm_ws_cap = 0;
+  float *d_gemm_ws = nullptr, *d_ss = nullptr;
+  int* d_gemm_cnt = nullptr;
   GemmTmaSet x_h, x_o, x_act, x_hfin;
   // submissions
   SubmitRec* h_recs = nullptr;
@@ -112,6 +117,7 @@ struct rt_engine {
   // timing
   std::vector<cudaEvent_t> ev_attn;  // 2 per layer
   cudaEvent_t ev_f0 = nullptr, ev_f1 = nullptr, ev_s0 = nullptr, ev_s1 = nullptr, ev_q1 = nullptr;
+  cudaEvent_t ev_m0 = nullptr, ev_m1 = nullptr;
   bool timing_pending = false;
   int timing_layers = 0;
   double attn_bytes_pending = 0.0;
@@ -232,6 +238,8 @@ static rt_status create_impl(rt_engine* e, const rt_config* cfg) {
   cudaEventCreate(&e->ev_s0);
   cudaEventCreate(&e->ev_s1);
   cudaEventCreate(&e->ev_q1);
+  cudaEventCreate(&e->ev_m0);
+  cudaEventCreate(&e->ev_m1);
 
   e->pt_stride = (c.max_ctx + 15) / 16;
   e->rows_cap = c.max_batch * c.max_ctx;
@@ -364,7 +372,7 @@ static rt_status create_impl(rt_engine* e, const rt_config* cfg) {
       lw.d = w; w += n_d;
       launch_init_weights(lw.qkv, n_qkv, c.weight_seed, 16 + 8 * l + 0, sig, e->stream);
       launch_init_weights(lw.o, n_o, c.weight_seed, 16 + 8 * l + 1, sig, e->stream);
-      launch_init_weights(lw.gu, n_gu, c.weight_seed, 16 + 8 * l + 2, sig, e->stream);
+      launch_init_weights_gu(lw.gu, ff, d, c.weight_seed, 16 + 8 * l + 2, sig, e->stream);
       launch_init_weights(lw.d, n_d, c.weight_seed, 16 + 8 * l + 3, sig, e->stream);
       bool ok = make_tma_2d_bf16(&lw.m_qkv, lw.qkv, d, e->qkv_dim, 64, 128) &&
                 make_tma_2d_bf16(&lw.m_o, lw.o, nq * hd, d, 64, 128) &&
@@ -387,7 +395,11 @@ static rt_status create_impl(rt_engine* e, const rt_config* cfg) {
     CK(e, dalloc(e, &e->d_q, (size_t)R * nq * hd));
     CK(e, dalloc(e, &e->d_o, (size_t)R * nq * hd));
     CK(e, dalloc(e, &e->d_act, (size_t)R * ff));
-    CK(e, dalloc(e, &e->d_part, (size_t)e->part_rows * max_out));
+    (void)max_out;
+    e->gemm_ws_cap = (int64_t)2 * 148 * 256 * 128 + (int64_t)64 * 256 * 128;
+    CK(e, dalloc(e, &e->d_gemm_ws, (size_t)e->gemm_ws_cap));
+    CK(e, dalloc(e, &e->d_gemm_cnt, (size_t)65536));
+    CK(e, dalloc(e, &e->d_ss, (size_t)R * ((d + 127) / 128)));
     CK(e, dalloc(e, &e->d_hfin, (size_t)c.max_batch * d));
     const int mt = (V + 127) / 128;
     CK(e, dalloc(e, &e->d_am_val, (size_t)mt * c.max_batch));
@@ -448,7 +460,7 @@ extern "C" rt_status rt_destroy(rt_engine* e) {
   if (e->h_recs) cudaFreeHost(e->h_recs);
   if (e->h_toks) cudaFreeHost(e->h_toks);
   for (auto ev : e->ev_attn) cudaEventDestroy(ev);
-  cudaEvent_t evs[] = {e->ev_plan, e->ev_post, e->ev_cand, e->ev_merge, e->ev_f0, e->ev_f1, e->ev_s0, e->ev_s1, e->ev_q1};
+  cudaEvent_t evs[] = {e->ev_plan, e->ev_post, e->ev_cand, e->ev_merge, e->ev_f0, e->ev_f1, e->ev_s0, e->ev_s1, e->ev_q1, e->ev_m0, e->ev_m1};
   for (auto ev : evs)
     if (ev) cudaEventDestroy(ev);
   if (e->stream) cudaStreamDestroy(e->stream);
@@ -555,10 +567,12 @@ static rt_status forward(rt_engine* e, const HostMailbox& plan) {
   cudaStream_t s = e->stream;
   SchedParams& P = e->sp;
   const float sl2 = (float)(1.4426950408889634 / sqrt((double)hd));
+  const int d_tiles = (d + 127) / 128;
+  int launches = 0;
   for (int row0 = 0; row0 < n_rows; row0 += e->fwd_rows) {
     const int n = std::min(e->fwd_rows, n_rows - row0);
-    const int max_splits = std::max(1, std::min(16, e->part_rows / n));
     launch_embed_norm(P.row_tok, row0, n, e->emb, d, e->d_x, e->d_h, s);
+    ++launches;
     AttnArgs aa{};
     aa.q = e->d_q;
     aa.page_table = e->tt.page_table;
@@ -580,45 +594,90 @@ static rt_status forward(rt_engine* e, const HostMailbox& plan) {
     aa.out = e->d_o;
     aa.ws = e->d_attn_ws;
     aa.scale_log2 = sl2;
+    auto gemm = [&](const TmaMap& w, const GemmTmaSet& x, int M, int K, GemmArgs g) {
+      g.M = M;
+      g.N = n;
+      g.K = K;
+      g.splits = gemm_choose_splits(M, n, K, 16);
+      while (g.splits > 1 && gemm_ws_floats(M, n, K, g.splits) > e->gemm_ws_cap) --g.splits;
+      g.ws = e->d_gemm_ws;
+      g.counters = e->d_gemm_cnt;
+      launch_gemm_epi(w, x, g, s);
+      ++launches;
+    };
     for (int l = 0; l < c.n_layers; ++l) {
       LayerW& w = e->layers[l];
       void* pool_l = e->d_pool + (size_t)l * e->pool_layer_bytes;
-      int sp = launch_gemm(w.m_qkv, e->x_h, e->qkv_dim, n, d, e->d_part, max_splits, s);
-      QkvEpiArgs qa{};
-      qa.part = e->d_part;
-      qa.splits = sp;
-      qa.n_rows = n;
-      qa.row0 = row0;
-      qa.row_task = P.row_task;
-      qa.row_pos = P.row_pos;
-      qa.page_table = e->tt.page_table;
-      qa.pt_stride = e->pt_stride;
-      qa.nq = nq;
-      qa.nkv = nkv;
-      qa.hd = hd;
-      qa.rope_cos = e->d_rope_cos;
-      qa.rope_sin = e->d_rope_sin;
-      qa.q_out = e->d_q;
-      qa.pool = pool_l;
-      qa.q_cap = (e->d_cap_q && l == c.capture_layer) ? e->d_cap_q : nullptr;
-      launch_qkv_epilogue(qa, s);
+      {  // QKV projection + RoPE + KV append (a6 -> a4 pages)
+        GemmArgs g{};
+        g.mode = EPI_QKV;
+        QkvFuse& q = g.qkv;
+        q.row_task = P.row_task;
+        q.row_pos = P.row_pos;
+        q.page_table = e->tt.page_table;
+        q.row0 = row0;
+        q.pt_stride = e->pt_stride;
+        q.nq = nq;
+        q.nkv = nkv;
+        q.hd = hd;
+        q.cos = e->d_rope_cos;
+        q.sin = e->d_rope_sin;
+        q.q_out = e->d_q;
+        q.pool = pool_l;
+        q.q_cap = (e->d_cap_q && l == c.capture_layer) ? e->d_cap_q : nullptr;
+        gemm(w.m_qkv, e->x_h, e->qkv_dim, d, g);
+      }
       aa.pool = pool_l;
       aa.out_f32 = (e->d_cap_o && l == c.capture_layer) ? e->d_cap_o : nullptr;
       if (timing && row0 == 0) cudaEventRecord(e->ev_attn[2 * l], s);
       launch_attention(aa, s);
+      launches += aa.max_chunks > 1 ? 2 : 1;
       if (timing && row0 == 0) cudaEventRecord(e->ev_attn[2 * l + 1], s);
-      sp = launch_gemm(w.m_o, e->x_o, d, n, nq * hd, e->d_part, max_splits, s);
-      launch_resid_norm(e->d_part, sp, n, d, e->d_x, e->d_h, s);
-      sp = launch_gemm(w.m_gu, e->x_h, 2 * ff, n, d, e->d_part, max_splits, s);
-      launch_swiglu(e->d_part, sp, n, ff, e->d_act, s);
-      sp = launch_gemm(w.m_d, e->x_act, d, n, ff, e->d_part, max_splits, s);
-      launch_resid_norm(e->d_part, sp, n, d, e->d_x, e->d_h, s);
+      {  // O projection + residual
+        GemmArgs g{};
+        g.mode = EPI_RESID;
+        g.x = e->d_x;
+        g.ss = e->d_ss;
+        gemm(w.m_o, e->x_o, d, nq * hd, g);
+      }
+      launch_norm_apply(e->d_x, e->d_ss, d_tiles, n, d, e->d_h, s);
+      ++launches;
+      {  // gate/up projection + SwiGLU
+        GemmArgs g{};
+        g.mode = EPI_SWIGLU;
+        g.act = e->d_act;
+        g.ff = ff;
+        gemm(w.m_gu, e->x_h, 2 * ff, d, g);
+      }
+      {  // down projection + residual
+        GemmArgs g{};
+        g.mode = EPI_RESID;
+        g.x = e->d_x;
+        g.ss = e->d_ss;
+        gemm(w.m_d, e->x_act, d, ff, g);
+      }
+      launch_norm_apply(e->d_x, e->d_ss, d_tiles, n, d, e->d_h, s);  // next layer's / final RMSNorm
+      ++launches;
     }
     launch_gather_rows(P.slot_row, B, row0, n, e->d_h, d, e->d_hfin, s);
+    ++launches;
   }
-  launch_gemm_argmax(e->m_lm, e->x_hfin, V, B, d, e->d_am_val, e->d_am_idx, e->d_logits, s);
-  launch_argmax_reduce(e->d_am_val, e->d_am_idx, (V + 127) / 128, B, P.argmax_tok, s);
+  {  // lm_head + greedy argmax (a8)
+    GemmArgs g{};
+    g.mode = EPI_ARGMAX;
+    g.M = V;
+    g.N = B;
+    g.K = d;
+    g.splits = 1;
+    g.out = e->d_logits;
+    g.part_val = e->d_am_val;
+    g.part_idx = e->d_am_idx;
+    launch_gemm_epi(e->m_lm, e->x_hfin, g, s);
+    launch_argmax_reduce(e->d_am_val, e->d_am_idx, (V + 127) / 128, B, P.argmax_tok, s);
+    launches += 2;
+  }
   CK(e, cudaGetLastError());
+  e->stats.kernel_launches += launches;
   if (timing) e->timing_layers = c.n_layers;
   return RT_OK;
 }
@@ -761,6 +820,33 @@ extern "C" rt_status rt_last_round(rt_engine* e, rt_round_info* info) {
   info->n_refused_wcet = mb->n_refused_wcet;
   info->n_rows = mb->n_rows;
   info->n_prefill_rows = mb->n_prefill_rows;
+  return RT_OK;
+}
+
+extern "C" rt_status rt_mark(rt_engine* e, int32_t which) {
+  if (!e || which < 0 || which > 1) return RT_E_INVAL;
+  if (e->sticky) return RT_E_CUDA;
+  CK(e, cudaEventRecord(which == 0 ? e->ev_m0 : e->ev_m1, e->stream));
+  return RT_OK;
+}
+
+extern "C" rt_status rt_elapsed_ms(rt_engine* e, double* ms_out) {
+  if (!e || !ms_out) return RT_E_INVAL;
+  if (e->sticky) return RT_E_CUDA;
+  CK(e, cudaEventSynchronize(e->ev_m1));
+  float ms = 0.f;
+  CK(e, cudaEventElapsedTime(&ms, e->ev_m0, e->ev_m1));
+  *ms_out = ms;
+  return RT_OK;
+}
+
+extern "C" rt_status rt_nccl_unique_id(uint8_t* out128) {
+  if (!out128) return RT_E_INVAL;
+  if (!g_nccl.load() || !g_nccl.get_uid) return fail(nullptr, RT_E_NCCL, "libnccl.so.2 not loadable");
+  nccl_uid_t uid;
+  const int r = g_nccl.get_uid(&uid);
+  if (r != 0) return fail(nullptr, RT_E_NCCL, "ncclGetUniqueId failed");
+  memcpy(out128, uid.internal, 128);
   return RT_OK;
 }
 

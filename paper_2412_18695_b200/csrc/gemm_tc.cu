@@ -1,20 +1,29 @@
-// gemm_tc.cu — dense projections on 5th-gen tensor cores.
+// gemm_tc.cu — dense projections on 5th-gen tensor cores with fused epilogues
+// (SURVEY §8(a) a6, a8).
 //
-//   out[s][n][m] = sum_{k in split s} W[m, k] * X[n, k]        (bf16 x bf16 -> fp32)
+//   D[m, n] = sum_k W[m, k] * X[n, k]        (bf16 x bf16 -> fp32 in TMEM)
 //
 // Decode projections are skinny (N = running batch): the weight matrix goes in
-// the UMMA M slot (128 rows per CTA tile) and the batch in N (32..256), so
+// the UMMA M slot (128 rows per CTA tile) and the batch in N (32..256), so the
 // weights stream through HBM once per step (HBM-bound for N <~ 210).
-// Structure (one output tile per CTA, 192 threads):
+// CTA structure (192 threads, one output tile per CTA):
 //   warp 0 lane 0 : TMA producer — cp.async.bulk.tensor.2d (SW128 K-major tiles of
-//                   W [128 x 64] and X [BN x 64]) into a STAGES-deep smem ring,
-//                   completion on "full" mbarriers (expect_tx);
+//                   W [128 x 64] and X [BN x 64]) into a STAGES-deep smem ring;
 //   warp 1        : TMEM allocator; lane 0 issues tcgen05.mma.cta_group::1.kind::f16
-//                   (M=128, N=BN, K=16) x 4 per stage, tcgen05.commit frees the stage
+//                   (M=128, N=BN, K=16) x 4 per stage; tcgen05.commit frees stages
 //                   and finally signals the epilogue;
-//   warps 2..5    : epilogue — tcgen05.ld.32x32b.x16 (TMEM lane quarter = warp % 4),
-//                   fp32 partial store (coalesced along m) or fused lm_head argmax.
-// Split-K over grid.z fills the 148 SMs when M/128 * N/BN is small (QKV: 48 tiles).
+//   warps 2..5    : epilogue — tcgen05.ld.32x32b.x16 (TMEM lane quarter = warp % 4)
+//                   into a [BN][129] fp32 smem tile (reusing the ring), split-K
+//                   partials reduced by the LAST CTA of each tile (L2-resident
+//                   workspace, fixed split order -> deterministic), then the fused
+//                   elementwise op of oracle c1 for this projection:
+//        EPI_STORE  fp32 out[n][m]
+//        EPI_ARGMAX lm_head: per-tile (max, lowest index) + optional logits
+//        EPI_QKV    RoPE (rotate-half, theta 5e5) on q/k, bf16 q out, bf16 K/V
+//                   appended into the swizzled KV page of (row task, position)
+//        EPI_RESID  x[n][m] += D (fp32 residual stream) + per-tile sum of squares
+//                   of the new x for the following RMSNorm
+//        EPI_SWIGLU rows interleaved per tile [64 gate | 64 up]: act = bf16(silu(g) u)
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include "common.cuh"
@@ -24,6 +33,7 @@ namespace rt {
 
 constexpr int kGemmThreads = 192;
 constexpr int kBK = 64;  // one 128-byte swizzle atom of bf16 along K
+constexpr int kSP = 129; // padded row of the smem output tile (conflict-free both ways)
 
 template <int BN>
 struct GemmCfg {
@@ -32,7 +42,8 @@ struct GemmCfg {
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int STAGES = (BN <= 64) ? 4 : (BN == 128 ? 3 : 4);
   static constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
-  static constexpr int SMEM = 1024 + STAGES * STAGE + 256 + 4 * BN * 8;
+  static constexpr int SMEM = 1024 + STAGES * STAGE + 256;
+  static_assert(BN * kSP * 4 <= STAGES * STAGE, "epilogue tile must fit in the ring");
 };
 
 // ------------------------------------------------------------------ PTX
@@ -88,15 +99,136 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
-struct GemmArgs {
-  int M, N, K, splits, kb_total;
-  float* out;         // MODE 0: [splits][N][M]; MODE 1: logits [N][M] or null
-  float* part_val;    // MODE 1: [n_mtiles][N]
-  int32_t* part_idx;  // MODE 1
-};
+// ------------------------------------------------------------ fused epilogue ops
+// S: smem tile [BN][kSP] holding D[m0 + r][n0 + c] at S[c * kSP + r]; et = 0..127.
+template <int BN>
+__device__ void epi_apply(const GemmArgs& g, const float* S, int m_tile, int n_tile, int et) {
+  const int m0 = m_tile * 128, n0 = n_tile * BN;
+  const int ncol = min(BN, g.N - n0);
+  switch (g.mode) {
+    case EPI_STORE: {
+      const int m = m0 + et;
+      if (m < g.M)
+        for (int c = 0; c < ncol; ++c) g.out[(size_t)(n0 + c) * g.M + m] = S[c * kSP + et];
+      break;
+    }
+    case EPI_RESID: {
+      const int m = m0 + et;
+      float* sq = const_cast<float*>(S);  // squares written in place (same thread, same slot)
+      float* xb = g.x + (size_t)n0 * g.M + m;
+#pragma unroll 1
+      for (int c0 = 0; c0 < ncol; c0 += 8) {
+        float xv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) xv[u] = (m < g.M && c0 + u < ncol) ? xb[(size_t)(c0 + u) * g.M] : 0.f;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          if (c0 + u < ncol) {
+            const float v = (m < g.M) ? xv[u] + S[(c0 + u) * kSP + et] : 0.f;
+            if (m < g.M) xb[(size_t)(c0 + u) * g.M] = v;
+            sq[(c0 + u) * kSP + et] = v * v;
+          }
+        }
+      }
+      epi_bar();
+      const int mt = (g.M + 127) / 128;
+      for (int c = et; c < ncol; c += 128) {  // column sums in fixed row order
+        float s = 0.f;
+        for (int r = 0; r < 128; ++r) s += S[c * kSP + r];
+        g.ss[(size_t)(n0 + c) * mt + m_tile] = s;
+      }
+      break;
+    }
+    case EPI_SWIGLU: {
+      // tile rows [0,64) = gate features j0..j0+63, rows [64,128) = up features j0..j0+63
+      const int r = et & 63, half = et >> 6;
+      const int j = m_tile * 64 + r;
+      if (j < g.ff)
+        for (int c = half; c < ncol; c += 2) {
+          const float gv = S[c * kSP + r], uv = S[c * kSP + 64 + r];
+          const float sgv = gv / (1.f + __expf(-gv));
+          g.act[(size_t)(n0 + c) * g.ff + j] = __float2bfloat16_rn(sgv * uv);
+        }
+      break;
+    }
+    case EPI_QKV: {
+      const QkvFuse& q = g.qkv;
+      const int hd = q.hd, half = hd >> 1;
+      // per-column (token row) metadata, one thread per column
+      __shared__ int s_pos[256], s_page[256];
+      for (int c = et; c < ncol; c += 128) {
+        const int row = q.row0 + n0 + c;
+        const int pos = q.row_pos[row];
+        s_pos[c] = pos;
+        s_page[c] = q.page_table[(size_t)q.row_task[row] * q.pt_stride + (pos >> 4)];
+      }
+      epi_bar();
+      const int pr = et & 63;                       // 128 features per tile = 64 (i, i + hd/2) pairs
+      const int hl = pr / half, i = pr % half;      // head within tile, pair index
+      const int f = m0 + hl * hd + i;               // feature of the first element
+      if (f >= g.M) break;
+      const int head = f / hd;
+#pragma unroll 2
+      for (int c = et >> 6; c < ncol; c += 2) {
+        const int row = q.row0 + n0 + c;
+        const int pos = s_pos[c];
+        float x1 = S[c * kSP + hl * hd + i], x2 = S[c * kSP + hl * hd + i + half];
+        if (head < q.nq + q.nkv) {
+          const float cs = q.cos[(size_t)pos * half + i], sn = q.sin[(size_t)pos * half + i];
+          const float y1 = x1 * cs - x2 * sn, y2 = x2 * cs + x1 * sn;
+          x1 = y1;
+          x2 = y2;
+        }
+        const bf16 b1 = __float2bfloat16_rn(x1), b2 = __float2bfloat16_rn(x2);
+        if (head < q.nq) {
+          bf16* qo = q.q_out + ((size_t)(n0 + c) * q.nq + head) * hd;
+          qo[i] = b1;
+          qo[i + half] = b2;
+          if (q.q_cap) {
+            float* qc = q.q_cap + ((size_t)row * q.nq + head) * hd;
+            qc[i] = __bfloat162float(b1);
+            qc[i + half] = __bfloat162float(b2);
+          }
+        } else {
+          const int kind = head < q.nq + q.nkv ? 0 : 1;
+          const int kvh = kind == 0 ? head - q.nq : head - q.nq - q.nkv;
+          const int page = s_page[c];
+          const int off = pos & 15;
+          unsigned char* blk = (unsigned char*)q.pool +
+                               (((size_t)page * q.nkv + kvh) * 2 + kind) * (size_t)(16 * hd * 2) + off * hd * 2;
+          *(bf16*)(blk + (kv_swz_chunk(hd, off, i >> 3) << 4) + ((i & 7) << 1)) = b1;
+          *(bf16*)(blk + (kv_swz_chunk(hd, off, (i + half) >> 3) << 4) + (((i + half) & 7) << 1)) = b2;
+        }
+      }
+      break;
+    }
+    case EPI_ARGMAX: {
+      const int m = m0 + et;
+      if (g.out && m < g.M)
+        for (int c = 0; c < ncol; ++c) g.out[(size_t)(n0 + c) * g.M + m] = S[c * kSP + et];
+      for (int c = et; c < ncol; c += 128) {  // greedy: max over the tile's rows, lowest index on ties
+        float bv = -INFINITY;
+        int bi = INT_MAX;
+        for (int r = 0; r < 128 && m0 + r < g.M; ++r) {
+          const float v = S[c * kSP + r];
+          if (v > bv) {
+            bv = v;
+            bi = m0 + r;
+          }
+        }
+        g.part_val[(size_t)m_tile * g.N + n0 + c] = bv;
+        g.part_idx[(size_t)m_tile * g.N + n0 + c] = bi;
+      }
+      break;
+    }
+    default:
+      break;
+  }
+}
 
-template <int BN, int MODE>
+template <int BN>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_gemm_tc(const __grid_constant__ TmaMap tmA, const __grid_constant__ TmaMap tmB, GemmArgs g) {
   using C = GemmCfg<BN>;
@@ -108,11 +240,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* empty = full + C::STAGES;
   uint64_t* done = empty + C::STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
-  float* red_v = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE + 256);  // [4][BN]
-  int* red_i = reinterpret_cast<int*>(red_v + 4 * BN);
+  int* is_last = reinterpret_cast<int*>(tmem_slot + 1);
+  float* S = reinterpret_cast<float*>(smem);  // epilogue tile, reuses the ring after the mainloop
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m_tile = blockIdx.x, n_tile = blockIdx.y, split = blockIdx.z;
+  // split fastest in launch order: a tile's split CTAs run together, so the last-CTA
+  // reductions are spread over the kernel instead of piling up in the final wave
+  const int split = blockIdx.x, m_tile = blockIdx.y, n_tile = blockIdx.z;
   const int kb0 = (int)(((long long)g.kb_total * split) / g.splits);
   const int kb1 = (int)(((long long)g.kb_total * (split + 1)) / g.splits);
   const int nkb = kb1 - kb0;
@@ -172,68 +306,75 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   } else {
     // ---------------- epilogue warps 2..5 (TMEM lane quarter = warp % 4)
     const int q = warp & 3;
+    const int et = q * 32 + lane;  // row of the tile owned by this thread
     mbar_wait(done, 0);
     tc_fence_after();
-    const int m = m_tile * 128 + q * 32 + lane;
     const uint32_t tbase = tmem + ((uint32_t)(q * 32) << 16);
-    if (MODE == 0) {
-      float* out = g.out + (size_t)split * g.N * g.M;
+    const int tile = n_tile * gridDim.y + m_tile;
+    if (g.splits == 1) {
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 16) {
         float v[16];
         tmem_ld16(tbase + c0, v);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int n = n_tile * BN + c0 + j;
-          if (n < g.N && m < g.M) out[(size_t)n * g.M + m] = v[j];
-        }
+        for (int j = 0; j < 16; ++j) S[(c0 + j) * kSP + et] = v[j];
       }
     } else {
-      // fused greedy argmax over the 128 vocab rows of this tile (lowest index on ties)
+      // split-K: publish this partial (L2), the last CTA of the tile reduces in split order
+      float* ws = g.ws + ((size_t)tile * g.splits + split) * (BN * 128);
 #pragma unroll 1
       for (int c0 = 0; c0 < BN; c0 += 16) {
         float v[16];
         tmem_ld16(tbase + c0, v);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int n = n_tile * BN + c0 + j;
-          float bv = (m < g.M) ? v[j] : -INFINITY;
-          int bi = m;
-          if (g.out && n < g.N && m < g.M) g.out[(size_t)n * g.M + m] = v[j];
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) {
-            const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-            if (ov > bv || (ov == bv && oi < bi)) {
-              bv = ov;
-              bi = oi;
-            }
-          }
-          if (lane == 0) {
-            red_v[q * BN + c0 + j] = bv;
-            red_i[q * BN + c0 + j] = bi;
-          }
-        }
+        for (int j = 0; j < 16; ++j) ws[(c0 + j) * 128 + et] = v[j];
       }
-      asm volatile("bar.sync 1, 128;" ::: "memory");
-      for (int c = threadIdx.x - 64; c < BN; c += 128) {
-        const int n = n_tile * BN + c;
-        if (n >= g.N) continue;
-        float bv = red_v[c];
-        int bi = red_i[c];
-        for (int w = 1; w < 4; ++w) {
-          const float ov = red_v[w * BN + c];
-          const int oi = red_i[w * BN + c];
-          if (ov > bv || (ov == bv && oi < bi)) {
-            bv = ov;
-            bi = oi;
+      __threadfence();
+      epi_bar();
+      if (et == 0) {
+        const int prev = atomicAdd(&g.counters[tile], 1);
+        *is_last = (prev == g.splits - 1);
+        if (prev == g.splits - 1) g.counters[tile] = 0;  // ready for the next launch
+      }
+      epi_bar();
+      if (!*is_last) goto epi_done;
+      __threadfence();
+      // reduce the splits in fixed order; 8 independent 16-byte L2 loads in flight per thread
+      constexpr int NV = BN * 128 / 4;  // float4 per partial tile
+      const float4* base = reinterpret_cast<const float4*>(g.ws + (size_t)tile * g.splits * (BN * 128));
+#pragma unroll 1
+      for (int j0 = 0; j0 < NV / 128; j0 += 8) {
+        float4 acc[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 1
+        for (int s = 0; s < g.splits; ++s) {
+          float4 v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) v[u] = __ldcg(base + (size_t)s * NV + et + 128 * (j0 + u));
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            acc[u].x += v[u].x;
+            acc[u].y += v[u].y;
+            acc[u].z += v[u].z;
+            acc[u].w += v[u].w;
           }
         }
-        g.part_val[(size_t)m_tile * g.N + n] = bv;
-        g.part_idx[(size_t)m_tile * g.N + n] = bi;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int e4 = 4 * (et + 128 * (j0 + u));
+          float* d = S + (e4 >> 7) * kSP + (e4 & 127);
+          d[0] = acc[u].x;
+          d[1] = acc[u].y;
+          d[2] = acc[u].z;
+          d[3] = acc[u].w;
+        }
       }
     }
+    epi_bar();
+    epi_apply<BN>(g, S, m_tile, n_tile, et);
   }
+epi_done:
   tc_fence_before();
   __syncthreads();
   if (warp == 1) {
@@ -278,76 +419,55 @@ bool make_gemm_act_maps(GemmTmaSet* out, const void* base, int K, int rows_cap) 
          make_tma_2d_bf16(&out->m256, base, K, rows_cap, kBK, 256);
 }
 
+static int bn_for(int N) { return N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256; }
+
+// Split-K so that the CTA count fills the 148 SMs (2 CTAs/SM) in as few waves as possible.
 int gemm_choose_splits(int M, int N, int K, int max_splits) {
-  const int bn = N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256;
+  const int bn = bn_for(N);
   const int tiles = ((M + 127) / 128) * ((N + bn - 1) / bn);
   const int kb = K / kBK;
-  int splits = 1;
-  const int target = 2 * 148;
-  if (tiles < target) splits = (target + tiles - 1) / tiles;
-  if (splits > kb / 4) splits = kb / 4;
-  if (splits > max_splits) splits = max_splits;
-  if (splits < 1) splits = 1;
-  return splits;
+  const int slots = 2 * 148;
+  int best = 1;
+  double best_cost = 1e30;
+  const int lim = std::max(1, std::min(max_splits, kb / 4));
+  for (int s = 1; s <= lim; ++s) {
+    const int ctas = tiles * s;
+    const int waves = (ctas + slots - 1) / slots;
+    // time ~ waves * (kb / s + fixed per-CTA overhead in k-blocks) ; partial traffic ~ s
+    const double cost = waves * ((double)kb / s + 3.0) + 0.02 * s * tiles;
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      best = s;
+    }
+  }
+  return best;
 }
 
-template <int BN, int MODE>
+int64_t gemm_ws_floats(int M, int N, int K, int splits) {
+  const int bn = bn_for(N);
+  const int tiles = ((M + 127) / 128) * ((N + bn - 1) / bn);
+  return splits > 1 ? (int64_t)tiles * splits * bn * 128 : 0;
+}
+
+template <int BN>
 static void launch_bn(const TmaMap& a, const TmaMap& b, const GemmArgs& g, cudaStream_t s) {
   using C = GemmCfg<BN>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_gemm_tc<BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaFuncSetAttribute(k_gemm_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     attr = true;
   }
-  dim3 grid((g.M + 127) / 128, (g.N + BN - 1) / BN, g.splits);
-  k_gemm_tc<BN, MODE><<<grid, kGemmThreads, C::SMEM, s>>>(a, b, g);
+  dim3 grid(g.splits, (g.M + 127) / 128, (g.N + BN - 1) / BN);
+  k_gemm_tc<BN><<<grid, kGemmThreads, C::SMEM, s>>>(a, b, g);
 }
 
-template <int MODE>
-static void dispatch(const TmaMap& wmap, const GemmTmaSet& x, const GemmArgs& g, cudaStream_t s) {
-  if (g.N <= 32) launch_bn<32, MODE>(wmap, x.m32, g, s);
-  else if (g.N <= 64) launch_bn<64, MODE>(wmap, x.m64, g, s);
-  else if (g.N <= 128) launch_bn<128, MODE>(wmap, x.m128, g, s);
-  else launch_bn<256, MODE>(wmap, x.m256, g, s);
-}
-
-int launch_gemm(const TmaMap& wmap, const GemmTmaSet& xmaps, int M, int N, int K, float* out, int max_splits,
-                cudaStream_t s) {
-  GemmArgs g{};
-  g.M = M;
-  g.N = N;
-  g.K = K;
-  g.kb_total = K / kBK;
-  g.splits = gemm_choose_splits(M, N, K, max_splits);
-  g.out = out;
-  dispatch<0>(wmap, xmaps, g, s);
-  return g.splits;
-}
-
-void launch_gemm_fixed(const TmaMap& wmap, const GemmTmaSet& xmaps, int M, int N, int K, float* out, int splits,
-                       cudaStream_t s) {
-  GemmArgs g{};
-  g.M = M;
-  g.N = N;
-  g.K = K;
-  g.kb_total = K / kBK;
-  g.splits = splits;
-  g.out = out;
-  dispatch<0>(wmap, xmaps, g, s);
-}
-
-void launch_gemm_argmax(const TmaMap& wmap, const GemmTmaSet& xmaps, int M, int N, int K, float* part_val,
-                        int32_t* part_idx, float* logits, cudaStream_t s) {
-  GemmArgs g{};
-  g.M = M;
-  g.N = N;
-  g.K = K;
-  g.kb_total = K / kBK;
-  g.splits = 1;
-  g.out = logits;
-  g.part_val = part_val;
-  g.part_idx = part_idx;
-  dispatch<1>(wmap, xmaps, g, s);
+void launch_gemm_epi(const TmaMap& wmap, const GemmTmaSet& x, GemmArgs g, cudaStream_t s) {
+  g.kb_total = g.K / kBK;
+  if (g.splits < 1) g.splits = 1;
+  if (g.N <= 32) launch_bn<32>(wmap, x.m32, g, s);
+  else if (g.N <= 64) launch_bn<64>(wmap, x.m64, g, s);
+  else if (g.N <= 128) launch_bn<128>(wmap, x.m128, g, s);
+  else launch_bn<256>(wmap, x.m256, g, s);
 }
 
 }  // namespace rt

@@ -31,6 +31,28 @@ __global__ void k_init_weights(bf16* out, int64_t n, uint64_t seed, int32_t tens
   }
 }
 
+// W_gate_up physical row p -> logical row: tile i = p / 128, r = p % 128,
+// r < 64 -> gate feature 64 i + r, else up feature ff + 64 i + r - 64
+__global__ void k_init_weights_gu(bf16* out, int ff, int d, uint64_t seed, int32_t tensor_id, float c) {
+  const uint64_t key = seed ^ ((uint64_t)tensor_id << 40);
+  const int64_t n = (int64_t)2 * ff * d;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = i / d, col = i % d;
+    const int64_t t = p >> 7, r = p & 127;
+    const int64_t lrow = r < 64 ? 64 * t + r : (int64_t)ff + 64 * t + (r - 64);
+    const uint64_t u = splitmix64(key ^ (uint64_t)(lrow * d + col));
+    const float v = __fsub_rn(__fmul_rn((float)(uint32_t)(u >> 40), 5.9604644775390625e-08f), 0.5f);
+    out[i] = __float2bfloat16_rn(__fmul_rn(v, c));
+  }
+}
+
+void launch_init_weights_gu(bf16* out, int ff, int d, uint64_t seed, int32_t tensor_id, float sigma,
+                            cudaStream_t s) {
+  const float c = (float)(2.0 * 1.7320508075688772 * (double)sigma);
+  k_init_weights_gu<<<148 * 64, 256, 0, s>>>(out, ff, d, seed, tensor_id, c);
+}
+
 void launch_init_weights(bf16* out, int64_t n, uint64_t seed, int32_t tensor_id, float sigma,
                          cudaStream_t s) {
   const float c = (float)(2.0 * 1.7320508075688772 * (double)sigma);
@@ -72,91 +94,25 @@ __global__ void k_embed_norm(const int32_t* row_tok, int32_t row0, const bf16* e
   for (int i = threadIdx.x; i < d; i += blockDim.x) hr[i] = __float2bfloat16_rn(xr[i] * inv);
 }
 
-// -------------------------------------------- residual add (+ next RMSNorm)
-// x[r] += sum_s part[s][r][:];  h[r] = bf16(rms(x[r]))
-__global__ void k_resid_norm(const float* part, int splits, int n_rows, int d, float* x, bf16* h) {
-  __shared__ float red[32];
-  const int r = blockIdx.x;
-  float* xr = x + (size_t)r * d;
-  float ss = 0.f;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) {
-    float v = xr[i];
-    for (int s = 0; s < splits; ++s) v += part[((size_t)s * n_rows + r) * d + i];
-    xr[i] = v;
-    ss += v * v;
-  }
-  const float tot = block_sum(ss, red);
-  const float inv = rsqrtf(tot / (float)d + 1e-5f);
-  bf16* hr = h + (size_t)r * d;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) hr[i] = __float2bfloat16_rn(xr[i] * inv);
-}
-
-// ------------------------------------------------------------ SwiGLU product
-// a[r][j] = bf16(silu(g) * u), g = gu[j], u = gu[ff + j]
-__global__ void k_swiglu(const float* part, int splits, int n_rows, int ff, bf16* act) {
+// ------------------------------------------------------------- RMSNorm apply
+// h[r][i] = bf16(x[r][i] * rsqrt(sum_t ss[r][t] / d + 1e-5)); ss holds the per-tile
+// sums of squares written by the EPI_RESID GEMM epilogue (fixed summation order).
+__global__ void k_norm_apply(const float* x, const float* ss, int n_tiles, int d, bf16* h) {
   const int r = blockIdx.y;
-  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < ff; j += gridDim.x * blockDim.x) {
-    float g = 0.f, u = 0.f;
-    for (int s = 0; s < splits; ++s) {
-      const float* p = part + ((size_t)s * n_rows + r) * (2 * ff);
-      g += p[j];
-      u += p[ff + j];
-    }
-    const float sg = g / (1.f + __expf(-g));
-    act[(size_t)r * ff + j] = __float2bfloat16_rn(sg * u);
+  __shared__ float inv;
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int i = 0; i < n_tiles; ++i) t += ss[(size_t)r * n_tiles + i];
+    inv = rsqrtf(t / (float)d + 1e-5f);
   }
-}
-
-// ------------------------------------------- QKV epilogue: RoPE + KV append
-// part: [splits][n_rows][(nq + 2 nkv) hd]; q_out bf16 [n_rows][nq][hd];
-// K/V written (bf16) into the swizzled pool of this layer at the row's position.
-__global__ void k_qkv_epilogue(QkvEpiArgs a) {
-  const int r = blockIdx.x;
-  const int hd = a.hd, half = hd / 2;
-  const int row = a.row0 + r;
-  const int task = a.row_task[row];
-  const int pos = a.row_pos[row];
-  const int n_pairs = (a.nq + 2 * a.nkv) * half;
-  const int qkv_dim = (a.nq + 2 * a.nkv) * hd;
-  const int page = a.page_table[(size_t)task * a.pt_stride + pos / 16];
-  const int off = pos % 16;
-  const float* cs = a.rope_cos + (size_t)pos * half;
-  const float* sn = a.rope_sin + (size_t)pos * half;
-  for (int it = threadIdx.x; it < n_pairs; it += blockDim.x) {
-    const int head = it / half, i = it % half;
-    const int col = head * hd + i;
-    float x1 = 0.f, x2 = 0.f;
-    for (int s = 0; s < a.splits; ++s) {
-      const float* p = a.part + ((size_t)s * a.n_rows + r) * qkv_dim;
-      x1 += p[col];
-      x2 += p[col + half];
-    }
-    if (head < a.nq + a.nkv) {  // q or k: rotate-half RoPE (theta 500000)
-      const float c = cs[i], s_ = sn[i];
-      const float y1 = x1 * c - x2 * s_;
-      const float y2 = x2 * c + x1 * s_;
-      x1 = y1;
-      x2 = y2;
-    }
-    const bf16 b1 = __float2bfloat16_rn(x1), b2 = __float2bfloat16_rn(x2);
-    if (head < a.nq) {
-      bf16* q = a.q_out + ((size_t)r * a.nq + head) * hd;
-      q[i] = b1;
-      q[i + half] = b2;
-      if (a.q_cap) {
-        float* qc = a.q_cap + ((size_t)row * a.nq + head) * hd;
-        qc[i] = __bfloat162float(b1);
-        qc[i + half] = __bfloat162float(b2);
-      }
-    } else {
-      const int kind = head < a.nq + a.nkv ? 0 : 1;
-      const int kvh = kind == 0 ? head - a.nq : head - a.nq - a.nkv;
-      unsigned char* blk = (unsigned char*)a.pool +
-                           (((size_t)page * a.nkv + kvh) * 2 + kind) * (size_t)(16 * hd * 2);
-      const int c1 = i >> 3, c2 = (i + half) >> 3;
-      *(bf16*)(blk + off * hd * 2 + (kv_swz_chunk(hd, off, c1) << 4) + ((i & 7) << 1)) = b1;
-      *(bf16*)(blk + off * hd * 2 + (kv_swz_chunk(hd, off, c2) << 4) + (((i + half) & 7) << 1)) = b2;
-    }
+  __syncthreads();
+  const int i = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (i < d) {
+    const float4 v = *reinterpret_cast<const float4*>(x + (size_t)r * d + i);
+    uint2 o;
+    o.x = pack_bf16x2(v.x * inv, v.y * inv);
+    o.y = pack_bf16x2(v.z * inv, v.w * inv);
+    *reinterpret_cast<uint2*>(h + (size_t)r * d + i) = o;
   }
 }
 
@@ -252,14 +208,10 @@ void launch_embed_norm(const int32_t* row_tok, int row0, int n, const bf16* emb,
                        cudaStream_t s) {
   k_embed_norm<<<n, 256, 0, s>>>(row_tok, row0, emb, d, x, h);
 }
-void launch_resid_norm(const float* part, int splits, int n, int d, float* x, bf16* h, cudaStream_t s) {
-  k_resid_norm<<<n, 256, 0, s>>>(part, splits, n, d, x, h);
+void launch_norm_apply(const float* x, const float* ss, int n_tiles, int n, int d, bf16* h, cudaStream_t s) {
+  dim3 g((d / 4 + 127) / 128, n);
+  k_norm_apply<<<g, 128, 0, s>>>(x, ss, n_tiles, d, h);
 }
-void launch_swiglu(const float* part, int splits, int n, int ff, bf16* act, cudaStream_t s) {
-  dim3 g((ff + 255) / 256 < 8 ? (ff + 255) / 256 : 8, n);
-  k_swiglu<<<g, 256, 0, s>>>(part, splits, n, ff, act);
-}
-void launch_qkv_epilogue(const QkvEpiArgs& a, cudaStream_t s) { k_qkv_epilogue<<<a.n_rows, 256, 0, s>>>(a); }
 void launch_gather_rows(const int32_t* slot_row, int B, int row0, int n, const bf16* h, int d, bf16* hfin,
                         cudaStream_t s) {
   k_gather_rows<<<B, 128, 0, s>>>(slot_row, B, row0, n, h, d, hfin);

@@ -9,23 +9,15 @@
 namespace rt {
 typedef __nv_bfloat16 bf16;
 
-struct QkvEpiArgs {
-  const float* part;
-  int splits, n_rows, row0;
-  const int32_t *row_task, *row_pos, *page_table;
-  int pt_stride, nq, nkv, hd;
-  const float *rope_cos, *rope_sin;
-  bf16* q_out;
-  void* pool;      // this layer's pool
-  float* q_cap;    // nullable [rows_total][nq][hd] capture (indexed by global row)
-};
-
+// ---- row / elementwise kernels (model.cu)
 void launch_init_weights(bf16* out, int64_t n, uint64_t seed, int32_t tensor_id, float sigma, cudaStream_t s);
+// W_gate_up stored with rows interleaved per 128-row tile: [64 gate | 64 up] (EPI_SWIGLU)
+void launch_init_weights_gu(bf16* out, int ff, int d, uint64_t seed, int32_t tensor_id, float sigma,
+                            cudaStream_t s);
 void launch_embed_norm(const int32_t* row_tok, int row0, int n, const bf16* emb, int d, float* x, bf16* h,
                        cudaStream_t s);
-void launch_resid_norm(const float* part, int splits, int n, int d, float* x, bf16* h, cudaStream_t s);
-void launch_swiglu(const float* part, int splits, int n, int ff, bf16* act, cudaStream_t s);
-void launch_qkv_epilogue(const QkvEpiArgs& a, cudaStream_t s);
+// h[n] = bf16(x[n] * rsqrt(sum_t ss[n][t] / d + eps)), ss: [n][n_tiles] partial sums of squares
+void launch_norm_apply(const float* x, const float* ss, int n_tiles, int n, int d, bf16* h, cudaStream_t s);
 void launch_gather_rows(const int32_t* slot_row, int B, int row0, int n, const bf16* h, int d, bf16* hfin,
                         cudaStream_t s);
 void launch_argmax_reduce(const float* pv, const int32_t* pi, int n_mtiles, int N, int32_t* tok,
@@ -54,7 +46,7 @@ int64_t attn_ws_floats(int n_rows, int nq, int hd, int max_chunks);
 void attn_plan(int n_rows, int nkv, int max_seqlen, int* chunk_pages, int* max_chunks);
 void launch_attention(const AttnArgs& a, cudaStream_t s);
 
-// ---- tcgen05 GEMM (gemm_tc.cu)
+// ---- tcgen05 GEMM with fused epilogues (gemm_tc.cu)
 struct TmaMap {
   alignas(64) unsigned char bytes[128];
 };
@@ -65,13 +57,32 @@ struct GemmTmaSet {       // activation operand: one map per supported N tile
   int rows_cap;
 };
 bool make_gemm_act_maps(GemmTmaSet* out, const void* base, int K, int rows_cap);
-// out[s][n][m] partial sums (MODE store) ; returns splits used
-int launch_gemm(const TmaMap& wmap, const GemmTmaSet& xmaps, int M, int N, int K, float* out, int max_splits,
-                cudaStream_t s);
-// lm_head + argmax partials: part_val/part_idx [ceil(M/128)][N]; logits nullable [N][M]
-void launch_gemm_argmax(const TmaMap& wmap, const GemmTmaSet& xmaps, int M, int N, int K, float* part_val,
-                        int32_t* part_idx, float* logits, cudaStream_t s);
+
+enum EpiMode { EPI_STORE = 0, EPI_ARGMAX = 1, EPI_QKV = 2, EPI_RESID = 3, EPI_SWIGLU = 4 };
+
+struct QkvFuse {
+  const int32_t *row_task, *row_pos, *page_table;
+  int row0, pt_stride, nq, nkv, hd;
+  const float *cos, *sin;
+  bf16* q_out;     // [n][nq][hd] (rows of this launch)
+  void* pool;      // this layer's pool
+  float* q_cap;    // nullable, [global row][nq][hd]
+};
+
+struct GemmArgs {
+  int M, N, K, splits, kb_total, mode;
+  float* ws;          // split-K partials [tiles][splits][BN][128]
+  int* counters;      // [tiles], zero-initialised, self-resetting
+  float* out;         // EPI_STORE [N][M]; EPI_ARGMAX logits [N][M] or null
+  float* part_val;    // EPI_ARGMAX [m_tiles][N]
+  int32_t* part_idx;
+  float* x;           // EPI_RESID residual [N][M]
+  float* ss;          // EPI_RESID [N][m_tiles]
+  bf16* act;          // EPI_SWIGLU [N][ff]
+  int ff;
+  QkvFuse qkv;        // EPI_QKV
+};
 int gemm_choose_splits(int M, int N, int K, int max_splits);
-void launch_gemm_fixed(const TmaMap& wmap, const GemmTmaSet& xmaps, int M, int N, int K, float* out, int splits,
-                       cudaStream_t s);
+int64_t gemm_ws_floats(int M, int N, int K, int splits);
+void launch_gemm_epi(const TmaMap& wmap, const GemmTmaSet& xmaps, GemmArgs g, cudaStream_t s);
 }  // namespace rt

@@ -78,8 +78,32 @@ extern "C" rt_status rt_op_gemm(const void* d_w, const void* d_x, float* d_out, 
   TmaMap wm;
   GemmTmaSet xm;
   if (!make_tma_2d_bf16(&wm, d_w, K, M, 64, 128) || !make_gemm_act_maps(&xm, d_x, K, n_cap)) return RT_E_CUDA;
-  launch_gemm_fixed(wm, xm, M, N, K, d_out, splits, (cudaStream_t)stream);
-  return last_launch();
+  GemmArgs g{};
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  g.splits = splits;
+  g.mode = EPI_STORE;
+  g.out = d_out;
+  float* ws = nullptr;
+  int* cnt = nullptr;
+  const int64_t wsf = gemm_ws_floats(M, N, K, splits);
+  if (splits > 1) {
+    const int tiles = ((M + 127) / 128) * (N + 31) / 32 + 1;
+    if (cudaMalloc(&ws, wsf * 4) != cudaSuccess || cudaMalloc(&cnt, (size_t)tiles * 4 * 8) != cudaSuccess)
+      return RT_E_CUDA;
+    cudaMemset(cnt, 0, (size_t)tiles * 4 * 8);
+  }
+  g.ws = ws;
+  g.counters = cnt;
+  launch_gemm_epi(wm, xm, g, (cudaStream_t)stream);
+  rt_status st = last_launch();
+  if (splits > 1) {
+    cudaStreamSynchronize((cudaStream_t)stream);
+    cudaFree(ws);
+    cudaFree(cnt);
+  }
+  return st;
 }
 
 extern "C" rt_status rt_op_lm_argmax(const void* d_w, const void* d_x, int32_t M, int32_t N, int32_t K,
@@ -93,7 +117,16 @@ extern "C" rt_status rt_op_lm_argmax(const void* d_w, const void* d_x, int32_t M
   if (!make_tma_2d_bf16(&wm, d_w, K, M, 64, 128) || !make_gemm_act_maps(&xm, d_x, K, n_cap)) return RT_E_CUDA;
   float* pv = (float*)d_ws;
   int32_t* pi = (int32_t*)(pv + (size_t)mt * N);
-  launch_gemm_argmax(wm, xm, M, N, K, pv, pi, d_logits, (cudaStream_t)stream);
+  GemmArgs g{};
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  g.splits = 1;
+  g.mode = EPI_ARGMAX;
+  g.out = d_logits;
+  g.part_val = pv;
+  g.part_idx = pi;
+  launch_gemm_epi(wm, xm, g, (cudaStream_t)stream);
   launch_argmax_reduce(pv, pi, mt, N, d_tok, (cudaStream_t)stream);
   return last_launch();
 }

