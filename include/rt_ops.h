@@ -42,13 +42,20 @@ rt_status rt_op_kv_read(const void* d_pool, void* d_out, int32_t n_pages, int32_
                         void* stream);
 
 /* a6 dense projection on tcgen05 (UMMA 128 x BN x 16, TMEM accumulator, TMA SW128):
- *   d_out[n][m] = sum_k W[m, k] * X[n, k]     fp32, split-K over `splits` CTAs per
- *   tile reduced in split order by the last CTA of each tile (deterministic).
+ *   d_out[n][m] = sum_k W[m, k] * X[n, k]     fp32; split-K over a cluster of
+ *   `splits` CTAs per tile (1..16, <= K/64), reduced through distributed shared
+ *   memory in rank order (deterministic); splits <= 0 picks the engine's choice.
  * d_w bf16 [M][K] row-major, d_x bf16 [N][K] row-major (n_cap >= N rows allocated),
- * 1 <= splits <= K / 64, K % 64 == 0.  Synchronises `stream` when splits > 1
- * (temporary workspace). */
+ * K % 64 == 0. */
 rt_status rt_op_gemm(const void* d_w, const void* d_x, float* d_out, int32_t M, int32_t N, int32_t K,
                      int32_t n_cap, int32_t splits, void* stream);
+
+/* The engine's weight layout: pack a row-major bf16 [M][K] matrix into
+ * UMMA-ready 128 x 64 tiles (d_dst holds ceil(M/128)*128*K elements), and run the
+ * projection directly on a packed matrix (same semantics as rt_op_gemm). */
+rt_status rt_op_pack_tiled(const void* d_src, void* d_dst, int32_t M, int32_t K, void* stream);
+rt_status rt_op_gemm_tiled(const void* d_w_tiled, const void* d_x, float* d_out, int32_t M, int32_t N,
+                           int32_t K, int32_t n_cap, int32_t splits, void* stream);
 
 /* a8 lm_head + greedy argmax (lowest index on ties) over the vocabulary:
  * d_tok[n] = argmax_m sum_k W[m,k] X[n,k]; d_logits (nullable) fp32 [N][M]. */

@@ -40,6 +40,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32) k_attn(AttnArgs a) {
   extern __shared__ __align__(1024) unsigned char smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (C::RING > C::MERGE ? C::RING : C::MERGE));
 
+  if (threadIdx.x == 0) pdl_trigger();
   const int chunk = blockIdx.x, h = blockIdx.y, r = blockIdx.z;
   const int row = a.row0 + r;
   const int seqlen = a.row_seqlen ? a.row_seqlen[row] : a.row_pos[row] + 1;
@@ -67,6 +68,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32) k_attn(AttnArgs a) {
     fence_mbar_init();
   }
   __syncwarp();
+  pdl_wait();  // q and the KV pages come from the QKV GEMM that precedes this kernel
   // page ids of the first 32 pages of this warp, one per lane
   int my_page = (lane < n_my) ? ptab[p_begin + warp + lane * kAttnWarps] : 0;
 #pragma unroll
@@ -219,6 +221,8 @@ __global__ void __launch_bounds__(kAttnWarps * 32) k_attn(AttnArgs a) {
 // combine split-KV partials of rows with more than one chunk
 template <int HD>
 __global__ void k_attn_combine(AttnArgs a) {
+  if (threadIdx.x == 0) pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.x, qh = blockIdx.y;
   const int row = a.row0 + r;
   const int seqlen = a.row_seqlen ? a.row_seqlen[row] : a.row_pos[row] + 1;
@@ -270,8 +274,8 @@ static void launch_hd(const AttnArgs& a, cudaStream_t s) {
     attr = true;
   }
   dim3 grid(a.max_chunks, a.nkv, a.n_rows);
-  k_attn<HD><<<grid, kAttnWarps * 32, C::SMEM, s>>>(a);
-  if (a.max_chunks > 1) k_attn_combine<HD><<<dim3(a.n_rows, a.nq), 128, 0, s>>>(a);
+  launch_pdl(k_attn<HD>, grid, dim3(kAttnWarps * 32), C::SMEM, s, a);
+  if (a.max_chunks > 1) launch_pdl(k_attn_combine<HD>, dim3(a.n_rows, a.nq), dim3(128), 0, s, a);
 }
 
 void launch_attention(const AttnArgs& a, cudaStream_t s) {

@@ -64,7 +64,7 @@ static const int kNcclFloat64 = 8;
 
 struct LayerW {
   bf16 *qkv, *o, *gu, *d;
-  TmaMap m_qkv, m_o, m_gu, m_d;
+
 };
 
 struct rt_engine {
@@ -80,7 +80,7 @@ struct rt_engine {
   void* d_wbuf = nullptr;
   bf16 *emb = nullptr, *lm = nullptr;
   std::vector<LayerW> layers;
-  TmaMap m_lm;
+
   // KV pool
   unsigned char* d_pool = nullptr;
   // scheduler state
@@ -351,18 +351,20 @@ static rt_status create_impl(rt_engine* e, const rt_config* cfg) {
   // ---- model
   if (model) {
     const int ff = c.d_ff, V = c.vocab;
-    const size_t n_emb = (size_t)V * d, n_qkv = (size_t)e->qkv_dim * d, n_o = (size_t)d * nq * hd,
-                 n_gu = (size_t)2 * ff * d, n_d = (size_t)d * ff;
-    const size_t total = 2 * n_emb + L * (n_qkv + n_o + n_gu + n_d);
+    // projection weights live in the UMMA-tiled layout; the embedding is
+    // row-major (gathered by token id)
+    const size_t n_emb = (size_t)V * d, n_lm = tiled_elems(V, d), n_qkv = tiled_elems(e->qkv_dim, d),
+                 n_o = tiled_elems(d, nq * hd), n_gu = tiled_elems(2 * ff, d), n_d = tiled_elems(d, ff);
+    const size_t total = n_emb + n_lm + L * (n_qkv + n_o + n_gu + n_d);
     if (cudaMalloc(&e->d_wbuf, total * 2) != cudaSuccess) return done(fail(e, RT_E_NOMEM, "weights do not fit in HBM"));
     bf16* w = (bf16*)e->d_wbuf;
     const float sig = c.init_std > 0 ? c.init_std : 0.02f;
     e->emb = w;
     w += n_emb;
     e->lm = w;
-    w += n_emb;
+    w += n_lm;
     launch_init_weights(e->emb, n_emb, c.weight_seed, 0, sig, e->stream);
-    launch_init_weights(e->lm, n_emb, c.weight_seed, 1, sig, e->stream);
+    launch_init_weights_tiled(e->lm, V, d, 0, c.weight_seed, 1, sig, e->stream);
     e->layers.resize(L);
     for (int l = 0; l < L; ++l) {
       LayerW& lw = e->layers[l];
@@ -370,17 +372,11 @@ static rt_status create_impl(rt_engine* e, const rt_config* cfg) {
       lw.o = w; w += n_o;
       lw.gu = w; w += n_gu;
       lw.d = w; w += n_d;
-      launch_init_weights(lw.qkv, n_qkv, c.weight_seed, 16 + 8 * l + 0, sig, e->stream);
-      launch_init_weights(lw.o, n_o, c.weight_seed, 16 + 8 * l + 1, sig, e->stream);
-      launch_init_weights_gu(lw.gu, ff, d, c.weight_seed, 16 + 8 * l + 2, sig, e->stream);
-      launch_init_weights(lw.d, n_d, c.weight_seed, 16 + 8 * l + 3, sig, e->stream);
-      bool ok = make_tma_2d_bf16(&lw.m_qkv, lw.qkv, d, e->qkv_dim, 64, 128) &&
-                make_tma_2d_bf16(&lw.m_o, lw.o, nq * hd, d, 64, 128) &&
-                make_tma_2d_bf16(&lw.m_gu, lw.gu, d, 2 * ff, 64, 128) &&
-                make_tma_2d_bf16(&lw.m_d, lw.d, ff, d, 64, 128);
-      if (!ok) return done(fail(e, RT_E_CUDA, "cuTensorMapEncodeTiled failed (weights)"));
+      launch_init_weights_tiled(lw.qkv, e->qkv_dim, d, 0, c.weight_seed, 16 + 8 * l + 0, sig, e->stream);
+      launch_init_weights_tiled(lw.o, d, nq * hd, 0, c.weight_seed, 16 + 8 * l + 1, sig, e->stream);
+      launch_init_weights_tiled(lw.gu, 2 * ff, d, ff, c.weight_seed, 16 + 8 * l + 2, sig, e->stream);
+      launch_init_weights_tiled(lw.d, d, ff, 0, c.weight_seed, 16 + 8 * l + 3, sig, e->stream);
     }
-    if (!make_tma_2d_bf16(&e->m_lm, e->lm, d, V, 64, 128)) return done(fail(e, RT_E_CUDA, "tensor map lm_head"));
     // KV pool
     e->pool_layer_bytes = (int64_t)n_pages * nkv * 64 * hd;
     if (cudaMalloc(&e->d_pool, (size_t)e->pool_layer_bytes * L) != cudaSuccess)
@@ -396,9 +392,6 @@ static rt_status create_impl(rt_engine* e, const rt_config* cfg) {
     CK(e, dalloc(e, &e->d_o, (size_t)R * nq * hd));
     CK(e, dalloc(e, &e->d_act, (size_t)R * ff));
     (void)max_out;
-    e->gemm_ws_cap = (int64_t)2 * 148 * 256 * 128 + (int64_t)64 * 256 * 128;
-    CK(e, dalloc(e, &e->d_gemm_ws, (size_t)e->gemm_ws_cap));
-    CK(e, dalloc(e, &e->d_gemm_cnt, (size_t)65536));
     CK(e, dalloc(e, &e->d_ss, (size_t)R * ((d + 127) / 128)));
     CK(e, dalloc(e, &e->d_hfin, (size_t)c.max_batch * d));
     const int mt = (V + 127) / 128;
@@ -594,15 +587,11 @@ static rt_status forward(rt_engine* e, const HostMailbox& plan) {
     aa.out = e->d_o;
     aa.ws = e->d_attn_ws;
     aa.scale_log2 = sl2;
-    auto gemm = [&](const TmaMap& w, const GemmTmaSet& x, int M, int K, GemmArgs g) {
+    auto gemm = [&](const bf16* w, const GemmTmaSet& x, int M, int K, GemmArgs g) {
       g.M = M;
       g.N = n;
       g.K = K;
-      g.splits = gemm_choose_splits(M, n, K, 16);
-      while (g.splits > 1 && gemm_ws_floats(M, n, K, g.splits) > e->gemm_ws_cap) --g.splits;
-      g.ws = e->d_gemm_ws;
-      g.counters = e->d_gemm_cnt;
-      launch_gemm_epi(w, x, g, s);
+      launch_gemm_epi(w, x, g, 0, s);
       ++launches;
     };
     for (int l = 0; l < c.n_layers; ++l) {
@@ -625,7 +614,7 @@ static rt_status forward(rt_engine* e, const HostMailbox& plan) {
         q.q_out = e->d_q;
         q.pool = pool_l;
         q.q_cap = (e->d_cap_q && l == c.capture_layer) ? e->d_cap_q : nullptr;
-        gemm(w.m_qkv, e->x_h, e->qkv_dim, d, g);
+        gemm(w.qkv, e->x_h, e->qkv_dim, d, g);
       }
       aa.pool = pool_l;
       aa.out_f32 = (e->d_cap_o && l == c.capture_layer) ? e->d_cap_o : nullptr;
@@ -638,7 +627,7 @@ static rt_status forward(rt_engine* e, const HostMailbox& plan) {
         g.mode = EPI_RESID;
         g.x = e->d_x;
         g.ss = e->d_ss;
-        gemm(w.m_o, e->x_o, d, nq * hd, g);
+        gemm(w.o, e->x_o, d, nq * hd, g);
       }
       launch_norm_apply(e->d_x, e->d_ss, d_tiles, n, d, e->d_h, s);
       ++launches;
@@ -647,14 +636,14 @@ static rt_status forward(rt_engine* e, const HostMailbox& plan) {
         g.mode = EPI_SWIGLU;
         g.act = e->d_act;
         g.ff = ff;
-        gemm(w.m_gu, e->x_h, 2 * ff, d, g);
+        gemm(w.gu, e->x_h, 2 * ff, d, g);
       }
       {  // down projection + residual
         GemmArgs g{};
         g.mode = EPI_RESID;
         g.x = e->d_x;
         g.ss = e->d_ss;
-        gemm(w.m_d, e->x_act, d, ff, g);
+        gemm(w.d, e->x_act, d, ff, g);
       }
       launch_norm_apply(e->d_x, e->d_ss, d_tiles, n, d, e->d_h, s);  // next layer's / final RMSNorm
       ++launches;
@@ -668,11 +657,10 @@ static rt_status forward(rt_engine* e, const HostMailbox& plan) {
     g.M = V;
     g.N = B;
     g.K = d;
-    g.splits = 1;
     g.out = e->d_logits;
     g.part_val = e->d_am_val;
     g.part_idx = e->d_am_idx;
-    launch_gemm_epi(e->m_lm, e->x_hfin, g, s);
+    launch_gemm_epi(e->lm, e->x_hfin, g, 0, s);
     launch_argmax_reduce(e->d_am_val, e->d_am_idx, (V + 127) / 128, B, P.argmax_tok, s);
     launches += 2;
   }

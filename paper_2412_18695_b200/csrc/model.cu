@@ -53,6 +53,71 @@ void launch_init_weights_gu(bf16* out, int ff, int d, uint64_t seed, int32_t ten
   k_init_weights_gu<<<148 * 64, 256, 0, s>>>(out, ff, d, seed, tensor_id, c);
 }
 
+// ------------------------------------------- UMMA-tiled weight layout
+// A [M, K] weight is stored as contiguous 128 x 64 bf16 tiles (16 KiB), tile (mt, kb)
+// at index mt * KB + kb, each tile in the SW128 K-major smem image: row r, 16-byte
+// chunk c stored at chunk c ^ (r & 7).  One cp.async.bulk of 16 KiB per k-block
+// lands a ready UMMA operand; a CTA streams one contiguous HBM range.
+// Logical row of tiled row p (gu_ff > 0: gate/up interleave [64 gate | 64 up] per tile).
+__device__ __forceinline__ int64_t tiled_logical_row(int64_t p, int gu_ff) {
+  if (gu_ff <= 0) return p;
+  const int64_t t = p >> 7, r = p & 127;
+  return r < 64 ? 64 * t + r : (int64_t)gu_ff + 64 * t + (r - 64);
+}
+// element i of the tiled buffer -> (physical row p, logical column col)
+__device__ __forceinline__ void tiled_coords(int64_t i, int KB, int64_t* p, int* col) {
+  const int64_t tile = i >> 13;            // 8192 elements per tile
+  const int rem = (int)(i & 8191);
+  const int r = rem >> 6, pc = (rem >> 3) & 7, e = rem & 7;
+  const int64_t mt = tile / KB, kb = tile % KB;
+  *p = mt * 128 + r;
+  *col = (int)(kb * 64 + ((pc ^ (r & 7)) << 3) + e);
+}
+
+__global__ void k_init_weights_tiled(bf16* out, int M, int K, int gu_ff, uint64_t seed, int32_t tensor_id,
+                                     float c) {
+  const uint64_t key = seed ^ ((uint64_t)tensor_id << 40);
+  const int KB = K / 64;
+  const int64_t n = (int64_t)((M + 127) / 128) * 128 * K;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t p;
+    int col;
+    tiled_coords(i, KB, &p, &col);
+    if (p >= M) {
+      out[i] = __float2bfloat16_rn(0.f);
+      continue;
+    }
+    const int64_t lrow = tiled_logical_row(p, gu_ff);
+    const uint64_t u = splitmix64(key ^ (uint64_t)(lrow * K + col));
+    const float v = __fsub_rn(__fmul_rn((float)(uint32_t)(u >> 40), 5.9604644775390625e-08f), 0.5f);
+    out[i] = __float2bfloat16_rn(__fmul_rn(v, c));
+  }
+}
+
+void launch_init_weights_tiled(bf16* out, int M, int K, int gu_ff, uint64_t seed, int32_t tensor_id, float sigma,
+                               cudaStream_t s) {
+  const float c = (float)(2.0 * 1.7320508075688772 * (double)sigma);
+  k_init_weights_tiled<<<148 * 64, 256, 0, s>>>(out, M, K, gu_ff, seed, tensor_id, c);
+}
+
+// row-major [M, K] -> tiled (zero-padded rows); used by the op-level GEMM entry points
+__global__ void k_pack_tiled(const bf16* src, bf16* dst, int M, int K) {
+  const int KB = K / 64;
+  const int64_t n = (int64_t)((M + 127) / 128) * 128 * K;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t p;
+    int col;
+    tiled_coords(i, KB, &p, &col);
+    dst[i] = p < M ? src[p * K + col] : __float2bfloat16_rn(0.f);
+  }
+}
+
+void launch_pack_tiled(const bf16* src, bf16* dst, int M, int K, cudaStream_t s) {
+  k_pack_tiled<<<148 * 16, 256, 0, s>>>(src, dst, M, K);
+}
+
 void launch_init_weights(bf16* out, int64_t n, uint64_t seed, int32_t tensor_id, float sigma,
                          cudaStream_t s) {
   const float c = (float)(2.0 * 1.7320508075688772 * (double)sigma);
@@ -98,6 +163,8 @@ __global__ void k_embed_norm(const int32_t* row_tok, int32_t row0, const bf16* e
 // h[r][i] = bf16(x[r][i] * rsqrt(sum_t ss[r][t] / d + 1e-5)); ss holds the per-tile
 // sums of squares written by the EPI_RESID GEMM epilogue (fixed summation order).
 __global__ void k_norm_apply(const float* x, const float* ss, int n_tiles, int d, bf16* h) {
+  if (threadIdx.x == 0) pdl_trigger();
+  pdl_wait();
   const int r = blockIdx.y;
   __shared__ float inv;
   if (threadIdx.x == 0) {
@@ -210,7 +277,7 @@ void launch_embed_norm(const int32_t* row_tok, int row0, int n, const bf16* emb,
 }
 void launch_norm_apply(const float* x, const float* ss, int n_tiles, int n, int d, bf16* h, cudaStream_t s) {
   dim3 g((d / 4 + 127) / 128, n);
-  k_norm_apply<<<g, 128, 0, s>>>(x, ss, n_tiles, d, h);
+  launch_pdl(k_norm_apply, g, dim3(128), 0, s, x, ss, n_tiles, d, h);
 }
 void launch_gather_rows(const int32_t* slot_row, int B, int row0, int n, const bf16* h, int d, bf16* hfin,
                         cudaStream_t s) {

@@ -14,6 +14,12 @@ void launch_init_weights(bf16* out, int64_t n, uint64_t seed, int32_t tensor_id,
 // W_gate_up stored with rows interleaved per 128-row tile: [64 gate | 64 up] (EPI_SWIGLU)
 void launch_init_weights_gu(bf16* out, int ff, int d, uint64_t seed, int32_t tensor_id, float sigma,
                             cudaStream_t s);
+// UMMA-tiled weights: 128 x 64 bf16 tiles (16 KiB, SW128 image), tile (mt, kb) at mt*KB+kb;
+// gu_ff > 0 interleaves gate/up rows per tile.  Buffer size ceil(M/128)*128*K elements.
+void launch_init_weights_tiled(bf16* out, int M, int K, int gu_ff, uint64_t seed, int32_t tensor_id, float sigma,
+                               cudaStream_t s);
+void launch_pack_tiled(const bf16* src, bf16* dst, int M, int K, cudaStream_t s);
+inline int64_t tiled_elems(int M, int K) { return (int64_t)((M + 127) / 128) * 128 * K; }
 void launch_embed_norm(const int32_t* row_tok, int row0, int n, const bf16* emb, int d, float* x, bf16* h,
                        cudaStream_t s);
 // h[n] = bf16(x[n] * rsqrt(sum_t ss[n][t] / d + eps)), ss: [n][n_tiles] partial sums of squares
@@ -70,9 +76,8 @@ struct QkvFuse {
 };
 
 struct GemmArgs {
-  int M, N, K, splits, kb_total, mode;
-  float* ws;          // split-K partials [tiles][splits][BN][128]
-  int* counters;      // [tiles], zero-initialised, self-resetting
+  const bf16* w;      // UMMA-tiled weights (launch_init_weights_tiled / launch_pack_tiled)
+  int M, N, K, kb_total, m_tiles, mode;
   float* out;         // EPI_STORE [N][M]; EPI_ARGMAX logits [N][M] or null
   float* part_val;    // EPI_ARGMAX [m_tiles][N]
   int32_t* part_idx;
@@ -82,7 +87,8 @@ struct GemmArgs {
   int ff;
   QkvFuse qkv;        // EPI_QKV
 };
-int gemm_choose_splits(int M, int N, int K, int max_splits);
-int64_t gemm_ws_floats(int M, int N, int K, int splits);
-void launch_gemm_epi(const TmaMap& wmap, const GemmTmaSet& xmaps, GemmArgs g, cudaStream_t s);
+int gemm_bn(int N);
+int gemm_choose_splits(int M, int N, int K);   // cluster split-K factor (1..16)
+// splits <= 0: gemm_choose_splits
+cudaError_t launch_gemm_epi(const bf16* w_tiled, const GemmTmaSet& xmaps, GemmArgs g, int splits, cudaStream_t s);
 }  // namespace rt

@@ -2,6 +2,7 @@
 // device buffers, for per-op parity tests and microbenchmarks.
 #include <cuda_runtime.h>
 #include <math.h>
+#include <algorithm>
 #include "rt_ops.h"
 #include "internal.h"
 #include "model.h"
@@ -75,35 +76,43 @@ extern "C" rt_status rt_op_kv_read(const void* d_pool, void* d_out, int32_t n_pa
 extern "C" rt_status rt_op_gemm(const void* d_w, const void* d_x, float* d_out, int32_t M, int32_t N, int32_t K,
                                 int32_t n_cap, int32_t splits, void* stream) {
   if (M < 1 || N < 1 || K < 64 || K % 64 || n_cap < N || splits < 1 || splits > K / 64) return RT_E_INVAL;
-  TmaMap wm;
   GemmTmaSet xm;
-  if (!make_tma_2d_bf16(&wm, d_w, K, M, 64, 128) || !make_gemm_act_maps(&xm, d_x, K, n_cap)) return RT_E_CUDA;
+  if (!make_gemm_act_maps(&xm, d_x, K, n_cap)) return RT_E_CUDA;
+  bf16* wt = nullptr;  // the engine keeps weights UMMA-tiled; pack the caller's row-major W
+  if (cudaMalloc(&wt, tiled_elems(M, K) * 2) != cudaSuccess) return RT_E_CUDA;
+  launch_pack_tiled((const bf16*)d_w, wt, M, K, (cudaStream_t)stream);
   GemmArgs g{};
   g.M = M;
   g.N = N;
   g.K = K;
-  g.splits = splits;
   g.mode = EPI_STORE;
   g.out = d_out;
-  float* ws = nullptr;
-  int* cnt = nullptr;
-  const int64_t wsf = gemm_ws_floats(M, N, K, splits);
-  if (splits > 1) {
-    const int tiles = ((M + 127) / 128) * (N + 31) / 32 + 1;
-    if (cudaMalloc(&ws, wsf * 4) != cudaSuccess || cudaMalloc(&cnt, (size_t)tiles * 4 * 8) != cudaSuccess)
-      return RT_E_CUDA;
-    cudaMemset(cnt, 0, (size_t)tiles * 4 * 8);
-  }
-  g.ws = ws;
-  g.counters = cnt;
-  launch_gemm_epi(wm, xm, g, (cudaStream_t)stream);
+  launch_gemm_epi(wt, xm, g, splits, (cudaStream_t)stream);
   rt_status st = last_launch();
-  if (splits > 1) {
-    cudaStreamSynchronize((cudaStream_t)stream);
-    cudaFree(ws);
-    cudaFree(cnt);
-  }
+  cudaStreamSynchronize((cudaStream_t)stream);
+  cudaFree(wt);
   return st;
+}
+
+extern "C" rt_status rt_op_pack_tiled(const void* d_src, void* d_dst, int32_t M, int32_t K, void* stream) {
+  if (M < 1 || K < 64 || K % 64) return RT_E_INVAL;
+  launch_pack_tiled((const bf16*)d_src, (bf16*)d_dst, M, K, (cudaStream_t)stream);
+  return last_launch();
+}
+
+extern "C" rt_status rt_op_gemm_tiled(const void* d_w_tiled, const void* d_x, float* d_out, int32_t M, int32_t N,
+                                      int32_t K, int32_t n_cap, int32_t splits, void* stream) {
+  if (M < 1 || N < 1 || K < 64 || K % 64 || n_cap < N || splits < 0 || splits > K / 64) return RT_E_INVAL;
+  GemmTmaSet xm;
+  if (!make_gemm_act_maps(&xm, d_x, K, n_cap)) return RT_E_CUDA;
+  GemmArgs g{};
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  g.mode = EPI_STORE;
+  g.out = d_out;
+  launch_gemm_epi((const bf16*)d_w_tiled, xm, g, splits, (cudaStream_t)stream);
+  return last_launch();
 }
 
 extern "C" rt_status rt_op_lm_argmax(const void* d_w, const void* d_x, int32_t M, int32_t N, int32_t K,
@@ -112,23 +121,27 @@ extern "C" rt_status rt_op_lm_argmax(const void* d_w, const void* d_x, int32_t M
   if (M < 1 || N < 1 || K < 64 || K % 64 || n_cap < N) return RT_E_INVAL;
   const int mt = (M + 127) / 128;
   if (ws_bytes < (int64_t)mt * N * 8) return RT_E_INVAL;
-  TmaMap wm;
   GemmTmaSet xm;
-  if (!make_tma_2d_bf16(&wm, d_w, K, M, 64, 128) || !make_gemm_act_maps(&xm, d_x, K, n_cap)) return RT_E_CUDA;
+  if (!make_gemm_act_maps(&xm, d_x, K, n_cap)) return RT_E_CUDA;
+  bf16* wt = nullptr;
+  if (cudaMalloc(&wt, tiled_elems(M, K) * 2) != cudaSuccess) return RT_E_CUDA;
+  launch_pack_tiled((const bf16*)d_w, wt, M, K, (cudaStream_t)stream);
   float* pv = (float*)d_ws;
   int32_t* pi = (int32_t*)(pv + (size_t)mt * N);
   GemmArgs g{};
   g.M = M;
   g.N = N;
   g.K = K;
-  g.splits = 1;
   g.mode = EPI_ARGMAX;
   g.out = d_logits;
   g.part_val = pv;
   g.part_idx = pi;
-  launch_gemm_epi(wm, xm, g, (cudaStream_t)stream);
+  launch_gemm_epi(wt, xm, g, 0, (cudaStream_t)stream);
   launch_argmax_reduce(pv, pi, mt, N, d_tok, (cudaStream_t)stream);
-  return last_launch();
+  rt_status st = last_launch();
+  cudaStreamSynchronize((cudaStream_t)stream);
+  cudaFree(wt);
+  return st;
 }
 
 extern "C" rt_status rt_op_init_weights(void* d_out, int64_t n, uint64_t seed, int32_t tensor_id, float sigma,

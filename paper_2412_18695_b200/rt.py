@@ -25,7 +25,7 @@ EXPORTED = ["rt_create", "rt_destroy", "rt_submit_request", "rt_step", "rt_poll_
             "rt_sync", "rt_get_stats", "rt_reset_stats", "rt_debug_dump", "rt_last_error", "rt_version",
             "rt_op_paged_attention", "rt_op_attention_ws_bytes", "rt_op_kv_write", "rt_op_kv_read",
             "rt_op_gemm", "rt_op_lm_argmax", "rt_op_init_weights", "rt_op_priority", "rt_mark", "rt_elapsed_ms",
-            "rt_nccl_unique_id"]
+            "rt_nccl_unique_id", "rt_op_pack_tiled", "rt_op_gemm_tiled"]
 
 
 class RtError(RuntimeError):
@@ -112,6 +112,8 @@ def lib():
     L.rt_mark.argtypes = [vp, i32]
     L.rt_elapsed_ms.argtypes = [vp, C.POINTER(C.c_double)]
     L.rt_nccl_unique_id.argtypes = [vp]
+    L.rt_op_pack_tiled.argtypes = [vp, vp, i32, i32, vp]
+    L.rt_op_gemm_tiled.argtypes = [vp, vp, vp, i32, i32, i32, i32, i32, vp]
     for f in EXPORTED:
         if f not in ("rt_last_error", "rt_version", "rt_op_attention_ws_bytes"):
             getattr(L, f).restype = C.c_int32
@@ -333,6 +335,14 @@ def kv_read(pool, out, n_pages, n_kv, hd, stream=None):
 
 def gemm(w, x, out, M, N, K, n_cap, splits=1, stream=None):
     _check(lib().rt_op_gemm(_ptr(w), _ptr(x), _ptr(out), M, N, K, n_cap, splits, _stream(stream)))
+
+
+def pack_tiled(w, out, M, K, stream=None):
+    _check(lib().rt_op_pack_tiled(_ptr(w), _ptr(out), M, K, _stream(stream)))
+
+
+def gemm_tiled(wt, x, out, M, N, K, n_cap, splits=0, stream=None):
+    _check(lib().rt_op_gemm_tiled(_ptr(wt), _ptr(x), _ptr(out), M, N, K, n_cap, splits, _stream(stream)))
 
 
 def lm_argmax(w, x, M, N, K, n_cap, tok, logits=None, ws=None, stream=None):
