@@ -48,60 +48,71 @@ def peaks():
 
 # ------------------------------------------------------------------ clocks
 class ClockSampler:
-    """nvidia-smi sampling DURING the timed region (B200_PROFILING.md clocks line)."""
+    """SM clock + throttle reasons sampled DURING the timed region (B200_PROFILING.md
+    clocks line), polled through NVML every 5 ms in a background thread (nvidia-smi -lms
+    is too coarse for a timed region of ~100 ms); falls back to nvidia-smi."""
+
+    R_HW, R_HW_THERM, R_SW_THERM, R_SW_POWER = 0x8, 0x40, 0x20, 0x4   # nvmlClocksEventReason*
 
     def __init__(self, gpu):
-        self.gpu, self.rows, self.p = gpu, [], None
+        self.gpu, self.rows = gpu, []
         self.t_lo = self.t_hi = None
+        self._stop = False
+        self.th = None
 
     def __enter__(self):
-        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
         try:
-            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
-                                       "--format=csv,noheader,nounits", "-lms", "20"],
-                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
-            self.t.start()
+            import pynvml
+            pynvml.nvmlInit()
+            idx = self.gpu
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            if vis:
+                try:
+                    idx = int(vis.split(",")[self.gpu])
+                except (ValueError, IndexError):
+                    pass
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(idx)
+            self.nv = pynvml
+            self.max_sm = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.th = threading.Thread(target=self._poll, daemon=True)
+            self.th.start()
         except Exception:
-            self.p = None
+            self.th = None
         return self
 
-    def _read(self):
-        for line in self.p.stdout:
-            self.rows.append((time.perf_counter(), [x.strip() for x in line.split(",")]))
-
-    def window(self, lo, hi):
-        """Timed region [lo, hi] (perf_counter); samples within 60 ms of it are kept."""
-        self.t_lo, self.t_hi = lo - 0.06, hi + 0.06
-
-    def __exit__(self, *a):
-        if self.p:
-            self.p.terminate()
+    def _poll(self):
+        nv = self.nv
+        while not self._stop:
             try:
-                self.p.wait(timeout=5)
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                pw = nv.nvmlDeviceGetPowerUsage(self.h) / 1000.0
+                self.rows.append((time.perf_counter(), sm, rs, pw))
             except Exception:
                 pass
-            self.t.join(timeout=2)
+            time.sleep(0.005)
+
+    def window(self, lo, hi):
+        self.t_lo, self.t_hi = lo, hi
+
+    def __exit__(self, *a):
+        self._stop = True
+        if self.th:
+            self.th.join(timeout=2)
 
     def summary(self):
-        rows = [r for t, r in self.rows if self.t_lo is None or self.t_lo <= t <= self.t_hi]
-        if not rows and self.rows:   # very short timed region: nearest samples around it
+        rows = [r for r in self.rows if self.t_lo is None or self.t_lo <= r[0] <= self.t_hi]
+        if not rows and self.rows:
             mid = 0.5 * (self.t_lo + self.t_hi)
-            rows = [r for t, r in sorted(self.rows, key=lambda x: abs(x[0] - mid))[:3]]
-        self_rows = rows
-        if not self_rows:
+            rows = sorted(self.rows, key=lambda r: abs(r[0] - mid))[:3]
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
-        rows = self_rows
-        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4)
-                          if len(r) > 4 + i and r[4 + i].lower() == "active"})
-        pw = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(rows), "power_w_max": max(pw) if pw else None}
+        names = {self.R_HW: "hw_slowdown", self.R_HW_THERM: "hw_thermal_slowdown",
+                 self.R_SW_THERM: "sw_thermal_slowdown", self.R_SW_POWER: "sw_power_cap"}
+        reasons = sorted({n for r in rows for bit, n in names.items() if r[2] & bit})
+        return {"sm_mhz": float(np.median([r[1] for r in rows])), "sm_max_mhz": float(self.max_sm),
+                "reasons": reasons, "samples": len(rows), "power_w_max": max(r[3] for r in rows),
+                "source": "nvml 5 ms poll"}
 
 
 # ------------------------------------------------------------------ workload
@@ -162,7 +173,7 @@ def run_ours(args, rank, world, dist):
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(dev) as clk:
-        time.sleep(0.25)
+        time.sleep(0.05)
         t_lo = time.perf_counter()
         eng.mark(0)
         tok = 0

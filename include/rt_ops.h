@@ -24,7 +24,8 @@ extern "C" {
  *   o[r, h] = softmax(q[r, h] . K[0:seqlen[r]]^T / sqrt(hd)) V[0:seqlen[r]],
  *   K/V of kv head h / G from pages page_table[row_task[r] * pt_stride + p / 16].
  * d_q bf16 [n_rows][n_q][hd]; d_out bf16 [n_rows][n_q][hd]; d_out_f32 (nullable)
- * fp32 same shape; d_ws workspace >= rt_op_attention_ws_bytes(...).
+ * fp32 same shape; d_ws workspace >= rt_op_attention_ws_bytes(...), ZERO-FILLED before
+ * its first use (it holds self-resetting split-KV merge tickets, left zero on return).
  * hd in {32, 64, 128}; G = n_q / n_kv in {1..8}. */
 rt_status rt_op_paged_attention(const void* d_q, const void* d_pool, const int32_t* d_page_table,
                                 int32_t pt_stride, const int32_t* d_row_task,

@@ -19,6 +19,7 @@
 //    kernel (flash-decoding split-KV).
 #include "common.cuh"
 #include "model.h"
+#include <cstdlib>
 
 namespace rt {
 
@@ -216,28 +217,31 @@ __global__ void __launch_bounds__(kAttnWarps * 32) k_attn(AttnArgs a) {
       }
     }
   }
-}
-
-// combine split-KV partials of rows with more than one chunk
-template <int HD>
-__global__ void k_attn_combine(AttnArgs a) {
-  if (threadIdx.x == 0) pdl_trigger();
-  pdl_wait();
-  const int r = blockIdx.x, qh = blockIdx.y;
-  const int row = a.row0 + r;
-  const int seqlen = a.row_seqlen ? a.row_seqlen[row] : a.row_pos[row] + 1;
-  const int n_pages = (seqlen + 15) >> 4;
-  const int n_chunks = (n_pages + a.chunk_pages - 1) / a.chunk_pages;
-  if (n_chunks <= 1) return;
-  const float* wp = a.ws + ((size_t)r * a.nq + qh) * a.max_chunks * (HD + 2);
-  float M = -INFINITY;
-  for (int c = 0; c < n_chunks; ++c) M = fmaxf(M, wp[c * (HD + 2) + HD]);
-  for (int d = threadIdx.x; d < HD; d += blockDim.x) {
+  if (single) return;
+  // ---- split-KV merge by the last chunk CTA of this (row, kv head): no combine launch
+  __shared__ int s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int* tk = a.tickets + (size_t)r * a.nkv + h;
+    const int prev = atomicAdd(tk, 1);
+    s_last = (prev == n_chunks - 1);
+    if (s_last) *tk = 0;  // self-resetting for the next launch
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  for (int it = threadIdx.x; it < G * HD; it += blockDim.x) {
+    const int g = it / HD, d = it % HD;
+    const int qh = h * G + g;
+    const float* wp = a.ws + ((size_t)r * a.nq + qh) * a.max_chunks * (HD + 2);
+    float M = -INFINITY;
+    for (int c = 0; c < n_chunks; ++c) M = fmaxf(M, __ldcg(wp + c * (HD + 2) + HD));
     float L = 0.f, O = 0.f;
-    for (int c = 0; c < n_chunks; ++c) {
-      const float f = exp2f(wp[c * (HD + 2) + HD] - M);
-      L += wp[c * (HD + 2) + HD + 1] * f;
-      O += wp[c * (HD + 2) + d] * f;
+    for (int c = 0; c < n_chunks; ++c) {  // fixed chunk order -> deterministic
+      const float f = exp2f(__ldcg(wp + c * (HD + 2) + HD) - M);
+      L += __ldcg(wp + c * (HD + 2) + HD + 1) * f;
+      O += __ldcg(wp + c * (HD + 2) + d) * f;
     }
     const float o = O / L;
     a.out[((size_t)r * a.nq + qh) * HD + d] = __float2bfloat16_rn(o);
@@ -249,17 +253,28 @@ int64_t attn_ws_floats(int n_rows, int nq, int hd, int max_chunks) {
   return (int64_t)n_rows * nq * max_chunks * (hd + 2);
 }
 
-// Split-KV plan: enough CTAs to cover the 148 SMs a few times over.
+// Split-KV plan (measured on B200, tools/attn_bench.py): one CTA per (row, kv head)
+// streams at 96-110 % of the measured copy bandwidth from 64 rows x 8 kv heads up (C2
+// 64 x 1310: 55 us; 64 x 8192: 90 % of 8 TB/s); extra chunks only add pipeline fills
+// and the merge, and were never faster for >= 32 (row, head) pairs.  Below that the
+// step is latency-bound and c = ceil(64 / pairs) <= 8 chunks help (1 row x 4096:
+// 32 -> 14.5 us).  RT_ATTN_CHUNKS overrides c (tuning).
 void attn_plan(int n_rows, int nkv, int max_seqlen, int* chunk_pages, int* max_chunks) {
   const int max_pages = (max_seqlen + 15) / 16;
   const long long base = (long long)n_rows * nkv;
-  int cp = max_pages;
-  const long long target = 148LL * 6;
-  if (base < target && max_pages > 2 * kAttnWarps) {
-    long long want = (target + base - 1) / base;  // chunks per row
-    cp = (int)((max_pages + want - 1) / want);
-    if (cp < 2 * kAttnWarps) cp = 2 * kAttnWarps;
+  int best_c = 1;
+  if (base < 32) {
+    best_c = (int)((64 + base - 1) / base);
+    if (best_c > 8) best_c = 8;
+    while (best_c > 1 && max_pages / best_c < 2 * kAttnWarps) --best_c;
   }
+  static int forced = -2;
+  if (forced == -2) {
+    const char* e = getenv("RT_ATTN_CHUNKS");
+    forced = e ? atoi(e) : -1;
+  }
+  if (forced > 0) best_c = forced;
+  int cp = (max_pages + best_c - 1) / best_c;
   if (cp < 1) cp = 1;
   *chunk_pages = cp;
   *max_chunks = (max_pages + cp - 1) / cp;
@@ -275,7 +290,6 @@ static void launch_hd(const AttnArgs& a, cudaStream_t s) {
   }
   dim3 grid(a.max_chunks, a.nkv, a.n_rows);
   launch_pdl(k_attn<HD>, grid, dim3(kAttnWarps * 32), C::SMEM, s, a);
-  if (a.max_chunks > 1) launch_pdl(k_attn_combine<HD>, dim3(a.n_rows, a.nq), dim3(128), 0, s, a);
 }
 
 void launch_attention(const AttnArgs& a, cudaStream_t s) {

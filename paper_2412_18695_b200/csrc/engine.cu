@@ -100,6 +100,7 @@ struct rt_engine {
   float *d_cap_q = nullptr, *d_cap_o = nullptr, *d_rope_cos = nullptr, *d_rope_sin = nullptr;
   int64_t attn_ws_cap = 0, gemm_ws_cap = 0;
   float *d_gemm_ws = nullptr, *d_ss = nullptr;
+  int* d_attn_tickets = nullptr;
   int* d_gemm_cnt = nullptr;
   GemmTmaSet x_h, x_o, x_act, x_hfin;
   // submissions
@@ -400,6 +401,7 @@ static rt_status create_impl(rt_engine* e, const rt_config* cfg) {
     if (c.flags & RT_FLAG_KEEP_LOGITS) CK(e, dalloc(e, &e->d_logits, (size_t)c.max_batch * V));
     e->attn_ws_cap = (int64_t)(148 * 8 + (int64_t)R * nkv) * 8 * (hd + 2) * 2;
     CK(e, dalloc(e, &e->d_attn_ws, (size_t)e->attn_ws_cap));
+    CK(e, dalloc(e, &e->d_attn_tickets, (size_t)R * nkv));
     if (c.flags & RT_FLAG_CAPTURE) {
       CK(e, dalloc(e, &e->d_cap_q, (size_t)e->rows_cap * nq * hd));
       CK(e, dalloc(e, &e->d_cap_o, (size_t)e->rows_cap * nq * hd));
@@ -586,6 +588,7 @@ static rt_status forward(rt_engine* e, const HostMailbox& plan) {
     }
     aa.out = e->d_o;
     aa.ws = e->d_attn_ws;
+    aa.tickets = e->d_attn_tickets;
     aa.scale_log2 = sl2;
     auto gemm = [&](const bf16* w, const GemmTmaSet& x, int M, int K, GemmArgs g) {
       g.M = M;
@@ -620,7 +623,7 @@ static rt_status forward(rt_engine* e, const HostMailbox& plan) {
       aa.out_f32 = (e->d_cap_o && l == c.capture_layer) ? e->d_cap_o : nullptr;
       if (timing && row0 == 0) cudaEventRecord(e->ev_attn[2 * l], s);
       launch_attention(aa, s);
-      launches += aa.max_chunks > 1 ? 2 : 1;
+      ++launches;
       if (timing && row0 == 0) cudaEventRecord(e->ev_attn[2 * l + 1], s);
       {  // O projection + residual
         GemmArgs g{};

@@ -45,7 +45,8 @@ struct AttnArgs {
   int chunk_pages, max_chunks;
   bf16* out;                // [n_rows][nq][hd]
   float* out_f32;           // nullable, indexed by global row (row0 + r)
-  float* ws;                // partials
+  float* ws;                // split-KV partials [rows][nq][max_chunks][hd + 2]
+  int* tickets;             // [rows][nkv] zero-initialised, self-resetting (split-KV merge)
   float scale_log2;
 };
 int64_t attn_ws_floats(int n_rows, int nq, int hd, int max_chunks);

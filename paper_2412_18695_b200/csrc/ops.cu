@@ -19,8 +19,11 @@ static rt_status last_launch() { return cudaGetLastError() == cudaSuccess ? RT_O
 extern "C" int64_t rt_op_attention_ws_bytes(int32_t n_rows, int32_t max_seqlen, int32_t n_q, int32_t hd) {
   int cp = 0, mc = 0;
   attn_plan(n_rows, 1, max_seqlen, &cp, &mc);
-  // nkv only changes the plan through n_rows * nkv >= target; bound with nkv = 1
-  return attn_ws_floats(n_rows, n_q, hd, mc) * 4;
+  int mc8 = 0;
+  attn_plan(n_rows, 8, max_seqlen, &cp, &mc8);
+  mc = mc > mc8 ? mc : mc8;
+  const int64_t tk_bytes = (((int64_t)n_rows * n_q * 4) + 255) & ~(int64_t)255;
+  return tk_bytes + attn_ws_floats(n_rows, n_q, hd, mc > 8 ? mc : 8) * 4;
 }
 
 extern "C" rt_status rt_op_paged_attention(const void* d_q, const void* d_pool, const int32_t* d_page_table,
@@ -52,7 +55,10 @@ extern "C" rt_status rt_op_paged_attention(const void* d_q, const void* d_pool, 
   }
   a.out = (bf16*)d_out;
   a.out_f32 = d_out_f32;
-  a.ws = (float*)d_ws;
+  // workspace = [merge tickets: n_rows * n_q ints, 256-B padded][split-KV partials]
+  const size_t tk_bytes = (((size_t)n_rows * n_q * 4) + 255) & ~(size_t)255;
+  a.tickets = (int*)d_ws;
+  a.ws = (float*)((char*)d_ws + tk_bytes);
   a.scale_log2 = (float)(1.4426950408889634 / sqrt((double)hd));
   launch_attention(a, (cudaStream_t)stream);
   return last_launch();

@@ -316,7 +316,7 @@ def paged_attention(q, pool, page_table, row_task, row_seqlen, max_seqlen, n_q, 
     L = lib()
     need = L.rt_op_attention_ws_bytes(int(q.shape[0]), int(max_seqlen), n_q, hd)
     if ws is None or ws.numel() * ws.element_size() < need:
-        ws = torch.empty(max(need, 16), dtype=torch.uint8, device=q.device)
+        ws = torch.zeros(max(need, 16), dtype=torch.uint8, device=q.device)  # tickets must start at 0
     _check(L.rt_op_paged_attention(_ptr(q), _ptr(pool), _ptr(page_table), int(page_table.shape[1]),
                                    _ptr(row_task), _ptr(row_seqlen), int(q.shape[0]), int(max_seqlen), n_q, n_kv,
                                    hd, _ptr(out), _ptr(out_f32), _ptr(ws), ws.numel() * ws.element_size(),
