@@ -566,20 +566,22 @@ static int max_clusters_bn(int bn, int S) {
   return max_clusters<256>(S);
 }
 
-// Cluster split count (measured on B200, tools/gemm_bench.py): a split-K cluster only
-// pays off while every cluster is co-resident in ONE wave (cudaOccupancyMaxActiveClusters);
-// with >= 148 tiles plain tiles (S = 1) already cover the SMs.  Otherwise take the
-// largest portable S (<= 8) whose clusters all fit, keeping >= 4 k-blocks per CTA.
+// Cluster split count (measured on B200, tools/gemm_bench.py, N = 64): a split-K cluster
+// only pays off while every cluster is co-resident in ONE wave; with >= 148 tiles plain
+// tiles (S = 1) already cover the SMs.  Measured co-residency of 2-CTA/SM clusters holds
+// up to 256 CTAs (O / down: 32 x 8 = 256 -> 11.7 / 26 us) but not 288 (QKV 48 x 6:
+// 12 -> 19 us, 32 x 9: 11 -> 19 us), so S = max{S <= 8 : tiles x S <= 256, >= 4 k-blocks
+// per CTA} (cudaOccupancyMaxActiveClusters under-reports and is only a cap).
 int gemm_choose_splits(int M, int N, int K) {
   const int bn = gemm_bn(N);
   const int tiles = ((M + 127) / 128) * ((N + bn - 1) / bn);
   const int kb = K / kBK;
   if (tiles >= 148) return 1;
+  const int budget = bn <= 128 ? 256 : 128;
   int best = 1;
-  for (int s = 2; s <= 8 && kb / s >= 4; ++s) {
-    const int mc = max_clusters_bn(bn, s);
-    if (mc >= tiles) best = s;
-  }
+  for (int s = 2; s <= 8 && kb / s >= 4; ++s)
+    if (tiles * s <= budget) best = s;
+  (void)max_clusters_bn;
   return best;
 }
 
