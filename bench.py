@@ -39,6 +39,20 @@ MAX_CTX = 2048
 TRACE_POOL = list(range(1, 9))   # drone traces 1-8 (tab:task_list)
 
 
+def ncu_traffic(kernel):
+    """dram__bytes_read + write per launch of `kernel` from the committed ncu capture."""
+    try:
+        for d in json.load(open(os.path.join(ROOT, "profiles", "r01_ncu_attention_full.json"))):
+            if kernel in d["Kernel Name"]:
+                rd = float(d["dram__bytes_read.sum"].split()[0])
+                wr = float(d["dram__bytes_write.sum"].split()[0])
+                scale = {"Mbyte": 1e6, "Gbyte": 1e9, "Kbyte": 1e3, "byte": 1.0}[d["dram__bytes_read.sum"].split()[1]]
+                return (rd + wr) * scale
+    except Exception:
+        return None
+    return None
+
+
 def peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -208,7 +222,9 @@ def run_ours(args, rank, world, dist):
                 "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": (attn_gbs / pk["hbm_gbs"]) if attn_gbs else None,
                 "frac_of_8000": (attn_gbs / 8000.0) if attn_gbs else None,
-                "traffic": None, "alg_bytes_per_launch": st["attn_bytes"] / max(st["attn_launches"], 1),
+                "traffic": ncu_traffic("k_attn"), "traffic_source": "profiles/r01_ncu_attention_full.json "
+                "(ncu --set full, same C2 launch: B=64, ctx~1310, 8 kv heads)",
+                "alg_bytes_per_launch": st["attn_bytes"] / max(st["attn_launches"], 1),
                 "ms_per_launch": st["attn_ms"] / max(st["attn_launches"], 1),
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if not pk.get("fallback") else "fallback"}
     step_roof = {"alg_bytes_per_step": step_bytes, "achieved_gbs": step_bytes / (ms / K / 1e3) / 1e9,
