@@ -49,7 +49,8 @@ enum {
   RT_FLAG_NO_MODEL = 1,     /* scheduling-only engine: scripted tokens, no forward pass */
   RT_FLAG_KEEP_LOGITS = 2,  /* materialise fp32 logits of the last round (parity tests) */
   RT_FLAG_CAPTURE = 4,      /* keep q / attention output (fp32) of layer capture_layer */
-  RT_FLAG_TIMING = 8        /* CUDA-event timing of attention / GEMM launches (rt_stats) */
+  RT_FLAG_TIMING = 8,       /* CUDA-event timing of attention / GEMM launches (rt_stats) */
+  RT_FLAG_FORCE_EXCHANGE = 16 /* run the per-round NCCL allgather + merge even when world == 1 */
 };
 
 typedef struct rt_engine rt_engine;

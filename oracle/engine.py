@@ -171,6 +171,9 @@ class OracleEngine:
                 return info
         n_waiting = len(waiting)
         order = sorted(waiting, key=lambda r: self._key(r, t))
+        # local top-K candidates {Pri (0 for FCFS/EDF), arrival, id, rank} (c13 / a12)
+        topk = [((r.pri if p.policy == POLICY_PUD else 0.0), r.arrival, r.id, self.rank)
+                for r in order[:16]]
 
         # ---- WCET gate, judged on history up to round r-1 (AMB-8)
         n = min(p.speed_window, len(self.hist))
@@ -332,7 +335,7 @@ class OracleEngine:
                     n_refused_wcet=refused_wcet)
         self.round_log.append(dict(info, admitted=[a.id for a in admitted], slots=list(slots),
                                    tokens=toks, argmax=[argmax.get(r) for r in slots],
-                                   stops=stops, popped=popped, free=len(self.free),
+                                   stops=stops, popped=popped, free=len(self.free), topk=topk,
                                    logits=logits if self.model is not None else None))
         return info
 

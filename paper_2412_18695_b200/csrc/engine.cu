@@ -75,7 +75,7 @@ struct rt_engine {
   int64_t pool_layer_bytes = 0;
   cudaStream_t stream = nullptr, side = nullptr;
   cudaEvent_t ev_plan = nullptr, ev_post = nullptr, ev_cand = nullptr, ev_merge = nullptr;
-  bool post_pending = false, merge_pending = false;
+  bool post_pending = false, merge_pending = false, exchange = false;
   // weights
   void* d_wbuf = nullptr;
   bf16 *emb = nullptr, *lm = nullptr;
@@ -427,11 +427,16 @@ static rt_status create_impl(rt_engine* e, const rt_config* cfg) {
     for (auto& ev : e->ev_attn) cudaEventCreate(&ev);
   }
   // ---- replicas: NCCL communicator (one allgather of top-K candidates per round)
-  if (c.world > 1) {
-    if (!cfg->nccl_id) return done(fail(e, RT_E_INVAL, "nccl_id required when world > 1"));
+  e->exchange = c.world > 1 || (c.flags & RT_FLAG_FORCE_EXCHANGE);
+  if (e->exchange) {
+    if (c.world > 1 && !cfg->nccl_id) return done(fail(e, RT_E_INVAL, "nccl_id required when world > 1"));
     if (!g_nccl.load()) return done(fail(e, RT_E_NCCL, "libnccl.so.2 not loadable"));
     nccl_uid_t uid;
-    memcpy(uid.internal, cfg->nccl_id, 128);
+    if (cfg->nccl_id) {
+      memcpy(uid.internal, cfg->nccl_id, 128);
+    } else if (!g_nccl.get_uid || g_nccl.get_uid(&uid) != 0) {  // single-rank communicator
+      return done(fail(e, RT_E_NCCL, "ncclGetUniqueId failed"));
+    }
     int r = g_nccl.init(&e->comm, c.world, uid, c.rank);
     if (r != 0) return done(fail(e, RT_E_NCCL, std::string("ncclCommInitRank: ") + (g_nccl.errstr ? g_nccl.errstr(r) : "?")));
     CK(e, dalloc(e, &e->d_cand_all, (size_t)c.world * kTopK * 4));
@@ -710,7 +715,7 @@ extern "C" rt_status rt_step(rt_engine* e, int64_t now_us, rt_round_info* info) 
     info->n_prefill_rows = plan.n_prefill_rows;
   }
   if (plan.idle || plan.B == 0) return RT_OK;
-  if (c.world > 1) {  // a12: allgather of this round's local top-K candidates on the side stream
+  if (e->exchange) {  // a12: allgather of this round's local top-K candidates on the side stream
     CK(e, cudaEventRecord(e->ev_cand, s));
     CK(e, cudaStreamWaitEvent(e->side, e->ev_cand, 0));
     int r = g_nccl.allgather(e->sp.cand, e->d_cand_all, kTopK * 4, kNcclFloat64, e->comm, e->side);

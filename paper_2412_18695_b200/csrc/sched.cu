@@ -336,11 +336,12 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
 
   // ---- local top-K candidates for the round allgather (a12)
   if (tid < kTopK) {
-    if (tid < n) {
+    if (tid < n) {  // record {Pri (0 for FCFS/EDF), arrival, global id, rank}
       const int x = S.perm[tid];
-      p.cand[tid * 4 + 0] = S.a0[x];
-      p.cand[tid * 4 + 1] = (double)S.a1[x];
-      p.cand[tid * 4 + 2] = (double)S.a2[x];
+      const int task = S.cslot[x];
+      p.cand[tid * 4 + 0] = p.policy == 0 ? S.a0[x] : 0.0;
+      p.cand[tid * 4 + 1] = (double)T.arrival[task];
+      p.cand[tid * 4 + 2] = (double)T.rid[task];
       p.cand[tid * 4 + 3] = (double)p.rank;
     } else {
       p.cand[tid * 4 + 0] = -INFINITY;

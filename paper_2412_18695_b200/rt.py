@@ -16,7 +16,7 @@ RT_OK, RT_E_INVAL, RT_E_NOMEM, RT_E_CUDA, RT_E_NCCL, RT_E_STATE = 0, -1, -2, -3,
 RT_CLOCK_VIRTUAL, RT_CLOCK_WALL = 0, 1
 RT_POLICY_PUD, RT_POLICY_FCFS, RT_POLICY_EDF = 0, 1, 2
 RT_STOP_NONE, RT_STOP_EOS, RT_STOP_MAXNEW, RT_STOP_SKILL, RT_STOP_CAP = 0, 1, 2, 3, 4
-RT_FLAG_NO_MODEL, RT_FLAG_KEEP_LOGITS, RT_FLAG_CAPTURE, RT_FLAG_TIMING = 1, 2, 4, 8
+RT_FLAG_NO_MODEL, RT_FLAG_KEEP_LOGITS, RT_FLAG_CAPTURE, RT_FLAG_TIMING, RT_FLAG_FORCE_EXCHANGE = 1, 2, 4, 8, 16
 (RT_DUMP_TASKS, RT_DUMP_PAGE_TABLES, RT_DUMP_ROUND, RT_DUMP_LOGITS, RT_DUMP_HIDDEN, RT_DUMP_CAPTURE_Q,
  RT_DUMP_CAPTURE_O, RT_DUMP_ROWS, RT_DUMP_KV_LAYER, RT_DUMP_FREE_STACK, RT_DUMP_TASK_SLOTS,
  RT_DUMP_MERGED) = range(1, 13)

@@ -125,6 +125,32 @@ def test_sched_parity_wall_clock_replay(rt):
     lockstep(eng, ora, max_rounds=20000, now=lambda i: int(clock[i]), check_every=4)
 
 
+def test_round_exchange_single_rank_nccl(rt):
+    """a12 on hardware: the per-round ncclAllGather + device merge (1-rank communicator,
+    RT_FLAG_FORCE_EXCHANGE) yields exactly the oracle's top-16 (Pri, arrival, id) keys."""
+    v = make_vocab(512)
+    p = engine_params("paper-4090", max_batch=8, max_tasks=512, max_ctx=256, n_pages=96)
+    reqs = compose_workload(64, 8.0, 16, range(1, 12), 3.0, 9, v, prompt_len_range=(20, 100), max_requests=300)
+    eng, ora = make_pair(rt, v, p, flags=rt.RT_FLAG_FORCE_EXCHANGE)
+    submit_both(eng, ora, reqs)
+    checked = 0
+    for n in range(3000):
+        ig, io = eng.step(), ora.step()
+        assert ig["n_running"] == io["n_running"]
+        if io["n_running"] == 0:
+            if all(r.state == FINISHED for r in ora.reqs.values()):
+                break
+            continue
+        merged = eng.dump(rt.RT_DUMP_MERGED, np.float64).reshape(16, 4)
+        exp = ora.round_log[-1]["topk"]
+        got = [tuple(m) for m in merged if m[2] >= 0]
+        assert len(got) == len(exp), n
+        for g, e in zip(got, exp):
+            assert g[0] == e[0] and g[1] == e[1] and g[2] == e[2] and g[3] == e[3], (n, g, e)
+        checked += int(len(exp) > 1)
+    assert checked > 20
+
+
 def test_submit_errors(rt):
     v = make_vocab(512)
     p = engine_params("paper-4090", max_batch=4, max_tasks=2, max_ctx=64, n_pages=2)
