@@ -731,7 +731,8 @@ extern "C" rt_status rt_step(rt_engine* e, int64_t now_us, rt_round_info* info) 
   }
   if (timing) {
     cudaEventRecord(e->ev_f1, s);
-    e->timing_pending = !(c.flags & RT_FLAG_NO_MODEL);
+    e->timing_pending = true;
+    if (c.flags & RT_FLAG_NO_MODEL) e->timing_layers = 0;
   }
   launch_sched_post(e->sp, s);
   if (timing) {

@@ -252,6 +252,83 @@ def test_tiny_model_free_running_tokens(rt):
     assert checked > 10 and agree == checked
 
 
+def _sampled_checks(rt, eng, shape, p, seed, n_rows_check=8, n_vocab=512):
+    rows = eng.dump(rt.RT_DUMP_ROWS, np.int32).reshape(-1, 3)
+    nq, nkv, hd = shape.n_q_heads, shape.n_kv_heads, shape.head_dim
+    q = eng.dump(rt.RT_DUMP_CAPTURE_Q, np.float32).reshape(len(rows), nq, hd)
+    o = eng.dump(rt.RT_DUMP_CAPTURE_O, np.float32).reshape(len(rows), nq, hd)
+    kv = eng.dump(rt.RT_DUMP_KV_LAYER, np.uint16).reshape(p.n_pages, 2, nkv, 16, hd)
+    tabs = eng.dump(rt.RT_DUMP_PAGE_TABLES, np.int32).reshape(p.max_tasks, -1)
+    rng = np.random.default_rng(seed)
+    worst = 0.0
+    for i in rng.choice(len(rows), min(n_rows_check, len(rows)), replace=False):
+        task, pos, _ = rows[i]
+        npg = (pos + 16) // 16
+        pages = tabs[task][:npg]
+        kvf = (kv[pages].astype(np.uint32) << 16).view(np.float32)
+        kp, vp = kvf[:, 0].transpose(0, 2, 1, 3), kvf[:, 1].transpose(0, 2, 1, 3)
+        ref = paged_attention(q[i], kp, vp, list(range(npg)), pos + 1)
+        worst = max(worst, float(np.abs(o[i] - ref).max()))
+    B = eng.last_round()["n_running"]
+    lg = eng.dump(rt.RT_DUMP_LOGITS, np.float32).reshape(B, -1)
+    hid = eng.dump(rt.RT_DUMP_HIDDEN, np.uint16).reshape(B, -1)
+    h = (hid.astype(np.uint32) << 16).view(np.float32).astype(np.float64)
+    cols = np.concatenate([rng.choice(shape.vocab, n_vocab, replace=False), np.argmax(lg, axis=1)])
+    W = OW.matrix(seed, OW.TID_LM, cols, shape.d_model)
+    lerr = float(np.abs(h @ W.T - lg[:, cols]).max())
+    return worst, lerr
+
+
+def test_c3_mixed_256_shape_sampled(rt):
+    """BASELINE configs[2] shape: 256 mixed drone / robot-arm agents (prompts 1300 / 2884),
+    8B layer dims with 4 layers (the decode GEMMs run at N = 256, the BN = 256 path)."""
+    from synth.configs import ModelShape
+    s8 = MODEL_SHAPES["llama3-8b"]
+    shape = ModelShape("c3", 4, s8.d_model, s8.n_q_heads, s8.n_kv_heads, s8.head_dim, s8.d_ff, s8.vocab)
+    v = make_vocab(shape.vocab)
+    p = engine_params("b200-roofline", max_batch=256, max_tasks=512, max_ctx=3072, n_pages=256 * 186)
+    flags = rt.RT_FLAG_KEEP_LOGITS | rt.RT_FLAG_CAPTURE
+    eng = rt.Engine(shape, p, v, seed=13, flags=flags, capture_layer=3, max_rows_per_forward=8192)
+    from synth.traces import make_trace
+    for a in range(256):
+        tid = (a % 8) + 1 if a % 2 == 0 else 9 + (a % 3)
+        tr = make_trace(tid, v, seed=a)
+        eng.submit(a, tr.prompt, 0, tr.ert_us, tr.alpha, tr.beta, 90000, script=tr.plan)
+    for _ in range(30):
+        info = eng.step()
+        if info["n_running"] == 256 and info["n_prefill_rows"] == 0:
+            break
+    assert info["n_running"] == 256 and info["n_prefill_rows"] == 0
+    worst, lerr = _sampled_checks(rt, eng, shape, p, 13)
+    assert worst < 6e-3, worst
+    assert lerr < 1e-2, lerr
+
+
+def test_llama70b_dims_sampled(rt):
+    """BASELINE configs[4] layer dims (d 8192, 64 / 8 heads: G = 8, ff 28672), 2 layers,
+    128 running requests with short unique prompts (C5 plans)."""
+    from synth.configs import ModelShape
+    s70 = MODEL_SHAPES["llama3-70b"]
+    shape = ModelShape("c5", 2, s70.d_model, s70.n_q_heads, s70.n_kv_heads, s70.head_dim, s70.d_ff, s70.vocab)
+    v = make_vocab(shape.vocab)
+    p = engine_params("b200-roofline", max_batch=128, max_tasks=256, max_ctx=512, n_pages=128 * 32)
+    flags = rt.RT_FLAG_KEEP_LOGITS | rt.RT_FLAG_CAPTURE
+    eng = rt.Engine(shape, p, v, seed=17, flags=flags, capture_layer=1, max_rows_per_forward=8192)
+    rng = np.random.default_rng(5)
+    from synth.traces import make_trace
+    for a in range(128):
+        tr = make_trace(9 + a % 3, v, seed=a, prompt_len=int(rng.integers(100, 160)), plan_len=150)
+        eng.submit(a, tr.prompt, 0, tr.ert_us, tr.alpha, tr.beta, 90000, script=tr.plan)
+    for _ in range(30):
+        info = eng.step()
+        if info["n_running"] == 128 and info["n_prefill_rows"] == 0:
+            break
+    assert info["n_running"] == 128
+    worst, lerr = _sampled_checks(rt, eng, shape, p, 17)
+    assert worst < 6e-3, worst
+    assert lerr < 1e-2, lerr
+
+
 def test_llama8b_shape_sampled(rt):
     """BASELINE configs[1] shape (Llama-3-8B dims, random init) at the bench's
     launch configuration: per-op attention on sampled (row, head) pairs and
