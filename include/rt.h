@@ -50,7 +50,9 @@ enum {
   RT_FLAG_KEEP_LOGITS = 2,  /* materialise fp32 logits of the last round (parity tests) */
   RT_FLAG_CAPTURE = 4,      /* keep q / attention output (fp32) of layer capture_layer */
   RT_FLAG_TIMING = 8,       /* CUDA-event timing of attention / GEMM launches (rt_stats) */
-  RT_FLAG_FORCE_EXCHANGE = 16 /* run the per-round NCCL allgather + merge even when world == 1 */
+  RT_FLAG_FORCE_EXCHANGE = 16, /* run the per-round NCCL allgather + merge even when world == 1 */
+  RT_FLAG_GRAPHS = 32,         /* replay decode-only forwards from CUDA graphs keyed by batch size */
+  RT_FLAG_TRACE = 64           /* per-CTA %globaltimer records of every kernel (RT_DUMP_TRACE) */
 };
 
 typedef struct rt_engine rt_engine;
@@ -173,12 +175,27 @@ rt_status rt_reset_stats(rt_engine* e);
  *   RT_DUMP_KV_LAYER    bf16 logical [n_pages][2][n_kv_heads][16][head_dim] of capture_layer
  *   RT_DUMP_FREE_STACK  int32 [free_top]
  *   RT_DUMP_TASK_SLOTS  int32 [B] task slot of each batch slot of the last round
- *   RT_DUMP_MERGED      int64 [K][4] merged global top-K (world > 1) */
+ *   RT_DUMP_MERGED      int64 [K][4] merged global top-K (world > 1)
+ *   RT_DUMP_TRACE       rt_trace_rec [n] since the last rt_reset_stats (RT_FLAG_TRACE; at most
+ *                       2^20 records, one per CTA; the buffer is process-wide: with several
+ *                       traced engines in one process the last created one owns it) */
 enum {
   RT_DUMP_TASKS = 1, RT_DUMP_PAGE_TABLES = 2, RT_DUMP_ROUND = 3, RT_DUMP_LOGITS = 4,
   RT_DUMP_HIDDEN = 5, RT_DUMP_CAPTURE_Q = 6, RT_DUMP_CAPTURE_O = 7, RT_DUMP_ROWS = 8,
-  RT_DUMP_KV_LAYER = 9, RT_DUMP_FREE_STACK = 10, RT_DUMP_TASK_SLOTS = 11, RT_DUMP_MERGED = 12
+  RT_DUMP_KV_LAYER = 9, RT_DUMP_FREE_STACK = 10, RT_DUMP_TASK_SLOTS = 11, RT_DUMP_MERGED = 12,
+  RT_DUMP_TRACE = 13
 };
+/* One kernel CTA: grid = %gridid (unique per launch); kind = 1 GEMM (| epilogue mode << 8 |
+ * cluster split << 16), 2 attention, 3 norm, 4 embed, 5/6 scheduler pre/post, 7 gather,
+ * 8 argmax reduce, 9 candidate merge; t_* = %globaltimer ns at CTA entry, after its
+ * dependency wait (griddepcontrol.wait; = entry for kernels without one), t_aux = GEMM:
+ * accumulator complete (last tcgen05.mma retired, seen by the epilogue; 0 elsewhere) and
+ * t_exit at CTA exit. */
+typedef struct {
+  uint64_t grid;
+  uint32_t kind, smid;
+  uint64_t t_entry, t_ready, t_aux, t_exit;
+} rt_trace_rec;
 rt_status rt_debug_dump(rt_engine* e, int32_t what, void* dst, int64_t bytes, int64_t* bytes_out);
 
 /* Device-time markers on the engine's stream (CUDA events): which = 0 records the

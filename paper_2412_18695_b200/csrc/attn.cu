@@ -41,6 +41,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32) k_attn(AttnArgs a) {
   extern __shared__ __align__(1024) unsigned char smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + (C::RING > C::MERGE ? C::RING : C::MERGE));
 
+  TraceScope tr(TK_ATTN);
   if (threadIdx.x == 0) pdl_trigger();
   const int chunk = blockIdx.x, h = blockIdx.y, r = blockIdx.z;
   const int row = a.row0 + r;
@@ -70,6 +71,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32) k_attn(AttnArgs a) {
   }
   __syncwarp();
   pdl_wait();  // q and the KV pages come from the QKV GEMM that precedes this kernel
+  tr.ready();
   // page ids of the first 32 pages of this warp, one per lane
   int my_page = (lane < n_my) ? ptab[p_begin + warp + lane * kAttnWarps] : 0;
 #pragma unroll
@@ -301,5 +303,7 @@ void launch_attention(const AttnArgs& a, cudaStream_t s) {
     default: break;
   }
 }
+
+RT_TRACE_BINDER(trace_bind_attn)
 
 }  // namespace rt

@@ -4,6 +4,7 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 #include <utility>
+#include <stdlib.h>
 
 #define RT_DEV __device__ __forceinline__
 
@@ -38,6 +39,12 @@ RT_DEV float warp_max(float v) {
 RT_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 RT_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// RT_NO_PDL=1 disables programmatic dependent launch (A/B measurements)
+inline bool pdl_enabled() {
+  static const bool on = getenv("RT_NO_PDL") == nullptr;
+  return on;
+}
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                               Args&&... args) {
@@ -48,11 +55,88 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   cfg.stream = s;
   cudaLaunchAttribute at[1];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
+
+// ------------------------------------------------ device trace (RT_FLAG_TRACE)
+// One record per CTA: %gridid identifies the launch, %globaltimer stamps kernel entry,
+// the end of its dependency wait (pdl_wait) and exit — the real in-pipeline timeline
+// with PDL overlap, which neither CUDA events (they serialise) nor ncu (it replays)
+// can show.  Thread 0 of every CTA writes; off (rec == nullptr) it costs one load.
+// t_aux: a kernel-specific phase mark (GEMM: accumulator complete; 0 = none).
+// Layout must match rt_trace_rec in rt.h (48 bytes).
+struct TraceRec {
+  unsigned long long grid;
+  uint32_t kind, smid;
+  unsigned long long t_entry, t_ready, t_aux, t_exit;
+};
+struct TraceBuf {
+  TraceRec* rec;
+  unsigned* n;
+  unsigned cap;
+};
+static __device__ TraceBuf g_trace;  // per translation unit, bound by trace_bind_<tu>()
+
+enum TraceKind : uint32_t {
+  TK_GEMM = 1, TK_ATTN = 2, TK_NORM = 3, TK_EMBED = 4, TK_SCHED_PRE = 5, TK_SCHED_POST = 6,
+  TK_GATHER = 7, TK_ARGMAX = 8, TK_MERGE = 9, TK_PHASE = 0x80
+};
+
+RT_DEV unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+struct TraceScope {
+  unsigned long long t0 = 0, t1 = 0, t2 = 0;
+  uint32_t kind;
+  __device__ explicit TraceScope(uint32_t k) : kind(k) {
+    if (threadIdx.x == 0 && g_trace.rec) t0 = t1 = gtimer();
+  }
+  __device__ void ready() {
+    if (threadIdx.x == 0 && g_trace.rec) t1 = gtimer();
+  }
+  __device__ void aux(unsigned long long t) { t2 = t; }  // thread 0 only
+  __device__ ~TraceScope() {
+    if (threadIdx.x != 0 || !g_trace.rec) return;
+    const unsigned i = atomicAdd(g_trace.n, 1u);
+    if (i >= g_trace.cap) return;
+    TraceRec r;
+    asm volatile("mov.u64 %0, %%gridid;" : "=l"(r.grid));
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(r.smid));
+    r.kind = kind;
+    r.t_entry = t0;
+    r.t_ready = t1;
+    r.t_aux = t2;
+    r.t_exit = gtimer();
+    g_trace.rec[i] = r;
+  }
+};
+// an extra record with four phase marks of one CTA (kind TK_PHASE | ...), for kernels
+// whose internal phases are being profiled
+RT_DEV void trace_phase(uint32_t kind, unsigned long long a, unsigned long long b, unsigned long long c,
+                        unsigned long long d) {
+  if (!g_trace.rec) return;
+  const unsigned i = atomicAdd(g_trace.n, 1u);
+  if (i >= g_trace.cap) return;
+  TraceRec r;
+  asm volatile("mov.u64 %0, %%gridid;" : "=l"(r.grid));
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(r.smid));
+  r.kind = kind;
+  r.t_entry = a;
+  r.t_ready = b;
+  r.t_aux = c;
+  r.t_exit = d;
+  g_trace.rec[i] = r;
+}
+#define RT_TRACE_BINDER(fn)                                       \
+  void fn(void* rec, unsigned* n, unsigned cap) {                 \
+    TraceBuf b{reinterpret_cast<TraceRec*>(rec), n, cap};         \
+    cudaMemcpyToSymbol(g_trace, &b, sizeof b);                    \
+  }
 
 // --------------------------------------------------------------- PTX wrappers
 RT_DEV uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }

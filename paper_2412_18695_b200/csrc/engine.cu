@@ -115,6 +115,17 @@ struct rt_engine {
   int64_t n_submitted = 0;
   int64_t seg_read = 0;
   HostMailbox plan{};
+  // CUDA graphs of decode-only forwards, keyed by (B, split-KV plan, timing)
+  std::unordered_map<int64_t, cudaGraphExec_t> graphs;
+  bool no_graphs = false;
+  // next-projection L2 prefetch budget (RT_L2_PF_MB; off by default: measured 2% slower,
+  // the prefetch competes with the running projection's own stream)
+  int64_t l2_pf_bytes = 0;
+  // RT_FLAG_TRACE: per-CTA kernel records (common.cuh TraceScope)
+  uint64_t* d_trace = nullptr;
+  unsigned* d_trace_n = nullptr;
+  unsigned trace_cap = 0;
+  int graph_launches = 0;
   // timing
   std::vector<cudaEvent_t> ev_attn;  // 2 per layer
   cudaEvent_t ev_f0 = nullptr, ev_f1 = nullptr, ev_s0 = nullptr, ev_s1 = nullptr, ev_q1 = nullptr;
@@ -220,6 +231,10 @@ static rt_status create_impl(rt_engine* e, const rt_config* cfg) {
   e->tok_skill.assign(cfg->tok_skill, cfg->tok_skill + cfg->vocab);
   e->tok_exec.assign(cfg->tok_exec_min_us, cfg->tok_exec_min_us + cfg->vocab);
   e->cfg.tok_skill = nullptr;
+  // graphs are opt-in: with PDL already hiding launch gaps they measured ~1% slower on the
+  // llama3-8b B=64 step (profiles/r01_summary.md), they pay off where the host is the bound
+  e->no_graphs = !(c.flags & RT_FLAG_GRAPHS) || getenv("RT_NO_GRAPHS") != nullptr;
+  if (const char* pf = getenv("RT_L2_PF_MB")) e->l2_pf_bytes = (int64_t)atoi(pf) << 20;
   e->cfg.tok_exec_min_us = nullptr;
   e->cfg.nccl_id = nullptr;
   if (e->cfg.max_admit_per_round <= 0) e->cfg.max_admit_per_round = 1 << 30;
@@ -365,7 +380,7 @@ static rt_status create_impl(rt_engine* e, const rt_config* cfg) {
     e->lm = w;
     w += n_lm;
     launch_init_weights(e->emb, n_emb, c.weight_seed, 0, sig, e->stream);
-    launch_init_weights_tiled(e->lm, V, d, 0, c.weight_seed, 1, sig, e->stream);
+    launch_init_weights_tiled(e->lm, V, d, 0, 0, c.weight_seed, 1, sig, e->stream);
     e->layers.resize(L);
     for (int l = 0; l < L; ++l) {
       LayerW& lw = e->layers[l];
@@ -373,10 +388,10 @@ static rt_status create_impl(rt_engine* e, const rt_config* cfg) {
       lw.o = w; w += n_o;
       lw.gu = w; w += n_gu;
       lw.d = w; w += n_d;
-      launch_init_weights_tiled(lw.qkv, e->qkv_dim, d, 0, c.weight_seed, 16 + 8 * l + 0, sig, e->stream);
-      launch_init_weights_tiled(lw.o, d, nq * hd, 0, c.weight_seed, 16 + 8 * l + 1, sig, e->stream);
-      launch_init_weights_tiled(lw.gu, 2 * ff, d, ff, c.weight_seed, 16 + 8 * l + 2, sig, e->stream);
-      launch_init_weights_tiled(lw.d, d, ff, 0, c.weight_seed, 16 + 8 * l + 3, sig, e->stream);
+      launch_init_weights_tiled(lw.qkv, e->qkv_dim, d, 0, hd, c.weight_seed, 16 + 8 * l + 0, sig, e->stream);
+      launch_init_weights_tiled(lw.o, d, nq * hd, 0, 0, c.weight_seed, 16 + 8 * l + 1, sig, e->stream);
+      launch_init_weights_tiled(lw.gu, 2 * ff, d, ff, 0, c.weight_seed, 16 + 8 * l + 2, sig, e->stream);
+      launch_init_weights_tiled(lw.d, d, ff, 0, 0, c.weight_seed, 16 + 8 * l + 3, sig, e->stream);
     }
     // KV pool
     e->pool_layer_bytes = (int64_t)n_pages * nkv * 64 * hd;
@@ -426,6 +441,16 @@ static rt_status create_impl(rt_engine* e, const rt_config* cfg) {
     e->ev_attn.resize(2 * L);
     for (auto& ev : e->ev_attn) cudaEventCreate(&ev);
   }
+  if (c.flags & RT_FLAG_TRACE) {  // 48-byte records, bound process-wide (last engine wins)
+    e->trace_cap = 1u << 20;
+    CK(e, dalloc(e, &e->d_trace, (size_t)e->trace_cap * 6));
+    CK(e, dalloc(e, &e->d_trace_n, 1));
+    trace_bind_model(e->d_trace, e->d_trace_n, e->trace_cap);
+    trace_bind_attn(e->d_trace, e->d_trace_n, e->trace_cap);
+    trace_bind_gemm(e->d_trace, e->d_trace_n, e->trace_cap);
+    trace_bind_sched(e->d_trace, e->d_trace_n, e->trace_cap);
+    CK(e, cudaGetLastError());
+  }
   // ---- replicas: NCCL communicator (one allgather of top-K candidates per round)
   e->exchange = c.world > 1 || (c.flags & RT_FLAG_FORCE_EXCHANGE);
   if (e->exchange) {
@@ -452,6 +477,12 @@ extern "C" rt_status rt_destroy(rt_engine* e) {
   if (e->stream) cudaStreamSynchronize(e->stream);
   if (e->side) cudaStreamSynchronize(e->side);
   if (e->comm && g_nccl.destroy) g_nccl.destroy(e->comm);
+  if (e->d_trace) {  // unbind before the buffer goes away
+    trace_bind_model(nullptr, nullptr, 0);
+    trace_bind_attn(nullptr, nullptr, 0);
+    trace_bind_gemm(nullptr, nullptr, 0);
+    trace_bind_sched(nullptr, nullptr, 0);
+  }
   for (void* p : e->allocs) cudaFree(p);
   if (e->d_wbuf) cudaFree(e->d_wbuf);
   if (e->d_pool) cudaFree(e->d_pool);
@@ -460,6 +491,7 @@ extern "C" rt_status rt_destroy(rt_engine* e) {
   if (e->h_recs) cudaFreeHost(e->h_recs);
   if (e->h_toks) cudaFreeHost(e->h_toks);
   for (auto ev : e->ev_attn) cudaEventDestroy(ev);
+  for (auto& kv : e->graphs) cudaGraphExecDestroy(kv.second);
   cudaEvent_t evs[] = {e->ev_plan, e->ev_post, e->ev_cand, e->ev_merge, e->ev_f0, e->ev_f1, e->ev_s0, e->ev_s1, e->ev_q1, e->ev_m0, e->ev_m1};
   for (auto ev : evs)
     if (ev) cudaEventDestroy(ev);
@@ -556,9 +588,26 @@ static void harvest_timing(rt_engine* e) {
   if (cudaEventElapsedTime(&ms, e->ev_f0, e->ev_f1) == cudaSuccess) e->stats.gemm_ms += ms;
   e->stats.attn_bytes += e->attn_bytes_pending;
   e->timing_pending = false;
+  // an event pair that was not recorded this round (e.g. no forward) is not an error of the
+  // step: drop the non-sticky error it left so the next CK(cudaGetLastError()) does not see it
+  cudaError_t le = cudaPeekAtLastError();
+  if (le == cudaErrorInvalidResourceHandle || le == cudaErrorNotReady || le == cudaErrorInvalidValue)
+    cudaGetLastError();
 }
 
 // ------------------------------------------------------------------ forward
+// A plain cudaEventRecord inside stream capture becomes an internal dependency node and the
+// event is never actually recorded; cudaEventRecordExternal makes it a real timing record that
+// fires on every graph replay.
+static void record_timing_event(cudaEvent_t ev, cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &cs);
+  if (cs == cudaStreamCaptureStatusActive)
+    cudaEventRecordWithFlags(ev, s, cudaEventRecordExternal);
+  else
+    cudaEventRecord(ev, s);
+}
+
 static rt_status forward(rt_engine* e, const HostMailbox& plan) {
   const rt_config& c = e->cfg;
   const int d = c.d_model, hd = c.head_dim, nq = c.n_q_heads, nkv = c.n_kv_heads, ff = c.d_ff, V = c.vocab;
@@ -571,7 +620,7 @@ static rt_status forward(rt_engine* e, const HostMailbox& plan) {
   int launches = 0;
   for (int row0 = 0; row0 < n_rows; row0 += e->fwd_rows) {
     const int n = std::min(e->fwd_rows, n_rows - row0);
-    launch_embed_norm(P.row_tok, row0, n, e->emb, d, e->d_x, e->d_h, s);
+    launch_embed(P.row_tok, row0, n, e->emb, d, e->d_x, e->d_h, e->d_ss, s);  // d_h = bf16(x), un-normed
     ++launches;
     AttnArgs aa{};
     aa.q = e->d_q;
@@ -587,10 +636,9 @@ static rt_status forward(rt_engine* e, const HostMailbox& plan) {
     aa.hd = hd;
     aa.G = nq / nkv;
     attn_plan(n, nkv, plan.max_seqlen, &aa.chunk_pages, &aa.max_chunks);
-    if (attn_ws_floats(n, nq, hd, aa.max_chunks) > e->attn_ws_cap) {
-      aa.chunk_pages = (plan.max_seqlen + 15) / 16;
-      aa.max_chunks = 1;
-    }
+    if (attn_ws_floats(n, nq, hd, aa.max_chunks) > e->attn_ws_cap) aa.max_chunks = 1;
+    // single chunk: make the kernel arguments independent of max_seqlen (graph replay)
+    if (aa.max_chunks == 1) aa.chunk_pages = e->pt_stride;
     aa.out = e->d_o;
     aa.ws = e->d_attn_ws;
     aa.tickets = e->d_attn_tickets;
@@ -622,28 +670,33 @@ static rt_status forward(rt_engine* e, const HostMailbox& plan) {
         q.q_out = e->d_q;
         q.pool = pool_l;
         q.q_cap = (e->d_cap_q && l == c.capture_layer) ? e->d_cap_q : nullptr;
+        g.rs_ss = e->d_ss;  // attention RMSNorm applied as the epilogue's row scale
+        g.rs_tiles = d_tiles;
         gemm(w.qkv, e->x_h, e->qkv_dim, d, g);
       }
       aa.pool = pool_l;
       aa.out_f32 = (e->d_cap_o && l == c.capture_layer) ? e->d_cap_o : nullptr;
-      if (timing && row0 == 0) cudaEventRecord(e->ev_attn[2 * l], s);
+      if (timing && row0 == 0) record_timing_event(e->ev_attn[2 * l], s);
       launch_attention(aa, s);
       ++launches;
-      if (timing && row0 == 0) cudaEventRecord(e->ev_attn[2 * l + 1], s);
+      if (timing && row0 == 0) record_timing_event(e->ev_attn[2 * l + 1], s);
       {  // O projection + residual
         GemmArgs g{};
         g.mode = EPI_RESID;
         g.x = e->d_x;
         g.ss = e->d_ss;
+        g.xb = e->d_h;
+        gemm_set_prefetch(g, w.gu, 2 * ff, n, d, 0, e->l2_pf_bytes);
         gemm(w.o, e->x_o, d, nq * hd, g);
       }
-      launch_norm_apply(e->d_x, e->d_ss, d_tiles, n, d, e->d_h, s);
-      ++launches;
-      {  // gate/up projection + SwiGLU
+      {  // gate/up projection (FFN RMSNorm as row scale) + SwiGLU
         GemmArgs g{};
         g.mode = EPI_SWIGLU;
         g.act = e->d_act;
         g.ff = ff;
+        g.rs_ss = e->d_ss;
+        g.rs_tiles = d_tiles;
+        gemm_set_prefetch(g, w.d, d, n, ff, 0, e->l2_pf_bytes);
         gemm(w.gu, e->x_h, 2 * ff, d, g);
       }
       {  // down projection + residual
@@ -651,12 +704,16 @@ static rt_status forward(rt_engine* e, const HostMailbox& plan) {
         g.mode = EPI_RESID;
         g.x = e->d_x;
         g.ss = e->d_ss;
+        g.xb = e->d_h;
+        if (l + 1 < c.n_layers)  // the next layer's QKV projection
+          gemm_set_prefetch(g, e->layers[l + 1].qkv, e->qkv_dim, n, d, 0, e->l2_pf_bytes);
+        else if (row0 + n >= n_rows)  // the lm_head of the logits rows
+          gemm_set_prefetch(g, e->lm, V, B, d, 0, e->l2_pf_bytes);
         gemm(w.d, e->x_act, d, ff, g);
       }
-      launch_norm_apply(e->d_x, e->d_ss, d_tiles, n, d, e->d_h, s);  // next layer's / final RMSNorm
-      ++launches;
     }
-    launch_gather_rows(P.slot_row, B, row0, n, e->d_h, d, e->d_hfin, s);
+    // logits rows: final RMSNorm applied while gathering them
+    launch_gather_norm(P.slot_row, B, row0, n, e->d_x, e->d_ss, d, e->d_hfin, s);
     ++launches;
   }
   {  // lm_head + greedy argmax (a8)
@@ -674,6 +731,7 @@ static rt_status forward(rt_engine* e, const HostMailbox& plan) {
   }
   CK(e, cudaGetLastError());
   e->stats.kernel_launches += launches;
+  e->graph_launches = launches;
   if (timing) e->timing_layers = c.n_layers;
   return RT_OK;
 }
@@ -726,8 +784,36 @@ extern "C" rt_status rt_step(rt_engine* e, int64_t now_us, rt_round_info* info) 
   }
   if (timing) cudaEventRecord(e->ev_f0, s);
   if (!(c.flags & RT_FLAG_NO_MODEL)) {
-    st = forward(e, plan);
-    if (st != RT_OK) return st;
+    // Decode-only rounds replay a CUDA graph of the whole forward (launch-gap free,
+    // programmatic-dependency edges kept); its arguments depend only on B and the
+    // split-KV plan, which form the cache key.  Prefill rounds launch directly.
+    const bool graphable = !e->no_graphs && plan.n_prefill_rows == 0 && plan.n_rows == plan.B &&
+                           plan.B <= e->fwd_rows;
+    if (graphable) {
+      int cp = 0, mc = 0;
+      attn_plan(plan.B, c.n_kv_heads, plan.max_seqlen, &cp, &mc);
+      const int64_t key = (int64_t)plan.B | ((int64_t)(mc > 1 ? cp : 0) << 20) | ((int64_t)timing << 40);
+      auto it = e->graphs.find(key);
+      if (it == e->graphs.end()) {
+        cudaGraph_t g = nullptr;
+        cudaGraphExec_t ge = nullptr;
+        CK(e, cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        st = forward(e, plan);
+        cudaError_t ce = cudaStreamEndCapture(s, &g);
+        if (st != RT_OK) return st;
+        CK(e, ce);
+        CK(e, cudaGraphInstantiate(&ge, g, 0));
+        cudaGraphDestroy(g);
+        it = e->graphs.emplace(key, ge).first;
+      } else {
+        e->stats.kernel_launches += e->graph_launches;
+      }
+      CK(e, cudaGraphLaunch(it->second, s));
+      if (timing) e->timing_layers = c.n_layers;
+    } else {
+      st = forward(e, plan);
+      if (st != RT_OK) return st;
+    }
   }
   if (timing) {
     cudaEventRecord(e->ev_f1, s);
@@ -860,6 +946,7 @@ extern "C" rt_status rt_reset_stats(rt_engine* e) {
   rt_status st = rt_sync(e);
   if (st != RT_OK) return st;
   memset(&e->stats, 0, sizeof(e->stats));
+  if (e->d_trace_n) CK(e, cudaMemset(e->d_trace_n, 0, sizeof(unsigned)));
   return RT_OK;
 }
 
@@ -976,6 +1063,13 @@ extern "C" rt_status rt_debug_dump(rt_engine* e, int32_t what, void* dst, int64_
       std::vector<int64_t> v(kTopK * 4);
       for (int i = 0; i < kTopK * 4; ++i) memcpy(&v[i], &m[i], 8);
       return copy_out(e, dst, bytes, v.data(), (int64_t)v.size() * 8, bytes_out, false);
+    }
+    case RT_DUMP_TRACE: {
+      if (!e->d_trace) return fail(e, RT_E_STATE, "RT_FLAG_TRACE not set");
+      unsigned n = 0;
+      CK(e, cudaMemcpy(&n, e->d_trace_n, sizeof n, cudaMemcpyDeviceToHost));
+      n = std::min(n, e->trace_cap);
+      return copy_out(e, dst, bytes, e->d_trace, (int64_t)n * 48, bytes_out);
     }
     default:
       return fail(e, RT_E_INVAL, "unknown dump kind");

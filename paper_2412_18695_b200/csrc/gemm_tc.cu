@@ -26,15 +26,19 @@
 //                   streaming overlaps the previous kernel's tail;
 //   warp 1        : TMEM allocator; lane 0 issues tcgen05.mma.cta_group::1.kind::f16
 //                   (M=128, N=BN, K=16), tcgen05.commit frees stages / signals the epilogue;
-//   warps 2..5    : epilogue — tcgen05.ld.32x32b.x16 (lane quarter = warp % 4), fused
-//                   op of oracle c1 applied from registers in 16-column chunks:
+//   warps 2..5    : epilogue — tcgen05.ld.32x32b.x16 (lane quarter = warp % 4) parks
+//                   the accumulator in shared memory; split-K partials are exchanged
+//                   inside the cluster (DSMEM bulk push, fixed-order sum); then a compact
+//                   4-column loop applies the fused op of oracle c1 (the RMSNorm of the
+//                   input folded in as a per-column scale, g.rs_ss):
 //        EPI_STORE  fp32 out[n][m]
 //        EPI_ARGMAX lm_head: per-tile (max, lowest index) + optional logits
 //        EPI_QKV    RoPE (rotate-half, theta 5e5) on q/k, bf16 q out, bf16 K/V
-//                   appended into the swizzled KV page of (row task, position)
-//        EPI_RESID  x[n][m] += D (fp32 residual stream) + per-tile sum of squares of
-//                   the new x for the following RMSNorm
-//        EPI_SWIGLU rows interleaved per tile [64 gate | 64 up]: act = bf16(silu(g) u)
+//                   appended into the swizzled KV page of (row task, position); the
+//                   rotate-half partners are adjacent weight rows (lane shuffle)
+//        EPI_RESID  x[n][m] += D (fp32 residual stream), bf16 copy for the next GEMM,
+//                   per-tile sum of squares of the new x for the next RMSNorm
+//        EPI_SWIGLU gate / up rows adjacent per feature: act = bf16(silu(g) u)
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include "common.cuh"
@@ -53,11 +57,15 @@ struct GemmCfg {
   static constexpr int STAGES = BN <= 64 ? 4 : (BN == 128 ? 3 : 4);
   static constexpr int CTAS_PER_SM = BN <= 128 ? 2 : 1;
   static constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
-  static constexpr int XCH = 16 * 64 * 4;                       // exchange [16][64] fp32
-  static constexpr int META = 2 * 256 * 4;                      // per-column pos / page
-  static constexpr int RED = 4 * 16 * 8;                        // per-warp column partials
-  static constexpr int SMEM = 1024 + STAGES * STAGE + 512 + XCH + META + RED;
+  static constexpr int META = 3 * BN * 4;                       // per-column pos / page / rms scale
+  static constexpr int RED = 2 * 4 * BN * 4;                    // per-warp column partials (val, idx)
+  static constexpr int XP = 16 * 128 * 4;                       // prefetched epilogue inputs
+  static constexpr int SMEM = 1024 + STAGES * STAGE + 512 + META + RED + XP;
   static_assert(BN * 128 * 4 <= STAGES * STAGE, "partial tile must fit in the ring");
+  static_assert(BN > 128 || SMEM + 1024 <= 233472 / 2, "two CTAs per SM");
+  // push reduction: partial tile + S receive slots of ceil(BN/S) columns (<= BN + 16
+  // columns for S <= 16 ... checked per launch) fit in the ring
+  static constexpr bool PUSH = (2 * BN + 16) * 128 * 4 <= STAGES * STAGE;
 };
 
 // ------------------------------------------------------------------ PTX
@@ -114,9 +122,6 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 __device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
-__device__ __forceinline__ void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -135,141 +140,163 @@ __device__ __forceinline__ float ld_dsmem(uint32_t addr) {
 }
 
 struct EpiSmem {
-  float* xch;    // [16][64]
-  int* pos;      // [256]
-  int* page;     // [256]
-  float* redv;   // [4][16]
-  int* redi;     // [4][16]
+  int* pos;      // [BN] KV position of each column's row (EPI_QKV)
+  int* page;     // [BN] KV page of each column's row (EPI_QKV)
+  float* inv;    // [BN] per-column RMSNorm scale (g.rs_ss)
+  int bn;
+  float* redv;   // [4][BN] per-warp column partials (EPI_RESID sum of squares, EPI_ARGMAX max)
+  int* redi;     // [4][BN] per-warp argmax index
+  float* xp;     // [16][128] epilogue inputs prefetched during the mainloop (EPI_RESID x;
+                 //  EPI_QKV cos [16][64] then sin [16][64])
+  long long* mark;  // clock64 phase marks (trace), written by thread et == 0
 };
+#define EPI_MARK(i) \
+  if (et == 0) sm.mark[i] = clock64()
+
+// Where the finished tile's value (column c, row r) comes from: this CTA's parked partial
+// P [BN][128] (S = 1), or the S split-K partials summed in fixed rank order from the local
+// receive slots (push) or from the peers' P over DSMEM (pull).
+struct TileSrc {
+  const float* P;
+  const float* R;
+  uint32_t pl;  // smem address of P (pull)
+  int S, rank, slot_cols, cb, kind;  // kind 0 local, 1 push, 2 pull
+};
+// v[k] = value of columns c0 + k (k < 4) at row r; 4 independent loads per rank
+__device__ __forceinline__ void tile_vals4(const TileSrc& t, int c0, int r, float (&v)[4]) {
+  if (t.kind == 0) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = t.P[(c0 + k) * 128 + r];
+    return;
+  }
+#pragma unroll
+  for (int k = 0; k < 4; ++k) v[k] = 0.f;
+#pragma unroll 1
+  for (int rk = 0; rk < t.S; ++rk) {
+    float w[4];
+    if (t.kind == 1) {
+      const float* src = rk == t.rank ? t.P + (size_t)c0 * 128 : t.R + ((size_t)rk * t.slot_cols + (c0 - t.cb)) * 128;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) w[k] = src[k * 128 + r];
+    } else {
+      const uint32_t base = dsmem_addr(t.pl, (uint32_t)rk) + (uint32_t)((c0 * 128 + r) * 4);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) w[k] = ld_dsmem(base + k * 512);
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] += w[k];
+  }
+}
 
 // ------------------------------------------------------------ fused epilogue ops
-// v[16] = D[m0 + et][n0 + c0 .. c0 + nv - 1] (nv <= 16 valid columns); executed by
-// the 128 epilogue threads of one CTA (every thread must call it: named barriers).
-template <int BN>
-__device__ void epi_chunk(const GemmArgs& g, const EpiSmem& sm, const float* v, int m_tile, int n0, int c0,
-                          int nv, int et) {
-  const int NL = min(g.N, n0 + c0 + nv);  // columns >= NL are not owned / out of range
+// The finished columns [cb, ce) of this CTA, 4 per iteration of a non-unrolled loop:
+// the epilogue runs once per CTA, so its code must stay small (instruction-cache misses
+// from a fully unrolled epilogue cost several microseconds per launch) and it is inlined
+// at ONE call site (a non-inlined call would pass the kernel parameters through local
+// memory).  All 128 epilogue threads call it (named barrier at the end).
+template <int MODE>
+__device__ __forceinline__ void epilogue(const GemmArgs& g, const EpiSmem& sm, const TileSrc& ts, int m_tile,
+                                      int n0, int cb, int ce, int et, bool pre) {
   const int m0 = m_tile * 128;
   const int m = m0 + et;
   const int lane = et & 31, wq = et >> 5;
-  switch (g.mode) {
-    case EPI_STORE: {
-      if (m < g.M)
+  const int NL = min(g.N - n0, ce);  // columns >= NL are out of range
+  // The pairwise ops read the partner row from the adjacent TMEM lane (et ^ 1; the weight
+  // rows are laid out pairwise, tiled_logical_row in model.cu) with one shuffle.
+  bool active = m < g.M;
+  if constexpr (MODE == EPI_SWIGLU) active = m_tile * 64 + (et >> 1) < g.ff;
+#pragma unroll 1
+  for (int c0 = cb; c0 < ce; c0 += 4) {
+    float v[4], u[4];
+    tile_vals4(ts, c0, et, v);
+    if (g.rs_ss)
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
-          if (n0 + c0 + j < NL) g.out[(size_t)(n0 + c0 + j) * g.M + m] = v[j];
-      break;
-    }
-    case EPI_RESID: {
-      float sq[16];
-      float xv[16];
+      for (int k = 0; k < 4; ++k) v[k] *= (c0 + k < NL) ? sm.inv[c0 + k] : 0.f;
+    if (MODE == EPI_SWIGLU || MODE == EPI_QKV)
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int n = n0 + c0 + j;
-        xv[j] = (n < NL && m < g.M) ? g.x[(size_t)n * g.M + m] : 0.f;
-      }
+      for (int k = 0; k < 4; ++k) u[k] = __shfl_xor_sync(0xffffffffu, v[k], 1);
+    if constexpr (MODE == EPI_STORE) {
+      if (active)
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        const int n = n0 + c0 + j;
+        for (int k = 0; k < 4; ++k)
+          if (c0 + k < NL) g.out[(size_t)(n0 + c0 + k) * g.M + m] = v[k];
+    } else if constexpr (MODE == EPI_RESID) {
+      float xv[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        xv[k] = (active && c0 + k < NL) ? (pre ? sm.xp[(c0 - cb + k) * 128 + et] : g.x[(size_t)(n0 + c0 + k) * g.M + m])
+                                        : 0.f;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
         float xn = 0.f;
-        if (n < NL && m < g.M) {
-          xn = xv[j] + v[j];
-          g.x[(size_t)n * g.M + m] = xn;
+        if (active && c0 + k < NL) {
+          xn = xv[k] + v[k];
+          g.x[(size_t)(n0 + c0 + k) * g.M + m] = xn;
+          if (g.xb) g.xb[(size_t)(n0 + c0 + k) * g.M + m] = __float2bfloat16_rn(xn);
         }
-        sq[j] = xn * xn;
+        const float sq = warp_sum(xn * xn);
+        if (lane == 0) sm.redv[wq * sm.bn + c0 + k] = sq;
       }
+    } else if constexpr (MODE == EPI_SWIGLU) {
+      // even lane: gate row, odd lane: up row of feature jf; the even lane writes columns
+      // c0, c0 + 1 and the odd lane c0 + 2, c0 + 3
+      const bool odd = et & 1;
+      const int jf = m_tile * 64 + (et >> 1);
+      if (active)
 #pragma unroll
-      for (int j = 0; j < 16; ++j) sq[j] = warp_sum(sq[j]);
-      if (lane == 0)
-#pragma unroll
-        for (int j = 0; j < 16; ++j) sm.redv[wq * 16 + j] = sq[j];
-      epi_bar();
-      if (et < 16 && n0 + c0 + et < NL) {
-        const float s = ((sm.redv[et] + sm.redv[16 + et]) + sm.redv[32 + et]) + sm.redv[48 + et];
-        g.ss[(size_t)(n0 + c0 + et) * ((g.M + 127) / 128) + m_tile] = s;
-      }
-      epi_bar();
-      break;
-    }
-    case EPI_SWIGLU: {
-      // rows [0,64) = gate features j0..j0+63, rows [64,128) = up features j0..j0+63
-      if (et >= 64)
-#pragma unroll
-        for (int j = 0; j < 16; ++j) sm.xch[j * 64 + (et - 64)] = v[j];
-      epi_bar();
-      const int jf = m_tile * 64 + et;
-      if (et < 64 && jf < g.ff)
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int n = n0 + c0 + j;
-          if (n < NL) {
-            const float gv = v[j], uv = sm.xch[j * 64 + et];
-            const float sgv = gv / (1.f + __expf(-gv));
-            g.act[(size_t)n * g.ff + jf] = __float2bfloat16_rn(sgv * uv);
+        for (int kk = 0; kk < 2; ++kk) {
+          const int k = kk + (odd ? 2 : 0);
+          if (c0 + k < NL) {
+            const float gv = odd ? u[k] : v[k], uv = odd ? v[k] : u[k];
+            const float sgv = __fdividef(gv, 1.f + __expf(-gv));
+            g.act[(size_t)(n0 + c0 + k) * g.ff + jf] = __float2bfloat16_rn(sgv * uv);
           }
         }
-      epi_bar();
-      break;
-    }
-    case EPI_QKV: {
+    } else if constexpr (MODE == EPI_QKV) {
+      // row 2i of a head = dim i, row 2i + 1 = dim i + hd/2 (rotate-half partners); every
+      // lane produces its own dim: y_i = x_i cos - x_{i+h} sin, y_{i+h} = x_{i+h} cos + x_i sin
       const QkvFuse& q = g.qkv;
       const int hd = q.hd, half = hd >> 1;
-      const int hl = et / hd, i_full = et % hd;     // head within tile, dim within head
-      const bool upper = i_full >= half;
-      const int pidx = hl * half + (i_full % half); // pair index in [0, 64)
-      if (upper)
+      const int r = et % hd, i = r >> 1;
+      const bool odd = r & 1;
+      const int dim = odd ? i + half : i;
+      const int head = m / hd;
+      const bool rope = head < q.nq + q.nkv;
+      if (active)
 #pragma unroll
-        for (int j = 0; j < 16; ++j) sm.xch[j * 64 + pidx] = v[j];
-      epi_bar();
-      const int f = m0 + hl * hd + i_full;          // feature of this (lower) element
-      if (!upper && f < g.M) {
-        const int head = f / hd, i = i_full;
-#pragma unroll 4
-        for (int j = 0; j < 16; ++j) {
-          const int c = c0 + j, n = n0 + c;
-          if (n >= NL) break;
-          const int pos = sm.pos[c];
-          float x1 = v[j], x2 = sm.xch[j * 64 + pidx];
-          if (head < q.nq + q.nkv) {
-            const float cs = q.cos[(size_t)pos * half + i], sn = q.sin[(size_t)pos * half + i];
-            const float y1 = x1 * cs - x2 * sn, y2 = x2 * cs + x1 * sn;
-            x1 = y1;
-            x2 = y2;
-          }
-          const bf16 b1 = __float2bfloat16_rn(x1), b2 = __float2bfloat16_rn(x2);
-          if (head < q.nq) {
-            bf16* qo = q.q_out + ((size_t)n * q.nq + head) * hd;
-            qo[i] = b1;
-            qo[i + half] = b2;
-            if (q.q_cap) {
-              float* qc = q.q_cap + ((size_t)(q.row0 + n) * q.nq + head) * hd;
-              qc[i] = __bfloat162float(b1);
-              qc[i + half] = __bfloat162float(b2);
+        for (int k = 0; k < 4; ++k) {
+          const int c = c0 + k;
+          if (c < NL) {
+            const int pos = sm.pos[c];
+            float y = v[k];
+            if (rope) {
+              const float cs = pre ? sm.xp[(c - cb) * 64 + i] : q.cos[(size_t)pos * half + i];
+              const float sn = pre ? sm.xp[1024 + (c - cb) * 64 + i] : q.sin[(size_t)pos * half + i];
+              y = odd ? v[k] * cs + u[k] * sn : v[k] * cs - u[k] * sn;
             }
-          } else {
-            const int kind = head < q.nq + q.nkv ? 0 : 1;
-            const int kvh = kind == 0 ? head - q.nq : head - q.nq - q.nkv;
-            const int off = pos & 15;
-            unsigned char* blk = (unsigned char*)q.pool +
-                                 (((size_t)sm.page[c] * q.nkv + kvh) * 2 + kind) * (size_t)(16 * hd * 2) +
-                                 off * hd * 2;
-            *(bf16*)(blk + (kv_swz_chunk(hd, off, i >> 3) << 4) + ((i & 7) << 1)) = b1;
-            *(bf16*)(blk + (kv_swz_chunk(hd, off, (i + half) >> 3) << 4) + (((i + half) & 7) << 1)) = b2;
+            const bf16 b = __float2bfloat16_rn(y);
+            const int n = n0 + c;
+            if (head < q.nq) {
+              q.q_out[((size_t)n * q.nq + head) * hd + dim] = b;
+              if (q.q_cap) q.q_cap[((size_t)(q.row0 + n) * q.nq + head) * hd + dim] = __bfloat162float(b);
+            } else {
+              const int kind = rope ? 0 : 1;
+              const int kvh = kind == 0 ? head - q.nq : head - q.nq - q.nkv;
+              const int off = pos & 15;
+              unsigned char* blk = (unsigned char*)q.pool +
+                                   (((size_t)sm.page[c] * q.nkv + kvh) * 2 + kind) * (size_t)(16 * hd * 2) +
+                                   off * hd * 2;
+              *(bf16*)(blk + (kv_swz_chunk(hd, off, dim >> 3) << 4) + ((dim & 7) << 1)) = b;
+            }
           }
         }
-      }
-      epi_bar();
-      break;
-    }
-    case EPI_ARGMAX: {
-      if (g.out && m < g.M)
+    } else if constexpr (MODE == EPI_ARGMAX) {
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
-          if (n0 + c0 + j < NL) g.out[(size_t)(n0 + c0 + j) * g.M + m] = v[j];
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {  // greedy: max over the tile's rows, lowest index on ties
-        float bv = (m < g.M) ? v[j] : -INFINITY;
-        int bi = (m < g.M) ? m : INT_MAX;
+      for (int k = 0; k < 4; ++k) {  // greedy: max over the tile's rows, lowest index on ties
+        const bool ok = active && c0 + k < NL;
+        if (ok && g.out) g.out[(size_t)(n0 + c0 + k) * g.M + m] = v[k];
+        float bv = ok ? v[k] : -INFINITY;
+        int bi = ok ? m : INT_MAX;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) {
           const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
@@ -280,35 +307,103 @@ __device__ void epi_chunk(const GemmArgs& g, const EpiSmem& sm, const float* v, 
           }
         }
         if (lane == 0) {
-          sm.redv[wq * 16 + j] = bv;
-          sm.redi[wq * 16 + j] = bi;
+          sm.redv[wq * sm.bn + c0 + k] = bv;
+          sm.redi[wq * sm.bn + c0 + k] = bi;
         }
       }
-      epi_bar();
-      if (et < 16 && n0 + c0 + et < NL) {
-        float bv = sm.redv[et];
-        int bi = sm.redi[et];
+    }
+  }
+  EPI_MARK(6);
+  if constexpr (MODE == EPI_RESID || MODE == EPI_ARGMAX) {
+    epi_bar();
+    for (int c = cb + et; c < NL; c += 128) {  // fixed order over the 4 row quarters
+      if constexpr (MODE == EPI_RESID) {
+        const float t = ((sm.redv[c] + sm.redv[sm.bn + c]) + sm.redv[2 * sm.bn + c]) + sm.redv[3 * sm.bn + c];
+        g.ss[(size_t)(n0 + c) * ((g.M + 127) / 128) + m_tile] = t;
+      } else {
+        float bv = sm.redv[c];
+        int bi = sm.redi[c];
         for (int w = 1; w < 4; ++w) {
-          const float ov = sm.redv[w * 16 + et];
-          const int oi = sm.redi[w * 16 + et];
+          const float ov = sm.redv[w * sm.bn + c];
+          const int oi = sm.redi[w * sm.bn + c];
           if (ov > bv || (ov == bv && oi < bi)) {
             bv = ov;
             bi = oi;
           }
         }
-        g.part_val[(size_t)m_tile * g.N + n0 + c0 + et] = bv;
-        g.part_idx[(size_t)m_tile * g.N + n0 + c0 + et] = bi;
+        g.part_val[(size_t)m_tile * g.N + n0 + c] = bv;
+        g.part_idx[(size_t)m_tile * g.N + n0 + c] = bi;
       }
-      epi_bar();
-      break;
     }
-    default:
-      break;
   }
+  EPI_MARK(7);
 }
 
+// Per-column metadata of columns [cb, ce) for the 128 epilogue threads: KV position /
+// page of the row (EPI_QKV) and the RMSNorm scale of the row (g.rs_ss; summation order
+// of the per-tile sums fixed, t = 0 .. rs_tiles - 1).  Then, when the CTA finishes at most
+// 16 columns, its epilogue's global inputs are prefetched into sm.xp while the mainloop
+// runs (returns true).
+template <int MODE>
+__device__ __forceinline__ bool column_meta(const GemmArgs& g, const EpiSmem& sm, int m_tile, int n0, int cb, int ce,
+                                         int et) {
+  if (MODE != EPI_QKV && MODE != EPI_RESID && !g.rs_ss) return false;
+  for (int cc = cb + et; cc < ce; cc += 128) {
+    const int n = n0 + cc;
+    if (n >= g.N) {
+      sm.inv[cc] = 0.f;
+      continue;
+    }
+    if (MODE == EPI_QKV) {
+      const int row = g.qkv.row0 + n;
+      const int pos = g.qkv.row_pos[row];
+      sm.pos[cc] = pos;
+      sm.page[cc] = g.qkv.page_table[(size_t)g.qkv.row_task[row] * g.qkv.pt_stride + (pos >> 4)];
+    }
+    if (g.rs_ss) {
+      float t = 0.f;
+      for (int i = 0; i < g.rs_tiles; ++i) t += g.rs_ss[(size_t)n * g.rs_tiles + i];
+      sm.inv[cc] = rsqrtf(t / (float)g.K + 1e-5f);
+    }
+  }
+  epi_bar();
+  if (ce - cb > 16) return false;
+  const int m = m_tile * 128 + et;
+  if constexpr (MODE == EPI_RESID) {
+#pragma unroll 1
+    for (int c = cb; c < ce; ++c)
+      if (m < g.M && n0 + c < g.N) sm.xp[(c - cb) * 128 + et] = g.x[(size_t)(n0 + c) * g.M + m];
+    return true;
+  } else if constexpr (MODE == EPI_QKV) {
+    const int half = g.qkv.hd >> 1;
+    if (et < 64) {  // cos / sin of the rotation (position of the column, frequency i)
+      const int i = et % half;
+#pragma unroll 1
+      for (int c = cb; c < ce; ++c)
+        if (n0 + c < g.N) {
+          const int pos = sm.pos[c];
+          sm.xp[(c - cb) * 64 + et] = g.qkv.cos[(size_t)pos * half + i];
+          sm.xp[1024 + (c - cb) * 64 + et] = g.qkv.sin[(size_t)pos * half + i];
+        }
+    }
+    return true;
+  }
+  return false;
+}
 
-template <int BN>
+__device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.aligned;" ::: "memory"); }
+__device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.aligned;" ::: "memory"); }
+// DSMEM push: bulk copy of `bytes` from this CTA's shared memory to the same-offset-space
+// address `dst` of another CTA of the cluster, completing on that CTA's mbarrier `bar`
+// (both cluster addresses from mapa)
+__device__ __forceinline__ void bulk_s2cluster(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+      "r"(smem_u32(src)), "r"(bytes), "r"(bar)
+      : "memory");
+}
+
+template <int BN, int MODE>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_gemm_tc(const __grid_constant__ TmaMap tmB, GemmArgs g) {
   using C = GemmCfg<BN>;
@@ -320,15 +415,25 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(ctl);
   uint64_t* empty = full + C::STAGES;
   uint64_t* done = empty + C::STAGES;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
-  float* P = reinterpret_cast<float*>(smem);  // [BN][128] partial tile, reuses the ring after the mainloop
+  uint64_t* recv_bar = done + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(recv_bar + 1);
+  // after the mainloop the ring holds this CTA's fp32 partial tile P [BN][128] (column
+  // major) and, with the push reduction, the receive slots [S][slot_cols][128]
+  float* P = reinterpret_cast<float*>(smem);
+  float* R = P + BN * 128;
   EpiSmem sm;
-  sm.xch = reinterpret_cast<float*>(ctl + 512);
-  sm.pos = reinterpret_cast<int*>(ctl + 512 + C::XCH);
-  sm.page = sm.pos + 256;
-  sm.redv = reinterpret_cast<float*>(ctl + 512 + C::XCH + C::META);
-  sm.redi = reinterpret_cast<int*>(sm.redv + 64);
+  sm.pos = reinterpret_cast<int*>(ctl + 512);
+  sm.page = sm.pos + BN;
+  sm.inv = reinterpret_cast<float*>(sm.page + BN);
+  sm.redv = reinterpret_cast<float*>(ctl + 512 + C::META);
+  sm.redi = reinterpret_cast<int*>(sm.redv + 4 * BN);
+  sm.bn = BN;
+  sm.xp = reinterpret_cast<float*>(ctl + 512 + C::META + C::RED);
+  __shared__ long long s_mark[9];  // clock64 phase marks (SM cycles), RT_FLAG_TRACE
+  sm.mark = s_mark;
 
+  TraceScope tr(TK_GEMM | ((uint32_t)MODE << 8) | (gridDim.x << 16));
+  __shared__ unsigned long long s_tdone;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int S = gridDim.x;                 // cluster = the S split-K CTAs of one tile
   const int rank = S > 1 ? (int)cluster_rank() : 0;
@@ -337,6 +442,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int kb1 = (int)(((long long)g.kb_total * (rank + 1)) / S);
   const int nkb = kb1 - kb0;
   const int n0 = n_tile * BN;
+  const int cb = (BN * rank) / S, ce = (BN * (rank + 1)) / S;  // columns this CTA finishes
+  const int slot_cols = (BN + S - 1) / S;
+  const bool push = C::PUSH && S > 1;
+  bool pre = false;  // epilogue inputs prefetched into sm.xp
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmB);
@@ -345,6 +454,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       mbar_init(&empty[s], 1);
     }
     mbar_init(done, 1);
+    mbar_init(recv_bar, 1);
     fence_mbar_init();
   }
   if (warp == 1) {
@@ -362,17 +472,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     if (lane == 0) {
       // weights do not depend on the previous kernel: request the first stages' W tiles
       // before waiting for it (programmatic dependent launch)
-      const int pre = min(C::STAGES, nkb);
+      const int pre_k = min(C::STAGES, nkb);
       // UMMA-tiled weights: k-block kb of m-tile mt is one contiguous 16 KiB SW128 image
       const bf16* wt = g.w + ((size_t)m_tile * g.kb_total + kb0) * (128 * kBK);
-      for (int i = 0; i < pre; ++i) {
+      for (int i = 0; i < pre_k; ++i) {
         mbar_arrive_expect_tx(&full[i], C::STAGE);
         bulk_g2s(sA + i * C::A_BYTES, wt + (size_t)i * (128 * kBK), C::A_BYTES, &full[i]);
       }
       pdl_wait();
-      for (int i = 0; i < pre; ++i)
+      tr.ready();
+      for (int i = 0; i < pre_k; ++i)
         tma_load_2d(sB + i * C::B_BYTES, &tmB, (kb0 + i) * kBK, n0, &full[i]);
-      for (int i = pre; i < nkb; ++i) {
+      for (int i = pre_k; i < nkb; ++i) {
         const int s = i % C::STAGES;
         const uint32_t ph = (uint32_t)((i / C::STAGES) & 1);
         mbar_wait(&empty[s], ph ^ 1u);
@@ -380,7 +491,22 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         bulk_g2s(sA + s * C::A_BYTES, wt + (size_t)i * (128 * kBK), C::A_BYTES, &full[s]);
         tma_load_2d(sB + s * C::B_BYTES, &tmB, (kb0 + i) * kBK, n0, &full[s]);
       }
+      if (g.pf_w && n_tile == 0) {  // next launch's first k-blocks -> L2 (weights only)
+        const int L = blockIdx.x + gridDim.x * blockIdx.y, T = gridDim.x * gridDim.y;
+        for (int j = L; j < g.pf_S * g.pf_m_tiles; j += T) {
+          const int pr = j % g.pf_S, pm = j / g.pf_S;
+          const int pk0 = (int)(((long long)g.pf_kb_total * pr) / g.pf_S);
+          const int pk1 = (int)(((long long)g.pf_kb_total * (pr + 1)) / g.pf_S);
+          const int cnt = min(g.pf_kb, pk1 - pk0);
+          if (cnt > 0)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
+                             g.pf_w + ((size_t)pm * g.pf_kb_total + pk0) * (128 * kBK)),
+                         "r"((uint32_t)cnt * C::A_BYTES)
+                         : "memory");
+        }
+      }
     }
+    __syncwarp();
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc = umma_idesc(128, BN);
@@ -404,79 +530,81 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int q = warp & 3;
     const int et = q * 32 + lane;  // tile row owned by this thread
     const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16);
+    // per-column metadata + epilogue inputs of the columns this CTA finishes, while the
+    // mainloop runs
+    pre = column_meta<MODE>(g, sm, m_tile, n0, cb, ce, et);
     mbar_wait(done, 0);
     tc_fence_after();
-    if (S == 1) {
-      if (g.mode == EPI_QKV) {
-        for (int cc = et; cc < BN; cc += 128) {
-          const int n = n0 + cc;
-          if (n < g.N) {
-            const int row = g.qkv.row0 + n;
-            const int pos = g.qkv.row_pos[row];
-            sm.pos[cc] = pos;
-            sm.page[cc] = g.qkv.page_table[(size_t)g.qkv.row_task[row] * g.qkv.pt_stride + (pos >> 4)];
-          }
-        }
-        epi_bar();
-      }
-#pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 16) {
-        float v[16];
-        tmem_ld16(tb + c0, v);
-        epi_chunk<BN>(g, sm, v, m_tile, n0, c0, 16, et);
-      }
-    } else {
-#pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 16) {  // park the partial in this CTA's smem
-        float v[16];
-        tmem_ld16(tb + c0, v);
+    if (et == 0) {
+      s_tdone = gtimer();
+      const long long t = clock64();
 #pragma unroll
-        for (int j = 0; j < 16; ++j) P[(c0 + j) * 128 + et] = v[j];
-      }
+      for (int i = 0; i < 9; ++i) s_mark[i] = t;
     }
+#pragma unroll 1
+    for (int c0 = 0; c0 < BN; c0 += 16) {  // park the accumulator in shared memory
+      float v[16];
+      tmem_ld16(tb + c0, v);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) P[(c0 + j) * 128 + et] = v[j];
+    }
+    if (push) fence_proxy_async();  // P is read by the bulk-copy (async) proxy
+    EPI_MARK(1);
   }
+  // ---- cluster split-K: CTA `rank` finishes columns [cb, ce) of the tile.  The barrier
+  // also certifies that every CTA's mainloop is over (its ring is free for the slices).
   if (S > 1) {
-    // ---- cluster reduction: CTA `rank` finishes columns [cb, ce) of the tile
-    __syncwarp();        // reconverge the producer / MMA warps (aligned cluster barrier)
-    cluster_sync_all();  // every partial of the cluster is in shared memory
-    if (warp >= 2) {
-      const int et = (warp & 3) * 32 + lane;
-      const int cb = (BN * rank) / S, ce = (BN * (rank + 1)) / S;
-      if (g.mode == EPI_QKV) {
-        for (int cc = cb + et; cc < ce; cc += 128) {
-          const int n = n0 + cc;
-          if (n < g.N) {
-            const int row = g.qkv.row0 + n;
-            const int pos = g.qkv.row_pos[row];
-            sm.pos[cc] = pos;
-            sm.page[cc] = g.qkv.page_table[(size_t)g.qkv.row_task[row] * g.qkv.pt_stride + (pos >> 4)];
-          }
+    __syncwarp();
+    cluster_arrive();
+    cluster_wait();
+  }
+  if (warp >= 2) {
+    const int et = (warp & 3) * 32 + lane;
+    EPI_MARK(2);
+    if (S > 1 && push) {
+      // push: each CTA sends the column slice of every other rank straight into that
+      // rank's receive slot [my rank] (one bulk copy per peer, TMA engine), then sums the
+      // S slices of its own columns from local shared memory
+      if (et == 0) {
+        mbar_arrive_expect_tx(recv_bar, (uint32_t)((S - 1) * (ce - cb) * 512));
+        const uint32_t rslot = smem_u32(R + (size_t)rank * slot_cols * 128);
+        for (int r = 0; r < S; ++r) {
+          if (r == rank) continue;
+          const int rb = (BN * r) / S, re = (BN * (r + 1)) / S;
+          bulk_s2cluster(dsmem_addr(rslot, (uint32_t)r), P + (size_t)rb * 128, (uint32_t)((re - rb) * 512),
+                         dsmem_addr(smem_u32(recv_bar), (uint32_t)r));
         }
-        epi_bar();
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
       }
-      const uint32_t pl = smem_u32(P);
-#pragma unroll 1
-      for (int c0 = cb; c0 < ce; c0 += 16) {
-        const int nv = min(16, ce - c0);
-        float v[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) v[j] = 0.f;
-#pragma unroll 1
-        for (int rk = 0; rk < S; ++rk) {  // fixed rank order -> deterministic
-          const uint32_t base = dsmem_addr(pl, (uint32_t)rk);
-          float w[16];
-#pragma unroll
-          for (int j = 0; j < 16; ++j) w[j] = (j < nv) ? ld_dsmem(base + (uint32_t)(((c0 + j) * 128 + et) * 4)) : 0.f;
-#pragma unroll
-          for (int j = 0; j < 16; ++j) v[j] += w[j];
-        }
-        epi_chunk<BN>(g, sm, v, m_tile, n0, c0, nv, et);
-      }
+      mbar_wait(recv_bar, 0);
     }
-    cluster_sync_all();  // keep shared memory alive until every CTA has read it
+    EPI_MARK(3);
+    EPI_MARK(4);
+    EPI_MARK(5);
+    const TileSrc ts{P, R, smem_u32(P), S, rank, slot_cols, cb, S == 1 ? 0 : (push ? 1 : 2)};
+    epilogue<MODE>(g, sm, ts, m_tile, n0, cb, ce, et, pre);
+    if (push && et == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+    EPI_MARK(8);
+  }
+  if (S > 1 && !push) {  // keep shared memory alive until every CTA has read it
+    __syncwarp();
+    cluster_arrive();
+    cluster_wait();
   }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) {
+    tr.aux(s_tdone);
+    // SM-cycle durations of the 8 phases after the accumulator is complete (clock64; the
+    // %globaltimer granularity is too coarse for them), two per 64-bit field: park |
+    // cluster barrier | slices received | - | - | epilogue loop | final reduction | exit
+    auto dd = [&](int i) {
+      const long long d = s_mark[i + 1] - s_mark[i];
+      return (unsigned long long)(uint32_t)(d > 0 ? d : 0);
+    };
+    trace_phase(TK_PHASE | TK_GEMM | ((uint32_t)MODE << 8) | (gridDim.x << 16), dd(0) | (dd(1) << 32),
+                dd(2) | (dd(3) << 32), dd(4) | (dd(5) << 32), dd(6) | (dd(7) << 32));
+  }
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::TMEM_COLS));
@@ -521,49 +649,15 @@ bool make_gemm_act_maps(GemmTmaSet* out, const void* base, int K, int rows_cap) 
 
 int gemm_bn(int N) { return N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256; }
 
-template <int BN>
+template <int BN, int MODE>
 static void ensure_attrs() {
   using C = GemmCfg<BN>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_gemm_tc<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    cudaFuncSetAttribute(k_gemm_tc<BN>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(k_gemm_tc<BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaFuncSetAttribute(k_gemm_tc<BN, MODE>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     attr = true;
   }
-}
-
-// how many S-CTA clusters of k_gemm_tc<BN> can be co-resident (cached per S)
-template <int BN>
-static int max_clusters(int S) {
-  using C = GemmCfg<BN>;
-  static int cache[17] = {0};
-  if (S < 1 || S > 16) return 0;
-  if (!cache[S]) {
-    ensure_attrs<BN>();
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(S, 64, 1);
-    cfg.blockDim = dim3(kGemmThreads);
-    cfg.dynamicSmemBytes = C::SMEM;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = S;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    int n = 0;
-    if (cudaOccupancyMaxActiveClusters(&n, (void*)k_gemm_tc<BN>, &cfg) != cudaSuccess) n = 0;
-    cudaGetLastError();
-    cache[S] = n > 0 ? n : -1;
-  }
-  return cache[S] > 0 ? cache[S] : 0;
-}
-
-static int max_clusters_bn(int bn, int S) {
-  if (bn == 32) return max_clusters<32>(S);
-  if (bn == 64) return max_clusters<64>(S);
-  if (bn == 128) return max_clusters<128>(S);
-  return max_clusters<256>(S);
 }
 
 // Cluster split count (measured on B200, tools/gemm_bench.py, N = 64): a split-K cluster
@@ -581,14 +675,13 @@ int gemm_choose_splits(int M, int N, int K) {
   int best = 1;
   for (int s = 2; s <= 8 && kb / s >= 4; ++s)
     if (tiles * s <= budget) best = s;
-  (void)max_clusters_bn;
   return best;
 }
 
-template <int BN>
+template <int BN, int MODE>
 static cudaError_t launch_bn(const TmaMap& b, const GemmArgs& g, int S, cudaStream_t s) {
   using C = GemmCfg<BN>;
-  ensure_attrs<BN>();
+  ensure_attrs<BN, MODE>();
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(S, (g.M + 127) / 128, (g.N + BN - 1) / BN);
   cfg.blockDim = dim3(kGemmThreads);
@@ -596,14 +689,39 @@ static cudaError_t launch_bn(const TmaMap& b, const GemmArgs& g, int S, cudaStre
   cfg.stream = s;
   cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   at[1].id = cudaLaunchAttributeClusterDimension;
   at[1].val.clusterDim.x = S;
   at[1].val.clusterDim.y = 1;
   at[1].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, k_gemm_tc<BN>, b, g);
+  return cudaLaunchKernelEx(&cfg, k_gemm_tc<BN, MODE>, b, g);
+}
+
+void gemm_set_prefetch(GemmArgs& g, const bf16* w, int M, int N, int K, int splits, int64_t budget_bytes) {
+  if (!w || budget_bytes <= 0) {
+    g.pf_w = nullptr;
+    return;
+  }
+  const int kbt = K / kBK;
+  int S = splits > 0 ? splits : gemm_choose_splits(M, N, K);
+  S = std::max(1, std::min(S, std::min(16, kbt)));
+  const int mt = (M + 127) / 128;
+  const int64_t per_kb = (int64_t)S * mt * (128 * kBK * 2);
+  g.pf_w = w;
+  g.pf_S = S;
+  g.pf_m_tiles = mt;
+  g.pf_kb_total = kbt;
+  g.pf_kb = (int)std::max<int64_t>(1, std::min<int64_t>((kbt + S - 1) / S, budget_bytes / per_kb));
+}
+
+template <int MODE>
+static cudaError_t launch_mode(const GemmTmaSet& x, const GemmArgs& g, int bn, int S, cudaStream_t s) {
+  if (bn == 32) return launch_bn<32, MODE>(x.m32, g, S, s);
+  if (bn == 64) return launch_bn<64, MODE>(x.m64, g, S, s);
+  if (bn == 128) return launch_bn<128, MODE>(x.m128, g, S, s);
+  return launch_bn<256, MODE>(x.m256, g, S, s);
 }
 
 cudaError_t launch_gemm_epi(const bf16* w_tiled, const GemmTmaSet& x, GemmArgs g, int splits, cudaStream_t s) {
@@ -613,10 +731,16 @@ cudaError_t launch_gemm_epi(const bf16* w_tiled, const GemmTmaSet& x, GemmArgs g
   g.m_tiles = (g.M + 127) / 128;
   if (splits <= 0) splits = gemm_choose_splits(g.M, g.N, g.K);
   splits = std::max(1, std::min(splits, std::min(16, g.kb_total)));
-  if (bn == 32) return launch_bn<32>(x.m32, g, splits, s);
-  if (bn == 64) return launch_bn<64>(x.m64, g, splits, s);
-  if (bn == 128) return launch_bn<128>(x.m128, g, splits, s);
-  return launch_bn<256>(x.m256, g, splits, s);
+  switch (g.mode) {
+    case EPI_STORE: return launch_mode<EPI_STORE>(x, g, bn, splits, s);
+    case EPI_ARGMAX: return launch_mode<EPI_ARGMAX>(x, g, bn, splits, s);
+    case EPI_QKV: return launch_mode<EPI_QKV>(x, g, bn, splits, s);
+    case EPI_RESID: return launch_mode<EPI_RESID>(x, g, bn, splits, s);
+    case EPI_SWIGLU: return launch_mode<EPI_SWIGLU>(x, g, bn, splits, s);
+    default: return cudaErrorInvalidValue;
+  }
 }
+
+RT_TRACE_BINDER(trace_bind_gemm)
 
 }  // namespace rt

@@ -31,38 +31,31 @@ __global__ void k_init_weights(bf16* out, int64_t n, uint64_t seed, int32_t tens
   }
 }
 
-// W_gate_up physical row p -> logical row: tile i = p / 128, r = p % 128,
-// r < 64 -> gate feature 64 i + r, else up feature ff + 64 i + r - 64
-__global__ void k_init_weights_gu(bf16* out, int ff, int d, uint64_t seed, int32_t tensor_id, float c) {
-  const uint64_t key = seed ^ ((uint64_t)tensor_id << 40);
-  const int64_t n = (int64_t)2 * ff * d;
-  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t p = i / d, col = i % d;
-    const int64_t t = p >> 7, r = p & 127;
-    const int64_t lrow = r < 64 ? 64 * t + r : (int64_t)ff + 64 * t + (r - 64);
-    const uint64_t u = splitmix64(key ^ (uint64_t)(lrow * d + col));
-    const float v = __fsub_rn(__fmul_rn((float)(uint32_t)(u >> 40), 5.9604644775390625e-08f), 0.5f);
-    out[i] = __float2bfloat16_rn(__fmul_rn(v, c));
-  }
-}
-
-void launch_init_weights_gu(bf16* out, int ff, int d, uint64_t seed, int32_t tensor_id, float sigma,
-                            cudaStream_t s) {
-  const float c = (float)(2.0 * 1.7320508075688772 * (double)sigma);
-  k_init_weights_gu<<<148 * 64, 256, 0, s>>>(out, ff, d, seed, tensor_id, c);
-}
 
 // ------------------------------------------- UMMA-tiled weight layout
 // A [M, K] weight is stored as contiguous 128 x 64 bf16 tiles (16 KiB), tile (mt, kb)
 // at index mt * KB + kb, each tile in the SW128 K-major smem image: row r, 16-byte
 // chunk c stored at chunk c ^ (r & 7).  One cp.async.bulk of 16 KiB per k-block
 // lands a ready UMMA operand; a CTA streams one contiguous HBM range.
-// Logical row of tiled row p (gu_ff > 0: gate/up interleave [64 gate | 64 up] per tile).
-__device__ __forceinline__ int64_t tiled_logical_row(int64_t p, int gu_ff) {
-  if (gu_ff <= 0) return p;
-  const int64_t t = p >> 7, r = p & 127;
-  return r < 64 ? 64 * t + r : (int64_t)gu_ff + 64 * t + (r - 64);
+// Logical row of tiled row p, or -1 for a zero pad row.  The GEMM epilogues combine PAIRS
+// of rows, which the layout puts in adjacent rows (adjacent TMEM lanes -> one warp
+// shuffle, no shared-memory exchange):
+//   gu_ff > 0   (W_gate_up, [2 ff, d]): tile t holds features [64 t, 64 t + 64), physical
+//               row 2k = gate of feature 64 t + k, row 2k + 1 = its up row;
+//   rope_hd > 0 (W_qkv): inside every head block of rope_hd rows, physical row 2k = dim k,
+//               row 2k + 1 = dim k + rope_hd / 2 (the rotate-half partner).
+__device__ __forceinline__ int64_t tiled_logical_row(int64_t p, int M, int gu_ff, int rope_hd) {
+  if (gu_ff > 0) {
+    const int64_t j = 64 * (p >> 7) + ((p & 127) >> 1);
+    if (j >= gu_ff) return -1;
+    return (p & 1) ? (int64_t)gu_ff + j : j;
+  }
+  if (p >= M) return -1;
+  if (rope_hd > 0) {
+    const int64_t h = p / rope_hd, r = p % rope_hd;
+    return h * rope_hd + (r >> 1) + ((r & 1) ? rope_hd / 2 : 0);
+  }
+  return p;
 }
 // element i of the tiled buffer -> (physical row p, logical column col)
 __device__ __forceinline__ void tiled_coords(int64_t i, int KB, int64_t* p, int* col) {
@@ -74,8 +67,8 @@ __device__ __forceinline__ void tiled_coords(int64_t i, int KB, int64_t* p, int*
   *col = (int)(kb * 64 + ((pc ^ (r & 7)) << 3) + e);
 }
 
-__global__ void k_init_weights_tiled(bf16* out, int M, int K, int gu_ff, uint64_t seed, int32_t tensor_id,
-                                     float c) {
+__global__ void k_init_weights_tiled(bf16* out, int M, int K, int gu_ff, int rope_hd, uint64_t seed,
+                                     int32_t tensor_id, float c) {
   const uint64_t key = seed ^ ((uint64_t)tensor_id << 40);
   const int KB = K / 64;
   const int64_t n = (int64_t)((M + 127) / 128) * 128 * K;
@@ -84,21 +77,21 @@ __global__ void k_init_weights_tiled(bf16* out, int M, int K, int gu_ff, uint64_
     int64_t p;
     int col;
     tiled_coords(i, KB, &p, &col);
-    if (p >= M) {
+    const int64_t lrow = tiled_logical_row(p, M, gu_ff, rope_hd);
+    if (lrow < 0) {
       out[i] = __float2bfloat16_rn(0.f);
       continue;
     }
-    const int64_t lrow = tiled_logical_row(p, gu_ff);
     const uint64_t u = splitmix64(key ^ (uint64_t)(lrow * K + col));
     const float v = __fsub_rn(__fmul_rn((float)(uint32_t)(u >> 40), 5.9604644775390625e-08f), 0.5f);
     out[i] = __float2bfloat16_rn(__fmul_rn(v, c));
   }
 }
 
-void launch_init_weights_tiled(bf16* out, int M, int K, int gu_ff, uint64_t seed, int32_t tensor_id, float sigma,
-                               cudaStream_t s) {
+void launch_init_weights_tiled(bf16* out, int M, int K, int gu_ff, int rope_hd, uint64_t seed, int32_t tensor_id,
+                               float sigma, cudaStream_t s) {
   const float c = (float)(2.0 * 1.7320508075688772 * (double)sigma);
-  k_init_weights_tiled<<<148 * 64, 256, 0, s>>>(out, M, K, gu_ff, seed, tensor_id, c);
+  k_init_weights_tiled<<<148 * 64, 256, 0, s>>>(out, M, K, gu_ff, rope_hd, seed, tensor_id, c);
 }
 
 // row-major [M, K] -> tiled (zero-padded rows); used by the op-level GEMM entry points
@@ -138,68 +131,76 @@ __device__ float block_sum(float v, float* red) {
   return t;
 }
 
-// ---------------------------------------------------- embedding + first norm
-// x[r] = emb[tok[r]] (fp32), h[r] = bf16(rms(x[r]))
-__global__ void k_embed_norm(const int32_t* row_tok, int32_t row0, const bf16* emb, int d, float* x,
-                             bf16* h) {
-  __shared__ float red[32];
+// ---------------------------------------------------------------- embedding
+// x[r] = emb[tok[r]] (fp32 residual), xb[r] = bf16(x[r]) (GEMM operand), ss[r][t] = sum of
+// squares of x[r] over feature tile t (128 features) — the same un-normalised form the
+// EPI_RESID epilogue leaves, so the first RMSNorm is applied by the QKV GEMM epilogue.
+__global__ void k_embed(const int32_t* row_tok, int32_t row0, const bf16* emb, int d, int n_tiles, float* x,
+                        bf16* xb, float* ss) {
+  TraceScope tr(TK_EMBED);
+  if (threadIdx.x == 0) pdl_trigger();
+  pdl_wait();  // row_tok comes from the scheduler kernel
+  tr.ready();
   const int r = blockIdx.x;
   const int tok = row_tok[row0 + r];
   const bf16* e = emb + (size_t)tok * d;
   float* xr = x + (size_t)r * d;
-  float ss = 0.f;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) {
-    const float v = __bfloat162float(e[i]);
-    xr[i] = v;
-    ss += v * v;
+  bf16* hr = xb + (size_t)r * d;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int t = warp; t < n_tiles; t += nw) {
+    float sq = 0.f;
+    for (int i = t * 128 + lane; i < min(d, t * 128 + 128); i += 32) {
+      const bf16 b = e[i];
+      const float v = __bfloat162float(b);
+      xr[i] = v;
+      hr[i] = b;
+      sq += v * v;
+    }
+    sq = warp_sum(sq);
+    if (lane == 0) ss[(size_t)r * n_tiles + t] = sq;
   }
-  const float tot = block_sum(ss, red);
-  const float inv = rsqrtf(tot / (float)d + 1e-5f);
-  bf16* hr = h + (size_t)r * d;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) hr[i] = __float2bfloat16_rn(xr[i] * inv);
 }
 
-// ------------------------------------------------------------- RMSNorm apply
-// h[r][i] = bf16(x[r][i] * rsqrt(sum_t ss[r][t] / d + 1e-5)); ss holds the per-tile
-// sums of squares written by the EPI_RESID GEMM epilogue (fixed summation order).
-__global__ void k_norm_apply(const float* x, const float* ss, int n_tiles, int d, bf16* h) {
+// RMSNorm scale of row r from the per-tile sums of squares (fixed order, shared with the
+// GEMM epilogue's row scaling): rsqrt(sum_t ss[r][t] / d + 1e-5)
+__device__ __forceinline__ float rms_inv(const float* ss, int n_tiles, int r, int d) {
+  float t = 0.f;
+  for (int i = 0; i < n_tiles; ++i) t += ss[(size_t)r * n_tiles + i];
+  return rsqrtf(t / (float)d + 1e-5f);
+}
+
+// ------------------------------------------- gather logits rows + final RMSNorm
+// hfin[s] = bf16(x[r] * rms_inv(r)), r = slot_row[s] - row0, for slots whose logits row
+// lies in this chunk
+__global__ void k_gather_norm(const int32_t* slot_row, int B, int row0, int n_rows, const float* x,
+                              const float* ss, int n_tiles, int d, bf16* hfin) {
+  TraceScope tr(TK_GATHER);
   if (threadIdx.x == 0) pdl_trigger();
   pdl_wait();
-  const int r = blockIdx.y;
-  __shared__ float inv;
-  if (threadIdx.x == 0) {
-    float t = 0.f;
-    for (int i = 0; i < n_tiles; ++i) t += ss[(size_t)r * n_tiles + i];
-    inv = rsqrtf(t / (float)d + 1e-5f);
-  }
-  __syncthreads();
-  const int i = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
-  if (i < d) {
-    const float4 v = *reinterpret_cast<const float4*>(x + (size_t)r * d + i);
-    uint2 o;
-    o.x = pack_bf16x2(v.x * inv, v.y * inv);
-    o.y = pack_bf16x2(v.z * inv, v.w * inv);
-    *reinterpret_cast<uint2*>(h + (size_t)r * d + i) = o;
-  }
-}
-
-// -------------------------------------------------- gather logits rows
-// hfin[s] = h[slot_row[s] - row0] for slots whose logits row lies in this chunk
-__global__ void k_gather_rows(const int32_t* slot_row, int B, int row0, int n_rows, const bf16* h, int d,
-                              bf16* hfin) {
+  tr.ready();
   const int s = blockIdx.x;
   if (s >= B) return;
   const int r = slot_row[s] - row0;
   if (r < 0 || r >= n_rows) return;
-  const uint4* src = (const uint4*)(h + (size_t)r * d);
-  uint4* dst = (uint4*)(hfin + (size_t)s * d);
-  for (int i = threadIdx.x; i < d / 8; i += blockDim.x) dst[i] = src[i];
+  __shared__ float inv;
+  if (threadIdx.x == 0) inv = rms_inv(ss, n_tiles, r, d);
+  __syncthreads();
+  const float4* src = (const float4*)(x + (size_t)r * d);
+  uint2* dst = (uint2*)(hfin + (size_t)s * d);
+  for (int i = threadIdx.x; i < d / 4; i += blockDim.x) {
+    const float4 v = src[i];
+    dst[i] = make_uint2(pack_bf16x2(v.x * inv, v.y * inv), pack_bf16x2(v.z * inv, v.w * inv));
+  }
 }
 
 // ------------------------------------------------------ argmax final reduce
 // part_val/part_idx [n_mtiles][N]; lowest index wins ties (c3)
 __global__ void k_argmax_reduce(const float* part_val, const int32_t* part_idx, int n_mtiles, int N,
                                 int32_t* tok) {
+  TraceScope tr(TK_ARGMAX);
+  if (threadIdx.x == 0) pdl_trigger();
+  pdl_wait();
+  tr.ready();
   const int n = blockIdx.x;
   float best = -INFINITY;
   int bi = INT_MAX;
@@ -271,21 +272,17 @@ __global__ void k_kv_read(const unsigned char* pool, bf16* out, int nkv, int hd)
 }
 
 // ------------------------------------------------------------- launchers
-void launch_embed_norm(const int32_t* row_tok, int row0, int n, const bf16* emb, int d, float* x, bf16* h,
-                       cudaStream_t s) {
-  k_embed_norm<<<n, 256, 0, s>>>(row_tok, row0, emb, d, x, h);
+void launch_embed(const int32_t* row_tok, int row0, int n, const bf16* emb, int d, float* x, bf16* xb, float* ss,
+                  cudaStream_t s) {
+  launch_pdl(k_embed, dim3(n), dim3(256), 0, s, row_tok, row0, emb, d, (d + 127) / 128, x, xb, ss);
 }
-void launch_norm_apply(const float* x, const float* ss, int n_tiles, int n, int d, bf16* h, cudaStream_t s) {
-  dim3 g((d / 4 + 127) / 128, n);
-  launch_pdl(k_norm_apply, g, dim3(128), 0, s, x, ss, n_tiles, d, h);
-}
-void launch_gather_rows(const int32_t* slot_row, int B, int row0, int n, const bf16* h, int d, bf16* hfin,
-                        cudaStream_t s) {
-  k_gather_rows<<<B, 128, 0, s>>>(slot_row, B, row0, n, h, d, hfin);
+void launch_gather_norm(const int32_t* slot_row, int B, int row0, int n, const float* x, const float* ss, int d,
+                        bf16* hfin, cudaStream_t s) {
+  launch_pdl(k_gather_norm, dim3(B), dim3(128), 0, s, slot_row, B, row0, n, x, ss, (d + 127) / 128, d, hfin);
 }
 void launch_argmax_reduce(const float* pv, const int32_t* pi, int n_mtiles, int N, int32_t* tok,
                           cudaStream_t s) {
-  k_argmax_reduce<<<N, 256, 0, s>>>(pv, pi, n_mtiles, N, tok);
+  launch_pdl(k_argmax_reduce, dim3(N), dim3(256), 0, s, pv, pi, n_mtiles, N, tok);
 }
 void launch_kv_write(void* pool, const bf16* k, const bf16* v, const int32_t* slot, int n, int nkv, int hd,
                      cudaStream_t s) {
@@ -294,5 +291,7 @@ void launch_kv_write(void* pool, const bf16* k, const bf16* v, const int32_t* sl
 void launch_kv_read(const void* pool, bf16* out, int n_pages, int nkv, int hd, cudaStream_t s) {
   k_kv_read<<<n_pages, 256, 0, s>>>((const unsigned char*)pool, out, nkv, hd);
 }
+
+RT_TRACE_BINDER(trace_bind_model)
 
 }  // namespace rt

@@ -11,21 +11,20 @@ typedef __nv_bfloat16 bf16;
 
 // ---- row / elementwise kernels (model.cu)
 void launch_init_weights(bf16* out, int64_t n, uint64_t seed, int32_t tensor_id, float sigma, cudaStream_t s);
-// W_gate_up stored with rows interleaved per 128-row tile: [64 gate | 64 up] (EPI_SWIGLU)
-void launch_init_weights_gu(bf16* out, int ff, int d, uint64_t seed, int32_t tensor_id, float sigma,
-                            cudaStream_t s);
 // UMMA-tiled weights: 128 x 64 bf16 tiles (16 KiB, SW128 image), tile (mt, kb) at mt*KB+kb;
-// gu_ff > 0 interleaves gate/up rows per tile.  Buffer size ceil(M/128)*128*K elements.
-void launch_init_weights_tiled(bf16* out, int M, int K, int gu_ff, uint64_t seed, int32_t tensor_id, float sigma,
-                               cudaStream_t s);
+// gu_ff > 0 pairs gate/up rows (row 2k gate, 2k+1 up of feature 64 t + k in tile t);
+// rope_hd > 0 pairs the rotate-half partners inside each head (row 2k dim k, 2k+1 dim
+// k + hd/2).  Buffer size ceil(M/128)*128*K elements.
+void launch_init_weights_tiled(bf16* out, int M, int K, int gu_ff, int rope_hd, uint64_t seed, int32_t tensor_id,
+                               float sigma, cudaStream_t s);
 void launch_pack_tiled(const bf16* src, bf16* dst, int M, int K, cudaStream_t s);
 inline int64_t tiled_elems(int M, int K) { return (int64_t)((M + 127) / 128) * 128 * K; }
-void launch_embed_norm(const int32_t* row_tok, int row0, int n, const bf16* emb, int d, float* x, bf16* h,
-                       cudaStream_t s);
-// h[n] = bf16(x[n] * rsqrt(sum_t ss[n][t] / d + eps)), ss: [n][n_tiles] partial sums of squares
-void launch_norm_apply(const float* x, const float* ss, int n_tiles, int n, int d, bf16* h, cudaStream_t s);
-void launch_gather_rows(const int32_t* slot_row, int B, int row0, int n, const bf16* h, int d, bf16* hfin,
-                        cudaStream_t s);
+// x = emb[tok] (fp32), xb = bf16(x), ss [n][ceil(d/128)] per-tile sums of squares of x
+void launch_embed(const int32_t* row_tok, int row0, int n, const bf16* emb, int d, float* x, bf16* xb, float* ss,
+                  cudaStream_t s);
+// hfin[s] = bf16(RMSNorm(x[slot_row[s] - row0])) from x fp32 and its ss partials
+void launch_gather_norm(const int32_t* slot_row, int B, int row0, int n, const float* x, const float* ss, int d,
+                        bf16* hfin, cudaStream_t s);
 void launch_argmax_reduce(const float* pv, const int32_t* pi, int n_mtiles, int N, int32_t* tok,
                           cudaStream_t s);
 void launch_kv_write(void* pool, const bf16* k, const bf16* v, const int32_t* slot, int n, int nkv, int hd,
@@ -83,13 +82,33 @@ struct GemmArgs {
   float* part_val;    // EPI_ARGMAX [m_tiles][N]
   int32_t* part_idx;
   float* x;           // EPI_RESID residual [N][M]
-  float* ss;          // EPI_RESID [N][m_tiles]
+  float* ss;          // EPI_RESID [N][m_tiles] per-tile sums of squares of the new x
+  bf16* xb;           // EPI_RESID nullable: bf16(new x) [N][M], the next GEMM's operand
+  // RMSNorm folded into the epilogue (all modes, nullable): D[m][n] *= rsqrt(sum_t
+  // rs_ss[n][t] / K + 1e-5) — the GEMM ran on bf16(x) and the row scale is linear
+  const float* rs_ss;
+  int rs_tiles;
   bf16* act;          // EPI_SWIGLU [N][ff]
   int ff;
   QkvFuse qkv;        // EPI_QKV
+  // L2 prefetch of the NEXT projection's weights (nullable): when its loads are issued,
+  // the producer prefetches the first pf_kb k-blocks of every CTA of the next launch
+  // (grid pf_S x pf_m_tiles, K = pf_kb_total k-blocks) so that kernel starts on L2 hits
+  // while this one drains its pipeline and runs its epilogue (HBM would idle).
+  const bf16* pf_w;
+  int pf_S, pf_m_tiles, pf_kb_total, pf_kb;
 };
+// fill g.pf_* for a next launch of weights w [M x K] at N columns (splits <= 0: auto),
+// prefetching at most budget_bytes in total
+void gemm_set_prefetch(GemmArgs& g, const bf16* w, int M, int N, int K, int splits, int64_t budget_bytes);
 int gemm_bn(int N);
 int gemm_choose_splits(int M, int N, int K);   // cluster split-K factor (1..16)
 // splits <= 0: gemm_choose_splits
 cudaError_t launch_gemm_epi(const bf16* w_tiled, const GemmTmaSet& xmaps, GemmArgs g, int splits, cudaStream_t s);
+
+// ---- device trace buffers (common.cuh TraceScope), one binder per translation unit
+void trace_bind_model(void* rec, unsigned* n, unsigned cap);
+void trace_bind_attn(void* rec, unsigned* n, unsigned cap);
+void trace_bind_gemm(void* rec, unsigned* n, unsigned cap);
+void trace_bind_sched(void* rec, unsigned* n, unsigned cap);
 }  // namespace rt

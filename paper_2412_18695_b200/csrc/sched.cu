@@ -176,6 +176,7 @@ __device__ __forceinline__ bool key_before(const PreSmem& S, int x, int y, int n
 }
 
 __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, int64_t now_us) {
+  TraceScope tr(TK_SCHED_PRE);
   extern __shared__ __align__(16) unsigned char dsm[];
   PreSmem& S = *reinterpret_cast<PreSmem*>(dsm);
   __shared__ long long s_t;
@@ -582,6 +583,7 @@ struct PostSmem {
 };
 
 __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_post(SchedParams p) {
+  TraceScope tr(TK_SCHED_POST);
   extern __shared__ __align__(16) unsigned char dsm[];
   PostSmem& S = *reinterpret_cast<PostSmem*>(dsm);
   __shared__ int wbuf[32];
@@ -736,6 +738,7 @@ void launch_sched_post(const SchedParams& p, cudaStream_t s) {
 // all: [world][kTopK][4] (pri, arrival, rid, rank); merged: global top-K by
 // (pri desc, arrival asc, rid asc) over the union (AMB-22); rid < 0 = empty.
 __global__ void k_merge_cand(const double* all, int world, double* merged) {
+  TraceScope tr(TK_MERGE);
   __shared__ double key[8 * kTopK][4];
   __shared__ int perm[8 * kTopK];
   const int n = world * kTopK;
@@ -788,5 +791,7 @@ void launch_priority_batch(const int64_t* trde, const int32_t* k, const double* 
                            int g_us, int net_us, int eps_l_us, double* pri, cudaStream_t s) {
   if (n > 0) k_priority_batch<<<(n + 127) / 128, 128, 0, s>>>(trde, k, alpha, beta, n, g_us, net_us, eps_l_us, pri);
 }
+
+RT_TRACE_BINDER(trace_bind_sched)
 
 }  // namespace rt

@@ -17,9 +17,15 @@ RT_CLOCK_VIRTUAL, RT_CLOCK_WALL = 0, 1
 RT_POLICY_PUD, RT_POLICY_FCFS, RT_POLICY_EDF = 0, 1, 2
 RT_STOP_NONE, RT_STOP_EOS, RT_STOP_MAXNEW, RT_STOP_SKILL, RT_STOP_CAP = 0, 1, 2, 3, 4
 RT_FLAG_NO_MODEL, RT_FLAG_KEEP_LOGITS, RT_FLAG_CAPTURE, RT_FLAG_TIMING, RT_FLAG_FORCE_EXCHANGE = 1, 2, 4, 8, 16
+RT_FLAG_GRAPHS, RT_FLAG_TRACE = 32, 64
 (RT_DUMP_TASKS, RT_DUMP_PAGE_TABLES, RT_DUMP_ROUND, RT_DUMP_LOGITS, RT_DUMP_HIDDEN, RT_DUMP_CAPTURE_Q,
  RT_DUMP_CAPTURE_O, RT_DUMP_ROWS, RT_DUMP_KV_LAYER, RT_DUMP_FREE_STACK, RT_DUMP_TASK_SLOTS,
- RT_DUMP_MERGED) = range(1, 13)
+ RT_DUMP_MERGED, RT_DUMP_TRACE) = range(1, 14)
+# rt_trace_rec (include/rt.h)
+TRACE_DTYPE = np.dtype([("grid", "<u8"), ("kind", "<u4"), ("smid", "<u4"), ("t_entry", "<u8"),
+                        ("t_ready", "<u8"), ("t_aux", "<u8"), ("t_exit", "<u8")])
+TRACE_KINDS = {1: "gemm", 2: "attn", 3: "norm", 4: "embed", 5: "sched_pre", 6: "sched_post", 7: "gather",
+               8: "argmax", 9: "merge"}
 
 EXPORTED = ["rt_create", "rt_destroy", "rt_submit_request", "rt_step", "rt_poll_segment", "rt_last_round",
             "rt_sync", "rt_get_stats", "rt_reset_stats", "rt_debug_dump", "rt_last_error", "rt_version",
@@ -283,6 +289,10 @@ class Engine:
         buf = np.zeros(max(need.value, 1), dtype=np.uint8)
         _check(lib().rt_debug_dump(self.h, what, buf.ctypes.data, buf.nbytes, C.byref(need)), self.h)
         return buf[:need.value].view(dtype)
+
+    def trace(self):
+        """Per-CTA kernel records since the last reset_stats (RT_FLAG_TRACE)."""
+        return self.dump(RT_DUMP_TRACE, TRACE_DTYPE)
 
 
 def _info_dict(i):

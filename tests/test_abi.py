@@ -75,6 +75,9 @@ def test_struct_layouts_match_header(tmp_path):
         lines.append(f'printf("{name} %zu\\n", sizeof({name}));')
         for f, _ in cls._fields_:
             lines.append(f'printf("{name}.{f} %zu\\n", offsetof({name}, {f}));')
+    lines.append('printf("rt_trace_rec %zu\\n", sizeof(rt_trace_rec));')
+    for f in rt.TRACE_DTYPE.names:
+        lines.append(f'printf("rt_trace_rec.{f} %zu\\n", offsetof(rt_trace_rec, {f}));')
     lines.append("return 0;}")
     src = tmp_path / "layout.c"
     src.write_text("\n".join(lines))
@@ -85,3 +88,6 @@ def test_struct_layouts_match_header(tmp_path):
         assert int(got[name]) == C.sizeof(cls), name
         for f, _ in cls._fields_:
             assert int(got[f"{name}.{f}"]) == getattr(cls, f).offset, (name, f)
+    assert int(got["rt_trace_rec"]) == rt.TRACE_DTYPE.itemsize == 48
+    for f in rt.TRACE_DTYPE.names:
+        assert int(got[f"rt_trace_rec.{f}"]) == rt.TRACE_DTYPE.fields[f][1], f

@@ -175,12 +175,13 @@ def test_submit_errors(rt):
 
 
 # ------------------------------------------------------------- model parity
-def test_tiny_model_e2e_and_per_op(rt):
+@pytest.mark.parametrize("graphs", [False, True])
+def test_tiny_model_e2e_and_per_op(rt, graphs):
     shape = MODEL_SHAPES["tiny"]
     v = make_vocab(shape.vocab)
     p = engine_params("paper-4090", max_batch=4, max_tasks=64, max_ctx=256, n_pages=64)
     reqs = compose_workload(4, 1.0, 2, range(1, 9), 30.0, 0, v, prompt_len_range=(40, 64), max_requests=12)
-    flags = rt.RT_FLAG_KEEP_LOGITS | rt.RT_FLAG_CAPTURE
+    flags = rt.RT_FLAG_KEEP_LOGITS | rt.RT_FLAG_CAPTURE | (rt.RT_FLAG_GRAPHS if graphs else 0)
     eng, ora = make_pair(rt, v, p, shape=shape, seed=3, flags=flags, model=True, capture_layer=1)
     submit_both(eng, ora, reqs)
     worst_logit = worst_attn = worst_lm = 0.0
@@ -373,3 +374,33 @@ def test_llama8b_shape_sampled(rt):
     W = OW.matrix(11, OW.TID_LM, cols, shape.d_model)
     err = np.abs(h @ W.T - lg[:, cols]).max()
     assert err < 1e-2, err
+
+
+def test_device_trace_records(rt):
+    """RT_FLAG_TRACE: one record per CTA with ordered timestamps, every kernel role present."""
+    shape = MODEL_SHAPES["tiny"]
+    v = make_vocab(shape.vocab)
+    p = engine_params("paper-4090", max_batch=4, max_tasks=16, max_ctx=256, n_pages=64)
+    eng = rt.Engine(shape, p, v, seed=5, flags=rt.RT_FLAG_TRACE)
+    for i in range(3):
+        eng.submit(i, [1 + i, 2, 3, 4], 0, 1_000_000, -1.0, 1.0, 0, max_new_tokens=8)
+    eng.step()
+    eng.reset_stats()
+    for _ in range(3):
+        eng.step()
+    eng.sync()
+    tr = eng.trace()
+    assert len(tr) > 0
+    tr = tr[(tr["kind"] & 0x80) == 0]   # phase records carry cycle counts, not timestamps
+    assert (tr["t_entry"] <= tr["t_ready"]).all() and (tr["t_ready"] <= tr["t_exit"]).all()
+    kinds = set(int(k) & 0xFF for k in tr["kind"])
+    assert {1, 2, 4, 5, 6, 7, 8} <= kinds, kinds
+    gemm = tr[(tr["kind"] & 0xFF) == 1]
+    assert (gemm["t_aux"] >= gemm["t_ready"]).all() and (gemm["t_aux"] <= gemm["t_exit"]).all()
+    # 3 decode rounds: one launch of the scheduler pre/post kernels each
+    grids = {int(k) & 0xFF: set() for k in tr["kind"]}
+    for r in tr:
+        grids[int(r["kind"]) & 0xFF].add(int(r["grid"]))
+    assert len(grids[5]) == 3 and len(grids[6]) == 3
+    assert len(grids[2]) > 0 and len(grids[2]) % shape.n_layers == 0
+    eng.close()

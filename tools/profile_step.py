@@ -15,18 +15,14 @@ from synth import MODEL_SHAPES, make_vocab, engine_params  # noqa: E402
 from paper_2412_18695_b200 import rt  # noqa: E402
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--steps", type=int, default=1)
-    ap.add_argument("--agents", type=int, default=bench.AGENTS_PER_GPU)
-    a = ap.parse_args()
+def setup(B, flags=0):
+    """The bench's steady state: B drone agents resident, decode-only rounds."""
     shape = MODEL_SHAPES["llama3-8b"]
     vocab = make_vocab(shape.vocab)
-    B = a.agents
     n_pages = B * 3 * ((bench.MAX_CTX + 15) // 16) // 2
     p = engine_params("b200-roofline", max_batch=B, max_tasks=4 * B, max_ctx=bench.MAX_CTX, n_pages=n_pages,
                       clock_mode=1)
-    eng = rt.Engine(shape, p, vocab, seed=1234, flags=0, max_rows_per_forward=8192)
+    eng = rt.Engine(shape, p, vocab, seed=1234, flags=flags, max_rows_per_forward=8192)
     t0 = time.perf_counter()
     now = lambda: int((time.perf_counter() - t0) * 1e6)  # noqa: E731
     for j in range(B):
@@ -43,6 +39,15 @@ def main():
     for _ in range(6):
         info = eng.step(now())
     eng.sync()
+    return eng, now
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--steps", type=int, default=1)
+    ap.add_argument("--agents", type=int, default=bench.AGENTS_PER_GPU)
+    a = ap.parse_args()
+    eng, now = setup(a.agents)
     torch.cuda.synchronize()
     torch.cuda.profiler.start()
     for _ in range(a.steps):
