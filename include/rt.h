@@ -187,7 +187,7 @@ enum {
 };
 /* One kernel CTA: grid = %gridid (unique per launch); kind = 1 GEMM (| epilogue mode << 8 |
  * cluster split << 16), 2 attention, 3 norm, 4 embed, 5/6 scheduler pre/post, 7 gather,
- * 8 argmax reduce, 9 candidate merge; t_* = %globaltimer ns at CTA entry, after its
+ * 8 argmax reduce, 9 candidate merge, 10 prefill attention; t_* = %globaltimer ns at CTA entry, after its
  * dependency wait (griddepcontrol.wait; = entry for kernels without one), t_aux = GEMM:
  * accumulator complete (last tcgen05.mma retired, seen by the epilogue; 0 elsewhere) and
  * t_exit at CTA exit. */

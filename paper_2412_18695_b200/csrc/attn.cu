@@ -43,8 +43,10 @@ __global__ void __launch_bounds__(kAttnWarps * 32) k_attn(AttnArgs a) {
 
   TraceScope tr(TK_ATTN);
   if (threadIdx.x == 0) pdl_trigger();
-  const int chunk = blockIdx.x, h = blockIdx.y, r = blockIdx.z;
-  const int row = a.row0 + r;
+  const int chunk = blockIdx.x, h = blockIdx.y;
+  const int row = a.row_list ? a.row_list[blockIdx.z] : a.row0 + (int)blockIdx.z;
+  const int r = row - a.row0;  // row within this forward chunk
+  if (a.row_list && (r < 0 || r >= a.chunk_rows)) return;
   const int seqlen = a.row_seqlen ? a.row_seqlen[row] : a.row_pos[row] + 1;
   const int n_pages = (seqlen + 15) >> 4;
   const int n_chunks = (n_pages + a.chunk_pages - 1) / a.chunk_pages;
@@ -251,6 +253,194 @@ __global__ void __launch_bounds__(kAttnWarps * 32) k_attn(AttnArgs a) {
   }
 }
 
+
+// ---------------------------------------------------------------- prefill attention
+// Causal attention of the prompt rows of k = 0 admissions (oracle c1: the
+// same softmax(q K^T / sqrt(hd)) V over positions <= the row's own).  The decode kernel
+// above would re-read a prompt's K/V once per ROW; here one CTA serves a tile of 16
+// consecutive positions for all G q heads of a kv head, so every (page, kv head) block
+// is read once per tile and feeds 16 x G query rows:
+//  * CTA = (tile, kv head), warp g = q head h*G + g, the warp's 16 query rows = the tile's
+//    positions (mma.sync M dimension);
+//  * pages 0 .. pos0/16 stream through a CTA-shared ring of STAGES (page, kv head)
+//    blocks, one cp.async.bulk each, full / empty mbarriers (G consumer warps);
+//  * S = Q K^T and O += P V on m16n8k16 (bf16 in, fp32 acc), online softmax in fp32 with
+//    exp2, causal mask on the diagonal page only; longest tiles are scheduled first.
+template <int HD>
+struct PfCfg {
+  static constexpr int BLOCK = 64 * HD;
+  static constexpr int STAGES = 4;
+  static constexpr int SMEM = STAGES * BLOCK + 2 * STAGES * 8 + 64;
+};
+
+template <int HD>
+__global__ void __launch_bounds__(256) k_attn_prefill(PrefillArgs a) {
+  using C = PfCfg<HD>;
+  using SW = KvSwz<HD>;
+  extern __shared__ __align__(1024) unsigned char smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::BLOCK);
+  uint64_t* empty = full + C::STAGES;
+
+  TraceScope tr(TK_ATTN_PREFILL);
+  if (threadIdx.x == 0) pdl_trigger();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gq = lane >> 2, qq = lane & 3;
+  const int G = a.G;
+  const int h = blockIdx.y;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], G);
+    }
+    fence_mbar_init();
+  }
+  __syncthreads();
+  pdl_wait();  // q and the prompt's K/V pages come from the QKV GEMM before this kernel
+  tr.ready();
+  const int4 T = a.tiles[a.n_tiles - 1 - (int)blockIdx.x];  // (row, rows, pos0, task)
+  const int rb = T.x, re = T.x + T.y;
+  if (max(rb, a.row0) >= min(re, a.row0 + a.n_rows)) return;  // not in this forward chunk
+  const int np = (T.z >> 4) + 1;                                // pages 0 .. pos0 / 16
+  const int32_t* ptab = a.page_table + (size_t)T.w * a.pt_stride;
+  const unsigned char* pool = (const unsigned char*)a.pool;
+  const size_t head_off = (size_t)h * C::BLOCK;
+  const size_t page_stride = (size_t)a.nkv * C::BLOCK;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < C::STAGES && i < np; ++i) {
+      mbar_arrive_expect_tx(&full[i], C::BLOCK);
+      bulk_g2s(smem + i * C::BLOCK, pool + (size_t)ptab[i] * page_stride + head_off, C::BLOCK, &full[i]);
+    }
+
+  // q fragments (A operand, rows = the tile's positions), rows outside the chunk are zero
+  const int qh = h * G + warp;
+  uint32_t qa[HD / 16][4];
+  {
+    const int r0 = rb + gq, r1 = rb + gq + 8;
+    const bool ok0 = r0 < re && r0 >= a.row0 && r0 < a.row0 + a.n_rows;
+    const bool ok1 = r1 < re && r1 >= a.row0 && r1 < a.row0 + a.n_rows;
+    const uint32_t* q0 = reinterpret_cast<const uint32_t*>(a.q + ((size_t)(r0 - a.row0) * a.nq + qh) * HD);
+    const uint32_t* q1 = reinterpret_cast<const uint32_t*>(a.q + ((size_t)(r1 - a.row0) * a.nq + qh) * HD);
+#pragma unroll
+    for (int ks = 0; ks < HD / 16; ++ks) {
+      qa[ks][0] = ok0 ? q0[ks * 8 + qq] : 0u;
+      qa[ks][1] = ok1 ? q1[ks * 8 + qq] : 0u;
+      qa[ks][2] = ok0 ? q0[ks * 8 + 4 + qq] : 0u;
+      qa[ks][3] = ok1 ? q1[ks * 8 + 4 + qq] : 0u;
+    }
+  }
+  float o[HD / 8][4];
+#pragma unroll
+  for (int nt = 0; nt < HD / 8; ++nt) o[nt][0] = o[nt][1] = o[nt][2] = o[nt][3] = 0.f;
+  float m0 = -INFINITY, m1 = -INFINITY, l0 = 0.f, l1 = 0.f;
+  const float sl2 = a.scale_log2;
+  const int mi = lane >> 3;
+  const int ltok = ((mi >> 1) << 3) + (lane & 7);
+  const int lcsel = mi & 1;
+  const int qp0 = T.z + gq, qp1 = T.z + gq + 8;  // positions of this lane's two rows
+
+  for (int i = 0; i < np; ++i) {
+    const int s = i % C::STAGES;
+    mbar_wait(&full[s], (uint32_t)((i / C::STAGES) & 1));
+    const uint32_t kbase = smem_u32(smem + s * C::BLOCK);
+    const uint32_t vbase = kbase + SW::MAT_BYTES;
+    // ---- S (16 positions x 16 keys) = Q K^T
+    float s0[4] = {0.f, 0.f, 0.f, 0.f}, s1[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int ks = 0; ks < HD / 16; ++ks) {
+      uint32_t b0, b1, b2, b3;
+      ldmatrix_x4(b0, b1, b2, b3, kbase + SW::chunk_off(ltok, 2 * ks + lcsel));
+      const uint32_t bf0[2] = {b0, b1}, bf1[2] = {b2, b3};
+      mma_bf16_16816(s0, qa[ks], bf0);
+      mma_bf16_16816(s1, qa[ks], bf1);
+    }
+    // ---- causal mask (diagonal page) + online softmax; row gq: s*[0..1], row gq+8: s*[2..3]
+    const int k0 = i * 16 + 2 * qq;
+    float x[8] = {s0[0] * sl2, s0[1] * sl2, s1[0] * sl2, s1[1] * sl2,
+                  s0[2] * sl2, s0[3] * sl2, s1[2] * sl2, s1[3] * sl2};
+    if (i == np - 1) {
+      const int kk[4] = {k0, k0 + 1, k0 + 8, k0 + 9};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        if (kk[j] > qp0) x[j] = -INFINITY;
+        if (kk[j] > qp1) x[4 + j] = -INFINITY;
+      }
+    }
+    float mp0 = fmaxf(fmaxf(x[0], x[1]), fmaxf(x[2], x[3]));
+    float mp1 = fmaxf(fmaxf(x[4], x[5]), fmaxf(x[6], x[7]));
+    mp0 = fmaxf(mp0, __shfl_xor_sync(0xffffffffu, mp0, 1));
+    mp0 = fmaxf(mp0, __shfl_xor_sync(0xffffffffu, mp0, 2));
+    mp1 = fmaxf(mp1, __shfl_xor_sync(0xffffffffu, mp1, 1));
+    mp1 = fmaxf(mp1, __shfl_xor_sync(0xffffffffu, mp1, 2));
+    const float mn0 = fmaxf(m0, mp0), mn1 = fmaxf(m1, mp1);
+    const float c0 = exp2f(m0 - mn0), c1 = exp2f(m1 - mn1);
+    float pr[8];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      pr[j] = exp2f(x[j] - mn0);
+      pr[4 + j] = exp2f(x[4 + j] - mn1);
+    }
+    l0 = l0 * c0 + ((pr[0] + pr[1]) + (pr[2] + pr[3]));
+    l1 = l1 * c1 + ((pr[4] + pr[5]) + (pr[6] + pr[7]));
+    m0 = mn0;
+    m1 = mn1;
+    // P as the A operand: (row gq | gq+8) x (keys 2qq.. | 8+2qq..)
+    const uint32_t pa[4] = {pack_bf16x2(pr[0], pr[1]), pack_bf16x2(pr[4], pr[5]), pack_bf16x2(pr[2], pr[3]),
+                            pack_bf16x2(pr[6], pr[7])};
+    // ---- O (16 x hd) += P V
+#pragma unroll
+    for (int n2 = 0; n2 < HD / 16; ++n2) {
+      uint32_t v0, v1, v2, v3;
+      ldmatrix_x4_trans(v0, v1, v2, v3, vbase + SW::chunk_off(ltok, 2 * n2 + lcsel));
+      const uint32_t blo[2] = {v0, v2}, bhi[2] = {v1, v3};
+      o[2 * n2][0] *= c0;
+      o[2 * n2][1] *= c0;
+      o[2 * n2][2] *= c1;
+      o[2 * n2][3] *= c1;
+      o[2 * n2 + 1][0] *= c0;
+      o[2 * n2 + 1][1] *= c0;
+      o[2 * n2 + 1][2] *= c1;
+      o[2 * n2 + 1][3] *= c1;
+      mma_bf16_16816(o[2 * n2], pa, blo);
+      mma_bf16_16816(o[2 * n2 + 1], pa, bhi);
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+    // refill stage s with page i + STAGES once every warp released it
+    if (threadIdx.x == 0 && i + C::STAGES < np) {
+      mbar_wait(&empty[s], (uint32_t)((i / C::STAGES) & 1));
+      fence_proxy_async();
+      mbar_arrive_expect_tx(&full[s], C::BLOCK);
+      bulk_g2s(smem + s * C::BLOCK, pool + (size_t)ptab[i + C::STAGES] * page_stride + head_off, C::BLOCK,
+               &full[s]);
+    }
+  }
+  // ---- normalise and store rows gq, gq + 8 (dims 8 nt + 2 qq, +1)
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
+  l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
+  l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+  const float i0 = 1.f / l0, i1 = 1.f / l1;
+#pragma unroll
+  for (int hf = 0; hf < 2; ++hf) {
+    const int row = rb + gq + 8 * hf;
+    if (row >= re || row < a.row0 || row >= a.row0 + a.n_rows) continue;
+    const float inv = hf ? i1 : i0;
+    bf16* orow = a.out + ((size_t)(row - a.row0) * a.nq + qh) * HD;
+    float* frow = a.out_f32 ? a.out_f32 + ((size_t)row * a.nq + qh) * HD : nullptr;
+#pragma unroll
+    for (int nt = 0; nt < HD / 8; ++nt) {
+      const int d = nt * 8 + 2 * qq;
+      const float v0 = o[nt][2 * hf] * inv, v1 = o[nt][2 * hf + 1] * inv;
+      const bf16 b0 = __float2bfloat16_rn(v0), b1 = __float2bfloat16_rn(v1);
+      *reinterpret_cast<uint32_t*>(orow + d) = pack_bf16x2(v0, v1);
+      if (frow) {
+        frow[d] = __bfloat162float(b0);
+        frow[d + 1] = __bfloat162float(b1);
+      }
+    }
+  }
+}
+
 int64_t attn_ws_floats(int n_rows, int nq, int hd, int max_chunks) {
   return (int64_t)n_rows * nq * max_chunks * (hd + 2);
 }
@@ -265,7 +455,7 @@ void attn_plan(int n_rows, int nkv, int max_seqlen, int* chunk_pages, int* max_c
   const int max_pages = (max_seqlen + 15) / 16;
   const long long base = (long long)n_rows * nkv;
   int best_c = 1;
-  if (base < 32) {
+  if (base > 0 && base < 32) {
     best_c = (int)((64 + base - 1) / base);
     if (best_c > 8) best_c = 8;
     while (best_c > 1 && max_pages / best_c < 2 * kAttnWarps) --best_c;
@@ -300,6 +490,27 @@ void launch_attention(const AttnArgs& a, cudaStream_t s) {
     case 128: launch_hd<128>(a, s); break;
     case 64: launch_hd<64>(a, s); break;
     case 32: launch_hd<32>(a, s); break;
+    default: break;
+  }
+}
+
+template <int HD>
+static void launch_prefill_hd(const PrefillArgs& a, cudaStream_t s) {
+  using C = PfCfg<HD>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_attn_prefill<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    attr = true;
+  }
+  launch_pdl(k_attn_prefill<HD>, dim3(a.n_tiles, a.nkv), dim3(32 * a.G), C::SMEM, s, a);
+}
+
+void launch_attention_prefill(const PrefillArgs& a, cudaStream_t s) {
+  if (a.n_tiles <= 0 || a.G < 1 || a.G > 8) return;
+  switch (a.hd) {
+    case 128: launch_prefill_hd<128>(a, s); break;
+    case 64: launch_prefill_hd<64>(a, s); break;
+    case 32: launch_prefill_hd<32>(a, s); break;
     default: break;
   }
 }

@@ -313,6 +313,9 @@ static rt_status create_impl(rt_engine* e, const rt_config* cfg) {
   CK(e, dalloc(e, &P.admitted, c.max_batch));
   CK(e, dalloc(e, &P.row_task, e->rows_cap));
   CK(e, dalloc(e, &P.row_pos, e->rows_cap));
+  CK(e, dalloc(e, &P.dec_rows, c.max_batch));
+  P.pf_tiles_cap = e->rows_cap / 16 + c.max_batch;
+  CK(e, dalloc(e, &P.pf_tiles, (size_t)P.pf_tiles_cap));
   CK(e, dalloc(e, &P.row_tok, e->rows_cap));
   CK(e, dalloc(e, &P.argmax_tok, c.max_batch));
   CK(e, dalloc(e, &P.slot_tok, c.max_batch));
@@ -643,6 +646,29 @@ static rt_status forward(rt_engine* e, const HostMailbox& plan) {
     aa.ws = e->d_attn_ws;
     aa.tickets = e->d_attn_tickets;
     aa.scale_log2 = sl2;
+    if (plan.n_prefill_rows > 0) {  // decode rows only (prompt rows: k_attn_prefill)
+      aa.row_list = P.dec_rows;
+      aa.chunk_rows = n;
+      aa.n_rows = plan.n_dec_rows;
+      attn_plan(plan.n_dec_rows, nkv, plan.max_seqlen, &aa.chunk_pages, &aa.max_chunks);
+      if (attn_ws_floats(n, nq, hd, aa.max_chunks) > e->attn_ws_cap) aa.max_chunks = 1;
+      if (aa.max_chunks == 1) aa.chunk_pages = e->pt_stride;
+    }
+    PrefillArgs pa{};
+    pa.q = e->d_q;
+    pa.page_table = e->tt.page_table;
+    pa.pt_stride = e->pt_stride;
+    pa.tiles = P.pf_tiles;
+    pa.n_tiles = plan.n_pf_tiles;
+    pa.row0 = row0;
+    pa.n_rows = n;
+    pa.nq = nq;
+    pa.nkv = nkv;
+    pa.hd = hd;
+    pa.G = nq / nkv;
+    pa.out = e->d_o;
+    pa.scale_log2 = sl2;
+    const bool any_decode = plan.n_rows > plan.n_prefill_rows;
     auto gemm = [&](const bf16* w, const GemmTmaSet& x, int M, int K, GemmArgs g) {
       g.M = M;
       g.N = n;
@@ -677,9 +703,17 @@ static rt_status forward(rt_engine* e, const HostMailbox& plan) {
       aa.pool = pool_l;
       aa.out_f32 = (e->d_cap_o && l == c.capture_layer) ? e->d_cap_o : nullptr;
       if (timing && row0 == 0) record_timing_event(e->ev_attn[2 * l], s);
-      launch_attention(aa, s);
-      ++launches;
+      if (any_decode) {
+        launch_attention(aa, s);
+        ++launches;
+      }
       if (timing && row0 == 0) record_timing_event(e->ev_attn[2 * l + 1], s);
+      if (pa.n_tiles > 0) {  // prompt rows of k = 0 admissions
+        pa.pool = pool_l;
+        pa.out_f32 = aa.out_f32;
+        launch_attention_prefill(pa, s);
+        ++launches;
+      }
       {  // O projection + residual
         GemmArgs g{};
         g.mode = EPI_RESID;

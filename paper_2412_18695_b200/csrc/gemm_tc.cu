@@ -153,6 +153,47 @@ struct EpiSmem {
 #define EPI_MARK(i) \
   if (et == 0) sm.mark[i] = clock64()
 
+// Reductions of 4 columns across the 32 lanes at once (reduce-scatter: 6 shuffles instead
+// of 4 x 5): the result for column j = (lane >> 3) & 3 ends on lanes with lane & 7 == 0.
+__device__ __forceinline__ float warp_sum4(const float (&v)[4], int lane) {
+  const bool hi16 = lane & 16, hi8 = lane & 8;
+  float a0 = hi16 ? v[2] : v[0], a1 = hi16 ? v[3] : v[1];
+  const float b0 = hi16 ? v[0] : v[2], b1 = hi16 ? v[1] : v[3];
+  a0 += __shfl_xor_sync(0xffffffffu, b0, 16);
+  a1 += __shfl_xor_sync(0xffffffffu, b1, 16);
+  float c = hi8 ? a1 : a0;
+  const float d = hi8 ? a0 : a1;
+  c += __shfl_xor_sync(0xffffffffu, d, 8);
+  c += __shfl_xor_sync(0xffffffffu, c, 4);
+  c += __shfl_xor_sync(0xffffffffu, c, 2);
+  c += __shfl_xor_sync(0xffffffffu, c, 1);
+  return c;
+}
+__device__ __forceinline__ void amax_merge(float& bv, int& bi, float ov, int oi) {
+  if (ov > bv || (ov == bv && oi < bi)) {
+    bv = ov;
+    bi = oi;
+  }
+}
+// (max, lowest index on ties) of 4 columns, same lane mapping as warp_sum4
+__device__ __forceinline__ void warp_argmax4(const float (&v)[4], const int (&ix)[4], int lane, float& rv, int& ri) {
+  const bool hi16 = lane & 16, hi8 = lane & 8;
+  float a0 = hi16 ? v[2] : v[0], a1 = hi16 ? v[3] : v[1];
+  int i0 = hi16 ? ix[2] : ix[0], i1 = hi16 ? ix[3] : ix[1];
+  const float b0 = hi16 ? v[0] : v[2], b1 = hi16 ? v[1] : v[3];
+  const int j0 = hi16 ? ix[0] : ix[2], j1 = hi16 ? ix[1] : ix[3];
+  amax_merge(a0, i0, __shfl_xor_sync(0xffffffffu, b0, 16), __shfl_xor_sync(0xffffffffu, j0, 16));
+  amax_merge(a1, i1, __shfl_xor_sync(0xffffffffu, b1, 16), __shfl_xor_sync(0xffffffffu, j1, 16));
+  rv = hi8 ? a1 : a0;
+  ri = hi8 ? i1 : i0;
+  const float d = hi8 ? a0 : a1;
+  const int di = hi8 ? i0 : i1;
+  amax_merge(rv, ri, __shfl_xor_sync(0xffffffffu, d, 8), __shfl_xor_sync(0xffffffffu, di, 8));
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1)
+    amax_merge(rv, ri, __shfl_xor_sync(0xffffffffu, rv, o), __shfl_xor_sync(0xffffffffu, ri, o));
+}
+
 // Where the finished tile's value (column c, row r) comes from: this CTA's parked partial
 // P [BN][128] (S = 1), or the S split-K partials summed in fixed rank order from the local
 // receive slots (push) or from the peers' P over DSMEM (pull).
@@ -205,8 +246,40 @@ __device__ __forceinline__ void epilogue(const GemmArgs& g, const EpiSmem& sm, c
   // rows are laid out pairwise, tiled_logical_row in model.cu) with one shuffle.
   bool active = m < g.M;
   if constexpr (MODE == EPI_SWIGLU) active = m_tile * 64 + (et >> 1) < g.ff;
+  // global inputs of a 4-column chunk (EPI_RESID: residual x; EPI_QKV: cos / sin of the
+  // rotation), software-pipelined one chunk ahead so a long column loop (prefill rows)
+  // does not pay a memory round trip per chunk
+  const int qi = (MODE == EPI_QKV) ? (et % g.qkv.hd) >> 1 : 0;
+  const bool qrope = (MODE == EPI_QKV) && (m / g.qkv.hd) < g.qkv.nq + g.qkv.nkv;
+  auto load_in = [&](int c, float (&ia)[4], float (&ib)[4]) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      ia[k] = 0.f;
+      ib[k] = 0.f;
+      if (!active || c + k >= NL) continue;
+      if constexpr (MODE == EPI_RESID) {
+        ia[k] = pre ? sm.xp[(c - cb + k) * 128 + et] : g.x[(size_t)(n0 + c + k) * g.M + m];
+      } else if constexpr (MODE == EPI_QKV) {
+        if (qrope) {
+          const int half = g.qkv.hd >> 1, pos = sm.pos[c + k];
+          ia[k] = pre ? sm.xp[(c - cb + k) * 64 + qi] : g.qkv.cos[(size_t)pos * half + qi];
+          ib[k] = pre ? sm.xp[1024 + (c - cb + k) * 64 + qi] : g.qkv.sin[(size_t)pos * half + qi];
+        }
+      }
+    }
+  };
+  float in_a[4], in_b[4];
+  load_in(cb, in_a, in_b);
 #pragma unroll 1
   for (int c0 = cb; c0 < ce; c0 += 4) {
+    float ca[4], cbv[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      ca[k] = in_a[k];
+      cbv[k] = in_b[k];
+    }
+    if (MODE == EPI_RESID || MODE == EPI_QKV)
+      if (c0 + 4 < ce) load_in(c0 + 4, in_a, in_b);
     float v[4], u[4];
     tile_vals4(ts, c0, et, v);
     if (g.rs_ss)
@@ -221,11 +294,8 @@ __device__ __forceinline__ void epilogue(const GemmArgs& g, const EpiSmem& sm, c
         for (int k = 0; k < 4; ++k)
           if (c0 + k < NL) g.out[(size_t)(n0 + c0 + k) * g.M + m] = v[k];
     } else if constexpr (MODE == EPI_RESID) {
-      float xv[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-        xv[k] = (active && c0 + k < NL) ? (pre ? sm.xp[(c0 - cb + k) * 128 + et] : g.x[(size_t)(n0 + c0 + k) * g.M + m])
-                                        : 0.f;
+      const float (&xv)[4] = ca;
+      float sq[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
         float xn = 0.f;
@@ -234,9 +304,10 @@ __device__ __forceinline__ void epilogue(const GemmArgs& g, const EpiSmem& sm, c
           g.x[(size_t)(n0 + c0 + k) * g.M + m] = xn;
           if (g.xb) g.xb[(size_t)(n0 + c0 + k) * g.M + m] = __float2bfloat16_rn(xn);
         }
-        const float sq = warp_sum(xn * xn);
-        if (lane == 0) sm.redv[wq * sm.bn + c0 + k] = sq;
+        sq[k] = xn * xn;
       }
+      const float t = warp_sum4(sq, lane);  // column c0 + ((lane >> 3) & 3) on lanes 8j
+      if ((lane & 7) == 0) sm.redv[wq * sm.bn + c0 + ((lane >> 3) & 3)] = t;
     } else if constexpr (MODE == EPI_SWIGLU) {
       // even lane: gate row, odd lane: up row of feature jf; the even lane writes columns
       // c0, c0 + 1 and the odd lane c0 + 2, c0 + 3
@@ -270,8 +341,7 @@ __device__ __forceinline__ void epilogue(const GemmArgs& g, const EpiSmem& sm, c
             const int pos = sm.pos[c];
             float y = v[k];
             if (rope) {
-              const float cs = pre ? sm.xp[(c - cb) * 64 + i] : q.cos[(size_t)pos * half + i];
-              const float sn = pre ? sm.xp[1024 + (c - cb) * 64 + i] : q.sin[(size_t)pos * half + i];
+              const float cs = ca[k], sn = cbv[k];
               y = odd ? v[k] * cs + u[k] * sn : v[k] * cs - u[k] * sn;
             }
             const bf16 b = __float2bfloat16_rn(y);
@@ -291,25 +361,21 @@ __device__ __forceinline__ void epilogue(const GemmArgs& g, const EpiSmem& sm, c
           }
         }
     } else if constexpr (MODE == EPI_ARGMAX) {
+      float bv[4];
+      int bi[4];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {  // greedy: max over the tile's rows, lowest index on ties
         const bool ok = active && c0 + k < NL;
         if (ok && g.out) g.out[(size_t)(n0 + c0 + k) * g.M + m] = v[k];
-        float bv = ok ? v[k] : -INFINITY;
-        int bi = ok ? m : INT_MAX;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) {
-          const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
-          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-          if (ov > bv || (ov == bv && oi < bi)) {
-            bv = ov;
-            bi = oi;
-          }
-        }
-        if (lane == 0) {
-          sm.redv[wq * sm.bn + c0 + k] = bv;
-          sm.redi[wq * sm.bn + c0 + k] = bi;
-        }
+        bv[k] = ok ? v[k] : -INFINITY;
+        bi[k] = ok ? m : INT_MAX;
+      }
+      float rv;
+      int ri;
+      warp_argmax4(bv, bi, lane, rv, ri);  // column c0 + ((lane >> 3) & 3) on lanes 8j
+      if ((lane & 7) == 0) {
+        sm.redv[wq * sm.bn + c0 + ((lane >> 3) & 3)] = rv;
+        sm.redi[wq * sm.bn + c0 + ((lane >> 3) & 3)] = ri;
       }
     }
   }

@@ -54,6 +54,8 @@ struct HostMailbox {
   int64_t seg_written;
   int64_t round_seq;
   int64_t attn_tokens;   // sum over rows of attended positions (algorithmic attention bytes)
+  int32_t n_pf_tiles;    // prefill attention tiles of this round (SchedParams::pf_tiles)
+  int32_t n_dec_rows;    // decode rows of this round (SchedParams::dec_rows)
 };
 
 struct SegRec {  // identical layout to rt_segment
@@ -78,6 +80,10 @@ struct SchedParams {
   int32_t* admitted;         // [max_batch]   admitted task slots (this round, in order)
   int32_t* row_task;         // [rows_cap]
   int32_t* row_pos;          // [rows_cap]
+  int32_t* dec_rows;         // [max_batch]   forward rows of the decode slots (slot order)
+  int4* pf_tiles;            // [pf_tiles_cap] prefill attention tiles: (first row, rows <= 16,
+                             //                first position (multiple of 16), task slot)
+  int32_t pf_tiles_cap;
   int32_t* row_tok;          // [rows_cap]
   int32_t* argmax_tok;       // [max_batch]   lm_head argmax per slot
   int32_t* slot_tok;         // [max_batch]   selected token per slot (log)

@@ -47,10 +47,31 @@ struct AttnArgs {
   float* ws;                // split-KV partials [rows][nq][max_chunks][hd + 2]
   int* tickets;             // [rows][nkv] zero-initialised, self-resetting (split-KV merge)
   float scale_log2;
+  const int32_t* row_list;   // nullable: CTA z serves row row_list[z] (global row; rows
+                             // outside [row0, row0 + chunk_rows) are skipped); n_rows = list size
+  int chunk_rows;
 };
 int64_t attn_ws_floats(int n_rows, int nq, int hd, int max_chunks);
 void attn_plan(int n_rows, int nkv, int max_seqlen, int* chunk_pages, int* max_chunks);
 void launch_attention(const AttnArgs& a, cudaStream_t s);
+
+// ---- causal prefill attention over paged KV (attn.cu): prompt rows of k = 0 admissions,
+// tiles of <= 16 consecutive positions; CTA = (tile, kv head), one warp per q head of the
+// GQA group, K/V page blocks shared by the warps through a TMA-fed ring
+struct PrefillArgs {
+  const bf16* q;            // [n_rows][nq][hd] rows of this forward chunk
+  const void* pool;         // this layer's pool
+  const int32_t* page_table;
+  int pt_stride;
+  const int4* tiles;        // (first row, rows, first position, task)
+  int n_tiles;
+  int row0, n_rows;         // forward chunk: rows outside it are skipped
+  int nq, nkv, hd, G;
+  bf16* out;                // [n_rows][nq][hd]
+  float* out_f32;           // nullable, indexed by global row
+  float scale_log2;
+};
+void launch_attention_prefill(const PrefillArgs& a, cudaStream_t s);
 
 // ---- tcgen05 GEMM with fused epilogues (gemm_tc.cu)
 struct TmaMap {

@@ -184,7 +184,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
   __shared__ unsigned long long s_min_arr;
   __shared__ int wbuf[32];
   __shared__ unsigned long long s_sum_ctx, s_sum_prompt, s_attn_tok;
-  __shared__ int s_max_seqlen;
+  __shared__ int s_max_seqlen, s_ndec;
 
   TaskTable T = p.tt;
   DevState* st = p.st;
@@ -258,6 +258,8 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
         mb->B = 0;
         mb->n_rows = 0;
         mb->n_prefill_rows = 0;
+        mb->n_pf_tiles = 0;
+        mb->n_dec_rows = 0;
         mb->max_seqlen = 0;
         mb->n_admitted = 0;
         mb->n_waiting = 0;
@@ -504,7 +506,9 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
       atomicMax(&s_max_seqlen, c + 1);
     }
   }
-  // prefill rows filled slot by slot, all threads in parallel
+  // prefill rows filled slot by slot, all threads in parallel; the prompt is cut into
+  // 16-position attention tiles (page-aligned: the prompt starts at position 0)
+  int n_pf_tiles = 0;
   for (int s = n_run; s < B; ++s) {
     if (!p.slot_is_prefill[s]) continue;
     const int task = p.slot_task[s];
@@ -516,7 +520,21 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
       p.row_pos[off + j] = j;
       p.row_tok[off + j] = pr[j];
     }
+    const int nt16 = (P + 15) >> 4;
+    for (int t16 = tid; t16 < nt16; t16 += nt)
+      if (n_pf_tiles + t16 < p.pf_tiles_cap)
+        p.pf_tiles[n_pf_tiles + t16] = make_int4(off + 16 * t16, min(16, P - 16 * t16), 16 * t16, task);
+    n_pf_tiles += nt16;
     n_prefill_rows += P;
+  }
+  // rows of the decode slots (running slots, then k > 0 resumes in admission order): the
+  // decode attention grid of rounds that also carry prompt rows
+  for (int s = tid; s < n_run; s += nt) p.dec_rows[s] = S.cnt_a[s];
+  if (tid == 0) {
+    int k = n_run;
+    for (int s = n_run; s < B; ++s)
+      if (!p.slot_is_prefill[s]) p.dec_rows[k++] = S.cnt_a[s];
+    s_ndec = k;
   }
   __syncthreads();
 
@@ -553,6 +571,8 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
     mb->B = B;
     mb->n_rows = n_rows;
     mb->n_prefill_rows = n_prefill_rows;
+    mb->n_pf_tiles = min(n_pf_tiles, p.pf_tiles_cap);
+    mb->n_dec_rows = s_ndec;
     mb->max_seqlen = s_max_seqlen;
     mb->n_admitted = nadm;
     mb->n_waiting = n;
