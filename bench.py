@@ -31,10 +31,11 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 from synth import MODEL_SHAPES, make_vocab, engine_params  # noqa: E402
-from synth.traces import make_trace, TRACE_CLASSES  # noqa: E402
+from synth.traces import make_trace, system_prefix, TRACE_CLASSES  # noqa: E402
 
 AGENTS_PER_GPU = 64
 PROMPT = 1300            # drone prompt (170.35 MB / 128 KiB per token)
+PREFIX = 1216            # its fixed, server-stored part (DESIGN R-PFX): 76 pages
 MAX_CTX = 2048
 TRACE_POOL = list(range(1, 9))   # drone traces 1-8 (tab:task_list)
 
@@ -130,10 +131,10 @@ class ClockSampler:
 
 
 # ------------------------------------------------------------------ workload
-def drone_request(vocab, agent, ordinal, seed, plan_len=None):
+def drone_request(vocab, agent, ordinal, seed, plan_len=None, prefix=None):
     tid = TRACE_POOL[(agent * 7 + ordinal * 3 + seed) % len(TRACE_POOL)]
     tr = make_trace(tid, vocab, seed=seed * 1000003 + agent * 9973 + ordinal, prompt_len=PROMPT,
-                    plan_len=plan_len)
+                    plan_len=plan_len, prefix=prefix)
     return tr
 
 
@@ -231,11 +232,22 @@ def run_ours(args, rank, world, dist):
                  "frac": step_bytes / (ms / K / 1e3) / 1e9 / pk["hbm_gbs"],
                  "attn_share_of_step": st["attn_ms"] / max(st["step_ms"], 1e-9)}
 
-    # ---- e2e: closed loop through the C ABI with host buffers (paper plans: 20-token drone)
-    e2e = run_e2e(args, eng, vocab, p, rank, world, now, dist, reqs)
+    # ---- e2e: closed loop through the C ABI with host buffers (paper plans: 20-token drone).
+    # (A) every prompt private (1300 tokens prefilled per request); then drain; (B) the drone's
+    # fixed prompt part registered once as a shared prefix, requests prefill
+    # only their 84-token task part.  B is the headline `e2e` (the paper's server stores the
+    # fixed prompt components), A is reported beside it.
+    launches_per_step = st["kernel_launches"] / max(st["rounds"], 1) + 2   # forward + sched pre/post
+    e2e_private = run_e2e(args, eng, vocab, p, rank, world, now, dist, reqs, prefix=None)
+    e2e_private.pop("_segments")
+    drain(eng, now)
+    pfx = system_prefix(vocab, "drone", PREFIX, seed=args.seed)
+    eng.register_prefix(pfx)
+    e2e = run_e2e(args, eng, vocab, p, rank, world, now, dist, reqs, prefix=pfx,
+                  start_agents=[rank + world * j for j in range(B)])
+    e2e["shared_prefix_tokens"] = PREFIX
     util = M.report(e2e.pop("_segments"), reqs, vocab, net_us=p.net_us, seed=args.seed)
 
-    launches_per_step = (1 + 1 + shape.n_layers * 9 + 1 + 2 + 1)
     out = None
     if rank == 0:
         cpu = cpu_baseline_sample(args) if world == 1 and not args.no_cpu else None
@@ -249,7 +261,8 @@ def run_ours(args, rank, world, dist):
                        "parallelism": f"replicas x{world} (agent partition, 1 allgather/round)",
                        "l2": "inputs > L2 (16 GB weights + 11 GB KV per step)"},
             "segments_per_s": seg_per_s, "roofline": roofline, "step_roofline": step_roof,
-            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches_per_step * K,
+            "cpu_baseline": cpu, "e2e": e2e, "e2e_private_prompts": e2e_private,
+            "gpu_launches": int(round(launches_per_step * K)),
             "clocks": clk.summary(), "time_utility": util,
             "breakdown_ms_per_step": {"attention": st["attn_ms"] / K, "scheduler": st["sched_ms"] / K,
                                       "forward": st["gemm_ms"] / K, "device_step": st["step_ms"] / K},
@@ -258,33 +271,47 @@ def run_ours(args, rank, world, dist):
     return out
 
 
-def run_e2e(args, eng, vocab, p, rank, world, now, dist, reqs):
-    """Closed loop (SURVEY §8d saturation mode): finished agents resubmit at once."""
+def drain(eng, now, max_rounds=2000):
+    """Run (untimed) until nothing is running or waiting, without resubmitting."""
+    for _ in range(max_rounds):
+        info = eng.step(now())
+        if info["n_running"] == 0 and info["n_waiting"] == 0:
+            break
+    eng.poll()
+    eng.sync()
+
+
+def run_e2e(args, eng, vocab, p, rank, world, now, dist, reqs, prefix=None, start_agents=()):
+    """Closed loop (SURVEY §8d saturation mode): finished agents resubmit at once;
+    `start_agents` (idle agents) submit at the start of the timed region."""
     import torch
     K = args.steps
     seg_all = []
     ordinal = {}
     h2d = d2h = 0
     tok = 0
-    # switch the resident long plans to the paper's drone plans for new requests
     eng.sync()
     if dist:
         dist.barrier()
+
+    def submit(agent):
+        o = ordinal[agent] = ordinal.get(agent, 0) + 1
+        tr = drone_request(vocab, agent, o, args.seed, prefix=prefix)
+        arr = now()
+        rid = eng.submit(agent, tr.prompt, arr, tr.ert_us, tr.alpha, tr.beta, p.g_us, script=tr.plan)
+        reqs[rid] = dict(arrival_us=arr, beta=tr.beta, alpha=tr.alpha, ert_us=tr.ert_us, cls=tr.cls, agent=agent)
+        return 4 * (len(tr.prompt) + len(tr.plan)) + 64
+
     t_start = time.perf_counter()
+    for agent in start_agents:
+        h2d += submit(agent)
     for _ in range(K):
         segs = eng.poll()
         d2h += 112 * len(segs) + 64
         seg_all += segs
         for s in segs:
             if s["reason"] in (1, 2):
-                agent = s["agent_id"]
-                o = ordinal[agent] = ordinal.get(agent, 0) + 1
-                tr = drone_request(vocab, agent, o, args.seed)
-                arr = now()
-                rid = eng.submit(agent, tr.prompt, arr, tr.ert_us, tr.alpha, tr.beta, p.g_us, script=tr.plan)
-                reqs[rid] = dict(arrival_us=arr, beta=tr.beta, alpha=tr.alpha, ert_us=tr.ert_us, cls=tr.cls,
-                                 agent=agent)
-                h2d += 4 * (len(tr.prompt) + len(tr.plan)) + 64
+                h2d += submit(s["agent_id"])
         info = eng.step(now())
         tok += info["n_running"]
     segs = eng.poll()

@@ -140,6 +140,18 @@ rt_status rt_submit_request(rt_engine* e, int32_t agent_id, const int32_t* promp
                             int32_t exec_window_us, int32_t max_new_tokens,
                             const int32_t* script, int32_t n_script, int64_t* request_id_out);
 
+/* Register a shared prompt prefix ("fixed prompt components
+ * ... pre-stored on the server"; DESIGN.md R-PFX).  tokens[n_tokens], n_tokens a positive
+ * multiple of page_tokens (16) below max_ctx.  Pops n_tokens/16 pages from the free stack
+ * (the order an admission pops them), computes their KV once (a forward over the prefix
+ * rows, no logits) and keeps them for the engine's lifetime, read-only.  Every later
+ * rt_submit_request whose prompt starts with a registered prefix and is longer than it (the
+ * longest such prefix) shares those pages: its reservation, page pops and prefill cover only
+ * the rest of the prompt, and finishing frees only its own pages.  Synchronises.  Errors:
+ * RT_E_INVAL (length / token ids), RT_E_NOMEM (more than 8 prefixes, or fewer than
+ * n_tokens/16 pages free after the outstanding reservations). */
+rt_status rt_register_prefix(rt_engine* e, const int32_t* tokens, int32_t n_tokens, int32_t* prefix_id_out);
+
 /* One scheduling round + one decoding iteration (DESIGN.md R-ROUND).  now_us is
  * the round start in WALL mode and ignored in VIRTUAL mode.  info (nullable)
  * receives the round summary available at return (t_us, n_waiting, n_running,

@@ -80,6 +80,7 @@ class OracleEngine:
         self.last_nonempty = False
         self.segments = []
         self.round_log = []
+        self.prefixes = []  # registered shared prefixes: dict(tokens, pages) (reading R-PFX)
 
     # ------------------------------------------------------------------ API
     def submit(self, agent_id, prompt, arrival_us, ert_us, alpha, beta, exec_window_us,
@@ -100,7 +101,8 @@ class OracleEngine:
         if max_new_tokens < 1 or len(prompt) + max_new_tokens > p.max_ctx:
             raise OracleError("INVAL", "context too long")
         R = ceil_div(len(prompt) + max_new_tokens, p.page_tokens)
-        if R > p.n_pages:
+        pfx, npfx = self._match_prefix(prompt)
+        if R - npfx > p.n_pages:
             raise OracleError("NOMEM", "request larger than pool")
         live = sum(1 for r in self.reqs.values() if not r.polled_final)
         if live >= p.max_tasks:
@@ -113,8 +115,39 @@ class OracleEngine:
             prompt=prompt, script=script, max_new=int(max_new_tokens), state=PENDING,
             k=0, D=int(arrival_us) + int(ert_us), ref=int(arrival_us), end_est=None,
             n_gen=0, seg_tok=0, seg_exec=0, seg_nsk=0, pending=None, ctx=0, pages=[],
-            R=R, holder=False, out=[], polled_final=False, argmax=[])
+            R=R, holder=False, out=[], polled_final=False, argmax=[], pfx=pfx, npfx=npfx)
         return rid
+
+    def register_prefix(self, tokens):
+        """Shared prompt prefix (PAPER.md:211 fixed prompt components stored
+        on the server; DESIGN R-PFX): len a positive multiple of page_tokens below max_ctx.
+        Pops len/16 pages now (admission pop order), keeps them read-only forever, and
+        computes their KV once."""
+        p = self.p
+        tokens = [int(x) for x in tokens]
+        n = len(tokens) // p.page_tokens
+        if (len(tokens) < p.page_tokens or len(tokens) % p.page_tokens or len(tokens) >= p.max_ctx
+                or any(t < 0 or t >= self.vocab for t in tokens)):
+            raise OracleError("INVAL", "bad prefix")
+        if len(self.prefixes) >= 8:
+            raise OracleError("NOMEM", "too many prefixes")
+        if self._avail() < n:
+            raise OracleError("NOMEM", "not enough free pages for the prefix")
+        pages = [self.free.pop() for _ in range(n)]
+        pid = len(self.prefixes)
+        self.prefixes.append(dict(tokens=tokens, pages=pages))
+        if self.model is not None:
+            self.model.forward([(("pfx", pid), i, t) for i, t in enumerate(tokens)])
+        return pid
+
+    def _match_prefix(self, prompt):
+        """Longest registered prefix that is a proper head of the prompt -> (id, pages)."""
+        best, npfx = -1, 0
+        for i, pf in enumerate(self.prefixes):
+            lp = len(pf["tokens"])
+            if lp < len(prompt) and lp // self.p.page_tokens > npfx and prompt[:lp] == pf["tokens"]:
+                best, npfx = i, lp // self.p.page_tokens
+        return best, npfx
 
     def poll(self):
         out, self.segments = self.segments, []
@@ -197,12 +230,12 @@ class OracleEngine:
             if not gate_ok:
                 refused_wcet = 1
                 break
-            if c.k == 0:
-                if mem_blocked or avail < c.R:
+            if c.k == 0:  # own pages only: a shared prefix is already resident (R-PFX)
+                if mem_blocked or avail < c.R - c.npfx:
                     mem_blocked = True
                     refused_mem += 1
                     continue
-                avail -= c.R
+                avail -= c.R - c.npfx
             admitted.append(c)
 
         # ---- page allocation + batch assembly (c2, AMB-14)
@@ -213,7 +246,9 @@ class OracleEngine:
             if a.k == 0:
                 prefill.add(a.id)
                 a.holder = True
-                for _ in range(ceil_div(len(a.prompt), p.page_tokens)):
+                if a.pfx >= 0:
+                    a.pages = list(self.prefixes[a.pfx]["pages"])
+                for _ in range(ceil_div(len(a.prompt), p.page_tokens) - a.npfx):
                     pg = self.free.pop()
                     a.pages.append(pg)
                     popped.append((a.id, pg))
@@ -233,11 +268,14 @@ class OracleEngine:
         for rid in slots:
             r = self.reqs[rid]
             if rid in prefill:
-                for i, tok in enumerate(r.prompt):
-                    rows.append((rid, i, tok))
+                lp = r.npfx * p.page_tokens  # prefix positions are not recomputed (R-PFX)
+                if r.pfx >= 0 and self.model is not None:
+                    self.model.share_prefix(("pfx", r.pfx), rid, lp)
+                for i in range(lp, len(r.prompt)):
+                    rows.append((rid, i, r.prompt[i]))
                 last_row[rid] = len(rows) - 1
                 r.ctx = len(r.prompt)
-                sum_prompt += len(r.prompt)
+                sum_prompt += len(r.prompt) - lp
             else:
                 rows.append((rid, r.ctx, r.pending))
                 last_row[rid] = len(rows) - 1
@@ -315,7 +353,7 @@ class OracleEngine:
                 r.seg_tok = r.seg_exec = r.seg_nsk = 0
                 r.state = WAITING
         for r in sorted(finished, key=lambda r: r.id):
-            for pg in reversed(r.pages):
+            for pg in reversed(r.pages[r.npfx:]):  # own pages; the prefix's stay (R-PFX)
                 self.free.append(pg)
             r.pages = []
             r.holder = False

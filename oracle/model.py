@@ -125,6 +125,14 @@ class OracleModel:
     def drop(self, rid):
         self.cache.pop(rid, None)
 
+    def share_prefix(self, src, dst, n):
+        """Request dst starts with the n positions of registered prefix src: the keys and
+        values of a position depend only on the tokens up to it, so they are the prefix's."""
+        K, V = self._kv(src)
+        K2, V2 = self._kv(dst)
+        K2[:, :n] = K[:, :n]
+        V2[:, :n] = V[:, :n]
+
     # ---- forward over a set of rows --------------------------------------
     def forward(self, rows, capture=None):
         """rows: list of (req_id, pos, token).  Returns final-normed hidden (bf16

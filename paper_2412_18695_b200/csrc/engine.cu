@@ -111,6 +111,9 @@ struct rt_engine {
   int n_staged = 0, recs_cap = 0;
   int64_t toks_staged = 0, toks_cap = 0;
   std::vector<int> free_slots;
+  // registered shared prompt prefixes (rt_register_prefix): tokens (a multiple of 16) and
+  // their read-only pages = page-table row max_tasks + id
+  std::vector<std::vector<int32_t>> prefixes;
   std::unordered_map<int64_t, int> rid_slot;
   int64_t n_submitted = 0;
   int64_t seg_read = 0;
@@ -281,8 +284,8 @@ static rt_status create_impl(rt_engine* e, const rt_config* cfg) {
   A(alpha, MT); A(beta, MT); A(pri, MT);
   A(state, MT); A(agent, MT); A(k, MT); A(n_prompt, MT); A(max_new, MT); A(window, MT); A(scripted, MT);
   A(n_gen, MT); A(seg_tok, MT); A(n_skills, MT); A(pending, MT); A(ctx, MT); A(n_pages, MT); A(R, MT);
-  A(holder, MT); A(argmax_last, MT);
-  A(page_table, (size_t)MT * e->pt_stride);
+  A(holder, MT); A(argmax_last, MT); A(pfx, MT); A(n_pfx, MT);
+  A(page_table, (size_t)(MT + kMaxPrefixes) * e->pt_stride);
   A(prompt, (size_t)MT * c.max_ctx);
   A(script, (size_t)MT * c.max_ctx);
   A(out, (size_t)MT * c.max_ctx);
@@ -328,6 +331,7 @@ static rt_status create_impl(rt_engine* e, const rt_config* cfg) {
   CK(e, cudaMemcpy(d_skill, e->tok_skill.data(), c.vocab * 2, cudaMemcpyHostToDevice));
   CK(e, cudaMemcpy(d_exec, e->tok_exec.data(), c.vocab * 4, cudaMemcpyHostToDevice));
   P.tt = T;
+  P.pfx_pages = T.page_table + (size_t)MT * e->pt_stride;
   P.st = e->d_st;
   P.mb = e->d_mb;
   P.seg_ring = e->d_ring;
@@ -540,7 +544,17 @@ extern "C" rt_status rt_submit_request(rt_engine* e, int32_t agent_id, const int
   if (max_new_tokens < 1 || (int64_t)n_prompt + max_new_tokens > c.max_ctx)
     return fail(e, RT_E_INVAL, "n_prompt + max_new_tokens > max_ctx");
   const int R = (n_prompt + max_new_tokens + 15) / 16;
-  if (R > c.n_pages) return fail(e, RT_E_NOMEM, "request larger than the page pool");
+  // shared prefix: the longest registered prefix that is a proper head of the prompt
+  int pfx = -1, n_pfx = 0;
+  for (int i = 0; i < (int)e->prefixes.size(); ++i) {
+    const std::vector<int32_t>& pt = e->prefixes[i];
+    const int lp = (int)pt.size();
+    if (lp < n_prompt && lp / 16 > n_pfx && memcmp(pt.data(), prompt, 4 * (size_t)lp) == 0) {
+      pfx = i;
+      n_pfx = lp / 16;
+    }
+  }
+  if (R - n_pfx > c.n_pages) return fail(e, RT_E_NOMEM, "request larger than the page pool");
   if (e->free_slots.empty()) return fail(e, RT_E_NOMEM, "task table full");
   const int64_t need = (int64_t)n_prompt + (scripted ? n_script : 0);
   if (e->n_staged >= e->recs_cap || e->toks_staged + need > e->toks_cap) {
@@ -563,6 +577,8 @@ extern "C" rt_status rt_submit_request(rt_engine* e, int32_t agent_id, const int
   r.max_new = max_new_tokens;
   r.window = exec_window_us;
   r.scripted = scripted ? 1 : 0;
+  r.pfx = pfx;
+  r.n_pfx = n_pfx;
   r.tok_off = e->toks_staged;
   memcpy(e->h_toks + e->toks_staged, prompt, 4 * (size_t)n_prompt);
   e->toks_staged += n_prompt;
@@ -572,6 +588,75 @@ extern "C" rt_status rt_submit_request(rt_engine* e, int32_t agent_id, const int
   }
   e->rid_slot[r.rid] = slot;
   if (request_id_out) *request_id_out = r.rid;
+  return RT_OK;
+}
+
+static rt_status forward(rt_engine* e, const HostMailbox& plan);
+
+// ------------------------------------------------------------ shared prefixes
+// NEXT-1 (fixed prompt components pre-stored on the server): the prefix's pages are
+// popped from the free stack like an admission's and never freed; its KV is computed once by
+// a forward over its rows (B = 0: no logits).  Later submissions whose prompt starts with it
+// point their first page-table entries at these pages and prefill only the rest (DESIGN R-PFX).
+extern "C" rt_status rt_register_prefix(rt_engine* e, const int32_t* tokens, int32_t n_tokens,
+                                        int32_t* prefix_id_out) {
+  if (!e) return RT_E_INVAL;
+  if (e->sticky) return RT_E_CUDA;
+  const rt_config& c = e->cfg;
+  if (!tokens || n_tokens < 16 || n_tokens % 16 != 0 || n_tokens >= c.max_ctx)
+    return fail(e, RT_E_INVAL, "prefix length must be a positive multiple of 16 below max_ctx");
+  for (int i = 0; i < n_tokens; ++i)
+    if (tokens[i] < 0 || tokens[i] >= c.vocab) return fail(e, RT_E_INVAL, "prefix token out of range");
+  if ((int)e->prefixes.size() >= kMaxPrefixes) return fail(e, RT_E_NOMEM, "too many prefixes");
+  rt_status st = flush_staging(e);
+  if (st != RT_OK) return st;
+  st = rt_sync(e);
+  if (st != RT_OK) return st;
+  const int MT = c.max_tasks, n = n_tokens / 16, pid = (int)e->prefixes.size();
+  // pages available = free stack - outstanding reservations of admitted requests (AMB-26)
+  DevState ds;
+  CK(e, cudaMemcpy(&ds, e->d_st, sizeof(ds), cudaMemcpyDeviceToHost));
+  std::vector<int32_t> holder(MT), R(MT), np(MT);
+  CK(e, cudaMemcpy(holder.data(), e->tt.holder, 4 * MT, cudaMemcpyDeviceToHost));
+  CK(e, cudaMemcpy(R.data(), e->tt.R, 4 * MT, cudaMemcpyDeviceToHost));
+  CK(e, cudaMemcpy(np.data(), e->tt.n_pages, 4 * MT, cudaMemcpyDeviceToHost));
+  int64_t outstanding = 0;
+  for (int i = 0; i < MT; ++i)
+    if (holder[i]) outstanding += R[i] - np[i];
+  if (ds.free_top - outstanding < n) return fail(e, RT_E_NOMEM, "not enough free pages for the prefix");
+  // pop n pages in stack order (the same order an admission pops them)
+  std::vector<int32_t> top(n), pages(n);
+  CK(e, cudaMemcpy(top.data(), e->sp.free_stack + ds.free_top - n, 4 * (size_t)n, cudaMemcpyDeviceToHost));
+  for (int m = 0; m < n; ++m) pages[m] = top[n - 1 - m];
+  const int slot = MT + pid;  // the prefix's page-table row
+  CK(e, cudaMemcpy(e->tt.page_table + (size_t)slot * e->pt_stride, pages.data(), 4 * (size_t)n,
+                   cudaMemcpyHostToDevice));
+  const int32_t new_top = ds.free_top - n;
+  CK(e, cudaMemcpy(&e->d_st->free_top, &new_top, 4, cudaMemcpyHostToDevice));
+  if (!(c.flags & RT_FLAG_NO_MODEL)) {
+    // rows (slot, position, token) and 16-position tiles of the prefix, then the forward
+    if (n_tokens > e->rows_cap) return fail(e, RT_E_INVAL, "prefix longer than the forward row capacity");
+    std::vector<int32_t> rt(n_tokens, slot), rp(n_tokens);
+    for (int j = 0; j < n_tokens; ++j) rp[j] = j;
+    std::vector<int4> tiles(n);
+    for (int t = 0; t < n; ++t) tiles[t] = make_int4(16 * t, 16, 16 * t, slot);
+    CK(e, cudaMemcpy(e->sp.row_task, rt.data(), 4 * (size_t)n_tokens, cudaMemcpyHostToDevice));
+    CK(e, cudaMemcpy(e->sp.row_pos, rp.data(), 4 * (size_t)n_tokens, cudaMemcpyHostToDevice));
+    CK(e, cudaMemcpy(e->sp.row_tok, tokens, 4 * (size_t)n_tokens, cudaMemcpyHostToDevice));
+    CK(e, cudaMemcpy(e->sp.pf_tiles, tiles.data(), sizeof(int4) * (size_t)n, cudaMemcpyHostToDevice));
+    HostMailbox plan{};
+    plan.B = 0;
+    plan.n_rows = n_tokens;
+    plan.n_prefill_rows = n_tokens;
+    plan.n_pf_tiles = n;
+    plan.n_dec_rows = 0;
+    plan.max_seqlen = n_tokens;
+    st = forward(e, plan);
+    if (st != RT_OK) return st;
+    CK(e, cudaStreamSynchronize(e->stream));
+  }
+  e->prefixes.emplace_back(tokens, tokens + n_tokens);
+  if (prefix_id_out) *prefix_id_out = pid;
   return RT_OK;
 }
 
@@ -747,10 +832,12 @@ static rt_status forward(rt_engine* e, const HostMailbox& plan) {
       }
     }
     // logits rows: final RMSNorm applied while gathering them
-    launch_gather_norm(P.slot_row, B, row0, n, e->d_x, e->d_ss, d, e->d_hfin, s);
-    ++launches;
+    if (B > 0) {
+      launch_gather_norm(P.slot_row, B, row0, n, e->d_x, e->d_ss, d, e->d_hfin, s);
+      ++launches;
+    }
   }
-  {  // lm_head + greedy argmax (a8)
+  if (B > 0) {  // lm_head + greedy argmax (a8); B = 0: prefix registration (KV only)
     GemmArgs g{};
     g.mode = EPI_ARGMAX;
     g.M = V;

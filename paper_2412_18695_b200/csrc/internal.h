@@ -10,6 +10,7 @@ enum TaskState : int32_t { T_FREE = -1, T_PENDING = 0, T_WAITING = 1, T_RUNNING 
 constexpr int kMaxSegTok = 16;
 constexpr int kMaxTasks = 2048;
 constexpr int kSchedThreads = 1024;
+constexpr int kMaxPrefixes = 8;    // registered shared prompt prefixes (NEXT-1)
 constexpr int kTopK = 16;          // per-rank candidates exchanged per round (a12)
 
 // Submission record staged in pinned host memory, applied on device at the next step.
@@ -17,6 +18,7 @@ struct SubmitRec {
   int64_t rid, arrival, ert;
   double alpha, beta;
   int32_t slot, agent, n_prompt, max_new, window, scripted;
+  int32_t pfx, n_pfx;  // shared prefix id (-1 none) and its page count
   int64_t tok_off;  // offset of prompt (then script) tokens in the staging token pool
 };
 
@@ -26,7 +28,9 @@ struct TaskTable {
   double *alpha, *beta, *pri;
   int32_t *state, *agent, *k, *n_prompt, *max_new, *window, *scripted;
   int32_t *n_gen, *seg_tok, *n_skills, *pending, *ctx, *n_pages, *R, *holder, *argmax_last;
-  int32_t* page_table;   // [max_tasks][pt_stride]
+  int32_t *pfx, *n_pfx;  // shared prefix id (-1 none) and its page count (leading page-table
+                         // entries that are the prefix's read-only pages)
+  int32_t* page_table;   // [max_tasks + kMaxPrefixes][pt_stride] (prefix rows at the end)
   int32_t* prompt;       // [max_tasks][max_ctx]
   int32_t* script;       // [max_tasks][max_ctx]
   int32_t* out;          // [max_tasks][max_ctx]
@@ -91,6 +95,7 @@ struct SchedParams {
   const int16_t* tok_skill;
   const int32_t* tok_exec;
   double* cand;              // [kTopK][4] local top-K candidates (pri, arrival, rid, rank)
+  const int32_t* pfx_pages;  // [kMaxPrefixes][pt_stride] page ids of each registered prefix
   int32_t max_tasks, max_batch, max_ctx, pt_stride, n_pages, page_tokens, rows_cap;
   int32_t max_seg_tokens, g_us, net_us, eps_l_us, speed_window, max_admit, policy, clock_mode;
   int32_t base_us, gamma_ppm, kv_us_per_1k, prefill_us_per_tok;

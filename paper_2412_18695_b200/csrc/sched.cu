@@ -127,6 +127,8 @@ __global__ void k_apply_submits(SchedParams p, const SubmitRec* recs, const int3
     T.max_new[i] = r.max_new;
     T.window[i] = r.window;
     T.scripted[i] = r.scripted;
+    T.pfx[i] = r.pfx;
+    T.n_pfx[i] = r.n_pfx;
     T.n_gen[i] = 0;
     T.seg_tok[i] = 0;
     T.n_skills[i] = 0;
@@ -305,7 +307,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
     S.a3[pos] = a3;
     S.cslot[pos] = i;
     S.ck[pos] = k;
-    S.cR[pos] = T.R[i];
+    S.cR[pos] = T.R[i] - T.n_pfx[i];  // own pages (a shared prefix is already resident)
   }
   // outstanding reservations sum_active (R - held)  (AMB-26)
   int my_out = 0;
@@ -441,7 +443,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
     const int task = p.slot_task[s];
     p.round_slots[s] = task;
     if (p.slot_is_prefill[s]) {
-      S.cnt_a[s] = ceil_div_i(T.n_prompt[task], p.page_tokens);
+      S.cnt_a[s] = ceil_div_i(T.n_prompt[task], p.page_tokens) - T.n_pfx[task];
       S.cnt_b[s] = 0;
     } else {
       S.cnt_a[s] = 0;
@@ -457,10 +459,13 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
     int32_t* pt = T.page_table + (size_t)task * p.pt_stride;
     if (p.slot_is_prefill[s]) {
       const int npg = ceil_div_i(T.n_prompt[task], p.page_tokens);
-      for (int m = 0; m < npg; ++m) {
+      const int npf = T.n_pfx[task];
+      const int32_t* pp = p.pfx_pages + (size_t)max(T.pfx[task], 0) * p.pt_stride;
+      for (int m = 0; m < npf; ++m) pt[m] = pp[m];  // shared prefix pages, read-only
+      for (int m = 0; m < npg - npf; ++m) {
         const int q = S.cnt_a[s] + m;
         const int pg = p.free_stack[top - 1 - q];
-        pt[m] = pg;
+        pt[npf + m] = pg;
         p.popped[2 * q] = task;
         p.popped[2 * q + 1] = pg;
       }
@@ -479,7 +484,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
   // forward rows: prefill slot -> n_prompt rows, decode slot -> 1 row (AMB-13)
   for (int s = tid; s < B; s += nt) {
     const int task = p.slot_task[s];
-    S.cnt_a[s] = p.slot_is_prefill[s] ? T.n_prompt[task] : 1;
+    S.cnt_a[s] = p.slot_is_prefill[s] ? T.n_prompt[task] - p.page_tokens * T.n_pfx[task] : 1;
   }
   __syncthreads();
   const int n_rows = block_scan_excl(S.cnt_a, B, wbuf);
@@ -489,10 +494,11 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
     const int off = S.cnt_a[s];
     if (p.slot_is_prefill[s]) {
       const int P = T.n_prompt[task];
-      p.slot_row[s] = off + P - 1;
+      const int Lp = p.page_tokens * T.n_pfx[task];  // prefix positions are not recomputed
+      p.slot_row[s] = off + (P - Lp) - 1;
       T.ctx[task] = P;
-      atomicAdd(&s_sum_prompt, (unsigned long long)P);
-      atomicAdd(&s_attn_tok, (unsigned long long)P * (P + 1) / 2);
+      atomicAdd(&s_sum_prompt, (unsigned long long)(P - Lp));
+      atomicAdd(&s_attn_tok, (unsigned long long)P * (P + 1) / 2 - (unsigned long long)Lp * (Lp + 1) / 2);
       atomicMax(&s_max_seqlen, P);
     } else {
       const int c = T.ctx[task];
@@ -514,18 +520,20 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
     const int task = p.slot_task[s];
     const int off = S.cnt_a[s];
     const int P = T.n_prompt[task];
+    const int Lp = p.page_tokens * T.n_pfx[task];  // rows start after the shared prefix
     const int32_t* pr = T.prompt + (size_t)task * p.max_ctx;
-    for (int j = tid; j < P; j += nt) {
+    for (int j = tid; j < P - Lp; j += nt) {
       p.row_task[off + j] = task;
-      p.row_pos[off + j] = j;
-      p.row_tok[off + j] = pr[j];
+      p.row_pos[off + j] = Lp + j;
+      p.row_tok[off + j] = pr[Lp + j];
     }
-    const int nt16 = (P + 15) >> 4;
+    const int nt16 = (P - Lp + 15) >> 4;
     for (int t16 = tid; t16 < nt16; t16 += nt)
       if (n_pf_tiles + t16 < p.pf_tiles_cap)
-        p.pf_tiles[n_pf_tiles + t16] = make_int4(off + 16 * t16, min(16, P - 16 * t16), 16 * t16, task);
+        p.pf_tiles[n_pf_tiles + t16] =
+            make_int4(off + 16 * t16, min(16, P - Lp - 16 * t16), Lp + 16 * t16, task);
     n_pf_tiles += nt16;
-    n_prefill_rows += P;
+    n_prefill_rows += P - Lp;
   }
   // rows of the decode slots (running slots, then k > 0 resumes in admission order): the
   // decode attention grid of rounds that also carry prompt rows
@@ -714,15 +722,15 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_post(SchedParams p) 
     }
   }
   __syncthreads();
-  for (int f = tid; f < nfin; f += nt) S.fin_off[f] = T.n_pages[S.fin[f]];
+  for (int f = tid; f < nfin; f += nt) S.fin_off[f] = T.n_pages[S.fin[f]] - T.n_pfx[S.fin[f]];  // own pages
   __syncthreads();
   const int n_push = block_scan_excl(S.fin_off, nfin, wbuf);
   const int top = st->free_top;
   for (int f = tid; f < nfin; f += nt) {
     const int task = S.fin[f];
-    const int np = T.n_pages[task];
+    const int np = T.n_pages[task], npf = T.n_pfx[task];
     const int32_t* pt = T.page_table + (size_t)task * p.pt_stride;
-    for (int m = 0; m < np; ++m) p.free_stack[top + S.fin_off[f] + m] = pt[np - 1 - m];
+    for (int m = 0; m < np - npf; ++m) p.free_stack[top + S.fin_off[f] + m] = pt[np - 1 - m];
     T.n_pages[task] = 0;
   }
   __syncthreads();

@@ -27,7 +27,7 @@ TRACE_DTYPE = np.dtype([("grid", "<u8"), ("kind", "<u4"), ("smid", "<u4"), ("t_e
 TRACE_KINDS = {1: "gemm", 2: "attn", 3: "norm", 4: "embed", 5: "sched_pre", 6: "sched_post", 7: "gather",
                8: "argmax", 9: "merge", 10: "attn_prefill"}
 
-EXPORTED = ["rt_create", "rt_destroy", "rt_submit_request", "rt_step", "rt_poll_segment", "rt_last_round",
+EXPORTED = ["rt_create", "rt_destroy", "rt_submit_request", "rt_register_prefix", "rt_step", "rt_poll_segment", "rt_last_round",
             "rt_sync", "rt_get_stats", "rt_reset_stats", "rt_debug_dump", "rt_last_error", "rt_version",
             "rt_op_paged_attention", "rt_op_attention_ws_bytes", "rt_op_kv_write", "rt_op_kv_read",
             "rt_op_gemm", "rt_op_lm_argmax", "rt_op_init_weights", "rt_op_priority", "rt_mark", "rt_elapsed_ms",
@@ -96,6 +96,7 @@ def lib():
                                     rt_utility, C.c_int32, C.c_int32, C.c_void_p, C.c_int32,
                                     C.POINTER(C.c_int64)]
     L.rt_step.argtypes = [C.c_void_p, C.c_int64, C.POINTER(rt_round_info)]
+    L.rt_register_prefix.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.POINTER(C.c_int32)]
     L.rt_poll_segment.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.POINTER(C.c_int32)]
     L.rt_last_round.argtypes = [C.c_void_p, C.POINTER(rt_round_info)]
     L.rt_sync.argtypes = [C.c_void_p]
@@ -199,6 +200,13 @@ class Engine:
                                        sc.ctypes.data if sc is not None else None,
                                        len(sc) if sc is not None else 0, C.byref(rid)), self.h)
         return rid.value
+
+    def register_prefix(self, tokens):
+        """Shared read-only prompt prefix (len a multiple of 16); returns its id."""
+        t = _i32(tokens)
+        pid = C.c_int32()
+        _check(lib().rt_register_prefix(self.h, t.ctypes.data, len(t), C.byref(pid)), self.h)
+        return pid.value
 
     def step(self, now_us=0):
         info = rt_round_info()

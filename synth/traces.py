@@ -81,13 +81,28 @@ def make_plan(cls: str, trace_id: int, vocab: SkillVocab, rng, plan_len=None) ->
     return plan
 
 
-def make_trace(trace_id: int, vocab: SkillVocab, seed: int, prompt_len=None, plan_len=None) -> Trace:
-    """One scripted request of the given trace id; deterministic in ``seed``."""
+def system_prefix(vocab: SkillVocab, robot: str = "drone", n_tokens: int = 1216, seed: int = 0) -> np.ndarray:
+    """The fixed part of a robot's prompt — skill set, guidance and examples, which PAPER.md:211
+    says are pre-stored on the server — as seeded filler tokens; shared by every request of that
+    robot type (DESIGN reading R-PFX: 1216 of the drone's 1300 prompt tokens = 76 pages, the
+    last 84 are the task)."""
+    rng = np.random.Generator(np.random.PCG64([seed, 0x5E5, len(robot)]))
+    return _filler(vocab, rng, n_tokens)
+
+
+def make_trace(trace_id: int, vocab: SkillVocab, seed: int, prompt_len=None, plan_len=None,
+               prefix=None) -> Trace:
+    """One scripted request of the given trace id; deterministic in ``seed``.  ``prefix``
+    (optional): the prompt starts with these tokens and the rest is per-request filler."""
     cls = TRACE_CLASSES[trace_id]
     rng = np.random.Generator(np.random.PCG64([seed, trace_id]))
     spec = _CLASS[cls]
     pl = spec["prompt"] if prompt_len is None else int(prompt_len)
-    prompt = _filler(vocab, rng, pl)
+    if prefix is None:
+        prompt = _filler(vocab, rng, pl)
+    else:
+        prefix = np.asarray(prefix, dtype=np.int32)
+        prompt = np.concatenate([prefix, _filler(vocab, rng, pl - len(prefix))]).astype(np.int32)
     plan = make_plan(cls, trace_id, vocab, rng, plan_len)
     beta, alpha, ert = spec["tuf"]
     return Trace(trace_id, cls, prompt, plan, beta, alpha, ert)

@@ -404,3 +404,71 @@ def test_device_trace_records(rt):
     assert len(grids[5]) == 3 and len(grids[6]) == 3
     assert len(grids[2]) > 0 and len(grids[2]) % shape.n_layers == 0
     eng.close()
+
+
+# ------------------------------------------------------------- shared prefixes (NEXT-1)
+PFX = [7 + (i * 13) % 300 for i in range(48)]   # 3 pages
+
+
+@pytest.mark.parametrize("n_pages", [64, 24])
+def test_sched_parity_with_shared_prefix(rt, n_pages):
+    """Prefix pages popped at registration, shared read-only by every prefixed request,
+    reservations of own pages only: page tables, free stack and segments bit-exact."""
+    v = make_vocab(512)
+    p = engine_params("paper-4090", max_batch=4, max_tasks=64, max_ctx=256, n_pages=n_pages)
+    reqs = compose_workload(4, 1.0, 2, range(1, 9), 30.0, 4, v, prompt_len_range=(20, 64), max_requests=12)
+    eng, ora = make_pair(rt, v, p)
+    assert eng.register_prefix(PFX) == ora.register_prefix(PFX) == 0
+    for i, r in enumerate(reqs):   # two thirds of the requests carry the prefix
+        r.prompt = (PFX + list(r.prompt)) if i % 3 else list(r.prompt)
+    submit_both(eng, ora, reqs)
+    lockstep(eng, ora)
+    tabs = eng.dump(rt.RT_DUMP_PAGE_TABLES, np.int32)
+    assert sorted(list(eng.dump(rt.RT_DUMP_FREE_STACK, np.int32)) + ora.prefixes[0]["pages"]) == list(range(n_pages))
+
+
+def test_tiny_model_shared_prefix_parity(rt):
+    """Prefix KV computed once by the registration forward; prefixed requests prefill only
+    their own rows: logits and per-op attention vs the oracle."""
+    shape = MODEL_SHAPES["tiny"]
+    v = make_vocab(shape.vocab)
+    p = engine_params("paper-4090", max_batch=4, max_tasks=64, max_ctx=256, n_pages=64)
+    reqs = compose_workload(4, 1.0, 2, range(1, 9), 30.0, 6, v, prompt_len_range=(20, 40), max_requests=8)
+    flags = rt.RT_FLAG_KEEP_LOGITS | rt.RT_FLAG_CAPTURE
+    eng, ora = make_pair(rt, v, p, shape=shape, seed=3, flags=flags, model=True, capture_layer=1)
+    assert eng.register_prefix(PFX) == ora.register_prefix(PFX)
+    for r in reqs:
+        r.prompt = PFX + list(r.prompt)
+    submit_both(eng, ora, reqs)
+    worst_logit = worst_attn = 0.0
+    n_pf_rows = 0
+    for n in range(400):
+        ig, io = eng.step(), ora.step()
+        assert ig["n_running"] == io["n_running"]
+        if io["n_running"] == 0:
+            if all(r.state == FINISHED for r in ora.reqs.values()):
+                break
+            continue
+        n_pf_rows += ig["n_prefill_rows"]
+        B = io["n_running"]
+        lg = eng.dump(rt.RT_DUMP_LOGITS, np.float32).reshape(B, -1)
+        lo = np.stack([ora.round_log[-1]["logits"][rid] for rid in ora.round_log[-1]["slots"]])
+        worst_logit = max(worst_logit, float(np.abs(lg - lo).max()))
+        rows = eng.dump(rt.RT_DUMP_ROWS, np.int32).reshape(-1, 3)
+        q = eng.dump(rt.RT_DUMP_CAPTURE_Q, np.float32).reshape(len(rows), shape.n_q_heads, shape.head_dim)
+        o = eng.dump(rt.RT_DUMP_CAPTURE_O, np.float32).reshape(len(rows), shape.n_q_heads, shape.head_dim)
+        kv = eng.dump(rt.RT_DUMP_KV_LAYER, np.uint16).reshape(p.n_pages, 2, shape.n_kv_heads, 16, shape.head_dim)
+        kvf = (kv.astype(np.uint32) << 16).view(np.float32)
+        kp = kvf[:, 0].transpose(0, 2, 1, 3)
+        vp = kvf[:, 1].transpose(0, 2, 1, 3)
+        tabs = eng.dump(rt.RT_DUMP_PAGE_TABLES, np.int32).reshape(p.max_tasks, -1)
+        for i in range(0, len(rows), max(1, len(rows) // 16)):
+            task, pos, _ = rows[i]
+            assert pos >= 0
+            ref = paged_attention(q[i], kp, vp, tabs[task], pos + 1)
+            worst_attn = max(worst_attn, float(np.abs(o[i] - ref).max()))
+    # every prefill round computed only the rows after the 48 shared positions
+    assert n_pf_rows == sum(len(r.prompt) - 48 for r in reqs)
+    assert worst_attn < 6e-3, worst_attn
+    assert worst_logit < 1e-2, worst_logit
+    assert eng.poll() == ora.poll()
