@@ -71,6 +71,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32) k_attn(AttnArgs a) {
     for (int s = 0; s < C::STAGES; ++s) mbar_init(&bar[s], 1);
     fence_mbar_init();
   }
+  const uint64_t pol = a.l2_evict_first ? l2_policy_evict_first() : 0ull;
   __syncwarp();
   pdl_wait();  // q and the KV pages come from the QKV GEMM that precedes this kernel
   tr.ready();
@@ -81,7 +82,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32) k_attn(AttnArgs a) {
     const int pg = __shfl_sync(0xffffffffu, my_page, i);
     if (lane == 0 && i < n_my) {
       mbar_arrive_expect_tx(&bar[i], C::BLOCK);
-      bulk_g2s(ring + i * C::BLOCK, pool + (size_t)pg * page_stride + head_off, C::BLOCK, &bar[i]);
+      bulk_g2s_hint(ring + i * C::BLOCK, pool + (size_t)pg * page_stride + head_off, C::BLOCK, &bar[i], pol);
     }
   }
 
@@ -167,7 +168,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32) k_attn(AttnArgs a) {
       if (lane == 0) {
         fence_proxy_async();
         mbar_arrive_expect_tx(&bar[s], C::BLOCK);
-        bulk_g2s(ring + s * C::BLOCK, pool + (size_t)pg * page_stride + head_off, C::BLOCK, &bar[s]);
+        bulk_g2s_hint(ring + s * C::BLOCK, pool + (size_t)pg * page_stride + head_off, C::BLOCK, &bar[s], pol);
       }
     }
   }
@@ -484,8 +485,10 @@ static void launch_hd(const AttnArgs& a, cudaStream_t s) {
   launch_pdl(k_attn<HD>, grid, dim3(kAttnWarps * 32), C::SMEM, s, a);
 }
 
-void launch_attention(const AttnArgs& a, cudaStream_t s) {
-  if (a.n_rows <= 0) return;
+void launch_attention(const AttnArgs& a0, cudaStream_t s) {
+  if (a0.n_rows <= 0) return;
+  AttnArgs a = a0;
+  a.l2_evict_first = l2_hint_enabled() ? 1 : 0;
   switch (a.hd) {
     case 128: launch_hd<128>(a, s); break;
     case 64: launch_hd<64>(a, s); break;

@@ -170,10 +170,9 @@ __device__ __forceinline__ float warp_sum4(const float (&v)[4], int lane) {
   return c;
 }
 __device__ __forceinline__ void amax_merge(float& bv, int& bi, float ov, int oi) {
-  if (ov > bv || (ov == bv && oi < bi)) {
-    bv = ov;
-    bi = oi;
-  }
+  const bool t = ov > bv || (ov == bv && oi < bi);  // selects, no branch
+  bv = t ? ov : bv;
+  bi = t ? oi : bi;
 }
 // (max, lowest index on ties) of 4 columns, same lane mapping as warp_sum4
 __device__ __forceinline__ void warp_argmax4(const float (&v)[4], const int (&ix)[4], int lane, float& rv, int& ri) {
@@ -203,41 +202,54 @@ struct TileSrc {
   uint32_t pl;  // smem address of P (pull)
   int S, rank, slot_cols, cb, kind;  // kind 0 local, 1 push, 2 pull
 };
-// v[k] = value of columns c0 + k (k < 4) at row r; 4 independent loads per rank
-__device__ __forceinline__ void tile_vals4(const TileSrc& t, int c0, int r, float (&v)[4]) {
+// Epilogue chunk: 16 columns per iteration.  The loop is latency-bound (4 epilogue warps,
+// one per SM sub-partition, nothing else to hide behind), so every load of a chunk is
+// issued before any of its math and the 4-column reductions of a chunk are independent
+// chains (measured: 4 columns per iteration ran at ~500 cycles per iteration).
+constexpr int kEpiCh = 16;
+__device__ __forceinline__ float lds_f32(uint32_t a) {
+  float v;
+  asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+  return v;
+}
+// v[k] = value of columns c0 + k (k < 16, columns >= ce read as 0) at row r (explicit
+// shared-window loads: P / R are shared memory)
+__device__ __forceinline__ void tile_vals16(const TileSrc& t, int c0, int ce, int r, float (&v)[kEpiCh]) {
   if (t.kind == 0) {
+    const uint32_t base = smem_u32(t.P) + (uint32_t)((c0 * 128 + r) * 4);
 #pragma unroll
-    for (int k = 0; k < 4; ++k) v[k] = t.P[(c0 + k) * 128 + r];
+    for (int k = 0; k < kEpiCh; ++k) v[k] = (c0 + k < ce) ? lds_f32(base + k * 512) : 0.f;
     return;
   }
 #pragma unroll
-  for (int k = 0; k < 4; ++k) v[k] = 0.f;
+  for (int k = 0; k < kEpiCh; ++k) v[k] = 0.f;
 #pragma unroll 1
   for (int rk = 0; rk < t.S; ++rk) {
-    float w[4];
+    float w[kEpiCh];
     if (t.kind == 1) {
       const float* src = rk == t.rank ? t.P + (size_t)c0 * 128 : t.R + ((size_t)rk * t.slot_cols + (c0 - t.cb)) * 128;
+      const uint32_t base = smem_u32(src) + (uint32_t)(r * 4);
 #pragma unroll
-      for (int k = 0; k < 4; ++k) w[k] = src[k * 128 + r];
+      for (int k = 0; k < kEpiCh; ++k) w[k] = (c0 + k < ce) ? lds_f32(base + k * 512) : 0.f;
     } else {
       const uint32_t base = dsmem_addr(t.pl, (uint32_t)rk) + (uint32_t)((c0 * 128 + r) * 4);
 #pragma unroll
-      for (int k = 0; k < 4; ++k) w[k] = ld_dsmem(base + k * 512);
+      for (int k = 0; k < kEpiCh; ++k) w[k] = (c0 + k < ce) ? ld_dsmem(base + k * 512) : 0.f;
     }
 #pragma unroll
-    for (int k = 0; k < 4; ++k) v[k] += w[k];
+    for (int k = 0; k < kEpiCh; ++k) v[k] += w[k];
   }
 }
 
 // ------------------------------------------------------------ fused epilogue ops
-// The finished columns [cb, ce) of this CTA, 4 per iteration of a non-unrolled loop:
-// the epilogue runs once per CTA, so its code must stay small (instruction-cache misses
-// from a fully unrolled epilogue cost several microseconds per launch) and it is inlined
-// at ONE call site (a non-inlined call would pass the kernel parameters through local
-// memory).  All 128 epilogue threads call it (named barrier at the end).
+// The finished columns [cb, ce) of this CTA, kEpiCh per iteration of a non-unrolled loop
+// (the epilogue runs once per CTA; one chunk body keeps the code small), inlined at ONE
+// call site (a non-inlined call would pass the kernel parameters through local memory).
+// All 128 epilogue threads call it (named barrier at the end).
 template <int MODE>
 __device__ __forceinline__ void epilogue(const GemmArgs& g, const EpiSmem& sm, const TileSrc& ts, int m_tile,
                                       int n0, int cb, int ce, int et, bool pre) {
+  constexpr int CH = kEpiCh;
   const int m0 = m_tile * 128;
   const int m = m0 + et;
   const int lane = et & 31, wq = et >> 5;
@@ -246,82 +258,111 @@ __device__ __forceinline__ void epilogue(const GemmArgs& g, const EpiSmem& sm, c
   // rows are laid out pairwise, tiled_logical_row in model.cu) with one shuffle.
   bool active = m < g.M;
   if constexpr (MODE == EPI_SWIGLU) active = m_tile * 64 + (et >> 1) < g.ff;
-  // global inputs of a 4-column chunk (EPI_RESID: residual x; EPI_QKV: cos / sin of the
-  // rotation), software-pipelined one chunk ahead so a long column loop (prefill rows)
-  // does not pay a memory round trip per chunk
+  // global inputs of a chunk (EPI_RESID: residual x; EPI_QKV: cos / sin of the rotation),
+  // from the mainloop-time prefetch (pre) or software-pipelined one chunk ahead so a long
+  // column loop (prefill rows) does not pay a memory round trip per chunk
+  constexpr bool HAS_IN = MODE == EPI_RESID || MODE == EPI_QKV;
   const int qi = (MODE == EPI_QKV) ? (et % g.qkv.hd) >> 1 : 0;
   const bool qrope = (MODE == EPI_QKV) && (m / g.qkv.hd) < g.qkv.nq + g.qkv.nkv;
-  auto load_in = [&](int c, float (&ia)[4], float (&ib)[4]) {
+  auto load_in = [&](int c, float (&ia)[CH], float (&ib)[CH]) {
+    // predicated loads (no per-column branches, so all 16 are in flight at once)
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      ia[k] = 0.f;
-      ib[k] = 0.f;
-      if (!active || c + k >= NL) continue;
+    for (int k = 0; k < CH; ++k) {
+      const bool ok = active && c + k < NL;
       if constexpr (MODE == EPI_RESID) {
-        ia[k] = pre ? sm.xp[(c - cb + k) * 128 + et] : g.x[(size_t)(n0 + c + k) * g.M + m];
+        ia[k] = !ok ? 0.f : pre ? sm.xp[(c - cb + k) * 128 + et] : g.x[(size_t)(n0 + c + k) * g.M + m];
+        ib[k] = 0.f;
       } else if constexpr (MODE == EPI_QKV) {
-        if (qrope) {
-          const int half = g.qkv.hd >> 1, pos = sm.pos[c + k];
-          ia[k] = pre ? sm.xp[(c - cb + k) * 64 + qi] : g.qkv.cos[(size_t)pos * half + qi];
-          ib[k] = pre ? sm.xp[1024 + (c - cb + k) * 64 + qi] : g.qkv.sin[(size_t)pos * half + qi];
+        const bool okr = ok && qrope;
+        const int half = g.qkv.hd >> 1;
+        if (pre) {
+          ia[k] = okr ? sm.xp[(c - cb + k) * 64 + qi] : 0.f;
+          ib[k] = okr ? sm.xp[1024 + (c - cb + k) * 64 + qi] : 0.f;
+        } else {
+          const int pos = okr ? sm.pos[c + k] : 0;
+          ia[k] = okr ? g.qkv.cos[(size_t)pos * half + qi] : 0.f;
+          ib[k] = okr ? g.qkv.sin[(size_t)pos * half + qi] : 0.f;
         }
+      } else {
+        ia[k] = ib[k] = 0.f;
       }
     }
   };
-  float in_a[4], in_b[4];
-  load_in(cb, in_a, in_b);
+  float in_a[CH], in_b[CH];
+  if constexpr (HAS_IN) load_in(cb, in_a, in_b);
 #pragma unroll 1
-  for (int c0 = cb; c0 < ce; c0 += 4) {
-    float ca[4], cbv[4];
+  for (int c0 = cb; c0 < ce; c0 += CH) {
+    float ca[CH], cbv[CH];
+    if constexpr (HAS_IN) {
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      ca[k] = in_a[k];
-      cbv[k] = in_b[k];
+      for (int k = 0; k < CH; ++k) {
+        ca[k] = in_a[k];
+        cbv[k] = in_b[k];
+      }
+      if (c0 + CH < ce) load_in(c0 + CH, in_a, in_b);
     }
-    if (MODE == EPI_RESID || MODE == EPI_QKV)
-      if (c0 + 4 < ce) load_in(c0 + 4, in_a, in_b);
-    float v[4], u[4];
-    tile_vals4(ts, c0, et, v);
-    if (g.rs_ss)
+    float v[CH], u[CH];
+    tile_vals16(ts, c0, ce, et, v);
+    if (et == 0 && c0 == cb && sm.mark) {  // trace: partial sums loaded (data-dependent mark)
+      const long long t = clock64() + (v[0] == 1.2345e-30f ? 1 : 0);
+      sm.mark[4] = t;
+      sm.mark[5] = t;
+    }
+    if (g.rs_ss) {
+      const uint32_t ib = smem_u32(sm.inv + c0);
 #pragma unroll
-      for (int k = 0; k < 4; ++k) v[k] *= (c0 + k < NL) ? sm.inv[c0 + k] : 0.f;
+      for (int k = 0; k < CH; ++k) v[k] *= (c0 + k < NL) ? lds_f32(ib + 4 * k) : 0.f;
+    }
     if (MODE == EPI_SWIGLU || MODE == EPI_QKV)
 #pragma unroll
-      for (int k = 0; k < 4; ++k) u[k] = __shfl_xor_sync(0xffffffffu, v[k], 1);
+      for (int k = 0; k < CH; ++k) u[k] = __shfl_xor_sync(0xffffffffu, v[k], 1);
     if constexpr (MODE == EPI_STORE) {
       if (active)
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
+        for (int k = 0; k < CH; ++k)
           if (c0 + k < NL) g.out[(size_t)(n0 + c0 + k) * g.M + m] = v[k];
     } else if constexpr (MODE == EPI_RESID) {
-      const float (&xv)[4] = ca;
-      float sq[4];
+      // math first for all columns (no branches: independent chains interleave), then
+      // the guarded stores
+      float sq[CH], xn[CH];
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        float xn = 0.f;
-        if (active && c0 + k < NL) {
-          xn = xv[k] + v[k];
-          g.x[(size_t)(n0 + c0 + k) * g.M + m] = xn;
-          if (g.xb) g.xb[(size_t)(n0 + c0 + k) * g.M + m] = __float2bfloat16_rn(xn);
-        }
-        sq[k] = xn * xn;
+      for (int k = 0; k < CH; ++k) {
+        xn[k] = (active && c0 + k < NL) ? ca[k] + v[k] : 0.f;
+        sq[k] = xn[k] * xn[k];
       }
-      const float t = warp_sum4(sq, lane);  // column c0 + ((lane >> 3) & 3) on lanes 8j
-      if ((lane & 7) == 0) sm.redv[wq * sm.bn + c0 + ((lane >> 3) & 3)] = t;
-    } else if constexpr (MODE == EPI_SWIGLU) {
-      // even lane: gate row, odd lane: up row of feature jf; the even lane writes columns
-      // c0, c0 + 1 and the odd lane c0 + 2, c0 + 3
-      const bool odd = et & 1;
-      const int jf = m_tile * 64 + (et >> 1);
       if (active)
 #pragma unroll
-        for (int kk = 0; kk < 2; ++kk) {
-          const int k = kk + (odd ? 2 : 0);
-          if (c0 + k < NL) {
-            const float gv = odd ? u[k] : v[k], uv = odd ? v[k] : u[k];
-            const float sgv = __fdividef(gv, 1.f + __expf(-gv));
-            g.act[(size_t)(n0 + c0 + k) * g.ff + jf] = __float2bfloat16_rn(sgv * uv);
-          }
+        for (int k = 0; k < CH; ++k)
+          if (c0 + k < NL) g.x[(size_t)(n0 + c0 + k) * g.M + m] = xn[k];
+      if (active && g.xb)
+#pragma unroll
+        for (int k = 0; k < CH; ++k)
+          if (c0 + k < NL) g.xb[(size_t)(n0 + c0 + k) * g.M + m] = __float2bfloat16_rn(xn[k]);
+#pragma unroll
+      for (int j = 0; j < CH / 4; ++j) {
+        const float q4[4] = {sq[4 * j], sq[4 * j + 1], sq[4 * j + 2], sq[4 * j + 3]};
+        const float t = warp_sum4(q4, lane);  // column c0 + 4j + ((lane >> 3) & 3) on lanes 8i
+        const int c = c0 + 4 * j + ((lane >> 3) & 3);
+        if ((lane & 7) == 0 && c < ce) sm.redv[wq * sm.bn + c] = t;
+      }
+    } else if constexpr (MODE == EPI_SWIGLU) {
+      // even lane: gate row, odd lane: up row of feature jf; the even lane writes the first
+      // two columns of each group of 4 and the odd lane the last two.  Math for the 8
+      // columns of this lane first (selects, no branches), then the guarded stores.
+      const bool odd = et & 1;
+      const int jf = m_tile * 64 + (et >> 1);
+      float h[CH / 2];
+#pragma unroll
+      for (int j = 0; j < CH / 2; ++j) {
+        const int ka = 4 * (j >> 1) + (j & 1), kb = ka + 2;
+        const float gv = odd ? u[kb] : v[ka], uv = odd ? v[kb] : u[ka];
+        h[j] = __fdividef(gv, 1.f + __expf(-gv)) * uv;
+      }
+      if (active)
+#pragma unroll
+        for (int j = 0; j < CH / 2; ++j) {
+          const int c = c0 + 4 * (j >> 1) + (j & 1) + (odd ? 2 : 0);
+          if (c < NL) g.act[(size_t)(n0 + c) * g.ff + jf] = __float2bfloat16_rn(h[j]);
         }
     } else if constexpr (MODE == EPI_QKV) {
       // row 2i of a head = dim i, row 2i + 1 = dim i + hd/2 (rotate-half partners); every
@@ -333,49 +374,65 @@ __device__ __forceinline__ void epilogue(const GemmArgs& g, const EpiSmem& sm, c
       const int dim = odd ? i + half : i;
       const int head = m / hd;
       const bool rope = head < q.nq + q.nkv;
-      if (active)
+      bf16 yb[CH];  // math first (no branches), then the guarded stores
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          const int c = c0 + k;
-          if (c < NL) {
-            const int pos = sm.pos[c];
-            float y = v[k];
-            if (rope) {
-              const float cs = ca[k], sn = cbv[k];
-              y = odd ? v[k] * cs + u[k] * sn : v[k] * cs - u[k] * sn;
-            }
-            const bf16 b = __float2bfloat16_rn(y);
-            const int n = n0 + c;
-            if (head < q.nq) {
-              q.q_out[((size_t)n * q.nq + head) * hd + dim] = b;
-              if (q.q_cap) q.q_cap[((size_t)(q.row0 + n) * q.nq + head) * hd + dim] = __bfloat162float(b);
-            } else {
-              const int kind = rope ? 0 : 1;
-              const int kvh = kind == 0 ? head - q.nq : head - q.nq - q.nkv;
-              const int off = pos & 15;
-              unsigned char* blk = (unsigned char*)q.pool +
-                                   (((size_t)sm.page[c] * q.nkv + kvh) * 2 + kind) * (size_t)(16 * hd * 2) +
-                                   off * hd * 2;
-              *(bf16*)(blk + (kv_swz_chunk(hd, off, dim >> 3) << 4) + ((dim & 7) << 1)) = b;
-            }
-          }
-        }
-    } else if constexpr (MODE == EPI_ARGMAX) {
-      float bv[4];
-      int bi[4];
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {  // greedy: max over the tile's rows, lowest index on ties
-        const bool ok = active && c0 + k < NL;
-        if (ok && g.out) g.out[(size_t)(n0 + c0 + k) * g.M + m] = v[k];
-        bv[k] = ok ? v[k] : -INFINITY;
-        bi[k] = ok ? m : INT_MAX;
+      for (int k = 0; k < CH; ++k) {
+        const float y = rope ? (odd ? v[k] * ca[k] + u[k] * cbv[k] : v[k] * ca[k] - u[k] * cbv[k]) : v[k];
+        yb[k] = __float2bfloat16_rn(y);
       }
-      float rv;
-      int ri;
-      warp_argmax4(bv, bi, lane, rv, ri);  // column c0 + ((lane >> 3) & 3) on lanes 8j
-      if ((lane & 7) == 0) {
-        sm.redv[wq * sm.bn + c0 + ((lane >> 3) & 3)] = rv;
-        sm.redi[wq * sm.bn + c0 + ((lane >> 3) & 3)] = ri;
+      if (active) {
+        if (head < q.nq) {  // warp-uniform (a head is 128 rows)
+#pragma unroll
+          for (int k = 0; k < CH; ++k)
+            if (c0 + k < NL) q.q_out[((size_t)(n0 + c0 + k) * q.nq + head) * hd + dim] = yb[k];
+          if (q.q_cap)
+#pragma unroll
+            for (int k = 0; k < CH; ++k)
+              if (c0 + k < NL)
+                q.q_cap[((size_t)(q.row0 + n0 + c0 + k) * q.nq + head) * hd + dim] = __bfloat162float(yb[k]);
+        } else {
+          // KV append into the swizzled page of (row task, position): addresses of all
+          // columns first (predicated shared loads), then the stores
+          const int kind = rope ? 0 : 1;
+          const int kvh = kind == 0 ? head - q.nq : head - q.nq - q.nkv;
+          unsigned char* dst[CH];
+#pragma unroll
+          for (int k = 0; k < CH; ++k) {
+            const bool ok = c0 + k < NL;
+            const int pos = ok ? sm.pos[c0 + k] : 0, pg = ok ? sm.page[c0 + k] : 0;
+            const int off = pos & 15;
+            dst[k] = (unsigned char*)q.pool + (((size_t)pg * q.nkv + kvh) * 2 + kind) * (size_t)(16 * hd * 2) +
+                     off * hd * 2 + (kv_swz_chunk(hd, off, dim >> 3) << 4) + ((dim & 7) << 1);
+          }
+#pragma unroll
+          for (int k = 0; k < CH; ++k)
+            if (c0 + k < NL) *(bf16*)dst[k] = yb[k];
+        }
+      }
+    } else if constexpr (MODE == EPI_ARGMAX) {
+      if (g.out && active)  // logits (parity mode only)
+#pragma unroll
+        for (int k = 0; k < CH; ++k)
+          if (c0 + k < NL) g.out[(size_t)(n0 + c0 + k) * g.M + m] = v[k];
+#pragma unroll
+      for (int j = 0; j < CH / 4; ++j) {
+        float bv[4];
+        int bi[4];
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {  // greedy: max over the tile's rows, lowest index on ties
+          const int k = 4 * j + kk;
+          const bool ok = active && c0 + k < NL;
+          bv[kk] = ok ? v[k] : -INFINITY;
+          bi[kk] = ok ? m : INT_MAX;
+        }
+        float rv;
+        int ri;
+        warp_argmax4(bv, bi, lane, rv, ri);  // column c0 + 4j + ((lane >> 3) & 3) on lanes 8i
+        const int c = c0 + 4 * j + ((lane >> 3) & 3);
+        if ((lane & 7) == 0 && c < ce) {
+          sm.redv[wq * sm.bn + c] = rv;
+          sm.redi[wq * sm.bn + c] = ri;
+        }
       }
     }
   }
@@ -470,7 +527,7 @@ __device__ __forceinline__ void bulk_s2cluster(uint32_t dst, const void* src, ui
 }
 
 template <int BN, int MODE>
-__global__ void __launch_bounds__(kGemmThreads, 1)
+__global__ void __launch_bounds__(kGemmThreads, GemmCfg<BN>::CTAS_PER_SM)
     k_gemm_tc(const __grid_constant__ TmaMap tmB, GemmArgs g) {
   using C = GemmCfg<BN>;
   extern __shared__ unsigned char smem_raw[];
@@ -541,9 +598,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int pre_k = min(C::STAGES, nkb);
       // UMMA-tiled weights: k-block kb of m-tile mt is one contiguous 16 KiB SW128 image
       const bf16* wt = g.w + ((size_t)m_tile * g.kb_total + kb0) * (128 * kBK);
+      const uint64_t pol = g.l2_evict_first ? l2_policy_evict_first() : 0ull;
       for (int i = 0; i < pre_k; ++i) {
         mbar_arrive_expect_tx(&full[i], C::STAGE);
-        bulk_g2s(sA + i * C::A_BYTES, wt + (size_t)i * (128 * kBK), C::A_BYTES, &full[i]);
+        bulk_g2s_hint(sA + i * C::A_BYTES, wt + (size_t)i * (128 * kBK), C::A_BYTES, &full[i], pol);
       }
       pdl_wait();
       tr.ready();
@@ -554,7 +612,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         const uint32_t ph = (uint32_t)((i / C::STAGES) & 1);
         mbar_wait(&empty[s], ph ^ 1u);
         mbar_arrive_expect_tx(&full[s], C::STAGE);
-        bulk_g2s(sA + s * C::A_BYTES, wt + (size_t)i * (128 * kBK), C::A_BYTES, &full[s]);
+        bulk_g2s_hint(sA + s * C::A_BYTES, wt + (size_t)i * (128 * kBK), C::A_BYTES, &full[s], pol);
         tma_load_2d(sB + s * C::B_BYTES, &tmB, (kb0 + i) * kBK, n0, &full[s]);
       }
       if (g.pf_w && n_tile == 0) {  // next launch's first k-blocks -> L2 (weights only)
@@ -599,7 +657,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     // per-column metadata + epilogue inputs of the columns this CTA finishes, while the
     // mainloop runs
     pre = column_meta<MODE>(g, sm, m_tile, n0, cb, ce, et);
-    mbar_wait(done, 0);
+    if (g.epi_backoff_ns) mbar_wait_backoff(done, 0, (uint32_t)g.epi_backoff_ns);
+    else mbar_wait(done, 0);
     tc_fence_after();
     if (et == 0) {
       s_tdone = gtimer();
@@ -645,8 +704,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       mbar_wait(recv_bar, 0);
     }
     EPI_MARK(3);
-    EPI_MARK(4);
-    EPI_MARK(5);
     const TileSrc ts{P, R, smem_u32(P), S, rank, slot_cols, cb, S == 1 ? 0 : (push ? 1 : 2)};
     epilogue<MODE>(g, sm, ts, m_tile, n0, cb, ce, et, pre);
     if (push && et == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
@@ -792,6 +849,11 @@ static cudaError_t launch_mode(const GemmTmaSet& x, const GemmArgs& g, int bn, i
 
 cudaError_t launch_gemm_epi(const bf16* w_tiled, const GemmTmaSet& x, GemmArgs g, int splits, cudaStream_t s) {
   g.w = w_tiled;
+  g.l2_evict_first = l2_hint_enabled() ? 1 : 0;
+  {
+    static const int ns = getenv("RT_EPI_BACKOFF_NS") ? atoi(getenv("RT_EPI_BACKOFF_NS")) : 0;
+    g.epi_backoff_ns = ns;
+  }
   const int bn = gemm_bn(g.N);
   g.kb_total = g.K / kBK;
   g.m_tiles = (g.M + 127) / 128;

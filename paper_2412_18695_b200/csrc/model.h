@@ -50,6 +50,7 @@ struct AttnArgs {
   const int32_t* row_list;   // nullable: CTA z serves row row_list[z] (global row; rows
                              // outside [row0, row0 + chunk_rows) are skipped); n_rows = list size
   int chunk_rows;
+  int l2_evict_first;        // set by launch_attention: K/V pages are read once per step
 };
 int64_t attn_ws_floats(int n_rows, int nq, int hd, int max_chunks);
 void attn_plan(int n_rows, int nkv, int max_seqlen, int* chunk_pages, int* max_chunks);
@@ -118,6 +119,8 @@ struct GemmArgs {
   // while this one drains its pipeline and runs its epilogue (HBM would idle).
   const bf16* pf_w;
   int pf_S, pf_m_tiles, pf_kb_total, pf_kb;
+  int l2_evict_first;  // set by launch_gemm_epi: weight tiles are read once per step
+  int epi_backoff_ns;  // set by launch_gemm_epi: nanosleep between the epilogue warps' polls
 };
 // fill g.pf_* for a next launch of weights w [M x K] at N columns (splits <= 0: auto),
 // prefetching at most budget_bytes in total

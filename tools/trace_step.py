@@ -114,7 +114,7 @@ def main():
         rows.append(dict(role=name, launches=cnt, lead_us=lead / cnt, gap_us=gap / cnt, body_us=body / cnt,
                          us_per_step=per_step, ctas=ctas // cnt, cta_main_us=mm, cta_epilogue_us=me))
     print("GEMM epilogue phases after the accumulator is complete (median us at 1.965 GHz): park | "
-          "cluster barrier | slices received | - | - | epilogue loop | final reduction | bulk-copy drain")
+          "cluster barrier | slices received | partials loaded | - | epilogue loop | final reduction | bulk-copy drain")
     for name, v in ph.items():
         m = np.median(np.array(v), axis=0)
         print(f"  {name:28s} " + " ".join(f"{x:7.2f}" for x in m))
