@@ -103,6 +103,17 @@ struct rt_engine {
   int* d_attn_tickets = nullptr;
   int* d_gemm_cnt = nullptr;
   GemmTmaSet x_h, x_o, x_act, x_hfin;
+  // projection chain (launch_chain): per job slot (0 O, 1 gate/up, 2 down, 3 next QKV)
+  // partial-tile workspace, self-resetting tile tickets, cumulative done counters and the
+  // host copy of their bases (the value each counter holds before the next launch)
+  bool chain_on = false;
+  float* d_chain_ws[kChainMaxJobs] = {};
+  int chain_slots_n[kChainMaxJobs] = {};
+  unsigned* d_chain_cnt[kChainMaxJobs] = {};
+  unsigned* d_chain_done = nullptr;
+  unsigned chain_base[kChainMaxJobs] = {};
+  int chain_grid_n = 0;
+  int chain_pf_ahead = 16;  // RT_CHAIN_PF
   // submissions
   SubmitRec* h_recs = nullptr;
   int32_t* h_toks = nullptr;
@@ -447,6 +458,28 @@ static rt_status create_impl(rt_engine* e, const rt_config* cfg) {
     if (!ok) return done(fail(e, RT_E_CUDA, "cuTensorMapEncodeTiled failed (activations)"));
     e->ev_attn.resize(2 * L);
     for (auto& ev : e->ev_attn) cudaEventCreate(&ev);
+    // projection chain for decode rounds of <= 64 rows: OPT-IN (RT_CHAIN=1).  Measured at
+    // C2 it is slower than one launch per projection (182 vs ~104 us per layer, DESIGN.md
+    // §9): each job boundary pays a chain of loaded-HBM latencies (store fence, ticket,
+    // partial loads, release / acquire) that the 96 KB ring per SM cannot cover.
+    {
+      const int cm[kChainMaxJobs] = {d, 2 * ff, d, e->qkv_dim}, ck[kChainMaxJobs] = {nq * hd, d, ff, d};
+      const int P = chain_grid(cm, ck, kChainMaxJobs);
+      bool ok_c = getenv("RT_CHAIN") != nullptr && atoi(getenv("RT_CHAIN")) != 0;
+      for (int j = 0; j < kChainMaxJobs; ++j) ok_c = ok_c && ck[j] % 64 == 0;
+      if (ok_c) {
+        e->chain_grid_n = P;
+        if (const char* pf = getenv("RT_CHAIN_PF")) e->chain_pf_ahead = atoi(pf);
+        for (int j = 0; j < kChainMaxJobs; ++j) {
+          const int mtiles = (cm[j] + 127) / 128;
+          e->chain_slots_n[j] = chain_slots(cm[j], ck[j], P);
+          CK(e, dalloc(e, &e->d_chain_ws[j], (size_t)mtiles * e->chain_slots_n[j] * 64 * 128));
+          CK(e, dalloc(e, &e->d_chain_cnt[j], (size_t)mtiles));
+        }
+        CK(e, dalloc(e, &e->d_chain_done, (size_t)kChainMaxJobs));
+        e->chain_on = true;
+      }
+    }
   }
   if (c.flags & RT_FLAG_TRACE) {  // 48-byte records, bound process-wide (last engine wins)
     e->trace_cap = 1u << 20;
@@ -761,28 +794,66 @@ static rt_status forward(rt_engine* e, const HostMailbox& plan) {
       launch_gemm_epi(w, x, g, 0, s);
       ++launches;
     };
+    // epilogue arguments of the four decode-layer projections (a6)
+    auto args_qkv = [&](int l) {  // QKV projection + RoPE + KV append (a6 -> a4 pages)
+      GemmArgs g{};
+      g.mode = EPI_QKV;
+      QkvFuse& q = g.qkv;
+      q.row_task = P.row_task;
+      q.row_pos = P.row_pos;
+      q.page_table = e->tt.page_table;
+      q.row0 = row0;
+      q.pt_stride = e->pt_stride;
+      q.nq = nq;
+      q.nkv = nkv;
+      q.hd = hd;
+      q.cos = e->d_rope_cos;
+      q.sin = e->d_rope_sin;
+      q.q_out = e->d_q;
+      q.pool = e->d_pool + (size_t)l * e->pool_layer_bytes;
+      q.q_cap = (e->d_cap_q && l == c.capture_layer) ? e->d_cap_q : nullptr;
+      g.rs_ss = e->d_ss;  // attention RMSNorm applied as the epilogue's row scale
+      g.rs_tiles = d_tiles;
+      g.M = e->qkv_dim;
+      g.N = n;
+      g.K = d;
+      return g;
+    };
+    auto args_resid = [&](int M, int K) {  // O / down projection + residual
+      GemmArgs g{};
+      g.mode = EPI_RESID;
+      g.x = e->d_x;
+      g.ss = e->d_ss;
+      g.xb = e->d_h;
+      g.M = M;
+      g.N = n;
+      g.K = K;
+      return g;
+    };
+    auto args_gu = [&]() {  // gate/up projection (FFN RMSNorm as row scale) + SwiGLU
+      GemmArgs g{};
+      g.mode = EPI_SWIGLU;
+      g.act = e->d_act;
+      g.ff = ff;
+      g.rs_ss = e->d_ss;
+      g.rs_tiles = d_tiles;
+      g.M = 2 * ff;
+      g.N = n;
+      g.K = d;
+      return g;
+    };
+    // decode-only chunks of <= 64 rows: O, gate/up, down and the next layer's QKV run as
+    // ONE persistent chain launch per layer (launch_chain)
+    // (not under graph capture: the chain's done targets are per-launch values)
+    cudaStreamCaptureStatus cap_st = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cap_st);
+    const bool use_chain = e->chain_on && n <= 64 && plan.n_prefill_rows == 0 && pa.n_tiles == 0 &&
+                           cap_st == cudaStreamCaptureStatusNone;
     for (int l = 0; l < c.n_layers; ++l) {
       LayerW& w = e->layers[l];
       void* pool_l = e->d_pool + (size_t)l * e->pool_layer_bytes;
-      {  // QKV projection + RoPE + KV append (a6 -> a4 pages)
-        GemmArgs g{};
-        g.mode = EPI_QKV;
-        QkvFuse& q = g.qkv;
-        q.row_task = P.row_task;
-        q.row_pos = P.row_pos;
-        q.page_table = e->tt.page_table;
-        q.row0 = row0;
-        q.pt_stride = e->pt_stride;
-        q.nq = nq;
-        q.nkv = nkv;
-        q.hd = hd;
-        q.cos = e->d_rope_cos;
-        q.sin = e->d_rope_sin;
-        q.q_out = e->d_q;
-        q.pool = pool_l;
-        q.q_cap = (e->d_cap_q && l == c.capture_layer) ? e->d_cap_q : nullptr;
-        g.rs_ss = e->d_ss;  // attention RMSNorm applied as the epilogue's row scale
-        g.rs_tiles = d_tiles;
+      if (!use_chain || l == 0) {
+        GemmArgs g = args_qkv(l);
         gemm(w.qkv, e->x_h, e->qkv_dim, d, g);
       }
       aa.pool = pool_l;
@@ -799,31 +870,50 @@ static rt_status forward(rt_engine* e, const HostMailbox& plan) {
         launch_attention_prefill(pa, s);
         ++launches;
       }
+      if (use_chain) {
+        ChainArgs ca{};
+        ca.job[0] = args_resid(d, nq * hd);
+        ca.job[0].w = w.o;
+        ca.xmap[0] = e->x_o.m64;
+        ca.job[1] = args_gu();
+        ca.job[1].w = w.gu;
+        ca.xmap[1] = e->x_h.m64;
+        ca.job[2] = args_resid(d, ff);
+        ca.job[2].w = w.d;
+        ca.xmap[2] = e->x_act.m64;
+        ca.n_jobs = 3;
+        if (l + 1 < c.n_layers) {
+          ca.job[3] = args_qkv(l + 1);
+          ca.job[3].w = e->layers[l + 1].qkv;
+          ca.xmap[3] = e->x_h.m64;
+          ca.n_jobs = 4;
+        }
+        for (int j = 0; j < ca.n_jobs; ++j) {
+          ca.ws[j] = e->d_chain_ws[j];
+          ca.ws_slots[j] = e->chain_slots_n[j];
+          ca.tile_cnt[j] = e->d_chain_cnt[j];
+          e->chain_base[j] += (unsigned)((ca.job[j].M + 127) / 128);
+          ca.done_target[j] = e->chain_base[j];
+        }
+        ca.done = e->d_chain_done;
+        ca.grid = e->chain_grid_n;
+        ca.pf_ahead = e->chain_pf_ahead;
+        CK(e, launch_chain(ca, s));
+        ++launches;
+        continue;
+      }
       {  // O projection + residual
-        GemmArgs g{};
-        g.mode = EPI_RESID;
-        g.x = e->d_x;
-        g.ss = e->d_ss;
-        g.xb = e->d_h;
+        GemmArgs g = args_resid(d, nq * hd);
         gemm_set_prefetch(g, w.gu, 2 * ff, n, d, 0, e->l2_pf_bytes);
         gemm(w.o, e->x_o, d, nq * hd, g);
       }
       {  // gate/up projection (FFN RMSNorm as row scale) + SwiGLU
-        GemmArgs g{};
-        g.mode = EPI_SWIGLU;
-        g.act = e->d_act;
-        g.ff = ff;
-        g.rs_ss = e->d_ss;
-        g.rs_tiles = d_tiles;
+        GemmArgs g = args_gu();
         gemm_set_prefetch(g, w.d, d, n, ff, 0, e->l2_pf_bytes);
         gemm(w.gu, e->x_h, 2 * ff, d, g);
       }
       {  // down projection + residual
-        GemmArgs g{};
-        g.mode = EPI_RESID;
-        g.x = e->d_x;
-        g.ss = e->d_ss;
-        g.xb = e->d_h;
+        GemmArgs g = args_resid(d, ff);
         if (l + 1 < c.n_layers)  // the next layer's QKV projection
           gemm_set_prefetch(g, e->layers[l + 1].qkv, e->qkv_dim, n, d, 0, e->l2_pf_bytes);
         else if (row0 + n >= n_rows)  // the lm_head of the logits rows

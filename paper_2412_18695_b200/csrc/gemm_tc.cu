@@ -146,6 +146,7 @@ struct EpiSmem {
   int bn;
   float* redv;   // [4][BN] per-warp column partials (EPI_RESID sum of squares, EPI_ARGMAX max)
   int* redi;     // [4][BN] per-warp argmax index
+  int xp_sin;    // offset (floats) of the sin table in xp (EPI_QKV)
   float* xp;     // [16][128] epilogue inputs prefetched during the mainloop (EPI_RESID x;
                  //  EPI_QKV cos [16][64] then sin [16][64])
   long long* mark;  // clock64 phase marks (trace), written by thread et == 0
@@ -200,7 +201,8 @@ struct TileSrc {
   const float* P;
   const float* R;
   uint32_t pl;  // smem address of P (pull)
-  int S, rank, slot_cols, cb, kind;  // kind 0 local, 1 push, 2 pull
+  int S, rank, slot_cols, cb, kind;  // kind 0 local, 1 push, 2 pull, 3 global slots (chain)
+  const float* G;                    // kind 3: S partial tiles [S][BN][128] in global memory
 };
 // Epilogue chunk: 16 columns per iteration.  The loop is latency-bound (4 epilogue warps,
 // one per SM sub-partition, nothing else to hide behind), so every load of a chunk is
@@ -231,6 +233,10 @@ __device__ __forceinline__ void tile_vals16(const TileSrc& t, int c0, int ce, in
       const uint32_t base = smem_u32(src) + (uint32_t)(r * 4);
 #pragma unroll
       for (int k = 0; k < kEpiCh; ++k) w[k] = (c0 + k < ce) ? lds_f32(base + k * 512) : 0.f;
+    } else if (t.kind == 3) {  // written by other SMs in this launch: L2 (ld.global.cg)
+      const float* src = t.G + ((size_t)rk * t.slot_cols + c0) * 128 + r;
+#pragma unroll
+      for (int k = 0; k < kEpiCh; ++k) w[k] = (c0 + k < ce) ? __ldcg(src + k * 128) : 0.f;
     } else {
       const uint32_t base = dsmem_addr(t.pl, (uint32_t)rk) + (uint32_t)((c0 * 128 + r) * 4);
 #pragma unroll
@@ -270,14 +276,15 @@ __device__ __forceinline__ void epilogue(const GemmArgs& g, const EpiSmem& sm, c
     for (int k = 0; k < CH; ++k) {
       const bool ok = active && c + k < NL;
       if constexpr (MODE == EPI_RESID) {
-        ia[k] = !ok ? 0.f : pre ? sm.xp[(c - cb + k) * 128 + et] : g.x[(size_t)(n0 + c + k) * g.M + m];
+        // __ldcg: in the projection chain x was written by another SM in this launch
+        ia[k] = !ok ? 0.f : pre ? sm.xp[(c - cb + k) * 128 + et] : __ldcg(g.x + (size_t)(n0 + c + k) * g.M + m);
         ib[k] = 0.f;
       } else if constexpr (MODE == EPI_QKV) {
         const bool okr = ok && qrope;
         const int half = g.qkv.hd >> 1;
         if (pre) {
           ia[k] = okr ? sm.xp[(c - cb + k) * 64 + qi] : 0.f;
-          ib[k] = okr ? sm.xp[1024 + (c - cb + k) * 64 + qi] : 0.f;
+          ib[k] = okr ? sm.xp[sm.xp_sin + (c - cb + k) * 64 + qi] : 0.f;
         } else {
           const int pos = okr ? sm.pos[c + k] : 0;
           ia[k] = okr ? g.qkv.cos[(size_t)pos * half + qi] : 0.f;
@@ -485,7 +492,16 @@ __device__ __forceinline__ bool column_meta(const GemmArgs& g, const EpiSmem& sm
     }
     if (g.rs_ss) {
       float t = 0.f;
-      for (int i = 0; i < g.rs_tiles; ++i) t += g.rs_ss[(size_t)n * g.rs_tiles + i];
+      const float* rs = g.rs_ss + (size_t)n * g.rs_tiles;
+      if (g.rs_tiles == 32 && ((uintptr_t)rs & 15) == 0) {  // d = 4096: all 8 loads in flight
+        float4 r4[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) r4[i] = __ldcg(reinterpret_cast<const float4*>(rs) + i);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) t = (((t + r4[i].x) + r4[i].y) + r4[i].z) + r4[i].w;
+      } else {
+        for (int i = 0; i < g.rs_tiles; ++i) t += __ldcg(rs + i);
+      }
       sm.inv[cc] = rsqrtf(t / (float)g.K + 1e-5f);
     }
   }
@@ -552,6 +568,7 @@ __global__ void __launch_bounds__(kGemmThreads, GemmCfg<BN>::CTAS_PER_SM)
   sm.redi = reinterpret_cast<int*>(sm.redv + 4 * BN);
   sm.bn = BN;
   sm.xp = reinterpret_cast<float*>(ctl + 512 + C::META + C::RED);
+  sm.xp_sin = 1024;
   __shared__ long long s_mark[9];  // clock64 phase marks (SM cycles), RT_FLAG_TRACE
   sm.mark = s_mark;
 
@@ -704,7 +721,7 @@ __global__ void __launch_bounds__(kGemmThreads, GemmCfg<BN>::CTAS_PER_SM)
       mbar_wait(recv_bar, 0);
     }
     EPI_MARK(3);
-    const TileSrc ts{P, R, smem_u32(P), S, rank, slot_cols, cb, S == 1 ? 0 : (push ? 1 : 2)};
+    const TileSrc ts{P, R, smem_u32(P), S, rank, slot_cols, cb, S == 1 ? 0 : (push ? 1 : 2), nullptr};
     epilogue<MODE>(g, sm, ts, m_tile, n0, cb, ce, et, pre);
     if (push && et == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     EPI_MARK(8);
@@ -731,6 +748,429 @@ __global__ void __launch_bounds__(kGemmThreads, GemmCfg<BN>::CTAS_PER_SM)
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::TMEM_COLS));
+  }
+}
+
+// ============================================================ projection chain
+// One persistent CTA per SM runs up to 4 dependent decode projections (model.h ChainArgs,
+// DESIGN.md §6).  Per job, the m-tile x k-block iterations are split evenly over the CTAs
+// (stream-K); a CTA accumulates each tile segment of its range in one of two TMEM buffers.
+// Roles as k_gemm_tc: warp 0 lane 0 = producer, warp 1 = TMEM owner + MMA issuer, warps
+// 2..5 = epilogue.  The producer streams weight k-blocks into the ring continuously across
+// job boundaries (weights do not depend on activations) and issues a stage's activation
+// tile only once the job it belongs to may read its input (job 0: the previous kernel,
+// griddepcontrol.wait; job j > 0: every tile of job j - 1 finished, an acquire poll of the
+// cumulative done[j - 1] counter).  So HBM keeps streaming while the tail of job j - 1
+// (last MMAs, partial-tile fixup, epilogue) completes — the bubbles a launch per
+// projection pays (pipeline fill, split-K exchange, epilogue, exit) overlap the stream.
+// Segments that are not a whole tile store their fp32 partial to the job's workspace slot;
+// the last contributor (atomic ticket) sums the slots in slot order (deterministic) and
+// runs the fused epilogue of that job's mode.
+namespace chain {
+constexpr int BN = 64;
+constexpr int STAGES = 6;
+constexpr int A_BYTES = 128 * kBK * 2;  // 16 KB weight k-block
+constexpr int B_BYTES = BN * kBK * 2;   // 8 KB activation k-block
+constexpr int P_BYTES = BN * 128 * 4;   // whole-tile accumulator staging
+constexpr int CTL = 256;
+constexpr int META = 3 * BN * 4;
+constexpr int RED = 2 * 4 * BN * 4;
+constexpr int SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + 2 * P_BYTES + CTL + META + RED;
+static_assert(SMEM <= 227 * 1024, "chain smem");
+
+// k-block iterations of a job: I = m_tiles * kb; CTA c owns [q0(c), q0(c + 1))
+__host__ __device__ inline int q0(long long I, int c, int P) { return (int)((I * c) / P); }
+// the CTA whose range contains iteration q (valid when I >= P: no empty ranges)
+__host__ __device__ inline int owner(long long q, long long I, int P) { return (int)(((q + 1) * P - 1) / I); }
+
+struct Cursor {  // walk of this CTA's k-block iterations across the jobs of the launch
+  int j, q, qend, kb, kbt;
+  const bf16* wq;  // weight k-block q of job j (UMMA-tiled: k-block q at w + q * 128 * 64)
+};
+__device__ __forceinline__ void cur_job(const ChainArgs& a, Cursor& c, int cta, int P) {
+  for (;;) {
+    ++c.j;
+    if (c.j >= a.n_jobs) return;
+    const GemmArgs& g = a.job[c.j];
+    const long long I = (long long)g.m_tiles * g.kb_total;
+    c.q = q0(I, cta, P);
+    c.qend = q0(I, cta + 1, P);
+    c.kbt = g.kb_total;
+    c.kb = c.q % c.kbt;
+    c.wq = g.w + (size_t)c.q * (128 * kBK);
+    if (c.q < c.qend) return;
+  }
+}
+__device__ __forceinline__ void cur_init(const ChainArgs& a, Cursor& c, int cta, int P) {
+  c.j = -1;
+  cur_job(a, c, cta, P);
+}
+__device__ __forceinline__ void cur_adv(const ChainArgs& a, Cursor& c, int cta, int P) {
+  c.wq += 128 * kBK;
+  if (++c.kb == c.kbt) c.kb = 0;
+  if (++c.q >= c.qend) cur_job(a, c, cta, P);
+}
+__device__ __forceinline__ bool done_reached(const unsigned* p, unsigned target) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return (int)(v - target) >= 0;
+}
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred P1;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, P1;\n\t}"
+      : "=r"(ok)
+      : "r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+}  // namespace chain
+
+// Epilogue inputs of a chain tile, loaded into registers (all in flight at once) while the
+// partial-tile fixup runs, then parked in sm.xp: EPI_RESID the residual x [64 cols][128];
+// EPI_QKV cos / sin [64 cols][64 freqs] (thread: frequency et & 63, columns et >> 6 + 2k).
+__device__ __forceinline__ void chain_inputs_load(const GemmArgs& g, const EpiSmem& sm, int t, int et,
+                                                  float (&in)[chain::BN]) {
+  if (g.mode == EPI_RESID) {
+    const int m = t * 128 + et;
+#pragma unroll
+    for (int c = 0; c < chain::BN; ++c)
+      in[c] = (m < g.M && c < g.N) ? __ldcg(g.x + (size_t)c * g.M + m) : 0.f;
+  } else if (g.mode == EPI_QKV) {
+    const int i = et & 63, half = g.qkv.hd >> 1;
+#pragma unroll
+    for (int k = 0; k < chain::BN / 2; ++k) {
+      const int c = (et >> 6) + 2 * k;
+      const bool ok = c < g.N && i < half;
+      const int pos = ok ? sm.pos[c] : 0;
+      in[k] = ok ? g.qkv.cos[(size_t)pos * half + i] : 0.f;
+      in[chain::BN / 2 + k] = ok ? g.qkv.sin[(size_t)pos * half + i] : 0.f;
+    }
+  }
+}
+__device__ __forceinline__ void chain_inputs_park(const GemmArgs& g, const EpiSmem& sm, int et,
+                                                  const float (&in)[chain::BN]) {
+  if (g.mode == EPI_RESID) {
+#pragma unroll
+    for (int c = 0; c < chain::BN; ++c) sm.xp[c * 128 + et] = in[c];
+  } else if (g.mode == EPI_QKV) {
+    const int i = et & 63;
+#pragma unroll
+    for (int k = 0; k < chain::BN / 2; ++k) {
+      const int c = (et >> 6) + 2 * k;
+      sm.xp[c * 64 + i] = in[k];
+      sm.xp[sm.xp_sin + c * 64 + i] = in[chain::BN / 2 + k];
+    }
+  }
+}
+template <int MODE>
+__device__ __forceinline__ void chain_epilogue(const GemmArgs& g, const EpiSmem& sm, const TileSrc& ts, int t,
+                                               int et) {
+  epilogue<MODE>(g, sm, ts, t, 0, 0, chain::BN, et, MODE == EPI_RESID || MODE == EPI_QKV);
+}
+
+__global__ void __launch_bounds__(kGemmThreads, 1) k_chain(const __grid_constant__ ChainArgs a) {
+  using namespace chain;
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  unsigned char* sA = smem;
+  unsigned char* sB = smem + STAGES * A_BYTES;
+  float* P = reinterpret_cast<float*>(sB + STAGES * B_BYTES);
+  float* Q = P + BN * 128;  // second staging buffer of the partial-tile fixup
+  unsigned char* ctl = reinterpret_cast<unsigned char*>(Q) + P_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(ctl);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* fxbar = tempty + 2;  // [2] fixup staging loads (P, Q)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fxbar + 2);
+  int* s_last = reinterpret_cast<int*>(tmem_slot + 1);
+  EpiSmem sm;
+  sm.pos = reinterpret_cast<int*>(ctl + CTL);
+  sm.page = sm.pos + BN;
+  sm.inv = reinterpret_cast<float*>(sm.page + BN);
+  sm.redv = reinterpret_cast<float*>(ctl + CTL + META);
+  sm.redi = reinterpret_cast<int*>(sm.redv + 4 * BN);
+  sm.bn = BN;
+  sm.xp = Q;  // epilogue inputs (chain_inputs_park), after the fixup is done with Q
+  sm.xp_sin = BN * 64;
+  __shared__ long long s_mark[9];
+  sm.mark = s_mark;
+
+  TraceScope tr(TK_CHAIN | ((uint32_t)a.n_jobs << 8));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cta = blockIdx.x, NP = gridDim.x;
+
+  if (warp == 0 && lane == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 1);
+      mbar_init(&fxbar[i], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(2 * BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) pdl_trigger();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // W cursor runs ahead of the X cursor by up to the ring depth
+      for (int j = 0; j < a.n_jobs; ++j) prefetch_tmap(&a.xmap[j]);
+      Cursor cw, cx, cp;
+      cur_init(a, cw, cta, NP);
+      cur_init(a, cx, cta, NP);
+      cur_init(a, cp, cta, NP);
+      int np = 0;  // weight k-blocks prefetched into L2 (lookahead a.pf_ahead beyond the ring)
+      const uint64_t pol = a.job[0].l2_evict_first ? l2_policy_evict_first() : 0ull;
+      int nw = 0, nx = 0, dep_job = -1;  // dep_job: highest job whose X may be loaded
+      bool waited = false;
+      unsigned long long t_dep[kChainMaxJobs] = {0, 0, 0, 0};  // trace: input of job j ready
+      while (cx.j < a.n_jobs) {
+        bool prog = false;
+        if (cw.j < a.n_jobs) {
+          const int st = nw % STAGES;
+          if (nw < STAGES || chain::mbar_test(&empty[st], (uint32_t)(((nw / STAGES) & 1) ^ 1))) {
+            mbar_arrive_expect_tx(&full[st], A_BYTES + B_BYTES);
+            bulk_g2s_hint(sA + st * A_BYTES, cw.wq, A_BYTES, &full[st], pol);
+            cur_adv(a, cw, cta, NP);
+            ++nw;
+            prog = true;
+          }
+        }
+        if (cp.j < a.n_jobs && np < nw + a.pf_ahead) {
+          // keep HBM streaming through job boundaries: the ring stalls while job j - 1
+          // finishes, the L2 prefetch does not
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(cp.wq), "r"((uint32_t)A_BYTES) : "memory");
+          cur_adv(a, cp, cta, NP);
+          ++np;
+          prog = true;
+        }
+        if (nx < nw) {
+          const int j = cx.j;
+          if (dep_job < j) {
+            if (j == 0) {
+              // the previous kernel (attention) produced job 0's input: wait only once the
+              // ring holds as many weight k-blocks as it can
+              if (!prog || cw.j >= a.n_jobs) {
+                pdl_wait();
+                tr.ready();
+                waited = true;
+                dep_job = 0;
+                t_dep[0] = gtimer();
+              }
+            } else if (chain::done_reached(a.done + (j - 1), a.done_target[j - 1])) {
+              asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> TMA reads
+              dep_job = j;
+              t_dep[j] = gtimer();
+            }
+          }
+          if (dep_job >= j) {
+            const int st = nx % STAGES;
+            tma_load_2d(sB + st * B_BYTES, &a.xmap[j], cx.kb * kBK, 0, &full[st]);
+            cur_adv(a, cx, cta, NP);
+            ++nx;
+            prog = true;
+          }
+        }
+        if (!prog) __nanosleep(32);
+      }
+      if (!waited) pdl_wait();
+      trace_phase(TK_PHASE | TK_CHAIN | (1u << 8), t_dep[0], t_dep[1], t_dep[2], t_dep[3]);
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = umma_idesc(128, BN);
+      int n = 0, seg = 0;
+      unsigned long long t_mma[kChainMaxJobs] = {0, 0, 0, 0};  // trace: last MMA of job j issued
+      for (int j = 0; j < a.n_jobs; ++j) {
+        const GemmArgs& g = a.job[j];
+        const int kbt = g.kb_total;
+        const long long I = (long long)g.m_tiles * kbt;
+        const int qa = q0(I, cta, NP), qb = q0(I, cta + 1, NP);
+        for (int q = qa; q < qb;) {
+          const int t = q / kbt;
+          const int lo = q - t * kbt, hi = min(qb - t * kbt, kbt);
+          const int buf = seg & 1;
+          if (seg >= 2) mbar_wait(&tempty[buf], (uint32_t)(((seg >> 1) - 1) & 1));
+          tc_fence_after();
+          const uint32_t acc = tmem + (uint32_t)(buf * BN);
+          for (int kb = lo; kb < hi; ++kb, ++n) {
+            const int st = n % STAGES;
+            mbar_wait(&full[st], (uint32_t)((n / STAGES) & 1));
+            tc_fence_after();
+            const uint32_t a0 = smem_u32(sA + st * A_BYTES);
+            const uint32_t b0 = smem_u32(sB + st * B_BYTES);
+#pragma unroll
+            for (int k = 0; k < kBK / 16; ++k)
+              umma_f16(acc, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
+                       (kb > lo || k > 0) ? 1u : 0u);
+            umma_commit(&empty[st]);
+          }
+          umma_commit(&tfull[buf]);
+          ++seg;
+          q = t * kbt + hi;
+        }
+        t_mma[j] = gtimer();
+      }
+      trace_phase(TK_PHASE | TK_CHAIN | (2u << 8), t_mma[0], t_mma[1], t_mma[2], t_mma[3]);
+    }
+    __syncwarp();
+  } else {
+    pdl_wait();
+    const int et = (warp & 3) * 32 + lane;
+    const uint32_t tb = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+    int seg = 0, meta_job = -1;
+    uint32_t fx_phase[2] = {0u, 0u};
+    unsigned long long fx_t0 = 0, fx_t1 = 0, t_seg0 = 0;  // trace marks (thread et == 0)
+    unsigned long long t_epi[kChainMaxJobs] = {0, 0, 0, 0};  // trace: this CTA done with job j
+    for (int j = 0; j < a.n_jobs; ++j) {
+      const GemmArgs& g = a.job[j];
+      const int kbt = g.kb_total;
+      const long long I = (long long)g.m_tiles * kbt;
+      const int qa = q0(I, cta, NP), qb = q0(I, cta + 1, NP);
+      if (j > 0 && et == 0) t_epi[j - 1] = gtimer();
+      for (int q = qa; q < qb;) {
+        const int t = q / kbt;
+        const int hi = min(qb - t * kbt, kbt);
+        const int buf = seg & 1;
+        const int c_first = owner((long long)t * kbt, I, NP), c_last = owner((long long)(t + 1) * kbt - 1, I, NP);
+        const int nc = c_last - c_first + 1;
+        mbar_wait(&tfull[buf], (uint32_t)((seg >> 1) & 1));
+        tc_fence_after();
+        if (et == 0) t_seg0 = gtimer();
+        epi_bar();  // the previous segment's epilogue is done with P / sm
+        TileSrc ts{P, nullptr, 0u, 1, 0, BN, 0, 0, nullptr};
+        bool run = true;
+        // this job's inputs written by earlier jobs (RMSNorm sums, residual) + column metadata
+        auto job_meta = [&]() {
+          if (meta_job == j) return;
+          for (int i = 0; i < j; ++i)
+            while (!chain::done_reached(a.done + i, a.done_target[i])) __nanosleep(64);
+          switch (g.mode) {
+            case EPI_RESID: column_meta<EPI_RESID>(g, sm, t, 0, 0, BN, et); break;
+            case EPI_SWIGLU: column_meta<EPI_SWIGLU>(g, sm, t, 0, 0, BN, et); break;
+            case EPI_QKV: column_meta<EPI_QKV>(g, sm, t, 0, 0, BN, et); break;
+            default: break;
+          }
+          meta_job = j;
+        };
+        float in[BN];
+        if (nc == 1) {
+          job_meta();
+          chain_inputs_load(g, sm, t, et, in);
+#pragma unroll 1
+          for (int c0 = 0; c0 < BN; c0 += 16) {
+            float v[16];
+            tmem_ld16(tb + (uint32_t)(buf * BN + c0), v);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) P[(c0 + i) * 128 + et] = v[i];
+          }
+          tc_fence_before();
+          epi_bar();
+          if (et == 0) mbar_arrive(&tempty[buf]);
+        } else {
+          float* wsl = a.ws[j] + (size_t)t * a.ws_slots[j] * (BN * 128);
+#pragma unroll 1
+          for (int c0 = 0; c0 < BN; c0 += 16) {
+            float v[16];
+            tmem_ld16(tb + (uint32_t)(buf * BN + c0), v);
+#pragma unroll
+            for (int i = 0; i < 16; ++i) __stcg(wsl + ((size_t)(cta - c_first) * BN + c0 + i) * 128 + et, v[i]);
+          }
+          tc_fence_before();
+          __threadfence();
+          epi_bar();
+          if (et == 0) {
+            mbar_arrive(&tempty[buf]);
+            const unsigned old = atomicAdd(a.tile_cnt[j] + t, 1u);
+            *s_last = (old == (unsigned)(nc - 1)) ? 1 : 0;
+          }
+          epi_bar();
+          run = *s_last != 0;
+          if (run) {
+            // last contributor: sum the nc partials in slot order (deterministic) with
+            // double-buffered 32 KB bulk loads (TMA engine: latency-bound per-thread L2
+            // loads measured ~4 GB/s per SM under the weight stream), into P, while the
+            // epilogue inputs load into registers
+            __threadfence();
+            if (et == 0) {
+              a.tile_cnt[j][t] = 0u;  // self-reset for the next launch
+              asm volatile("fence.proxy.async.global;" ::: "memory");
+              fx_t0 = gtimer();
+            }
+            job_meta();
+            chain_inputs_load(g, sm, t, et, in);
+            float acc[BN];
+#pragma unroll
+            for (int c = 0; c < BN; ++c) acc[c] = 0.f;
+            for (int sl = 0; sl < nc; sl += 2) {
+              if (et == 0)
+                for (int b = 0; b < 2 && sl + b < nc; ++b) {
+                  mbar_arrive_expect_tx(&fxbar[b], P_BYTES);
+                  bulk_g2s(b ? (void*)Q : (void*)P, wsl + (size_t)(sl + b) * BN * 128, P_BYTES, &fxbar[b]);
+                }
+              for (int b = 0; b < 2 && sl + b < nc; ++b) {
+                mbar_wait(&fxbar[b], fx_phase[b]);
+                fx_phase[b] ^= 1u;
+                const float* buf2 = b ? Q : P;
+#pragma unroll
+                for (int c = 0; c < BN; ++c) acc[c] += buf2[c * 128 + et];
+              }
+              epi_bar();  // P / Q free for the next loads
+            }
+#pragma unroll
+            for (int c = 0; c < BN; ++c) P[c * 128 + et] = acc[c];
+            if (et == 0) fx_t1 = gtimer();
+          }
+        }
+        if (run) {
+          chain_inputs_park(g, sm, et, in);
+          epi_bar();
+          switch (g.mode) {
+            case EPI_RESID: chain_epilogue<EPI_RESID>(g, sm, ts, t, et); break;
+            case EPI_SWIGLU: chain_epilogue<EPI_SWIGLU>(g, sm, ts, t, et); break;
+            case EPI_QKV: chain_epilogue<EPI_QKV>(g, sm, ts, t, et); break;
+            default: break;
+          }
+          __threadfence();
+          epi_bar();
+          if (et == 0) {
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.done + j) : "memory");
+            trace_phase(TK_PHASE | TK_CHAIN | (4u << 8), fx_t0 ? fx_t0 : t_seg0, fx_t1 ? fx_t1 : t_seg0, gtimer(),
+                        ((unsigned long long)j << 32) | (unsigned)nc);
+            fx_t0 = fx_t1 = 0;
+          }
+        }
+        ++seg;
+        q = t * kbt + hi;
+      }
+    }
+    if (et == 0) {
+      t_epi[a.n_jobs - 1] = gtimer();
+      trace_phase(TK_PHASE | TK_CHAIN | (3u << 8), t_epi[0], t_epi[1], t_epi[2], t_epi[3]);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
   }
 }
 
@@ -867,6 +1307,57 @@ cudaError_t launch_gemm_epi(const bf16* w_tiled, const GemmTmaSet& x, GemmArgs g
     case EPI_SWIGLU: return launch_mode<EPI_SWIGLU>(x, g, bn, splits, s);
     default: return cudaErrorInvalidValue;
   }
+}
+
+
+// ------------------------------------------------------------ chain host side
+int chain_grid(const int* M, const int* K, int n_jobs) {
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  long long g = sms;
+  for (int j = 0; j < n_jobs; ++j) g = std::min(g, (long long)((M[j] + 127) / 128) * (K[j] / kBK));
+  return (int)std::max(1LL, g);
+}
+int chain_slots(int M, int K, int ctas) {
+  const int T = (M + 127) / 128, kb = K / kBK;
+  const long long I = (long long)T * kb;
+  int best = 1;
+  for (int t = 0; t < T; ++t)
+    best = std::max(best, chain::owner((long long)(t + 1) * kb - 1, I, ctas) - chain::owner((long long)t * kb, I, ctas) + 1);
+  return best;
+}
+cudaError_t launch_chain(ChainArgs& a, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, chain::SMEM);
+    attr = true;
+  }
+  for (int j = 0; j < a.n_jobs; ++j) {
+    GemmArgs& g = a.job[j];
+    if (g.N > chain::BN || g.K % kBK || (long long)((g.M + 127) / 128) * (g.K / kBK) < a.grid)
+      return cudaErrorInvalidValue;
+    g.kb_total = g.K / kBK;
+    g.m_tiles = (g.M + 127) / 128;
+    g.l2_evict_first = l2_hint_enabled() ? 1 : 0;
+    g.pf_w = nullptr;
+  }
+  cudaLaunchConfig_t cfg{};
+  if (a.grid < 1) return cudaErrorInvalidValue;
+  cfg.gridDim = dim3(a.grid);
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = chain::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_chain, (const ChainArgs)a);
 }
 
 RT_TRACE_BINDER(trace_bind_gemm)

@@ -130,6 +130,33 @@ int gemm_choose_splits(int M, int N, int K);   // cluster split-K factor (1..16)
 // splits <= 0: gemm_choose_splits
 cudaError_t launch_gemm_epi(const bf16* w_tiled, const GemmTmaSet& xmaps, GemmArgs g, int splits, cudaStream_t s);
 
+// ---- persistent projection chain (gemm_tc.cu): up to 4 dependent decode
+// projections (O + residual, gate/up + SwiGLU, down + residual, next layer's QKV + RoPE +
+// KV append) in ONE launch of one CTA per SM.  Every job's k-block iterations (m-tile x
+// k-block, N <= 64 rows in one 64-wide tile) are split evenly over the CTAs (stream-K);
+// weight tiles stream ahead across job boundaries (they do not depend on activations),
+// only the activation (X) loads of job j wait for job j - 1 to finish.  Partial tiles
+// go to a global workspace; the last contributor of a tile sums them in fixed order and
+// runs the fused epilogue.
+constexpr int kChainMaxJobs = 4;
+struct ChainArgs {
+  GemmArgs job[kChainMaxJobs];   // as launch_gemm_epi (w, M, N <= 64, K, mode, epilogue fields)
+  TmaMap xmap[kChainMaxJobs];    // activation operand of each job (box 64 x 64)
+  float* ws[kChainMaxJobs];      // partial tiles [m_tiles][ws_slots][64][128] fp32
+  int ws_slots[kChainMaxJobs];
+  unsigned* tile_cnt[kChainMaxJobs];  // [m_tiles] zero-initialised, self-resetting
+  unsigned* done;                // [kChainMaxJobs] cumulative finished tiles (never reset)
+  unsigned done_target[kChainMaxJobs];  // done[j] value when job j of THIS launch is complete
+  int n_jobs;
+  int grid;                      // CTAs: <= SM count and <= every job's k-block iterations
+  int pf_ahead;                  // weight k-blocks prefetched into L2 beyond the smem ring
+};
+// max contributors of one m-tile of an (M, K) job over `ctas` CTAs (the ws_slots to allocate)
+int chain_slots(int M, int K, int ctas);
+// CTAs of a chain over jobs (M[j], K[j]): min(SM count, every job's m-tile x k-block count)
+int chain_grid(const int* M, const int* K, int n_jobs);
+cudaError_t launch_chain(ChainArgs& a, cudaStream_t s);
+
 // ---- device trace buffers (common.cuh TraceScope), one binder per translation unit
 void trace_bind_model(void* rec, unsigned* n, unsigned cap);
 void trace_bind_attn(void* rec, unsigned* n, unsigned cap);

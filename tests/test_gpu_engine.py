@@ -175,8 +175,15 @@ def test_submit_errors(rt):
 
 
 # ------------------------------------------------------------- model parity
-@pytest.mark.parametrize("graphs", [False, True])
-def test_tiny_model_e2e_and_per_op(rt, graphs):
+@pytest.mark.parametrize("graphs,chain", [(False, False), (True, False), (False, True)])
+def test_tiny_model_e2e_and_per_op(rt, graphs, chain, monkeypatch):
+    """C1 end to end against the oracle; chain=True runs the decode projections through the
+    opt-in persistent projection chain (RT_CHAIN=1; 2 CTAs at these dims, so both the
+    whole-tile and the partial-tile fixup paths run)."""
+    if chain:
+        monkeypatch.setenv("RT_CHAIN", "1")
+    else:
+        monkeypatch.delenv("RT_CHAIN", raising=False)
     shape = MODEL_SHAPES["tiny"]
     v = make_vocab(shape.vocab)
     p = engine_params("paper-4090", max_batch=4, max_tasks=64, max_ctx=256, n_pages=64)
@@ -472,3 +479,47 @@ def test_tiny_model_shared_prefix_parity(rt):
     assert worst_attn < 6e-3, worst_attn
     assert worst_logit < 1e-2, worst_logit
     assert eng.poll() == ora.poll()
+
+
+def test_projection_chain_matches_per_projection_launches(rt, monkeypatch):
+    """The opt-in persistent projection chain (RT_CHAIN=1: O, gate/up, down, next QKV in one
+    launch, stream-K split with a global partial-tile fixup) against one launch per projection, at 8B layer
+    dims (2 layers, 64 decode rows): same scripted rounds, logits and the layer-1 q (produced
+    by layer 0's chain) agree to fp32 summation-order / bf16 rounding-flip level; the tiny C1
+    model's end-to-end oracle parity (test_tiny_model_e2e_and_per_op[chain]) runs through the
+    chain too (grid = min(SMs, iterations) = 2 CTAs there)."""
+    from synth.configs import ModelShape
+    s8 = MODEL_SHAPES["llama3-8b"]
+    shape = ModelShape("chain", 2, s8.d_model, s8.n_q_heads, s8.n_kv_heads, s8.head_dim, s8.d_ff, s8.vocab)
+    v = make_vocab(shape.vocab)
+    p = engine_params("b200-roofline", max_batch=64, max_tasks=128, max_ctx=256, n_pages=64 * 16)
+    from synth.traces import make_trace
+    out = {}
+    for mode in ("chain", "per_projection"):
+        if mode == "chain":
+            monkeypatch.setenv("RT_CHAIN", "1")
+        else:
+            monkeypatch.delenv("RT_CHAIN", raising=False)
+        eng = rt.Engine(shape, p, v, seed=21, flags=rt.RT_FLAG_KEEP_LOGITS | rt.RT_FLAG_CAPTURE, capture_layer=1,
+                        max_rows_per_forward=4096)
+        for a in range(64):
+            tr = make_trace(1 + a % 8, v, seed=a, prompt_len=40 + a % 17, plan_len=40)
+            eng.submit(a, tr.prompt, 0, tr.ert_us, tr.alpha, tr.beta, 90000, script=tr.plan)
+        logs = []
+        for _ in range(12):
+            info = eng.step()
+            if info["n_running"] == 64 and info["n_prefill_rows"] == 0:
+                lg = eng.dump(rt.RT_DUMP_LOGITS, np.float32).reshape(64, -1)
+                rows = eng.dump(rt.RT_DUMP_ROWS, np.int32).reshape(-1, 3)
+                q = eng.dump(rt.RT_DUMP_CAPTURE_Q, np.float32).reshape(len(rows), -1)
+                logs.append((lg.copy(), q.copy()))
+        out[mode] = (logs, eng.poll())
+        eng.close()
+    (lc, sc), (lp, sp) = out["chain"], out["per_projection"]
+    assert sc == sp  # scripted streams: identical segments
+    assert len(lc) == len(lp) and len(lc) >= 3
+    worst_l = max(float(np.abs(a[0] - b[0]).max()) for a, b in zip(lc, lp))
+    worst_q = max(float(np.abs(a[1] - b[1]).max()) for a, b in zip(lc, lp))
+    scale = max(float(np.abs(b[0]).max()) for b in lp)
+    assert worst_q < 5e-2, worst_q          # q of layer 1 (bf16, |q| ~ O(1))
+    assert worst_l < 2e-2 * max(1.0, scale), (worst_l, scale)
