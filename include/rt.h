@@ -44,6 +44,18 @@ enum { RT_CLOCK_VIRTUAL = 0, RT_CLOCK_WALL = 1 };
 enum { RT_POLICY_PUD = 0, RT_POLICY_FCFS = 1, RT_POLICY_EDF = 2 };
 /* Stop reasons, in priority order EOS > MAXNEW > SKILL_WINDOW > CAP (DESIGN.md a9). */
 enum { RT_STOP_NONE = 0, RT_STOP_EOS = 1, RT_STOP_MAXNEW = 2, RT_STOP_SKILL = 3, RT_STOP_CAP = 4 };
+/* Segmentation modes (rt_config.seg_mode, the paper's comparison systems,
+ * PAPER.md:576-584, 657-661):
+ *   RT_SEG_SUSPEND  the method: a segment ends at the stop checker's boundary, the request
+ *                   is suspended (KV retained) and re-enters the priority queue
+ *   RT_SEG_STREAM   "vLLM-stream": a segment record is delivered at every skill boundary
+ *                   (window rule) but the request keeps decoding in its slot (no suspension,
+ *                   no CAP boundary)
+ *   RT_SEG_NONE     "vLLM": no segmentation, one record at EOS / max_new_tokens
+ * In STREAM / NONE modes a delivered segment is at most RT_SEG_MAX_TOKENS tokens (a longer
+ * run is cut there with reason RT_STOP_CAP). */
+enum { RT_SEG_SUSPEND = 0, RT_SEG_STREAM = 1, RT_SEG_NONE = 2 };
+#define RT_SEG_MAX_TOKENS 128
 /* rt_config.flags */
 enum {
   RT_FLAG_NO_MODEL = 1,     /* scheduling-only engine: scripted tokens, no forward pass */
@@ -96,6 +108,8 @@ typedef struct {
   int32_t eos_id;
   int32_t flags;                    /* RT_FLAG_* */
   int32_t capture_layer;
+  int32_t seg_mode;                 /* RT_SEG_* (0 = the method) */
+  int32_t wcet_off;                 /* 1: no WCET admission gate (the baselines) */
 } rt_config;
 
 typedef struct {
@@ -103,7 +117,7 @@ typedef struct {
   int32_t agent_id, k, tok_begin, tok_end, n_skills, reason;
   int64_t est_exec_us;              /* sum of E_min over the segment's skills */
   int64_t dispatch_us;              /* clock at the end of the producing round */
-  int32_t tokens[16];               /* tok_end - tok_begin <= max_seg_tokens valid */
+  int32_t tokens[RT_SEG_MAX_TOKENS]; /* the first tok_end - tok_begin are valid */
 } rt_segment;
 
 typedef struct {

@@ -10,16 +10,18 @@ TUF_0 at the actual response time.
 c5: action_start_k = max(dispatch_k + net, action_end_{k-1})  (fig:con_infer
 caption PAPER.md:217: network hidden when overlapped; 8 ms).
 Realized duration of a skill = choice from its profiled alternatives by
-splitmix64(seed ^ (request_id << 32) ^ (k << 16) ^ skill_idx) mod n
-("randomly sample from this profiled data"; reading AMB-18).
+splitmix64(seed ^ (request_id << 32) ^ ordinal) mod n, ordinal = the skill's index in the
+request's whole response ("randomly sample from this profiled data"; reading
+AMB-18) — independent of where segment boundaries fall, so the same trace served by
+different systems executes the same actions.
 """
 from .tuf import tuf0
 from .weights import splitmix64_int, M64
 
 
-def realized_us(vocab, seed, request_id, k, skill_idx, tok):
+def realized_us(vocab, seed, request_id, ordinal, tok):
     alts = vocab.realized[tok]
-    h = splitmix64_int((seed ^ (request_id << 32) ^ (k << 16) ^ skill_idx) & M64)
+    h = splitmix64_int((seed ^ (request_id << 32) ^ ordinal) & M64)
     return int(alts[h % len(alts)])
 
 
@@ -27,13 +29,13 @@ def simulate_request(segments, arrival_us, vocab, net_us, seed, request_id):
     """segments: this request's records in k order -> per-segment (start, end, W, E)."""
     out = []
     prev_end = None
+    ordinal = 0
     for s in sorted(segments, key=lambda s: s["k"]):
         E = 0
-        si = 0
         for tok in s["tokens"]:
             if vocab.tok_skill[tok] >= 0:
-                E += realized_us(vocab, seed, request_id, s["k"], si, tok)
-                si += 1
+                E += realized_us(vocab, seed, request_id, ordinal, tok)
+                ordinal += 1
         start = s["dispatch_us"] + net_us
         if prev_end is not None:
             start = max(start, prev_end)

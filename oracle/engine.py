@@ -30,6 +30,13 @@ from .priority import priority
 from . import model as M
 
 STOP_NONE, STOP_EOS, STOP_MAXNEW, STOP_SKILL, STOP_CAP = 0, 1, 2, 3, 4
+# Segmentation modes (the paper's comparison systems, PAPER.md:576-584,
+# 657-661): SUSPEND = the method (segment ends, request suspended and re-queued,
+# PAPER.md:180); STREAM = "vLLM-stream" (a segment is delivered at each skill boundary but
+# the generation continues uninterrupted); NONE = "vLLM" (whole response delivered at the
+# end).  Delivered segments are cut at SEG_MAX_TOKENS in STREAM / NONE.
+SEG_SUSPEND, SEG_STREAM, SEG_NONE = 0, 1, 2
+SEG_MAX_TOKENS = 128
 PENDING, WAITING, RUNNING, FINISHED = 0, 1, 2, 3
 POLICY_PUD, POLICY_FCFS, POLICY_EDF = 0, 1, 2
 CLOCK_VIRTUAL, CLOCK_WALL = 0, 1
@@ -213,7 +220,7 @@ class OracleEngine:
         S = sum(self.hist[len(self.hist) - n:]) if n else 0
         gate_ok = True
         cands = [g for g in running if g.D - t >= 0]
-        if cands and n > 0:
+        if cands and n > 0 and not getattr(p, "wcet_off", 0):
             g = min(cands, key=lambda g: (g.D - t, g.id))
             gate_ok = wcet_gate_pass(p.max_seg_tokens, g.seg_tok, S, n, g.D - t)
 
@@ -317,13 +324,15 @@ class OracleEngine:
             if sk >= 0:
                 r.seg_exec += self.tok_e[tok]
                 r.seg_nsk += 1
+            mode = getattr(p, "seg_mode", SEG_SUSPEND)
+            cap = p.max_seg_tokens if mode == SEG_SUSPEND else SEG_MAX_TOKENS
             if tok == self.eos:
                 reason = STOP_EOS
             elif r.n_gen == r.max_new:
                 reason = STOP_MAXNEW
-            elif sk >= 0 and r.seg_exec >= r.window:
+            elif mode != SEG_NONE and sk >= 0 and r.seg_exec >= r.window:
                 reason = STOP_SKILL
-            elif r.seg_tok == p.max_seg_tokens:
+            elif r.seg_tok == cap:
                 reason = STOP_CAP
             else:
                 reason = STOP_NONE
@@ -342,6 +351,11 @@ class OracleEngine:
                 dispatch_us=dispatch, tokens=list(r.out[r.n_gen - r.seg_tok:r.n_gen])))
             if reason in (STOP_EOS, STOP_MAXNEW):
                 finished.append(r)
+            elif getattr(p, "seg_mode", SEG_SUSPEND) != SEG_SUSPEND:
+                # STREAM / NONE cut: delivered, the generation goes on in its slot
+                r.k += 1
+                r.seg_tok = r.seg_exec = r.seg_nsk = 0
+                stopped_ids.discard(rid)
             else:
                 base = dispatch + p.net_us
                 if r.end_est is not None:

@@ -91,7 +91,7 @@ struct rt_engine {
   HostMailbox* d_mb = nullptr;
   SegRec* h_ring = nullptr;
   SegRec* d_ring = nullptr;
-  int64_t ring_cap = 65536;
+  int64_t ring_cap = 32768;
   SchedParams sp{};
   // activations
   float *d_x = nullptr, *d_part = nullptr, *d_attn_ws = nullptr, *d_logits = nullptr, *d_am_val = nullptr;
@@ -203,6 +203,8 @@ static rt_status validate(const rt_config* c) {
   if (c->speed_window < 1 || c->speed_window > 8) return RT_E_INVAL;
   if (c->g_us <= 0 || c->eps_l_us <= 0 || c->net_us < 0) return RT_E_INVAL;
   if (c->policy < 0 || c->policy > 2 || c->clock_mode < 0 || c->clock_mode > 1) return RT_E_INVAL;
+  if (c->seg_mode < RT_SEG_SUSPEND || c->seg_mode > RT_SEG_NONE || c->wcet_off < 0 || c->wcet_off > 1)
+    return RT_E_INVAL;
   if (c->vocab < 2 || !c->tok_skill || !c->tok_exec_min_us) return RT_E_INVAL;
   if (c->eos_id < 0 || c->eos_id >= c->vocab) return RT_E_INVAL;
   if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return RT_E_INVAL;
@@ -363,6 +365,8 @@ static rt_status create_impl(rt_engine* e, const rt_config* cfg) {
   P.speed_window = c.speed_window;
   P.max_admit = e->cfg.max_admit_per_round;
   P.policy = c.policy;
+  P.seg_mode = c.seg_mode;
+  P.wcet_off = c.wcet_off;
   P.clock_mode = c.clock_mode;
   P.base_us = c.base_us;
   P.gamma_ppm = c.gamma_ppm;

@@ -2,6 +2,7 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include "rt.h"
 
 namespace rt {
 
@@ -67,7 +68,7 @@ struct SegRec {  // identical layout to rt_segment
   int32_t agent_id, k, tok_begin, tok_end, n_skills, reason;
   int64_t est_exec_us;
   int64_t dispatch_us;
-  int32_t tokens[16];
+  int32_t tokens[RT_SEG_MAX_TOKENS];
 };
 
 struct SchedParams {
@@ -100,6 +101,7 @@ struct SchedParams {
   int32_t max_seg_tokens, g_us, net_us, eps_l_us, speed_window, max_admit, policy, clock_mode;
   int32_t base_us, gamma_ppm, kv_us_per_1k, prefill_us_per_tok;
   int32_t eos_id, rank, world, no_model;
+  int32_t seg_mode, wcet_off;  // RT_SEG_*, WCET gate disabled (baselines)
 };
 
 // launchers (sched.cu)

@@ -383,7 +383,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
     if (tid == 0) {
       int gate = 1;
       const int nh = min(p.speed_window, st->hist_n);
-      if (best_bud != LLONG_MAX && nh > 0) {
+      if (best_bud != LLONG_MAX && nh > 0 && !p.wcet_off) {
         long long sum = 0;
         for (int j = 1; j <= nh; ++j) sum += st->hist[(st->hist_pos - j + 8) & 7];
         const long long rem = max(0, p.max_seg_tokens - best_seg);
@@ -643,11 +643,16 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_post(SchedParams p) 
       sx += p.tok_exec[tok];
       ++nsk;
     }
+    // EOS > MAXNEW > SKILL_WINDOW > CAP; STREAM: no CAP below RT_SEG_MAX_TOKENS; NONE: no
+    // skill boundary either (the comparison systems, rt.h RT_SEG_*)
+    const int cap = p.seg_mode == RT_SEG_SUSPEND ? p.max_seg_tokens : RT_SEG_MAX_TOKENS;
     int reason = 0;
     if (tok == p.eos_id) reason = 1;
     else if (ng == T.max_new[task]) reason = 2;
-    else if (sk >= 0 && sx >= (int64_t)T.window[task]) reason = 3;
-    else if (segt == p.max_seg_tokens) reason = 4;
+    else if (p.seg_mode != RT_SEG_NONE && sk >= 0 && sx >= (int64_t)T.window[task]) reason = 3;
+    else if (segt == cap) reason = 4;
+    // STREAM: a delivered segment does not suspend the request (it keeps its slot)
+    const bool keep = reason == 0 || (p.seg_mode != RT_SEG_SUSPEND && (reason == 3 || reason == 4));
     T.n_gen[task] = ng;
     T.seg_tok[task] = segt;
     T.seg_exec[task] = sx;
@@ -655,7 +660,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_post(SchedParams p) 
     p.slot_tok[s] = tok;
     S.reason[s] = reason;
     S.stop_off[s] = reason != 0;
-    S.keep_off[s] = reason == 0;
+    S.keep_off[s] = keep;
     S.keep_task[s] = task;
   }
   __syncthreads();
@@ -667,10 +672,9 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_post(SchedParams p) 
   for (int s = tid; s < B; s += nt) {
     const int task = S.keep_task[s];
     const int reason = S.reason[s];
-    if (reason == 0) {
-      p.slot_task[S.keep_off[s]] = task;  // stable compaction (reads use keep_task copy)
-      continue;
-    }
+    const bool keep = reason == 0 || (p.seg_mode != RT_SEG_SUSPEND && (reason == 3 || reason == 4));
+    if (keep) p.slot_task[S.keep_off[s]] = task;  // stable compaction (reads use keep_task copy)
+    if (reason == 0) continue;
     const int ng = T.n_gen[task], segt = T.seg_tok[task];
     const int64_t idx = seg_base + S.stop_off[s];
     SegRec* r = p.seg_ring + (idx % p.seg_ring_cap);
@@ -684,12 +688,17 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_post(SchedParams p) 
     r->est_exec_us = T.seg_exec[task];
     r->dispatch_us = dispatch;
     const int32_t* o = T.out + (size_t)task * p.max_ctx;
-    for (int j = 0; j < 16; ++j) r->tokens[j] = (j < segt) ? o[ng - segt + j] : -1;
+    for (int j = 0; j < segt; ++j) r->tokens[j] = o[ng - segt + j];
     if (reason == 1 || reason == 2) {  // finish: free pages + reservation
       T.state[task] = T_FINISHED;
       T.holder[task] = 0;
       const int f = atomicAdd(&s_nfin, 1);
       S.fin[f] = task;
+    } else if (keep) {  // STREAM / NONE cut: the request keeps decoding; next segment index
+      T.k[task] = T.k[task] + 1;
+      T.seg_tok[task] = 0;
+      T.seg_exec[task] = 0;
+      T.n_skills[task] = 0;
     } else {  // suspend: completion estimate of the dispatched segment
       int64_t b = dispatch + (int64_t)p.net_us;
       const int64_t prev = T.end_est[task];

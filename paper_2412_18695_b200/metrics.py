@@ -5,8 +5,9 @@ response time W(s_0) = first action start - arrival; robot waiting time
 sum_k W(s_k); completion C = sum_k (W(s_k) + E(s_k)); time utility = Eq. 1 at
 the response time.  Agents are simulated in virtual time: action k starts at
 max(dispatch_k + net, end of action k-1) (fig:con_infer) and lasts
-the sum of its skills' realized durations, sampled per (request, k, skill) by
-splitmix64(seed ^ (rid << 32) ^ (k << 16) ^ skill_idx) (PAPER.md:495).
+the sum of its skills' realized durations, sampled per (request, skill ordinal in the
+whole response) by splitmix64(seed ^ (rid << 32) ^ ordinal) — independent
+of segment boundaries, so every serving mode (rt.h RT_SEG_*) executes the same actions.
 """
 M64 = (1 << 64) - 1
 
@@ -37,14 +38,14 @@ def report(segments, requests, vocab, net_us=8000, seed=0):
         prev_end = None
         waits = []
         e_tot = 0
+        ordinal = 0
         for s in sorted(segs, key=lambda s: s["k"]):
             e = 0
-            si = 0
             for tok in s["tokens"]:
                 if vocab.tok_skill[tok] >= 0:
                     alts = vocab.realized[tok]
-                    e += alts[_mix((seed ^ (rid << 32) ^ (s["k"] << 16) ^ si) & M64) % len(alts)]
-                    si += 1
+                    e += alts[_mix((seed ^ (rid << 32) ^ ordinal) & M64) % len(alts)]
+                    ordinal += 1
             start = s["dispatch_us"] + net_us if prev_end is None else max(s["dispatch_us"] + net_us, prev_end)
             waits.append(start - (req["arrival_us"] if prev_end is None else prev_end))
             prev_end = start + e
@@ -59,5 +60,8 @@ def report(segments, requests, vocab, net_us=8000, seed=0):
                        response_s=sum(m["response_us"] for m in v) / len(v) / 1e6,
                        waiting_s=sum(m["waiting_us"] for m in v) / len(v) / 1e6) for c, v in out.items()}
     total = sum(m["utility"] for m in per)
-    return dict(by_class=summary, n=len(per), total_utility=total,
-                mean_utility=(total / len(per)) if per else None)
+    n = len(per)
+    return dict(by_class=summary, n=n, total_utility=total,
+                mean_utility=(total / n) if per else None,
+                mean_response_s=(sum(m["response_us"] for m in per) / n / 1e6) if per else None,
+                mean_waiting_s=(sum(m["waiting_us"] for m in per) / n / 1e6) if per else None)

@@ -40,6 +40,10 @@ class RtError(RuntimeError):
         self.code = code
 
 
+RT_SEG_SUSPEND, RT_SEG_STREAM, RT_SEG_NONE = 0, 1, 2   # rt.h segmentation modes
+RT_SEG_MAX_TOKENS = 128
+
+
 class rt_utility(C.Structure):
     _fields_ = [("alpha", C.c_double), ("beta", C.c_double)]
 
@@ -57,7 +61,7 @@ class rt_config(C.Structure):
         ("clock_mode", C.c_int32), ("base_us", C.c_int32), ("gamma_ppm", C.c_int32),
         ("kv_us_per_1k", C.c_int32), ("prefill_us_per_tok", C.c_int32), ("t0_us", C.c_int64),
         ("tok_skill", C.c_void_p), ("tok_exec_min_us", C.c_void_p), ("eos_id", C.c_int32),
-        ("flags", C.c_int32), ("capture_layer", C.c_int32),
+        ("flags", C.c_int32), ("capture_layer", C.c_int32), ("seg_mode", C.c_int32), ("wcet_off", C.c_int32),
     ]
 
 
@@ -65,7 +69,7 @@ class rt_segment(C.Structure):
     _fields_ = [("request_id", C.c_int64), ("agent_id", C.c_int32), ("k", C.c_int32),
                 ("tok_begin", C.c_int32), ("tok_end", C.c_int32), ("n_skills", C.c_int32),
                 ("reason", C.c_int32), ("est_exec_us", C.c_int64), ("dispatch_us", C.c_int64),
-                ("tokens", C.c_int32 * 16)]
+                ("tokens", C.c_int32 * RT_SEG_MAX_TOKENS)]
 
 
 class rt_round_info(C.Structure):
@@ -173,6 +177,7 @@ class Engine:
         c.tok_exec_min_us = self._exec.ctypes.data
         c.eos_id = vocab.eos_id
         c.flags, c.capture_layer = flags, capture_layer
+        c.seg_mode, c.wcet_off = p.seg_mode, p.wcet_off
         self.cfg = c
         self.shape, self.params, self.vocab = shape, params, vocab
         h = C.c_void_p()

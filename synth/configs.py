@@ -70,6 +70,7 @@ CLOCK_PRESETS = {
 
 POLICY_PUD, POLICY_FCFS, POLICY_EDF = 0, 1, 2
 CLOCK_VIRTUAL, CLOCK_WALL = 0, 1
+SEG_SUSPEND, SEG_STREAM, SEG_NONE = 0, 1, 2   # rt.h RT_SEG_*
 
 
 @dataclass
@@ -92,6 +93,8 @@ class EngineParams:
     kv_us_per_1k: int = 0
     prefill_us_per_tok: int = 114
     t0_us: int = 0
+    seg_mode: int = SEG_SUSPEND     # the method; STREAM / NONE = the comparison systems
+    wcet_off: int = 0               # 1: no WCET admission gate (the baselines)
     extra: dict = field(default_factory=dict)
 
     def as_dict(self):

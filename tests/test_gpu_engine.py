@@ -20,7 +20,7 @@ from oracle.model import OracleModel, paged_attention     # noqa: E402
 from oracle import weights as OW                          # noqa: E402
 from oracle.bf16 import bf16                              # noqa: E402
 from synth import MODEL_SHAPES, make_vocab, engine_params, compose_workload  # noqa: E402
-from synth.configs import POLICY_FCFS, POLICY_EDF, CLOCK_WALL  # noqa: E402
+from synth.configs import POLICY_FCFS, POLICY_EDF, CLOCK_WALL, SEG_STREAM, SEG_NONE  # noqa: E402
 
 
 @pytest.fixture(scope="module")
@@ -101,6 +101,26 @@ def test_sched_parity_contention(rt, policy, max_admit):
     submit_both(eng, ora, reqs)
     n, segs = lockstep(eng, ora, max_rounds=20000, check_every=3)
     assert any(r["n_refused_mem"] > 0 for r in ora.round_log)
+
+
+@pytest.mark.parametrize("policy,seg_mode", [(POLICY_FCFS, SEG_NONE), (POLICY_FCFS, SEG_STREAM),
+                                             (0, SEG_STREAM), (POLICY_EDF, SEG_NONE)])
+def test_sched_parity_comparison_systems(rt, policy, seg_mode):
+    """SURVEY NEXT-3 on the device scheduler: vLLM (FCFS, no segmentation), vLLM-stream
+    (segments delivered, generation never suspended), both without the WCET gate, bit-exact
+    against the oracle every round on a contended trace (memory refusals, arm plans > 16
+    tokens so NONE-mode records exceed the method's 10-token cap)."""
+    v = make_vocab(512)
+    p = engine_params("paper-4090", max_batch=16, max_tasks=1024, max_ctx=256, n_pages=96, policy=policy,
+                      seg_mode=seg_mode, wcet_off=1)
+    reqs = compose_workload(64, 8.0, 16, range(1, 12), 6.0, 7, v, prompt_len_range=(20, 120), max_requests=400)
+    eng, ora = make_pair(rt, v, p)
+    submit_both(eng, ora, reqs)
+    n, segs = lockstep(eng, ora, max_rounds=20000, check_every=3)
+    if seg_mode == SEG_NONE:
+        assert any(s["tok_end"] - s["tok_begin"] > 16 for s in segs)
+    admits = [a for r in ora.round_log for a in r["admitted"]]
+    assert len(admits) == len(set(admits)) == len(reqs)   # never suspended / re-queued
 
 
 def test_sched_parity_wcet_gate(rt):
