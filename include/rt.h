@@ -110,6 +110,12 @@ typedef struct {
   int32_t capture_layer;
   int32_t seg_mode;                 /* RT_SEG_* (0 = the method) */
   int32_t wcet_off;                 /* 1: no WCET admission gate (the baselines) */
+  /* KV eviction to host memory + restore (PAPER.md:226-229 context caching; DESIGN.md
+   * R-EVICT): host_pages pinned host pages of one 16-token page across all layers
+   * (n_layers x n_kv_heads x 2 x 16 x head_dim bf16 = 2 MiB at 8B dims); 0 = off.
+   * swap_us_per_page: VIRTUAL clock cost of one evicted or restored page. */
+  int32_t host_pages;
+  int32_t swap_us_per_page;
 } rt_config;
 
 typedef struct {
@@ -124,6 +130,7 @@ typedef struct {
   int64_t t_us, round_us;
   int32_t n_waiting, n_running, n_admitted, n_stopped, n_refused_mem, n_refused_wcet;
   int32_t n_rows, n_prefill_rows;
+  int32_t n_evicted, n_restored;    /* requests whose KV went to / came back from host */
 } rt_round_info;
 
 typedef struct {
@@ -200,6 +207,9 @@ rt_status rt_reset_stats(rt_engine* e);
  *   RT_DUMP_ROWS        int32 [n_rows][3] (task slot, position, token) of the last round
  *   RT_DUMP_KV_LAYER    bf16 logical [n_pages][2][n_kv_heads][16][head_dim] of capture_layer
  *   RT_DUMP_FREE_STACK  int32 [free_top]
+ *   RT_DUMP_HOST_PAGE_TABLES int32 [max_tasks][pages_per_task] host pages of evicted requests
+ *                       (RT_DUMP_TASKS column 8 = evicted, 9 = host pages held)
+ *   RT_DUMP_HOST_FREE_STACK  int32 [host free top]
  *   RT_DUMP_TASK_SLOTS  int32 [B] task slot of each batch slot of the last round
  *   RT_DUMP_MERGED      int64 [K][4] merged global top-K (world > 1)
  *   RT_DUMP_TRACE       rt_trace_rec [n] since the last rt_reset_stats (RT_FLAG_TRACE; at most
@@ -209,7 +219,7 @@ enum {
   RT_DUMP_TASKS = 1, RT_DUMP_PAGE_TABLES = 2, RT_DUMP_ROUND = 3, RT_DUMP_LOGITS = 4,
   RT_DUMP_HIDDEN = 5, RT_DUMP_CAPTURE_Q = 6, RT_DUMP_CAPTURE_O = 7, RT_DUMP_ROWS = 8,
   RT_DUMP_KV_LAYER = 9, RT_DUMP_FREE_STACK = 10, RT_DUMP_TASK_SLOTS = 11, RT_DUMP_MERGED = 12,
-  RT_DUMP_TRACE = 13
+  RT_DUMP_TRACE = 13, RT_DUMP_HOST_PAGE_TABLES = 14, RT_DUMP_HOST_FREE_STACK = 15
 };
 /* One kernel CTA: grid = %gridid (unique per launch); kind = 1 GEMM (| epilogue mode << 8 |
  * cluster split << 16), 2 attention, 3 norm, 4 embed, 5/6 scheduler pre/post, 7 gather,

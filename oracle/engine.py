@@ -37,6 +37,16 @@ STOP_NONE, STOP_EOS, STOP_MAXNEW, STOP_SKILL, STOP_CAP = 0, 1, 2, 3, 4
 # end).  Delivered segments are cut at SEG_MAX_TOKENS in STREAM / NONE.
 SEG_SUSPEND, SEG_STREAM, SEG_NONE = 0, 1, 2
 SEG_MAX_TOKENS = 128
+
+# KV eviction to host memory + restore ("context caching":
+# a suspended generation's KV moves to host memory when GPU memory is insufficient and is
+# copied back on resume, 9.50 ms instead of a 133.31 ms re-prefill).  Reading R-EVICT
+# (DESIGN.md): when a candidate that needs memory (k = 0, or an evicted resume) does not
+# fit, suspended holders that come LATER in this round's key order are evicted, lowest
+# priority first, if evicting them (within the host pool) makes it fit; an evicted request
+# releases its whole reservation, its own pages go to host pages (host free stack, pops
+# 0, 1, 2, ...), and it needs its reservation again to resume (memory check like k = 0),
+# when it re-pops device pages in admission order and its KV is restored.
 PENDING, WAITING, RUNNING, FINISHED = 0, 1, 2, 3
 POLICY_PUD, POLICY_FCFS, POLICY_EDF = 0, 1, 2
 CLOCK_VIRTUAL, CLOCK_WALL = 0, 1
@@ -79,6 +89,8 @@ class OracleEngine:
         self.rank, self.world = rank, world
         self.t = int(params.t0_us)
         self.free = list(range(params.n_pages - 1, -1, -1))  # top = end; pops 0, 1, 2, ...
+        self.host_pages = int(getattr(params, "host_pages", 0))
+        self.hfree = list(range(self.host_pages - 1, -1, -1))  # host KV pages (R-EVICT)
         self.reqs = {}
         self.n_submitted = 0
         self.slots = []
@@ -122,7 +134,8 @@ class OracleEngine:
             prompt=prompt, script=script, max_new=int(max_new_tokens), state=PENDING,
             k=0, D=int(arrival_us) + int(ert_us), ref=int(arrival_us), end_est=None,
             n_gen=0, seg_tok=0, seg_exec=0, seg_nsk=0, pending=None, ctx=0, pages=[],
-            R=R, holder=False, out=[], polled_final=False, argmax=[], pfx=pfx, npfx=npfx)
+            R=R, holder=False, out=[], polled_final=False, argmax=[], pfx=pfx, npfx=npfx,
+            evicted=False, hpages=[])
         return rid
 
     def register_prefix(self, tokens):
@@ -165,6 +178,9 @@ class OracleEngine:
 
     def page_tables(self):
         return {r.id: list(r.pages) for r in self.reqs.values() if r.holder}
+
+    def host_page_tables(self):
+        return {r.id: list(r.hpages) for r in self.reqs.values() if r.evicted}
 
     # ---------------------------------------------------------------- round
     def _ingest(self, t):
@@ -224,12 +240,14 @@ class OracleEngine:
             g = min(cands, key=lambda g: (g.D - t, g.id))
             gate_ok = wcet_gate_pass(p.max_seg_tokens, g.seg_tok, S, n, g.D - t)
 
-        # ---- admission (c8 + reading R-MEM)
+        # ---- admission (c8 + reading R-MEM; eviction R-EVICT)
         admitted = []
+        evicted_now = []
         refused_mem = refused_wcet = 0
         mem_blocked = False
         avail = self._avail()
-        for c in order:
+        havail = len(self.hfree)
+        for ci, c in enumerate(order):
             if len(admitted) >= p.max_admit_per_round:
                 break
             if len(running) + len(admitted) >= p.max_batch:
@@ -237,17 +255,52 @@ class OracleEngine:
             if not gate_ok:
                 refused_wcet = 1
                 break
-            if c.k == 0:  # own pages only: a shared prefix is already resident (R-PFX)
-                if mem_blocked or avail < c.R - c.npfx:
+            if c in evicted_now:          # evicted earlier in this round: not resumable now
+                refused_mem += 1
+                continue
+            if c.k == 0 or c.evicted:  # own pages only: a shared prefix is already resident (R-PFX)
+                need = c.R - c.npfx
+                if not mem_blocked and avail < need and self.host_pages > 0:
+                    # victims: suspended holders later in the key order, lowest priority first
+                    vict, gain, hneed = [], 0, 0
+                    for v in reversed(order[ci + 1:]):
+                        if avail + gain >= need:
+                            break
+                        if v.k > 0 and v.holder and not v.evicted and v not in evicted_now:
+                            own = len(v.pages) - v.npfx
+                            if hneed + own > havail:
+                                continue
+                            vict.append(v)
+                            gain += v.R - v.npfx
+                            hneed += own
+                    if avail + gain >= need:
+                        for v in vict:
+                            evicted_now.append(v)
+                            avail += v.R - v.npfx
+                            havail -= len(v.pages) - v.npfx
+                if mem_blocked or avail < need:
                     mem_blocked = True
                     refused_mem += 1
                     continue
-                avail -= c.R - c.npfx
+                avail -= need
             admitted.append(c)
+
+        # ---- evictions: own pages -> host pages, device pages pushed back (R-EVICT)
+        swaps = []  # (direction, rid, device page, host page); 0 = to host, 1 = restore
+        for v in evicted_now:
+            own = v.pages[v.npfx:]
+            v.hpages = [self.hfree.pop() for _ in own]
+            swaps += [(0, v.id, dp, hp) for dp, hp in zip(own, v.hpages)]
+            for pg in reversed(own):
+                self.free.append(pg)
+            v.pages = v.pages[:v.npfx]
+            v.holder = False
+            v.evicted = True
 
         # ---- page allocation + batch assembly (c2, AMB-14)
         popped = []
         prefill = set()
+        restored = []
         for a in admitted:
             a.state = RUNNING
             if a.k == 0:
@@ -259,6 +312,19 @@ class OracleEngine:
                     pg = self.free.pop()
                     a.pages.append(pg)
                     popped.append((a.id, pg))
+            elif a.evicted:  # restore: re-pop its own pages, KV copied back from host
+                a.holder = True
+                a.evicted = False
+                for hp in a.hpages:
+                    pg = self.free.pop()
+                    a.pages.append(pg)
+                    popped.append((a.id, pg))
+                    swaps.append((1, a.id, pg, hp))
+                restored.append(a)
+        for a in restored:  # host pages back (reverse order), in admission order
+            for hp in reversed(a.hpages):
+                self.hfree.append(hp)
+            a.hpages = []
         slots = self.slots + [a.id for a in admitted]
         for rid in slots:
             r = self.reqs[rid]
@@ -300,7 +366,8 @@ class OracleEngine:
         B = len(slots)
         if p.clock_mode == CLOCK_VIRTUAL:
             round_us = (p.base_us + (p.base_us * p.gamma_ppm * (B - 1)) // 1000000
-                        + (p.kv_us_per_1k * sum_ctx) // 1024 + p.prefill_us_per_tok * sum_prompt)
+                        + (p.kv_us_per_1k * sum_ctx) // 1024 + p.prefill_us_per_tok * sum_prompt
+                        + getattr(p, "swap_us_per_page", 0) * len(swaps))
             dispatch = t + round_us
         else:
             round_us = self.hist[-1] if self.hist else 0
@@ -384,8 +451,8 @@ class OracleEngine:
 
         info = dict(t_us=t, round_us=round_us, n_waiting=n_waiting, n_running=B,
                     n_admitted=len(admitted), n_stopped=len(stops), n_refused_mem=refused_mem,
-                    n_refused_wcet=refused_wcet)
-        self.round_log.append(dict(info, admitted=[a.id for a in admitted], slots=list(slots),
+                    n_refused_wcet=refused_wcet, n_evicted=len(evicted_now), n_restored=len(restored))
+        self.round_log.append(dict(info, admitted=[a.id for a in admitted], slots=list(slots), swaps=swaps,
                                    tokens=toks, argmax=[argmax.get(r) for r in slots],
                                    stops=stops, popped=popped, free=len(self.free), topk=topk,
                                    logits=logits if self.model is not None else None))

@@ -87,6 +87,8 @@ struct rt_engine {
   TaskTable tt{};
   std::vector<void*> allocs;
   DevState* d_st = nullptr;
+  void *h_hpool = nullptr, *d_hpool = nullptr;  // host KV pool (R-EVICT), mapped pinned
+  int64_t hpool_page_bytes = 0;
   HostMailbox* h_mb = nullptr;
   HostMailbox* d_mb = nullptr;
   SegRec* h_ring = nullptr;
@@ -205,6 +207,7 @@ static rt_status validate(const rt_config* c) {
   if (c->policy < 0 || c->policy > 2 || c->clock_mode < 0 || c->clock_mode > 1) return RT_E_INVAL;
   if (c->seg_mode < RT_SEG_SUSPEND || c->seg_mode > RT_SEG_NONE || c->wcet_off < 0 || c->wcet_off > 1)
     return RT_E_INVAL;
+  if (c->host_pages < 0 || c->swap_us_per_page < 0) return RT_E_INVAL;
   if (c->vocab < 2 || !c->tok_skill || !c->tok_exec_min_us) return RT_E_INVAL;
   if (c->eos_id < 0 || c->eos_id >= c->vocab) return RT_E_INVAL;
   if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return RT_E_INVAL;
@@ -297,7 +300,8 @@ static rt_status create_impl(rt_engine* e, const rt_config* cfg) {
   A(alpha, MT); A(beta, MT); A(pri, MT);
   A(state, MT); A(agent, MT); A(k, MT); A(n_prompt, MT); A(max_new, MT); A(window, MT); A(scripted, MT);
   A(n_gen, MT); A(seg_tok, MT); A(n_skills, MT); A(pending, MT); A(ctx, MT); A(n_pages, MT); A(R, MT);
-  A(holder, MT); A(argmax_last, MT); A(pfx, MT); A(n_pfx, MT);
+  A(holder, MT); A(argmax_last, MT); A(pfx, MT); A(n_pfx, MT); A(evicted, MT); A(n_hpages, MT);
+  A(hpage_table, (size_t)MT * e->pt_stride);
   A(page_table, (size_t)(MT + kMaxPrefixes) * e->pt_stride);
   A(prompt, (size_t)MT * c.max_ctx);
   A(script, (size_t)MT * c.max_ctx);
@@ -313,7 +317,23 @@ static rt_status create_impl(rt_engine* e, const rt_config* cfg) {
     DevState st{};
     st.t = c.t0_us;
     st.free_top = n_pages;
+    st.hfree_top = c.host_pages;
     CK(e, cudaMemcpy(e->d_st, &st, sizeof(st), cudaMemcpyHostToDevice));
+  }
+  // KV eviction to host (R-EVICT): host free stack, per-round copy list, pinned mapped
+  // host pool of host_pages pages x all layers (zero-copy target of k_kv_swap)
+  P.host_pages = c.host_pages;
+  P.swap_us_per_page = c.swap_us_per_page;
+  P.swap_cap = 2 * n_pages;
+  CK(e, dalloc(e, &P.hfree_stack, std::max(1, c.host_pages)));
+  if (c.host_pages > 0) launch_init_free_stack(P.hfree_stack, c.host_pages, e->stream);
+  CK(e, dalloc(e, &P.swap, (size_t)P.swap_cap));
+  if (model && c.host_pages > 0) {
+    e->hpool_page_bytes = page_bytes_all_layers;
+    if (cudaHostAlloc(&e->h_hpool, (size_t)c.host_pages * page_bytes_all_layers, cudaHostAllocMapped) !=
+        cudaSuccess)
+      return done(fail(e, RT_E_NOMEM, "host KV pool (pinned) allocation failed"));
+    CK(e, cudaHostGetDevicePointer(&e->d_hpool, e->h_hpool, 0));
   }
   CK(e, cudaHostAlloc((void**)&e->h_mb, sizeof(HostMailbox), cudaHostAllocMapped));
   memset(e->h_mb, 0, sizeof(HostMailbox));
@@ -532,6 +552,7 @@ extern "C" rt_status rt_destroy(rt_engine* e) {
   if (e->d_pool) cudaFree(e->d_pool);
   if (e->h_mb) cudaFreeHost(e->h_mb);
   if (e->h_ring) cudaFreeHost(e->h_ring);
+  if (e->h_hpool) cudaFreeHost(e->h_hpool);
   if (e->h_recs) cudaFreeHost(e->h_recs);
   if (e->h_toks) cudaFreeHost(e->h_toks);
   for (auto ev : e->ev_attn) cudaEventDestroy(ev);
@@ -986,8 +1007,20 @@ extern "C" rt_status rt_step(rt_engine* e, int64_t now_us, rt_round_info* info) 
     info->n_refused_wcet = plan.n_refused_wcet;
     info->n_rows = plan.n_rows;
     info->n_prefill_rows = plan.n_prefill_rows;
+    info->n_evicted = plan.n_evicted;
+    info->n_restored = plan.n_restored;
   }
   if (plan.idle || plan.B == 0) return RT_OK;
+  // KV eviction / restore copies of this round (before the forward reuses the pages):
+  // evictions first (a restore may re-pop a page an eviction just released)
+  if (plan.n_swap > 0 && e->h_hpool) {
+    const int L = c.n_layers;
+    const int64_t blk = e->hpool_page_bytes / L;
+    launch_kv_swap(e->sp.swap, plan.n_swap_ev, e->d_pool, e->pool_layer_bytes, e->d_hpool, blk, L, s);
+    launch_kv_swap(e->sp.swap + plan.n_swap_ev, plan.n_swap - plan.n_swap_ev, e->d_pool, e->pool_layer_bytes,
+                   e->d_hpool, blk, L, s);
+    CK(e, cudaGetLastError());
+  }
   if (e->exchange) {  // a12: allgather of this round's local top-K candidates on the side stream
     CK(e, cudaEventRecord(e->ev_cand, s));
     CK(e, cudaStreamWaitEvent(e->side, e->ev_cand, 0));
@@ -1189,15 +1222,16 @@ extern "C" rt_status rt_debug_dump(rt_engine* e, int32_t what, void* dst, int64_
   const int B = ds.B, n_rows = ds.n_rows;
   switch (what) {
     case RT_DUMP_TASKS: {
-      std::vector<int64_t> v((size_t)MT * 8);
+      std::vector<int64_t> v((size_t)MT * 10);
       std::vector<int64_t> rid(MT);
       std::vector<int32_t> a(MT);
       CK(e, cudaMemcpy(rid.data(), e->tt.rid, 8 * MT, cudaMemcpyDeviceToHost));
-      for (int i = 0; i < MT; ++i) v[(size_t)i * 8] = rid[i];
-      int32_t* fields[] = {e->tt.state, e->tt.k, e->tt.ctx, e->tt.n_pages, e->tt.n_gen, e->tt.seg_tok, e->tt.R};
-      for (int f = 0; f < 7; ++f) {
+      for (int i = 0; i < MT; ++i) v[(size_t)i * 10] = rid[i];
+      int32_t* fields[] = {e->tt.state, e->tt.k,       e->tt.ctx, e->tt.n_pages, e->tt.n_gen,
+                           e->tt.seg_tok, e->tt.R, e->tt.evicted, e->tt.n_hpages};
+      for (int f = 0; f < 9; ++f) {
         CK(e, cudaMemcpy(a.data(), fields[f], 4 * MT, cudaMemcpyDeviceToHost));
-        for (int i = 0; i < MT; ++i) v[(size_t)i * 8 + 1 + f] = a[i];
+        for (int i = 0; i < MT; ++i) v[(size_t)i * 10 + 1 + f] = a[i];
       }
       return copy_out(e, dst, bytes, v.data(), (int64_t)v.size() * 8, bytes_out, false);
     }
@@ -1269,6 +1303,10 @@ extern "C" rt_status rt_debug_dump(rt_engine* e, int32_t what, void* dst, int64_
     }
     case RT_DUMP_FREE_STACK:
       return copy_out(e, dst, bytes, e->sp.free_stack, (int64_t)ds.free_top * 4, bytes_out);
+    case RT_DUMP_HOST_PAGE_TABLES:
+      return copy_out(e, dst, bytes, e->tt.hpage_table, (int64_t)MT * e->pt_stride * 4, bytes_out);
+    case RT_DUMP_HOST_FREE_STACK:
+      return copy_out(e, dst, bytes, e->sp.hfree_stack, (int64_t)ds.hfree_top * 4, bytes_out);
     case RT_DUMP_TASK_SLOTS:
       return copy_out(e, dst, bytes, e->sp.round_slots, (int64_t)B * 4, bytes_out);
     case RT_DUMP_MERGED: {

@@ -31,6 +31,8 @@ struct TaskTable {
   int32_t *n_gen, *seg_tok, *n_skills, *pending, *ctx, *n_pages, *R, *holder, *argmax_last;
   int32_t *pfx, *n_pfx;  // shared prefix id (-1 none) and its page count (leading page-table
                          // entries that are the prefix's read-only pages)
+  int32_t *evicted, *n_hpages;  // KV evicted to host pages (R-EVICT) and how many
+  int32_t* hpage_table;  // [max_tasks][pt_stride] host pages of an evicted request's own pages
   int32_t* page_table;   // [max_tasks + kMaxPrefixes][pt_stride] (prefix rows at the end)
   int32_t* prompt;       // [max_tasks][max_ctx]
   int32_t* script;       // [max_tasks][max_ctx]
@@ -49,6 +51,8 @@ struct DevState {
   int64_t seg_written;   // segment records published so far
   int32_t n_admitted, n_waiting, n_refused_mem, n_refused_wcet, n_stopped, n_pops;
   int32_t error;
+  int32_t hfree_top;     // host free-stack size (R-EVICT)
+  int32_t n_swap, n_evicted, n_restored;  // this round's page copies / requests
 };
 
 // Round plan / summary published to the host (mapped pinned memory).
@@ -61,6 +65,8 @@ struct HostMailbox {
   int64_t attn_tokens;   // sum over rows of attended positions (algorithmic attention bytes)
   int32_t n_pf_tiles;    // prefill attention tiles of this round (SchedParams::pf_tiles)
   int32_t n_dec_rows;    // decode rows of this round (SchedParams::dec_rows)
+  int32_t n_swap, n_evicted, n_restored;  // KV page copies (SchedParams::swap) / requests
+  int32_t n_swap_ev;     // the first n_swap_ev copies are evictions (device -> host)
 };
 
 struct SegRec {  // identical layout to rt_segment
@@ -102,6 +108,10 @@ struct SchedParams {
   int32_t base_us, gamma_ppm, kv_us_per_1k, prefill_us_per_tok;
   int32_t eos_id, rank, world, no_model;
   int32_t seg_mode, wcet_off;  // RT_SEG_*, WCET gate disabled (baselines)
+  int32_t host_pages, swap_us_per_page;  // KV eviction to host (R-EVICT); 0 pages = off
+  int32_t* hfree_stack;        // [host_pages] host free stack (top = end, pops 0, 1, 2, ...)
+  int4* swap;                  // [swap_cap] (dir 0 evict / 1 restore, task, device page, host page)
+  int32_t swap_cap;
 };
 
 // launchers (sched.cu)

@@ -284,6 +284,27 @@ void launch_argmax_reduce(const float* pv, const int32_t* pi, int n_mtiles, int 
                           cudaStream_t s) {
   launch_pdl(k_argmax_reduce, dim3(N), dim3(256), 0, s, pv, pi, n_mtiles, N, tok);
 }
+// KV eviction / restore (R-EVICT): entry i = (dir, task, device page, host
+// page); block (i, layer) copies the page's [n_kv][K|V][16][hd] block of that layer between
+// the device pool and the mapped pinned host pool ([host page][layer][block]), 16-byte
+// vectors over PCIe (zero-copy: no staging buffer, no host involvement)
+__global__ void k_kv_swap(const int4* swap, unsigned char* pool, int64_t pool_layer_bytes, unsigned char* host,
+                          int64_t blk, int L) {
+  const int4 w = swap[blockIdx.x];
+  const int l = blockIdx.y;
+  unsigned char* dev = pool + (size_t)l * pool_layer_bytes + (size_t)w.z * blk;
+  unsigned char* hst = host + ((size_t)w.w * L + l) * blk;
+  const uint4* src = reinterpret_cast<const uint4*>(w.x == 0 ? dev : hst);
+  uint4* dst = reinterpret_cast<uint4*>(w.x == 0 ? hst : dev);
+  for (int64_t j = threadIdx.x; j < blk / 16; j += blockDim.x) dst[j] = src[j];
+}
+void launch_kv_swap(const int4* swap, int n, void* pool, int64_t pool_layer_bytes, void* host, int64_t blk, int L,
+                    cudaStream_t s) {
+  if (n > 0)
+    k_kv_swap<<<dim3(n, L), 256, 0, s>>>(swap, (unsigned char*)pool, pool_layer_bytes, (unsigned char*)host, blk,
+                                         L);
+}
+
 void launch_kv_write(void* pool, const bf16* k, const bf16* v, const int32_t* slot, int n, int nkv, int hd,
                      cudaStream_t s) {
   k_kv_write<<<n, 256, 0, s>>>((unsigned char*)pool, k, v, slot, nkv, hd);

@@ -30,6 +30,10 @@ void launch_argmax_reduce(const float* pv, const int32_t* pi, int n_mtiles, int 
 void launch_kv_write(void* pool, const bf16* k, const bf16* v, const int32_t* slot, int n, int nkv, int hd,
                      cudaStream_t s);
 void launch_kv_read(const void* pool, bf16* out, int n_pages, int nkv, int hd, cudaStream_t s);
+// KV eviction / restore copies (swap[i] = (dir 0 to host / 1 to device, task, device page,
+// host page)); blk = bytes of one (page, layer) block; host pool [host page][L][blk]
+void launch_kv_swap(const int4* swap, int n, void* pool, int64_t pool_layer_bytes, void* host, int64_t blk, int L,
+                    cudaStream_t s);
 
 // ---- paged decode attention (attn.cu)
 struct AttnArgs {

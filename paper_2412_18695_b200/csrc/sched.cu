@@ -137,6 +137,8 @@ __global__ void k_apply_submits(SchedParams p, const SubmitRec* recs, const int3
     T.n_pages[i] = 0;
     T.R[i] = ceil_div_i(r.n_prompt + r.max_new, p.page_tokens);
     T.holder[i] = 0;
+    T.evicted[i] = 0;
+    T.n_hpages[i] = 0;
     T.argmax_last[i] = -1;
     __threadfence();
     T.state[i] = T_PENDING;
@@ -165,6 +167,8 @@ struct PreSmem {
   int cslot[kMaxTasks], ck[kMaxTasks], cR[kMaxTasks];
   int cnt_a[kMaxTasks], cnt_b[kMaxTasks];
   int adm[kMaxTasks];
+  int evn[kMaxTasks];   // candidate evicted this round (R-EVICT)
+  int vic[kMaxTasks];   // victims (task slots) in eviction order
 };
 
 __device__ __forceinline__ bool key_before(const PreSmem& S, int x, int y, int n) {
@@ -183,6 +187,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
   PreSmem& S = *reinterpret_cast<PreSmem*>(dsm);
   __shared__ long long s_t;
   __shared__ int s_nwait, s_nc, s_nadm, s_gate_ok, s_refused_mem, s_refused_wcet, s_outstanding;
+  __shared__ int s_nvic, s_nswap, s_nrest, s_ftop;
   __shared__ unsigned long long s_min_arr;
   __shared__ int wbuf[32];
   __shared__ unsigned long long s_sum_ctx, s_sum_prompt, s_attn_tok;
@@ -267,6 +272,10 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
         mb->n_waiting = 0;
         mb->n_refused_mem = 0;
         mb->n_refused_wcet = 0;
+        mb->n_swap = 0;
+        mb->n_swap_ev = 0;
+        mb->n_evicted = 0;
+        mb->n_restored = 0;
         for (int j = 0; j < kTopK; ++j) {
           p.cand[j * 4 + 0] = -INFINITY;
           p.cand[j * 4 + 2] = -1.0;
@@ -308,6 +317,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
     S.cslot[pos] = i;
     S.ck[pos] = k;
     S.cR[pos] = T.R[i] - T.n_pfx[i];  // own pages (a shared prefix is already resident)
+    S.evn[pos] = 0;
   }
   // outstanding reservations sum_active (R - held)  (AMB-26)
   int my_out = 0;
@@ -394,10 +404,14 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
   }
   __syncthreads();
 
-  // ---- (3b) admission in key order (reading R-MEM)
+  // ---- (3b) admission in key order (reading R-MEM), with KV eviction to
+  // host memory when a candidate that needs memory does not fit (R-EVICT):
+  // suspended holders LATER in the key order are evicted, lowest priority first, only if
+  // evicting them (within the host pool) makes the candidate fit
   if (tid == 0) {
     long long avail = (long long)st->free_top - s_outstanding;
-    int nadm = 0, rmem = 0, rwcet = 0;
+    int havail = p.host_pages > 0 ? st->hfree_top : 0;
+    int nadm = 0, rmem = 0, rwcet = 0, nvic = 0;
     bool mem_blocked = false;
     for (int c = 0; c < n; ++c) {
       if (nadm >= p.max_admit) break;
@@ -407,19 +421,75 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
         break;
       }
       const int x = S.perm[c];
-      if (S.ck[x] == 0) {
-        if (mem_blocked || avail < S.cR[x]) {
+      if (S.evn[x]) {  // evicted earlier in this round: not resumable now
+        ++rmem;
+        continue;
+      }
+      if (S.ck[x] == 0 || T.evicted[S.cslot[x]]) {
+        const int need = S.cR[x];
+        if (!mem_blocked && avail < need && p.host_pages > 0) {
+          long long gain = 0;
+          int hneed = 0, nv = 0;
+          for (int cj = n - 1; cj > c && avail + gain < need; --cj) {
+            const int y = S.perm[cj];
+            const int vt = S.cslot[y];
+            if (S.ck[y] > 0 && T.holder[vt] && !T.evicted[vt] && !S.evn[y]) {
+              const int own = T.n_pages[vt] - T.n_pfx[vt];
+              if (hneed + own > havail) continue;
+              S.cnt_b[nv++] = y;  // scratch: tentative victims
+              gain += S.cR[y];
+              hneed += own;
+            }
+          }
+          if (avail + gain >= need) {
+            for (int v = 0; v < nv; ++v) {
+              const int y = S.cnt_b[v];
+              S.evn[y] = 1;
+              S.vic[nvic++] = S.cslot[y];
+              avail += S.cR[y];
+            }
+            havail -= hneed;
+          }
+        }
+        if (mem_blocked || avail < need) {
           mem_blocked = true;
           ++rmem;
           continue;
         }
-        avail -= S.cR[x];
+        avail -= need;
       }
       S.adm[nadm++] = S.cslot[x];
     }
     s_nadm = nadm;
     s_refused_mem = rmem;
     s_refused_wcet = rwcet;
+    s_nvic = nvic;
+    // evictions: own pages -> host pages (host pops in page-table order), device pages
+    // pushed back in reverse page-table order, victims in eviction order
+    int ftop = st->free_top, htop = st->hfree_top, nsw = 0;
+    for (int v = 0; v < nvic; ++v) {
+      const int vt = S.vic[v];
+      const int npf = T.n_pfx[vt], own = T.n_pages[vt] - npf;
+      int32_t* pt = T.page_table + (size_t)vt * p.pt_stride;
+      int32_t* hpt = T.hpage_table + (size_t)vt * p.pt_stride;
+      for (int m = 0; m < own; ++m) {
+        const int hp = p.hfree_stack[htop - 1 - m];
+        hpt[m] = hp;
+        if (nsw < p.swap_cap) p.swap[nsw] = make_int4(0, vt, pt[npf + m], hp);
+        ++nsw;
+      }
+      htop -= own;
+      for (int m = 0; m < own; ++m) p.free_stack[ftop + m] = pt[npf + own - 1 - m];
+      ftop += own;
+      T.n_hpages[vt] = own;
+      T.n_pages[vt] = npf;
+      T.holder[vt] = 0;
+      T.evicted[vt] = 1;
+    }
+    st->hfree_top = htop;
+    s_ftop = ftop;
+    s_nswap = nsw;
+    p.mb->n_swap_ev = min(nsw, p.swap_cap);
   }
   __syncthreads();
   const int nadm = s_nadm;
@@ -438,22 +508,39 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
   }
   for (int s = tid; s < n_run; s += nt) p.slot_is_prefill[s] = 0;
   __syncthreads();
+  // restores (evicted resumes admitted this round): re-pop their own pages with the
+  // admissions (admission order), KV copied back from the host pages, host pages pushed back
+  // (admission order, each in reverse order) after this round's eviction pops
+  if (tid == 0) {
+    int htop = st->hfree_top, nrest = 0;
+    for (int j = 0; j < nadm; ++j) {
+      const int task = S.adm[j];
+      if (!T.evicted[task] || T.k[task] == 0) continue;
+      ++nrest;
+      const int nh = T.n_hpages[task];
+      const int32_t* hpt = T.hpage_table + (size_t)task * p.pt_stride;
+      for (int m = 0; m < nh; ++m) p.hfree_stack[htop + m] = hpt[nh - 1 - m];
+      htop += nh;
+    }
+    st->hfree_top = htop;
+    s_nrest = nrest;
+  }
+  __syncthreads();
   // page pops: prefill admissions (admission order) first, then decode slots in slot order
   for (int s = tid; s < B; s += nt) {
     const int task = p.slot_task[s];
     p.round_slots[s] = task;
     if (p.slot_is_prefill[s]) {
       S.cnt_a[s] = ceil_div_i(T.n_prompt[task], p.page_tokens) - T.n_pfx[task];
-      S.cnt_b[s] = 0;
     } else {
-      S.cnt_a[s] = 0;
-      S.cnt_b[s] = (T.ctx[task] % p.page_tokens == 0) ? 1 : 0;
+      S.cnt_a[s] = (s >= n_run && T.evicted[task]) ? T.n_hpages[task] : 0;  // restore pops
     }
+    S.cnt_b[s] = p.slot_is_prefill[s] ? 0 : ((T.ctx[task] % p.page_tokens == 0) ? 1 : 0);
   }
   __syncthreads();
   const int tot_a = block_scan_excl(S.cnt_a, B, wbuf);
   const int tot_b = block_scan_excl(S.cnt_b, B, wbuf);
-  const int top = st->free_top;
+  const int top = s_ftop;
   for (int s = tid; s < B; s += nt) {
     const int task = p.slot_task[s];
     int32_t* pt = T.page_table + (size_t)task * p.pt_stride;
@@ -470,15 +557,49 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
         p.popped[2 * q + 1] = pg;
       }
       T.n_pages[task] = npg;
-    } else if (T.ctx[task] % p.page_tokens == 0) {
-      const int q = tot_a + S.cnt_b[s];
-      const int pg = p.free_stack[top - 1 - q];
-      const int np = T.n_pages[task];
-      pt[np] = pg;
-      T.n_pages[task] = np + 1;
-      p.popped[2 * q] = task;
-      p.popped[2 * q + 1] = pg;
+    } else {
+      if (s >= n_run && T.evicted[task]) {  // restore: own pages re-popped, KV from host
+        const int npf = T.n_pfx[task], nh = T.n_hpages[task];
+        const int32_t* hpt = T.hpage_table + (size_t)task * p.pt_stride;
+        for (int m = 0; m < nh; ++m) {
+          const int q = S.cnt_a[s] + m;
+          const int pg = p.free_stack[top - 1 - q];
+          pt[npf + m] = pg;
+          p.popped[2 * q] = task;
+          p.popped[2 * q + 1] = pg;
+        }
+        T.n_pages[task] = npf + nh;
+      }
+      if (T.ctx[task] % p.page_tokens == 0) {
+        const int q = tot_a + S.cnt_b[s];
+        const int pg = p.free_stack[top - 1 - q];
+        const int np = T.n_pages[task];
+        pt[np] = pg;
+        T.n_pages[task] = np + 1;
+        p.popped[2 * q] = task;
+        p.popped[2 * q + 1] = pg;
+      }
     }
+  }
+  __syncthreads();
+  // restore copy list (after the evictions', in admission order) and restored state
+  if (tid == 0) {
+    int nsw = s_nswap;
+    for (int s = n_run; s < B; ++s) {
+      const int task = p.slot_task[s];
+      if (p.slot_is_prefill[s] || !T.evicted[task]) continue;
+      const int npf = T.n_pfx[task], nh = T.n_hpages[task];
+      const int32_t* pt = T.page_table + (size_t)task * p.pt_stride;
+      const int32_t* hpt = T.hpage_table + (size_t)task * p.pt_stride;
+      for (int m = 0; m < nh; ++m) {
+        if (nsw < p.swap_cap) p.swap[nsw] = make_int4(1, task, pt[npf + m], hpt[m]);
+        ++nsw;
+      }
+      T.evicted[task] = 0;
+      T.n_hpages[task] = 0;
+      T.holder[task] = 1;
+    }
+    s_nswap = nsw;
   }
   __syncthreads();
   // forward rows: prefill slot -> n_prompt rows, decode slot -> 1 row (AMB-13)
@@ -552,7 +673,8 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
     long long round_us, dispatch;
     if (!wall) {
       round_us = (long long)p.base_us + ((long long)p.base_us * p.gamma_ppm * (long long)(B - 1)) / 1000000 +
-                 ((long long)p.kv_us_per_1k * sum_ctx) / 1024 + (long long)p.prefill_us_per_tok * sum_prompt;
+                 ((long long)p.kv_us_per_1k * sum_ctx) / 1024 + (long long)p.prefill_us_per_tok * sum_prompt +
+                 (long long)p.swap_us_per_page * s_nswap;
       dispatch = t + round_us;
     } else {
       round_us = st->hist_n > 0 ? st->hist[(st->hist_pos + 7) & 7] : 0;
@@ -572,7 +694,13 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
     st->n_refused_mem = s_refused_mem;
     st->n_refused_wcet = s_refused_wcet;
     st->n_pops = tot_a + tot_b;
+    st->n_swap = s_nswap;
+    st->n_evicted = s_nvic;
+    st->n_restored = s_nrest;
     HostMailbox* mb = p.mb;
+    mb->n_swap = min(s_nswap, p.swap_cap);
+    mb->n_evicted = s_nvic;
+    mb->n_restored = s_nrest;
     mb->t_us = t;
     mb->round_us = round_us;
     mb->idle = 0;

@@ -20,7 +20,7 @@ RT_FLAG_NO_MODEL, RT_FLAG_KEEP_LOGITS, RT_FLAG_CAPTURE, RT_FLAG_TIMING, RT_FLAG_
 RT_FLAG_GRAPHS, RT_FLAG_TRACE = 32, 64
 (RT_DUMP_TASKS, RT_DUMP_PAGE_TABLES, RT_DUMP_ROUND, RT_DUMP_LOGITS, RT_DUMP_HIDDEN, RT_DUMP_CAPTURE_Q,
  RT_DUMP_CAPTURE_O, RT_DUMP_ROWS, RT_DUMP_KV_LAYER, RT_DUMP_FREE_STACK, RT_DUMP_TASK_SLOTS,
- RT_DUMP_MERGED, RT_DUMP_TRACE) = range(1, 14)
+ RT_DUMP_MERGED, RT_DUMP_TRACE, RT_DUMP_HOST_PAGE_TABLES, RT_DUMP_HOST_FREE_STACK) = range(1, 16)
 # rt_trace_rec (include/rt.h)
 TRACE_DTYPE = np.dtype([("grid", "<u8"), ("kind", "<u4"), ("smid", "<u4"), ("t_entry", "<u8"),
                         ("t_ready", "<u8"), ("t_aux", "<u8"), ("t_exit", "<u8")])
@@ -62,6 +62,7 @@ class rt_config(C.Structure):
         ("kv_us_per_1k", C.c_int32), ("prefill_us_per_tok", C.c_int32), ("t0_us", C.c_int64),
         ("tok_skill", C.c_void_p), ("tok_exec_min_us", C.c_void_p), ("eos_id", C.c_int32),
         ("flags", C.c_int32), ("capture_layer", C.c_int32), ("seg_mode", C.c_int32), ("wcet_off", C.c_int32),
+        ("host_pages", C.c_int32), ("swap_us_per_page", C.c_int32),
     ]
 
 
@@ -76,7 +77,7 @@ class rt_round_info(C.Structure):
     _fields_ = [("t_us", C.c_int64), ("round_us", C.c_int64), ("n_waiting", C.c_int32),
                 ("n_running", C.c_int32), ("n_admitted", C.c_int32), ("n_stopped", C.c_int32),
                 ("n_refused_mem", C.c_int32), ("n_refused_wcet", C.c_int32), ("n_rows", C.c_int32),
-                ("n_prefill_rows", C.c_int32)]
+                ("n_prefill_rows", C.c_int32), ("n_evicted", C.c_int32), ("n_restored", C.c_int32)]
 
 
 class rt_stats(C.Structure):
@@ -178,6 +179,7 @@ class Engine:
         c.eos_id = vocab.eos_id
         c.flags, c.capture_layer = flags, capture_layer
         c.seg_mode, c.wcet_off = p.seg_mode, p.wcet_off
+        c.host_pages, c.swap_us_per_page = p.host_pages, p.swap_us_per_page
         self.cfg = c
         self.shape, self.params, self.vocab = shape, params, vocab
         h = C.c_void_p()
@@ -271,8 +273,20 @@ class Engine:
         _check(lib().rt_reset_stats(self.h), self.h)
 
     def tasks(self):
-        """RT_DUMP_TASKS decoded: rows of (rid, state, k, ctx, n_pages, n_gen, seg_tok, R)."""
-        return self.dump(RT_DUMP_TASKS, np.int64).reshape(-1, 8)
+        """RT_DUMP_TASKS decoded: rows of (rid, state, k, ctx, n_pages, n_gen, seg_tok, R, evicted,
+        host pages)."""
+        return self.dump(RT_DUMP_TASKS, np.int64).reshape(-1, 10)
+
+    def host_page_tables(self):
+        """{request_id: [host pages]} of every request whose KV is evicted to host (R-EVICT)."""
+        t = self.tasks()
+        pts = self.dump(RT_DUMP_HOST_PAGE_TABLES, np.int32).reshape(t.shape[0], -1)
+        out = {}
+        for i in range(t.shape[0]):
+            rid, state = int(t[i, 0]), int(t[i, 1])
+            if state in (1, 2) and t[i, 8]:
+                out[rid] = [int(x) for x in pts[i, :int(t[i, 9])]]
+        return out
 
     def page_tables(self):
         """{request_id: [pages]} of every request holding pages (admitted, not finished)."""
@@ -281,7 +295,7 @@ class Engine:
         out = {}
         for i in range(t.shape[0]):
             rid, state, _, _, npg = (int(x) for x in t[i, :5])
-            if state in (1, 2) and npg > 0:
+            if state in (1, 2) and npg > 0 and not t[i, 8]:  # holders (an evicted request is not)
                 out[rid] = [int(x) for x in pts[i, :npg]]
         return out
 

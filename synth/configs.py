@@ -95,6 +95,8 @@ class EngineParams:
     t0_us: int = 0
     seg_mode: int = SEG_SUSPEND     # the method; STREAM / NONE = the comparison systems
     wcet_off: int = 0               # 1: no WCET admission gate (the baselines)
+    host_pages: int = 0             # host KV pages for eviction (0: off)
+    swap_us_per_page: int = 0       # VIRTUAL clock cost of one evicted / restored page
     extra: dict = field(default_factory=dict)
 
     def as_dict(self):

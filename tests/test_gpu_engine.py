@@ -123,6 +123,68 @@ def test_sched_parity_comparison_systems(rt, policy, seg_mode):
     assert len(admits) == len(set(admits)) == len(reqs)   # never suspended / re-queued
 
 
+def _evict_workload(v, **kw):
+    p = engine_params("paper-4090", max_batch=8, max_tasks=512, max_ctx=256, n_pages=40, host_pages=64,
+                      swap_us_per_page=116, **kw)
+    reqs = compose_workload(24, 6.0, 8, range(1, 12), 8.0, 9, v, prompt_len_range=(20, 90), max_requests=120)
+    return p, reqs
+
+
+def test_sched_parity_kv_eviction(rt):
+    """NEXT-2 on the device scheduler (R-EVICT): the same contended trace as the oracle pin
+    (tests/test_oracle_evict.py) — evictions / restores per round, page tables, host page
+    tables, free stack and host free stack bit-exact every round."""
+    v = make_vocab(512)
+    p, reqs = _evict_workload(v)
+    eng, ora = make_pair(rt, v, p)
+    submit_both(eng, ora, reqs)
+    n_ev = 0
+    for n in range(20000):
+        ig, io = eng.step(), ora.step()
+        for key in ("t_us", "n_running", "n_admitted", "n_refused_mem"):
+            assert ig[key] == io[key], (n, key, ig, io)
+        assert (ig["n_evicted"], ig["n_restored"]) == (io.get("n_evicted", 0), io.get("n_restored", 0)), n
+        n_ev += io.get("n_evicted", 0)
+        if io["n_running"]:
+            assert eng.round_log()["slots"] == ora.round_log[-1]["slots"], n
+        assert eng.page_tables() == ora.page_tables(), n
+        assert eng.host_page_tables() == ora.host_page_tables(), n
+        assert list(eng.dump(rt.RT_DUMP_HOST_FREE_STACK, np.int32)) == ora.hfree, n
+        if io["n_running"] == 0 and all(r.state == FINISHED for r in ora.reqs.values()):
+            break
+    assert n_ev > 0
+    assert eng.poll() == ora.poll()
+    assert list(eng.dump(rt.RT_DUMP_FREE_STACK, np.int32)) == ora.free
+
+
+def test_tiny_model_kv_eviction_e2e(rt):
+    """KV evicted to pinned host pages and restored (no re-prefill) keeps the model exact:
+    C1-shaped tiny model under the eviction workload, logits of every round against the
+    oracle (whose KV never moves) and the segment stream bit-exact."""
+    shape = MODEL_SHAPES["tiny"]
+    v = make_vocab(shape.vocab)
+    p, reqs = _evict_workload(v)
+    eng, ora = make_pair(rt, v, p, shape=shape, seed=5, flags=rt.RT_FLAG_KEEP_LOGITS, model=True)
+    submit_both(eng, ora, reqs[:60])
+    worst = 0.0
+    n_ev = n_rs = 0
+    for n in range(20000):
+        ig, io = eng.step(), ora.step()
+        assert ig["n_running"] == io["n_running"] and ig["n_evicted"] == io.get("n_evicted", 0), n
+        n_ev += ig["n_evicted"]
+        n_rs += ig["n_restored"]
+        if io["n_running"]:
+            B = io["n_running"]
+            lg = eng.dump(rt.RT_DUMP_LOGITS, np.float32).reshape(B, -1)
+            lo = np.stack([ora.round_log[-1]["logits"][rid] for rid in ora.round_log[-1]["slots"]])
+            worst = max(worst, float(np.abs(lg - lo).max()))
+        if io["n_running"] == 0 and all(r.state == FINISHED for r in ora.reqs.values()):
+            break
+    assert n_ev > 0 and n_rs > 0
+    assert worst < 1e-2, worst
+    assert eng.poll() == ora.poll()
+
+
 def test_sched_parity_wcet_gate(rt):
     # slow paper-4090 clock with gamma: urgent running tasks block admissions (WCET)
     v = make_vocab(512)
