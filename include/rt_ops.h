@@ -42,6 +42,17 @@ rt_status rt_op_kv_write(void* d_pool, const void* d_k, const void* d_v, const i
 rt_status rt_op_kv_read(const void* d_pool, void* d_out, int32_t n_pages, int32_t n_kv, int32_t hd,
                         void* stream);
 
+/* KV eviction / restore copies (PAPER.md:226-229 context caching; DESIGN.md R-EVICT):
+ * d_swap int32 [n][4] = (dir 0 device->host / 1 host->device, task (unused), device page,
+ * host page); for every layer l < n_layers the (page, layer) block of blk_bytes =
+ * n_kv * 2 * 16 * hd * 2 bytes is copied between layer l of the device pool (layer stride
+ * pool_layer_bytes) and host page h at h_host + (h * n_layers + l) * blk_bytes.  h_host is a
+ * page-locked host allocation addressable from the device (cudaHostAlloc / pinned memory under
+ * UVA): the copy is zero-copy over PCIe.  Entries of one call must not read a page another
+ * entry of the same call writes. */
+rt_status rt_op_kv_swap(const int32_t* d_swap, int32_t n, void* d_pool, int64_t pool_layer_bytes, void* h_host,
+                        int64_t blk_bytes, int32_t n_layers, void* stream);
+
 /* a6 dense projection on tcgen05 (UMMA 128 x BN x 16, TMEM accumulator, TMA SW128):
  *   d_out[n][m] = sum_k W[m, k] * X[n, k]     fp32; split-K over a cluster of
  *   `splits` CTAs per tile (1..16, <= K/64), reduced through distributed shared

@@ -72,6 +72,15 @@ extern "C" rt_status rt_op_kv_write(void* d_pool, const void* d_k, const void* d
   return last_launch();
 }
 
+extern "C" rt_status rt_op_kv_swap(const int32_t* d_swap, int32_t n, void* d_pool, int64_t pool_layer_bytes,
+                                   void* h_host, int64_t blk_bytes, int32_t n_layers, void* stream) {
+  if (n < 0 || n_layers < 1 || blk_bytes % 16 || !d_pool || !h_host) return RT_E_INVAL;
+  if (n == 0) return RT_OK;
+  launch_kv_swap(reinterpret_cast<const int4*>(d_swap), n, d_pool, pool_layer_bytes, h_host, blk_bytes, n_layers,
+                 (cudaStream_t)stream);
+  return last_launch();
+}
+
 extern "C" rt_status rt_op_kv_read(const void* d_pool, void* d_out, int32_t n_pages, int32_t n_kv, int32_t hd,
                                    void* stream) {
   if (n_pages < 1 || n_kv < 1 || hd % 8) return RT_E_INVAL;

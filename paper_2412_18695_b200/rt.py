@@ -29,7 +29,7 @@ TRACE_KINDS = {1: "gemm", 2: "attn", 3: "norm", 4: "embed", 5: "sched_pre", 6: "
 
 EXPORTED = ["rt_create", "rt_destroy", "rt_submit_request", "rt_register_prefix", "rt_step", "rt_poll_segment", "rt_last_round",
             "rt_sync", "rt_get_stats", "rt_reset_stats", "rt_debug_dump", "rt_last_error", "rt_version",
-            "rt_op_paged_attention", "rt_op_attention_ws_bytes", "rt_op_kv_write", "rt_op_kv_read",
+            "rt_op_paged_attention", "rt_op_attention_ws_bytes", "rt_op_kv_write", "rt_op_kv_read", "rt_op_kv_swap",
             "rt_op_gemm", "rt_op_lm_argmax", "rt_op_init_weights", "rt_op_priority", "rt_mark", "rt_elapsed_ms",
             "rt_nccl_unique_id", "rt_op_pack_tiled", "rt_op_gemm_tiled"]
 
@@ -117,6 +117,7 @@ def lib():
     L.rt_op_attention_ws_bytes.restype = i64
     L.rt_op_kv_write.argtypes = [vp, vp, vp, vp, i32, i32, i32, vp]
     L.rt_op_kv_read.argtypes = [vp, vp, i32, i32, i32, vp]
+    L.rt_op_kv_swap.argtypes = [vp, i32, vp, i64, vp, i64, i32, vp]
     L.rt_op_gemm.argtypes = [vp, vp, vp, i32, i32, i32, i32, i32, vp]
     L.rt_op_lm_argmax.argtypes = [vp, vp, i32, i32, i32, i32, vp, vp, vp, i64, vp]
     L.rt_op_init_weights.argtypes = [vp, i64, C.c_uint64, i32, C.c_float, vp]
@@ -368,6 +369,13 @@ def kv_write(pool, k, v, slot, n_kv, hd, stream=None):
 
 def kv_read(pool, out, n_pages, n_kv, hd, stream=None):
     _check(lib().rt_op_kv_read(_ptr(pool), _ptr(out), n_pages, n_kv, hd, _stream(stream)))
+
+
+def kv_swap(swap, pool, pool_layer_bytes, host, blk_bytes, n_layers, stream=None):
+    """swap: int32 cuda tensor [n][4] (dir, task, device page, host page); host: pinned CPU
+    tensor (device-addressable under UVA)."""
+    _check(lib().rt_op_kv_swap(_ptr(swap), int(swap.shape[0]), _ptr(pool), int(pool_layer_bytes), _ptr(host),
+                               int(blk_bytes), int(n_layers), _stream(stream)))
 
 
 def gemm(w, x, out, M, N, K, n_cap, splits=1, stream=None):

@@ -160,3 +160,29 @@ def test_paged_attention_c2_operating_point_sampled(rt):
     # 64 rows at ctx 1310 (C2), 8B heads; all rows checked (cheap in numpy)
     e32, e16 = _attn_case(rt, 128, 32, 8, [1310] * 64, seed=9)
     assert e32 < 6e-3 and e16 <= 0.0
+
+
+def test_kv_swap_roundtrip(rt):
+    """rt_op_kv_swap (R-EVICT copies): pages evicted to pinned host pages and restored into
+    different device pages are bit-identical, every layer, untouched pages unchanged."""
+    L, n_pages, nkv, hd = 3, 12, 2, 64
+    blk = nkv * 2 * 16 * hd * 2
+    g = torch.Generator(device="cuda").manual_seed(0)
+    pool = torch.randint(0, 255, (L, n_pages * blk), dtype=torch.uint8, device="cuda", generator=g)
+    orig = pool.clone()
+    host = torch.zeros(8 * L * blk, dtype=torch.uint8).pin_memory()
+    ev = torch.tensor([[0, 0, 3, 5], [0, 0, 7, 0], [0, 1, 1, 2]], dtype=torch.int32, device="cuda")
+    rt.kv_swap(ev, pool, n_pages * blk, host, blk, L)
+    torch.cuda.synchronize()
+    hv = host.view(8, L, blk)
+    for _, _, dp, hp in ev.tolist():
+        for l in range(L):
+            assert torch.equal(hv[hp, l].cuda(), orig[l, dp * blk:(dp + 1) * blk])
+    rs = torch.tensor([[1, 0, 10, 5], [1, 0, 11, 0], [1, 1, 4, 2]], dtype=torch.int32, device="cuda")
+    rt.kv_swap(rs, pool, n_pages * blk, host, blk, L)
+    torch.cuda.synchronize()
+    for (_, _, src, _), (_, _, dst, _) in zip(ev.tolist(), rs.tolist()):
+        assert torch.equal(pool[:, dst * blk:(dst + 1) * blk], orig[:, src * blk:(src + 1) * blk])
+    keep = [p for p in range(n_pages) if p not in (10, 11, 4)]
+    for p in keep:
+        assert torch.equal(pool[:, p * blk:(p + 1) * blk], orig[:, p * blk:(p + 1) * blk])
