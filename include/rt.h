@@ -55,6 +55,11 @@ enum { RT_STOP_NONE = 0, RT_STOP_EOS = 1, RT_STOP_MAXNEW = 2, RT_STOP_SKILL = 3,
  * In STREAM / NONE modes a delivered segment is at most RT_SEG_MAX_TOKENS tokens (a longer
  * run is cut there with reason RT_STOP_CAP). */
 enum { RT_SEG_SUSPEND = 0, RT_SEG_STREAM = 1, RT_SEG_NONE = 2 };
+enum { RT_GRAMMAR_TOKEN = 0, RT_GRAMMAR_SKILL = 1, RT_GRAMMAR_SENTENCE = 2, RT_GRAMMAR_PARAGRAPH = 3 };
+/* token classes of rt_config.tok_class: 1 .. 63 skill names, digits RT_TC_DIGIT0 + d */
+enum { RT_TC_OTHER = 0, RT_TC_DIGIT0 = 64, RT_TC_LPAREN = 80, RT_TC_RPAREN = 81, RT_TC_SEMI = 82,
+       RT_TC_WORD = 90, RT_TC_SENT_END = 91, RT_TC_PARA_END = 92 };
+#define RT_MAX_SKILL_NAMES 63
 #define RT_SEG_MAX_TOKENS 128
 /* rt_config.flags */
 enum {
@@ -116,6 +121,22 @@ typedef struct {
    * swap_us_per_page: VIRTUAL clock cost of one evicted or restored page. */
   int32_t host_pages;
   int32_t swap_us_per_page;
+  /* Stop grammar ("detokenizes token IDs as they are
+   * generated in order to check an executable skill has been generated"
+   * "regular expression matching", PAPER.md:606-609 chatbot sentence / paragraph segments):
+   *   RT_GRAMMAR_TOKEN      one token = one (skill, parameter): tok_skill / tok_exec_min_us
+   *   RT_GRAMMAR_SKILL      multi-token statements  name ( digits ) ;  recognised by a DFA over
+   *                         tok_class; E_min = skill_base_us[name] + skill_unit_us[name] * arg
+   *   RT_GRAMMAR_SENTENCE   chatbot: every word token adds word_us of reading time, a sentence
+   *                         end (or paragraph end) is the boundary
+   *   RT_GRAMMAR_PARAGRAPH  chatbot: a paragraph end is the boundary
+   * tok_class [vocab] (copied; NULL only with RT_GRAMMAR_TOKEN): RT_TC_* below; names are
+   * classes 1 .. 63 (skill index + 1).  skill_base_us / skill_unit_us [63] (copied). */
+  int32_t stop_grammar;
+  const int16_t* tok_class;
+  const int32_t* skill_base_us;
+  const int32_t* skill_unit_us;
+  int32_t word_us;
 } rt_config;
 
 typedef struct {

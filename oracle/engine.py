@@ -25,6 +25,7 @@ Exact round order (reading R-ROUND):
   6 stop check (a9)   7 retire: suspend or finish + free   8 advance clock
 """
 import math
+import re
 
 from .priority import priority
 from . import model as M
@@ -37,6 +38,15 @@ STOP_NONE, STOP_EOS, STOP_MAXNEW, STOP_SKILL, STOP_CAP = 0, 1, 2, 3, 4
 # end).  Delivered segments are cut at SEG_MAX_TOKENS in STREAM / NONE.
 SEG_SUSPEND, SEG_STREAM, SEG_NONE = 0, 1, 2
 SEG_MAX_TOKENS = 128
+
+# Stop grammars.  The paper's checker "detokenizes token IDs as they are
+# generated in order to check an executable skill has been generated"
+# with "regular expression matching"; chatbots end segments at sentences or
+# paragraphs and execute them as reading time at 300 words per minute.
+# The oracle does exactly that on the token TEXTS: GRAMMAR_SKILL appends each token's text
+# to the text since the last complete statement and searches  name(digits);  at its end;
+# the chat grammars count word-bearing tokens and test the token text for . ! ? / \n\n.
+GRAMMAR_TOKEN, GRAMMAR_SKILL, GRAMMAR_SENTENCE, GRAMMAR_PARAGRAPH = 0, 1, 2, 3
 
 # KV eviction to host memory + restore ("context caching":
 # a suspended generation's KV moves to host memory when GPU memory is insufficient and is
@@ -79,8 +89,13 @@ def wcet_gate_pass(max_seg_tokens, seg_tok, hist_sum_us, n, budget_us):
 
 class OracleEngine:
     def __init__(self, params, tok_skill, tok_exec_min_us, eos_id, vocab, model=None,
-                 rank=0, world=1):
+                 rank=0, world=1, grammar=None):
         self.p = params
+        self.grammar = grammar  # tok_text, names, skill_base_us, skill_unit_us (NEXT-4)
+        if grammar is not None:
+            alts = "|".join(re.escape(n) for n in sorted(grammar.names, key=len, reverse=True))
+            self._stmt_re = re.compile(r"(?<![A-Za-z])(" + alts + r")\((\d*)\);$")
+            self._name_idx = {n: i for i, n in enumerate(grammar.names)}
         self.tok_skill = [int(x) for x in tok_skill]
         self.tok_e = [int(x) for x in tok_exec_min_us]
         self.eos = int(eos_id)
@@ -135,7 +150,7 @@ class OracleEngine:
             k=0, D=int(arrival_us) + int(ert_us), ref=int(arrival_us), end_est=None,
             n_gen=0, seg_tok=0, seg_exec=0, seg_nsk=0, pending=None, ctx=0, pages=[],
             R=R, holder=False, out=[], polled_final=False, argmax=[], pfx=pfx, npfx=npfx,
-            evicted=False, hpages=[])
+            evicted=False, hpages=[], stmt_text="")
         return rid
 
     def register_prefix(self, tokens):
@@ -387,9 +402,8 @@ class OracleEngine:
             r.seg_tok += 1
             r.out.append(tok)
             r.pending = tok
-            sk = self.tok_skill[tok]
+            sk = self._stop_unit(r, tok)
             if sk >= 0:
-                r.seg_exec += self.tok_e[tok]
                 r.seg_nsk += 1
             mode = getattr(p, "seg_mode", SEG_SUSPEND)
             cap = p.max_seg_tokens if mode == SEG_SUSPEND else SEG_MAX_TOKENS
@@ -459,6 +473,33 @@ class OracleEngine:
         return info
 
     # -------------------------------------------------------------- helpers
+    def _stop_unit(self, r, tok):
+        """Does token `tok` complete an executable unit of request r (>= 0) — and add its
+        execution estimate to the segment (c4 / a9, per stop grammar)."""
+        g = getattr(self.p, "stop_grammar", GRAMMAR_TOKEN)
+        if g == GRAMMAR_TOKEN:
+            sk = self.tok_skill[tok]
+            if sk >= 0:
+                r.seg_exec += self.tok_e[tok]
+            return sk
+        text = self.grammar.tok_text[tok]
+        if g == GRAMMAR_SKILL:
+            r.stmt_text += text
+            m = self._stmt_re.search(r.stmt_text)
+            if m is None:
+                return -1
+            name = m.group(1)
+            arg = min(int(m.group(2)) if m.group(2) else 0, 1000000)
+            i = self._name_idx[name]
+            r.seg_exec += int(self.grammar.skill_base_us[i]) + int(self.grammar.skill_unit_us[i]) * arg
+            r.stmt_text = ""
+            return i
+        if re.search(r"[A-Za-z0-9]", text):      # a word (reading time, 300 wpm)
+            r.seg_exec += int(getattr(self.p, "word_us", 200000))
+        if text == "\n\n" or (g == GRAMMAR_SENTENCE and text in (".", "!", "?")):
+            return 0
+        return -1
+
     def run_until_idle(self, max_rounds=100000):
         for _ in range(max_rounds):
             info = self.step()

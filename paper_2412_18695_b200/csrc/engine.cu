@@ -71,6 +71,8 @@ struct rt_engine {
   rt_config cfg{};
   std::vector<int16_t> tok_skill;
   std::vector<int32_t> tok_exec;
+  std::vector<int16_t> tok_class;                 // stop grammar (NEXT-4)
+  std::vector<int32_t> skill_base, skill_unit;
   int qkv_dim = 0, pt_stride = 0, rows_cap = 0, fwd_rows = 0, part_rows = 0;
   int64_t pool_layer_bytes = 0;
   cudaStream_t stream = nullptr, side = nullptr;
@@ -208,6 +210,10 @@ static rt_status validate(const rt_config* c) {
   if (c->seg_mode < RT_SEG_SUSPEND || c->seg_mode > RT_SEG_NONE || c->wcet_off < 0 || c->wcet_off > 1)
     return RT_E_INVAL;
   if (c->host_pages < 0 || c->swap_us_per_page < 0) return RT_E_INVAL;
+  if (c->stop_grammar < RT_GRAMMAR_TOKEN || c->stop_grammar > RT_GRAMMAR_PARAGRAPH || c->word_us < 0) return RT_E_INVAL;
+  if (c->stop_grammar != RT_GRAMMAR_TOKEN &&
+      (!c->tok_class || (c->stop_grammar == RT_GRAMMAR_SKILL && (!c->skill_base_us || !c->skill_unit_us))))
+    return RT_E_INVAL;
   if (c->vocab < 2 || !c->tok_skill || !c->tok_exec_min_us) return RT_E_INVAL;
   if (c->eos_id < 0 || c->eos_id >= c->vocab) return RT_E_INVAL;
   if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return RT_E_INVAL;
@@ -250,6 +256,15 @@ static rt_status create_impl(rt_engine* e, const rt_config* cfg) {
   e->tok_skill.assign(cfg->tok_skill, cfg->tok_skill + cfg->vocab);
   e->tok_exec.assign(cfg->tok_exec_min_us, cfg->tok_exec_min_us + cfg->vocab);
   e->cfg.tok_skill = nullptr;
+  if (cfg->tok_class) e->tok_class.assign(cfg->tok_class, cfg->tok_class + cfg->vocab);
+  else e->tok_class.assign(cfg->vocab, (int16_t)RT_TC_OTHER);
+  e->skill_base.assign(RT_MAX_SKILL_NAMES, 0);
+  e->skill_unit.assign(RT_MAX_SKILL_NAMES, 0);
+  if (cfg->skill_base_us) e->skill_base.assign(cfg->skill_base_us, cfg->skill_base_us + RT_MAX_SKILL_NAMES);
+  if (cfg->skill_unit_us) e->skill_unit.assign(cfg->skill_unit_us, cfg->skill_unit_us + RT_MAX_SKILL_NAMES);
+  e->cfg.tok_class = nullptr;
+  e->cfg.skill_base_us = nullptr;
+  e->cfg.skill_unit_us = nullptr;
   // graphs are opt-in: with PDL already hiding launch gaps they measured ~1% slower on the
   // llama3-8b B=64 step (profiles/r01_summary.md), they pay off where the host is the bound
   e->no_graphs = !(c.flags & RT_FLAG_GRAPHS) || getenv("RT_NO_GRAPHS") != nullptr;
@@ -301,6 +316,7 @@ static rt_status create_impl(rt_engine* e, const rt_config* cfg) {
   A(state, MT); A(agent, MT); A(k, MT); A(n_prompt, MT); A(max_new, MT); A(window, MT); A(scripted, MT);
   A(n_gen, MT); A(seg_tok, MT); A(n_skills, MT); A(pending, MT); A(ctx, MT); A(n_pages, MT); A(R, MT);
   A(holder, MT); A(argmax_last, MT); A(pfx, MT); A(n_pfx, MT); A(evicted, MT); A(n_hpages, MT);
+  A(dfa_s, MT); A(dfa_n, MT); A(dfa_v, MT);
   A(hpage_table, (size_t)MT * e->pt_stride);
   A(page_table, (size_t)(MT + kMaxPrefixes) * e->pt_stride);
   A(prompt, (size_t)MT * c.max_ctx);
@@ -371,6 +387,21 @@ static rt_status create_impl(rt_engine* e, const rt_config* cfg) {
   P.seg_ring_cap = e->ring_cap;
   P.tok_skill = d_skill;
   P.tok_exec = d_exec;
+  {
+    int16_t* d_class;
+    int32_t *d_base, *d_unit;
+    CK(e, dalloc(e, &d_class, c.vocab));
+    CK(e, dalloc(e, &d_base, RT_MAX_SKILL_NAMES));
+    CK(e, dalloc(e, &d_unit, RT_MAX_SKILL_NAMES));
+    CK(e, cudaMemcpy(d_class, e->tok_class.data(), c.vocab * 2, cudaMemcpyHostToDevice));
+    CK(e, cudaMemcpy(d_base, e->skill_base.data(), RT_MAX_SKILL_NAMES * 4, cudaMemcpyHostToDevice));
+    CK(e, cudaMemcpy(d_unit, e->skill_unit.data(), RT_MAX_SKILL_NAMES * 4, cudaMemcpyHostToDevice));
+    P.tok_class = d_class;
+    P.skill_base_us = d_base;
+    P.skill_unit_us = d_unit;
+    P.stop_grammar = c.stop_grammar;
+    P.word_us = c.word_us;
+  }
   P.max_tasks = MT;
   P.max_batch = c.max_batch;
   P.max_ctx = c.max_ctx;

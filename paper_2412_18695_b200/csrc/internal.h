@@ -32,6 +32,7 @@ struct TaskTable {
   int32_t *pfx, *n_pfx;  // shared prefix id (-1 none) and its page count (leading page-table
                          // entries that are the prefix's read-only pages)
   int32_t *evicted, *n_hpages;  // KV evicted to host pages (R-EVICT) and how many
+  int32_t *dfa_s, *dfa_n, *dfa_v;  // stop-grammar DFA state, skill name, argument (NEXT-4)
   int32_t* hpage_table;  // [max_tasks][pt_stride] host pages of an evicted request's own pages
   int32_t* page_table;   // [max_tasks + kMaxPrefixes][pt_stride] (prefix rows at the end)
   int32_t* prompt;       // [max_tasks][max_ctx]
@@ -109,6 +110,10 @@ struct SchedParams {
   int32_t eos_id, rank, world, no_model;
   int32_t seg_mode, wcet_off;  // RT_SEG_*, WCET gate disabled (baselines)
   int32_t host_pages, swap_us_per_page;  // KV eviction to host (R-EVICT); 0 pages = off
+  int32_t stop_grammar, word_us;         // RT_GRAMMAR_* (NEXT-4)
+  const int16_t* tok_class;              // [vocab]
+  const int32_t* skill_base_us;          // [RT_MAX_SKILL_NAMES]
+  const int32_t* skill_unit_us;
   int32_t* hfree_stack;        // [host_pages] host free stack (top = end, pops 0, 1, 2, ...)
   int4* swap;                  // [swap_cap] (dir 0 evict / 1 restore, task, device page, host page)
   int32_t swap_cap;

@@ -139,6 +139,9 @@ __global__ void k_apply_submits(SchedParams p, const SubmitRec* recs, const int3
     T.holder[i] = 0;
     T.evicted[i] = 0;
     T.n_hpages[i] = 0;
+    T.dfa_s[i] = 0;
+    T.dfa_n[i] = 0;
+    T.dfa_v[i] = 0;
     T.argmax_last[i] = -1;
     __threadfence();
     T.state[i] = T_PENDING;
@@ -766,11 +769,46 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_post(SchedParams p) 
     T.pending[task] = tok;
     int64_t sx = T.seg_exec[task];
     int nsk = T.n_skills[task];
-    const int sk = p.tok_skill[tok];
-    if (sk >= 0) {
-      sx += p.tok_exec[tok];
-      ++nsk;
+    int sk = -1;  // >= 0: this token completes an executable unit (a segment boundary candidate)
+    if (p.stop_grammar == RT_GRAMMAR_TOKEN) {
+      sk = p.tok_skill[tok];
+      if (sk >= 0) sx += p.tok_exec[tok];
+    } else if (p.stop_grammar == RT_GRAMMAR_SKILL) {
+      // DFA of  name ( digits ) ;  (the paper's regex over detokenized text)
+      const int cls = p.tok_class[tok];
+      int ds = T.dfa_s[task], dn = T.dfa_n[task], dv = T.dfa_v[task];
+      if (cls >= 1 && cls <= RT_MAX_SKILL_NAMES) {
+        ds = 1;
+        dn = cls - 1;
+        dv = 0;
+      } else if (cls == RT_TC_LPAREN) {
+        ds = ds == 1 ? 2 : 0;
+      } else if (cls >= RT_TC_DIGIT0 && cls < RT_TC_DIGIT0 + 10) {
+        if (ds == 2 || ds == 3) {
+          ds = 3;
+          dv = min(dv * 10 + (cls - RT_TC_DIGIT0), 1000000);
+        } else {
+          ds = 0;
+        }
+      } else if (cls == RT_TC_RPAREN) {
+        ds = (ds == 2 || ds == 3) ? 4 : 0;
+      } else if (cls == RT_TC_SEMI && ds == 4) {
+        sk = dn;
+        sx += (int64_t)p.skill_base_us[dn] + (int64_t)p.skill_unit_us[dn] * dv;
+        ds = 0;
+      } else {
+        ds = 0;
+      }
+      T.dfa_s[task] = ds;
+      T.dfa_n[task] = dn;
+      T.dfa_v[task] = dv;
+    } else {  // chatbot: reading time per word, sentence / paragraph ends
+      const int cls = p.tok_class[tok];
+      // a word-bearing token (word, skill name, digit) adds reading time
+      if (cls == RT_TC_WORD || (cls >= 1 && cls < RT_TC_DIGIT0 + 10)) sx += p.word_us;
+      if (cls == RT_TC_PARA_END || (cls == RT_TC_SENT_END && p.stop_grammar == RT_GRAMMAR_SENTENCE)) sk = 0;
     }
+    if (sk >= 0) ++nsk;
     // EOS > MAXNEW > SKILL_WINDOW > CAP; STREAM: no CAP below RT_SEG_MAX_TOKENS; NONE: no
     // skill boundary either (the comparison systems, rt.h RT_SEG_*)
     const int cap = p.seg_mode == RT_SEG_SUSPEND ? p.max_seg_tokens : RT_SEG_MAX_TOKENS;

@@ -63,6 +63,8 @@ class rt_config(C.Structure):
         ("tok_skill", C.c_void_p), ("tok_exec_min_us", C.c_void_p), ("eos_id", C.c_int32),
         ("flags", C.c_int32), ("capture_layer", C.c_int32), ("seg_mode", C.c_int32), ("wcet_off", C.c_int32),
         ("host_pages", C.c_int32), ("swap_us_per_page", C.c_int32),
+        ("stop_grammar", C.c_int32), ("tok_class", C.c_void_p), ("skill_base_us", C.c_void_p),
+        ("skill_unit_us", C.c_void_p), ("word_us", C.c_int32),
     ]
 
 
@@ -181,6 +183,14 @@ class Engine:
         c.flags, c.capture_layer = flags, capture_layer
         c.seg_mode, c.wcet_off = p.seg_mode, p.wcet_off
         c.host_pages, c.swap_us_per_page = p.host_pages, p.swap_us_per_page
+        c.stop_grammar, c.word_us = p.stop_grammar, p.word_us
+        if getattr(vocab, "tok_class", None) is not None:   # synth.grammar.GrammarVocab (NEXT-4)
+            self._cls = np.ascontiguousarray(vocab.tok_class, dtype=np.int16)
+            self._sbase = np.ascontiguousarray(vocab.skill_base_us, dtype=np.int32)
+            self._sunit = np.ascontiguousarray(vocab.skill_unit_us, dtype=np.int32)
+            c.tok_class = self._cls.ctypes.data
+            c.skill_base_us = self._sbase.ctypes.data
+            c.skill_unit_us = self._sunit.ctypes.data
         self.cfg = c
         self.shape, self.params, self.vocab = shape, params, vocab
         h = C.c_void_p()

@@ -97,6 +97,8 @@ class EngineParams:
     wcet_off: int = 0               # 1: no WCET admission gate (the baselines)
     host_pages: int = 0             # host KV pages for eviction (0: off)
     swap_us_per_page: int = 0       # VIRTUAL clock cost of one evicted / restored page
+    stop_grammar: int = 0           # rt.h RT_GRAMMAR_*
+    word_us: int = 200000           # chatbot reading time per word (300 wpm)
     extra: dict = field(default_factory=dict)
 
     def as_dict(self):

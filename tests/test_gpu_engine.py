@@ -605,3 +605,31 @@ def test_projection_chain_matches_per_projection_launches(rt, monkeypatch):
     scale = max(float(np.abs(b[0]).max()) for b in lp)
     assert worst_q < 5e-2, worst_q          # q of layer 1 (bf16, |q| ~ O(1))
     assert worst_l < 2e-2 * max(1.0, scale), (worst_l, scale)
+
+
+@pytest.mark.parametrize("grammar", [1, 2, 3])
+def test_sched_parity_stop_grammars(rt, grammar):
+    """NEXT-4 on the device: the DFA / chat stop checker against the oracle's regex over the
+    detokenized text, bit-exact segments every round, on
+    (a) generated robot plans / chat text and (b) fuzz scripts of random special tokens
+    (names, parentheses, digits, ";", words, sentence ends) that exercise every near miss."""
+    from synth.grammar import make_grammar_vocab, robot_plan, chat_text
+    gv = make_grammar_vocab(512)
+    p = engine_params("paper-4090", max_batch=8, max_tasks=256, max_ctx=256, n_pages=256, stop_grammar=grammar,
+                      max_seg_tokens=12)
+    eng = rt.Engine(None, p, gv)
+    ora = OracleEngine(p, gv.tok_skill, gv.tok_exec_min_us, gv.eos_id, gv.vocab, grammar=gv)
+    rng = np.random.default_rng(grammar)
+    special = [t for t in range(gv.words[1], gv.eos_id)] + list(range(0, 8))
+    for i in range(48):
+        if i % 2 == 0:
+            script = robot_plan(gv, rng, n_stmts=4) if grammar == 1 else chat_text(gv, rng)
+        else:
+            script = np.array([special[int(x)] for x in rng.integers(0, len(special), 60)] + [gv.eos_id])
+        prompt = rng.integers(0, gv.words[1], 20)
+        arr = int(i * 20000)
+        a = eng.submit(i % 16, prompt, arr, 1_000_000, -2.0, 1.0, 0, len(script), script=script)
+        b = ora.submit(i % 16, prompt, arr, 1_000_000, -2.0, 1.0, 0, len(script), script=script)
+        assert a == b
+    n, segs = lockstep(eng, ora, max_rounds=20000, check_every=7)
+    assert sum(1 for s in segs if s["reason"] == 3) > 20
