@@ -24,9 +24,11 @@ def utility(beta, alpha, ert_us, w_us):
     return beta if beta <= y else y
 
 
-def report(segments, requests, vocab, net_us=8000, seed=0):
+def report(segments, requests, vocab, net_us=8000, seed=0, exec_from="tokens"):
     """segments: rt_poll_segment records; requests: {rid: dict(arrival_us, beta, alpha,
-    ert_us, cls)}.  Returns per-class means and totals over completed requests."""
+    ert_us, cls)}.  Returns per-class means and totals over completed requests.
+    exec_from="est": a segment executes for its est_exec_us (multi-token stop grammars, e.g.
+    the chatbot's reading time) instead of sampled per-skill durations."""
     by_rid = {}
     for s in segments:
         by_rid.setdefault(s["request_id"], []).append(s)
@@ -40,8 +42,8 @@ def report(segments, requests, vocab, net_us=8000, seed=0):
         e_tot = 0
         ordinal = 0
         for s in sorted(segs, key=lambda s: s["k"]):
-            e = 0
-            for tok in s["tokens"]:
+            e = s["est_exec_us"] if exec_from == "est" else 0
+            for tok in (s["tokens"] if exec_from != "est" else ()):
                 if vocab.tok_skill[tok] >= 0:
                     alts = vocab.realized[tok]
                     e += alts[_mix((seed ^ (rid << 32) ^ ordinal) & M64) % len(alts)]

@@ -42,6 +42,13 @@ SYSTEMS = {
     "Seg-EDF": dict(policy=POLICY_EDF, seg_mode=SEG_SUSPEND, wcet_off=0),
     "Ours (PUD)": dict(policy=POLICY_PUD, seg_mode=SEG_SUSPEND, wcet_off=0),
 }
+# chatbot (fig:chatbot): story generation read at 300 wpm; segments end at
+# paragraphs (Ours-Para) or sentences (Ours-Sen) instead of skills; TUF of normal robot tasks
+CHAT_SYSTEMS = {
+    "vLLM": dict(policy=POLICY_FCFS, seg_mode=SEG_NONE, wcet_off=1, stop_grammar=2),
+    "Ours-Para": dict(policy=POLICY_PUD, seg_mode=SEG_SUSPEND, wcet_off=0, stop_grammar=3, max_seg_tokens=16),
+    "Ours-Sen": dict(policy=POLICY_PUD, seg_mode=SEG_SUSPEND, wcet_off=0, stop_grammar=2, max_seg_tokens=16),
+}
 WORKLOADS = {  # agents, EPS, max TPE, duration s, trace pool, prompt length
     "WID1": (25, 0.25, 8, 260.0, range(1, 9), 1300),
     "WID2": (42, 0.25, 16, 300.0, range(1, 9), 1300),
@@ -119,6 +126,60 @@ def summarize(segs, rids, vocab, net_us):
     return rep
 
 
+def chat_workload(gv, seed, n=120, eps=0.5, dur=240.0):
+    """Chat requests: Poisson arrivals, 64-token prompts, 2-3 paragraphs of 2-4 sentences."""
+    import numpy as np
+    from synth.grammar import chat_text
+    rng = np.random.Generator(np.random.PCG64([seed, 77]))
+    t, out = 0.0, []
+    while len(out) < n:
+        t += rng.exponential(1.0 / eps)
+        if t >= dur:
+            break
+        out.append(dict(arrival_us=int(t * 1e6), prompt=rng.integers(0, gv.words[1], 64).astype(np.int32),
+                        plan=chat_text(gv, rng, n_par=int(rng.integers(2, 4)))))
+    return out
+
+
+def run_chat(seed, max_batch, oracle=False):
+    from synth.grammar import make_grammar_vocab
+    gv = make_grammar_vocab(128256)
+    reqs = chat_workload(gv, seed)
+    res = {}
+    for name, kw in CHAT_SYSTEMS.items():
+        p = engine_params("paper-4090", max_batch=max_batch, max_tasks=2048, max_ctx=1024, n_pages=1 << 14, **kw)
+        if oracle:
+            from oracle.engine import OracleEngine
+            eng = OracleEngine(p, gv.tok_skill, gv.tok_exec_min_us, gv.eos_id, gv.vocab, grammar=gv)
+        else:
+            from paper_2412_18695_b200 import rt
+            eng = rt.Engine(None, p, gv)
+        rids = {}
+        for i, r in enumerate(reqs):
+            rid = eng.submit(i % 64, r["prompt"], r["arrival_us"], 1_000_000, -2.0, 1.0, 0, len(r["plan"]),
+                             script=r["plan"])
+            rids[rid] = dict(arrival_us=r["arrival_us"], beta=1.0, alpha=-2.0, ert_us=1_000_000, cls="chat")
+        segs = []
+        if oracle:
+            eng.run_until_idle(max_rounds=2_000_000)
+            segs = eng.poll()
+        else:
+            done = set()
+            for k in range(2_000_000):
+                eng.step()
+                if k % 64 == 63:
+                    new = eng.poll()
+                    segs += new
+                    done |= {s["request_id"] for s in new if s["reason"] in (1, 2)}
+                    if len(done) == len(reqs):
+                        break
+            segs += eng.poll()
+            eng.close()
+        rep = metrics.report(segs, rids, gv, net_us=p.net_us, exec_from="est")
+        res[name] = {k: rep[k] for k in ("mean_utility", "mean_response_s", "mean_waiting_s", "n")}
+    return dict(n_requests=len(reqs), systems=res)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workloads", default="WID1,WID2,WID3,ARM")
@@ -128,6 +189,7 @@ def main():
     ap.add_argument("--json", default=None)
     ap.add_argument("--no-prefix", action="store_true", help="prefill every prompt in full")
     ap.add_argument("--oracle-only", action="store_true", help="CPU oracle only (no GPU)")
+    ap.add_argument("--chat", action="store_true", help="also the chatbot comparison (NEXT-4 grammars)")
     a = ap.parse_args()
     vocab = make_vocab(128256)
     out = dict(clock="paper-4090 VIRTUAL (PAPER.md:76, SURVEY AMB-24)", max_batch=a.max_batch,
@@ -172,6 +234,11 @@ def main():
         r = w["utility_ratio_vs_vllm"]
         print(f"  PUD vs vLLM: utility x{r:.2f}" if r is not None else "  PUD vs vLLM: utility ratio n/a",
               f", waiting -{100 * w['waiting_reduction_vs_vllm']:.0f}%")
+    if a.chat:
+        out["chat"] = run_chat(a.seed, a.max_batch, oracle=a.oracle_only)
+        print(f"== CHAT (story generation, 300 wpm reading): {out['chat']['n_requests']} requests")
+        for sname, rep in out["chat"]["systems"].items():
+            print(f"  {sname:12s} {rep['mean_utility']:8.3f} {rep['mean_response_s']:10.3f} {rep['mean_waiting_s']:10.3f}")
     if a.json:
         json.dump(out, open(a.json, "w"), indent=1)
 
