@@ -37,6 +37,7 @@ AGENTS_PER_GPU = 64
 PROMPT = 1300            # drone prompt (170.35 MB / 128 KiB per token)
 PREFIX = 1216            # its fixed, server-stored part (DESIGN R-PFX): 76 pages
 MAX_CTX = 2048
+SEG_BYTES = 560          # sizeof(rt_segment): ids, range, counts, times + 128 token slots
 TRACE_POOL = list(range(1, 9))   # drone traces 1-8 (tab:task_list)
 
 
@@ -165,7 +166,7 @@ def run_ours(args, rank, world, dist):
 
     # ---- setup: every agent's request admitted and prefilled (contexts resident)
     K, W = args.steps, args.warmup
-    plan_len = W + K + 16
+    plan_len = W + 2 * K + 16   # two passes of K rounds (throughput, then attention roofline)
     reqs = {}
     for j in range(B):
         agent = rank + world * j
@@ -183,6 +184,10 @@ def run_ours(args, rank, world, dist):
         eng.step(now())
     eng.poll()
     eng.sync()
+    # pass A (the timed region of `value`): no per-kernel CUDA events — the events around each
+    # attention launch sit between dependent kernels and cost their programmatic-dependent-
+    # launch overlap (~0.45 ms per round, tools/timing_overhead.py)
+    eng.set_timing(False)
     eng.reset_stats()
     if dist:
         dist.barrier()
@@ -199,8 +204,21 @@ def run_ours(args, rank, world, dist):
         ms = eng.elapsed_ms()
         clk.window(t_lo, time.perf_counter())
     torch.cuda.synchronize()
-    st = eng.stats()
+    st_a = eng.stats()
     segs_timed = eng.poll()
+    # pass B: the same K rounds again with CUDA events on the engine stream around every
+    # attention launch (the graded kernel's launch durations for `roofline`)
+    eng.set_timing(True)
+    eng.reset_stats()
+    for _ in range(K):
+        eng.step(now())
+    eng.sync()
+    eng.step(now())          # harvests the last round's events
+    eng.sync()
+    st = eng.stats()
+    st["kernel_launches"], st["rounds"] = st_a["kernel_launches"], st_a["rounds"]
+    eng.poll()
+    eng.set_timing(False)
     if dist:
         t = torch.tensor([ms], dtype=torch.float64, device="cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -227,7 +245,10 @@ def run_ours(args, rank, world, dist):
                 "(ncu --set full, same C2 launch: B=64, ctx~1310, 8 kv heads)",
                 "alg_bytes_per_launch": st["attn_bytes"] / max(st["attn_launches"], 1),
                 "ms_per_launch": st["attn_ms"] / max(st["attn_launches"], 1),
-                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if not pk.get("fallback") else "fallback"}
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs" if not pk.get("fallback") else "fallback",
+                "timing": "CUDA events around every attention launch on the engine stream, second pass of "
+                          "K rounds right after the value pass (the events cost PDL overlap, so `value` is "
+                          "timed without them)"}
     step_roof = {"alg_bytes_per_step": step_bytes, "achieved_gbs": step_bytes / (ms / K / 1e3) / 1e9,
                  "frac": step_bytes / (ms / K / 1e3) / 1e9 / pk["hbm_gbs"],
                  "attn_share_of_step": st["attn_ms"] / max(st["step_ms"], 1e-9)}
@@ -335,7 +356,7 @@ def run_e2e(args, eng, vocab, p, rank, world, now, dist, reqs, prefix=None, star
         h2d += submit(agent)
     for _ in range(K):
         segs = eng.poll()
-        d2h += 112 * len(segs) + 64
+        d2h += SEG_BYTES * len(segs) + 64
         seg_all += segs
         for s in segs:
             if s["reason"] in (1, 2):
@@ -344,7 +365,7 @@ def run_e2e(args, eng, vocab, p, rank, world, now, dist, reqs, prefix=None, star
         tok += info["n_running"]
     segs = eng.poll()
     seg_all += segs
-    d2h += 112 * len(segs)
+    d2h += SEG_BYTES * len(segs)
     eng.sync()
     el = time.perf_counter() - t_start
     if dist:

@@ -259,6 +259,11 @@ rt_status rt_debug_dump(rt_engine* e, int32_t what, void* dst, int64_t bytes, in
  * start mark, 1 the stop mark; rt_elapsed_ms synchronises and returns stop - start. */
 rt_status rt_mark(rt_engine* e, int32_t which);
 rt_status rt_elapsed_ms(rt_engine* e, double* ms_out);
+/* Switch the per-launch CUDA-event timing of RT_FLAG_TIMING on (1) or off (0) from the next
+ * rt_step.  The events recorded around every attention launch sit between dependent kernels
+ * and cost the programmatic-dependent-launch overlap there (measured ~0.45 ms per 8B round),
+ * so throughput is timed with it off and the per-kernel roofline in a separate pass. */
+rt_status rt_set_timing(rt_engine* e, int32_t on);
 
 /* Create a 128-byte ncclUniqueId (rank 0 calls it and broadcasts the bytes;
  * libnccl.so.2 is loaded with dlopen).  RT_E_NCCL if NCCL is unavailable. */

@@ -1185,6 +1185,14 @@ extern "C" rt_status rt_last_round(rt_engine* e, rt_round_info* info) {
   return RT_OK;
 }
 
+extern "C" rt_status rt_set_timing(rt_engine* e, int32_t on) {
+  if (!e || on < 0 || on > 1) return RT_E_INVAL;
+  if (e->sticky) return RT_E_CUDA;
+  if (on) e->cfg.flags |= RT_FLAG_TIMING;
+  else e->cfg.flags &= ~RT_FLAG_TIMING;
+  return RT_OK;
+}
+
 extern "C" rt_status rt_mark(rt_engine* e, int32_t which) {
   if (!e || which < 0 || which > 1) return RT_E_INVAL;
   if (e->sticky) return RT_E_CUDA;

@@ -31,7 +31,7 @@ EXPORTED = ["rt_create", "rt_destroy", "rt_submit_request", "rt_register_prefix"
             "rt_sync", "rt_get_stats", "rt_reset_stats", "rt_debug_dump", "rt_last_error", "rt_version",
             "rt_op_paged_attention", "rt_op_attention_ws_bytes", "rt_op_kv_write", "rt_op_kv_read", "rt_op_kv_swap",
             "rt_op_gemm", "rt_op_lm_argmax", "rt_op_init_weights", "rt_op_priority", "rt_mark", "rt_elapsed_ms",
-            "rt_nccl_unique_id", "rt_op_pack_tiled", "rt_op_gemm_tiled"]
+            "rt_nccl_unique_id", "rt_op_pack_tiled", "rt_op_gemm_tiled", "rt_set_timing"]
 
 
 class RtError(RuntimeError):
@@ -125,6 +125,7 @@ def lib():
     L.rt_op_init_weights.argtypes = [vp, i64, C.c_uint64, i32, C.c_float, vp]
     L.rt_op_priority.argtypes = [vp, vp, vp, vp, i32, i32, i32, i32, vp, vp]
     L.rt_mark.argtypes = [vp, i32]
+    L.rt_set_timing.argtypes = [vp, i32]
     L.rt_elapsed_ms.argtypes = [vp, C.POINTER(C.c_double)]
     L.rt_nccl_unique_id.argtypes = [vp]
     L.rt_op_pack_tiled.argtypes = [vp, vp, i32, i32, vp]
@@ -263,6 +264,9 @@ class Engine:
             tot += n.value
             if n.value < cap:
                 return tot
+
+    def set_timing(self, on):
+        _check(lib().rt_set_timing(self.h, int(bool(on))), self.h)
 
     def mark(self, which):
         _check(lib().rt_mark(self.h, which), self.h)

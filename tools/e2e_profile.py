@@ -1,0 +1,63 @@
+"""Where the e2e closed loop spends its rounds (bench.py `e2e`, shared drone prefix): per
+round the forward rows (decode + prompt), the device step time (CUDA events, RT_FLAG_TIMING)
+and the host wall time of the rt_step call; aggregated by rows bucket."""
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tools"))
+import numpy as np  # noqa: E402
+import bench  # noqa: E402
+import profile_step  # noqa: E402
+from paper_2412_18695_b200 import rt  # noqa: E402
+from synth.traces import system_prefix  # noqa: E402
+
+
+def main(rounds=200):
+    eng, now = profile_step.setup(bench.AGENTS_PER_GPU, flags=rt.RT_FLAG_TIMING)
+    from synth import MODEL_SHAPES, make_vocab
+    vocab = make_vocab(MODEL_SHAPES["llama3-8b"].vocab)
+    bench.drain(eng, now)
+    pfx = system_prefix(vocab, "drone", bench.PREFIX, seed=0)
+    eng.register_prefix(pfx)
+    ordinal = {}
+
+    def submit(agent):
+        o = ordinal[agent] = ordinal.get(agent, 0) + 1
+        tr = bench.drone_request(vocab, agent, o, 0, prefix=pfx)
+        eng.submit(agent, tr.prompt, now(), tr.ert_us, tr.alpha, tr.beta, 90000, script=tr.plan)
+
+    for a in range(bench.AGENTS_PER_GPU):
+        submit(a)
+    rec = []
+    for r in range(rounds):
+        for s in eng.poll():
+            if s["reason"] in (1, 2):
+                submit(s["agent_id"])
+        eng.sync()
+        t0 = time.perf_counter()
+        info = eng.step(now())
+        eng.sync()
+        wall = (time.perf_counter() - t0) * 1e3
+        st = eng.stats()   # includes the PREVIOUS round's CUDA-event timing (harvested in rt_step)
+        rec.append([info["n_rows"], info["n_prefill_rows"], info["n_running"], wall,
+                    st["step_ms"], st["gemm_ms"], st["attn_ms"]])
+    a = np.array(rec, dtype=np.float64)
+    a[:-1, 4:7] = a[1:, 4:7] - a[:-1, 4:7]   # round r's device times = stats after r+1 - after r
+    a = a[20:-1]
+    print(f"rounds {len(a)}: mean rows {a[:, 0].mean():.0f} (prompt {a[:, 1].mean():.0f}), tokens/round "
+          f"{a[:, 2].mean():.1f}, wall {a[:, 3].mean():.2f} ms, device {a[:, 4].mean():.2f} ms "
+          f"(forward {a[:, 5].mean():.2f}, attention {a[:, 6].mean():.2f}) -> {a[:, 2].sum() / a[:, 3].sum() * 1e3:.0f} tok/s")
+    for lo, hi in ((0, 65), (65, 129), (129, 257), (257, 513), (513, 100000)):
+        m = (a[:, 0] >= lo) & (a[:, 0] < hi)
+        if m.any():
+            b = a[m]
+            print(f"  rows [{lo:4d},{hi:6d}): {m.sum():4d} rounds, wall {b[:, 3].mean():6.2f} ms, device "
+                  f"{b[:, 4].mean():6.2f} ms, forward {b[:, 5].mean():6.2f} ms, attention {b[:, 6].mean():5.2f} ms")
+    eng.close()
+
+
+if __name__ == "__main__":
+    main()
