@@ -56,7 +56,7 @@ struct GemmCfg {
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int STAGES = BN <= 64 ? 4 : (BN == 128 ? 3 : 4);
   static constexpr int CTAS_PER_SM = BN <= 128 ? 2 : 1;
-  static constexpr int TMEM_COLS = BN < 32 ? 32 : BN;
+  static constexpr int TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;  // power of 2
   static constexpr int META = 3 * BN * 4;                       // per-column pos / page / rms scale
   static constexpr int RED = 2 * 4 * BN * 4;                    // per-warp column partials (val, idx)
   static constexpr int XP = 16 * 128 * 4;                       // prefetched epilogue inputs
@@ -577,7 +577,9 @@ __global__ void __launch_bounds__(kGemmThreads, GemmCfg<BN>::CTAS_PER_SM)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int S = gridDim.x;                 // cluster = the S split-K CTAs of one tile
   const int rank = S > 1 ? (int)cluster_rank() : 0;
-  const int m_tile = blockIdx.y, n_tile = blockIdx.z;
+  // several n-tiles (prefill rows > BN): the n-tiles of one m-tile are adjacent in the grid
+  // (blockIdx.y) so they run together and the second reads the weight tile from L2
+  const int m_tile = g.nt_fast ? blockIdx.z : blockIdx.y, n_tile = g.nt_fast ? blockIdx.y : blockIdx.z;
   const int kb0 = (int)(((long long)g.kb_total * rank) / S);
   const int kb1 = (int)(((long long)g.kb_total * (rank + 1)) / S);
   const int nkb = kb1 - kb0;
@@ -1207,10 +1209,32 @@ bool make_gemm_act_maps(GemmTmaSet* out, const void* base, int K, int rows_cap) 
   return make_tma_2d_bf16(&out->m32, base, K, rows_cap, kBK, 32) &&
          make_tma_2d_bf16(&out->m64, base, K, rows_cap, kBK, 64) &&
          make_tma_2d_bf16(&out->m128, base, K, rows_cap, kBK, 128) &&
+         make_tma_2d_bf16(&out->m160, base, K, rows_cap, kBK, 160) &&
+         make_tma_2d_bf16(&out->m192, base, K, rows_cap, kBK, 192) &&
          make_tma_2d_bf16(&out->m256, base, K, rows_cap, kBK, 256);
 }
 
-int gemm_bn(int N) { return N <= 32 ? 32 : N <= 64 ? 64 : N <= 128 ? 128 : 256; }
+// N tile (UMMA N) for N activation rows.  Up to 128 rows the powers of two (decode); above,
+// the width among {160, 192, 256} with the least padded MMA work (n-tiles x BN), then fewer
+// n-tiles: prefill-heavy rounds are tensor-bound and a padded column costs a full MMA column
+// (tools/gemm_sweep_n.py: N = 320 on 2 x 256 ran at the speed of N = 512).
+int gemm_bn(int N) {
+  if (N <= 32) return 32;
+  if (N <= 64) return 64;
+  if (N <= 128) return 128;
+  int best = 256, best_t = INT_MAX;
+  long long best_w = LLONG_MAX;
+  for (int bn : {160, 192, 256}) {
+    const int t = (N + bn - 1) / bn;
+    const long long w = (long long)t * bn;
+    if (w < best_w || (w == best_w && t < best_t)) {
+      best = bn;
+      best_w = w;
+      best_t = t;
+    }
+  }
+  return best;
+}
 
 template <int BN, int MODE>
 static void ensure_attrs() {
@@ -1246,7 +1270,8 @@ static cudaError_t launch_bn(const TmaMap& b, const GemmArgs& g, int S, cudaStre
   using C = GemmCfg<BN>;
   ensure_attrs<BN, MODE>();
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(S, (g.M + 127) / 128, (g.N + BN - 1) / BN);
+  const int mt = (g.M + 127) / 128, nt = (g.N + BN - 1) / BN;
+  cfg.gridDim = g.nt_fast ? dim3(S, nt, mt) : dim3(S, mt, nt);
   cfg.blockDim = dim3(kGemmThreads);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = s;
@@ -1284,12 +1309,17 @@ static cudaError_t launch_mode(const GemmTmaSet& x, const GemmArgs& g, int bn, i
   if (bn == 32) return launch_bn<32, MODE>(x.m32, g, S, s);
   if (bn == 64) return launch_bn<64, MODE>(x.m64, g, S, s);
   if (bn == 128) return launch_bn<128, MODE>(x.m128, g, S, s);
+  if (bn == 160) return launch_bn<160, MODE>(x.m160, g, S, s);
+  if (bn == 192) return launch_bn<192, MODE>(x.m192, g, S, s);
   return launch_bn<256, MODE>(x.m256, g, S, s);
 }
 
 cudaError_t launch_gemm_epi(const bf16* w_tiled, const GemmTmaSet& x, GemmArgs g, int splits, cudaStream_t s) {
   g.w = w_tiled;
-  g.l2_evict_first = l2_hint_enabled() ? 1 : 0;
+  // weights are read once per n-tile; with several n-tiles the later ones should hit L2
+  const int n_tiles = (g.N + gemm_bn(g.N) - 1) / gemm_bn(g.N);
+  g.nt_fast = (n_tiles > 1 && getenv("RT_NO_NT_FAST") == nullptr) ? 1 : 0;
+  g.l2_evict_first = (l2_hint_enabled() && n_tiles == 1) ? 1 : 0;
   {
     static const int ns = getenv("RT_EPI_BACKOFF_NS") ? atoi(getenv("RT_EPI_BACKOFF_NS")) : 0;
     g.epi_backoff_ns = ns;

@@ -85,7 +85,7 @@ struct TmaMap {
 bool make_tma_2d_bf16(TmaMap* out, const void* base, uint64_t inner, uint64_t rows, uint32_t box_inner,
                       uint32_t box_rows);
 struct GemmTmaSet {       // activation operand: one map per supported N tile
-  TmaMap m32, m64, m128, m256;
+  TmaMap m32, m64, m128, m160, m192, m256;
   int rows_cap;
 };
 bool make_gemm_act_maps(GemmTmaSet* out, const void* base, int K, int rows_cap);
@@ -125,6 +125,7 @@ struct GemmArgs {
   int pf_S, pf_m_tiles, pf_kb_total, pf_kb;
   int l2_evict_first;  // set by launch_gemm_epi: weight tiles are read once per step
   int epi_backoff_ns;  // set by launch_gemm_epi: nanosleep between the epilogue warps' polls
+  int nt_fast;         // set by launch_gemm_epi: grid (S, n-tiles, m-tiles) instead of (S, m, n)
 };
 // fill g.pf_* for a next launch of weights w [M x K] at N columns (splits <= 0: auto),
 // prefetching at most budget_bytes in total

@@ -90,7 +90,8 @@ extern "C" rt_status rt_op_kv_read(const void* d_pool, void* d_out, int32_t n_pa
 
 extern "C" rt_status rt_op_gemm(const void* d_w, const void* d_x, float* d_out, int32_t M, int32_t N, int32_t K,
                                 int32_t n_cap, int32_t splits, void* stream) {
-  if (M < 1 || N < 1 || K < 64 || K % 64 || n_cap < N || splits < 1 || splits > K / 64) return RT_E_INVAL;
+  // splits <= 0: the engine's choice (rt_ops.h)
+  if (M < 1 || N < 1 || K < 64 || K % 64 || n_cap < N || splits > K / 64) return RT_E_INVAL;
   GemmTmaSet xm;
   if (!make_gemm_act_maps(&xm, d_x, K, n_cap)) return RT_E_CUDA;
   bf16* wt = nullptr;  // the engine keeps weights UMMA-tiled; pack the caller's row-major W
