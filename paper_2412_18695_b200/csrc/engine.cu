@@ -117,6 +117,9 @@ struct rt_engine {
   unsigned* d_chain_done = nullptr;
   unsigned chain_base[kChainMaxJobs] = {};
   int chain_grid_n = 0;
+  float* d_sk_ws = nullptr;      // stream-K partial tiles (prefill projections, N > 128 rows)
+  unsigned* d_sk_cnt = nullptr;  // stream-K tile tickets
+  int sk_cnt_cap = 0;
   int chain_pf_ahead = 16;  // RT_CHAIN_PF
   // submissions
   SubmitRec* h_recs = nullptr;
@@ -513,6 +516,13 @@ static rt_status create_impl(rt_engine* e, const rt_config* cfg) {
     if (!ok) return done(fail(e, RT_E_CUDA, "cuTensorMapEncodeTiled failed (activations)"));
     e->ev_attn.resize(2 * L);
     for (auto& ev : e->ev_attn) cudaEventCreate(&ev);
+    // stream-K workspace of the prefill projections (gemm_tc.cu k_gemm_sk; opt-in RT_STREAMK=1)
+    if (getenv("RT_STREAMK") && atoi(getenv("RT_STREAMK")) != 0) {
+      const int max_mt = (std::max(std::max(e->qkv_dim, d), 2 * ff) + 127) / 128;
+      e->sk_cnt_cap = max_mt * ((R + 159) / 160);
+      CK(e, dalloc(e, &e->d_sk_ws, (size_t)gemm_sk_ws_floats()));
+      CK(e, dalloc(e, &e->d_sk_cnt, (size_t)e->sk_cnt_cap));
+    }
     // projection chain for decode rounds of <= 64 rows: OPT-IN (RT_CHAIN=1).  Measured at
     // C2 it is slower than one launch per projection (182 vs ~104 us per layer, DESIGN.md
     // §9): each job boundary pays a chain of loaded-HBM latencies (store fence, ticket,
@@ -847,6 +857,9 @@ static rt_status forward(rt_engine* e, const HostMailbox& plan) {
       g.M = M;
       g.N = n;
       g.K = K;
+      g.sk_ws = e->d_sk_ws;
+      g.sk_cnt = e->d_sk_cnt;
+      g.sk_cnt_cap = e->sk_cnt_cap;
       launch_gemm_epi(w, x, g, 0, s);
       ++launches;
     };

@@ -1176,6 +1176,273 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_chain(const __grid_constant
   }
 }
 
+// ============================================================ stream-K projection (prefill)
+// Rounds with prompt rows run the projections at N = 130 .. 8192 rows, where the GEMM is
+// tensor-bound and one tile per CTA quantises badly on 148 SMs (gate/up at N = 256: 224
+// tiles = 1.5 waves; N = 320 on 160-wide tiles: 448 tiles = 3.03 waves).  k_gemm_sk: one
+// CTA per SM; the T x kb k-block iterations of all tiles (n-tiles of an m-tile adjacent, so
+// the second reads the weight tile from L2) are split evenly over the CTAs (stream-K).  A
+// CTA accumulates each tile segment of its range in one of two TMEM buffers (the epilogue of
+// segment i overlaps the MMAs of segment i + 1).  A segment that is not a whole tile stores
+// its fp32 partial to the CTA's workspace slot (0: the tile its range starts in, 1: the tile
+// it ends in) and takes a ticket; the last contributor sums the partials in contributor order
+// (deterministic) from double-buffered 32 KB bulk loads and runs the fused epilogue in
+// 64-column chunks.
+namespace sk {
+constexpr int STAGES = 3;
+constexpr int A_BYTES = 128 * kBK * 2;
+constexpr int CHUNK = 64;                       // epilogue columns per staging buffer
+constexpr int STG_BYTES = CHUNK * 128 * 4;      // 32 KB
+template <int BN>
+struct Cfg {
+  static constexpr int B_BYTES = BN * kBK * 2;
+  static constexpr int TMEM_COLS = 2 * BN <= 256 ? 256 : 512;
+  static constexpr int CTL = 256;
+  static constexpr int META = 3 * BN * 4;
+  static constexpr int RED = 2 * 4 * BN * 4;
+  static constexpr int SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + 2 * STG_BYTES + CTL + META + RED;
+  static_assert(SMEM <= 227 * 1024, "stream-K smem");
+  static_assert(BN % CHUNK == 0 || BN == 160, "chunking");
+};
+}  // namespace sk
+
+struct SkArgs {
+  int P;             // CTAs
+  int n_tiles;       // tiles along N (BN rows each)
+  float* ws;         // [P][2][BN][128] partial tiles
+  unsigned* cnt;     // [m_tiles * n_tiles] zero-initialised, self-resetting tickets
+};
+
+template <int BN, int MODE>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    k_gemm_sk(const __grid_constant__ TmaMap tmB, GemmArgs g, SkArgs a) {
+  using C = sk::Cfg<BN>;
+  using namespace sk;
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  unsigned char* sA = smem;
+  unsigned char* sB = smem + STAGES * A_BYTES;
+  float* stg0 = reinterpret_cast<float*>(sB + STAGES * C::B_BYTES);
+  float* stg1 = stg0 + CHUNK * 128;
+  unsigned char* ctl = reinterpret_cast<unsigned char*>(stg1 + CHUNK * 128);
+  uint64_t* full = reinterpret_cast<uint64_t*>(ctl);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* fxbar = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fxbar + 2);
+  int* s_last = reinterpret_cast<int*>(tmem_slot + 1);
+  EpiSmem sm;
+  sm.pos = reinterpret_cast<int*>(ctl + C::CTL);
+  sm.page = sm.pos + BN;
+  sm.inv = reinterpret_cast<float*>(sm.page + BN);
+  sm.redv = reinterpret_cast<float*>(ctl + C::CTL + C::META);
+  sm.redi = reinterpret_cast<int*>(sm.redv + 4 * BN);
+  sm.bn = BN;
+  sm.xp = stg1;  // unused (pre = false)
+  sm.xp_sin = 0;
+  __shared__ long long s_mark[9];
+  sm.mark = s_mark;
+
+  TraceScope tr(TK_GEMM | ((uint32_t)MODE << 8) | (1u << 16));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cta = blockIdx.x, NP = a.P;
+  const int kbt = g.kb_total;
+  const long long I = (long long)g.m_tiles * a.n_tiles * kbt;
+  const int qa = chain::q0(I, cta, NP), qb = chain::q0(I, cta + 1, NP);
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmB);
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 1);
+      mbar_init(&fxbar[i], 1);
+    }
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(C::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) pdl_trigger();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // tile t = m_tile * n_tiles + n_tile (n fastest); iteration q = t * kbt + kb
+      bool waited = false;
+      int t = qa / kbt, kb = qa - (qa / kbt) * kbt;
+      for (int q = qa, n = 0; q < qb; ++q, ++n) {
+        const int st = n % STAGES;
+        if (n >= STAGES) mbar_wait(&empty[st], (uint32_t)(((n / STAGES) & 1) ^ 1));
+        const int m_tile = t / a.n_tiles, n_tile = t - m_tile * a.n_tiles;
+        mbar_arrive_expect_tx(&full[st], A_BYTES + C::B_BYTES);
+        bulk_g2s(sA + st * A_BYTES, g.w + ((size_t)m_tile * kbt + kb) * (128 * kBK), A_BYTES, &full[st]);
+        if (!waited) {  // weights before the previous kernel finishes, activations after
+          pdl_wait();
+          tr.ready();
+          waited = true;
+        }
+        tma_load_2d(sB + st * C::B_BYTES, &tmB, kb * kBK, n_tile * BN, &full[st]);
+        if (++kb == kbt) {
+          kb = 0;
+          ++t;
+        }
+      }
+      if (!waited) pdl_wait();
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = umma_idesc(128, BN);
+      int n = 0, seg = 0;
+      for (int q = qa; q < qb;) {
+        const int t = q / kbt;
+        const int lo = q - t * kbt, hi = min(qb - t * kbt, kbt);
+        const int buf = seg & 1;
+        if (seg >= 2) mbar_wait(&tempty[buf], (uint32_t)(((seg >> 1) - 1) & 1));
+        tc_fence_after();
+        const uint32_t acc = tmem + (uint32_t)(buf * BN);
+        for (int kb = lo; kb < hi; ++kb, ++n) {
+          const int st = n % STAGES;
+          mbar_wait(&full[st], (uint32_t)((n / STAGES) & 1));
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + st * A_BYTES);
+          const uint32_t b0 = smem_u32(sB + st * C::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k)
+            umma_f16(acc, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
+                     (kb > lo || k > 0) ? 1u : 0u);
+          umma_commit(&empty[st]);
+        }
+        umma_commit(&tfull[buf]);
+        ++seg;
+        q = t * kbt + hi;
+      }
+    }
+    __syncwarp();
+  } else {
+    pdl_wait();
+    const int et = (warp & 3) * 32 + lane;
+    const uint32_t tb = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+    const int first_tile = qa / kbt;
+    uint32_t fx_phase[2] = {0u, 0u};
+    int seg = 0;
+    for (int q = qa; q < qb;) {
+      const int t = q / kbt;
+      const int hi = min(qb - t * kbt, kbt);
+      const int buf = seg & 1;
+      const int m_tile = t / a.n_tiles, n_tile = t - m_tile * a.n_tiles;
+      const int n0 = n_tile * BN;
+      const int c_first = chain::owner((long long)t * kbt, I, NP);
+      const int c_last = chain::owner((long long)(t + 1) * kbt - 1, I, NP);
+      const int nc = c_last - c_first + 1;
+      mbar_wait(&tfull[buf], (uint32_t)((seg >> 1) & 1));
+      tc_fence_after();
+      epi_bar();  // the previous segment's epilogue is done with the staging buffers / sm
+      bool run = true;
+      const uint32_t tacc = tb + (uint32_t)(buf * BN);
+      if (nc > 1) {
+        float* mine = a.ws + ((size_t)cta * 2 + (t == first_tile ? 0 : 1)) * (BN * 128);
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 16) {
+          float v[16];
+          tmem_ld16(tacc + (uint32_t)c0, v);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) __stcg(mine + (size_t)(c0 + i) * 128 + et, v[i]);
+        }
+        tc_fence_before();
+        __threadfence();
+        epi_bar();
+        if (et == 0) {
+          mbar_arrive(&tempty[buf]);
+          const unsigned old = atomicAdd(a.cnt + t, 1u);
+          *s_last = (old == (unsigned)(nc - 1)) ? 1 : 0;
+        }
+        epi_bar();
+        run = *s_last != 0;
+        if (run) {
+          __threadfence();
+          if (et == 0) {
+            a.cnt[t] = 0u;
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+          }
+        }
+      }
+      if (run) {
+        column_meta<MODE>(g, sm, m_tile, n0, 0, BN, et);  // per-column metadata of this tile's rows
+        const TileSrc ts0{nullptr, nullptr, 0u, 1, 0, BN, 0, 0, nullptr};
+#pragma unroll 1
+        for (int cb = 0; cb < BN; cb += CHUNK) {
+          const int ce = min(BN, cb + CHUNK);
+          float* stg = stg0;
+          if (nc == 1) {  // whole tile: TMEM -> staging
+#pragma unroll 1
+            for (int c0 = cb; c0 < ce; c0 += 16) {
+              float v[16];
+              tmem_ld16(tacc + (uint32_t)c0, v);
+#pragma unroll
+              for (int i = 0; i < 16; ++i) stg[(c0 - cb + i) * 128 + et] = v[i];
+            }
+          } else {  // sum the nc partials of columns [cb, ce) in contributor order
+            float acc[CHUNK];
+#pragma unroll
+            for (int c = 0; c < CHUNK; ++c) acc[c] = 0.f;
+            const uint32_t bytes = (uint32_t)((ce - cb) * 512);
+            for (int r = 0; r < nc; r += 2) {
+              if (et == 0)
+                for (int b = 0; b < 2 && r + b < nc; ++b) {
+                  const int c = c_first + r + b;
+                  const float* src =
+                      a.ws + ((size_t)c * 2 + (t == chain::q0(I, c, NP) / kbt ? 0 : 1)) * (BN * 128) + (size_t)cb * 128;
+                  mbar_arrive_expect_tx(&fxbar[b], bytes);
+                  bulk_g2s(b ? (void*)stg1 : (void*)stg0, src, bytes, &fxbar[b]);
+                }
+              for (int b = 0; b < 2 && r + b < nc; ++b) {
+                mbar_wait(&fxbar[b], fx_phase[b]);
+                fx_phase[b] ^= 1u;
+                const float* bb = b ? stg1 : stg0;
+#pragma unroll
+                for (int c = 0; c < CHUNK; ++c)
+                  if (cb + c < ce) acc[c] += bb[c * 128 + et];
+              }
+              epi_bar();
+            }
+#pragma unroll
+            for (int c = 0; c < CHUNK; ++c)
+              if (cb + c < ce) stg[c * 128 + et] = acc[c];
+          }
+          epi_bar();
+          TileSrc ts = ts0;
+          ts.P = stg - (size_t)cb * 128;  // the epilogue indexes absolute columns
+          epilogue<MODE>(g, sm, ts, m_tile, n0, cb, ce, et, false);
+          epi_bar();
+        }
+        if (nc == 1) {
+          tc_fence_before();
+          if (et == 0) mbar_arrive(&tempty[buf]);
+        }
+      }
+      ++seg;
+      q = t * kbt + hi;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::TMEM_COLS));
+  }
+}
+
 // ------------------------------------------------------------- host side
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -1314,7 +1581,75 @@ static cudaError_t launch_mode(const GemmTmaSet& x, const GemmArgs& g, int bn, i
   return launch_bn<256, MODE>(x.m256, g, S, s);
 }
 
+static int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <int BN, int MODE>
+static cudaError_t launch_sk_bn(const TmaMap& b, const GemmArgs& g, const SkArgs& a, cudaStream_t s) {
+  using C = sk::Cfg<BN>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_gemm_sk<BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(a.P);
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_gemm_sk<BN, MODE>, b, g, a);
+}
+template <int MODE>
+static cudaError_t launch_sk_mode(const GemmTmaSet& x, const GemmArgs& g, const SkArgs& a, int bn, cudaStream_t s) {
+  if (bn == 160) return launch_sk_bn<160, MODE>(x.m160, g, a, s);
+  if (bn == 192) return launch_sk_bn<192, MODE>(x.m192, g, a, s);
+  return launch_sk_bn<256, MODE>(x.m256, g, a, s);
+}
+
+int64_t gemm_sk_ws_floats() { return (int64_t)sm_count() * 2 * 256 * 128; }
+
 cudaError_t launch_gemm_epi(const bf16* w_tiled, const GemmTmaSet& x, GemmArgs g, int splits, cudaStream_t s) {
+  // stream-K for the tensor-bound prefill path (N > 128 rows): OPT-IN (RT_STREAMK=1), when the
+  // caller provides its workspace.  Measured slower than one tile per CTA on every prefill
+  // shape (tools/gemm_sweep_n.py: gate/up N = 256 77.8 vs 65.4 us, down 54.8 vs 33.8 us): its
+  // 3-stage ring at 1 CTA / SM cannot hide the load latency of 48 KB stages and the partial
+  // fixups of the K-heavy down projection cost more than the balance gains
+  if (g.sk_ws && g.sk_cnt && g.N > 128 && g.mode != EPI_ARGMAX && g.K % kBK == 0) {
+    g.w = w_tiled;
+    g.kb_total = g.K / kBK;
+    g.m_tiles = (g.M + 127) / 128;
+    g.l2_evict_first = 0;
+    g.nt_fast = 0;
+    const int bn = gemm_bn(g.N);
+    SkArgs a;
+    a.n_tiles = (g.N + bn - 1) / bn;
+    const long long I = (long long)g.m_tiles * a.n_tiles * g.kb_total;
+    if ((long long)g.m_tiles * a.n_tiles <= g.sk_cnt_cap) {
+      a.P = (int)std::min<long long>(sm_count(), I);
+      a.ws = g.sk_ws;
+      a.cnt = g.sk_cnt;
+      switch (g.mode) {
+        case EPI_STORE: return launch_sk_mode<EPI_STORE>(x, g, a, bn, s);
+        case EPI_QKV: return launch_sk_mode<EPI_QKV>(x, g, a, bn, s);
+        case EPI_RESID: return launch_sk_mode<EPI_RESID>(x, g, a, bn, s);
+        case EPI_SWIGLU: return launch_sk_mode<EPI_SWIGLU>(x, g, a, bn, s);
+        default: break;
+      }
+    }
+  }
   g.w = w_tiled;
   // weights are read once per n-tile; with several n-tiles the later ones should hit L2
   const int n_tiles = (g.N + gemm_bn(g.N) - 1) / gemm_bn(g.N);

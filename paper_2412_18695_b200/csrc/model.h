@@ -126,7 +126,13 @@ struct GemmArgs {
   int l2_evict_first;  // set by launch_gemm_epi: weight tiles are read once per step
   int epi_backoff_ns;  // set by launch_gemm_epi: nanosleep between the epilogue warps' polls
   int nt_fast;         // set by launch_gemm_epi: grid (S, n-tiles, m-tiles) instead of (S, m, n)
+  // stream-K workspace for N > 128 rows (nullable: one tile per CTA): partial tiles
+  // [SMs][2][256][128] fp32 (gemm_sk_ws_floats) and zeroed self-resetting tile tickets
+  float* sk_ws;
+  unsigned* sk_cnt;
+  int sk_cnt_cap;
 };
+int64_t gemm_sk_ws_floats();
 // fill g.pf_* for a next launch of weights w [M x K] at N columns (splits <= 0: auto),
 // prefetching at most budget_bytes in total
 void gemm_set_prefetch(GemmArgs& g, const bf16* w, int M, int N, int K, int splits, int64_t budget_bytes);

@@ -2,6 +2,7 @@
 // device buffers, for per-op parity tests and microbenchmarks.
 #include <cuda_runtime.h>
 #include <math.h>
+#include <stdlib.h>
 #include <algorithm>
 #include "rt_ops.h"
 #include "internal.h"
@@ -127,6 +128,23 @@ extern "C" rt_status rt_op_gemm_tiled(const void* d_w_tiled, const void* d_x, fl
   g.K = K;
   g.mode = EPI_STORE;
   g.out = d_out;
+  // stream-K path for N > 128 (as in the engine): a process-wide workspace on first use
+  static float* sk_ws = nullptr;
+  static unsigned* sk_cnt = nullptr;
+  static int sk_cap = 0;
+  const int need = ((M + 127) / 128) * ((N + 159) / 160);
+  if (N > 128 && splits <= 0 && getenv("RT_STREAMK") && atoi(getenv("RT_STREAMK")) != 0) {
+    if (!sk_ws && cudaMalloc(&sk_ws, (size_t)gemm_sk_ws_floats() * 4) != cudaSuccess) return RT_E_CUDA;
+    if (need > sk_cap) {
+      if (sk_cnt) cudaFree(sk_cnt);
+      sk_cap = std::max(need, 4096);
+      if (cudaMalloc(&sk_cnt, (size_t)sk_cap * 4) != cudaSuccess) return RT_E_CUDA;
+      cudaMemset(sk_cnt, 0, (size_t)sk_cap * 4);
+    }
+    g.sk_ws = sk_ws;
+    g.sk_cnt = sk_cnt;
+    g.sk_cnt_cap = sk_cap;
+  }
   launch_gemm_epi((const bf16*)d_w_tiled, xm, g, splits, (cudaStream_t)stream);
   return last_launch();
 }

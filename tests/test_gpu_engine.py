@@ -257,15 +257,18 @@ def test_submit_errors(rt):
 
 
 # ------------------------------------------------------------- model parity
-@pytest.mark.parametrize("graphs,chain", [(False, False), (True, False), (False, True)])
-def test_tiny_model_e2e_and_per_op(rt, graphs, chain, monkeypatch):
+@pytest.mark.parametrize("graphs,chain,streamk", [(False, False, False), (True, False, False), (False, True, False),
+                                                  (False, False, True)])
+def test_tiny_model_e2e_and_per_op(rt, graphs, chain, streamk, monkeypatch):
     """C1 end to end against the oracle; chain=True runs the decode projections through the
     opt-in persistent projection chain (RT_CHAIN=1; 2 CTAs at these dims, so both the
-    whole-tile and the partial-tile fixup paths run)."""
-    if chain:
-        monkeypatch.setenv("RT_CHAIN", "1")
-    else:
-        monkeypatch.delenv("RT_CHAIN", raising=False)
+    whole-tile and the partial-tile fixup paths run); streamk=True runs the prefill
+    projections (N > 128 rows) through the opt-in stream-K kernel (RT_STREAMK=1)."""
+    for var, on in (("RT_CHAIN", chain), ("RT_STREAMK", streamk)):
+        if on:
+            monkeypatch.setenv(var, "1")
+        else:
+            monkeypatch.delenv(var, raising=False)
     shape = MODEL_SHAPES["tiny"]
     v = make_vocab(shape.vocab)
     p = engine_params("paper-4090", max_batch=4, max_tasks=64, max_ctx=256, n_pages=64)
