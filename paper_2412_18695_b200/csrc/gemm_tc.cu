@@ -579,7 +579,8 @@ __global__ void __launch_bounds__(kGemmThreads, GemmCfg<BN>::CTAS_PER_SM)
   const int rank = S > 1 ? (int)cluster_rank() : 0;
   // several n-tiles (prefill rows > BN): the n-tiles of one m-tile are adjacent in the grid
   // (blockIdx.y) so they run together and the second reads the weight tile from L2
-  const int m_tile = g.nt_fast ? blockIdx.z : blockIdx.y, n_tile = g.nt_fast ? blockIdx.y : blockIdx.z;
+  const int lt = g.tile0 + (int)blockIdx.y;  // linear tile, n-tiles of one m-tile adjacent
+  const int m_tile = lt / g.n_tiles, n_tile = lt - (lt / g.n_tiles) * g.n_tiles;
   const int kb0 = (int)(((long long)g.kb_total * rank) / S);
   const int kb1 = (int)(((long long)g.kb_total * (rank + 1)) / S);
   const int nkb = kb1 - kb0;
@@ -1537,8 +1538,7 @@ static cudaError_t launch_bn(const TmaMap& b, const GemmArgs& g, int S, cudaStre
   using C = GemmCfg<BN>;
   ensure_attrs<BN, MODE>();
   cudaLaunchConfig_t cfg{};
-  const int mt = (g.M + 127) / 128, nt = (g.N + BN - 1) / BN;
-  cfg.gridDim = g.nt_fast ? dim3(S, nt, mt) : dim3(S, mt, nt);
+  cfg.gridDim = dim3(S, g.tile_count, 1);
   cfg.blockDim = dim3(kGemmThreads);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = s;
@@ -1632,7 +1632,6 @@ cudaError_t launch_gemm_epi(const bf16* w_tiled, const GemmTmaSet& x, GemmArgs g
     g.kb_total = g.K / kBK;
     g.m_tiles = (g.M + 127) / 128;
     g.l2_evict_first = 0;
-    g.nt_fast = 0;
     const int bn = gemm_bn(g.N);
     SkArgs a;
     a.n_tiles = (g.N + bn - 1) / bn;
@@ -1653,7 +1652,6 @@ cudaError_t launch_gemm_epi(const bf16* w_tiled, const GemmTmaSet& x, GemmArgs g
   g.w = w_tiled;
   // weights are read once per n-tile; with several n-tiles the later ones should hit L2
   const int n_tiles = (g.N + gemm_bn(g.N) - 1) / gemm_bn(g.N);
-  g.nt_fast = (n_tiles > 1 && getenv("RT_NO_NT_FAST") == nullptr) ? 1 : 0;
   g.l2_evict_first = (l2_hint_enabled() && n_tiles == 1) ? 1 : 0;
   {
     static const int ns = getenv("RT_EPI_BACKOFF_NS") ? atoi(getenv("RT_EPI_BACKOFF_NS")) : 0;
@@ -1662,16 +1660,42 @@ cudaError_t launch_gemm_epi(const bf16* w_tiled, const GemmTmaSet& x, GemmArgs g
   const int bn = gemm_bn(g.N);
   g.kb_total = g.K / kBK;
   g.m_tiles = (g.M + 127) / 128;
+  g.n_tiles = n_tiles;
+  const int tiles = g.m_tiles * n_tiles;
+  const bool auto_split = splits <= 0;
   if (splits <= 0) splits = gemm_choose_splits(g.M, g.N, g.K);
   splits = std::max(1, std::min(splits, std::min(16, g.kb_total)));
-  switch (g.mode) {
-    case EPI_STORE: return launch_mode<EPI_STORE>(x, g, bn, splits, s);
-    case EPI_ARGMAX: return launch_mode<EPI_ARGMAX>(x, g, bn, splits, s);
-    case EPI_QKV: return launch_mode<EPI_QKV>(x, g, bn, splits, s);
-    case EPI_RESID: return launch_mode<EPI_RESID>(x, g, bn, splits, s);
-    case EPI_SWIGLU: return launch_mode<EPI_SWIGLU>(x, g, bn, splits, s);
-    default: return cudaErrorInvalidValue;
+  auto launch = [&](int tile0, int count, int S) -> cudaError_t {
+    g.tile0 = tile0;
+    g.tile_count = count;
+    switch (g.mode) {
+      case EPI_STORE: return launch_mode<EPI_STORE>(x, g, bn, S, s);
+      case EPI_ARGMAX: return launch_mode<EPI_ARGMAX>(x, g, bn, S, s);
+      case EPI_QKV: return launch_mode<EPI_QKV>(x, g, bn, S, s);
+      case EPI_RESID: return launch_mode<EPI_RESID>(x, g, bn, S, s);
+      case EPI_SWIGLU: return launch_mode<EPI_SWIGLU>(x, g, bn, S, s);
+      default: return cudaErrorInvalidValue;
+    }
+  };
+  // Wave-quantisation tail split (prefill rows, N > 64: tensor-bound, one tile per SM-slot):
+  // the full waves of whole tiles in one launch, the remaining tiles in a second launch with
+  // a cluster split-K wide enough to spread them over all SMs (gate/up at N = 256: 224 tiles =
+  // 148 + 76 -> the 76 tail tiles run as 2-CTA clusters instead of a half-empty second wave)
+  static const bool tail_off = getenv("RT_NO_TAIL_SPLIT") != nullptr;
+  const int P = sm_count() * (bn <= 128 ? 2 : 1);  // co-resident CTA slots
+  if (auto_split && splits == 1 && bn >= 128 && g.mode != EPI_ARGMAX && !tail_off && tiles > P && tiles % P) {
+    const int head = (tiles / P) * P, tail = tiles - head;
+    // S = the largest split that still fits the tail into one wave of the slots (a wider split
+    // that spills into another wave measured slower: the cluster reduction of 96-128 KB
+    // partials costs more than the balance gains, tools/gemm_sweep_n.py)
+    const int st = std::min(std::min(16, g.kb_total / 4), std::max(1, P / tail));
+    if (st > 1) {
+      cudaError_t r = launch(0, head, 1);
+      if (r != cudaSuccess) return r;
+      return launch(head, tail, st);
+    }
   }
+  return launch(0, tiles, splits);
 }
 
 

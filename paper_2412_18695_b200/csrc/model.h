@@ -125,7 +125,10 @@ struct GemmArgs {
   int pf_S, pf_m_tiles, pf_kb_total, pf_kb;
   int l2_evict_first;  // set by launch_gemm_epi: weight tiles are read once per step
   int epi_backoff_ns;  // set by launch_gemm_epi: nanosleep between the epilogue warps' polls
-  int nt_fast;         // set by launch_gemm_epi: grid (S, n-tiles, m-tiles) instead of (S, m, n)
+  // set by launch_gemm_epi: CTA (x, y) runs linear tile tile0 + y of the GEMM's m_tiles x
+  // n_tiles tiles (n fastest: the n-tiles of one m-tile are adjacent and the later ones read
+  // the weight tile from L2); tile_count tiles in this launch
+  int n_tiles, tile0, tile_count;
   // stream-K workspace for N > 128 rows (nullable: one tile per CTA): partial tiles
   // [SMs][2][256][128] fp32 (gemm_sk_ws_floats) and zeroed self-resetting tile tickets
   float* sk_ws;
