@@ -298,10 +298,16 @@ __global__ void __launch_bounds__(256) k_attn_prefill(PrefillArgs a) {
   __syncthreads();
   pdl_wait();  // q and the prompt's K/V pages come from the QKV GEMM before this kernel
   tr.ready();
-  const int4 T = a.tiles[a.n_tiles - 1 - (int)blockIdx.x];  // (row, rows, pos0, task)
+  const int tix = a.n_tiles - 1 - (int)blockIdx.x;
+  const int4 T = a.tiles[tix];  // (row, rows, pos0, task)
   const int rb = T.x, re = T.x + T.y;
   if (max(rb, a.row0) >= min(re, a.row0 + a.n_rows)) return;  // not in this forward chunk
-  const int np = (T.z >> 4) + 1;                                // pages 0 .. pos0 / 16
+  const int npt = (T.z >> 4) + 1;                               // pages 0 .. pos0 / 16
+  // split-KV: chunk c of C covers pages [pb, pe) (the diagonal page is in the last chunk)
+  const int NC = a.chunks, chunk = blockIdx.z;
+  const int cpp = (npt + NC - 1) / NC;
+  const int pb = min(npt, chunk * cpp), pe = min(npt, pb + cpp);
+  const int np = pe - pb;
   const int32_t* ptab = a.page_table + (size_t)T.w * a.pt_stride;
   const unsigned char* pool = (const unsigned char*)a.pool;
   const size_t head_off = (size_t)h * C::BLOCK;
@@ -309,7 +315,7 @@ __global__ void __launch_bounds__(256) k_attn_prefill(PrefillArgs a) {
   if (threadIdx.x == 0)
     for (int i = 0; i < C::STAGES && i < np; ++i) {
       mbar_arrive_expect_tx(&full[i], C::BLOCK);
-      bulk_g2s(smem + i * C::BLOCK, pool + (size_t)ptab[i] * page_stride + head_off, C::BLOCK, &full[i]);
+      bulk_g2s(smem + i * C::BLOCK, pool + (size_t)ptab[pb + i] * page_stride + head_off, C::BLOCK, &full[i]);
     }
 
   // q fragments (A operand, rows = the tile's positions), rows outside the chunk are zero
@@ -355,10 +361,10 @@ __global__ void __launch_bounds__(256) k_attn_prefill(PrefillArgs a) {
       mma_bf16_16816(s1, qa[ks], bf1);
     }
     // ---- causal mask (diagonal page) + online softmax; row gq: s*[0..1], row gq+8: s*[2..3]
-    const int k0 = i * 16 + 2 * qq;
+    const int k0 = (pb + i) * 16 + 2 * qq;
     float x[8] = {s0[0] * sl2, s0[1] * sl2, s1[0] * sl2, s1[1] * sl2,
                   s0[2] * sl2, s0[3] * sl2, s1[2] * sl2, s1[3] * sl2};
-    if (i == np - 1) {
+    if (pb + i == npt - 1) {
       const int kk[4] = {k0, k0 + 1, k0 + 8, k0 + 9};
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -411,15 +417,76 @@ __global__ void __launch_bounds__(256) k_attn_prefill(PrefillArgs a) {
       mbar_wait(&empty[s], (uint32_t)((i / C::STAGES) & 1));
       fence_proxy_async();
       mbar_arrive_expect_tx(&full[s], C::BLOCK);
-      bulk_g2s(smem + s * C::BLOCK, pool + (size_t)ptab[i + C::STAGES] * page_stride + head_off, C::BLOCK,
+      bulk_g2s(smem + s * C::BLOCK, pool + (size_t)ptab[pb + i + C::STAGES] * page_stride + head_off, C::BLOCK,
                &full[s]);
     }
   }
-  // ---- normalise and store rows gq, gq + 8 (dims 8 nt + 2 qq, +1)
   l0 += __shfl_xor_sync(0xffffffffu, l0, 1);
   l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
   l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
   l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+  if (NC > 1) {
+    // ---- split-KV: park (o unnormalised, m, l) of this chunk; the last chunk of the
+    // (tile, head) merges all chunks in chunk order (deterministic)
+    const int RW = HD + 2;
+    float* wsb = a.ws + (((size_t)tix * a.nkv + h) * NC) * (size_t)(G * 16 * RW);
+    float* mine = wsb + ((size_t)chunk * G + warp) * (16 * RW);
+#pragma unroll
+    for (int nt = 0; nt < HD / 8; ++nt) {
+      const int d = nt * 8 + 2 * qq;
+      mine[gq * RW + d] = o[nt][0];
+      mine[gq * RW + d + 1] = o[nt][1];
+      mine[(gq + 8) * RW + d] = o[nt][2];
+      mine[(gq + 8) * RW + d + 1] = o[nt][3];
+    }
+    if (qq == 0) {
+      mine[gq * RW + HD] = m0;
+      mine[gq * RW + HD + 1] = l0;
+      mine[(gq + 8) * RW + HD] = m1;
+      mine[(gq + 8) * RW + HD + 1] = l1;
+    }
+    __threadfence();
+    __syncthreads();
+    __shared__ int s_last;
+    if (threadIdx.x == 0) {
+      int* tk = a.tickets + (size_t)tix * a.nkv + h;
+      const int t = atomicAdd(tk, 1);
+      s_last = (t == NC - 1);
+      if (s_last) *tk = 0;  // self-reset for the next launch
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    // merge: M = max m_c, L = sum l_c 2^(m_c - M), O = sum o_c 2^(m_c - M)
+    float M0 = -INFINITY, M1 = -INFINITY;
+    for (int c = 0; c < NC; ++c) {
+      const float* pc = wsb + ((size_t)c * G + warp) * (16 * RW);
+      M0 = fmaxf(M0, __ldcg(pc + gq * RW + HD));
+      M1 = fmaxf(M1, __ldcg(pc + (gq + 8) * RW + HD));
+    }
+    float L0 = 0.f, L1 = 0.f;
+#pragma unroll
+    for (int nt = 0; nt < HD / 8; ++nt) o[nt][0] = o[nt][1] = o[nt][2] = o[nt][3] = 0.f;
+    for (int c = 0; c < NC; ++c) {
+      const float* pc = wsb + ((size_t)c * G + warp) * (16 * RW);
+      const float mc0 = __ldcg(pc + gq * RW + HD), mc1 = __ldcg(pc + (gq + 8) * RW + HD);
+      const float f0 = (mc0 == -INFINITY) ? 0.f : exp2f(mc0 - M0);
+      const float f1 = (mc1 == -INFINITY) ? 0.f : exp2f(mc1 - M1);
+      L0 += __ldcg(pc + gq * RW + HD + 1) * f0;
+      L1 += __ldcg(pc + (gq + 8) * RW + HD + 1) * f1;
+#pragma unroll
+      for (int nt = 0; nt < HD / 8; ++nt) {
+        const int d = nt * 8 + 2 * qq;
+        o[nt][0] += __ldcg(pc + gq * RW + d) * f0;
+        o[nt][1] += __ldcg(pc + gq * RW + d + 1) * f0;
+        o[nt][2] += __ldcg(pc + (gq + 8) * RW + d) * f1;
+        o[nt][3] += __ldcg(pc + (gq + 8) * RW + d + 1) * f1;
+      }
+    }
+    l0 = L0;
+    l1 = L1;
+  }
+  // ---- normalise and store rows gq, gq + 8 (dims 8 nt + 2 qq, +1)
   const float i0 = 1.f / l0, i1 = 1.f / l1;
 #pragma unroll
   for (int hf = 0; hf < 2; ++hf) {
@@ -505,11 +572,35 @@ static void launch_prefill_hd(const PrefillArgs& a, cudaStream_t s) {
     cudaFuncSetAttribute(k_attn_prefill<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     attr = true;
   }
-  launch_pdl(k_attn_prefill<HD>, dim3(a.n_tiles, a.nkv), dim3(32 * a.G), C::SMEM, s, a);
+  launch_pdl(k_attn_prefill<HD>, dim3(a.n_tiles, a.nkv, a.chunks), dim3(32 * a.G), C::SMEM, s, a);
 }
 
-void launch_attention_prefill(const PrefillArgs& a, cudaStream_t s) {
-  if (a.n_tiles <= 0 || a.G < 1 || a.G > 8) return;
+// Split-KV plan of the prefill attention: C page chunks per (tile, kv head), merged by the
+// last chunk's CTA (self-resetting tickets).  RT_PF_CHUNKS sets C (tests / tuning).
+static int prefill_chunks(const PrefillArgs& a) {
+  static int forced = -2;
+  if (forced == -2) {
+    const char* e = getenv("RT_PF_CHUNKS");
+    forced = e ? atoi(e) : -1;
+  }
+  const int max_np = (a.max_seqlen + 15) / 16;
+  const long long ctas = (long long)a.n_tiles * a.nkv;
+  // default 1: measured at the e2e operating point (~20 tiles x 8 kv heads, ~80 pages each)
+  // C = 1 / 2 / 4 / 8: 74.6 / 72.1 / 87.8 / 109 us per layer — the kernel is bound by the
+  // mma.sync work per SM, not by the page stream latency, so splitting only adds the merge
+  (void)max_np;
+  (void)ctas;
+  int c = forced > 0 ? forced : 1;
+  c = std::max(1, std::min(c, 16));
+  const int G = a.nq / a.nkv;
+  if (!a.ws || !a.tickets || (int64_t)ctas * c * G * 16 * (a.hd + 2) > a.ws_floats) c = 1;
+  return c;
+}
+
+void launch_attention_prefill(const PrefillArgs& a0, cudaStream_t s) {
+  if (a0.n_tiles <= 0 || a0.G < 1 || a0.G > 8) return;
+  PrefillArgs a = a0;
+  a.chunks = prefill_chunks(a);
   switch (a.hd) {
     case 128: launch_prefill_hd<128>(a, s); break;
     case 64: launch_prefill_hd<64>(a, s); break;

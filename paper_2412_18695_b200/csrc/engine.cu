@@ -117,6 +117,9 @@ struct rt_engine {
   unsigned* d_chain_done = nullptr;
   unsigned chain_base[kChainMaxJobs] = {};
   int chain_grid_n = 0;
+  float* d_pf_ws = nullptr;      // split-KV partials of the prefill attention
+  int64_t pf_ws_floats = 0;
+  int* d_pf_tickets = nullptr;
   float* d_sk_ws = nullptr;      // stream-K partial tiles (prefill projections, N > 128 rows)
   unsigned* d_sk_cnt = nullptr;  // stream-K tile tickets
   int sk_cnt_cap = 0;
@@ -516,6 +519,10 @@ static rt_status create_impl(rt_engine* e, const rt_config* cfg) {
     if (!ok) return done(fail(e, RT_E_CUDA, "cuTensorMapEncodeTiled failed (activations)"));
     e->ev_attn.resize(2 * L);
     for (auto& ev : e->ev_attn) cudaEventCreate(&ev);
+    // split-KV workspace of the prefill attention (attn.cu prefill_chunks): 64 MB
+    e->pf_ws_floats = (int64_t)16 << 20;
+    CK(e, dalloc(e, &e->d_pf_ws, (size_t)e->pf_ws_floats));
+    CK(e, dalloc(e, &e->d_pf_tickets, (size_t)(e->rows_cap / 16 + c.max_batch) * nkv));
     // stream-K workspace of the prefill projections (gemm_tc.cu k_gemm_sk; opt-in RT_STREAMK=1)
     if (getenv("RT_STREAMK") && atoi(getenv("RT_STREAMK")) != 0) {
       const int max_mt = (std::max(std::max(e->qkv_dim, d), 2 * ff) + 127) / 128;
@@ -852,6 +859,10 @@ static rt_status forward(rt_engine* e, const HostMailbox& plan) {
     pa.G = nq / nkv;
     pa.out = e->d_o;
     pa.scale_log2 = sl2;
+    pa.max_seqlen = plan.max_seqlen;
+    pa.ws = e->d_pf_ws;
+    pa.ws_floats = e->pf_ws_floats;
+    pa.tickets = e->d_pf_tickets;
     const bool any_decode = plan.n_rows > plan.n_prefill_rows;
     auto gemm = [&](const bf16* w, const GemmTmaSet& x, int M, int K, GemmArgs g) {
       g.M = M;

@@ -75,6 +75,13 @@ struct PrefillArgs {
   bf16* out;                // [n_rows][nq][hd]
   float* out_f32;           // nullable, indexed by global row
   float scale_log2;
+  // split-KV (set by launch_attention_prefill from the fields below): CTA (tile, head, chunk)
+  // streams chunk `chunk` of the tile's pages; partials -> ws, the last chunk's CTA merges
+  int chunks;
+  int max_seqlen;           // longest attended context of the launch (chunk plan)
+  float* ws;                // nullable: [tiles][nkv][chunks][G][16][hd + 2] fp32
+  int64_t ws_floats;
+  int* tickets;             // [tiles][nkv] zeroed, self-resetting
 };
 void launch_attention_prefill(const PrefillArgs& a, cudaStream_t s);
 

@@ -257,13 +257,25 @@ def test_submit_errors(rt):
 
 
 # ------------------------------------------------------------- model parity
-@pytest.mark.parametrize("graphs,chain,streamk", [(False, False, False), (True, False, False), (False, True, False),
-                                                  (False, False, True)])
-def test_tiny_model_e2e_and_per_op(rt, graphs, chain, streamk, monkeypatch):
+@pytest.mark.parametrize("graphs,chain,streamk,pf_chunks", [(False, False, False, 0), (True, False, False, 0),
+                                                            (False, True, False, 0), (False, False, True, 0),
+                                                            (False, False, False, 3)])
+def test_tiny_model_e2e_and_per_op(rt, graphs, chain, streamk, pf_chunks, monkeypatch):
     """C1 end to end against the oracle; chain=True runs the decode projections through the
     opt-in persistent projection chain (RT_CHAIN=1; 2 CTAs at these dims, so both the
     whole-tile and the partial-tile fixup paths run); streamk=True runs the prefill
-    projections (N > 128 rows) through the opt-in stream-K kernel (RT_STREAMK=1)."""
+    projections (N > 128 rows) through the opt-in stream-K kernel (RT_STREAMK=1); pf_chunks=3
+    forces the split-KV path of the prefill attention (3 page chunks per tile, merged by the
+    last chunk's CTA)."""
+    if pf_chunks:
+        # the chunk plan reads RT_PF_CHUNKS once per process: run in a fresh interpreter
+        import subprocess, sys, os
+        env = dict(os.environ, RT_PF_CHUNKS=str(pf_chunks))
+        r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", __file__ + "::test_tiny_model_e2e_and_per_op",
+                            "-k", "False-False-False-0", "-m", "gpu", "-p", "no:cacheprovider"],
+                           env=env, capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+        return
     for var, on in (("RT_CHAIN", chain), ("RT_STREAMK", streamk)):
         if on:
             monkeypatch.setenv(var, "1")

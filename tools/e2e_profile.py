@@ -15,8 +15,8 @@ from paper_2412_18695_b200 import rt  # noqa: E402
 from synth.traces import system_prefix  # noqa: E402
 
 
-def main(rounds=200):
-    eng, now = profile_step.setup(bench.AGENTS_PER_GPU, flags=rt.RT_FLAG_TIMING)
+def main(rounds=200, trace=False):
+    eng, now = profile_step.setup(bench.AGENTS_PER_GPU, flags=rt.RT_FLAG_TRACE if trace else rt.RT_FLAG_TIMING)
     from synth import MODEL_SHAPES, make_vocab
     vocab = make_vocab(MODEL_SHAPES["llama3-8b"].vocab)
     bench.drain(eng, now)
@@ -31,6 +31,27 @@ def main(rounds=200):
 
     for a in range(bench.AGENTS_PER_GPU):
         submit(a)
+    if trace:   # closed loop for a while, then the device trace of 10 rounds by kernel role
+        for r in range(60):
+            for s in eng.poll():
+                if s["reason"] in (1, 2):
+                    submit(s["agent_id"])
+            eng.step(now())
+        eng.sync()
+        eng.reset_stats()
+        for r in range(10):
+            for s in eng.poll():
+                if s["reason"] in (1, 2):
+                    submit(s["agent_id"])
+            eng.step(now())
+        eng.sync()
+        import trace_step
+        agg, span, n, _ = trace_step.analyse(eng.trace())
+        print(f"e2e trace: {n} launches, {span / 10:.0f} us per round")
+        for name, (cnt, lead, gap, body, ctas, mains, epis) in sorted(agg.items(), key=lambda x: -(x[1][2] + x[1][3])):
+            print(f"  {name:28s} n={cnt:5d} body+gap per round {(gap + body) / 10:9.1f} us")
+        eng.close()
+        return
     rec = []
     for r in range(rounds):
         for s in eng.poll():
@@ -60,4 +81,4 @@ def main(rounds=200):
 
 
 if __name__ == "__main__":
-    main()
+    main(trace=len(sys.argv) > 1 and sys.argv[1] == "trace")
