@@ -523,8 +523,9 @@ static rt_status create_impl(rt_engine* e, const rt_config* cfg) {
     e->pf_ws_floats = (int64_t)16 << 20;
     CK(e, dalloc(e, &e->d_pf_ws, (size_t)e->pf_ws_floats));
     CK(e, dalloc(e, &e->d_pf_tickets, (size_t)(e->rows_cap / 16 + c.max_batch) * nkv));
-    // stream-K workspace of the prefill projections (gemm_tc.cu k_gemm_sk; opt-in RT_STREAMK=1)
-    if (getenv("RT_STREAMK") && atoi(getenv("RT_STREAMK")) != 0) {
+    // hybrid DP + stream-K workspace of the prefill projections (gemm_tc.cu k_gemm_sk;
+    // RT_NO_STREAMK=1: one tile per CTA)
+    if (getenv("RT_NO_STREAMK") == nullptr) {
       const int max_mt = (std::max(std::max(e->qkv_dim, d), 2 * ff) + 127) / 128;
       e->sk_cnt_cap = max_mt * ((R + 159) / 160);
       CK(e, dalloc(e, &e->d_sk_ws, (size_t)gemm_sk_ws_floats()));

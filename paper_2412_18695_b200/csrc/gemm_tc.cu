@@ -1177,33 +1177,81 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_chain(const __grid_constant
   }
 }
 
-// ============================================================ stream-K projection (prefill)
+// ============================================================ hybrid DP + stream-K projection
 // Rounds with prompt rows run the projections at N = 130 .. 8192 rows, where the GEMM is
 // tensor-bound and one tile per CTA quantises badly on 148 SMs (gate/up at N = 256: 224
-// tiles = 1.5 waves; N = 320 on 160-wide tiles: 448 tiles = 3.03 waves).  k_gemm_sk: one
-// CTA per SM; the T x kb k-block iterations of all tiles (n-tiles of an m-tile adjacent, so
-// the second reads the weight tile from L2) are split evenly over the CTAs (stream-K).  A
-// CTA accumulates each tile segment of its range in one of two TMEM buffers (the epilogue of
-// segment i overlaps the MMAs of segment i + 1).  A segment that is not a whole tile stores
-// its fp32 partial to the CTA's workspace slot (0: the tile its range starts in, 1: the tile
-// it ends in) and takes a ticket; the last contributor sums the partials in contributor order
-// (deterministic) from double-buffered 32 KB bulk loads and runs the fused epilogue in
-// 64-column chunks.
+// tiles = 1.5 waves; N = 352 on 192-wide tiles: 448 tiles = 3.03 waves) and pays a pipeline
+// fill + an unoverlapped epilogue per tile.  k_gemm_sk: one persistent CTA per SM.  Tiles
+// (n-tiles of an m-tile adjacent) are split into data-parallel whole tiles, round-robin over
+// the CTAs (all full waves but one), and a stream-K part (the last full wave + the partial
+// one, so every stream-K tile has <= 3 contributors) whose k-block iterations are split
+// evenly over the CTAs.  Each segment accumulates in one of two TMEM buffers, so a
+// segment's epilogue overlaps the next segment's MMAs; the ring stays full across
+// segments.  A stream-K segment that is not a whole tile stores its fp32 partial to the
+// CTA's workspace slot (0: its first stream-K tile, 1: its last) and takes a ticket; the
+// last contributor sums the partials in contributor order (deterministic) and runs the
+// fused epilogue in column chunks staged through shared memory.
 namespace sk {
-constexpr int STAGES = 3;
+constexpr int STAGES = 4;
 constexpr int A_BYTES = 128 * kBK * 2;
-constexpr int CHUNK = 64;                       // epilogue columns per staging buffer
-constexpr int STG_BYTES = CHUNK * 128 * 4;      // 32 KB
 template <int BN>
 struct Cfg {
+  static constexpr int CHUNK = BN == 256 ? 32 : 64;      // epilogue columns per staging pass
+  static constexpr int STG_BYTES = CHUNK * 128 * 4;
   static constexpr int B_BYTES = BN * kBK * 2;
   static constexpr int TMEM_COLS = 2 * BN <= 256 ? 256 : 512;
   static constexpr int CTL = 256;
   static constexpr int META = 3 * BN * 4;
   static constexpr int RED = 2 * 4 * BN * 4;
-  static constexpr int SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + 2 * STG_BYTES + CTL + META + RED;
-  static_assert(SMEM <= 227 * 1024, "stream-K smem");
-  static_assert(BN % CHUNK == 0 || BN == 160, "chunking");
+  static constexpr int SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + STG_BYTES + CTL + META + RED;
+  static_assert(SMEM <= 227 * 1024, "hybrid stream-K smem");
+};
+// the segment sequence of one CTA: its data-parallel tiles, then its stream-K iterations
+struct Sched {
+  int P, cta, kbt, n_tiles;
+  int dp_tiles, dp_mine;     // data-parallel tiles (a multiple of P) and this CTA's count
+  long long I_sk;            // stream-K iterations (sk tiles x kbt)
+  int qa, qb;                // this CTA's stream-K range
+  __device__ void init(int P_, int cta_, int kbt_, int T, int n_tiles_) {
+    P = P_;
+    cta = cta_;
+    kbt = kbt_;
+    n_tiles = n_tiles_;
+    const int sk_tiles = T <= P ? T : (T % P) + P;
+    dp_tiles = T - sk_tiles;
+    dp_mine = dp_tiles / P;
+    I_sk = (long long)sk_tiles * kbt;
+    qa = chain::q0(I_sk, cta, P);
+    qb = chain::q0(I_sk, cta + 1, P);
+  }
+  // segment iterator: dp index d < dp_mine, then stream-K position q in [qa, qb)
+  struct Seg {
+    int tile, lo, hi;   // global tile index, k-block range
+    int sk_t;           // stream-K tile index (-1: data-parallel)
+  };
+  __device__ bool first(Seg& g, int& d, int& q) const {
+    d = 0;
+    q = qa;
+    return next(g, d, q);
+  }
+  __device__ bool next(Seg& g, int& d, int& q) const {
+    if (d < dp_mine) {
+      g.tile = cta + d * P;
+      g.lo = 0;
+      g.hi = kbt;
+      g.sk_t = -1;
+      ++d;
+      return true;
+    }
+    if (q >= qb) return false;
+    const int t = q / kbt;
+    g.sk_t = t;
+    g.tile = dp_tiles + t;
+    g.lo = q - t * kbt;
+    g.hi = min(qb - t * kbt, kbt);
+    q = t * kbt + g.hi;
+    return true;
+  }
 };
 }  // namespace sk
 
@@ -1219,19 +1267,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     k_gemm_sk(const __grid_constant__ TmaMap tmB, GemmArgs g, SkArgs a) {
   using C = sk::Cfg<BN>;
   using namespace sk;
+  constexpr int CHUNK = C::CHUNK;
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   unsigned char* sA = smem;
   unsigned char* sB = smem + STAGES * A_BYTES;
-  float* stg0 = reinterpret_cast<float*>(sB + STAGES * C::B_BYTES);
-  float* stg1 = stg0 + CHUNK * 128;
-  unsigned char* ctl = reinterpret_cast<unsigned char*>(stg1 + CHUNK * 128);
+  float* stg = reinterpret_cast<float*>(sB + STAGES * C::B_BYTES);
+  unsigned char* ctl = reinterpret_cast<unsigned char*>(stg) + C::STG_BYTES;
   uint64_t* full = reinterpret_cast<uint64_t*>(ctl);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint64_t* fxbar = tempty + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fxbar + 2);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fxbar + 1);
   int* s_last = reinterpret_cast<int*>(tmem_slot + 1);
   EpiSmem sm;
   sm.pos = reinterpret_cast<int*>(ctl + C::CTL);
@@ -1240,17 +1288,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   sm.redv = reinterpret_cast<float*>(ctl + C::CTL + C::META);
   sm.redi = reinterpret_cast<int*>(sm.redv + 4 * BN);
   sm.bn = BN;
-  sm.xp = stg1;  // unused (pre = false)
+  sm.xp = stg;  // unused (pre = false)
   sm.xp_sin = 0;
   __shared__ long long s_mark[9];
   sm.mark = s_mark;
 
   TraceScope tr(TK_GEMM | ((uint32_t)MODE << 8) | (1u << 16));
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int cta = blockIdx.x, NP = a.P;
+  const int cta = blockIdx.x;
   const int kbt = g.kb_total;
-  const long long I = (long long)g.m_tiles * a.n_tiles * kbt;
-  const int qa = chain::q0(I, cta, NP), qb = chain::q0(I, cta + 1, NP);
+  Sched S;
+  S.init(a.P, cta, kbt, g.m_tiles * a.n_tiles, a.n_tiles);
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmB);
@@ -1261,8 +1309,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 1);
-      mbar_init(&fxbar[i], 1);
     }
+    mbar_init(fxbar, 1);
     fence_mbar_init();
   }
   if (warp == 1) {
@@ -1278,24 +1326,22 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      // tile t = m_tile * n_tiles + n_tile (n fastest); iteration q = t * kbt + kb
       bool waited = false;
-      int t = qa / kbt, kb = qa - (qa / kbt) * kbt;
-      for (int q = qa, n = 0; q < qb; ++q, ++n) {
-        const int st = n % STAGES;
-        if (n >= STAGES) mbar_wait(&empty[st], (uint32_t)(((n / STAGES) & 1) ^ 1));
-        const int m_tile = t / a.n_tiles, n_tile = t - m_tile * a.n_tiles;
-        mbar_arrive_expect_tx(&full[st], A_BYTES + C::B_BYTES);
-        bulk_g2s(sA + st * A_BYTES, g.w + ((size_t)m_tile * kbt + kb) * (128 * kBK), A_BYTES, &full[st]);
-        if (!waited) {  // weights before the previous kernel finishes, activations after
-          pdl_wait();
-          tr.ready();
-          waited = true;
-        }
-        tma_load_2d(sB + st * C::B_BYTES, &tmB, kb * kBK, n_tile * BN, &full[st]);
-        if (++kb == kbt) {
-          kb = 0;
-          ++t;
+      int n = 0, d, q;
+      Sched::Seg sg;
+      for (bool ok = S.first(sg, d, q); ok; ok = S.next(sg, d, q)) {
+        const int m_tile = sg.tile / a.n_tiles, n_tile = sg.tile - m_tile * a.n_tiles;
+        for (int kb = sg.lo; kb < sg.hi; ++kb, ++n) {
+          const int st = n % STAGES;
+          if (n >= STAGES) mbar_wait(&empty[st], (uint32_t)(((n / STAGES) & 1) ^ 1));
+          mbar_arrive_expect_tx(&full[st], A_BYTES + C::B_BYTES);
+          bulk_g2s(sA + st * A_BYTES, g.w + ((size_t)m_tile * kbt + kb) * (128 * kBK), A_BYTES, &full[st]);
+          if (!waited) {  // weights before the previous kernel finishes, activations after
+            pdl_wait();
+            tr.ready();
+            waited = true;
+          }
+          tma_load_2d(sB + st * C::B_BYTES, &tmB, kb * kBK, n_tile * BN, &full[st]);
         }
       }
       if (!waited) pdl_wait();
@@ -1304,15 +1350,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   } else if (warp == 1) {
     if (lane == 0) {
       constexpr uint32_t idesc = umma_idesc(128, BN);
-      int n = 0, seg = 0;
-      for (int q = qa; q < qb;) {
-        const int t = q / kbt;
-        const int lo = q - t * kbt, hi = min(qb - t * kbt, kbt);
+      int n = 0, seg = 0, d, q;
+      Sched::Seg sg;
+      for (bool ok = S.first(sg, d, q); ok; ok = S.next(sg, d, q)) {
         const int buf = seg & 1;
         if (seg >= 2) mbar_wait(&tempty[buf], (uint32_t)(((seg >> 1) - 1) & 1));
         tc_fence_after();
         const uint32_t acc = tmem + (uint32_t)(buf * BN);
-        for (int kb = lo; kb < hi; ++kb, ++n) {
+        for (int kb = sg.lo; kb < sg.hi; ++kb, ++n) {
           const int st = n % STAGES;
           mbar_wait(&full[st], (uint32_t)((n / STAGES) & 1));
           tc_fence_after();
@@ -1321,12 +1366,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k)
             umma_f16(acc, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
-                     (kb > lo || k > 0) ? 1u : 0u);
+                     (kb > sg.lo || k > 0) ? 1u : 0u);
           umma_commit(&empty[st]);
         }
         umma_commit(&tfull[buf]);
         ++seg;
-        q = t * kbt + hi;
       }
     }
     __syncwarp();
@@ -1334,25 +1378,26 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     pdl_wait();
     const int et = (warp & 3) * 32 + lane;
     const uint32_t tb = tmem + ((uint32_t)((warp & 3) * 32) << 16);
-    const int first_tile = qa / kbt;
-    uint32_t fx_phase[2] = {0u, 0u};
-    int seg = 0;
-    for (int q = qa; q < qb;) {
-      const int t = q / kbt;
-      const int hi = min(qb - t * kbt, kbt);
+    const int first_sk = S.qa / kbt;
+    uint32_t fx_phase = 0u;
+    int seg = 0, d, q;
+    Sched::Seg sg;
+    for (bool ok = S.first(sg, d, q); ok; ok = S.next(sg, d, q)) {
       const int buf = seg & 1;
-      const int m_tile = t / a.n_tiles, n_tile = t - m_tile * a.n_tiles;
+      const int m_tile = sg.tile / a.n_tiles, n_tile = sg.tile - m_tile * a.n_tiles;
       const int n0 = n_tile * BN;
-      const int c_first = chain::owner((long long)t * kbt, I, NP);
-      const int c_last = chain::owner((long long)(t + 1) * kbt - 1, I, NP);
-      const int nc = c_last - c_first + 1;
+      int nc = 1, c_first = 0;
+      if (sg.sk_t >= 0) {
+        c_first = chain::owner((long long)sg.sk_t * kbt, S.I_sk, S.P);
+        nc = chain::owner((long long)(sg.sk_t + 1) * kbt - 1, S.I_sk, S.P) - c_first + 1;
+      }
       mbar_wait(&tfull[buf], (uint32_t)((seg >> 1) & 1));
       tc_fence_after();
-      epi_bar();  // the previous segment's epilogue is done with the staging buffers / sm
+      epi_bar();  // the previous segment's epilogue is done with the staging buffer / sm
       bool run = true;
       const uint32_t tacc = tb + (uint32_t)(buf * BN);
       if (nc > 1) {
-        float* mine = a.ws + ((size_t)cta * 2 + (t == first_tile ? 0 : 1)) * (BN * 128);
+        float* mine = a.ws + ((size_t)cta * 2 + (sg.sk_t == first_sk ? 0 : 1)) * (BN * 128);
 #pragma unroll 1
         for (int c0 = 0; c0 < BN; c0 += 16) {
           float v[16];
@@ -1365,7 +1410,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         epi_bar();
         if (et == 0) {
           mbar_arrive(&tempty[buf]);
-          const unsigned old = atomicAdd(a.cnt + t, 1u);
+          const unsigned old = atomicAdd(a.cnt + sg.tile, 1u);
           *s_last = (old == (unsigned)(nc - 1)) ? 1 : 0;
         }
         epi_bar();
@@ -1373,7 +1418,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if (run) {
           __threadfence();
           if (et == 0) {
-            a.cnt[t] = 0u;
+            a.cnt[sg.tile] = 0u;
             asm volatile("fence.proxy.async.global;" ::: "memory");
           }
         }
@@ -1384,7 +1429,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll 1
         for (int cb = 0; cb < BN; cb += CHUNK) {
           const int ce = min(BN, cb + CHUNK);
-          float* stg = stg0;
           if (nc == 1) {  // whole tile: TMEM -> staging
 #pragma unroll 1
             for (int c0 = cb; c0 < ce; c0 += 16) {
@@ -1398,28 +1442,24 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
             for (int c = 0; c < CHUNK; ++c) acc[c] = 0.f;
             const uint32_t bytes = (uint32_t)((ce - cb) * 512);
-            for (int r = 0; r < nc; r += 2) {
-              if (et == 0)
-                for (int b = 0; b < 2 && r + b < nc; ++b) {
-                  const int c = c_first + r + b;
-                  const float* src =
-                      a.ws + ((size_t)c * 2 + (t == chain::q0(I, c, NP) / kbt ? 0 : 1)) * (BN * 128) + (size_t)cb * 128;
-                  mbar_arrive_expect_tx(&fxbar[b], bytes);
-                  bulk_g2s(b ? (void*)stg1 : (void*)stg0, src, bytes, &fxbar[b]);
-                }
-              for (int b = 0; b < 2 && r + b < nc; ++b) {
-                mbar_wait(&fxbar[b], fx_phase[b]);
-                fx_phase[b] ^= 1u;
-                const float* bb = b ? stg1 : stg0;
-#pragma unroll
-                for (int c = 0; c < CHUNK; ++c)
-                  if (cb + c < ce) acc[c] += bb[c * 128 + et];
+            for (int r = 0; r < nc; ++r) {
+              const int c = c_first + r;
+              if (et == 0) {
+                const int fs = chain::q0(S.I_sk, c, S.P) / kbt;
+                const float* src = a.ws + ((size_t)c * 2 + (sg.sk_t == fs ? 0 : 1)) * (BN * 128) + (size_t)cb * 128;
+                mbar_arrive_expect_tx(fxbar, bytes);
+                bulk_g2s(stg, src, bytes, fxbar);
               }
-              epi_bar();
+              mbar_wait(fxbar, fx_phase);
+              fx_phase ^= 1u;
+#pragma unroll
+              for (int cc = 0; cc < CHUNK; ++cc)
+                if (cb + cc < ce) acc[cc] += stg[cc * 128 + et];
+              epi_bar();  // the staging buffer is free for the next partial
             }
 #pragma unroll
-            for (int c = 0; c < CHUNK; ++c)
-              if (cb + c < ce) stg[c * 128 + et] = acc[c];
+            for (int cc = 0; cc < CHUNK; ++cc)
+              if (cb + cc < ce) stg[cc * 128 + et] = acc[cc];
           }
           epi_bar();
           TileSrc ts = ts0;
@@ -1433,7 +1473,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
       }
       ++seg;
-      q = t * kbt + hi;
     }
   }
   tc_fence_before();
@@ -1622,11 +1661,9 @@ static cudaError_t launch_sk_mode(const GemmTmaSet& x, const GemmArgs& g, const 
 int64_t gemm_sk_ws_floats() { return (int64_t)sm_count() * 2 * 256 * 128; }
 
 cudaError_t launch_gemm_epi(const bf16* w_tiled, const GemmTmaSet& x, GemmArgs g, int splits, cudaStream_t s) {
-  // stream-K for the tensor-bound prefill path (N > 128 rows): OPT-IN (RT_STREAMK=1), when the
-  // caller provides its workspace.  Measured slower than one tile per CTA on every prefill
-  // shape (tools/gemm_sweep_n.py: gate/up N = 256 77.8 vs 65.4 us, down 54.8 vs 33.8 us): its
-  // 3-stage ring at 1 CTA / SM cannot hide the load latency of 48 KB stages and the partial
-  // fixups of the K-heavy down projection cost more than the balance gains
+  // hybrid data-parallel + stream-K persistent kernel for the tensor-bound prefill path
+  // (N > 128 rows, more than two waves of tiles) when the caller provides its workspace
+  // (RT_NO_STREAMK=1 in the engine: one tile per CTA below)
   if (g.sk_ws && g.sk_cnt && g.N > 128 && g.mode != EPI_ARGMAX && g.K % kBK == 0) {
     g.w = w_tiled;
     g.kb_total = g.K / kBK;
@@ -1635,9 +1672,14 @@ cudaError_t launch_gemm_epi(const bf16* w_tiled, const GemmTmaSet& x, GemmArgs g
     const int bn = gemm_bn(g.N);
     SkArgs a;
     a.n_tiles = (g.N + bn - 1) / bn;
-    const long long I = (long long)g.m_tiles * a.n_tiles * g.kb_total;
-    if ((long long)g.m_tiles * a.n_tiles <= g.sk_cnt_cap) {
-      a.P = (int)std::min<long long>(sm_count(), I);
+    const int T = g.m_tiles * a.n_tiles;
+    const int P = sm_count();
+    const long long I_sk = (long long)(T <= P ? T : (T % P) + P) * g.kb_total;
+    // only with a data-parallel part (T > 2 waves): measured faster there (gate/up N = 320 /
+    // 384 / 512: 103 / 108 / 122 -> 89 / 95 / 116 us) and slower for all-stream-K shapes
+    // (few-tile projections pay multi-contributor fixups; the cluster split-K path is better)
+    if (T <= g.sk_cnt_cap && I_sk >= P && T > 2 * P) {
+      a.P = P;
       a.ws = g.sk_ws;
       a.cnt = g.sk_cnt;
       switch (g.mode) {

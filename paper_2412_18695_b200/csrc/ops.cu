@@ -133,7 +133,7 @@ extern "C" rt_status rt_op_gemm_tiled(const void* d_w_tiled, const void* d_x, fl
   static unsigned* sk_cnt = nullptr;
   static int sk_cap = 0;
   const int need = ((M + 127) / 128) * ((N + 159) / 160);
-  if (N > 128 && splits <= 0 && getenv("RT_STREAMK") && atoi(getenv("RT_STREAMK")) != 0) {
+  if (N > 128 && splits <= 0 && getenv("RT_NO_STREAMK") == nullptr) {
     if (!sk_ws && cudaMalloc(&sk_ws, (size_t)gemm_sk_ws_floats() * 4) != cudaSuccess) return RT_E_CUDA;
     if (need > sk_cap) {
       if (sk_cnt) cudaFree(sk_cnt);

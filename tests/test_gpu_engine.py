@@ -257,14 +257,14 @@ def test_submit_errors(rt):
 
 
 # ------------------------------------------------------------- model parity
-@pytest.mark.parametrize("graphs,chain,streamk,pf_chunks", [(False, False, False, 0), (True, False, False, 0),
-                                                            (False, True, False, 0), (False, False, True, 0),
-                                                            (False, False, False, 3)])
+@pytest.mark.parametrize("graphs,chain,streamk,pf_chunks", [(False, False, True, 0), (True, False, True, 0),
+                                                            (False, True, True, 0), (False, False, False, 0),
+                                                            (False, False, True, 3)])
 def test_tiny_model_e2e_and_per_op(rt, graphs, chain, streamk, pf_chunks, monkeypatch):
     """C1 end to end against the oracle; chain=True runs the decode projections through the
     opt-in persistent projection chain (RT_CHAIN=1; 2 CTAs at these dims, so both the
-    whole-tile and the partial-tile fixup paths run); streamk=True runs the prefill
-    projections (N > 128 rows) through the opt-in stream-K kernel (RT_STREAMK=1); pf_chunks=3
+    whole-tile and the partial-tile fixup paths run); streamk=False disables the hybrid
+    DP + stream-K prefill projections (RT_NO_STREAMK=1, one tile per CTA); pf_chunks=3
     forces the split-KV path of the prefill attention (3 page chunks per tile, merged by the
     last chunk's CTA)."""
     if pf_chunks:
@@ -272,11 +272,11 @@ def test_tiny_model_e2e_and_per_op(rt, graphs, chain, streamk, pf_chunks, monkey
         import subprocess, sys, os
         env = dict(os.environ, RT_PF_CHUNKS=str(pf_chunks))
         r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", __file__ + "::test_tiny_model_e2e_and_per_op",
-                            "-k", "False-False-False-0", "-m", "gpu", "-p", "no:cacheprovider"],
+                            "-k", "False-False-True-0", "-m", "gpu", "-p", "no:cacheprovider"],
                            env=env, capture_output=True, text=True, timeout=600)
         assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
         return
-    for var, on in (("RT_CHAIN", chain), ("RT_STREAMK", streamk)):
+    for var, on in (("RT_CHAIN", chain), ("RT_NO_STREAMK", not streamk)):
         if on:
             monkeypatch.setenv(var, "1")
         else:
@@ -648,3 +648,38 @@ def test_sched_parity_stop_grammars(rt, grammar):
         assert a == b
     n, segs = lockstep(eng, ora, max_rounds=20000, check_every=7)
     assert sum(1 for s in segs if s["reason"] == 3) > 20
+
+
+def test_prefill_projections_hybrid_streamk_match_per_tile(rt, monkeypatch):
+    """The hybrid data-parallel + stream-K prefill projections (k_gemm_sk: > 2 waves of
+    tiles, here gate/up and QKV of a 1600-row prefill at 8B dims) against one tile per CTA
+    (RT_NO_STREAMK=1): same scripted rounds, the logits of the prefill round (token 0 of every
+    request) and of later decode rounds agree to fp32 summation-order level."""
+    from synth.configs import ModelShape
+    s8 = MODEL_SHAPES["llama3-8b"]
+    shape = ModelShape("sk", 2, s8.d_model, s8.n_q_heads, s8.n_kv_heads, s8.head_dim, s8.d_ff, s8.vocab)
+    v = make_vocab(shape.vocab)
+    p = engine_params("b200-roofline", max_batch=8, max_tasks=16, max_ctx=512, n_pages=8 * 32)
+    from synth.traces import make_trace
+    out = {}
+    for mode in ("hybrid", "per_tile"):
+        if mode == "per_tile":
+            monkeypatch.setenv("RT_NO_STREAMK", "1")
+        else:
+            monkeypatch.delenv("RT_NO_STREAMK", raising=False)
+        eng = rt.Engine(shape, p, v, seed=23, flags=rt.RT_FLAG_KEEP_LOGITS, max_rows_per_forward=4096)
+        for a in range(8):
+            tr = make_trace(1 + a, v, seed=a, prompt_len=200, plan_len=12)
+            eng.submit(a, tr.prompt, 0, tr.ert_us, tr.alpha, tr.beta, 90000, script=tr.plan)
+        logs = []
+        for _ in range(4):
+            info = eng.step()
+            B = info["n_running"]
+            logs.append((info["n_prefill_rows"], eng.dump(rt.RT_DUMP_LOGITS, np.float32).reshape(B, -1).copy()))
+        out[mode] = logs
+        eng.close()
+    assert out["hybrid"][0][0] == 1600
+    for (na, la), (nb, lb) in zip(out["hybrid"], out["per_tile"]):
+        assert na == nb
+        scale = max(1.0, float(np.abs(lb).max()))
+        assert float(np.abs(la - lb).max()) < 2e-2 * scale

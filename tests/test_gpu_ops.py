@@ -67,7 +67,8 @@ def test_priority_bitexact(rt):
                                           (4096, 64, 4096, 9), (1024, 64, 14336, 16), (640, 100, 2048, 3),
                                           (384, 150, 512, 1), (384, 190, 768, 2), (512, 350, 512, 1),
                                           (256, 470, 1024, 3), (6144, 161, 4096, 0),
-                                          (19200, 200, 512, 0), (20480, 150, 1024, 0), (9728, 300, 512, 0)])
+                                          (19200, 200, 512, 0), (20480, 150, 1024, 0), (9728, 300, 512, 0),
+                                          (28672, 320, 512, 0), (38400, 150, 256, 0)])
 def test_gemm_tcgen05(rt, M, N, K, splits):
     g = torch.Generator().manual_seed(M * 7 + N)
     W = (torch.randn(M, K, generator=g) * 0.05).to(torch.bfloat16)
