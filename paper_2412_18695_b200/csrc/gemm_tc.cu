@@ -686,6 +686,10 @@ __global__ void __launch_bounds__(kGemmThreads, GemmCfg<BN>::CTAS_PER_SM)
 #pragma unroll
       for (int i = 0; i < 9; ++i) s_mark[i] = t;
     }
+    // split-K: arrive on the cluster barrier as soon as this CTA's MMAs are done (its ring
+    // may then receive the peers' slices) and park the accumulator while the slower CTAs
+    // finish; the park writes P, the peers write the receive slots R (disjoint)
+    if (S > 1) cluster_arrive();
 #pragma unroll 1
     for (int c0 = 0; c0 < BN; c0 += 16) {  // park the accumulator in shared memory
       float v[16];
@@ -695,10 +699,11 @@ __global__ void __launch_bounds__(kGemmThreads, GemmCfg<BN>::CTAS_PER_SM)
     }
     if (push) fence_proxy_async();  // P is read by the bulk-copy (async) proxy
     EPI_MARK(1);
+    if (S > 1) cluster_wait();
   }
   // ---- cluster split-K: CTA `rank` finishes columns [cb, ce) of the tile.  The barrier
   // also certifies that every CTA's mainloop is over (its ring is free for the slices).
-  if (S > 1) {
+  if (S > 1 && warp < 2) {  // (the epilogue warps arrived / waited above)
     __syncwarp();
     cluster_arrive();
     cluster_wait();
