@@ -415,7 +415,47 @@ def cpu_baseline_sample(args):
     sec, tps = oracle_decode_layer_sample(args.seed)
     return {"value": tps, "unit": "tok/s", "cores": cores, "threads": torch.get_num_threads(), "kind": "oracle",
             "sample": f"1 of 32 llama3-8b decode layers (incl. counter-based weight generation) at B=64, ctx "
-                      f"{PROMPT}, {sec:.1f} s, extrapolated x32 layers (lm_head excluded)"}
+                      f"{PROMPT}, {sec:.1f} s, extrapolated x32 layers (lm_head excluded)",
+            "extra": oracle_extra_timings(args)}
+
+
+def oracle_extra_timings(args):
+    """SURVEY §8(d) CPU-oracle timings besides the decode round: the whole C1 trace (tiny
+    model + scheduler, wall seconds) and a scheduling-only replay of a C4-shaped trace (1024
+    agents, traces 1-11, Poisson) in rounds/s."""
+    from oracle.engine import OracleEngine
+    from oracle.model import OracleModel
+    from synth import compose_workload
+    out = {}
+    shape = MODEL_SHAPES["tiny"]
+    v = make_vocab(shape.vocab)
+    p = engine_params("paper-4090", max_batch=4, max_tasks=64, max_ctx=256, n_pages=64)
+    reqs = compose_workload(4, 1.0, 2, range(1, 9), 30.0, args.seed, v, prompt_len_range=(40, 64), max_requests=12)
+    t0 = time.perf_counter()
+    ora = OracleEngine(p, v.tok_skill, v.tok_exec_min_us, v.eos_id, v.vocab, model=OracleModel(shape, seed=3))
+    for r in reqs:
+        ora.submit(r.agent_id, r.prompt, r.arrival_us, r.ert_us, r.alpha, r.beta, r.exec_window_us, len(r.plan),
+                   script=r.plan)
+    ora.run_until_idle()
+    out["c1_trace_wall_s"] = time.perf_counter() - t0
+    v8 = make_vocab(128256)
+    p4 = engine_params("b200-roofline", max_batch=128, max_tasks=2048, max_ctx=4096, n_pages=1 << 16)
+    reqs = compose_workload(1024, 64.0, 16, range(1, 12), 10.0, args.seed, v8, prompt_len_range=(64, 64),
+                            max_requests=2000)
+    ora = OracleEngine(p4, v8.tok_skill, v8.tok_exec_min_us, v8.eos_id, v8.vocab)
+    for r in reqs:
+        ora.submit(r.agent_id, r.prompt, r.arrival_us, r.ert_us, r.alpha, r.beta, r.exec_window_us, len(r.plan),
+                   script=r.plan)
+    t0 = time.perf_counter()
+    n = 0
+    while time.perf_counter() - t0 < 10.0:
+        info = ora.step()
+        n += 1
+        if info["n_running"] == 0 and info["n_waiting"] == 0:
+            break
+    out["c4_sched_replay_rounds_per_s"] = n / (time.perf_counter() - t0)
+    out["c4_sched_replay"] = f"{len(reqs)} requests of 1024 agents, {n} rounds (<= 10 s)"
+    return out
 
 
 def run_reference(args, rank, world):

@@ -42,6 +42,8 @@ def main():
              (32, 2884), (64, 8192)]
     if len(sys.argv) > 1 and sys.argv[1] == "small":
         cases = [(1, 4096), (4, 1310), (8, 1310), (16, 2884), (32, 2884)]
+    if len(sys.argv) > 1 and sys.argv[1] == "grid":   # B x ctx at 8B / 70B dims
+        cases = [(b, c) for b in (8, 32, 64, 128, 256) for c in (512, 1310, 2884, 8192)]
     for B, ctx in cases:
         for nq in (32, 64):
             us, gbs = bench(B, ctx, nq=nq)
