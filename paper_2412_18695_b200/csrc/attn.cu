@@ -527,6 +527,11 @@ void attn_plan(int n_rows, int nkv, int max_seqlen, int* chunk_pages, int* max_c
     best_c = (int)((64 + base - 1) / base);
     if (best_c > 8) best_c = 8;
     while (best_c > 1 && max_pages / best_c < 2 * kAttnWarps) --best_c;
+  } else if (base < 96 && max_pages >= 128) {
+    // 32-95 (row, head) pairs leave most of the 148 SMs idle; with >= 2k-token contexts four
+    // chunks pay for the merge (tools/attn_small_b.py, 8 rows x 8 heads: ctx 2884 29.2 ->
+    // 20.7 us, ctx 8192 75.2 -> 46.4 us; 16 rows: no gain, 1310-token contexts: no gain)
+    best_c = 4;
   }
   static int forced = -2;
   if (forced == -2) {
