@@ -170,23 +170,6 @@ RT_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
-// mbar_wait for long waits of warps that are not on the critical path (a GEMM's epilogue
-// warps waiting for the whole mainloop): back off with nanosleep between polls so the
-// waiting warps leave the issue slots to co-resident CTAs' epilogues
-RT_DEV void mbar_wait_backoff(uint64_t* bar, uint32_t parity, uint32_t ns) {
-  uint32_t ok = 0;
-  for (;;) {
-    asm volatile(
-        "{\n\t.reg .pred P1;\n\t"
-        "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, P1;\n\t}"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-    if (ok) return;
-    __nanosleep(ns);
-  }
-}
 // 1-D bulk async copy global -> shared (TMA engine, no tensor map): SASS UBLKCP
 RT_DEV void bulk_g2s(void* smem_dst, const void* gmem_src, uint32_t bytes, uint64_t* bar) {
   asm volatile(

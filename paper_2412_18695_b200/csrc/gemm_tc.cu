@@ -677,8 +677,7 @@ __global__ void __launch_bounds__(kGemmThreads, GemmCfg<BN>::CTAS_PER_SM)
     // per-column metadata + epilogue inputs of the columns this CTA finishes, while the
     // mainloop runs
     pre = column_meta<MODE>(g, sm, m_tile, n0, cb, ce, et);
-    if (g.epi_backoff_ns) mbar_wait_backoff(done, 0, (uint32_t)g.epi_backoff_ns);
-    else mbar_wait(done, 0);
+    mbar_wait(done, 0);
     tc_fence_after();
     if (et == 0) {
       s_tdone = gtimer();
@@ -1700,10 +1699,6 @@ cudaError_t launch_gemm_epi(const bf16* w_tiled, const GemmTmaSet& x, GemmArgs g
   // weights are read once per n-tile; with several n-tiles the later ones should hit L2
   const int n_tiles = (g.N + gemm_bn(g.N) - 1) / gemm_bn(g.N);
   g.l2_evict_first = (l2_hint_enabled() && n_tiles == 1) ? 1 : 0;
-  {
-    static const int ns = getenv("RT_EPI_BACKOFF_NS") ? atoi(getenv("RT_EPI_BACKOFF_NS")) : 0;
-    g.epi_backoff_ns = ns;
-  }
   const int bn = gemm_bn(g.N);
   g.kb_total = g.K / kBK;
   g.m_tiles = (g.M + 127) / 128;

@@ -131,7 +131,6 @@ struct GemmArgs {
   const bf16* pf_w;
   int pf_S, pf_m_tiles, pf_kb_total, pf_kb;
   int l2_evict_first;  // set by launch_gemm_epi: weight tiles are read once per step
-  int epi_backoff_ns;  // set by launch_gemm_epi: nanosleep between the epilogue warps' polls
   // set by launch_gemm_epi: CTA (x, y) runs linear tile tile0 + y of the GEMM's m_tiles x
   // n_tiles tiles (n fastest: the n-tiles of one m-tile are adjacent and the later ones read
   // the weight tile from L2); tile_count tiles in this launch

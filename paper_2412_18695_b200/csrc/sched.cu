@@ -563,7 +563,6 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
     } else {
       if (s >= n_run && T.evicted[task]) {  // restore: own pages re-popped, KV from host
         const int npf = T.n_pfx[task], nh = T.n_hpages[task];
-        const int32_t* hpt = T.hpage_table + (size_t)task * p.pt_stride;
         for (int m = 0; m < nh; ++m) {
           const int q = S.cnt_a[s] + m;
           const int pg = p.free_stack[top - 1 - q];
