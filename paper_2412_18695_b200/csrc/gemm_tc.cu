@@ -1210,50 +1210,70 @@ struct Cfg {
   static constexpr int SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + STG_BYTES + CTL + META + RED;
   static_assert(SMEM <= 227 * 1024, "hybrid stream-K smem");
 };
-// the segment sequence of one CTA: its data-parallel tiles, then its stream-K iterations
+// the segment sequence of one CTA: its PARTIAL stream-K segments first (last one first: it
+// is the head of a tile whose tail the next CTA computes at its start, so both partials of a
+// tile are ready early and the fixup overlaps the whole tiles that follow), then its
+// data-parallel tiles, then its whole stream-K tiles
 struct Sched {
+  static constexpr int MAXS = 8;
   int P, cta, kbt, n_tiles;
   int dp_tiles, dp_mine;     // data-parallel tiles (a multiple of P) and this CTA's count
   long long I_sk;            // stream-K iterations (sk tiles x kbt)
   int qa, qb;                // this CTA's stream-K range
-  __device__ void init(int P_, int cta_, int kbt_, int T, int n_tiles_) {
+  int ns, sl[MAXS], sh[MAXS], st[MAXS];  // stream-K segments in range order (lo, hi, sk tile)
+  int np, order[MAXS];       // partial segments first (reversed), then whole ones
+  __device__ void init(int P_, int cta_, int kbt_, int T, int n_tiles_, bool all_sk) {
     P = P_;
     cta = cta_;
     kbt = kbt_;
     n_tiles = n_tiles_;
-    const int sk_tiles = T <= P ? T : (T % P) + P;
+    const int sk_tiles = (all_sk || T <= P) ? T : (T % P) + P;
     dp_tiles = T - sk_tiles;
     dp_mine = dp_tiles / P;
     I_sk = (long long)sk_tiles * kbt;
     qa = chain::q0(I_sk, cta, P);
     qb = chain::q0(I_sk, cta + 1, P);
+    ns = 0;
+    for (int q = qa; q < qb && ns < MAXS;) {
+      const int t = q / kbt;
+      sl[ns] = q - t * kbt;
+      sh[ns] = min(qb - t * kbt, kbt);
+      st[ns] = t;
+      q = t * kbt + sh[ns];
+      ++ns;
+    }
+    np = 0;
+    for (int i = ns - 1; i >= 0; --i)
+      if (sl[i] != 0 || sh[i] != kbt) order[np++] = i;
+    int k = np;
+    for (int i = 0; i < ns; ++i)
+      if (sl[i] == 0 && sh[i] == kbt) order[k++] = i;
   }
-  // segment iterator: dp index d < dp_mine, then stream-K position q in [qa, qb)
   struct Seg {
     int tile, lo, hi;   // global tile index, k-block range
     int sk_t;           // stream-K tile index (-1: data-parallel)
   };
-  __device__ bool first(Seg& g, int& d, int& q) const {
-    d = 0;
-    q = qa;
-    return next(g, d, q);
+  // step i: [0, np) partial stream-K, [np, np + dp_mine) data-parallel, then whole stream-K
+  __device__ bool first(Seg& g, int& i, int& unused) const {
+    i = 0;
+    unused = 0;
+    return next(g, i, unused);
   }
-  __device__ bool next(Seg& g, int& d, int& q) const {
-    if (d < dp_mine) {
-      g.tile = cta + d * P;
+  __device__ bool next(Seg& g, int& i, int&) const {
+    if (i >= ns + dp_mine) return false;
+    if (i >= np && i < np + dp_mine) {
+      g.tile = cta + (i - np) * P;
       g.lo = 0;
       g.hi = kbt;
       g.sk_t = -1;
-      ++d;
-      return true;
+    } else {
+      const int j = order[i < np ? i : i - dp_mine];
+      g.sk_t = st[j];
+      g.tile = dp_tiles + st[j];
+      g.lo = sl[j];
+      g.hi = sh[j];
     }
-    if (q >= qb) return false;
-    const int t = q / kbt;
-    g.sk_t = t;
-    g.tile = dp_tiles + t;
-    g.lo = q - t * kbt;
-    g.hi = min(qb - t * kbt, kbt);
-    q = t * kbt + g.hi;
+    ++i;
     return true;
   }
 };
@@ -1264,6 +1284,7 @@ struct SkArgs {
   int n_tiles;       // tiles along N (BN rows each)
   float* ws;         // [P][2][BN][128] partial tiles
   unsigned* cnt;     // [m_tiles * n_tiles] zero-initialised, self-resetting tickets
+  int all_sk;        // every tile stream-K (no data-parallel part)
 };
 
 template <int BN, int MODE>
@@ -1302,7 +1323,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int cta = blockIdx.x;
   const int kbt = g.kb_total;
   Sched S;
-  S.init(a.P, cta, kbt, g.m_tiles * a.n_tiles, a.n_tiles);
+  S.init(a.P, cta, kbt, g.m_tiles * a.n_tiles, a.n_tiles, a.all_sk != 0);
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmB);
@@ -1682,7 +1703,10 @@ cudaError_t launch_gemm_epi(const bf16* w_tiled, const GemmTmaSet& x, GemmArgs g
     // only with a data-parallel part (T > 2 waves): measured faster there (gate/up N = 320 /
     // 384 / 512: 103 / 108 / 122 -> 89 / 95 / 116 us) and slower for all-stream-K shapes
     // (few-tile projections pay multi-contributor fixups; the cluster split-K path is better)
-    if (T <= g.sk_cnt_cap && I_sk >= P && T > 2 * P) {
+    static const int sk_mode = getenv("RT_SK_MODE") ? atoi(getenv("RT_SK_MODE")) : 0;
+    const int min_t = sk_mode == 2 ? 1 : (sk_mode == 1 ? P + 1 : 2 * P + 1);
+    a.all_sk = T <= 2 * P ? 1 : 0;
+    if (T <= g.sk_cnt_cap && I_sk >= P && T >= min_t) {
       a.P = P;
       a.ws = g.sk_ws;
       a.cnt = g.sk_cnt;
