@@ -308,6 +308,12 @@ __global__ void __launch_bounds__(256) k_attn_prefill(PrefillArgs a) {
   const int cpp = (npt + NC - 1) / NC;
   const int pb = min(npt, chunk * cpp), pe = min(npt, pb + cpp);
   const int np = pe - pb;
+  // The CTAs of a round that prefill the tails of prompts sharing a long prefix all read the
+  // same prefix pages; walking them in the same order makes every CTA hit the same L2 lines
+  // at the same time.  Each CTA starts its walk at its own page (softmax is order-free; the
+  // diagonal page keeps its causal mask wherever it falls).  RT_PF_NO_ROTATE=1: in order.
+  const int rot = (a.rotate && np > 0) ? (int)(((unsigned)tix * 7u + (unsigned)h * 13u) % (unsigned)np) : 0;
+  auto page_at = [&](int i) { return pb + (i + rot >= np ? i + rot - np : i + rot); };
   const int32_t* ptab = a.page_table + (size_t)T.w * a.pt_stride;
   const unsigned char* pool = (const unsigned char*)a.pool;
   const size_t head_off = (size_t)h * C::BLOCK;
@@ -315,7 +321,7 @@ __global__ void __launch_bounds__(256) k_attn_prefill(PrefillArgs a) {
   if (threadIdx.x == 0)
     for (int i = 0; i < C::STAGES && i < np; ++i) {
       mbar_arrive_expect_tx(&full[i], C::BLOCK);
-      bulk_g2s(smem + i * C::BLOCK, pool + (size_t)ptab[pb + i] * page_stride + head_off, C::BLOCK, &full[i]);
+      bulk_g2s(smem + i * C::BLOCK, pool + (size_t)ptab[page_at(i)] * page_stride + head_off, C::BLOCK, &full[i]);
     }
 
   // q fragments (A operand, rows = the tile's positions), rows outside the chunk are zero
@@ -361,10 +367,11 @@ __global__ void __launch_bounds__(256) k_attn_prefill(PrefillArgs a) {
       mma_bf16_16816(s1, qa[ks], bf1);
     }
     // ---- causal mask (diagonal page) + online softmax; row gq: s*[0..1], row gq+8: s*[2..3]
-    const int k0 = (pb + i) * 16 + 2 * qq;
+    const int pg_i = page_at(i);
+    const int k0 = pg_i * 16 + 2 * qq;
     float x[8] = {s0[0] * sl2, s0[1] * sl2, s1[0] * sl2, s1[1] * sl2,
                   s0[2] * sl2, s0[3] * sl2, s1[2] * sl2, s1[3] * sl2};
-    if (pb + i == npt - 1) {
+    if (pg_i == npt - 1) {
       const int kk[4] = {k0, k0 + 1, k0 + 8, k0 + 9};
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -417,7 +424,7 @@ __global__ void __launch_bounds__(256) k_attn_prefill(PrefillArgs a) {
       mbar_wait(&empty[s], (uint32_t)((i / C::STAGES) & 1));
       fence_proxy_async();
       mbar_arrive_expect_tx(&full[s], C::BLOCK);
-      bulk_g2s(smem + s * C::BLOCK, pool + (size_t)ptab[pb + i + C::STAGES] * page_stride + head_off, C::BLOCK,
+      bulk_g2s(smem + s * C::BLOCK, pool + (size_t)ptab[page_at(i + C::STAGES)] * page_stride + head_off, C::BLOCK,
                &full[s]);
     }
   }
@@ -606,6 +613,8 @@ void launch_attention_prefill(const PrefillArgs& a0, cudaStream_t s) {
   if (a0.n_tiles <= 0 || a0.G < 1 || a0.G > 8) return;
   PrefillArgs a = a0;
   a.chunks = prefill_chunks(a);
+  static const int no_rot = getenv("RT_PF_NO_ROTATE") != nullptr;
+  a.rotate = no_rot ? 0 : 1;
   switch (a.hd) {
     case 128: launch_prefill_hd<128>(a, s); break;
     case 64: launch_prefill_hd<64>(a, s); break;

@@ -82,6 +82,7 @@ struct PrefillArgs {
   float* ws;                // nullable: [tiles][nkv][chunks][G][16][hd + 2] fp32
   int64_t ws_floats;
   int* tickets;             // [tiles][nkv] zeroed, self-resetting
+  int rotate;               // set by launch_attention_prefill: per-CTA page-walk start
 };
 void launch_attention_prefill(const PrefillArgs& a, cudaStream_t s);
 
