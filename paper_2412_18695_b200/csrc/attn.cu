@@ -283,7 +283,9 @@ __global__ void __launch_bounds__(256) k_attn_prefill(PrefillArgs a) {
   uint64_t* empty = full + C::STAGES;
 
   TraceScope tr(TK_ATTN_PREFILL);
-  if (threadIdx.x == 0) pdl_trigger();
+  // no early pdl_trigger here: the next kernel's CTAs (a projection whose MMA / epilogue
+  // warps wait spinning) co-resident with this latency-bound kernel cost it ~25 us per layer
+  // at the e2e operating point (tools/prefill_tail_bench.py); the implicit trigger at exit
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gq = lane >> 2, qq = lane & 3;
   const int G = a.G;
@@ -584,7 +586,13 @@ static void launch_prefill_hd(const PrefillArgs& a, cudaStream_t s) {
     cudaFuncSetAttribute(k_attn_prefill<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     attr = true;
   }
-  launch_pdl(k_attn_prefill<HD>, dim3(a.n_tiles, a.nkv, a.chunks), dim3(32 * a.G), C::SMEM, s, a);
+  // plain stream-ordered launch (no programmatic dependent launch): measured faster for this
+  // latency-bound kernel (tools/prefill_tail_bench.py, RT_PF_PDL=1 to compare)
+  static const bool pdl = getenv("RT_PF_PDL") != nullptr;
+  if (pdl)
+    launch_pdl(k_attn_prefill<HD>, dim3(a.n_tiles, a.nkv, a.chunks), dim3(32 * a.G), C::SMEM, s, a);
+  else
+    k_attn_prefill<HD><<<dim3(a.n_tiles, a.nkv, a.chunks), dim3(32 * a.G), C::SMEM, s>>>(a);
 }
 
 // Split-KV plan of the prefill attention: C page chunks per (tile, kv head), merged by the
