@@ -683,3 +683,37 @@ def test_prefill_projections_hybrid_streamk_match_per_tile(rt, monkeypatch):
         assert na == nb
         scale = max(1.0, float(np.abs(lb).max()))
         assert float(np.abs(la - lb).max()) < 2e-2 * scale
+
+
+def test_set_timing_toggles_event_stats_only(rt):
+    """rt_set_timing (bench pass A / pass B): per-kernel CUDA-event timing on or off does not
+    change any result; attention stats accumulate only while it is on."""
+    shape = MODEL_SHAPES["tiny"]
+    v = make_vocab(shape.vocab)
+    p = engine_params("paper-4090", max_batch=4, max_tasks=64, max_ctx=256, n_pages=64)
+    reqs = compose_workload(4, 1.0, 2, range(1, 9), 30.0, 2, v, prompt_len_range=(40, 64), max_requests=6)
+    outs = []
+    for toggle in (False, True):
+        eng = rt.Engine(shape, p, v, seed=4, flags=rt.RT_FLAG_TIMING | rt.RT_FLAG_KEEP_LOGITS)
+        for r in reqs:
+            eng.submit(r.agent_id, r.prompt, r.arrival_us, r.ert_us, r.alpha, r.beta, r.exec_window_us, len(r.plan),
+                       script=r.plan)
+        logits = []
+        for i in range(30):
+            if toggle:
+                eng.set_timing(i % 2 == 0)
+            info = eng.step()
+            if info["n_running"]:
+                logits.append(eng.dump(rt.RT_DUMP_LOGITS, np.float32).reshape(info["n_running"], -1).copy())
+        eng.sync()
+        segs = eng.poll()
+        if toggle:
+            eng.set_timing(False)
+            eng.reset_stats()
+            for _ in range(3):
+                eng.step()
+            assert eng.stats()["attn_launches"] == 0
+        outs.append((segs, logits))
+        eng.close()
+    assert outs[0][0] == outs[1][0]
+    assert all(np.array_equal(a, b) for a, b in zip(outs[0][1], outs[1][1]))
