@@ -54,7 +54,7 @@ struct GemmCfg {
   static constexpr int A_BYTES = 128 * kBK * 2;    // 16 KB
   static constexpr int B_BYTES = BN * kBK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int STAGES = BN <= 64 ? 4 : (BN == 128 ? 3 : 4);
+  static constexpr int STAGES = BN <= 64 ? 4 : (BN == 128 ? 3 : (BN == 256 ? 4 : 5));
   static constexpr int CTAS_PER_SM = BN <= 128 ? 2 : 1;
   static constexpr int TMEM_COLS = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;  // power of 2
   static constexpr int META = 3 * BN * 4;                       // per-column pos / page / rms scale
@@ -1196,11 +1196,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_chain(const __grid_constant
 // last contributor sums the partials in contributor order (deterministic) and runs the
 // fused epilogue in column chunks staged through shared memory.
 namespace sk {
-constexpr int STAGES = 4;
 constexpr int A_BYTES = 128 * kBK * 2;
 template <int BN>
 struct Cfg {
+  // ring depth: as many stages as fit beside the epilogue staging (the mainloop of these
+  // tensor-bound prefill tiles is latency bound on the L2 / HBM round trip of each stage;
+  // RT_SK_STAGES4 builds keep the earlier 4-stage ring for comparison)
+#ifdef RT_SK_STAGES4
+  static constexpr int STAGES = 4;
   static constexpr int CHUNK = BN == 256 ? 32 : 64;      // epilogue columns per staging pass
+#else
+  static constexpr int STAGES = BN <= 160 ? 5 : 4;
+  static constexpr int CHUNK = BN == 256 ? 32 : 64;
+#endif
   static constexpr int STG_BYTES = CHUNK * 128 * 4;
   static constexpr int B_BYTES = BN * kBK * 2;
   static constexpr int TMEM_COLS = 2 * BN <= 256 ? 256 : 512;
@@ -1293,6 +1301,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   using C = sk::Cfg<BN>;
   using namespace sk;
   constexpr int CHUNK = C::CHUNK;
+  constexpr int STAGES = C::STAGES;
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   unsigned char* sA = smem;
@@ -1551,6 +1560,8 @@ bool make_gemm_act_maps(GemmTmaSet* out, const void* base, int K, int rows_cap) 
 // n-tiles: prefill-heavy rounds are tensor-bound and a padded column costs a full MMA column
 // (tools/gemm_sweep_n.py: N = 320 on 2 x 256 ran at the speed of N = 512).
 int gemm_bn(int N) {
+  static const int force = getenv("RT_GEMM_BN") ? atoi(getenv("RT_GEMM_BN")) : 0;  // experiments
+  if (force && N > 128) return force;
   if (N <= 32) return 32;
   if (N <= 64) return 64;
   if (N <= 128) return 128;
