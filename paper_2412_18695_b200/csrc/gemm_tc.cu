@@ -43,6 +43,8 @@
 #include <cudaTypedefs.h>
 #include "common.cuh"
 #include "model.h"
+#include <map>
+#include <utility>
 
 namespace rt {
 
@@ -1517,6 +1519,343 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
 }
 
+// ------------------------------------------------------- CTA-pair (cta_group::2) path
+// Prefill projections (N > 128 activation rows) are tensor-bound, and with one SM per
+// 128 x BN tile they are bound by SHARED-MEMORY bandwidth: every k-block writes A (16 KB)
+// and B (BN x 128 B) into shared memory by TMA and the MMA reads both back, ~200 B per
+// clock at BN = 192 against ~128 B per clock per SM (ncu: 49 % tensor-pipe active, nothing
+// else saturated, profiles/r01_ncu_gemm_prefill384_full.json).  A CTA pair on the two SMs
+// of a TPC issues ONE tcgen05.mma.cta_group::2 with M = 256: each CTA holds the 128 weight
+// rows of its own m-tile (A) but only HALF of the BN activation rows (B), the tensor core
+// reading the other half from the peer — per SM the B traffic halves (BN = 256: 32 KB per
+// k-block instead of 48 KB).  Persistent, data-parallel: pair p takes the pair-tiles
+// p, p + n_pairs, ...; TMEM holds two BN-column accumulators per CTA (the epilogue of tile
+// i overlaps the mainloop of tile i + 1).
+//   both CTAs, warp 0 lane 0: TMA loads of its A tile (the pre-tiled weight image through a
+//     2-D map, no swizzle: the bytes are already SW128) and its half of X, both completing
+//     on the LEADER's full barrier (cp.async.bulk.tensor .cta_group::2); the leader alone
+//     expects the transaction bytes of both CTAs;
+//   leader, warp 1 lane 0: tcgen05.mma.cta_group::2 (M = 256, N = BN, K = 16), commits
+//     multicast to both CTAs' empty / accumulator-full barriers;
+//   both CTAs, warps 2..5: epilogue of their own 128 output features (the same fused
+//     epilogue as the single-SM kernels), then release the accumulator buffer on the
+//     leader's barrier (count 2: one arrival per CTA).
+namespace sm2 {
+template <int BN>
+struct Cfg {
+  static constexpr int HB = BN / 2;  // activation rows per CTA
+  static constexpr int A_BYTES = 128 * kBK * 2;
+  static constexpr int B_BYTES = HB * kBK * 2;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int CHUNK = 64;
+  static constexpr int STG_BYTES = CHUNK * 128 * 4;
+  static constexpr int TMEM_COLS = 2 * BN <= 256 ? 256 : 512;
+  static constexpr int CTL = 256;
+  static constexpr int META = 3 * BN * 4;
+  static constexpr int RED = 2 * 4 * BN * 4;
+  static constexpr int FIXED = 1024 + STG_BYTES + CTL + META + RED;
+  static constexpr int FIT = (227 * 1024 - FIXED) / STAGE;
+  static constexpr int STAGES = FIT > 8 ? 8 : FIT;
+  static constexpr int SMEM = FIXED + STAGES * STAGE;
+  static_assert(STAGES >= 4, "CTA-pair ring depth");
+};
+}  // namespace sm2
+
+__device__ __forceinline__ void tma_load_2d_pair(void* dst, const void* tmap, int c0, int c1, uint32_t bar_cluster) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, "
+      "%3}], [%4];" ::"r"(smem_u32(dst)),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(bar_cluster)
+      : "memory");
+}
+__device__ __forceinline__ void umma_f16_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                              uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+// arrive on the barrier at this offset in every CTA of `mask` once the issued MMAs complete
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)),
+      "h"(mask)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
+}
+
+// work of one pair: plain data-parallel pair-tiles (pair, pair + n_pairs, ...), or — with a
+// workspace — the hybrid data-parallel + stream-K order of k_gemm_sk over pair-tiles (the
+// last partial round of pair-tiles is spread over all pairs as k-ranges; each CTA of a pair
+// fixes up its own 128 rows of a split pair-tile through the workspace)
+struct PairSeq {
+  sk::Sched S;
+  bool skm;
+  int pair, n_pairs, PT, kbt;
+  __device__ void init(int pair_, int n_pairs_, int PT_, int kbt_, int n_tiles, bool skm_, bool all_sk) {
+    pair = pair_;
+    n_pairs = n_pairs_;
+    PT = PT_;
+    kbt = kbt_;
+    skm = skm_;
+    if (skm) S.init(n_pairs, pair, kbt, PT, n_tiles, all_sk);
+  }
+  __device__ bool next(sk::Sched::Seg& g, int& i) const {
+    if (skm) {
+      int u = 0;
+      return S.next(g, i, u);
+    }
+    const int t = pair + i * n_pairs;
+    if (t >= PT) return false;
+    g.tile = t;
+    g.lo = 0;
+    g.hi = kbt;
+    g.sk_t = -1;
+    ++i;
+    return true;
+  }
+};
+
+template <int BN, int MODE>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    k_gemm_2sm(const __grid_constant__ TmaMap tmA, const __grid_constant__ TmaMap tmB, GemmArgs g, SkArgs a) {
+  using C = sm2::Cfg<BN>;
+  constexpr int STAGES = C::STAGES, CHUNK = C::CHUNK;
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  unsigned char* sA = smem;
+  unsigned char* sB = smem + STAGES * C::A_BYTES;
+  float* stg = reinterpret_cast<float*>(sB + STAGES * C::B_BYTES);
+  unsigned char* ctl = reinterpret_cast<unsigned char*>(stg) + C::STG_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(ctl);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* fxbar = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fxbar + 1);
+  int* s_last = reinterpret_cast<int*>(tmem_slot + 1);
+  EpiSmem sm;
+  sm.pos = reinterpret_cast<int*>(ctl + C::CTL);
+  sm.page = sm.pos + BN;
+  sm.inv = reinterpret_cast<float*>(sm.page + BN);
+  sm.redv = reinterpret_cast<float*>(ctl + C::CTL + C::META);
+  sm.redi = reinterpret_cast<int*>(sm.redv + 4 * BN);
+  sm.bn = BN;
+  sm.xp = stg;  // unused (pre = false)
+  sm.xp_sin = 0;
+  __shared__ long long s_mark[9];
+  sm.mark = s_mark;
+
+  TraceScope tr(TK_GEMM | ((uint32_t)MODE << 8) | (2u << 16));
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int pair = blockIdx.x >> 1;
+  const int kbt = g.kb_total;
+  const int nt_n = a.n_tiles;
+  const int PT = (g.m_tiles >> 1) * nt_n;
+  PairSeq Q;
+  Q.init(pair, a.P, PT, kbt, nt_n, a.ws != nullptr, a.all_sk != 0);
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 2);
+    }
+    mbar_init(fxbar, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(C::TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_arrive();  // the peer's barriers are initialised before anyone signals them
+  cluster_wait();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) pdl_trigger();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint32_t full0 = dsmem_addr(smem_u32(full), 0);  // the leader's full barriers
+      bool waited = false;
+      int n = 0, i = 0;
+      sk::Sched::Seg sg;
+      while (Q.next(sg, i)) {
+        const int mp = sg.tile / nt_n, nt = sg.tile - mp * nt_n;
+        const int m_tile = 2 * mp + (int)rank;
+        for (int kb = sg.lo; kb < sg.hi; ++kb, ++n) {
+          const int st = n % STAGES;
+          if (n >= STAGES) mbar_wait(&empty[st], (uint32_t)(((n / STAGES) & 1) ^ 1));
+          if (rank == 0) mbar_arrive_expect_tx(&full[st], 2 * C::STAGE);
+          tma_load_2d_pair(sA + st * C::A_BYTES, &tmA, 0, (m_tile * kbt + kb) * 128, full0 + st * 8);
+          if (!waited) {  // weights before the previous kernel finishes, activations after
+            pdl_wait();
+            tr.ready();
+            waited = true;
+          }
+          tma_load_2d_pair(sB + st * C::B_BYTES, &tmB, kb * kBK, nt * BN + (int)rank * C::HB, full0 + st * 8);
+        }
+      }
+      if (!waited) pdl_wait();
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (rank == 0 && lane == 0) {
+      constexpr uint32_t idesc = umma_idesc(256, BN);
+      int n = 0, seg = 0, i = 0;
+      sk::Sched::Seg sg;
+      for (; Q.next(sg, i); ++seg) {
+        const int buf = seg & 1;
+        if (seg >= 2) mbar_wait(&tempty[buf], (uint32_t)(((seg >> 1) - 1) & 1));
+        tc_fence_after();
+        const uint32_t acc = tmem + (uint32_t)(buf * BN);
+        for (int kb = sg.lo; kb < sg.hi; ++kb, ++n) {
+          const int st = n % STAGES;
+          mbar_wait(&full[st], (uint32_t)((n / STAGES) & 1));
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sA + st * C::A_BYTES);
+          const uint32_t b0 = smem_u32(sB + st * C::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < kBK / 16; ++k)
+            umma_f16_pair(acc, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
+                          (kb > sg.lo || k > 0) ? 1u : 0u);
+          umma_commit_pair(&empty[st], 0x3);
+        }
+        umma_commit_pair(&tfull[buf], 0x3);
+      }
+    }
+    __syncwarp();
+  } else {
+    pdl_wait();
+    const int et = (warp & 3) * 32 + lane;
+    const uint32_t tb = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+    const uint32_t tempty0 = dsmem_addr(smem_u32(tempty), 0);
+    const int first_sk = Q.skm ? Q.S.qa / kbt : 0;
+    uint32_t fx_phase = 0u;
+    int seg = 0, i = 0;
+    sk::Sched::Seg sg;
+    for (; Q.next(sg, i); ++seg) {
+      const int buf = seg & 1;
+      const int mp = sg.tile / nt_n, nt = sg.tile - mp * nt_n;
+      const int m_tile = 2 * mp + (int)rank;
+      const int n0 = nt * BN;
+      int nc = 1, c_first = 0;
+      if (sg.sk_t >= 0) {
+        c_first = chain::owner((long long)sg.sk_t * kbt, Q.S.I_sk, Q.S.P);
+        nc = chain::owner((long long)(sg.sk_t + 1) * kbt - 1, Q.S.I_sk, Q.S.P) - c_first + 1;
+      }
+      mbar_wait(&tfull[buf], (uint32_t)((seg >> 1) & 1));
+      tc_fence_after();
+      epi_bar();  // the previous tile's epilogue is done with the staging buffer / sm
+      const uint32_t tacc = tb + (uint32_t)(buf * BN);
+      bool run = true;
+      if (nc > 1) {  // a k-range of a split pair-tile: park this CTA's rows in the workspace
+        float* mine = a.ws + ((size_t)blockIdx.x * 2 + (sg.sk_t == first_sk ? 0 : 1)) * (BN * 128);
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 16) {
+          float v[16];
+          tmem_ld16(tacc + (uint32_t)c0, v);
+#pragma unroll
+          for (int k = 0; k < 16; ++k) __stcg(mine + (size_t)(c0 + k) * 128 + et, v[k]);
+        }
+        tc_fence_before();
+        __threadfence();
+        epi_bar();
+        if (et == 0) {
+          if (rank == 0) mbar_arrive(&tempty[buf]);
+          else mbar_arrive_cluster(tempty0 + (uint32_t)buf * 8u);
+          const unsigned old = atomicAdd(a.cnt + sg.tile * 2 + rank, 1u);
+          *s_last = (old == (unsigned)(nc - 1)) ? 1 : 0;
+        }
+        epi_bar();
+        run = *s_last != 0;
+        if (run) {
+          __threadfence();
+          if (et == 0) {
+            a.cnt[sg.tile * 2 + rank] = 0u;
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+          }
+        }
+      }
+      if (run) {
+        column_meta<MODE>(g, sm, m_tile, n0, 0, BN, et);
+        const TileSrc ts0{nullptr, nullptr, 0u, 1, 0, BN, 0, 0, nullptr};
+#pragma unroll 1
+        for (int cb = 0; cb < BN; cb += CHUNK) {
+          const int ce = min(BN, cb + CHUNK);
+          if (nc == 1) {  // whole pair-tile: TMEM -> staging
+#pragma unroll 1
+            for (int c0 = cb; c0 < ce; c0 += 16) {
+              float v[16];
+              tmem_ld16(tacc + (uint32_t)c0, v);
+#pragma unroll
+              for (int k = 0; k < 16; ++k) stg[(c0 - cb + k) * 128 + et] = v[k];
+            }
+            if (ce == BN) {  // the accumulator buffer is read out: release it to the MMA issuer
+              tc_fence_before();
+              epi_bar();
+              if (et == 0) {
+                if (rank == 0) mbar_arrive(&tempty[buf]);
+                else mbar_arrive_cluster(tempty0 + (uint32_t)buf * 8u);
+              }
+            }
+          } else {  // sum the nc partials of columns [cb, ce) in contributor order
+            float acc[CHUNK];
+#pragma unroll
+            for (int c = 0; c < CHUNK; ++c) acc[c] = 0.f;
+            const uint32_t bytes = (uint32_t)((ce - cb) * 512);
+            for (int r = 0; r < nc; ++r) {
+              const int c = c_first + r;
+              if (et == 0) {
+                const int fs = chain::q0(Q.S.I_sk, c, Q.S.P) / kbt;
+                const float* src =
+                    a.ws + ((size_t)(2 * c + (int)rank) * 2 + (sg.sk_t == fs ? 0 : 1)) * (BN * 128) + (size_t)cb * 128;
+                mbar_arrive_expect_tx(fxbar, bytes);
+                bulk_g2s(stg, src, bytes, fxbar);
+              }
+              mbar_wait(fxbar, fx_phase);
+              fx_phase ^= 1u;
+#pragma unroll
+              for (int cc = 0; cc < CHUNK; ++cc)
+                if (cb + cc < ce) acc[cc] += stg[cc * 128 + et];
+              epi_bar();  // the staging buffer is free for the next partial
+            }
+#pragma unroll
+            for (int cc = 0; cc < CHUNK; ++cc)
+              if (cb + cc < ce) stg[cc * 128 + et] = acc[cc];
+          }
+          epi_bar();
+          TileSrc ts = ts0;
+          ts.P = stg - (size_t)cb * 128;  // the epilogue indexes absolute columns
+          epilogue<MODE>(g, sm, ts, m_tile, n0, cb, ce, et, false);
+          epi_bar();
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_arrive();  // no CTA leaves while its peer may still signal its barriers
+  cluster_wait();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(C::TMEM_COLS));
+  }
+}
+
 // ------------------------------------------------------------- host side
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -1528,6 +1867,20 @@ static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
       fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
   }
   return fn;
+}
+
+static bool make_tma_2d_bf16_sw(TmaMap* out, const void* base, uint64_t inner, uint64_t rows, uint32_t box_inner,
+                                uint32_t box_rows, CUtensorMapSwizzle sw) {
+  auto enc = get_encode();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {inner, rows};
+  cuuint64_t strides[1] = {inner * 2};
+  cuuint32_t box[2] = {box_inner, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(reinterpret_cast<CUtensorMap*>(out->bytes), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                   const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
 }
 
 bool make_tma_2d_bf16(TmaMap* out, const void* base, uint64_t inner, uint64_t rows, uint32_t box_inner,
@@ -1549,6 +1902,8 @@ bool make_gemm_act_maps(GemmTmaSet* out, const void* base, int K, int rows_cap) 
   out->rows_cap = rows_cap;
   return make_tma_2d_bf16(&out->m32, base, K, rows_cap, kBK, 32) &&
          make_tma_2d_bf16(&out->m64, base, K, rows_cap, kBK, 64) &&
+         make_tma_2d_bf16(&out->m80, base, K, rows_cap, kBK, 80) &&
+         make_tma_2d_bf16(&out->m96, base, K, rows_cap, kBK, 96) &&
          make_tma_2d_bf16(&out->m128, base, K, rows_cap, kBK, 128) &&
          make_tma_2d_bf16(&out->m160, base, K, rows_cap, kBK, 160) &&
          make_tma_2d_bf16(&out->m192, base, K, rows_cap, kBK, 192) &&
@@ -1694,9 +2049,143 @@ static cudaError_t launch_sk_mode(const GemmTmaSet& x, const GemmArgs& g, const 
   return launch_sk_bn<256, MODE>(x.m256, g, a, s);
 }
 
+// ---- CTA-pair launch (k_gemm_2sm)
+// weight operand of the pair kernel: the pre-tiled image read as rows of 64 bf16 (128 B), one
+// 16 KB box per (m-tile, k-block); the map depends only on (pointer, rows): cached
+static const TmaMap* weight_map(const bf16* w, uint64_t rows) {
+  static std::map<std::pair<const void*, uint64_t>, TmaMap> cache;
+  const auto key = std::make_pair((const void*)w, rows);
+  auto it = cache.find(key);
+  if (it != cache.end()) return &it->second;
+  TmaMap m;
+  if (!make_tma_2d_bf16_sw(&m, w, kBK, rows, kBK, 128, CU_TENSOR_MAP_SWIZZLE_NONE)) return nullptr;
+  return &cache.emplace(key, m).first->second;
+}
+template <int BN, int MODE>
+static cudaError_t launch_2sm_bn(const TmaMap& am, const TmaMap& bm, const GemmArgs& g, int PT, SkArgs a,
+                                 cudaStream_t s) {
+  using C = sm2::Cfg<BN>;
+  static int slots = 0;
+  if (PT <= 0) {  // query: co-resident pairs
+    if (slots) return cudaSuccess;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  if (!slots) {  // co-resident CTA pairs (persistent grid)
+    cudaFuncSetAttribute(k_gemm_2sm<BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cfg.gridDim = dim3(sm_count() & ~1);
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, k_gemm_2sm<BN, MODE>, &cfg) != cudaSuccess || n <= 0) {
+      cudaGetLastError();
+      n = sm_count() / 2;
+    }
+    slots = n;
+  }
+  if (PT <= 0) return cudaSuccess;
+  const int n_pairs = std::min(PT, slots);
+  a.P = n_pairs;
+  cfg.gridDim = dim3(2 * n_pairs);
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, k_gemm_2sm<BN, MODE>, am, bm, g, a);
+}
+template <int MODE>
+static cudaError_t launch_2sm_mode(const TmaMap& am, const GemmTmaSet& x, const GemmArgs& g, int bn, int PT,
+                                   const SkArgs& a, cudaStream_t s) {
+  if (bn == 160) return launch_2sm_bn<160, MODE>(am, x.m80, g, PT, a, s);
+  if (bn == 192) return launch_2sm_bn<192, MODE>(am, x.m96, g, PT, a, s);
+  return launch_2sm_bn<256, MODE>(am, x.m128, g, PT, a, s);
+}
+// RT_GEMM_PAIR: unset = tile widths 192 / 256 (measured: gate/up at 256 / 384 / 512 rows
+// 65.8 / 93.5 / 120.6 -> 61.7 / 90.2 / 103.5 us; at 160-wide tiles the pair rounds quantise
+// worse than the single-SM stream-K kernel, 83.3 -> 88.5 us at 320 rows), 0 = off, 1 = all widths
+static bool pair_enabled(int bn) {
+  const char* e = getenv("RT_GEMM_PAIR");
+  if (!e) return bn >= 192;
+  return atoi(e) != 0;
+}
+// co-resident CTA pairs of the pair kernel at this tile width (occupancy query, cached)
+template <int BN>
+static int pair_slots_bn() {
+  static int n = 0;
+  if (!n) {
+    GemmArgs g{};
+    TmaMap t{};
+    launch_2sm_bn<BN, EPI_STORE>(t, t, g, 0, SkArgs{}, nullptr);
+    cudaLaunchConfig_t cfg{};
+    cfg.blockDim = dim3(kGemmThreads);
+    cfg.dynamicSmemBytes = sm2::Cfg<BN>::SMEM;
+    cfg.gridDim = dim3(sm_count() & ~1);
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    if (cudaOccupancyMaxActiveClusters(&n, k_gemm_2sm<BN, EPI_STORE>, &cfg) != cudaSuccess || n <= 0) {
+      cudaGetLastError();
+      n = sm_count() / 2;
+    }
+  }
+  return n;
+}
+static int pair_slots(int bn) {
+  return bn == 160 ? pair_slots_bn<160>() : (bn == 192 ? pair_slots_bn<192>() : pair_slots_bn<256>());
+}
+
 int64_t gemm_sk_ws_floats() { return (int64_t)sm_count() * 2 * 256 * 128; }
 
 cudaError_t launch_gemm_epi(const bf16* w_tiled, const GemmTmaSet& x, GemmArgs g, int splits, cudaStream_t s) {
+  // CTA-pair kernel for the tensor-bound prefill path: every pair busy (at least one
+  // pair-tile per co-resident pair) and an even number of 128-row m-tiles
+  if (g.N > 128 && g.mode != EPI_ARGMAX && g.K % kBK == 0 && pair_enabled(gemm_bn(g.N))) {
+    const int bn = gemm_bn(g.N);
+    const int m_tiles = (g.M + 127) / 128, n_tiles = (g.N + bn - 1) / bn;
+    const int PT = (m_tiles / 2) * n_tiles;
+    static const int min_pt = getenv("RT_GEMM_PAIR_MIN") ? atoi(getenv("RT_GEMM_PAIR_MIN")) : 0;
+    const int slots = pair_slots(bn);
+    if (m_tiles % 2 == 0 && PT >= (min_pt > 0 ? min_pt : slots)) {
+      const TmaMap* am = weight_map(w_tiled, (uint64_t)m_tiles * (g.K / kBK) * 128);
+      if (am) {
+        g.w = w_tiled;
+        g.kb_total = g.K / kBK;
+        g.m_tiles = m_tiles;
+        g.n_tiles = n_tiles;
+        g.l2_evict_first = 0;
+        SkArgs a{};
+        a.n_tiles = n_tiles;
+        // a partial last round of pair-tiles (gate/up at 256..512 rows: 224 = 3 x 74 + 2) is
+        // spread over all pairs by stream-K when the caller provides the workspace
+        // (opt-in RT_PAIR_SK=1: measured slower — the fixups of 76 split pair-tiles cost more than
+        // the balance gains, gate/up 384 / 512 rows 90.2 / 103.5 -> 89.0 / 106.7 us, and far
+        // slower with every pair-tile split at 192 / 256 rows)
+        static const int pair_sk = getenv("RT_PAIR_SK") ? atoi(getenv("RT_PAIR_SK")) : 0;
+        if (pair_sk && g.sk_ws && g.sk_cnt && PT % slots != 0 && 2 * PT <= g.sk_cnt_cap) {
+          a.ws = g.sk_ws;
+          a.cnt = g.sk_cnt;
+          a.all_sk = PT <= 2 * slots ? 1 : 0;
+        }
+        switch (g.mode) {
+          case EPI_STORE: return launch_2sm_mode<EPI_STORE>(*am, x, g, bn, PT, a, s);
+          case EPI_QKV: return launch_2sm_mode<EPI_QKV>(*am, x, g, bn, PT, a, s);
+          case EPI_RESID: return launch_2sm_mode<EPI_RESID>(*am, x, g, bn, PT, a, s);
+          case EPI_SWIGLU: return launch_2sm_mode<EPI_SWIGLU>(*am, x, g, bn, PT, a, s);
+          default: return cudaErrorInvalidValue;
+        }
+      }
+    }
+  }
   // hybrid data-parallel + stream-K persistent kernel for the tensor-bound prefill path
   // (N > 128 rows, more than two waves of tiles) when the caller provides its workspace
   // (RT_NO_STREAMK=1 in the engine: one tile per CTA below)

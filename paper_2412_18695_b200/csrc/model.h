@@ -93,7 +93,7 @@ struct TmaMap {
 bool make_tma_2d_bf16(TmaMap* out, const void* base, uint64_t inner, uint64_t rows, uint32_t box_inner,
                       uint32_t box_rows);
 struct GemmTmaSet {       // activation operand: one map per supported N tile
-  TmaMap m32, m64, m128, m160, m192, m256;
+  TmaMap m32, m64, m80, m96, m128, m160, m192, m256;  // m80 / m96 / m128: CTA-pair halves
   int rows_cap;
 };
 bool make_gemm_act_maps(GemmTmaSet* out, const void* base, int K, int rows_cap);

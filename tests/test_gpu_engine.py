@@ -662,11 +662,15 @@ def test_prefill_projections_hybrid_streamk_match_per_tile(rt, monkeypatch):
     p = engine_params("b200-roofline", max_batch=8, max_tasks=16, max_ctx=512, n_pages=8 * 32)
     from synth.traces import make_trace
     out = {}
-    for mode in ("hybrid", "per_tile"):
+    for mode in ("hybrid", "per_tile", "pair"):
         if mode == "per_tile":
             monkeypatch.setenv("RT_NO_STREAMK", "1")
         else:
             monkeypatch.delenv("RT_NO_STREAMK", raising=False)
+        if mode == "pair":   # CTA-pair kernel (cta_group::2) for every projection of the prefill
+            monkeypatch.setenv("RT_GEMM_PAIR", "1")
+        else:
+            monkeypatch.delenv("RT_GEMM_PAIR", raising=False)
         eng = rt.Engine(shape, p, v, seed=23, flags=rt.RT_FLAG_KEEP_LOGITS, max_rows_per_forward=4096)
         for a in range(8):
             tr = make_trace(1 + a, v, seed=a, prompt_len=200, plan_len=12)
@@ -679,10 +683,11 @@ def test_prefill_projections_hybrid_streamk_match_per_tile(rt, monkeypatch):
         out[mode] = logs
         eng.close()
     assert out["hybrid"][0][0] == 1600
-    for (na, la), (nb, lb) in zip(out["hybrid"], out["per_tile"]):
-        assert na == nb
-        scale = max(1.0, float(np.abs(lb).max()))
-        assert float(np.abs(la - lb).max()) < 2e-2 * scale
+    for other in ("hybrid", "pair"):
+        for (na, la), (nb, lb) in zip(out[other], out["per_tile"]):
+            assert na == nb
+            scale = max(1.0, float(np.abs(lb).max()))
+            assert float(np.abs(la - lb).max()) < 2e-2 * scale, other
 
 
 def test_set_timing_toggles_event_stats_only(rt):

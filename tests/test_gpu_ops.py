@@ -85,6 +85,18 @@ def test_gemm_tcgen05(rt, M, N, K, splits):
     assert err < 1e-3 * max(1.0, (K / 512) ** 0.5), err
 
 
+@pytest.mark.parametrize("M,N,K", [(28672, 320, 512), (28672, 512, 4096), (19200, 200, 512), (38400, 150, 256),
+                                   (9728, 300, 512), (20480, 161, 1024), (6144, 1600, 1024), (4096, 1600, 2048)])
+def test_gemm_cta_pair(rt, M, N, K, monkeypatch):
+    """CTA-pair projections (tcgen05.mma.cta_group::2, RT_GEMM_PAIR=1): eligible shapes only
+    (N > 128, an even number of 128-row m-tiles, >= 74 pair-tiles: one per co-resident pair);
+    ragged N (161, 200, 300) leaves the second CTA's half of the last n-tile partly empty."""
+    monkeypatch.setenv("RT_GEMM_PAIR", "1")
+    bn = min((160, 192, 256), key=lambda b: (-(-N // b) * b, -(-N // b)))
+    assert (M // 128) % 2 == 0 and (M // 256) * -(-N // bn) >= 74
+    test_gemm_tcgen05(rt, M, N, K, 0)
+
+
 @pytest.mark.parametrize("M,N,K", [(512, 4, 128), (128256, 64, 1024), (1000, 33, 256)])
 def test_lm_argmax(rt, M, N, K):
     g = torch.Generator().manual_seed(N)
