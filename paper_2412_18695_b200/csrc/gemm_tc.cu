@@ -1295,6 +1295,9 @@ struct SkArgs {
   float* ws;         // [P][2][BN][128] partial tiles
   unsigned* cnt;     // [m_tiles * n_tiles] zero-initialised, self-resetting tickets
   int all_sk;        // every tile stream-K (no data-parallel part)
+  // CTA-pair kernel, data-parallel order: pair-tiles [head, PT) (the partial last round) run
+  // as sub_s sub-tiles of kPairSubW columns each, one per pair (0: no sub-tiles)
+  int head, sub_s;
 };
 
 template <int BN, int MODE>
@@ -1592,29 +1595,52 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
 // workspace — the hybrid data-parallel + stream-K order of k_gemm_sk over pair-tiles (the
 // last partial round of pair-tiles is spread over all pairs as k-ranges; each CTA of a pair
 // fixes up its own 128 rows of a split pair-tile through the workspace)
+constexpr int kPairSubW = 64;  // sub-tile width of the partial last round (32 rows per CTA)
+struct PSeg {
+  int tile, lo, hi;  // pair-tile, k-block range
+  int sk_t;          // stream-K tile index (-1: whole)
+  int sub;           // sub-tile (columns [sub * kPairSubW, +kPairSubW) of the pair-tile), -1: whole
+};
 struct PairSeq {
   sk::Sched S;
   bool skm;
-  int pair, n_pairs, PT, kbt;
-  __device__ void init(int pair_, int n_pairs_, int PT_, int kbt_, int n_tiles, bool skm_, bool all_sk) {
+  int pair, n_pairs, PT, kbt, head, sub_s;
+  __device__ void init(int pair_, int n_pairs_, int PT_, int kbt_, int n_tiles, bool skm_, bool all_sk, int head_,
+                       int sub_s_) {
     pair = pair_;
     n_pairs = n_pairs_;
     PT = PT_;
     kbt = kbt_;
     skm = skm_;
+    head = sub_s_ > 0 ? head_ : PT_;
+    sub_s = sub_s_;
     if (skm) S.init(n_pairs, pair, kbt, PT, n_tiles, all_sk);
   }
-  __device__ bool next(sk::Sched::Seg& g, int& i) const {
+  __device__ bool next(PSeg& g, int& i) const {
+    g.sub = -1;
     if (skm) {
       int u = 0;
-      return S.next(g, i, u);
+      sk::Sched::Seg q;
+      if (!S.next(q, i, u)) return false;
+      g.tile = q.tile;
+      g.lo = q.lo;
+      g.hi = q.hi;
+      g.sk_t = q.sk_t;
+      return true;
     }
-    const int t = pair + i * n_pairs;
-    if (t >= PT) return false;
-    g.tile = t;
     g.lo = 0;
     g.hi = kbt;
     g.sk_t = -1;
+    const int t = pair + i * n_pairs;
+    if (t < head) {
+      g.tile = t;
+      ++i;
+      return true;
+    }
+    // the partial last round: sub-tile u = pair of the tail pair-tiles' sub_s sub-tiles
+    if (sub_s == 0 || t - pair != head || pair >= (PT - head) * sub_s) return false;
+    g.tile = head + pair / sub_s;
+    g.sub = pair % sub_s;
     ++i;
     return true;
   }
@@ -1622,7 +1648,8 @@ struct PairSeq {
 
 template <int BN, int MODE>
 __global__ void __launch_bounds__(kGemmThreads, 1)
-    k_gemm_2sm(const __grid_constant__ TmaMap tmA, const __grid_constant__ TmaMap tmB, GemmArgs g, SkArgs a) {
+    k_gemm_2sm(const __grid_constant__ TmaMap tmA, const __grid_constant__ TmaMap tmB,
+               const __grid_constant__ TmaMap tmBs, GemmArgs g, SkArgs a) {
   using C = sm2::Cfg<BN>;
   constexpr int STAGES = C::STAGES, CHUNK = C::CHUNK;
   extern __shared__ unsigned char smem_raw[];
@@ -1658,11 +1685,12 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int nt_n = a.n_tiles;
   const int PT = (g.m_tiles >> 1) * nt_n;
   PairSeq Q;
-  Q.init(pair, a.P, PT, kbt, nt_n, a.ws != nullptr, a.all_sk != 0);
+  Q.init(pair, a.P, PT, kbt, nt_n, a.ws != nullptr, a.all_sk != 0, a.head, a.sub_s);
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA);
     prefetch_tmap(&tmB);
+    prefetch_tmap(&tmBs);
     for (int i = 0; i < STAGES; ++i) {
       mbar_init(&full[i], 1);
       mbar_init(&empty[i], 1);
@@ -1692,21 +1720,25 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const uint32_t full0 = dsmem_addr(smem_u32(full), 0);  // the leader's full barriers
       bool waited = false;
       int n = 0, i = 0;
-      sk::Sched::Seg sg;
+      PSeg sg;
       while (Q.next(sg, i)) {
         const int mp = sg.tile / nt_n, nt = sg.tile - mp * nt_n;
         const int m_tile = 2 * mp + (int)rank;
+        const bool sub = sg.sub >= 0;
+        // activation rows of this CTA: its half of the tile, or of the sub-tile
+        const int brow = sub ? nt * BN + sg.sub * kPairSubW + (int)rank * (kPairSubW / 2) : nt * BN + (int)rank * C::HB;
+        const uint32_t bytes = sub ? 2u * (C::A_BYTES + (kPairSubW / 2) * kBK * 2) : 2u * C::STAGE;
         for (int kb = sg.lo; kb < sg.hi; ++kb, ++n) {
           const int st = n % STAGES;
           if (n >= STAGES) mbar_wait(&empty[st], (uint32_t)(((n / STAGES) & 1) ^ 1));
-          if (rank == 0) mbar_arrive_expect_tx(&full[st], 2 * C::STAGE);
+          if (rank == 0) mbar_arrive_expect_tx(&full[st], bytes);
           tma_load_2d_pair(sA + st * C::A_BYTES, &tmA, 0, (m_tile * kbt + kb) * 128, full0 + st * 8);
           if (!waited) {  // weights before the previous kernel finishes, activations after
             pdl_wait();
             tr.ready();
             waited = true;
           }
-          tma_load_2d_pair(sB + st * C::B_BYTES, &tmB, kb * kBK, nt * BN + (int)rank * C::HB, full0 + st * 8);
+          tma_load_2d_pair(sB + st * C::B_BYTES, sub ? &tmBs : &tmB, kb * kBK, brow, full0 + st * 8);
         }
       }
       if (!waited) pdl_wait();
@@ -1714,10 +1746,10 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     __syncwarp();
   } else if (warp == 1) {
     if (rank == 0 && lane == 0) {
-      constexpr uint32_t idesc = umma_idesc(256, BN);
       int n = 0, seg = 0, i = 0;
-      sk::Sched::Seg sg;
+      PSeg sg;
       for (; Q.next(sg, i); ++seg) {
+        const uint32_t idesc = sg.sub >= 0 ? umma_idesc(256, kPairSubW) : umma_idesc(256, BN);
         const int buf = seg & 1;
         if (seg >= 2) mbar_wait(&tempty[buf], (uint32_t)(((seg >> 1) - 1) & 1));
         tc_fence_after();
@@ -1746,12 +1778,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int first_sk = Q.skm ? Q.S.qa / kbt : 0;
     uint32_t fx_phase = 0u;
     int seg = 0, i = 0;
-    sk::Sched::Seg sg;
+    PSeg sg;
     for (; Q.next(sg, i); ++seg) {
       const int buf = seg & 1;
       const int mp = sg.tile / nt_n, nt = sg.tile - mp * nt_n;
       const int m_tile = 2 * mp + (int)rank;
-      const int n0 = nt * BN;
+      const int n0 = nt * BN + (sg.sub >= 0 ? sg.sub * kPairSubW : 0);
+      const int W = sg.sub >= 0 ? kPairSubW : BN;  // accumulator columns of this segment
       int nc = 1, c_first = 0;
       if (sg.sk_t >= 0) {
         c_first = chain::owner((long long)sg.sk_t * kbt, Q.S.I_sk, Q.S.P);
@@ -1791,11 +1824,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         }
       }
       if (run) {
-        column_meta<MODE>(g, sm, m_tile, n0, 0, BN, et);
+        column_meta<MODE>(g, sm, m_tile, n0, 0, W, et);
         const TileSrc ts0{nullptr, nullptr, 0u, 1, 0, BN, 0, 0, nullptr};
 #pragma unroll 1
-        for (int cb = 0; cb < BN; cb += CHUNK) {
-          const int ce = min(BN, cb + CHUNK);
+        for (int cb = 0; cb < W; cb += CHUNK) {
+          const int ce = min(W, cb + CHUNK);
           if (nc == 1) {  // whole pair-tile: TMEM -> staging
 #pragma unroll 1
             for (int c0 = cb; c0 < ce; c0 += 16) {
@@ -1804,7 +1837,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
               for (int k = 0; k < 16; ++k) stg[(c0 - cb + k) * 128 + et] = v[k];
             }
-            if (ce == BN) {  // the accumulator buffer is read out: release it to the MMA issuer
+            if (ce == W) {  // the accumulator buffer is read out: release it to the MMA issuer
               tc_fence_before();
               epi_bar();
               if (et == 0) {
@@ -2062,8 +2095,8 @@ static const TmaMap* weight_map(const bf16* w, uint64_t rows) {
   return &cache.emplace(key, m).first->second;
 }
 template <int BN, int MODE>
-static cudaError_t launch_2sm_bn(const TmaMap& am, const TmaMap& bm, const GemmArgs& g, int PT, SkArgs a,
-                                 cudaStream_t s) {
+static cudaError_t launch_2sm_bn(const TmaMap& am, const TmaMap& bm, const TmaMap& bms, const GemmArgs& g, int PT,
+                                 SkArgs a, cudaStream_t s) {
   using C = sm2::Cfg<BN>;
   static int slots = 0;
   if (PT <= 0) {  // query: co-resident pairs
@@ -2095,16 +2128,26 @@ static cudaError_t launch_2sm_bn(const TmaMap& am, const TmaMap& bm, const GemmA
   if (PT <= 0) return cudaSuccess;
   const int n_pairs = std::min(PT, slots);
   a.P = n_pairs;
+  a.head = PT;
+  a.sub_s = 0;
+  // partial last round of whole pair-tiles: if its sub-tiles fit one per pair, run them
+  // instead (gate/up at 384 / 512 rows: 224 pair-tiles = 3 x 74 + 2 -> 2 x 3 / 2 x 4 sub-tiles)
+  static const bool sub_off = getenv("RT_PAIR_NO_SUB") != nullptr;
+  if (!a.ws && !sub_off && PT > n_pairs && PT % n_pairs && BN % kPairSubW == 0 &&
+      (PT % n_pairs) * (BN / kPairSubW) <= n_pairs) {
+    a.head = PT - PT % n_pairs;
+    a.sub_s = BN / kPairSubW;
+  }
   cfg.gridDim = dim3(2 * n_pairs);
   cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, k_gemm_2sm<BN, MODE>, am, bm, g, a);
+  return cudaLaunchKernelEx(&cfg, k_gemm_2sm<BN, MODE>, am, bm, bms, g, a);
 }
 template <int MODE>
 static cudaError_t launch_2sm_mode(const TmaMap& am, const GemmTmaSet& x, const GemmArgs& g, int bn, int PT,
                                    const SkArgs& a, cudaStream_t s) {
-  if (bn == 160) return launch_2sm_bn<160, MODE>(am, x.m80, g, PT, a, s);
-  if (bn == 192) return launch_2sm_bn<192, MODE>(am, x.m96, g, PT, a, s);
-  return launch_2sm_bn<256, MODE>(am, x.m128, g, PT, a, s);
+  if (bn == 160) return launch_2sm_bn<160, MODE>(am, x.m80, x.m32, g, PT, a, s);
+  if (bn == 192) return launch_2sm_bn<192, MODE>(am, x.m96, x.m32, g, PT, a, s);
+  return launch_2sm_bn<256, MODE>(am, x.m128, x.m32, g, PT, a, s);
 }
 // RT_GEMM_PAIR: unset = tile widths 192 / 256 (measured: gate/up at 256 / 384 / 512 rows
 // 65.8 / 93.5 / 120.6 -> 61.7 / 90.2 / 103.5 us; at 160-wide tiles the pair rounds quantise
@@ -2121,7 +2164,7 @@ static int pair_slots_bn() {
   if (!n) {
     GemmArgs g{};
     TmaMap t{};
-    launch_2sm_bn<BN, EPI_STORE>(t, t, g, 0, SkArgs{}, nullptr);
+    launch_2sm_bn<BN, EPI_STORE>(t, t, t, g, 0, SkArgs{}, nullptr);
     cudaLaunchConfig_t cfg{};
     cfg.blockDim = dim3(kGemmThreads);
     cfg.dynamicSmemBytes = sm2::Cfg<BN>::SMEM;

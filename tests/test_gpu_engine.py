@@ -650,11 +650,15 @@ def test_sched_parity_stop_grammars(rt, grammar):
     assert sum(1 for s in segs if s["reason"] == 3) > 20
 
 
-def test_prefill_projections_hybrid_streamk_match_per_tile(rt, monkeypatch):
+@pytest.mark.parametrize("prompt_len", [200, 64, 160])
+def test_prefill_projections_hybrid_streamk_match_per_tile(rt, monkeypatch, prompt_len):
     """The hybrid data-parallel + stream-K prefill projections (k_gemm_sk: > 2 waves of
     tiles, here gate/up and QKV of a 1600-row prefill at 8B dims) against one tile per CTA
     (RT_NO_STREAMK=1): same scripted rounds, the logits of the prefill round (token 0 of every
-    request) and of later decode rounds agree to fp32 summation-order level."""
+    request) and of later decode rounds agree to fp32 summation-order level.  "pair" runs the
+    CTA-pair kernel (cta_group::2) for every eligible projection; 512 prompt rows put gate/up's
+    partial last round into 64-column sub-tiles (SwiGLU epilogue), 1280 rows the O and down
+    projections' (residual epilogue), 1600 rows the 160-wide pair tiles."""
     from synth.configs import ModelShape
     s8 = MODEL_SHAPES["llama3-8b"]
     shape = ModelShape("sk", 2, s8.d_model, s8.n_q_heads, s8.n_kv_heads, s8.head_dim, s8.d_ff, s8.vocab)
@@ -667,13 +671,11 @@ def test_prefill_projections_hybrid_streamk_match_per_tile(rt, monkeypatch):
             monkeypatch.setenv("RT_NO_STREAMK", "1")
         else:
             monkeypatch.delenv("RT_NO_STREAMK", raising=False)
-        if mode == "pair":   # CTA-pair kernel (cta_group::2) for every projection of the prefill
-            monkeypatch.setenv("RT_GEMM_PAIR", "1")
-        else:
-            monkeypatch.delenv("RT_GEMM_PAIR", raising=False)
+        # CTA-pair kernel (cta_group::2) for every eligible projection, or single-SM kernels only
+        monkeypatch.setenv("RT_GEMM_PAIR", "1" if mode == "pair" else "0")
         eng = rt.Engine(shape, p, v, seed=23, flags=rt.RT_FLAG_KEEP_LOGITS, max_rows_per_forward=4096)
         for a in range(8):
-            tr = make_trace(1 + a, v, seed=a, prompt_len=200, plan_len=12)
+            tr = make_trace(1 + a, v, seed=a, prompt_len=prompt_len, plan_len=12)
             eng.submit(a, tr.prompt, 0, tr.ert_us, tr.alpha, tr.beta, 90000, script=tr.plan)
         logs = []
         for _ in range(4):
@@ -682,7 +684,7 @@ def test_prefill_projections_hybrid_streamk_match_per_tile(rt, monkeypatch):
             logs.append((info["n_prefill_rows"], eng.dump(rt.RT_DUMP_LOGITS, np.float32).reshape(B, -1).copy()))
         out[mode] = logs
         eng.close()
-    assert out["hybrid"][0][0] == 1600
+    assert out["hybrid"][0][0] == 8 * prompt_len
     for other in ("hybrid", "pair"):
         for (na, la), (nb, lb) in zip(out[other], out["per_tile"]):
             assert na == nb
