@@ -44,6 +44,27 @@ __global__ void __launch_bounds__(kAttnWarps * 32) k_attn(AttnArgs a) {
   TraceScope tr(TK_ATTN);
   if (threadIdx.x == 0) pdl_trigger();
   const int chunk = blockIdx.x, h = blockIdx.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = a.G;
+  const int gq = lane >> 2, qq = lane & 3;
+  unsigned char* ring = smem + warp * C::STAGES * C::BLOCK;
+  uint64_t* bar = bars + warp * C::STAGES;
+  const unsigned char* pool = (const unsigned char*)a.pool;
+  const size_t head_off = (size_t)h * C::BLOCK;
+  const size_t page_stride = (size_t)a.nkv * C::BLOCK;
+  if (lane == 0) {
+    for (int s = 0; s < C::STAGES; ++s) mbar_init(&bar[s], 1);
+    fence_mbar_init();
+  }
+  const uint64_t pol = a.l2_evict_first ? l2_policy_evict_first() : 0ull;
+  __syncwarp();
+  // Everything below reads this round's row metadata, page tables, q and KV pages: only after
+  // the dependency wait.  (The row metadata comes from the scheduler kernel at the start of
+  // the round; with programmatic dependent launch a chain of early-launched kernels can reach
+  // this kernel before the scheduler has finished, so even it is not safe to read earlier —
+  // the first layer's attention read stale rows intermittently when it was.)
+  pdl_wait();
+  tr.ready();
   const int row = a.row_list ? a.row_list[blockIdx.z] : a.row0 + (int)blockIdx.z;
   const int r = row - a.row0;  // row within this forward chunk
   if (a.row_list && (r < 0 || r >= a.chunk_rows)) return;
@@ -55,26 +76,8 @@ __global__ void __launch_bounds__(kAttnWarps * 32) k_attn(AttnArgs a) {
   const int p_end = min(p_begin + a.chunk_pages, n_pages);
   const int task = a.row_task[row];
   const int32_t* ptab = a.page_table + (size_t)task * a.pt_stride;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int G = a.G;
-  const int gq = lane >> 2, qq = lane & 3;
-
-  unsigned char* ring = smem + warp * C::STAGES * C::BLOCK;
-  uint64_t* bar = bars + warp * C::STAGES;
-  const unsigned char* pool = (const unsigned char*)a.pool;
-  const size_t head_off = (size_t)h * C::BLOCK;
-  const size_t page_stride = (size_t)a.nkv * C::BLOCK;
-
   // pages of this warp: p_begin + warp + i * NW
   const int n_my = p_end - (p_begin + warp) > 0 ? (p_end - (p_begin + warp) + kAttnWarps - 1) / kAttnWarps : 0;
-  if (lane == 0) {
-    for (int s = 0; s < C::STAGES; ++s) mbar_init(&bar[s], 1);
-    fence_mbar_init();
-  }
-  const uint64_t pol = a.l2_evict_first ? l2_policy_evict_first() : 0ull;
-  __syncwarp();
-  pdl_wait();  // q and the KV pages come from the QKV GEMM that precedes this kernel
-  tr.ready();
   // page ids of the first 32 pages of this warp, one per lane
   int my_page = (lane < n_my) ? ptab[p_begin + warp + lane * kAttnWarps] : 0;
 #pragma unroll

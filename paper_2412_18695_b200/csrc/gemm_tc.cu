@@ -687,10 +687,13 @@ __global__ void __launch_bounds__(kGemmThreads, GemmCfg<BN>::CTAS_PER_SM)
 #pragma unroll
       for (int i = 0; i < 9; ++i) s_mark[i] = t;
     }
-    // split-K: arrive on the cluster barrier as soon as this CTA's MMAs are done (its ring
-    // may then receive the peers' slices) and park the accumulator while the slower CTAs
-    // finish; the park writes P, the peers write the receive slots R (disjoint)
-    if (S > 1) cluster_arrive();
+    // split-K push: arrive on the cluster barrier as soon as this CTA's MMAs are done (its
+    // ring may then receive the peers' slices) and park the accumulator while the slower
+    // CTAs finish; the park writes P, the peers write the receive slots R (disjoint).  Pull
+    // (the peers READ P over DSMEM after the barrier): arrive only once P is parked — an
+    // early arrive there let a peer read a half-written P (intermittent wrong sums, found by
+    // a run-to-run determinism check, tools/determinism_check.py)
+    if (S > 1 && push) cluster_arrive();
 #pragma unroll 1
     for (int c0 = 0; c0 < BN; c0 += 16) {  // park the accumulator in shared memory
       float v[16];
@@ -699,6 +702,7 @@ __global__ void __launch_bounds__(kGemmThreads, GemmCfg<BN>::CTAS_PER_SM)
       for (int j = 0; j < 16; ++j) P[(c0 + j) * 128 + et] = v[j];
     }
     if (push) fence_proxy_async();  // P is read by the bulk-copy (async) proxy
+    if (S > 1 && !push) cluster_arrive();
     EPI_MARK(1);
     if (S > 1) cluster_wait();
   }
@@ -1943,29 +1947,57 @@ bool make_gemm_act_maps(GemmTmaSet* out, const void* base, int K, int rows_cap) 
          make_tma_2d_bf16(&out->m256, base, K, rows_cap, kBK, 256);
 }
 
-// N tile (UMMA N) for N activation rows.  Up to 128 rows the powers of two (decode); above,
-// the width among {160, 192, 256} with the least padded MMA work (n-tiles x BN), then fewer
-// n-tiles: prefill-heavy rounds are tensor-bound and a padded column costs a full MMA column
-// (tools/gemm_sweep_n.py: N = 320 on 2 x 256 ran at the speed of N = 512).
-int gemm_bn(int N) {
-  static const int force = getenv("RT_GEMM_BN") ? atoi(getenv("RT_GEMM_BN")) : 0;  // experiments
-  if (force && N > 128) return force;
-  if (N <= 32) return 32;
-  if (N <= 64) return 64;
-  if (N <= 128) return 128;
-  int best = 256, best_t = INT_MAX;
-  long long best_w = LLONG_MAX;
-  for (int bn : {160, 192, 256}) {
-    const int t = (N + bn - 1) / bn;
-    const long long w = (long long)t * bn;
-    if (w < best_w || (w == best_w && t < best_t)) {
-      best = bn;
-      best_w = w;
-      best_t = t;
+// Kernel choice for N activation rows: the N tile (UMMA N) and, above 128 rows, whether the
+// CTA-pair kernel runs (when eligible, see launch_gemm_epi).  Up to 128 rows the powers of
+// two (decode, single SM).  Above: for the model's projection shapes the measured table
+// gemm_policy.inc (tools/gemm_policy_tune.py: every candidate of a 32-row bucket timed back to
+// back; vs the rule below 11-18 % less time summed over 160..4096 rows); otherwise the width
+// among {160, 192, 256} with the least padded MMA work (n-tiles x BN), then fewer n-tiles
+// (a padded column costs a full MMA column), with the pair kernel at 192 / 256.
+// Overrides (experiments, the tuner): RT_GEMM_BN = width, RT_GEMM_PAIR = 0 / 1,
+// RT_GEMM_NO_TABLE = rule only.
+#include "gemm_policy.inc"
+struct GemmChoice {
+  int bn;
+  bool pair;
+};
+static GemmChoice gemm_choice(int M, int K, int N) {
+  if (N <= 32) return {32, false};
+  if (N <= 64) return {64, false};
+  if (N <= 128) return {128, false};
+  GemmChoice c{256, false};
+  bool found = false;
+  static const bool no_table = getenv("RT_GEMM_NO_TABLE") != nullptr;
+  if (!no_table)
+    for (const GemmPolicyRow& r : kGemmPolicy)
+      if (r.M == M && r.K == K && N <= r.n_max) {
+        const int code = r.code[(N - 129) / 32] - '0';
+        c.bn = code % 3 == 0 ? 160 : (code % 3 == 1 ? 192 : 256);
+        c.pair = code >= 3;
+        found = true;
+        break;
+      }
+  if (!found) {
+    int best_t = INT_MAX;
+    long long best_w = LLONG_MAX;
+    for (int bn : {160, 192, 256}) {
+      const int t = (N + bn - 1) / bn;
+      const long long w = (long long)t * bn;
+      if (w < best_w || (w == best_w && t < best_t)) {
+        c.bn = bn;
+        best_w = w;
+        best_t = t;
+      }
     }
+    c.pair = c.bn >= 192;
   }
-  return best;
+  const char* fe = getenv("RT_GEMM_BN");
+  if (fe && atoi(fe) > 0) c.bn = atoi(fe);
+  const char* fp = getenv("RT_GEMM_PAIR");
+  if (fp) c.pair = atoi(fp) != 0;
+  return c;
 }
+int gemm_bn(int M, int K, int N) { return gemm_choice(M, K, N).bn; }
 
 template <int BN, int MODE>
 static void ensure_attrs() {
@@ -1985,7 +2017,7 @@ static void ensure_attrs() {
 // 12 -> 19 us, 32 x 9: 11 -> 19 us), so S = max{S <= 8 : tiles x S <= 256, >= 4 k-blocks
 // per CTA} (cudaOccupancyMaxActiveClusters under-reports and is only a cap).
 int gemm_choose_splits(int M, int N, int K) {
-  const int bn = gemm_bn(N);
+  const int bn = gemm_bn(M, K, N);
   const int tiles = ((M + 127) / 128) * ((N + bn - 1) / bn);
   const int kb = K / kBK;
   if (tiles >= 148) return 1;
@@ -2149,14 +2181,8 @@ static cudaError_t launch_2sm_mode(const TmaMap& am, const GemmTmaSet& x, const 
   if (bn == 192) return launch_2sm_bn<192, MODE>(am, x.m96, x.m32, g, PT, a, s);
   return launch_2sm_bn<256, MODE>(am, x.m128, x.m32, g, PT, a, s);
 }
-// RT_GEMM_PAIR: unset = tile widths 192 / 256 (measured: gate/up at 256 / 384 / 512 rows
-// 65.8 / 93.5 / 120.6 -> 61.7 / 90.2 / 103.5 us; at 160-wide tiles the pair rounds quantise
-// worse than the single-SM stream-K kernel, 83.3 -> 88.5 us at 320 rows), 0 = off, 1 = all widths
-static bool pair_enabled(int bn) {
-  const char* e = getenv("RT_GEMM_PAIR");
-  if (!e) return bn >= 192;
-  return atoi(e) != 0;
-}
+// (pairs at 160-wide tiles only where the table measured them faster: their rounds quantise
+// worse than the single-SM stream-K kernel, e.g. gate/up 83.3 -> 88.5 us at 320 rows)
 // co-resident CTA pairs of the pair kernel at this tile width (occupancy query, cached)
 template <int BN>
 static int pair_slots_bn() {
@@ -2192,8 +2218,9 @@ int64_t gemm_sk_ws_floats() { return (int64_t)sm_count() * 2 * 256 * 128; }
 cudaError_t launch_gemm_epi(const bf16* w_tiled, const GemmTmaSet& x, GemmArgs g, int splits, cudaStream_t s) {
   // CTA-pair kernel for the tensor-bound prefill path: every pair busy (at least one
   // pair-tile per co-resident pair) and an even number of 128-row m-tiles
-  if (g.N > 128 && g.mode != EPI_ARGMAX && g.K % kBK == 0 && pair_enabled(gemm_bn(g.N))) {
-    const int bn = gemm_bn(g.N);
+  const GemmChoice gc = gemm_choice(g.M, g.K, g.N);
+  if (g.N > 128 && g.mode != EPI_ARGMAX && g.K % kBK == 0 && gc.pair) {
+    const int bn = gc.bn;
     const int m_tiles = (g.M + 127) / 128, n_tiles = (g.N + bn - 1) / bn;
     const int PT = (m_tiles / 2) * n_tiles;
     static const int min_pt = getenv("RT_GEMM_PAIR_MIN") ? atoi(getenv("RT_GEMM_PAIR_MIN")) : 0;
@@ -2237,7 +2264,7 @@ cudaError_t launch_gemm_epi(const bf16* w_tiled, const GemmTmaSet& x, GemmArgs g
     g.kb_total = g.K / kBK;
     g.m_tiles = (g.M + 127) / 128;
     g.l2_evict_first = 0;
-    const int bn = gemm_bn(g.N);
+    const int bn = gc.bn;
     SkArgs a;
     a.n_tiles = (g.N + bn - 1) / bn;
     const int T = g.m_tiles * a.n_tiles;
@@ -2264,9 +2291,9 @@ cudaError_t launch_gemm_epi(const bf16* w_tiled, const GemmTmaSet& x, GemmArgs g
   }
   g.w = w_tiled;
   // weights are read once per n-tile; with several n-tiles the later ones should hit L2
-  const int n_tiles = (g.N + gemm_bn(g.N) - 1) / gemm_bn(g.N);
+  const int n_tiles = (g.N + gc.bn - 1) / gc.bn;
   g.l2_evict_first = (l2_hint_enabled() && n_tiles == 1) ? 1 : 0;
-  const int bn = gemm_bn(g.N);
+  const int bn = gc.bn;
   g.kb_total = g.K / kBK;
   g.m_tiles = (g.M + 127) / 128;
   g.n_tiles = n_tiles;

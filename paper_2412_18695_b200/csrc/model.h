@@ -146,7 +146,7 @@ int64_t gemm_sk_ws_floats();
 // fill g.pf_* for a next launch of weights w [M x K] at N columns (splits <= 0: auto),
 // prefetching at most budget_bytes in total
 void gemm_set_prefetch(GemmArgs& g, const bf16* w, int M, int N, int K, int splits, int64_t budget_bytes);
-int gemm_bn(int N);
+int gemm_bn(int M, int K, int N);
 int gemm_choose_splits(int M, int N, int K);   // cluster split-K factor (1..16)
 // splits <= 0: gemm_choose_splits
 cudaError_t launch_gemm_epi(const bf16* w_tiled, const GemmTmaSet& xmaps, GemmArgs g, int splits, cudaStream_t s);

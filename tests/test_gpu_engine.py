@@ -686,10 +686,11 @@ def test_prefill_projections_hybrid_streamk_match_per_tile(rt, monkeypatch, prom
         eng.close()
     assert out["hybrid"][0][0] == 8 * prompt_len
     for other in ("hybrid", "pair"):
-        for (na, la), (nb, lb) in zip(out[other], out["per_tile"]):
+        for rnd, ((na, la), (nb, lb)) in enumerate(zip(out[other], out["per_tile"])):
             assert na == nb
             scale = max(1.0, float(np.abs(lb).max()))
-            assert float(np.abs(la - lb).max()) < 2e-2 * scale, other
+            err = float(np.abs(la - lb).max())
+            assert err < 2e-2 * scale, (other, rnd, err, scale, np.argwhere(np.abs(la - lb) > 2e-2 * scale)[:8])
 
 
 def test_set_timing_toggles_event_stats_only(rt):
@@ -724,3 +725,36 @@ def test_set_timing_toggles_event_stats_only(rt):
         eng.close()
     assert outs[0][0] == outs[1][0]
     assert all(np.array_equal(a, b) for a, b in zip(outs[0][1], outs[1][1]))
+
+
+@pytest.mark.parametrize("mode", ["hybrid", "per_tile", "pair"])
+def test_prefill_and_decode_rounds_bitwise_deterministic(rt, monkeypatch, mode):
+    """Run-to-run determinism of every projection path (the cluster split-K in pull mode once
+    let a peer read a half-parked partial tile: logits differed by up to 0.19 between identical
+    runs; tools/determinism_check.py): the same scripted rounds twice give bit-identical
+    logits."""
+    from synth.configs import ModelShape
+    from synth.traces import make_trace
+    s8 = MODEL_SHAPES["llama3-8b"]
+    shape = ModelShape("det", 2, s8.d_model, s8.n_q_heads, s8.n_kv_heads, s8.head_dim, s8.d_ff, s8.vocab)
+    v = make_vocab(shape.vocab)
+    p = engine_params("b200-roofline", max_batch=8, max_tasks=16, max_ctx=512, n_pages=8 * 32)
+    monkeypatch.setenv("RT_GEMM_PAIR", "1" if mode == "pair" else "0")
+    if mode == "per_tile":
+        monkeypatch.setenv("RT_NO_STREAMK", "1")
+    else:
+        monkeypatch.delenv("RT_NO_STREAMK", raising=False)
+    runs = []
+    for _ in range(2):
+        eng = rt.Engine(shape, p, v, seed=23, flags=rt.RT_FLAG_KEEP_LOGITS, max_rows_per_forward=4096)
+        for a in range(8):
+            tr = make_trace(1 + a, v, seed=a, prompt_len=64, plan_len=12)
+            eng.submit(a, tr.prompt, 0, tr.ert_us, tr.alpha, tr.beta, 90000, script=tr.plan)
+        logs = []
+        for _ in range(4):
+            B = eng.step()["n_running"]
+            logs.append(eng.dump(rt.RT_DUMP_LOGITS, np.float32).reshape(B, -1).copy())
+        eng.close()
+        runs.append(logs)
+    for a, b in zip(*runs):
+        assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
