@@ -270,16 +270,24 @@ __global__ void __launch_bounds__(kAttnWarps * 32) k_attn(AttnArgs a) {
 //    blocks, one cp.async.bulk each, full / empty mbarriers (G consumer warps);
 //  * S = Q K^T and O += P V on m16n8k16 (bf16 in, fp32 acc), online softmax in fp32 with
 //    exp2, causal mask on the diagonal page only; longest tiles are scheduled first.
-template <int HD>
+//  * few CTAs (light prefill rounds, G <= 4): two warp groups per CTA (8 warps); group j
+//    takes the pages i = j mod 2 with its own online-softmax state, merged in shared memory
+//    at the end (fixed order) — twice the warps per SM for this mma.sync-latency-bound loop
+//    without a global merge.  Measured (tools/prefill_tail_bench.py, 84-token tails on a
+//    1216-token prefix, 6 tiles x 8 kv heads per request): 1 / 2 / 3 requests (48 / 96 / 144
+//    CTAs) 52.4 / 52.9 / 53.3 -> 36.7 / 37.4 / 38.0 us per layer; from 4 requests (192 CTAs,
+//    more than one per SM) two groups lose (64.2 -> 71.2 us): one group there.
+template <int HD, int NG>
 struct PfCfg {
   static constexpr int BLOCK = 64 * HD;
-  static constexpr int STAGES = 4;
+  static constexpr int STAGES = 4 * NG;  // page i + STAGES belongs to the same warp group
   static constexpr int SMEM = STAGES * BLOCK + 2 * STAGES * 8 + 64;
+  static_assert(NG == 1 || 4 * 32 * (HD / 2 + 4) * 4 <= STAGES * BLOCK, "group merge fits in the ring");
 };
 
-template <int HD>
+template <int HD, int NG>
 __global__ void __launch_bounds__(256) k_attn_prefill(PrefillArgs a) {
-  using C = PfCfg<HD>;
+  using C = PfCfg<HD, NG>;
   using SW = KvSwz<HD>;
   extern __shared__ __align__(1024) unsigned char smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::BLOCK);
@@ -292,11 +300,12 @@ __global__ void __launch_bounds__(256) k_attn_prefill(PrefillArgs a) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gq = lane >> 2, qq = lane & 3;
   const int G = a.G;
+  const int grp = warp / G, wg = warp - grp * G;  // warp group, q head within the kv head
   const int h = blockIdx.y;
   if (threadIdx.x == 0) {
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], G);
+      mbar_init(&empty[s], G);  // one warp group consumes a page
     }
     fence_mbar_init();
   }
@@ -330,7 +339,7 @@ __global__ void __launch_bounds__(256) k_attn_prefill(PrefillArgs a) {
     }
 
   // q fragments (A operand, rows = the tile's positions), rows outside the chunk are zero
-  const int qh = h * G + warp;
+  const int qh = h * G + wg;
   uint32_t qa[HD / 16][4];
   {
     const int r0 = rb + gq, r1 = rb + gq + 8;
@@ -356,7 +365,7 @@ __global__ void __launch_bounds__(256) k_attn_prefill(PrefillArgs a) {
   const int lcsel = mi & 1;
   const int qp0 = T.z + gq, qp1 = T.z + gq + 8;  // positions of this lane's two rows
 
-  for (int i = 0; i < np; ++i) {
+  for (int i = grp; i < np; i += NG) {
     const int s = i % C::STAGES;
     mbar_wait(&full[s], (uint32_t)((i / C::STAGES) & 1));
     const uint32_t kbase = smem_u32(smem + s * C::BLOCK);
@@ -424,8 +433,8 @@ __global__ void __launch_bounds__(256) k_attn_prefill(PrefillArgs a) {
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
-    // refill stage s with page i + STAGES once every warp released it
-    if (threadIdx.x == 0 && i + C::STAGES < np) {
+    // refill stage s with page i + STAGES (same group) once every warp of the group released it
+    if (wg == 0 && lane == 0 && i + C::STAGES < np) {
       mbar_wait(&empty[s], (uint32_t)((i / C::STAGES) & 1));
       fence_proxy_async();
       mbar_arrive_expect_tx(&full[s], C::BLOCK);
@@ -437,21 +446,56 @@ __global__ void __launch_bounds__(256) k_attn_prefill(PrefillArgs a) {
   l0 += __shfl_xor_sync(0xffffffffu, l0, 2);
   l1 += __shfl_xor_sync(0xffffffffu, l1, 1);
   l1 += __shfl_xor_sync(0xffffffffu, l1, 2);
+  if constexpr (NG == 2) {  // group 1's state -> shared memory (the ring is idle), group 0 merges
+    __syncthreads();
+    float* xs = reinterpret_cast<float*>(smem) + (size_t)(wg * 32 + lane) * (HD / 2 + 4);
+    if (grp == 1) {
+#pragma unroll
+      for (int nt = 0; nt < HD / 8; ++nt)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) xs[nt * 4 + j] = o[nt][j];
+      xs[HD / 2] = m0;
+      xs[HD / 2 + 1] = m1;
+      xs[HD / 2 + 2] = l0;
+      xs[HD / 2 + 3] = l1;
+    }
+    __syncthreads();
+    if (grp == 0) {
+      const float pm0 = xs[HD / 2], pm1 = xs[HD / 2 + 1];
+      const float M0 = fmaxf(m0, pm0), M1 = fmaxf(m1, pm1);
+      const float fa0 = exp2f(m0 - M0), fa1 = exp2f(m1 - M1);
+      const float fb0 = pm0 == -INFINITY ? 0.f : exp2f(pm0 - M0);
+      const float fb1 = pm1 == -INFINITY ? 0.f : exp2f(pm1 - M1);
+      l0 = l0 * fa0 + xs[HD / 2 + 2] * fb0;
+      l1 = l1 * fa1 + xs[HD / 2 + 3] * fb1;
+#pragma unroll
+      for (int nt = 0; nt < HD / 8; ++nt) {
+        o[nt][0] = o[nt][0] * fa0 + xs[nt * 4 + 0] * fb0;
+        o[nt][1] = o[nt][1] * fa0 + xs[nt * 4 + 1] * fb0;
+        o[nt][2] = o[nt][2] * fa1 + xs[nt * 4 + 2] * fb1;
+        o[nt][3] = o[nt][3] * fa1 + xs[nt * 4 + 3] * fb1;
+      }
+      m0 = M0;
+      m1 = M1;
+    }
+  }
+  const bool active = grp == 0;  // group 0 holds the merged state of its q head
   if (NC > 1) {
     // ---- split-KV: park (o unnormalised, m, l) of this chunk; the last chunk of the
     // (tile, head) merges all chunks in chunk order (deterministic)
     const int RW = HD + 2;
     float* wsb = a.ws + (((size_t)tix * a.nkv + h) * NC) * (size_t)(G * 16 * RW);
-    float* mine = wsb + ((size_t)chunk * G + warp) * (16 * RW);
+    float* mine = wsb + ((size_t)chunk * G + wg) * (16 * RW);
 #pragma unroll
     for (int nt = 0; nt < HD / 8; ++nt) {
       const int d = nt * 8 + 2 * qq;
+      if (!active) break;
       mine[gq * RW + d] = o[nt][0];
       mine[gq * RW + d + 1] = o[nt][1];
       mine[(gq + 8) * RW + d] = o[nt][2];
       mine[(gq + 8) * RW + d + 1] = o[nt][3];
     }
-    if (qq == 0) {
+    if (active && qq == 0) {
       mine[gq * RW + HD] = m0;
       mine[gq * RW + HD + 1] = l0;
       mine[(gq + 8) * RW + HD] = m1;
@@ -467,12 +511,12 @@ __global__ void __launch_bounds__(256) k_attn_prefill(PrefillArgs a) {
       if (s_last) *tk = 0;  // self-reset for the next launch
     }
     __syncthreads();
-    if (!s_last) return;
+    if (!s_last || !active) return;
     __threadfence();
     // merge: M = max m_c, L = sum l_c 2^(m_c - M), O = sum o_c 2^(m_c - M)
     float M0 = -INFINITY, M1 = -INFINITY;
     for (int c = 0; c < NC; ++c) {
-      const float* pc = wsb + ((size_t)c * G + warp) * (16 * RW);
+      const float* pc = wsb + ((size_t)c * G + wg) * (16 * RW);
       M0 = fmaxf(M0, __ldcg(pc + gq * RW + HD));
       M1 = fmaxf(M1, __ldcg(pc + (gq + 8) * RW + HD));
     }
@@ -480,7 +524,7 @@ __global__ void __launch_bounds__(256) k_attn_prefill(PrefillArgs a) {
 #pragma unroll
     for (int nt = 0; nt < HD / 8; ++nt) o[nt][0] = o[nt][1] = o[nt][2] = o[nt][3] = 0.f;
     for (int c = 0; c < NC; ++c) {
-      const float* pc = wsb + ((size_t)c * G + warp) * (16 * RW);
+      const float* pc = wsb + ((size_t)c * G + wg) * (16 * RW);
       const float mc0 = __ldcg(pc + gq * RW + HD), mc1 = __ldcg(pc + (gq + 8) * RW + HD);
       const float f0 = (mc0 == -INFINITY) ? 0.f : exp2f(mc0 - M0);
       const float f1 = (mc1 == -INFINITY) ? 0.f : exp2f(mc1 - M1);
@@ -499,6 +543,7 @@ __global__ void __launch_bounds__(256) k_attn_prefill(PrefillArgs a) {
     l1 = L1;
   }
   // ---- normalise and store rows gq, gq + 8 (dims 8 nt + 2 qq, +1)
+  if (!active) return;
   const float i0 = 1.f / l0, i1 = 1.f / l1;
 #pragma unroll
   for (int hf = 0; hf < 2; ++hf) {
@@ -581,21 +626,40 @@ void launch_attention(const AttnArgs& a0, cudaStream_t s) {
   }
 }
 
-template <int HD>
-static void launch_prefill_hd(const PrefillArgs& a, cudaStream_t s) {
-  using C = PfCfg<HD>;
+template <int HD, int NG>
+static void launch_prefill_ng(const PrefillArgs& a, cudaStream_t s) {
+  using C = PfCfg<HD, NG>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_attn_prefill<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaFuncSetAttribute(k_attn_prefill<HD, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
     attr = true;
   }
   // plain stream-ordered launch (no programmatic dependent launch): measured faster for this
   // latency-bound kernel (tools/prefill_tail_bench.py, RT_PF_PDL=1 to compare)
   static const bool pdl = getenv("RT_PF_PDL") != nullptr;
+  const dim3 grid(a.n_tiles, a.nkv, a.chunks), block(32 * a.G * NG);
   if (pdl)
-    launch_pdl(k_attn_prefill<HD>, dim3(a.n_tiles, a.nkv, a.chunks), dim3(32 * a.G), C::SMEM, s, a);
+    launch_pdl(k_attn_prefill<HD, NG>, grid, block, C::SMEM, s, a);
   else
-    k_attn_prefill<HD><<<dim3(a.n_tiles, a.nkv, a.chunks), dim3(32 * a.G), C::SMEM, s>>>(a);
+    k_attn_prefill<HD, NG><<<grid, block, C::SMEM, s>>>(a);
+}
+template <int HD>
+static void launch_prefill_hd(const PrefillArgs& a, cudaStream_t s) {
+  // two warp groups while there is at most one CTA per SM (RT_PF_GROUPS=1/2 forces)
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    if (sms <= 0) sms = 148;
+  }
+  static const int forced = getenv("RT_PF_GROUPS") ? atoi(getenv("RT_PF_GROUPS")) : 0;
+  const long long ctas = (long long)a.n_tiles * a.nkv * a.chunks;
+  const int ng = a.G > 4 ? 1 : (forced ? forced : (ctas <= sms ? 2 : 1));
+  if (ng == 2)
+    launch_prefill_ng<HD, 2>(a, s);
+  else
+    launch_prefill_ng<HD, 1>(a, s);
 }
 
 // Split-KV plan of the prefill attention: C page chunks per (tile, kv head), merged by the

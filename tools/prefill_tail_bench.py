@@ -49,5 +49,5 @@ def main(R=4, reps=5):
 
 
 if __name__ == "__main__":
-    for R in (1, 4, 8):
+    for R in ([int(x) for x in sys.argv[1].split(",")] if len(sys.argv) > 1 else (1, 4, 8)):
         main(R)
