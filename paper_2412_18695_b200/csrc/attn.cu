@@ -57,14 +57,15 @@ __global__ void __launch_bounds__(kAttnWarps * 32) k_attn(AttnArgs a) {
     fence_mbar_init();
   }
   const uint64_t pol = a.l2_evict_first ? l2_policy_evict_first() : 0ull;
-  __syncwarp();
-  // Everything below reads this round's row metadata, page tables, q and KV pages: only after
-  // the dependency wait.  (The row metadata comes from the scheduler kernel at the start of
-  // the round; with programmatic dependent launch a chain of early-launched kernels can reach
-  // this kernel before the scheduler has finished, so even it is not safe to read earlier —
-  // the first layer's attention read stale rows intermittently when it was.)
-  pdl_wait();
-  tr.ready();
+  // The round's row metadata (rows, lengths, tasks; written by the scheduler kernel at the
+  // start of the round) is read BEFORE the dependency wait, overlapping the QKV projection's
+  // tail.  Safe by construction: the kernel this one depends on is always a QKV projection
+  // (k_gemm_tc / k_gemm_sk / k_gemm_2sm in EPI_QKV, or the chain whose last job is QKV), and
+  // those trigger their dependents only AFTER their own griddepcontrol.wait — so when this
+  // code runs, every kernel before the QKV projection, the scheduler included, has completed.
+  // (With the trigger at the QKV kernel's start, a chain of early launches could reach here
+  // while the scheduler was still writing: found as an intermittent stale read.)  q and the
+  // new KV entries come from the QKV projection itself: page ids, q and pages after the wait.
   const int row = a.row_list ? a.row_list[blockIdx.z] : a.row0 + (int)blockIdx.z;
   const int r = row - a.row0;  // row within this forward chunk
   if (a.row_list && (r < 0 || r >= a.chunk_rows)) return;
@@ -78,6 +79,9 @@ __global__ void __launch_bounds__(kAttnWarps * 32) k_attn(AttnArgs a) {
   const int32_t* ptab = a.page_table + (size_t)task * a.pt_stride;
   // pages of this warp: p_begin + warp + i * NW
   const int n_my = p_end - (p_begin + warp) > 0 ? (p_end - (p_begin + warp) + kAttnWarps - 1) / kAttnWarps : 0;
+  __syncwarp();
+  pdl_wait();
+  tr.ready();
   // page ids of the first 32 pages of this warp, one per lane
   int my_page = (lane < n_my) ? ptab[p_begin + warp + lane * kAttnWarps] : 0;
 #pragma unroll

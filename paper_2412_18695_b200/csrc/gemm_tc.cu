@@ -611,7 +611,10 @@ __global__ void __launch_bounds__(kGemmThreads, GemmCfg<BN>::CTAS_PER_SM)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  if (threadIdx.x == 0) pdl_trigger();
+  // EPI_QKV: dependents (the decode attention) may launch only once this kernel has passed
+  // its own dependency wait — the attention reads the round's row metadata before its wait,
+  // which is safe only if every kernel before it has completed (PDL)
+  if (MODE != EPI_QKV && threadIdx.x == 0) pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -626,6 +629,7 @@ __global__ void __launch_bounds__(kGemmThreads, GemmCfg<BN>::CTAS_PER_SM)
         bulk_g2s_hint(sA + i * C::A_BYTES, wt + (size_t)i * (128 * kBK), C::A_BYTES, &full[i], pol);
       }
       pdl_wait();
+      if (MODE == EPI_QKV) pdl_trigger();
       tr.ready();
       for (int i = 0; i < pre_k; ++i)
         tma_load_2d(sB + i * C::B_BYTES, &tmB, (kb0 + i) * kBK, n0, &full[i]);
@@ -937,7 +941,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_chain(const __grid_constant
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  if (threadIdx.x == 0) pdl_trigger();
+  // (dependents are triggered after the dependency wait: the chain's last job is a QKV)
 
   if (warp == 0) {
     if (lane == 0) {
@@ -980,6 +984,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_chain(const __grid_constant
               // ring holds as many weight k-blocks as it can
               if (!prog || cw.j >= a.n_jobs) {
                 pdl_wait();
+                pdl_trigger();
                 tr.ready();
                 waited = true;
                 dep_job = 0;
@@ -1002,6 +1007,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_chain(const __grid_constant
         if (!prog) __nanosleep(32);
       }
       if (!waited) pdl_wait();
+      if (!waited) pdl_trigger();
       trace_phase(TK_PHASE | TK_CHAIN | (1u << 8), t_dep[0], t_dep[1], t_dep[2], t_dep[3]);
     }
     __syncwarp();
@@ -1365,7 +1371,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  if (threadIdx.x == 0) pdl_trigger();
+  if (MODE != EPI_QKV && threadIdx.x == 0) pdl_trigger();  // EPI_QKV: after the wait (k_gemm_tc)
 
   if (warp == 0) {
     if (lane == 0) {
@@ -1381,13 +1387,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           bulk_g2s(sA + st * A_BYTES, g.w + ((size_t)m_tile * kbt + kb) * (128 * kBK), A_BYTES, &full[st]);
           if (!waited) {  // weights before the previous kernel finishes, activations after
             pdl_wait();
+            if (MODE == EPI_QKV) pdl_trigger();
             tr.ready();
             waited = true;
           }
           tma_load_2d(sB + st * C::B_BYTES, &tmB, kb * kBK, n_tile * BN, &full[st]);
         }
       }
-      if (!waited) pdl_wait();
+      if (!waited) {
+        pdl_wait();
+        if (MODE == EPI_QKV) pdl_trigger();
+      }
     }
     __syncwarp();
   } else if (warp == 1) {
@@ -1717,7 +1727,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   cluster_wait();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  if (threadIdx.x == 0) pdl_trigger();
+  if (MODE != EPI_QKV && threadIdx.x == 0) pdl_trigger();  // EPI_QKV: after the wait (k_gemm_tc)
 
   if (warp == 0) {
     if (lane == 0) {
@@ -1739,13 +1749,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           tma_load_2d_pair(sA + st * C::A_BYTES, &tmA, 0, (m_tile * kbt + kb) * 128, full0 + st * 8);
           if (!waited) {  // weights before the previous kernel finishes, activations after
             pdl_wait();
+            if (MODE == EPI_QKV) pdl_trigger();
             tr.ready();
             waited = true;
           }
           tma_load_2d_pair(sB + st * C::B_BYTES, sub ? &tmBs : &tmB, kb * kBK, brow, full0 + st * 8);
         }
       }
-      if (!waited) pdl_wait();
+      if (!waited) {
+        pdl_wait();
+        if (MODE == EPI_QKV) pdl_trigger();
+      }
     }
     __syncwarp();
   } else if (warp == 1) {
