@@ -44,6 +44,7 @@
 #include "common.cuh"
 #include "model.h"
 #include <map>
+#include <mutex>
 #include <utility>
 
 namespace rt {
@@ -2132,7 +2133,9 @@ static cudaError_t launch_sk_mode(const GemmTmaSet& x, const GemmArgs& g, const 
 // weight operand of the pair kernel: the pre-tiled image read as rows of 64 bf16 (128 B), one
 // 16 KB box per (m-tile, k-block); the map depends only on (pointer, rows): cached
 static const TmaMap* weight_map(const bf16* w, uint64_t rows) {
-  static std::map<std::pair<const void*, uint64_t>, TmaMap> cache;
+  static std::map<std::pair<const void*, uint64_t>, TmaMap> cache;  // node-based: pointers stay valid
+  static std::mutex mu;  // engines may run on different host threads
+  std::lock_guard<std::mutex> lock(mu);
   const auto key = std::make_pair((const void*)w, rows);
   auto it = cache.find(key);
   if (it != cache.end()) return &it->second;

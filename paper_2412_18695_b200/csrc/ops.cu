@@ -1,5 +1,6 @@
 // ops.cu — op-level C ABI (include/rt_ops.h): the hot-path kernels on caller-owned
 // device buffers, for per-op parity tests and microbenchmarks.
+#include <mutex>
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdlib.h>
@@ -132,6 +133,8 @@ extern "C" rt_status rt_op_gemm_tiled(const void* d_w_tiled, const void* d_x, fl
   static float* sk_ws = nullptr;
   static unsigned* sk_cnt = nullptr;
   static int sk_cap = 0;
+  static std::mutex sk_mu;  // callers on several host threads share the workspace allocation
+  std::lock_guard<std::mutex> lock(sk_mu);
   const int need = ((M + 127) / 128) * ((N + 159) / 160);
   if (N > 128 && splits <= 0 && getenv("RT_NO_STREAMK") == nullptr) {
     if (!sk_ws && cudaMalloc(&sk_ws, (size_t)gemm_sk_ws_floats() * 4) != cudaSuccess) return RT_E_CUDA;
