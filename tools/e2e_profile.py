@@ -62,12 +62,12 @@ def main(rounds=200, trace=False):
         info = eng.step(now())
         eng.sync()
         wall = (time.perf_counter() - t0) * 1e3
-        st = eng.stats()   # includes the PREVIOUS round's CUDA-event timing (harvested in rt_step)
+        st = eng.stats()   # cumulative; this round's CUDA-event timing was harvested by rt_sync
         rec.append([info["n_rows"], info["n_prefill_rows"], info["n_running"], wall,
                     st["step_ms"], st["gemm_ms"], st["attn_ms"]])
     a = np.array(rec, dtype=np.float64)
-    a[:-1, 4:7] = a[1:, 4:7] - a[:-1, 4:7]   # round r's device times = stats after r+1 - after r
-    a = a[20:-1]
+    a[1:, 4:7] = a[1:, 4:7] - a[:-1, 4:7]   # round r's device times = stats after r - after r-1
+    a = a[20:]
     print(f"rounds {len(a)}: mean rows {a[:, 0].mean():.0f} (prompt {a[:, 1].mean():.0f}), tokens/round "
           f"{a[:, 2].mean():.1f}, wall {a[:, 3].mean():.2f} ms, device {a[:, 4].mean():.2f} ms "
           f"(forward {a[:, 5].mean():.2f}, attention {a[:, 6].mean():.2f}) -> {a[:, 2].sum() / a[:, 3].sum() * 1e3:.0f} tok/s")
