@@ -650,15 +650,16 @@ def test_sched_parity_stop_grammars(rt, grammar):
     assert sum(1 for s in segs if s["reason"] == 3) > 20
 
 
-@pytest.mark.parametrize("prompt_len", [200, 64, 160])
-def test_prefill_projections_hybrid_streamk_match_per_tile(rt, monkeypatch, prompt_len):
+@pytest.mark.parametrize("prompt_len,pair_bn", [(200, 0), (64, 0), (160, 0), (96, 192)])
+def test_prefill_projections_hybrid_streamk_match_per_tile(rt, monkeypatch, prompt_len, pair_bn):
     """The hybrid data-parallel + stream-K prefill projections (k_gemm_sk: > 2 waves of
     tiles, here gate/up and QKV of a 1600-row prefill at 8B dims) against one tile per CTA
     (RT_NO_STREAMK=1): same scripted rounds, the logits of the prefill round (token 0 of every
     request) and of later decode rounds agree to fp32 summation-order level.  "pair" runs the
     CTA-pair kernel (cta_group::2) for every eligible projection; 512 prompt rows put gate/up's
     partial last round into 64-column sub-tiles (SwiGLU epilogue), 1280 rows the O and down
-    projections' (residual epilogue), 1600 rows the 160-wide pair tiles."""
+    projections' (residual epilogue), 1600 rows the 160-wide pair tiles; 768 rows with 192-wide
+    pair tiles forced (RT_GEMM_BN) the QKV projection's (RoPE + KV-append epilogue)."""
     from synth.configs import ModelShape
     s8 = MODEL_SHAPES["llama3-8b"]
     shape = ModelShape("sk", 2, s8.d_model, s8.n_q_heads, s8.n_kv_heads, s8.head_dim, s8.d_ff, s8.vocab)
@@ -673,6 +674,10 @@ def test_prefill_projections_hybrid_streamk_match_per_tile(rt, monkeypatch, prom
             monkeypatch.delenv("RT_NO_STREAMK", raising=False)
         # CTA-pair kernel (cta_group::2) for every eligible projection, or single-SM kernels only
         monkeypatch.setenv("RT_GEMM_PAIR", "1" if mode == "pair" else "0")
+        if mode == "pair" and pair_bn:
+            monkeypatch.setenv("RT_GEMM_BN", str(pair_bn))
+        else:
+            monkeypatch.delenv("RT_GEMM_BN", raising=False)
         eng = rt.Engine(shape, p, v, seed=23, flags=rt.RT_FLAG_KEEP_LOGITS, max_rows_per_forward=4096)
         for a in range(8):
             tr = make_trace(1 + a, v, seed=a, prompt_len=prompt_len, plan_len=12)
