@@ -277,11 +277,7 @@ def run_ours(args, rank, world, dist):
             "metric": "decode tok/s (segmented decode round, C2 drone agents)", "value": value, "unit": "tok/s",
             "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": ms / K, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": "C2: 64 drone agents per GPU, llama3-8b-shape random-init bf16, "
-                                   "contexts resident (prompt 1300 prefilled in setup), scripted drone plans",
-                       "model": "llama3-8b-shape", "global_batch": B * world, "ctx": PROMPT,
-                       "parallelism": f"replicas x{world} (agent partition, 1 allgather/round)",
-                       "l2": "inputs > L2 (16 GB weights + 11 GB KV per step)"},
+            "config": c2_config(world),
             "segments_per_s": seg_per_s, "roofline": roofline, "step_roofline": step_roof,
             "cpu_baseline": cpu, "e2e": e2e, "e2e_private_prompts": e2e_private,
             "gpu_launches": int(round(launches_per_step * K)),
@@ -465,6 +461,15 @@ def oracle_extra_timings(args):
     return out
 
 
+def c2_config(world):
+    """The workload both arms report (BASELINE configs[1])."""
+    return {"workload": "C2: 64 drone agents per GPU, llama3-8b-shape random-init bf16, "
+                        "contexts resident (prompt 1300 prefilled in setup), scripted drone plans",
+            "model": "llama3-8b-shape", "global_batch": AGENTS_PER_GPU * world, "ctx": PROMPT,
+            "parallelism": f"replicas x{world} (agent partition, 1 allgather/round)",
+            "l2": "inputs > L2 (16 GB weights + 11 GB KV per step)"}
+
+
 def run_reference(args, rank, world):
     """--impl reference: the CPU oracle as it stands, bounded sample per step."""
     if rank != 0:
@@ -484,11 +489,10 @@ def run_reference(args, rank, world):
             "unit": "tok/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64 (bf16 points)", "data": "synthetic",
-            "config": {"workload": "C2 sample: one decode step of 8 drone rows at ctx 1300, llama3-8b shape, "
-                                   "one layer per timed step extrapolated x32 (weights generated in warmup)",
-                       "model": "llama3-8b-shape"},
+            "config": c2_config(world),
             "cpu_baseline": {"value": v, "unit": "tok/s", "cores": cores, "kind": "oracle",
-                             "sample": "8 rows x 1 layer per timed step, extrapolated x32 layers"},
+                             "sample": "per timed step one C2 decode step of 8 of the drone rows at ctx 1300, "
+                                       "1 of 32 layers (weights generated in warmup), extrapolated x32 layers"},
             "e2e": {"value": v, "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
