@@ -68,9 +68,14 @@ enum {
   RT_FLAG_CAPTURE = 4,      /* keep q / attention output (fp32) of layer capture_layer */
   RT_FLAG_TIMING = 8,       /* CUDA-event timing of attention / GEMM launches (rt_stats) */
   RT_FLAG_FORCE_EXCHANGE = 16, /* run the per-round NCCL allgather + merge even when world == 1 */
-  RT_FLAG_GRAPHS = 32,         /* replay decode-only forwards from CUDA graphs keyed by batch size */
   RT_FLAG_TRACE = 64           /* per-CTA %globaltimer records of every kernel (RT_DUMP_TRACE) */
 };
+/* Projection kernel path (rt_config.gemm_path, rt_op_gemm_tiled): AUTO = the measured dispatch
+ * (DESIGN.md §6); the others force one kernel wherever it applies, for parity tests:
+ *   RT_GEMM_PATH_SPLITK   k_gemm_tc: one 128-row tile per CTA, cluster split-K
+ *   RT_GEMM_PATH_STREAMK  k_gemm_sk: hybrid data-parallel + stream-K (N > 128 rows)
+ *   RT_GEMM_PATH_PAIR     k_gemm_2sm: CTA pairs, tcgen05.mma.cta_group::2 (N > 128 rows) */
+enum { RT_GEMM_PATH_AUTO = 0, RT_GEMM_PATH_SPLITK = 1, RT_GEMM_PATH_STREAMK = 2, RT_GEMM_PATH_PAIR = 3 };
 
 typedef struct rt_engine rt_engine;
 
@@ -79,7 +84,10 @@ typedef struct rt_engine rt_engine;
 typedef struct { double alpha, beta; } rt_utility;
 
 typedef struct {
-  /* replicas (BASELINE.json: agents partitioned over GPUs, one allgather per round) */
+  /* replicas (BASELINE.json: agents partitioned over GPUs, one allgather per round):
+   * 1 <= world <= 8 (one node).  With world > 1 every rt_step call is a collective (one
+   * ncclAllGather of the round's candidates, idle rounds included): every rank must call
+   * rt_step the same number of times. */
   int32_t rank, world;
   const uint8_t* nccl_id;           /* 128-byte ncclUniqueId (host); NULL when world == 1 */
   int32_t device;                   /* CUDA device ordinal */
@@ -137,6 +145,7 @@ typedef struct {
   const int32_t* skill_base_us;
   const int32_t* skill_unit_us;
   int32_t word_us;
+  int32_t gemm_path;                /* RT_GEMM_PATH_* (0: measured dispatch) */
 } rt_config;
 
 typedef struct {

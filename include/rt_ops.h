@@ -64,10 +64,12 @@ rt_status rt_op_gemm(const void* d_w, const void* d_x, float* d_out, int32_t M, 
 
 /* The engine's weight layout: pack a row-major bf16 [M][K] matrix into
  * UMMA-ready 128 x 64 tiles (d_dst holds ceil(M/128)*128*K elements), and run the
- * projection directly on a packed matrix (same semantics as rt_op_gemm). */
+ * projection directly on a packed matrix (same semantics as rt_op_gemm).  path = RT_GEMM_PATH_*
+ * (AUTO: the engine's dispatch; a forced path falls back to SPLITK where it does not apply),
+ * bn = N tile width (0: by the dispatch; 32 / 64 / 128 / 160 / 192 / 256). */
 rt_status rt_op_pack_tiled(const void* d_src, void* d_dst, int32_t M, int32_t K, void* stream);
 rt_status rt_op_gemm_tiled(const void* d_w_tiled, const void* d_x, float* d_out, int32_t M, int32_t N,
-                           int32_t K, int32_t n_cap, int32_t splits, void* stream);
+                           int32_t K, int32_t n_cap, int32_t splits, int32_t path, int32_t bn, void* stream);
 
 /* a8 lm_head + greedy argmax (lowest index on ties) over the vocabulary:
  * d_tok[n] = argmax_m sum_k W[m,k] X[n,k]; d_logits (nullable) fp32 [N][M]. */
@@ -84,6 +86,14 @@ rt_status rt_op_init_weights(void* d_out, int64_t n, uint64_t seed, int32_t tens
 rt_status rt_op_priority(const int64_t* d_t_ref_d_ert /* [n][4]: t, ref, D, ERT */,
                          const int32_t* d_k, const double* d_alpha, const double* d_beta, int32_t n,
                          int32_t g_us, int32_t net_us, int32_t eps_l_us, double* d_pri, void* stream);
+
+/* a12 global ordering across replicas (BASELINE.json "one NCCL allgather ... per scheduling
+ * round so the global utility ordering stays exact"; DESIGN.md AMB-22): the device merge the
+ * engine runs on the allgathered candidates.  d_all fp64 [world][16][4] = per-rank top-16
+ * candidate records (pri, arrival_us, global request id, rank), rid < 0 = empty slot;
+ * d_merged fp64 [16][4] receives the top 16 of the union by (pri desc, arrival asc, rid asc),
+ * empty slots last.  1 <= world <= 8. */
+rt_status rt_op_merge_candidates(const double* d_all, int32_t world, double* d_merged, void* stream);
 
 #ifdef __cplusplus
 }

@@ -321,17 +321,13 @@ __global__ void __launch_bounds__(256) k_attn_prefill(PrefillArgs a) {
   const int rb = T.x, re = T.x + T.y;
   if (max(rb, a.row0) >= min(re, a.row0 + a.n_rows)) return;  // not in this forward chunk
   const int npt = (T.z >> 4) + 1;                               // pages 0 .. pos0 / 16
-  // split-KV: chunk c of C covers pages [pb, pe) (the diagonal page is in the last chunk)
-  const int NC = a.chunks, chunk = blockIdx.z;
-  const int cpp = (npt + NC - 1) / NC;
-  const int pb = min(npt, chunk * cpp), pe = min(npt, pb + cpp);
-  const int np = pe - pb;
+  const int np = npt;
   // The CTAs of a round that prefill the tails of prompts sharing a long prefix all read the
   // same prefix pages; walking them in the same order makes every CTA hit the same L2 lines
   // at the same time.  Each CTA starts its walk at its own page (softmax is order-free; the
-  // diagonal page keeps its causal mask wherever it falls).  RT_PF_NO_ROTATE=1: in order.
-  const int rot = (a.rotate && np > 0) ? (int)(((unsigned)tix * 7u + (unsigned)h * 13u) % (unsigned)np) : 0;
-  auto page_at = [&](int i) { return pb + (i + rot >= np ? i + rot - np : i + rot); };
+  // diagonal page keeps its causal mask wherever it falls).
+  const int rot = np > 0 ? (int)(((unsigned)tix * 7u + (unsigned)h * 13u) % (unsigned)np) : 0;
+  auto page_at = [&](int i) { return i + rot >= np ? i + rot - np : i + rot; };
   const int32_t* ptab = a.page_table + (size_t)T.w * a.pt_stride;
   const unsigned char* pool = (const unsigned char*)a.pool;
   const size_t head_off = (size_t)h * C::BLOCK;
@@ -484,68 +480,6 @@ __global__ void __launch_bounds__(256) k_attn_prefill(PrefillArgs a) {
     }
   }
   const bool active = grp == 0;  // group 0 holds the merged state of its q head
-  if (NC > 1) {
-    // ---- split-KV: park (o unnormalised, m, l) of this chunk; the last chunk of the
-    // (tile, head) merges all chunks in chunk order (deterministic)
-    const int RW = HD + 2;
-    float* wsb = a.ws + (((size_t)tix * a.nkv + h) * NC) * (size_t)(G * 16 * RW);
-    float* mine = wsb + ((size_t)chunk * G + wg) * (16 * RW);
-#pragma unroll
-    for (int nt = 0; nt < HD / 8; ++nt) {
-      const int d = nt * 8 + 2 * qq;
-      if (!active) break;
-      mine[gq * RW + d] = o[nt][0];
-      mine[gq * RW + d + 1] = o[nt][1];
-      mine[(gq + 8) * RW + d] = o[nt][2];
-      mine[(gq + 8) * RW + d + 1] = o[nt][3];
-    }
-    if (active && qq == 0) {
-      mine[gq * RW + HD] = m0;
-      mine[gq * RW + HD + 1] = l0;
-      mine[(gq + 8) * RW + HD] = m1;
-      mine[(gq + 8) * RW + HD + 1] = l1;
-    }
-    __threadfence();
-    __syncthreads();
-    __shared__ int s_last;
-    if (threadIdx.x == 0) {
-      int* tk = a.tickets + (size_t)tix * a.nkv + h;
-      const int t = atomicAdd(tk, 1);
-      s_last = (t == NC - 1);
-      if (s_last) *tk = 0;  // self-reset for the next launch
-    }
-    __syncthreads();
-    if (!s_last || !active) return;
-    __threadfence();
-    // merge: M = max m_c, L = sum l_c 2^(m_c - M), O = sum o_c 2^(m_c - M)
-    float M0 = -INFINITY, M1 = -INFINITY;
-    for (int c = 0; c < NC; ++c) {
-      const float* pc = wsb + ((size_t)c * G + wg) * (16 * RW);
-      M0 = fmaxf(M0, __ldcg(pc + gq * RW + HD));
-      M1 = fmaxf(M1, __ldcg(pc + (gq + 8) * RW + HD));
-    }
-    float L0 = 0.f, L1 = 0.f;
-#pragma unroll
-    for (int nt = 0; nt < HD / 8; ++nt) o[nt][0] = o[nt][1] = o[nt][2] = o[nt][3] = 0.f;
-    for (int c = 0; c < NC; ++c) {
-      const float* pc = wsb + ((size_t)c * G + wg) * (16 * RW);
-      const float mc0 = __ldcg(pc + gq * RW + HD), mc1 = __ldcg(pc + (gq + 8) * RW + HD);
-      const float f0 = (mc0 == -INFINITY) ? 0.f : exp2f(mc0 - M0);
-      const float f1 = (mc1 == -INFINITY) ? 0.f : exp2f(mc1 - M1);
-      L0 += __ldcg(pc + gq * RW + HD + 1) * f0;
-      L1 += __ldcg(pc + (gq + 8) * RW + HD + 1) * f1;
-#pragma unroll
-      for (int nt = 0; nt < HD / 8; ++nt) {
-        const int d = nt * 8 + 2 * qq;
-        o[nt][0] += __ldcg(pc + gq * RW + d) * f0;
-        o[nt][1] += __ldcg(pc + gq * RW + d + 1) * f0;
-        o[nt][2] += __ldcg(pc + (gq + 8) * RW + d) * f1;
-        o[nt][3] += __ldcg(pc + (gq + 8) * RW + d + 1) * f1;
-      }
-    }
-    l0 = L0;
-    l1 = L1;
-  }
   // ---- normalise and store rows gq, gq + 8 (dims 8 nt + 2 qq, +1)
   if (!active) return;
   const float i0 = 1.f / l0, i1 = 1.f / l1;
@@ -594,12 +528,6 @@ void attn_plan(int n_rows, int nkv, int max_seqlen, int* chunk_pages, int* max_c
     // 20.7 us, ctx 8192 75.2 -> 46.4 us; 16 rows: no gain, 1310-token contexts: no gain)
     best_c = 4;
   }
-  static int forced = -2;
-  if (forced == -2) {
-    const char* e = getenv("RT_ATTN_CHUNKS");
-    forced = e ? atoi(e) : -1;
-  }
-  if (forced > 0) best_c = forced;
   int cp = (max_pages + best_c - 1) / best_c;
   if (cp < 1) cp = 1;
   *chunk_pages = cp;
@@ -639,17 +567,13 @@ static void launch_prefill_ng(const PrefillArgs& a, cudaStream_t s) {
     attr = true;
   }
   // plain stream-ordered launch (no programmatic dependent launch): measured faster for this
-  // latency-bound kernel (tools/prefill_tail_bench.py, RT_PF_PDL=1 to compare)
-  static const bool pdl = getenv("RT_PF_PDL") != nullptr;
-  const dim3 grid(a.n_tiles, a.nkv, a.chunks), block(32 * a.G * NG);
-  if (pdl)
-    launch_pdl(k_attn_prefill<HD, NG>, grid, block, C::SMEM, s, a);
-  else
-    k_attn_prefill<HD, NG><<<grid, block, C::SMEM, s>>>(a);
+  // latency-bound kernel (tools/prefill_tail_bench.py)
+  const dim3 grid(a.n_tiles, a.nkv), block(32 * a.G * NG);
+  k_attn_prefill<HD, NG><<<grid, block, C::SMEM, s>>>(a);
 }
 template <int HD>
 static void launch_prefill_hd(const PrefillArgs& a, cudaStream_t s) {
-  // two warp groups while there is at most one CTA per SM (RT_PF_GROUPS=1/2 forces)
+  // two warp groups while there is at most one CTA per SM (a.groups = 1 / 2 forces)
   static int sms = 0;
   if (!sms) {
     int dev = 0;
@@ -657,43 +581,16 @@ static void launch_prefill_hd(const PrefillArgs& a, cudaStream_t s) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     if (sms <= 0) sms = 148;
   }
-  static const int forced = getenv("RT_PF_GROUPS") ? atoi(getenv("RT_PF_GROUPS")) : 0;
-  const long long ctas = (long long)a.n_tiles * a.nkv * a.chunks;
-  const int ng = a.G > 4 ? 1 : (forced ? forced : (ctas <= sms ? 2 : 1));
+  const long long ctas = (long long)a.n_tiles * a.nkv;
+  const int ng = a.G > 4 ? 1 : (a.groups ? a.groups : (ctas <= sms ? 2 : 1));
   if (ng == 2)
     launch_prefill_ng<HD, 2>(a, s);
   else
     launch_prefill_ng<HD, 1>(a, s);
 }
 
-// Split-KV plan of the prefill attention: C page chunks per (tile, kv head), merged by the
-// last chunk's CTA (self-resetting tickets).  RT_PF_CHUNKS sets C (tests / tuning).
-static int prefill_chunks(const PrefillArgs& a) {
-  static int forced = -2;
-  if (forced == -2) {
-    const char* e = getenv("RT_PF_CHUNKS");
-    forced = e ? atoi(e) : -1;
-  }
-  const int max_np = (a.max_seqlen + 15) / 16;
-  const long long ctas = (long long)a.n_tiles * a.nkv;
-  // default 1: measured at the e2e operating point (~20 tiles x 8 kv heads, ~80 pages each)
-  // C = 1 / 2 / 4 / 8: 74.6 / 72.1 / 87.8 / 109 us per layer — the kernel is bound by the
-  // mma.sync work per SM, not by the page stream latency, so splitting only adds the merge
-  (void)max_np;
-  (void)ctas;
-  int c = forced > 0 ? forced : 1;
-  c = std::max(1, std::min(c, 16));
-  const int G = a.nq / a.nkv;
-  if (!a.ws || !a.tickets || (int64_t)ctas * c * G * 16 * (a.hd + 2) > a.ws_floats) c = 1;
-  return c;
-}
-
-void launch_attention_prefill(const PrefillArgs& a0, cudaStream_t s) {
-  if (a0.n_tiles <= 0 || a0.G < 1 || a0.G > 8) return;
-  PrefillArgs a = a0;
-  a.chunks = prefill_chunks(a);
-  static const int no_rot = getenv("RT_PF_NO_ROTATE") != nullptr;
-  a.rotate = no_rot ? 0 : 1;
+void launch_attention_prefill(const PrefillArgs& a, cudaStream_t s) {
+  if (a.n_tiles <= 0 || a.G < 1 || a.G > 8) return;
   switch (a.hd) {
     case 128: launch_prefill_hd<128>(a, s); break;
     case 64: launch_prefill_hd<64>(a, s); break;

@@ -24,10 +24,6 @@
 using namespace rt;
 static_assert(sizeof(SegRec) == sizeof(rt_segment), "segment record layout");
 
-namespace rt {
-void launch_merge_cand(const double* all, int world, double* merged, cudaStream_t s);
-}
-
 // ----------------------------------------------------------------- NCCL (dlopen)
 typedef struct { char internal[128]; } nccl_uid_t;
 typedef void* nccl_comm_t;
@@ -107,23 +103,9 @@ struct rt_engine {
   int* d_attn_tickets = nullptr;
   int* d_gemm_cnt = nullptr;
   GemmTmaSet x_h, x_o, x_act, x_hfin;
-  // projection chain (launch_chain): per job slot (0 O, 1 gate/up, 2 down, 3 next QKV)
-  // partial-tile workspace, self-resetting tile tickets, cumulative done counters and the
-  // host copy of their bases (the value each counter holds before the next launch)
-  bool chain_on = false;
-  float* d_chain_ws[kChainMaxJobs] = {};
-  int chain_slots_n[kChainMaxJobs] = {};
-  unsigned* d_chain_cnt[kChainMaxJobs] = {};
-  unsigned* d_chain_done = nullptr;
-  unsigned chain_base[kChainMaxJobs] = {};
-  int chain_grid_n = 0;
-  float* d_pf_ws = nullptr;      // split-KV partials of the prefill attention
-  int64_t pf_ws_floats = 0;
-  int* d_pf_tickets = nullptr;
   float* d_sk_ws = nullptr;      // stream-K partial tiles (prefill projections, N > 128 rows)
   unsigned* d_sk_cnt = nullptr;  // stream-K tile tickets
   int sk_cnt_cap = 0;
-  int chain_pf_ahead = 16;  // RT_CHAIN_PF
   // submissions
   SubmitRec* h_recs = nullptr;
   int32_t* h_toks = nullptr;
@@ -135,21 +117,15 @@ struct rt_engine {
   // registered shared prompt prefixes (rt_register_prefix): tokens (a multiple of 16) and
   // their read-only pages = page-table row max_tasks + id
   std::vector<std::vector<int32_t>> prefixes;
+  int32_t pfx_pages = 0;  // pages held by registered prefixes (never freed)
   std::unordered_map<int64_t, int> rid_slot;
   int64_t n_submitted = 0;
   int64_t seg_read = 0;
   HostMailbox plan{};
-  // CUDA graphs of decode-only forwards, keyed by (B, split-KV plan, timing)
-  std::unordered_map<int64_t, cudaGraphExec_t> graphs;
-  bool no_graphs = false;
-  // next-projection L2 prefetch budget (RT_L2_PF_MB; off by default: measured 2% slower,
-  // the prefetch competes with the running projection's own stream)
-  int64_t l2_pf_bytes = 0;
   // RT_FLAG_TRACE: per-CTA kernel records (common.cuh TraceScope)
   uint64_t* d_trace = nullptr;
   unsigned* d_trace_n = nullptr;
   unsigned trace_cap = 0;
-  int graph_launches = 0;
   // timing
   std::vector<cudaEvent_t> ev_attn;  // 2 per layer
   cudaEvent_t ev_f0 = nullptr, ev_f1 = nullptr, ev_s0 = nullptr, ev_s1 = nullptr, ev_q1 = nullptr;
@@ -221,8 +197,11 @@ static rt_status validate(const rt_config* c) {
       (!c->tok_class || (c->stop_grammar == RT_GRAMMAR_SKILL && (!c->skill_base_us || !c->skill_unit_us))))
     return RT_E_INVAL;
   if (c->vocab < 2 || !c->tok_skill || !c->tok_exec_min_us) return RT_E_INVAL;
+  if (c->gemm_path < RT_GEMM_PATH_AUTO || c->gemm_path > RT_GEMM_PATH_PAIR) return RT_E_INVAL;
   if (c->eos_id < 0 || c->eos_id >= c->vocab) return RT_E_INVAL;
-  if (c->world < 1 || c->rank < 0 || c->rank >= c->world) return RT_E_INVAL;
+  // the device merge of the per-round candidates (k_merge_cand) holds world x kTopK keys in
+  // shared memory: one node of <= 8 GPUs (BASELINE.json: one 8xB200 box)
+  if (c->world < 1 || c->world > 8 || c->rank < 0 || c->rank >= c->world) return RT_E_INVAL;
   if (!(c->flags & RT_FLAG_NO_MODEL)) {
     if (c->n_layers < 1 || c->d_model % 64 || c->d_ff % 64 || c->n_q_heads < 1 || c->n_kv_heads < 1) return RT_E_INVAL;
     if (c->n_q_heads % c->n_kv_heads || c->n_q_heads / c->n_kv_heads > 8) return RT_E_INVAL;
@@ -271,10 +250,6 @@ static rt_status create_impl(rt_engine* e, const rt_config* cfg) {
   e->cfg.tok_class = nullptr;
   e->cfg.skill_base_us = nullptr;
   e->cfg.skill_unit_us = nullptr;
-  // graphs are opt-in: with PDL already hiding launch gaps they measured ~1% slower on the
-  // llama3-8b B=64 step (profiles/r01_summary.md), they pay off where the host is the bound
-  e->no_graphs = !(c.flags & RT_FLAG_GRAPHS) || getenv("RT_NO_GRAPHS") != nullptr;
-  if (const char* pf = getenv("RT_L2_PF_MB")) e->l2_pf_bytes = (int64_t)atoi(pf) << 20;
   e->cfg.tok_exec_min_us = nullptr;
   e->cfg.nccl_id = nullptr;
   if (e->cfg.max_admit_per_round <= 0) e->cfg.max_admit_per_round = 1 << 30;
@@ -519,39 +494,12 @@ static rt_status create_impl(rt_engine* e, const rt_config* cfg) {
     if (!ok) return done(fail(e, RT_E_CUDA, "cuTensorMapEncodeTiled failed (activations)"));
     e->ev_attn.resize(2 * L);
     for (auto& ev : e->ev_attn) cudaEventCreate(&ev);
-    // split-KV workspace of the prefill attention (attn.cu prefill_chunks): 64 MB
-    e->pf_ws_floats = (int64_t)16 << 20;
-    CK(e, dalloc(e, &e->d_pf_ws, (size_t)e->pf_ws_floats));
-    CK(e, dalloc(e, &e->d_pf_tickets, (size_t)(e->rows_cap / 16 + c.max_batch) * nkv));
-    // hybrid DP + stream-K workspace of the prefill projections (gemm_tc.cu k_gemm_sk;
-    // RT_NO_STREAMK=1: one tile per CTA)
-    if (getenv("RT_NO_STREAMK") == nullptr) {
+    // hybrid DP + stream-K workspace of the prefill projections (gemm_tc.cu k_gemm_sk)
+    {
       const int max_mt = (std::max(std::max(e->qkv_dim, d), 2 * ff) + 127) / 128;
       e->sk_cnt_cap = max_mt * ((R + 159) / 160);
       CK(e, dalloc(e, &e->d_sk_ws, (size_t)gemm_sk_ws_floats()));
       CK(e, dalloc(e, &e->d_sk_cnt, (size_t)e->sk_cnt_cap));
-    }
-    // projection chain for decode rounds of <= 64 rows: OPT-IN (RT_CHAIN=1).  Measured at
-    // C2 it is slower than one launch per projection (182 vs ~104 us per layer, DESIGN.md
-    // §9): each job boundary pays a chain of loaded-HBM latencies (store fence, ticket,
-    // partial loads, release / acquire) that the 96 KB ring per SM cannot cover.
-    {
-      const int cm[kChainMaxJobs] = {d, 2 * ff, d, e->qkv_dim}, ck[kChainMaxJobs] = {nq * hd, d, ff, d};
-      const int P = chain_grid(cm, ck, kChainMaxJobs);
-      bool ok_c = getenv("RT_CHAIN") != nullptr && atoi(getenv("RT_CHAIN")) != 0;
-      for (int j = 0; j < kChainMaxJobs; ++j) ok_c = ok_c && ck[j] % 64 == 0;
-      if (ok_c) {
-        e->chain_grid_n = P;
-        if (const char* pf = getenv("RT_CHAIN_PF")) e->chain_pf_ahead = atoi(pf);
-        for (int j = 0; j < kChainMaxJobs; ++j) {
-          const int mtiles = (cm[j] + 127) / 128;
-          e->chain_slots_n[j] = chain_slots(cm[j], ck[j], P);
-          CK(e, dalloc(e, &e->d_chain_ws[j], (size_t)mtiles * e->chain_slots_n[j] * 64 * 128));
-          CK(e, dalloc(e, &e->d_chain_cnt[j], (size_t)mtiles));
-        }
-        CK(e, dalloc(e, &e->d_chain_done, (size_t)kChainMaxJobs));
-        e->chain_on = true;
-      }
     }
   }
   if (c.flags & RT_FLAG_TRACE) {  // 48-byte records, bound process-wide (last engine wins)
@@ -605,7 +553,6 @@ extern "C" rt_status rt_destroy(rt_engine* e) {
   if (e->h_recs) cudaFreeHost(e->h_recs);
   if (e->h_toks) cudaFreeHost(e->h_toks);
   for (auto ev : e->ev_attn) cudaEventDestroy(ev);
-  for (auto& kv : e->graphs) cudaGraphExecDestroy(kv.second);
   cudaEvent_t evs[] = {e->ev_plan, e->ev_post, e->ev_cand, e->ev_merge, e->ev_f0, e->ev_f1, e->ev_s0, e->ev_s1, e->ev_q1, e->ev_m0, e->ev_m1};
   for (auto ev : evs)
     if (ev) cudaEventDestroy(ev);
@@ -661,7 +608,9 @@ extern "C" rt_status rt_submit_request(rt_engine* e, int32_t agent_id, const int
       n_pfx = lp / 16;
     }
   }
-  if (R - n_pfx > c.n_pages) return fail(e, RT_E_NOMEM, "request larger than the page pool");
+  // the request's own pages must fit beside the prefixes' permanent pages, or it could never
+  // be admitted (and, R-MEM, would refuse every later k = 0 request of each round)
+  if (R - n_pfx > c.n_pages - e->pfx_pages) return fail(e, RT_E_NOMEM, "request larger than the page pool");
   if (e->free_slots.empty()) return fail(e, RT_E_NOMEM, "task table full");
   const int64_t need = (int64_t)n_prompt + (scripted ? n_script : 0);
   if (e->n_staged >= e->recs_cap || e->toks_staged + need > e->toks_cap) {
@@ -736,10 +685,12 @@ extern "C" rt_status rt_register_prefix(rt_engine* e, const int32_t* tokens, int
   CK(e, cudaMemcpy(top.data(), e->sp.free_stack + ds.free_top - n, 4 * (size_t)n, cudaMemcpyDeviceToHost));
   for (int m = 0; m < n; ++m) pages[m] = top[n - 1 - m];
   const int slot = MT + pid;  // the prefix's page-table row
-  CK(e, cudaMemcpy(e->tt.page_table + (size_t)slot * e->pt_stride, pages.data(), 4 * (size_t)n,
-                   cudaMemcpyHostToDevice));
+  // every write below is ordered on the engine stream (non-blocking: the legacy default
+  // stream does not synchronise with it), and the host buffers live until the final sync
+  CK(e, cudaMemcpyAsync(e->tt.page_table + (size_t)slot * e->pt_stride, pages.data(), 4 * (size_t)n,
+                        cudaMemcpyHostToDevice, e->stream));
   const int32_t new_top = ds.free_top - n;
-  CK(e, cudaMemcpy(&e->d_st->free_top, &new_top, 4, cudaMemcpyHostToDevice));
+  CK(e, cudaMemcpyAsync(&e->d_st->free_top, &new_top, 4, cudaMemcpyHostToDevice, e->stream));
   if (!(c.flags & RT_FLAG_NO_MODEL)) {
     // rows (slot, position, token) and 16-position tiles of the prefix, then the forward
     if (n_tokens > e->rows_cap) return fail(e, RT_E_INVAL, "prefix longer than the forward row capacity");
@@ -747,10 +698,11 @@ extern "C" rt_status rt_register_prefix(rt_engine* e, const int32_t* tokens, int
     for (int j = 0; j < n_tokens; ++j) rp[j] = j;
     std::vector<int4> tiles(n);
     for (int t = 0; t < n; ++t) tiles[t] = make_int4(16 * t, 16, 16 * t, slot);
-    CK(e, cudaMemcpy(e->sp.row_task, rt.data(), 4 * (size_t)n_tokens, cudaMemcpyHostToDevice));
-    CK(e, cudaMemcpy(e->sp.row_pos, rp.data(), 4 * (size_t)n_tokens, cudaMemcpyHostToDevice));
-    CK(e, cudaMemcpy(e->sp.row_tok, tokens, 4 * (size_t)n_tokens, cudaMemcpyHostToDevice));
-    CK(e, cudaMemcpy(e->sp.pf_tiles, tiles.data(), sizeof(int4) * (size_t)n, cudaMemcpyHostToDevice));
+    CK(e, cudaMemcpyAsync(e->sp.row_task, rt.data(), 4 * (size_t)n_tokens, cudaMemcpyHostToDevice, e->stream));
+    CK(e, cudaMemcpyAsync(e->sp.row_pos, rp.data(), 4 * (size_t)n_tokens, cudaMemcpyHostToDevice, e->stream));
+    CK(e, cudaMemcpyAsync(e->sp.row_tok, tokens, 4 * (size_t)n_tokens, cudaMemcpyHostToDevice, e->stream));
+    CK(e, cudaMemcpyAsync(e->sp.pf_tiles, tiles.data(), sizeof(int4) * (size_t)n, cudaMemcpyHostToDevice,
+                          e->stream));
     HostMailbox plan{};
     plan.B = 0;
     plan.n_rows = n_tokens;
@@ -760,9 +712,10 @@ extern "C" rt_status rt_register_prefix(rt_engine* e, const int32_t* tokens, int
     plan.max_seqlen = n_tokens;
     st = forward(e, plan);
     if (st != RT_OK) return st;
-    CK(e, cudaStreamSynchronize(e->stream));
   }
+  CK(e, cudaStreamSynchronize(e->stream));
   e->prefixes.emplace_back(tokens, tokens + n_tokens);
+  e->pfx_pages += n;
   if (prefix_id_out) *prefix_id_out = pid;
   return RT_OK;
 }
@@ -791,17 +744,7 @@ static void harvest_timing(rt_engine* e) {
 }
 
 // ------------------------------------------------------------------ forward
-// A plain cudaEventRecord inside stream capture becomes an internal dependency node and the
-// event is never actually recorded; cudaEventRecordExternal makes it a real timing record that
-// fires on every graph replay.
-static void record_timing_event(cudaEvent_t ev, cudaStream_t s) {
-  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-  cudaStreamIsCapturing(s, &cs);
-  if (cs == cudaStreamCaptureStatusActive)
-    cudaEventRecordWithFlags(ev, s, cudaEventRecordExternal);
-  else
-    cudaEventRecord(ev, s);
-}
+static void record_timing_event(cudaEvent_t ev, cudaStream_t s) { cudaEventRecord(ev, s); }
 
 static rt_status forward(rt_engine* e, const HostMailbox& plan) {
   const rt_config& c = e->cfg;
@@ -832,7 +775,6 @@ static rt_status forward(rt_engine* e, const HostMailbox& plan) {
     aa.G = nq / nkv;
     attn_plan(n, nkv, plan.max_seqlen, &aa.chunk_pages, &aa.max_chunks);
     if (attn_ws_floats(n, nq, hd, aa.max_chunks) > e->attn_ws_cap) aa.max_chunks = 1;
-    // single chunk: make the kernel arguments independent of max_seqlen (graph replay)
     if (aa.max_chunks == 1) aa.chunk_pages = e->pt_stride;
     aa.out = e->d_o;
     aa.ws = e->d_attn_ws;
@@ -860,10 +802,6 @@ static rt_status forward(rt_engine* e, const HostMailbox& plan) {
     pa.G = nq / nkv;
     pa.out = e->d_o;
     pa.scale_log2 = sl2;
-    pa.max_seqlen = plan.max_seqlen;
-    pa.ws = e->d_pf_ws;
-    pa.ws_floats = e->pf_ws_floats;
-    pa.tickets = e->d_pf_tickets;
     const bool any_decode = plan.n_rows > plan.n_prefill_rows;
     auto gemm = [&](const bf16* w, const GemmTmaSet& x, int M, int K, GemmArgs g) {
       g.M = M;
@@ -872,6 +810,7 @@ static rt_status forward(rt_engine* e, const HostMailbox& plan) {
       g.sk_ws = e->d_sk_ws;
       g.sk_cnt = e->d_sk_cnt;
       g.sk_cnt_cap = e->sk_cnt_cap;
+      g.force_path = c.gemm_path;
       launch_gemm_epi(w, x, g, 0, s);
       ++launches;
     };
@@ -923,17 +862,10 @@ static rt_status forward(rt_engine* e, const HostMailbox& plan) {
       g.K = d;
       return g;
     };
-    // decode-only chunks of <= 64 rows: O, gate/up, down and the next layer's QKV run as
-    // ONE persistent chain launch per layer (launch_chain)
-    // (not under graph capture: the chain's done targets are per-launch values)
-    cudaStreamCaptureStatus cap_st = cudaStreamCaptureStatusNone;
-    cudaStreamIsCapturing(s, &cap_st);
-    const bool use_chain = e->chain_on && n <= 64 && plan.n_prefill_rows == 0 && pa.n_tiles == 0 &&
-                           cap_st == cudaStreamCaptureStatusNone;
     for (int l = 0; l < c.n_layers; ++l) {
       LayerW& w = e->layers[l];
       void* pool_l = e->d_pool + (size_t)l * e->pool_layer_bytes;
-      if (!use_chain || l == 0) {
+      {
         GemmArgs g = args_qkv(l);
         gemm(w.qkv, e->x_h, e->qkv_dim, d, g);
       }
@@ -951,54 +883,16 @@ static rt_status forward(rt_engine* e, const HostMailbox& plan) {
         launch_attention_prefill(pa, s);
         ++launches;
       }
-      if (use_chain) {
-        ChainArgs ca{};
-        ca.job[0] = args_resid(d, nq * hd);
-        ca.job[0].w = w.o;
-        ca.xmap[0] = e->x_o.m64;
-        ca.job[1] = args_gu();
-        ca.job[1].w = w.gu;
-        ca.xmap[1] = e->x_h.m64;
-        ca.job[2] = args_resid(d, ff);
-        ca.job[2].w = w.d;
-        ca.xmap[2] = e->x_act.m64;
-        ca.n_jobs = 3;
-        if (l + 1 < c.n_layers) {
-          ca.job[3] = args_qkv(l + 1);
-          ca.job[3].w = e->layers[l + 1].qkv;
-          ca.xmap[3] = e->x_h.m64;
-          ca.n_jobs = 4;
-        }
-        for (int j = 0; j < ca.n_jobs; ++j) {
-          ca.ws[j] = e->d_chain_ws[j];
-          ca.ws_slots[j] = e->chain_slots_n[j];
-          ca.tile_cnt[j] = e->d_chain_cnt[j];
-          e->chain_base[j] += (unsigned)((ca.job[j].M + 127) / 128);
-          ca.done_target[j] = e->chain_base[j];
-        }
-        ca.done = e->d_chain_done;
-        ca.grid = e->chain_grid_n;
-        ca.pf_ahead = e->chain_pf_ahead;
-        CK(e, launch_chain(ca, s));
-        ++launches;
-        continue;
-      }
       {  // O projection + residual
         GemmArgs g = args_resid(d, nq * hd);
-        gemm_set_prefetch(g, w.gu, 2 * ff, n, d, 0, e->l2_pf_bytes);
         gemm(w.o, e->x_o, d, nq * hd, g);
       }
       {  // gate/up projection (FFN RMSNorm as row scale) + SwiGLU
         GemmArgs g = args_gu();
-        gemm_set_prefetch(g, w.d, d, n, ff, 0, e->l2_pf_bytes);
         gemm(w.gu, e->x_h, 2 * ff, d, g);
       }
       {  // down projection + residual
         GemmArgs g = args_resid(d, ff);
-        if (l + 1 < c.n_layers)  // the next layer's QKV projection
-          gemm_set_prefetch(g, e->layers[l + 1].qkv, e->qkv_dim, n, d, 0, e->l2_pf_bytes);
-        else if (row0 + n >= n_rows)  // the lm_head of the logits rows
-          gemm_set_prefetch(g, e->lm, V, B, d, 0, e->l2_pf_bytes);
         gemm(w.d, e->x_act, d, ff, g);
       }
     }
@@ -1023,7 +917,6 @@ static rt_status forward(rt_engine* e, const HostMailbox& plan) {
   }
   CK(e, cudaGetLastError());
   e->stats.kernel_launches += launches;
-  e->graph_launches = launches;
   if (timing) e->timing_layers = c.n_layers;
   return RT_OK;
 }
@@ -1066,6 +959,18 @@ extern "C" rt_status rt_step(rt_engine* e, int64_t now_us, rt_round_info* info) 
     info->n_evicted = plan.n_evicted;
     info->n_restored = plan.n_restored;
   }
+  // a12: allgather of this round's local top-K candidates on the side stream.  EVERY round
+  // (idle and B == 0 rounds too, whose candidates are empty): the allgather is a collective,
+  // so every rank must issue exactly one per rt_step call
+  if (e->exchange) {
+    CK(e, cudaEventRecord(e->ev_cand, s));
+    CK(e, cudaStreamWaitEvent(e->side, e->ev_cand, 0));
+    int r = g_nccl.allgather(e->sp.cand, e->d_cand_all, kTopK * 4, kNcclFloat64, e->comm, e->side);
+    if (r != 0) return fail(e, RT_E_NCCL, "ncclAllGather failed");
+    launch_merge_cand(e->d_cand_all, c.world, e->d_merged, e->side);
+    CK(e, cudaEventRecord(e->ev_merge, e->side));
+    e->merge_pending = true;
+  }
   if (plan.idle || plan.B == 0) return RT_OK;
   // KV eviction / restore copies of this round (before the forward reuses the pages):
   // evictions first (a restore may re-pop a page an eviction just released)
@@ -1077,47 +982,10 @@ extern "C" rt_status rt_step(rt_engine* e, int64_t now_us, rt_round_info* info) 
                    e->d_hpool, blk, L, s);
     CK(e, cudaGetLastError());
   }
-  if (e->exchange) {  // a12: allgather of this round's local top-K candidates on the side stream
-    CK(e, cudaEventRecord(e->ev_cand, s));
-    CK(e, cudaStreamWaitEvent(e->side, e->ev_cand, 0));
-    int r = g_nccl.allgather(e->sp.cand, e->d_cand_all, kTopK * 4, kNcclFloat64, e->comm, e->side);
-    if (r != 0) return fail(e, RT_E_NCCL, "ncclAllGather failed");
-    launch_merge_cand(e->d_cand_all, c.world, e->d_merged, e->side);
-    CK(e, cudaEventRecord(e->ev_merge, e->side));
-    e->merge_pending = true;
-  }
   if (timing) cudaEventRecord(e->ev_f0, s);
   if (!(c.flags & RT_FLAG_NO_MODEL)) {
-    // Decode-only rounds replay a CUDA graph of the whole forward (launch-gap free,
-    // programmatic-dependency edges kept); its arguments depend only on B and the
-    // split-KV plan, which form the cache key.  Prefill rounds launch directly.
-    const bool graphable = !e->no_graphs && plan.n_prefill_rows == 0 && plan.n_rows == plan.B &&
-                           plan.B <= e->fwd_rows;
-    if (graphable) {
-      int cp = 0, mc = 0;
-      attn_plan(plan.B, c.n_kv_heads, plan.max_seqlen, &cp, &mc);
-      const int64_t key = (int64_t)plan.B | ((int64_t)(mc > 1 ? cp : 0) << 20) | ((int64_t)timing << 40);
-      auto it = e->graphs.find(key);
-      if (it == e->graphs.end()) {
-        cudaGraph_t g = nullptr;
-        cudaGraphExec_t ge = nullptr;
-        CK(e, cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
-        st = forward(e, plan);
-        cudaError_t ce = cudaStreamEndCapture(s, &g);
-        if (st != RT_OK) return st;
-        CK(e, ce);
-        CK(e, cudaGraphInstantiate(&ge, g, 0));
-        cudaGraphDestroy(g);
-        it = e->graphs.emplace(key, ge).first;
-      } else {
-        e->stats.kernel_launches += e->graph_launches;
-      }
-      CK(e, cudaGraphLaunch(it->second, s));
-      if (timing) e->timing_layers = c.n_layers;
-    } else {
-      st = forward(e, plan);
-      if (st != RT_OK) return st;
-    }
+    st = forward(e, plan);
+    if (st != RT_OK) return st;
   }
   if (timing) {
     cudaEventRecord(e->ev_f1, s);

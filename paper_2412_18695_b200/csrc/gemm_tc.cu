@@ -204,8 +204,7 @@ struct TileSrc {
   const float* P;
   const float* R;
   uint32_t pl;  // smem address of P (pull)
-  int S, rank, slot_cols, cb, kind;  // kind 0 local, 1 push, 2 pull, 3 global slots (chain)
-  const float* G;                    // kind 3: S partial tiles [S][BN][128] in global memory
+  int S, rank, slot_cols, cb, kind;  // kind 0 local, 1 push, 2 pull
 };
 // Epilogue chunk: 16 columns per iteration.  The loop is latency-bound (4 epilogue warps,
 // one per SM sub-partition, nothing else to hide behind), so every load of a chunk is
@@ -236,10 +235,6 @@ __device__ __forceinline__ void tile_vals16(const TileSrc& t, int c0, int ce, in
       const uint32_t base = smem_u32(src) + (uint32_t)(r * 4);
 #pragma unroll
       for (int k = 0; k < kEpiCh; ++k) w[k] = (c0 + k < ce) ? lds_f32(base + k * 512) : 0.f;
-    } else if (t.kind == 3) {  // written by other SMs in this launch: L2 (ld.global.cg)
-      const float* src = t.G + ((size_t)rk * t.slot_cols + c0) * 128 + r;
-#pragma unroll
-      for (int k = 0; k < kEpiCh; ++k) w[k] = (c0 + k < ce) ? __ldcg(src + k * 128) : 0.f;
     } else {
       const uint32_t base = dsmem_addr(t.pl, (uint32_t)rk) + (uint32_t)((c0 * 128 + r) * 4);
 #pragma unroll
@@ -279,8 +274,7 @@ __device__ __forceinline__ void epilogue(const GemmArgs& g, const EpiSmem& sm, c
     for (int k = 0; k < CH; ++k) {
       const bool ok = active && c + k < NL;
       if constexpr (MODE == EPI_RESID) {
-        // __ldcg: in the projection chain x was written by another SM in this launch
-        ia[k] = !ok ? 0.f : pre ? sm.xp[(c - cb + k) * 128 + et] : __ldcg(g.x + (size_t)(n0 + c + k) * g.M + m);
+        ia[k] = !ok ? 0.f : pre ? sm.xp[(c - cb + k) * 128 + et] : g.x[(size_t)(n0 + c + k) * g.M + m];
         ib[k] = 0.f;
       } else if constexpr (MODE == EPI_QKV) {
         const bool okr = ok && qrope;
@@ -642,20 +636,6 @@ __global__ void __launch_bounds__(kGemmThreads, GemmCfg<BN>::CTAS_PER_SM)
         bulk_g2s_hint(sA + s * C::A_BYTES, wt + (size_t)i * (128 * kBK), C::A_BYTES, &full[s], pol);
         tma_load_2d(sB + s * C::B_BYTES, &tmB, (kb0 + i) * kBK, n0, &full[s]);
       }
-      if (g.pf_w && n_tile == 0) {  // next launch's first k-blocks -> L2 (weights only)
-        const int L = blockIdx.x + gridDim.x * blockIdx.y, T = gridDim.x * gridDim.y;
-        for (int j = L; j < g.pf_S * g.pf_m_tiles; j += T) {
-          const int pr = j % g.pf_S, pm = j / g.pf_S;
-          const int pk0 = (int)(((long long)g.pf_kb_total * pr) / g.pf_S);
-          const int pk1 = (int)(((long long)g.pf_kb_total * (pr + 1)) / g.pf_S);
-          const int cnt = min(g.pf_kb, pk1 - pk0);
-          if (cnt > 0)
-            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(
-                             g.pf_w + ((size_t)pm * g.pf_kb_total + pk0) * (128 * kBK)),
-                         "r"((uint32_t)cnt * C::A_BYTES)
-                         : "memory");
-        }
-      }
     }
     __syncwarp();
   } else if (warp == 1) {
@@ -739,7 +719,7 @@ __global__ void __launch_bounds__(kGemmThreads, GemmCfg<BN>::CTAS_PER_SM)
       mbar_wait(recv_bar, 0);
     }
     EPI_MARK(3);
-    const TileSrc ts{P, R, smem_u32(P), S, rank, slot_cols, cb, S == 1 ? 0 : (push ? 1 : 2), nullptr};
+    const TileSrc ts{P, R, smem_u32(P), S, rank, slot_cols, cb, S == 1 ? 0 : (push ? 1 : 2)};
     epilogue<MODE>(g, sm, ts, m_tile, n0, cb, ce, et, pre);
     if (push && et == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     EPI_MARK(8);
@@ -769,431 +749,6 @@ __global__ void __launch_bounds__(kGemmThreads, GemmCfg<BN>::CTAS_PER_SM)
   }
 }
 
-// ============================================================ projection chain
-// One persistent CTA per SM runs up to 4 dependent decode projections (model.h ChainArgs,
-// DESIGN.md §6).  Per job, the m-tile x k-block iterations are split evenly over the CTAs
-// (stream-K); a CTA accumulates each tile segment of its range in one of two TMEM buffers.
-// Roles as k_gemm_tc: warp 0 lane 0 = producer, warp 1 = TMEM owner + MMA issuer, warps
-// 2..5 = epilogue.  The producer streams weight k-blocks into the ring continuously across
-// job boundaries (weights do not depend on activations) and issues a stage's activation
-// tile only once the job it belongs to may read its input (job 0: the previous kernel,
-// griddepcontrol.wait; job j > 0: every tile of job j - 1 finished, an acquire poll of the
-// cumulative done[j - 1] counter).  So HBM keeps streaming while the tail of job j - 1
-// (last MMAs, partial-tile fixup, epilogue) completes — the bubbles a launch per
-// projection pays (pipeline fill, split-K exchange, epilogue, exit) overlap the stream.
-// Segments that are not a whole tile store their fp32 partial to the job's workspace slot;
-// the last contributor (atomic ticket) sums the slots in slot order (deterministic) and
-// runs the fused epilogue of that job's mode.
-namespace chain {
-constexpr int BN = 64;
-constexpr int STAGES = 6;
-constexpr int A_BYTES = 128 * kBK * 2;  // 16 KB weight k-block
-constexpr int B_BYTES = BN * kBK * 2;   // 8 KB activation k-block
-constexpr int P_BYTES = BN * 128 * 4;   // whole-tile accumulator staging
-constexpr int CTL = 256;
-constexpr int META = 3 * BN * 4;
-constexpr int RED = 2 * 4 * BN * 4;
-constexpr int SMEM = 1024 + STAGES * (A_BYTES + B_BYTES) + 2 * P_BYTES + CTL + META + RED;
-static_assert(SMEM <= 227 * 1024, "chain smem");
-
-// k-block iterations of a job: I = m_tiles * kb; CTA c owns [q0(c), q0(c + 1))
-__host__ __device__ inline int q0(long long I, int c, int P) { return (int)((I * c) / P); }
-// the CTA whose range contains iteration q (valid when I >= P: no empty ranges)
-__host__ __device__ inline int owner(long long q, long long I, int P) { return (int)(((q + 1) * P - 1) / I); }
-
-struct Cursor {  // walk of this CTA's k-block iterations across the jobs of the launch
-  int j, q, qend, kb, kbt;
-  const bf16* wq;  // weight k-block q of job j (UMMA-tiled: k-block q at w + q * 128 * 64)
-};
-__device__ __forceinline__ void cur_job(const ChainArgs& a, Cursor& c, int cta, int P) {
-  for (;;) {
-    ++c.j;
-    if (c.j >= a.n_jobs) return;
-    const GemmArgs& g = a.job[c.j];
-    const long long I = (long long)g.m_tiles * g.kb_total;
-    c.q = q0(I, cta, P);
-    c.qend = q0(I, cta + 1, P);
-    c.kbt = g.kb_total;
-    c.kb = c.q % c.kbt;
-    c.wq = g.w + (size_t)c.q * (128 * kBK);
-    if (c.q < c.qend) return;
-  }
-}
-__device__ __forceinline__ void cur_init(const ChainArgs& a, Cursor& c, int cta, int P) {
-  c.j = -1;
-  cur_job(a, c, cta, P);
-}
-__device__ __forceinline__ void cur_adv(const ChainArgs& a, Cursor& c, int cta, int P) {
-  c.wq += 128 * kBK;
-  if (++c.kb == c.kbt) c.kb = 0;
-  if (++c.q >= c.qend) cur_job(a, c, cta, P);
-}
-__device__ __forceinline__ bool done_reached(const unsigned* p, unsigned target) {
-  unsigned v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
-  return (int)(v - target) >= 0;
-}
-__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
-  uint32_t ok;
-  asm volatile(
-      "{\n\t.reg .pred P1;\n\t"
-      "mbarrier.test_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
-      "selp.u32 %0, 1, 0, P1;\n\t}"
-      : "=r"(ok)
-      : "r"(smem_u32(bar)), "r"(parity)
-      : "memory");
-  return ok != 0;
-}
-}  // namespace chain
-
-// Epilogue inputs of a chain tile, loaded into registers (all in flight at once) while the
-// partial-tile fixup runs, then parked in sm.xp: EPI_RESID the residual x [64 cols][128];
-// EPI_QKV cos / sin [64 cols][64 freqs] (thread: frequency et & 63, columns et >> 6 + 2k).
-__device__ __forceinline__ void chain_inputs_load(const GemmArgs& g, const EpiSmem& sm, int t, int et,
-                                                  float (&in)[chain::BN]) {
-  if (g.mode == EPI_RESID) {
-    const int m = t * 128 + et;
-#pragma unroll
-    for (int c = 0; c < chain::BN; ++c)
-      in[c] = (m < g.M && c < g.N) ? __ldcg(g.x + (size_t)c * g.M + m) : 0.f;
-  } else if (g.mode == EPI_QKV) {
-    const int i = et & 63, half = g.qkv.hd >> 1;
-#pragma unroll
-    for (int k = 0; k < chain::BN / 2; ++k) {
-      const int c = (et >> 6) + 2 * k;
-      const bool ok = c < g.N && i < half;
-      const int pos = ok ? sm.pos[c] : 0;
-      in[k] = ok ? g.qkv.cos[(size_t)pos * half + i] : 0.f;
-      in[chain::BN / 2 + k] = ok ? g.qkv.sin[(size_t)pos * half + i] : 0.f;
-    }
-  }
-}
-__device__ __forceinline__ void chain_inputs_park(const GemmArgs& g, const EpiSmem& sm, int et,
-                                                  const float (&in)[chain::BN]) {
-  if (g.mode == EPI_RESID) {
-#pragma unroll
-    for (int c = 0; c < chain::BN; ++c) sm.xp[c * 128 + et] = in[c];
-  } else if (g.mode == EPI_QKV) {
-    const int i = et & 63;
-#pragma unroll
-    for (int k = 0; k < chain::BN / 2; ++k) {
-      const int c = (et >> 6) + 2 * k;
-      sm.xp[c * 64 + i] = in[k];
-      sm.xp[sm.xp_sin + c * 64 + i] = in[chain::BN / 2 + k];
-    }
-  }
-}
-template <int MODE>
-__device__ __forceinline__ void chain_epilogue(const GemmArgs& g, const EpiSmem& sm, const TileSrc& ts, int t,
-                                               int et) {
-  epilogue<MODE>(g, sm, ts, t, 0, 0, chain::BN, et, MODE == EPI_RESID || MODE == EPI_QKV);
-}
-
-__global__ void __launch_bounds__(kGemmThreads, 1) k_chain(const __grid_constant__ ChainArgs a) {
-  using namespace chain;
-  extern __shared__ unsigned char smem_raw[];
-  unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  unsigned char* sA = smem;
-  unsigned char* sB = smem + STAGES * A_BYTES;
-  float* P = reinterpret_cast<float*>(sB + STAGES * B_BYTES);
-  float* Q = P + BN * 128;  // second staging buffer of the partial-tile fixup
-  unsigned char* ctl = reinterpret_cast<unsigned char*>(Q) + P_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(ctl);
-  uint64_t* empty = full + STAGES;
-  uint64_t* tfull = empty + STAGES;
-  uint64_t* tempty = tfull + 2;
-  uint64_t* fxbar = tempty + 2;  // [2] fixup staging loads (P, Q)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fxbar + 2);
-  int* s_last = reinterpret_cast<int*>(tmem_slot + 1);
-  EpiSmem sm;
-  sm.pos = reinterpret_cast<int*>(ctl + CTL);
-  sm.page = sm.pos + BN;
-  sm.inv = reinterpret_cast<float*>(sm.page + BN);
-  sm.redv = reinterpret_cast<float*>(ctl + CTL + META);
-  sm.redi = reinterpret_cast<int*>(sm.redv + 4 * BN);
-  sm.bn = BN;
-  sm.xp = Q;  // epilogue inputs (chain_inputs_park), after the fixup is done with Q
-  sm.xp_sin = BN * 64;
-  __shared__ long long s_mark[9];
-  sm.mark = s_mark;
-
-  TraceScope tr(TK_CHAIN | ((uint32_t)a.n_jobs << 8));
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int cta = blockIdx.x, NP = gridDim.x;
-
-  if (warp == 0 && lane == 0) {
-    for (int i = 0; i < STAGES; ++i) {
-      mbar_init(&full[i], 1);
-      mbar_init(&empty[i], 1);
-    }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 1);
-      mbar_init(&fxbar[i], 1);
-    }
-    fence_mbar_init();
-  }
-  if (warp == 1) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(2 * BN));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
-  }
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  // (dependents are triggered after the dependency wait: the chain's last job is a QKV)
-
-  if (warp == 0) {
-    if (lane == 0) {
-      // W cursor runs ahead of the X cursor by up to the ring depth
-      for (int j = 0; j < a.n_jobs; ++j) prefetch_tmap(&a.xmap[j]);
-      Cursor cw, cx, cp;
-      cur_init(a, cw, cta, NP);
-      cur_init(a, cx, cta, NP);
-      cur_init(a, cp, cta, NP);
-      int np = 0;  // weight k-blocks prefetched into L2 (lookahead a.pf_ahead beyond the ring)
-      const uint64_t pol = a.job[0].l2_evict_first ? l2_policy_evict_first() : 0ull;
-      int nw = 0, nx = 0, dep_job = -1;  // dep_job: highest job whose X may be loaded
-      bool waited = false;
-      unsigned long long t_dep[kChainMaxJobs] = {0, 0, 0, 0};  // trace: input of job j ready
-      while (cx.j < a.n_jobs) {
-        bool prog = false;
-        if (cw.j < a.n_jobs) {
-          const int st = nw % STAGES;
-          if (nw < STAGES || chain::mbar_test(&empty[st], (uint32_t)(((nw / STAGES) & 1) ^ 1))) {
-            mbar_arrive_expect_tx(&full[st], A_BYTES + B_BYTES);
-            bulk_g2s_hint(sA + st * A_BYTES, cw.wq, A_BYTES, &full[st], pol);
-            cur_adv(a, cw, cta, NP);
-            ++nw;
-            prog = true;
-          }
-        }
-        if (cp.j < a.n_jobs && np < nw + a.pf_ahead) {
-          // keep HBM streaming through job boundaries: the ring stalls while job j - 1
-          // finishes, the L2 prefetch does not
-          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(cp.wq), "r"((uint32_t)A_BYTES) : "memory");
-          cur_adv(a, cp, cta, NP);
-          ++np;
-          prog = true;
-        }
-        if (nx < nw) {
-          const int j = cx.j;
-          if (dep_job < j) {
-            if (j == 0) {
-              // the previous kernel (attention) produced job 0's input: wait only once the
-              // ring holds as many weight k-blocks as it can
-              if (!prog || cw.j >= a.n_jobs) {
-                pdl_wait();
-                pdl_trigger();
-                tr.ready();
-                waited = true;
-                dep_job = 0;
-                t_dep[0] = gtimer();
-              }
-            } else if (chain::done_reached(a.done + (j - 1), a.done_target[j - 1])) {
-              asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> TMA reads
-              dep_job = j;
-              t_dep[j] = gtimer();
-            }
-          }
-          if (dep_job >= j) {
-            const int st = nx % STAGES;
-            tma_load_2d(sB + st * B_BYTES, &a.xmap[j], cx.kb * kBK, 0, &full[st]);
-            cur_adv(a, cx, cta, NP);
-            ++nx;
-            prog = true;
-          }
-        }
-        if (!prog) __nanosleep(32);
-      }
-      if (!waited) pdl_wait();
-      if (!waited) pdl_trigger();
-      trace_phase(TK_PHASE | TK_CHAIN | (1u << 8), t_dep[0], t_dep[1], t_dep[2], t_dep[3]);
-    }
-    __syncwarp();
-  } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = umma_idesc(128, BN);
-      int n = 0, seg = 0;
-      unsigned long long t_mma[kChainMaxJobs] = {0, 0, 0, 0};  // trace: last MMA of job j issued
-      for (int j = 0; j < a.n_jobs; ++j) {
-        const GemmArgs& g = a.job[j];
-        const int kbt = g.kb_total;
-        const long long I = (long long)g.m_tiles * kbt;
-        const int qa = q0(I, cta, NP), qb = q0(I, cta + 1, NP);
-        for (int q = qa; q < qb;) {
-          const int t = q / kbt;
-          const int lo = q - t * kbt, hi = min(qb - t * kbt, kbt);
-          const int buf = seg & 1;
-          if (seg >= 2) mbar_wait(&tempty[buf], (uint32_t)(((seg >> 1) - 1) & 1));
-          tc_fence_after();
-          const uint32_t acc = tmem + (uint32_t)(buf * BN);
-          for (int kb = lo; kb < hi; ++kb, ++n) {
-            const int st = n % STAGES;
-            mbar_wait(&full[st], (uint32_t)((n / STAGES) & 1));
-            tc_fence_after();
-            const uint32_t a0 = smem_u32(sA + st * A_BYTES);
-            const uint32_t b0 = smem_u32(sB + st * B_BYTES);
-#pragma unroll
-            for (int k = 0; k < kBK / 16; ++k)
-              umma_f16(acc, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
-                       (kb > lo || k > 0) ? 1u : 0u);
-            umma_commit(&empty[st]);
-          }
-          umma_commit(&tfull[buf]);
-          ++seg;
-          q = t * kbt + hi;
-        }
-        t_mma[j] = gtimer();
-      }
-      trace_phase(TK_PHASE | TK_CHAIN | (2u << 8), t_mma[0], t_mma[1], t_mma[2], t_mma[3]);
-    }
-    __syncwarp();
-  } else {
-    pdl_wait();
-    const int et = (warp & 3) * 32 + lane;
-    const uint32_t tb = tmem + ((uint32_t)((warp & 3) * 32) << 16);
-    int seg = 0, meta_job = -1;
-    uint32_t fx_phase[2] = {0u, 0u};
-    unsigned long long fx_t0 = 0, fx_t1 = 0, t_seg0 = 0;  // trace marks (thread et == 0)
-    unsigned long long t_epi[kChainMaxJobs] = {0, 0, 0, 0};  // trace: this CTA done with job j
-    for (int j = 0; j < a.n_jobs; ++j) {
-      const GemmArgs& g = a.job[j];
-      const int kbt = g.kb_total;
-      const long long I = (long long)g.m_tiles * kbt;
-      const int qa = q0(I, cta, NP), qb = q0(I, cta + 1, NP);
-      if (j > 0 && et == 0) t_epi[j - 1] = gtimer();
-      for (int q = qa; q < qb;) {
-        const int t = q / kbt;
-        const int hi = min(qb - t * kbt, kbt);
-        const int buf = seg & 1;
-        const int c_first = owner((long long)t * kbt, I, NP), c_last = owner((long long)(t + 1) * kbt - 1, I, NP);
-        const int nc = c_last - c_first + 1;
-        mbar_wait(&tfull[buf], (uint32_t)((seg >> 1) & 1));
-        tc_fence_after();
-        if (et == 0) t_seg0 = gtimer();
-        epi_bar();  // the previous segment's epilogue is done with P / sm
-        TileSrc ts{P, nullptr, 0u, 1, 0, BN, 0, 0, nullptr};
-        bool run = true;
-        // this job's inputs written by earlier jobs (RMSNorm sums, residual) + column metadata
-        auto job_meta = [&]() {
-          if (meta_job == j) return;
-          for (int i = 0; i < j; ++i)
-            while (!chain::done_reached(a.done + i, a.done_target[i])) __nanosleep(64);
-          switch (g.mode) {
-            case EPI_RESID: column_meta<EPI_RESID>(g, sm, t, 0, 0, BN, et); break;
-            case EPI_SWIGLU: column_meta<EPI_SWIGLU>(g, sm, t, 0, 0, BN, et); break;
-            case EPI_QKV: column_meta<EPI_QKV>(g, sm, t, 0, 0, BN, et); break;
-            default: break;
-          }
-          meta_job = j;
-        };
-        float in[BN];
-        if (nc == 1) {
-          job_meta();
-          chain_inputs_load(g, sm, t, et, in);
-#pragma unroll 1
-          for (int c0 = 0; c0 < BN; c0 += 16) {
-            float v[16];
-            tmem_ld16(tb + (uint32_t)(buf * BN + c0), v);
-#pragma unroll
-            for (int i = 0; i < 16; ++i) P[(c0 + i) * 128 + et] = v[i];
-          }
-          tc_fence_before();
-          epi_bar();
-          if (et == 0) mbar_arrive(&tempty[buf]);
-        } else {
-          float* wsl = a.ws[j] + (size_t)t * a.ws_slots[j] * (BN * 128);
-#pragma unroll 1
-          for (int c0 = 0; c0 < BN; c0 += 16) {
-            float v[16];
-            tmem_ld16(tb + (uint32_t)(buf * BN + c0), v);
-#pragma unroll
-            for (int i = 0; i < 16; ++i) __stcg(wsl + ((size_t)(cta - c_first) * BN + c0 + i) * 128 + et, v[i]);
-          }
-          tc_fence_before();
-          __threadfence();
-          epi_bar();
-          if (et == 0) {
-            mbar_arrive(&tempty[buf]);
-            const unsigned old = atomicAdd(a.tile_cnt[j] + t, 1u);
-            *s_last = (old == (unsigned)(nc - 1)) ? 1 : 0;
-          }
-          epi_bar();
-          run = *s_last != 0;
-          if (run) {
-            // last contributor: sum the nc partials in slot order (deterministic) with
-            // double-buffered 32 KB bulk loads (TMA engine: latency-bound per-thread L2
-            // loads measured ~4 GB/s per SM under the weight stream), into P, while the
-            // epilogue inputs load into registers
-            __threadfence();
-            if (et == 0) {
-              a.tile_cnt[j][t] = 0u;  // self-reset for the next launch
-              asm volatile("fence.proxy.async.global;" ::: "memory");
-              fx_t0 = gtimer();
-            }
-            job_meta();
-            chain_inputs_load(g, sm, t, et, in);
-            float acc[BN];
-#pragma unroll
-            for (int c = 0; c < BN; ++c) acc[c] = 0.f;
-            for (int sl = 0; sl < nc; sl += 2) {
-              if (et == 0)
-                for (int b = 0; b < 2 && sl + b < nc; ++b) {
-                  mbar_arrive_expect_tx(&fxbar[b], P_BYTES);
-                  bulk_g2s(b ? (void*)Q : (void*)P, wsl + (size_t)(sl + b) * BN * 128, P_BYTES, &fxbar[b]);
-                }
-              for (int b = 0; b < 2 && sl + b < nc; ++b) {
-                mbar_wait(&fxbar[b], fx_phase[b]);
-                fx_phase[b] ^= 1u;
-                const float* buf2 = b ? Q : P;
-#pragma unroll
-                for (int c = 0; c < BN; ++c) acc[c] += buf2[c * 128 + et];
-              }
-              epi_bar();  // P / Q free for the next loads
-            }
-#pragma unroll
-            for (int c = 0; c < BN; ++c) P[c * 128 + et] = acc[c];
-            if (et == 0) fx_t1 = gtimer();
-          }
-        }
-        if (run) {
-          chain_inputs_park(g, sm, et, in);
-          epi_bar();
-          switch (g.mode) {
-            case EPI_RESID: chain_epilogue<EPI_RESID>(g, sm, ts, t, et); break;
-            case EPI_SWIGLU: chain_epilogue<EPI_SWIGLU>(g, sm, ts, t, et); break;
-            case EPI_QKV: chain_epilogue<EPI_QKV>(g, sm, ts, t, et); break;
-            default: break;
-          }
-          __threadfence();
-          epi_bar();
-          if (et == 0) {
-            asm volatile("fence.proxy.async.global;" ::: "memory");
-            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.done + j) : "memory");
-            trace_phase(TK_PHASE | TK_CHAIN | (4u << 8), fx_t0 ? fx_t0 : t_seg0, fx_t1 ? fx_t1 : t_seg0, gtimer(),
-                        ((unsigned long long)j << 32) | (unsigned)nc);
-            fx_t0 = fx_t1 = 0;
-          }
-        }
-        ++seg;
-        q = t * kbt + hi;
-      }
-    }
-    if (et == 0) {
-      t_epi[a.n_jobs - 1] = gtimer();
-      trace_phase(TK_PHASE | TK_CHAIN | (3u << 8), t_epi[0], t_epi[1], t_epi[2], t_epi[3]);
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 1) {
-    tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
-  }
-}
-
 // ============================================================ hybrid DP + stream-K projection
 // Rounds with prompt rows run the projections at N = 130 .. 8192 rows, where the GEMM is
 // tensor-bound and one tile per CTA quantises badly on 148 SMs (gate/up at N = 256: 224
@@ -1209,19 +764,17 @@ __global__ void __launch_bounds__(kGemmThreads, 1) k_chain(const __grid_constant
 // last contributor sums the partials in contributor order (deterministic) and runs the
 // fused epilogue in column chunks staged through shared memory.
 namespace sk {
+// stream-K k-block iterations: I = tiles * kb; CTA c owns [q0(c), q0(c + 1))
+__host__ __device__ inline int q0(long long I, int c, int P) { return (int)((I * c) / P); }
+// the CTA whose range contains iteration q (valid when I >= P: no empty ranges)
+__host__ __device__ inline int owner(long long q, long long I, int P) { return (int)(((q + 1) * P - 1) / I); }
 constexpr int A_BYTES = 128 * kBK * 2;
 template <int BN>
 struct Cfg {
   // ring depth: as many stages as fit beside the epilogue staging (the mainloop of these
-  // tensor-bound prefill tiles is latency bound on the L2 / HBM round trip of each stage;
-  // RT_SK_STAGES4 builds keep the earlier 4-stage ring for comparison)
-#ifdef RT_SK_STAGES4
-  static constexpr int STAGES = 4;
-  static constexpr int CHUNK = BN == 256 ? 32 : 64;      // epilogue columns per staging pass
-#else
+  // tensor-bound prefill tiles is latency bound on the L2 / HBM round trip of each stage)
   static constexpr int STAGES = BN <= 160 ? 5 : 4;
-  static constexpr int CHUNK = BN == 256 ? 32 : 64;
-#endif
+  static constexpr int CHUNK = BN == 256 ? 32 : 64;      // epilogue columns per staging pass
   static constexpr int STG_BYTES = CHUNK * 128 * 4;
   static constexpr int B_BYTES = BN * kBK * 2;
   static constexpr int TMEM_COLS = 2 * BN <= 256 ? 256 : 512;
@@ -1252,8 +805,8 @@ struct Sched {
     dp_tiles = T - sk_tiles;
     dp_mine = dp_tiles / P;
     I_sk = (long long)sk_tiles * kbt;
-    qa = chain::q0(I_sk, cta, P);
-    qb = chain::q0(I_sk, cta + 1, P);
+    qa = q0(I_sk, cta, P);
+    qb = q0(I_sk, cta + 1, P);
     ns = 0;
     for (int q = qa; q < qb && ns < MAXS;) {
       const int t = q / kbt;
@@ -1381,7 +934,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       Sched::Seg sg;
       for (bool ok = S.first(sg, d, q); ok; ok = S.next(sg, d, q)) {
         const int m_tile = sg.tile / a.n_tiles, n_tile = sg.tile - m_tile * a.n_tiles;
-        for (int kb = sg.lo; kb < sg.hi; ++kb, ++n) {
+        for (int kb = 0; kb < kbt; ++kb, ++n) {
           const int st = n % STAGES;
           if (n >= STAGES) mbar_wait(&empty[st], (uint32_t)(((n / STAGES) & 1) ^ 1));
           mbar_arrive_expect_tx(&full[st], A_BYTES + C::B_BYTES);
@@ -1442,8 +995,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int n0 = n_tile * BN;
       int nc = 1, c_first = 0;
       if (sg.sk_t >= 0) {
-        c_first = chain::owner((long long)sg.sk_t * kbt, S.I_sk, S.P);
-        nc = chain::owner((long long)(sg.sk_t + 1) * kbt - 1, S.I_sk, S.P) - c_first + 1;
+        c_first = owner((long long)sg.sk_t * kbt, S.I_sk, S.P);
+        nc = owner((long long)(sg.sk_t + 1) * kbt - 1, S.I_sk, S.P) - c_first + 1;
       }
       mbar_wait(&tfull[buf], (uint32_t)((seg >> 1) & 1));
       tc_fence_after();
@@ -1479,7 +1032,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
       if (run) {
         column_meta<MODE>(g, sm, m_tile, n0, 0, BN, et);  // per-column metadata of this tile's rows
-        const TileSrc ts0{nullptr, nullptr, 0u, 1, 0, BN, 0, 0, nullptr};
+        const TileSrc ts0{nullptr, nullptr, 0u, 1, 0, BN, 0, 0};
 #pragma unroll 1
         for (int cb = 0; cb < BN; cb += CHUNK) {
           const int ce = min(BN, cb + CHUNK);
@@ -1499,7 +1052,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             for (int r = 0; r < nc; ++r) {
               const int c = c_first + r;
               if (et == 0) {
-                const int fs = chain::q0(S.I_sk, c, S.P) / kbt;
+                const int fs = q0(S.I_sk, c, S.P) / kbt;
                 const float* src = a.ws + ((size_t)c * 2 + (sg.sk_t == fs ? 0 : 1)) * (BN * 128) + (size_t)cb * 128;
                 mbar_arrive_expect_tx(fxbar, bytes);
                 bulk_g2s(stg, src, bytes, fxbar);
@@ -1606,46 +1159,24 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint32_t bar_cluster) {
   asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(bar_cluster) : "memory");
 }
 
-// work of one pair: plain data-parallel pair-tiles (pair, pair + n_pairs, ...), or — with a
-// workspace — the hybrid data-parallel + stream-K order of k_gemm_sk over pair-tiles (the
-// last partial round of pair-tiles is spread over all pairs as k-ranges; each CTA of a pair
-// fixes up its own 128 rows of a split pair-tile through the workspace)
+// work of one pair: data-parallel pair-tiles (pair, pair + n_pairs, ...); the partial last
+// round may run as sub-tiles of kPairSubW columns, one per pair
 constexpr int kPairSubW = 64;  // sub-tile width of the partial last round (32 rows per CTA)
 struct PSeg {
-  int tile, lo, hi;  // pair-tile, k-block range
-  int sk_t;          // stream-K tile index (-1: whole)
-  int sub;           // sub-tile (columns [sub * kPairSubW, +kPairSubW) of the pair-tile), -1: whole
+  int tile;  // pair-tile
+  int sub;   // sub-tile (columns [sub * kPairSubW, +kPairSubW) of the pair-tile), -1: whole
 };
 struct PairSeq {
-  sk::Sched S;
-  bool skm;
-  int pair, n_pairs, PT, kbt, head, sub_s;
-  __device__ void init(int pair_, int n_pairs_, int PT_, int kbt_, int n_tiles, bool skm_, bool all_sk, int head_,
-                       int sub_s_) {
+  int pair, n_pairs, PT, head, sub_s;
+  __device__ void init(int pair_, int n_pairs_, int PT_, int head_, int sub_s_) {
     pair = pair_;
     n_pairs = n_pairs_;
     PT = PT_;
-    kbt = kbt_;
-    skm = skm_;
     head = sub_s_ > 0 ? head_ : PT_;
     sub_s = sub_s_;
-    if (skm) S.init(n_pairs, pair, kbt, PT, n_tiles, all_sk);
   }
   __device__ bool next(PSeg& g, int& i) const {
     g.sub = -1;
-    if (skm) {
-      int u = 0;
-      sk::Sched::Seg q;
-      if (!S.next(q, i, u)) return false;
-      g.tile = q.tile;
-      g.lo = q.lo;
-      g.hi = q.hi;
-      g.sk_t = q.sk_t;
-      return true;
-    }
-    g.lo = 0;
-    g.hi = kbt;
-    g.sk_t = -1;
     const int t = pair + i * n_pairs;
     if (t < head) {
       g.tile = t;
@@ -1677,9 +1208,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint64_t* fxbar = tempty + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(fxbar + 1);
-  int* s_last = reinterpret_cast<int*>(tmem_slot + 1);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   EpiSmem sm;
   sm.pos = reinterpret_cast<int*>(ctl + C::CTL);
   sm.page = sm.pos + BN;
@@ -1700,7 +1229,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const int nt_n = a.n_tiles;
   const int PT = (g.m_tiles >> 1) * nt_n;
   PairSeq Q;
-  Q.init(pair, a.P, PT, kbt, nt_n, a.ws != nullptr, a.all_sk != 0, a.head, a.sub_s);
+  Q.init(pair, a.P, PT, a.head, a.sub_s);
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA);
@@ -1714,7 +1243,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       mbar_init(&tfull[i], 1);
       mbar_init(&tempty[i], 2);
     }
-    mbar_init(fxbar, 1);
     fence_mbar_init();
   }
   if (warp == 1) {
@@ -1743,7 +1271,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         // activation rows of this CTA: its half of the tile, or of the sub-tile
         const int brow = sub ? nt * BN + sg.sub * kPairSubW + (int)rank * (kPairSubW / 2) : nt * BN + (int)rank * C::HB;
         const uint32_t bytes = sub ? 2u * (C::A_BYTES + (kPairSubW / 2) * kBK * 2) : 2u * C::STAGE;
-        for (int kb = sg.lo; kb < sg.hi; ++kb, ++n) {
+        for (int kb = 0; kb < kbt; ++kb, ++n) {
           const int st = n % STAGES;
           if (n >= STAGES) mbar_wait(&empty[st], (uint32_t)(((n / STAGES) & 1) ^ 1));
           if (rank == 0) mbar_arrive_expect_tx(&full[st], bytes);
@@ -1773,7 +1301,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         if (seg >= 2) mbar_wait(&tempty[buf], (uint32_t)(((seg >> 1) - 1) & 1));
         tc_fence_after();
         const uint32_t acc = tmem + (uint32_t)(buf * BN);
-        for (int kb = sg.lo; kb < sg.hi; ++kb, ++n) {
+        for (int kb = 0; kb < kbt; ++kb, ++n) {
           const int st = n % STAGES;
           mbar_wait(&full[st], (uint32_t)((n / STAGES) & 1));
           tc_fence_after();
@@ -1782,7 +1310,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
           for (int k = 0; k < kBK / 16; ++k)
             umma_f16_pair(acc, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
-                          (kb > sg.lo || k > 0) ? 1u : 0u);
+                          (kb > 0 || k > 0) ? 1u : 0u);
           umma_commit_pair(&empty[st], 0x3);
         }
         umma_commit_pair(&tfull[buf], 0x3);
@@ -1794,8 +1322,6 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int et = (warp & 3) * 32 + lane;
     const uint32_t tb = tmem + ((uint32_t)((warp & 3) * 32) << 16);
     const uint32_t tempty0 = dsmem_addr(smem_u32(tempty), 0);
-    const int first_sk = Q.skm ? Q.S.qa / kbt : 0;
-    uint32_t fx_phase = 0u;
     int seg = 0, i = 0;
     PSeg sg;
     for (; Q.next(sg, i); ++seg) {
@@ -1804,97 +1330,35 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int m_tile = 2 * mp + (int)rank;
       const int n0 = nt * BN + (sg.sub >= 0 ? sg.sub * kPairSubW : 0);
       const int W = sg.sub >= 0 ? kPairSubW : BN;  // accumulator columns of this segment
-      int nc = 1, c_first = 0;
-      if (sg.sk_t >= 0) {
-        c_first = chain::owner((long long)sg.sk_t * kbt, Q.S.I_sk, Q.S.P);
-        nc = chain::owner((long long)(sg.sk_t + 1) * kbt - 1, Q.S.I_sk, Q.S.P) - c_first + 1;
-      }
       mbar_wait(&tfull[buf], (uint32_t)((seg >> 1) & 1));
       tc_fence_after();
       epi_bar();  // the previous tile's epilogue is done with the staging buffer / sm
       const uint32_t tacc = tb + (uint32_t)(buf * BN);
-      bool run = true;
-      if (nc > 1) {  // a k-range of a split pair-tile: park this CTA's rows in the workspace
-        float* mine = a.ws + ((size_t)blockIdx.x * 2 + (sg.sk_t == first_sk ? 0 : 1)) * (BN * 128);
+      column_meta<MODE>(g, sm, m_tile, n0, 0, W, et);
+      const TileSrc ts0{nullptr, nullptr, 0u, 1, 0, BN, 0, 0};
 #pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 16) {
+      for (int cb = 0; cb < W; cb += CHUNK) {
+        const int ce = min(W, cb + CHUNK);
+#pragma unroll 1
+        for (int c0 = cb; c0 < ce; c0 += 16) {  // TMEM -> staging
           float v[16];
           tmem_ld16(tacc + (uint32_t)c0, v);
 #pragma unroll
-          for (int k = 0; k < 16; ++k) __stcg(mine + (size_t)(c0 + k) * 128 + et, v[k]);
+          for (int k = 0; k < 16; ++k) stg[(c0 - cb + k) * 128 + et] = v[k];
         }
-        tc_fence_before();
-        __threadfence();
-        epi_bar();
-        if (et == 0) {
-          if (rank == 0) mbar_arrive(&tempty[buf]);
-          else mbar_arrive_cluster(tempty0 + (uint32_t)buf * 8u);
-          const unsigned old = atomicAdd(a.cnt + sg.tile * 2 + rank, 1u);
-          *s_last = (old == (unsigned)(nc - 1)) ? 1 : 0;
-        }
-        epi_bar();
-        run = *s_last != 0;
-        if (run) {
-          __threadfence();
+        if (ce == W) {  // the accumulator buffer is read out: release it to the MMA issuer
+          tc_fence_before();
+          epi_bar();
           if (et == 0) {
-            a.cnt[sg.tile * 2 + rank] = 0u;
-            asm volatile("fence.proxy.async.global;" ::: "memory");
+            if (rank == 0) mbar_arrive(&tempty[buf]);
+            else mbar_arrive_cluster(tempty0 + (uint32_t)buf * 8u);
           }
         }
-      }
-      if (run) {
-        column_meta<MODE>(g, sm, m_tile, n0, 0, W, et);
-        const TileSrc ts0{nullptr, nullptr, 0u, 1, 0, BN, 0, 0, nullptr};
-#pragma unroll 1
-        for (int cb = 0; cb < W; cb += CHUNK) {
-          const int ce = min(W, cb + CHUNK);
-          if (nc == 1) {  // whole pair-tile: TMEM -> staging
-#pragma unroll 1
-            for (int c0 = cb; c0 < ce; c0 += 16) {
-              float v[16];
-              tmem_ld16(tacc + (uint32_t)c0, v);
-#pragma unroll
-              for (int k = 0; k < 16; ++k) stg[(c0 - cb + k) * 128 + et] = v[k];
-            }
-            if (ce == W) {  // the accumulator buffer is read out: release it to the MMA issuer
-              tc_fence_before();
-              epi_bar();
-              if (et == 0) {
-                if (rank == 0) mbar_arrive(&tempty[buf]);
-                else mbar_arrive_cluster(tempty0 + (uint32_t)buf * 8u);
-              }
-            }
-          } else {  // sum the nc partials of columns [cb, ce) in contributor order
-            float acc[CHUNK];
-#pragma unroll
-            for (int c = 0; c < CHUNK; ++c) acc[c] = 0.f;
-            const uint32_t bytes = (uint32_t)((ce - cb) * 512);
-            for (int r = 0; r < nc; ++r) {
-              const int c = c_first + r;
-              if (et == 0) {
-                const int fs = chain::q0(Q.S.I_sk, c, Q.S.P) / kbt;
-                const float* src =
-                    a.ws + ((size_t)(2 * c + (int)rank) * 2 + (sg.sk_t == fs ? 0 : 1)) * (BN * 128) + (size_t)cb * 128;
-                mbar_arrive_expect_tx(fxbar, bytes);
-                bulk_g2s(stg, src, bytes, fxbar);
-              }
-              mbar_wait(fxbar, fx_phase);
-              fx_phase ^= 1u;
-#pragma unroll
-              for (int cc = 0; cc < CHUNK; ++cc)
-                if (cb + cc < ce) acc[cc] += stg[cc * 128 + et];
-              epi_bar();  // the staging buffer is free for the next partial
-            }
-#pragma unroll
-            for (int cc = 0; cc < CHUNK; ++cc)
-              if (cb + cc < ce) stg[cc * 128 + et] = acc[cc];
-          }
-          epi_bar();
-          TileSrc ts = ts0;
-          ts.P = stg - (size_t)cb * 128;  // the epilogue indexes absolute columns
-          epilogue<MODE>(g, sm, ts, m_tile, n0, cb, ce, et, false);
-          epi_bar();
-        }
+        epi_bar();
+        TileSrc ts = ts0;
+        ts.P = stg - (size_t)cb * 128;  // the epilogue indexes absolute columns
+        epilogue<MODE>(g, sm, ts, m_tile, n0, cb, ce, et, false);
+        epi_bar();
       }
     }
   }
@@ -1969,21 +1433,19 @@ bool make_gemm_act_maps(GemmTmaSet* out, const void* base, int K, int rows_cap) 
 // back; vs the rule below 11-18 % less time summed over 160..4096 rows); otherwise the width
 // among {160, 192, 256} with the least padded MMA work (n-tiles x BN), then fewer n-tiles
 // (a padded column costs a full MMA column), with the pair kernel at 192 / 256.
-// Overrides (experiments, the tuner): RT_GEMM_BN = width, RT_GEMM_PAIR = 0 / 1,
-// RT_GEMM_NO_TABLE = rule only.
+// Overrides (parity tests, the tuner): GemmArgs::force_bn / force_path.
 #include "gemm_policy.inc"
 struct GemmChoice {
   int bn;
   bool pair;
 };
-static GemmChoice gemm_choice(int M, int K, int N) {
-  if (N <= 32) return {32, false};
-  if (N <= 64) return {64, false};
-  if (N <= 128) return {128, false};
+static GemmChoice gemm_choice(int M, int K, int N, int force_bn = 0, int force_path = GEMM_PATH_AUTO) {
   GemmChoice c{256, false};
-  bool found = false;
-  static const bool no_table = getenv("RT_GEMM_NO_TABLE") != nullptr;
-  if (!no_table)
+  if (N <= 32) c = {32, false};
+  else if (N <= 64) c = {64, false};
+  else if (N <= 128) c = {128, false};
+  else {
+    bool found = false;
     for (const GemmPolicyRow& r : kGemmPolicy)
       if (r.M == M && r.K == K && N <= r.n_max) {
         const int code = r.code[(N - 129) / 32] - '0';
@@ -1992,24 +1454,23 @@ static GemmChoice gemm_choice(int M, int K, int N) {
         found = true;
         break;
       }
-  if (!found) {
-    int best_t = INT_MAX;
-    long long best_w = LLONG_MAX;
-    for (int bn : {160, 192, 256}) {
-      const int t = (N + bn - 1) / bn;
-      const long long w = (long long)t * bn;
-      if (w < best_w || (w == best_w && t < best_t)) {
-        c.bn = bn;
-        best_w = w;
-        best_t = t;
+    if (!found) {
+      int best_t = INT_MAX;
+      long long best_w = LLONG_MAX;
+      for (int bn : {160, 192, 256}) {
+        const int t = (N + bn - 1) / bn;
+        const long long w = (long long)t * bn;
+        if (w < best_w || (w == best_w && t < best_t)) {
+          c.bn = bn;
+          best_w = w;
+          best_t = t;
+        }
       }
+      c.pair = c.bn >= 192;
     }
-    c.pair = c.bn >= 192;
   }
-  const char* fe = getenv("RT_GEMM_BN");
-  if (fe && atoi(fe) > 0) c.bn = atoi(fe);
-  const char* fp = getenv("RT_GEMM_PAIR");
-  if (fp) c.pair = atoi(fp) != 0;
+  if (force_bn > 0) c.bn = force_bn;
+  if (force_path != GEMM_PATH_AUTO) c.pair = force_path == GEMM_PATH_PAIR;
   return c;
 }
 int gemm_bn(int M, int K, int N) { return gemm_choice(M, K, N).bn; }
@@ -2062,23 +1523,6 @@ static cudaError_t launch_bn(const TmaMap& b, const GemmArgs& g, int S, cudaStre
   cfg.attrs = at;
   cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, k_gemm_tc<BN, MODE>, b, g);
-}
-
-void gemm_set_prefetch(GemmArgs& g, const bf16* w, int M, int N, int K, int splits, int64_t budget_bytes) {
-  if (!w || budget_bytes <= 0) {
-    g.pf_w = nullptr;
-    return;
-  }
-  const int kbt = K / kBK;
-  int S = splits > 0 ? splits : gemm_choose_splits(M, N, K);
-  S = std::max(1, std::min(S, std::min(16, kbt)));
-  const int mt = (M + 127) / 128;
-  const int64_t per_kb = (int64_t)S * mt * (128 * kBK * 2);
-  g.pf_w = w;
-  g.pf_S = S;
-  g.pf_m_tiles = mt;
-  g.pf_kb_total = kbt;
-  g.pf_kb = (int)std::max<int64_t>(1, std::min<int64_t>((kbt + S - 1) / S, budget_bytes / per_kb));
 }
 
 template <int MODE>
@@ -2181,8 +1625,7 @@ static cudaError_t launch_2sm_bn(const TmaMap& am, const TmaMap& bm, const TmaMa
   a.sub_s = 0;
   // partial last round of whole pair-tiles: if its sub-tiles fit one per pair, run them
   // instead (gate/up at 384 / 512 rows: 224 pair-tiles = 3 x 74 + 2 -> 2 x 3 / 2 x 4 sub-tiles)
-  static const bool sub_off = getenv("RT_PAIR_NO_SUB") != nullptr;
-  if (!a.ws && !sub_off && PT > n_pairs && PT % n_pairs && BN % kPairSubW == 0 &&
+  if (PT > n_pairs && PT % n_pairs && BN % kPairSubW == 0 &&
       (PT % n_pairs) * (BN / kPairSubW) <= n_pairs) {
     a.head = PT - PT % n_pairs;
     a.sub_s = BN / kPairSubW;
@@ -2233,16 +1676,15 @@ static int pair_slots(int bn) {
 int64_t gemm_sk_ws_floats() { return (int64_t)sm_count() * 2 * 256 * 128; }
 
 cudaError_t launch_gemm_epi(const bf16* w_tiled, const GemmTmaSet& x, GemmArgs g, int splits, cudaStream_t s) {
+  const GemmChoice gc = gemm_choice(g.M, g.K, g.N, g.force_bn, g.force_path);
+  const int bn = gc.bn;
   // CTA-pair kernel for the tensor-bound prefill path: every pair busy (at least one
   // pair-tile per co-resident pair) and an even number of 128-row m-tiles
-  const GemmChoice gc = gemm_choice(g.M, g.K, g.N);
   if (g.N > 128 && g.mode != EPI_ARGMAX && g.K % kBK == 0 && gc.pair) {
-    const int bn = gc.bn;
     const int m_tiles = (g.M + 127) / 128, n_tiles = (g.N + bn - 1) / bn;
     const int PT = (m_tiles / 2) * n_tiles;
-    static const int min_pt = getenv("RT_GEMM_PAIR_MIN") ? atoi(getenv("RT_GEMM_PAIR_MIN")) : 0;
     const int slots = pair_slots(bn);
-    if (m_tiles % 2 == 0 && PT >= (min_pt > 0 ? min_pt : slots)) {
+    if (m_tiles % 2 == 0 && (PT >= slots || g.force_path == GEMM_PATH_PAIR)) {
       const TmaMap* am = weight_map(w_tiled, (uint64_t)m_tiles * (g.K / kBK) * 128);
       if (am) {
         g.w = w_tiled;
@@ -2252,17 +1694,6 @@ cudaError_t launch_gemm_epi(const bf16* w_tiled, const GemmTmaSet& x, GemmArgs g
         g.l2_evict_first = 0;
         SkArgs a{};
         a.n_tiles = n_tiles;
-        // a partial last round of pair-tiles (gate/up at 256..512 rows: 224 = 3 x 74 + 2) is
-        // spread over all pairs by stream-K when the caller provides the workspace
-        // (opt-in RT_PAIR_SK=1: measured slower — the fixups of 76 split pair-tiles cost more than
-        // the balance gains, gate/up 384 / 512 rows 90.2 / 103.5 -> 89.0 / 106.7 us, and far
-        // slower with every pair-tile split at 192 / 256 rows)
-        static const int pair_sk = getenv("RT_PAIR_SK") ? atoi(getenv("RT_PAIR_SK")) : 0;
-        if (pair_sk && g.sk_ws && g.sk_cnt && PT % slots != 0 && 2 * PT <= g.sk_cnt_cap) {
-          a.ws = g.sk_ws;
-          a.cnt = g.sk_cnt;
-          a.all_sk = PT <= 2 * slots ? 1 : 0;
-        }
         switch (g.mode) {
           case EPI_STORE: return launch_2sm_mode<EPI_STORE>(*am, x, g, bn, PT, a, s);
           case EPI_QKV: return launch_2sm_mode<EPI_QKV>(*am, x, g, bn, PT, a, s);
@@ -2275,14 +1706,13 @@ cudaError_t launch_gemm_epi(const bf16* w_tiled, const GemmTmaSet& x, GemmArgs g
   }
   // hybrid data-parallel + stream-K persistent kernel for the tensor-bound prefill path
   // (N > 128 rows, more than two waves of tiles) when the caller provides its workspace
-  // (RT_NO_STREAMK=1 in the engine: one tile per CTA below)
-  if (g.sk_ws && g.sk_cnt && g.N > 128 && g.mode != EPI_ARGMAX && g.K % kBK == 0) {
+  if (g.sk_ws && g.sk_cnt && g.N > 128 && g.mode != EPI_ARGMAX && g.K % kBK == 0 &&
+      g.force_path != GEMM_PATH_SPLITK) {
     g.w = w_tiled;
     g.kb_total = g.K / kBK;
     g.m_tiles = (g.M + 127) / 128;
     g.l2_evict_first = 0;
-    const int bn = gc.bn;
-    SkArgs a;
+    SkArgs a{};
     a.n_tiles = (g.N + bn - 1) / bn;
     const int T = g.m_tiles * a.n_tiles;
     const int P = sm_count();
@@ -2290,8 +1720,7 @@ cudaError_t launch_gemm_epi(const bf16* w_tiled, const GemmTmaSet& x, GemmArgs g
     // only with a data-parallel part (T > 2 waves): measured faster there (gate/up N = 320 /
     // 384 / 512: 103 / 108 / 122 -> 89 / 95 / 116 us) and slower for all-stream-K shapes
     // (few-tile projections pay multi-contributor fixups; the cluster split-K path is better)
-    static const int sk_mode = getenv("RT_SK_MODE") ? atoi(getenv("RT_SK_MODE")) : 0;
-    const int min_t = sk_mode == 2 ? 1 : (sk_mode == 1 ? P + 1 : 2 * P + 1);
+    const int min_t = g.force_path == GEMM_PATH_STREAMK ? 1 : 2 * P + 1;
     a.all_sk = T <= 2 * P ? 1 : 0;
     if (T <= g.sk_cnt_cap && I_sk >= P && T >= min_t) {
       a.P = P;
@@ -2308,9 +1737,8 @@ cudaError_t launch_gemm_epi(const bf16* w_tiled, const GemmTmaSet& x, GemmArgs g
   }
   g.w = w_tiled;
   // weights are read once per n-tile; with several n-tiles the later ones should hit L2
-  const int n_tiles = (g.N + gc.bn - 1) / gc.bn;
+  const int n_tiles = (g.N + bn - 1) / bn;
   g.l2_evict_first = (l2_hint_enabled() && n_tiles == 1) ? 1 : 0;
-  const int bn = gc.bn;
   g.kb_total = g.K / kBK;
   g.m_tiles = (g.M + 127) / 128;
   g.n_tiles = n_tiles;
@@ -2334,9 +1762,8 @@ cudaError_t launch_gemm_epi(const bf16* w_tiled, const GemmTmaSet& x, GemmArgs g
   // the full waves of whole tiles in one launch, the remaining tiles in a second launch with
   // a cluster split-K wide enough to spread them over all SMs (gate/up at N = 256: 224 tiles =
   // 148 + 76 -> the 76 tail tiles run as 2-CTA clusters instead of a half-empty second wave)
-  static const bool tail_off = getenv("RT_NO_TAIL_SPLIT") != nullptr;
   const int P = sm_count() * (bn <= 128 ? 2 : 1);  // co-resident CTA slots
-  if (auto_split && splits == 1 && bn >= 128 && g.mode != EPI_ARGMAX && !tail_off && tiles > P && tiles % P) {
+  if (auto_split && splits == 1 && bn >= 128 && g.mode != EPI_ARGMAX && tiles > P && tiles % P) {
     const int head = (tiles / P) * P, tail = tiles - head;
     // S = the largest split that still fits the tail into one wave of the slots (a wider split
     // that spills into another wave measured slower: the cluster reduction of 96-128 KB
@@ -2349,57 +1776,6 @@ cudaError_t launch_gemm_epi(const bf16* w_tiled, const GemmTmaSet& x, GemmArgs g
     }
   }
   return launch(0, tiles, splits);
-}
-
-
-// ------------------------------------------------------------ chain host side
-int chain_grid(const int* M, const int* K, int n_jobs) {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
-  }
-  long long g = sms;
-  for (int j = 0; j < n_jobs; ++j) g = std::min(g, (long long)((M[j] + 127) / 128) * (K[j] / kBK));
-  return (int)std::max(1LL, g);
-}
-int chain_slots(int M, int K, int ctas) {
-  const int T = (M + 127) / 128, kb = K / kBK;
-  const long long I = (long long)T * kb;
-  int best = 1;
-  for (int t = 0; t < T; ++t)
-    best = std::max(best, chain::owner((long long)(t + 1) * kb - 1, I, ctas) - chain::owner((long long)t * kb, I, ctas) + 1);
-  return best;
-}
-cudaError_t launch_chain(ChainArgs& a, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_chain, cudaFuncAttributeMaxDynamicSharedMemorySize, chain::SMEM);
-    attr = true;
-  }
-  for (int j = 0; j < a.n_jobs; ++j) {
-    GemmArgs& g = a.job[j];
-    if (g.N > chain::BN || g.K % kBK || (long long)((g.M + 127) / 128) * (g.K / kBK) < a.grid)
-      return cudaErrorInvalidValue;
-    g.kb_total = g.K / kBK;
-    g.m_tiles = (g.M + 127) / 128;
-    g.l2_evict_first = l2_hint_enabled() ? 1 : 0;
-    g.pf_w = nullptr;
-  }
-  cudaLaunchConfig_t cfg{};
-  if (a.grid < 1) return cudaErrorInvalidValue;
-  cfg.gridDim = dim3(a.grid);
-  cfg.blockDim = dim3(kGemmThreads);
-  cfg.dynamicSmemBytes = chain::SMEM;
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, k_chain, (const ChainArgs)a);
 }
 
 RT_TRACE_BINDER(trace_bind_gemm)

@@ -125,5 +125,7 @@ void launch_apply_submits(const SchedParams& p, const SubmitRec* d_recs, const i
 void launch_sched_pre(const SchedParams& p, int64_t now_us, cudaStream_t s);
 void launch_sched_post(const SchedParams& p, cudaStream_t s);
 void launch_init_free_stack(int32_t* stack, int n, cudaStream_t s);
+// a12: global top-kTopK of world x kTopK candidate records (sched.cu k_merge_cand)
+void launch_merge_cand(const double* all, int world, double* merged, cudaStream_t s);
 
 }  // namespace rt

@@ -75,14 +75,7 @@ struct PrefillArgs {
   bf16* out;                // [n_rows][nq][hd]
   float* out_f32;           // nullable, indexed by global row
   float scale_log2;
-  // split-KV (set by launch_attention_prefill from the fields below): CTA (tile, head, chunk)
-  // streams chunk `chunk` of the tile's pages; partials -> ws, the last chunk's CTA merges
-  int chunks;
-  int max_seqlen;           // longest attended context of the launch (chunk plan)
-  float* ws;                // nullable: [tiles][nkv][chunks][G][16][hd + 2] fp32
-  int64_t ws_floats;
-  int* tickets;             // [tiles][nkv] zeroed, self-resetting
-  int rotate;               // set by launch_attention_prefill: per-CTA page-walk start
+  int groups;               // warp groups per CTA (0: by load, 1 / 2 forced)
 };
 void launch_attention_prefill(const PrefillArgs& a, cudaStream_t s);
 
@@ -99,6 +92,10 @@ struct GemmTmaSet {       // activation operand: one map per supported N tile
 bool make_gemm_act_maps(GemmTmaSet* out, const void* base, int K, int rows_cap);
 
 enum EpiMode { EPI_STORE = 0, EPI_ARGMAX = 1, EPI_QKV = 2, EPI_RESID = 3, EPI_SWIGLU = 4 };
+// projection kernel paths (GemmArgs::force_path; the values of rt.h RT_GEMM_PATH_*):
+// AUTO = measured dispatch; SPLITK = k_gemm_tc (cluster split-K / one tile per CTA);
+// STREAMK = k_gemm_sk (hybrid data-parallel + stream-K, N > 128); PAIR = k_gemm_2sm (CTA pairs, N > 128)
+enum GemmPath { GEMM_PATH_AUTO = 0, GEMM_PATH_SPLITK = 1, GEMM_PATH_STREAMK = 2, GEMM_PATH_PAIR = 3 };
 
 struct QkvFuse {
   const int32_t *row_task, *row_pos, *page_table;
@@ -125,12 +122,6 @@ struct GemmArgs {
   bf16* act;          // EPI_SWIGLU [N][ff]
   int ff;
   QkvFuse qkv;        // EPI_QKV
-  // L2 prefetch of the NEXT projection's weights (nullable): when its loads are issued,
-  // the producer prefetches the first pf_kb k-blocks of every CTA of the next launch
-  // (grid pf_S x pf_m_tiles, K = pf_kb_total k-blocks) so that kernel starts on L2 hits
-  // while this one drains its pipeline and runs its epilogue (HBM would idle).
-  const bf16* pf_w;
-  int pf_S, pf_m_tiles, pf_kb_total, pf_kb;
   int l2_evict_first;  // set by launch_gemm_epi: weight tiles are read once per step
   // set by launch_gemm_epi: CTA (x, y) runs linear tile tile0 + y of the GEMM's m_tiles x
   // n_tiles tiles (n fastest: the n-tiles of one m-tile are adjacent and the later ones read
@@ -141,42 +132,15 @@ struct GemmArgs {
   float* sk_ws;
   unsigned* sk_cnt;
   int sk_cnt_cap;
+  // kernel choice overrides (parity tests / the tuner; 0 = the measured dispatch): the N
+  // tile width and the path (GEMM_PATH_*)
+  int force_bn, force_path;
 };
 int64_t gemm_sk_ws_floats();
-// fill g.pf_* for a next launch of weights w [M x K] at N columns (splits <= 0: auto),
-// prefetching at most budget_bytes in total
-void gemm_set_prefetch(GemmArgs& g, const bf16* w, int M, int N, int K, int splits, int64_t budget_bytes);
 int gemm_bn(int M, int K, int N);
 int gemm_choose_splits(int M, int N, int K);   // cluster split-K factor (1..16)
 // splits <= 0: gemm_choose_splits
 cudaError_t launch_gemm_epi(const bf16* w_tiled, const GemmTmaSet& xmaps, GemmArgs g, int splits, cudaStream_t s);
-
-// ---- persistent projection chain (gemm_tc.cu): up to 4 dependent decode
-// projections (O + residual, gate/up + SwiGLU, down + residual, next layer's QKV + RoPE +
-// KV append) in ONE launch of one CTA per SM.  Every job's k-block iterations (m-tile x
-// k-block, N <= 64 rows in one 64-wide tile) are split evenly over the CTAs (stream-K);
-// weight tiles stream ahead across job boundaries (they do not depend on activations),
-// only the activation (X) loads of job j wait for job j - 1 to finish.  Partial tiles
-// go to a global workspace; the last contributor of a tile sums them in fixed order and
-// runs the fused epilogue.
-constexpr int kChainMaxJobs = 4;
-struct ChainArgs {
-  GemmArgs job[kChainMaxJobs];   // as launch_gemm_epi (w, M, N <= 64, K, mode, epilogue fields)
-  TmaMap xmap[kChainMaxJobs];    // activation operand of each job (box 64 x 64)
-  float* ws[kChainMaxJobs];      // partial tiles [m_tiles][ws_slots][64][128] fp32
-  int ws_slots[kChainMaxJobs];
-  unsigned* tile_cnt[kChainMaxJobs];  // [m_tiles] zero-initialised, self-resetting
-  unsigned* done;                // [kChainMaxJobs] cumulative finished tiles (never reset)
-  unsigned done_target[kChainMaxJobs];  // done[j] value when job j of THIS launch is complete
-  int n_jobs;
-  int grid;                      // CTAs: <= SM count and <= every job's k-block iterations
-  int pf_ahead;                  // weight k-blocks prefetched into L2 beyond the smem ring
-};
-// max contributors of one m-tile of an (M, K) job over `ctas` CTAs (the ws_slots to allocate)
-int chain_slots(int M, int K, int ctas);
-// CTAs of a chain over jobs (M[j], K[j]): min(SM count, every job's m-tile x k-block count)
-int chain_grid(const int* M, const int* K, int n_jobs);
-cudaError_t launch_chain(ChainArgs& a, cudaStream_t s);
 
 // ---- device trace buffers (common.cuh TraceScope), one binder per translation unit
 void trace_bind_model(void* rec, unsigned* n, unsigned cap);

@@ -119,8 +119,12 @@ extern "C" rt_status rt_op_pack_tiled(const void* d_src, void* d_dst, int32_t M,
 }
 
 extern "C" rt_status rt_op_gemm_tiled(const void* d_w_tiled, const void* d_x, float* d_out, int32_t M, int32_t N,
-                                      int32_t K, int32_t n_cap, int32_t splits, void* stream) {
+                                      int32_t K, int32_t n_cap, int32_t splits, int32_t path, int32_t bn,
+                                      void* stream) {
   if (M < 1 || N < 1 || K < 64 || K % 64 || n_cap < N || splits < 0 || splits > K / 64) return RT_E_INVAL;
+  if (path < RT_GEMM_PATH_AUTO || path > RT_GEMM_PATH_PAIR) return RT_E_INVAL;
+  if (bn != 0 && bn != 32 && bn != 64 && bn != 128 && bn != 160 && bn != 192 && bn != 256) return RT_E_INVAL;
+  if (bn != 0 && bn <= 128 && N > 128) return RT_E_INVAL;
   GemmTmaSet xm;
   if (!make_gemm_act_maps(&xm, d_x, K, n_cap)) return RT_E_CUDA;
   GemmArgs g{};
@@ -129,6 +133,8 @@ extern "C" rt_status rt_op_gemm_tiled(const void* d_w_tiled, const void* d_x, fl
   g.K = K;
   g.mode = EPI_STORE;
   g.out = d_out;
+  g.force_path = path;
+  g.force_bn = bn;
   // stream-K path for N > 128 (as in the engine): a process-wide workspace on first use
   static float* sk_ws = nullptr;
   static unsigned* sk_cnt = nullptr;
@@ -136,7 +142,7 @@ extern "C" rt_status rt_op_gemm_tiled(const void* d_w_tiled, const void* d_x, fl
   static std::mutex sk_mu;  // callers on several host threads share the workspace allocation
   std::lock_guard<std::mutex> lock(sk_mu);
   const int need = ((M + 127) / 128) * ((N + 159) / 160);
-  if (N > 128 && splits <= 0 && getenv("RT_NO_STREAMK") == nullptr) {
+  if (N > 128 && splits <= 0) {
     if (!sk_ws && cudaMalloc(&sk_ws, (size_t)gemm_sk_ws_floats() * 4) != cudaSuccess) return RT_E_CUDA;
     if (need > sk_cap) {
       if (sk_cnt) cudaFree(sk_cnt);
@@ -194,5 +200,11 @@ extern "C" rt_status rt_op_priority(const int64_t* d_trde, const int32_t* d_k, c
                                     double* d_pri, void* stream) {
   if (n < 0 || g_us <= 0 || eps_l_us <= 0) return RT_E_INVAL;
   launch_priority_batch(d_trde, d_k, d_alpha, d_beta, n, g_us, net_us, eps_l_us, d_pri, (cudaStream_t)stream);
+  return last_launch();
+}
+
+extern "C" rt_status rt_op_merge_candidates(const double* d_all, int32_t world, double* d_merged, void* stream) {
+  if (!d_all || !d_merged || world < 1 || world > 8) return RT_E_INVAL;
+  launch_merge_cand(d_all, world, d_merged, (cudaStream_t)stream);
   return last_launch();
 }

@@ -17,7 +17,8 @@ RT_CLOCK_VIRTUAL, RT_CLOCK_WALL = 0, 1
 RT_POLICY_PUD, RT_POLICY_FCFS, RT_POLICY_EDF = 0, 1, 2
 RT_STOP_NONE, RT_STOP_EOS, RT_STOP_MAXNEW, RT_STOP_SKILL, RT_STOP_CAP = 0, 1, 2, 3, 4
 RT_FLAG_NO_MODEL, RT_FLAG_KEEP_LOGITS, RT_FLAG_CAPTURE, RT_FLAG_TIMING, RT_FLAG_FORCE_EXCHANGE = 1, 2, 4, 8, 16
-RT_FLAG_GRAPHS, RT_FLAG_TRACE = 32, 64
+RT_FLAG_TRACE = 64
+RT_GEMM_PATH_AUTO, RT_GEMM_PATH_SPLITK, RT_GEMM_PATH_STREAMK, RT_GEMM_PATH_PAIR = 0, 1, 2, 3
 (RT_DUMP_TASKS, RT_DUMP_PAGE_TABLES, RT_DUMP_ROUND, RT_DUMP_LOGITS, RT_DUMP_HIDDEN, RT_DUMP_CAPTURE_Q,
  RT_DUMP_CAPTURE_O, RT_DUMP_ROWS, RT_DUMP_KV_LAYER, RT_DUMP_FREE_STACK, RT_DUMP_TASK_SLOTS,
  RT_DUMP_MERGED, RT_DUMP_TRACE, RT_DUMP_HOST_PAGE_TABLES, RT_DUMP_HOST_FREE_STACK) = range(1, 16)
@@ -25,13 +26,14 @@ RT_FLAG_GRAPHS, RT_FLAG_TRACE = 32, 64
 TRACE_DTYPE = np.dtype([("grid", "<u8"), ("kind", "<u4"), ("smid", "<u4"), ("t_entry", "<u8"),
                         ("t_ready", "<u8"), ("t_aux", "<u8"), ("t_exit", "<u8")])
 TRACE_KINDS = {1: "gemm", 2: "attn", 3: "norm", 4: "embed", 5: "sched_pre", 6: "sched_post", 7: "gather",
-               8: "argmax", 9: "merge", 10: "attn_prefill", 11: "chain"}
+               8: "argmax", 9: "merge", 10: "attn_prefill"}
 
 EXPORTED = ["rt_create", "rt_destroy", "rt_submit_request", "rt_register_prefix", "rt_step", "rt_poll_segment", "rt_last_round",
             "rt_sync", "rt_get_stats", "rt_reset_stats", "rt_debug_dump", "rt_last_error", "rt_version",
             "rt_op_paged_attention", "rt_op_attention_ws_bytes", "rt_op_kv_write", "rt_op_kv_read", "rt_op_kv_swap",
             "rt_op_gemm", "rt_op_lm_argmax", "rt_op_init_weights", "rt_op_priority", "rt_mark", "rt_elapsed_ms",
-            "rt_nccl_unique_id", "rt_op_pack_tiled", "rt_op_gemm_tiled", "rt_set_timing"]
+            "rt_nccl_unique_id", "rt_op_pack_tiled", "rt_op_gemm_tiled", "rt_set_timing",
+            "rt_op_merge_candidates"]
 
 
 class RtError(RuntimeError):
@@ -64,7 +66,7 @@ class rt_config(C.Structure):
         ("flags", C.c_int32), ("capture_layer", C.c_int32), ("seg_mode", C.c_int32), ("wcet_off", C.c_int32),
         ("host_pages", C.c_int32), ("swap_us_per_page", C.c_int32),
         ("stop_grammar", C.c_int32), ("tok_class", C.c_void_p), ("skill_base_us", C.c_void_p),
-        ("skill_unit_us", C.c_void_p), ("word_us", C.c_int32),
+        ("skill_unit_us", C.c_void_p), ("word_us", C.c_int32), ("gemm_path", C.c_int32),
     ]
 
 
@@ -129,7 +131,8 @@ def lib():
     L.rt_elapsed_ms.argtypes = [vp, C.POINTER(C.c_double)]
     L.rt_nccl_unique_id.argtypes = [vp]
     L.rt_op_pack_tiled.argtypes = [vp, vp, i32, i32, vp]
-    L.rt_op_gemm_tiled.argtypes = [vp, vp, vp, i32, i32, i32, i32, i32, vp]
+    L.rt_op_gemm_tiled.argtypes = [vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, vp]
+    L.rt_op_merge_candidates.argtypes = [vp, i32, vp, vp]
     for f in EXPORTED:
         if f not in ("rt_last_error", "rt_version", "rt_op_attention_ws_bytes"):
             getattr(L, f).restype = C.c_int32
@@ -151,7 +154,7 @@ class Engine:
     """One engine per GPU/process (C ABI rt_engine)."""
 
     def __init__(self, shape, params, vocab, seed=0, flags=0, device=0, rank=0, world=1, nccl_id=None,
-                 init_std=0.02, capture_layer=0, max_rows_per_forward=0, kv_pool_bytes=0):
+                 init_std=0.02, capture_layer=0, max_rows_per_forward=0, kv_pool_bytes=0, gemm_path=0):
         L = lib()
         c = rt_config()
         c.rank, c.world, c.device = rank, world, device
@@ -185,6 +188,7 @@ class Engine:
         c.seg_mode, c.wcet_off = p.seg_mode, p.wcet_off
         c.host_pages, c.swap_us_per_page = p.host_pages, p.swap_us_per_page
         c.stop_grammar, c.word_us = p.stop_grammar, p.word_us
+        c.gemm_path = gemm_path
         if getattr(vocab, "tok_class", None) is not None:   # synth.grammar.GrammarVocab (NEXT-4)
             self._cls = np.ascontiguousarray(vocab.tok_class, dtype=np.int16)
             self._sbase = np.ascontiguousarray(vocab.skill_base_us, dtype=np.int32)
@@ -406,8 +410,9 @@ def pack_tiled(w, out, M, K, stream=None):
     _check(lib().rt_op_pack_tiled(_ptr(w), _ptr(out), M, K, _stream(stream)))
 
 
-def gemm_tiled(wt, x, out, M, N, K, n_cap, splits=0, stream=None):
-    _check(lib().rt_op_gemm_tiled(_ptr(wt), _ptr(x), _ptr(out), M, N, K, n_cap, splits, _stream(stream)))
+def gemm_tiled(wt, x, out, M, N, K, n_cap, splits=0, stream=None, path=RT_GEMM_PATH_AUTO, bn=0):
+    _check(lib().rt_op_gemm_tiled(_ptr(wt), _ptr(x), _ptr(out), M, N, K, n_cap, splits, path, bn,
+                                  _stream(stream)))
 
 
 def lm_argmax(w, x, M, N, K, n_cap, tok, logits=None, ws=None, stream=None):
@@ -426,3 +431,8 @@ def init_weights(out, n, seed, tensor_id, sigma=0.02, stream=None):
 def priority(trde, k, alpha, beta, g_us, net_us, eps_l_us, out, stream=None):
     _check(lib().rt_op_priority(_ptr(trde), _ptr(k), _ptr(alpha), _ptr(beta), int(k.shape[0]), g_us, net_us,
                                 eps_l_us, _ptr(out), _stream(stream)))
+
+
+def merge_candidates(all_cand, world, merged, stream=None):
+    """all_cand: float64 cuda tensor [world][16][4]; merged: float64 cuda tensor [16][4]."""
+    _check(lib().rt_op_merge_candidates(_ptr(all_cand), int(world), _ptr(merged), _stream(stream)))

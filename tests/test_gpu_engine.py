@@ -257,36 +257,18 @@ def test_submit_errors(rt):
 
 
 # ------------------------------------------------------------- model parity
-@pytest.mark.parametrize("graphs,chain,streamk,pf_chunks", [(False, False, True, 0), (True, False, True, 0),
-                                                            (False, True, True, 0), (False, False, False, 0),
-                                                            (False, False, True, 3)])
-def test_tiny_model_e2e_and_per_op(rt, graphs, chain, streamk, pf_chunks, monkeypatch):
-    """C1 end to end against the oracle; chain=True runs the decode projections through the
-    opt-in persistent projection chain (RT_CHAIN=1; 2 CTAs at these dims, so both the
-    whole-tile and the partial-tile fixup paths run); streamk=False disables the hybrid
-    DP + stream-K prefill projections (RT_NO_STREAMK=1, one tile per CTA); pf_chunks=3
-    forces the split-KV path of the prefill attention (3 page chunks per tile, merged by the
-    last chunk's CTA)."""
-    if pf_chunks:
-        # the chunk plan reads RT_PF_CHUNKS once per process: run in a fresh interpreter
-        import subprocess, sys, os
-        env = dict(os.environ, RT_PF_CHUNKS=str(pf_chunks))
-        r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", __file__ + "::test_tiny_model_e2e_and_per_op",
-                            "-k", "False-False-True-0", "-m", "gpu", "-p", "no:cacheprovider"],
-                           env=env, capture_output=True, text=True, timeout=600)
-        assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
-        return
-    for var, on in (("RT_CHAIN", chain), ("RT_NO_STREAMK", not streamk)):
-        if on:
-            monkeypatch.setenv(var, "1")
-        else:
-            monkeypatch.delenv(var, raising=False)
+@pytest.mark.parametrize("gemm_path", [0, 1, 2, 3])
+def test_tiny_model_e2e_and_per_op(rt, gemm_path):
+    """C1 end to end against the oracle, through every projection kernel path (rt_config.gemm_path:
+    the measured dispatch, split-K / one tile per CTA, hybrid stream-K, CTA pairs — the prefill
+    rounds' N > 128 rows take the forced path wherever it applies)."""
     shape = MODEL_SHAPES["tiny"]
     v = make_vocab(shape.vocab)
     p = engine_params("paper-4090", max_batch=4, max_tasks=64, max_ctx=256, n_pages=64)
     reqs = compose_workload(4, 1.0, 2, range(1, 9), 30.0, 0, v, prompt_len_range=(40, 64), max_requests=12)
-    flags = rt.RT_FLAG_KEEP_LOGITS | rt.RT_FLAG_CAPTURE | (rt.RT_FLAG_GRAPHS if graphs else 0)
-    eng, ora = make_pair(rt, v, p, shape=shape, seed=3, flags=flags, model=True, capture_layer=1)
+    flags = rt.RT_FLAG_KEEP_LOGITS | rt.RT_FLAG_CAPTURE
+    eng, ora = make_pair(rt, v, p, shape=shape, seed=3, flags=flags, model=True, capture_layer=1,
+                         gemm_path=gemm_path)
     submit_both(eng, ora, reqs)
     worst_logit = worst_attn = worst_lm = 0.0
     lm = OW.matrix(3, OW.TID_LM, range(shape.vocab), shape.d_model)
@@ -578,50 +560,6 @@ def test_tiny_model_shared_prefix_parity(rt):
     assert eng.poll() == ora.poll()
 
 
-def test_projection_chain_matches_per_projection_launches(rt, monkeypatch):
-    """The opt-in persistent projection chain (RT_CHAIN=1: O, gate/up, down, next QKV in one
-    launch, stream-K split with a global partial-tile fixup) against one launch per projection, at 8B layer
-    dims (2 layers, 64 decode rows): same scripted rounds, logits and the layer-1 q (produced
-    by layer 0's chain) agree to fp32 summation-order / bf16 rounding-flip level; the tiny C1
-    model's end-to-end oracle parity (test_tiny_model_e2e_and_per_op[chain]) runs through the
-    chain too (grid = min(SMs, iterations) = 2 CTAs there)."""
-    from synth.configs import ModelShape
-    s8 = MODEL_SHAPES["llama3-8b"]
-    shape = ModelShape("chain", 2, s8.d_model, s8.n_q_heads, s8.n_kv_heads, s8.head_dim, s8.d_ff, s8.vocab)
-    v = make_vocab(shape.vocab)
-    p = engine_params("b200-roofline", max_batch=64, max_tasks=128, max_ctx=256, n_pages=64 * 16)
-    from synth.traces import make_trace
-    out = {}
-    for mode in ("chain", "per_projection"):
-        if mode == "chain":
-            monkeypatch.setenv("RT_CHAIN", "1")
-        else:
-            monkeypatch.delenv("RT_CHAIN", raising=False)
-        eng = rt.Engine(shape, p, v, seed=21, flags=rt.RT_FLAG_KEEP_LOGITS | rt.RT_FLAG_CAPTURE, capture_layer=1,
-                        max_rows_per_forward=4096)
-        for a in range(64):
-            tr = make_trace(1 + a % 8, v, seed=a, prompt_len=40 + a % 17, plan_len=40)
-            eng.submit(a, tr.prompt, 0, tr.ert_us, tr.alpha, tr.beta, 90000, script=tr.plan)
-        logs = []
-        for _ in range(12):
-            info = eng.step()
-            if info["n_running"] == 64 and info["n_prefill_rows"] == 0:
-                lg = eng.dump(rt.RT_DUMP_LOGITS, np.float32).reshape(64, -1)
-                rows = eng.dump(rt.RT_DUMP_ROWS, np.int32).reshape(-1, 3)
-                q = eng.dump(rt.RT_DUMP_CAPTURE_Q, np.float32).reshape(len(rows), -1)
-                logs.append((lg.copy(), q.copy()))
-        out[mode] = (logs, eng.poll())
-        eng.close()
-    (lc, sc), (lp, sp) = out["chain"], out["per_projection"]
-    assert sc == sp  # scripted streams: identical segments
-    assert len(lc) == len(lp) and len(lc) >= 3
-    worst_l = max(float(np.abs(a[0] - b[0]).max()) for a, b in zip(lc, lp))
-    worst_q = max(float(np.abs(a[1] - b[1]).max()) for a, b in zip(lc, lp))
-    scale = max(float(np.abs(b[0]).max()) for b in lp)
-    assert worst_q < 5e-2, worst_q          # q of layer 1 (bf16, |q| ~ O(1))
-    assert worst_l < 2e-2 * max(1.0, scale), (worst_l, scale)
-
-
 @pytest.mark.parametrize("grammar", [1, 2, 3])
 def test_sched_parity_stop_grammars(rt, grammar):
     """NEXT-4 on the device: the DFA / chat stop checker against the oracle's regex over the
@@ -648,54 +586,6 @@ def test_sched_parity_stop_grammars(rt, grammar):
         assert a == b
     n, segs = lockstep(eng, ora, max_rounds=20000, check_every=7)
     assert sum(1 for s in segs if s["reason"] == 3) > 20
-
-
-@pytest.mark.parametrize("prompt_len,pair_bn", [(200, 0), (64, 0), (160, 0), (96, 192)])
-def test_prefill_projections_hybrid_streamk_match_per_tile(rt, monkeypatch, prompt_len, pair_bn):
-    """The hybrid data-parallel + stream-K prefill projections (k_gemm_sk: > 2 waves of
-    tiles, here gate/up and QKV of a 1600-row prefill at 8B dims) against one tile per CTA
-    (RT_NO_STREAMK=1): same scripted rounds, the logits of the prefill round (token 0 of every
-    request) and of later decode rounds agree to fp32 summation-order level.  "pair" runs the
-    CTA-pair kernel (cta_group::2) for every eligible projection; 512 prompt rows put gate/up's
-    partial last round into 64-column sub-tiles (SwiGLU epilogue), 1280 rows the O and down
-    projections' (residual epilogue), 1600 rows the 160-wide pair tiles; 768 rows with 192-wide
-    pair tiles forced (RT_GEMM_BN) the QKV projection's (RoPE + KV-append epilogue)."""
-    from synth.configs import ModelShape
-    s8 = MODEL_SHAPES["llama3-8b"]
-    shape = ModelShape("sk", 2, s8.d_model, s8.n_q_heads, s8.n_kv_heads, s8.head_dim, s8.d_ff, s8.vocab)
-    v = make_vocab(shape.vocab)
-    p = engine_params("b200-roofline", max_batch=8, max_tasks=16, max_ctx=512, n_pages=8 * 32)
-    from synth.traces import make_trace
-    out = {}
-    for mode in ("hybrid", "per_tile", "pair"):
-        if mode == "per_tile":
-            monkeypatch.setenv("RT_NO_STREAMK", "1")
-        else:
-            monkeypatch.delenv("RT_NO_STREAMK", raising=False)
-        # CTA-pair kernel (cta_group::2) for every eligible projection, or single-SM kernels only
-        monkeypatch.setenv("RT_GEMM_PAIR", "1" if mode == "pair" else "0")
-        if mode == "pair" and pair_bn:
-            monkeypatch.setenv("RT_GEMM_BN", str(pair_bn))
-        else:
-            monkeypatch.delenv("RT_GEMM_BN", raising=False)
-        eng = rt.Engine(shape, p, v, seed=23, flags=rt.RT_FLAG_KEEP_LOGITS, max_rows_per_forward=4096)
-        for a in range(8):
-            tr = make_trace(1 + a, v, seed=a, prompt_len=prompt_len, plan_len=12)
-            eng.submit(a, tr.prompt, 0, tr.ert_us, tr.alpha, tr.beta, 90000, script=tr.plan)
-        logs = []
-        for _ in range(4):
-            info = eng.step()
-            B = info["n_running"]
-            logs.append((info["n_prefill_rows"], eng.dump(rt.RT_DUMP_LOGITS, np.float32).reshape(B, -1).copy()))
-        out[mode] = logs
-        eng.close()
-    assert out["hybrid"][0][0] == 8 * prompt_len
-    for other in ("hybrid", "pair"):
-        for rnd, ((na, la), (nb, lb)) in enumerate(zip(out[other], out["per_tile"])):
-            assert na == nb
-            scale = max(1.0, float(np.abs(lb).max()))
-            err = float(np.abs(la - lb).max())
-            assert err < 2e-2 * scale, (other, rnd, err, scale, np.argwhere(np.abs(la - lb) > 2e-2 * scale)[:8])
 
 
 def test_set_timing_toggles_event_stats_only(rt):
@@ -732,8 +622,8 @@ def test_set_timing_toggles_event_stats_only(rt):
     assert all(np.array_equal(a, b) for a, b in zip(outs[0][1], outs[1][1]))
 
 
-@pytest.mark.parametrize("mode", ["hybrid", "per_tile", "pair"])
-def test_prefill_and_decode_rounds_bitwise_deterministic(rt, monkeypatch, mode):
+@pytest.mark.parametrize("gemm_path", [0, 1, 2, 3])
+def test_prefill_and_decode_rounds_bitwise_deterministic(rt, gemm_path):
     """Run-to-run determinism of every projection path (the cluster split-K in pull mode once
     let a peer read a half-parked partial tile: logits differed by up to 0.19 between identical
     runs; tools/determinism_check.py): the same scripted rounds twice give bit-identical
@@ -744,14 +634,10 @@ def test_prefill_and_decode_rounds_bitwise_deterministic(rt, monkeypatch, mode):
     shape = ModelShape("det", 2, s8.d_model, s8.n_q_heads, s8.n_kv_heads, s8.head_dim, s8.d_ff, s8.vocab)
     v = make_vocab(shape.vocab)
     p = engine_params("b200-roofline", max_batch=8, max_tasks=16, max_ctx=512, n_pages=8 * 32)
-    monkeypatch.setenv("RT_GEMM_PAIR", "1" if mode == "pair" else "0")
-    if mode == "per_tile":
-        monkeypatch.setenv("RT_NO_STREAMK", "1")
-    else:
-        monkeypatch.delenv("RT_NO_STREAMK", raising=False)
     runs = []
     for _ in range(2):
-        eng = rt.Engine(shape, p, v, seed=23, flags=rt.RT_FLAG_KEEP_LOGITS, max_rows_per_forward=4096)
+        eng = rt.Engine(shape, p, v, seed=23, flags=rt.RT_FLAG_KEEP_LOGITS, max_rows_per_forward=4096,
+                        gemm_path=gemm_path)
         for a in range(8):
             tr = make_trace(1 + a, v, seed=a, prompt_len=64, plan_len=12)
             eng.submit(a, tr.prompt, 0, tr.ert_us, tr.alpha, tr.beta, 90000, script=tr.plan)

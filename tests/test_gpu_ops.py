@@ -14,6 +14,7 @@ pytestmark = pytest.mark.gpu
 from oracle import weights as OW                      # noqa: E402
 from oracle.model import paged_attention as o_attn   # noqa: E402
 from oracle.priority import priority as o_priority   # noqa: E402
+from oracle.merge import merge_rank_topk            # noqa: E402
 
 
 @pytest.fixture(scope="module")
@@ -85,16 +86,48 @@ def test_gemm_tcgen05(rt, M, N, K, splits):
     assert err < 1e-3 * max(1.0, (K / 512) ** 0.5), err
 
 
+def _gemm_tiled_case(rt, M, N, K, path, bn=0, splits=0):
+    """The engine's layout (rt_op_pack_tiled) through one forced kernel path, vs fp64."""
+    g = torch.Generator().manual_seed(M * 7 + N + path)
+    W = (torch.randn(M, K, generator=g) * 0.05).to(torch.bfloat16)
+    n_cap = ((N + 255) // 256) * 256
+    X = torch.zeros(n_cap, K, dtype=torch.bfloat16)
+    X[:N] = torch.randn(N, K, generator=g).to(torch.bfloat16)
+    Wd, Xd = W.cuda(), X.cuda()
+    Wt = torch.zeros(((M + 127) // 128) * 128 * K, dtype=torch.bfloat16, device="cuda")
+    rt.pack_tiled(Wd, Wt, M, K)
+    out = torch.full((N, M), float("nan"), device="cuda")
+    rt.gemm_tiled(Wt, Xd, out, M, N, K, n_cap, splits, path=path, bn=bn)
+    torch.cuda.synchronize()
+    ref = X[:N].double() @ W.double().T
+    err = (out.double().cpu() - ref).abs().max().item()
+    assert err < 1e-3 * max(1.0, (K / 512) ** 0.5), err
+
+
 @pytest.mark.parametrize("M,N,K", [(28672, 320, 512), (28672, 512, 4096), (19200, 200, 512), (38400, 150, 256),
-                                   (9728, 300, 512), (20480, 161, 1024), (6144, 1600, 1024), (4096, 1600, 2048)])
-def test_gemm_cta_pair(rt, M, N, K, monkeypatch):
-    """CTA-pair projections (tcgen05.mma.cta_group::2, RT_GEMM_PAIR=1): eligible shapes only
-    (N > 128, an even number of 128-row m-tiles, >= 74 pair-tiles: one per co-resident pair);
-    ragged N (161, 200, 300) leaves the second CTA's half of the last n-tile partly empty."""
-    monkeypatch.setenv("RT_GEMM_PAIR", "1")
-    bn = min((160, 192, 256), key=lambda b: (-(-N // b) * b, -(-N // b)))
-    assert (M // 128) % 2 == 0 and (M // 256) * -(-N // bn) >= 74
-    test_gemm_tcgen05(rt, M, N, K, 0)
+                                   (9728, 300, 512), (20480, 161, 1024), (6144, 1600, 1024), (4096, 1600, 2048),
+                                   (6144, 256, 4096), (512, 200, 256)])
+def test_gemm_cta_pair(rt, M, N, K):
+    """CTA-pair projections (tcgen05.mma.cta_group::2, RT_GEMM_PATH_PAIR): N > 128 and an even
+    number of 128-row m-tiles; ragged N (161, 200, 300) leaves the second CTA's half of the last
+    n-tile partly empty; fewer pair-tiles than co-resident pairs (6144 x 256, 512 x 200) and a
+    partial last round (sub-tiles) are covered."""
+    assert (M // 128) % 2 == 0
+    _gemm_tiled_case(rt, M, N, K, rt.RT_GEMM_PATH_PAIR)
+
+
+@pytest.mark.parametrize("M,N,K,bn", [(28672, 256, 512, 256), (6144, 161, 1024, 160), (4096, 384, 2048, 192),
+                                      (1024, 300, 768, 0), (384, 150, 512, 0)])
+def test_gemm_streamk(rt, M, N, K, bn):
+    """Hybrid data-parallel + stream-K (k_gemm_sk) forced for any tile count (all-stream-K
+    at <= 2 waves: multi-contributor fixups)."""
+    _gemm_tiled_case(rt, M, N, K, rt.RT_GEMM_PATH_STREAMK, bn=bn)
+
+
+@pytest.mark.parametrize("M,N,K,bn", [(28672, 256, 512, 256), (6144, 200, 1024, 0), (4096, 384, 2048, 192)])
+def test_gemm_splitk_wide(rt, M, N, K, bn):
+    """k_gemm_tc forced on prefill-sized N (one tile per CTA / wave-tail split)."""
+    _gemm_tiled_case(rt, M, N, K, rt.RT_GEMM_PATH_SPLITK, bn=bn)
 
 
 @pytest.mark.parametrize("M,N,K", [(512, 4, 128), (128256, 64, 1024), (1000, 33, 256)])
@@ -202,3 +235,39 @@ def test_kv_swap_roundtrip(rt):
     keep = [p for p in range(n_pages) if p not in (10, 11, 4)]
     for p in keep:
         assert torch.equal(pool[:, p * blk:(p + 1) * blk], orig[:, p * blk:(p + 1) * blk])
+
+
+@pytest.mark.parametrize("world", [1, 2, 3, 5, 8])
+def test_merge_candidates_matches_oracle(rt, world):
+    """a12 device merge (rt_op_merge_candidates, the kernel every rank runs on the allgathered
+    candidates) against oracle c13 on G synthetic rank buffers: per-rank top-16 lists sorted by
+    (Pri desc, arrival asc, id asc) with ties in Pri and in (Pri, arrival) across ranks, empty
+    slots (rid -1) at the end of short lists, and -0.0 canonicalised upstream."""
+    K = 16
+    for trial in range(20):
+        rng = np.random.default_rng(world * 100 + trial)
+        lists, rid = [], 0
+        for r in range(world):
+            n = int(rng.integers(0, K + 1)) if trial % 3 else K
+            pri = rng.choice([13.7174, 15.6495, 202.02, -4400.0, 1.0], size=n) if trial % 2 else rng.normal(0, 50, n)
+            arr = rng.choice([0, 100000, 200000], size=n) if trial % 2 else rng.integers(0, 10 ** 7, n)
+            recs = []
+            for i in range(n):
+                recs.append((float(pri[i]), float(arr[i]), float(rid * world + r), float(r)))
+                rid += 1
+            recs.sort(key=lambda x: (-x[0], x[1], x[2]))
+            lists.append(recs)
+        buf = np.zeros((world, K, 4))
+        buf[:, :, 2] = -1.0
+        for r, recs in enumerate(lists):
+            if recs:
+                buf[r, :len(recs)] = np.array(recs)
+        d_all = torch.from_numpy(buf).cuda()
+        merged = torch.full((K, 4), float("nan"), dtype=torch.float64, device="cuda")
+        rt.merge_candidates(d_all, world, merged)
+        torch.cuda.synchronize()
+        got = merged.cpu().numpy()
+        ref = merge_rank_topk(lists, K)
+        n_valid = len(ref)
+        assert np.array_equal(got[:n_valid], np.array(ref).reshape(n_valid, 4)), (world, trial)
+        assert (got[n_valid:, 2] < 0).all()

@@ -12,23 +12,29 @@ sys.path.insert(0, ROOT)
 import torch  # noqa: E402
 import bench  # noqa: E402
 from synth import MODEL_SHAPES, make_vocab, engine_params  # noqa: E402
+from synth.traces import make_trace  # noqa: E402
 from paper_2412_18695_b200 import rt  # noqa: E402
 
 
-def setup(B, flags=0):
-    """The bench's steady state: B drone agents resident, decode-only rounds."""
+def setup(B, flags=0, config="c2"):
+    """The bench's steady state: B agents resident, decode-only rounds.  config "c2": drone
+    agents (prompt 1300); "c3": half drone, half robot arm (prompt 2884), SURVEY §8(d) C3."""
     shape = MODEL_SHAPES["llama3-8b"]
     vocab = make_vocab(shape.vocab)
-    n_pages = B * 3 * ((bench.MAX_CTX + 15) // 16) // 2
-    p = engine_params("b200-roofline", max_batch=B, max_tasks=4 * B, max_ctx=bench.MAX_CTX, n_pages=n_pages,
+    max_ctx = bench.MAX_CTX if config == "c2" else 4096
+    n_pages = B * 3 * ((max_ctx + 15) // 16) // 4 + 64
+    p = engine_params("b200-roofline", max_batch=B, max_tasks=4 * B, max_ctx=max_ctx, n_pages=n_pages,
                       clock_mode=1)
     eng = rt.Engine(shape, p, vocab, seed=1234, flags=flags, max_rows_per_forward=8192)
     t0 = time.perf_counter()
     now = lambda: int((time.perf_counter() - t0) * 1e6)  # noqa: E731
     for j in range(B):
-        tr = bench.drone_request(vocab, j, 0, 0, plan_len=64)
+        if config == "c2" or j % 2 == 0:
+            tr = bench.drone_request(vocab, j, 0, 0, plan_len=64)
+        else:
+            tr = make_trace(9 + (j // 2) % 3, vocab, seed=j, plan_len=64)
         eng.submit(j, tr.prompt, now(), tr.ert_us, tr.alpha, tr.beta, p.g_us, script=tr.plan)
-    for _ in range(50):
+    for _ in range(400):
         info = eng.step(now())
         if info["n_running"] == B and info["n_prefill_rows"] == 0:
             break

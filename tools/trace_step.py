@@ -140,10 +140,11 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--agents", type=int, default=bench.AGENTS_PER_GPU)
+    ap.add_argument("--config", default="c2", choices=["c2", "c3"])
     ap.add_argument("--json", default=None)
     ap.add_argument("--raw", default=None, help="save the raw per-CTA records (.npy)")
     a = ap.parse_args()
-    eng, now = profile_step.setup(a.agents, flags=rt.RT_FLAG_TRACE)
+    eng, now = profile_step.setup(a.agents, flags=rt.RT_FLAG_TRACE, config=a.config)
     eng.reset_stats()
     for _ in range(a.steps):
         eng.step(now())
