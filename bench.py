@@ -4,11 +4,16 @@
 Contract (driver): `python bench.py --gpus N --steps K --warmup W [--impl reference]`,
 one process per GPU under torchrun for N > 1; rank 0 prints ONE JSON line.
 
-Workload = BASELINE.json configs[1] ("64 drone agents, Llama-3-8B-shaped random-init
-bf16, Poisson arrivals, 1 B200"), per GPU (weak scaling: agents a -> rank a mod N).
-A step = one rt_step round: device scheduler (ingest, Eq. 4 scoring, admission,
-paging, batch assembly) + 32-layer decode forward (tcgen05 projections, paged
-attention) + lm_head/argmax + stop checker + retire/suspend + segment ring.
+Workload (default) = BASELINE.json configs[2], C3: "256 mixed drone + robot-arm agents,
+Llama-3-8B-shaped, varying job parallel degree, 1 B200" — the largest single-GPU config,
+per GPU (weak scaling: agents a -> rank a mod N, replicas.partition).  Half the agents are
+drones (traces 1-8, 1300-token prompts), half robot arms (traces 9-11,
+2884-token prompts).  `--workload C2` (configs[1], 64 drone agents) and
+`--workload C4` (configs[3]'s weak-scaling slice, 128 agents of traces 1-11 per GPU) run
+the same measurement on the other configs.
+A step = one rt_step round: device scheduler (ingest, Eq. 4 scoring, admission, paging,
+batch assembly) + 32-layer decode forward (tcgen05 projections, paged attention) +
+lm_head/argmax + stop checker + retire/suspend + segment ring.
 
 value : decode tokens/s of the timed rounds, every running request's KV context
         resident in HBM when the timed region starts (prompts prefilled in setup),
@@ -33,18 +38,44 @@ sys.path.insert(0, ROOT)
 from synth import MODEL_SHAPES, make_vocab, engine_params  # noqa: E402
 from synth.traces import make_trace, system_prefix, TRACE_CLASSES  # noqa: E402
 
-AGENTS_PER_GPU = 64
-PROMPT = 1300            # drone prompt (170.35 MB / 128 KiB per token)
-PREFIX = 1216            # its fixed, server-stored part (DESIGN R-PFX): 76 pages
-MAX_CTX = 2048
 SEG_BYTES = 560          # sizeof(rt_segment): ids, range, counts, times + 128 token slots
-TRACE_POOL = list(range(1, 9))   # drone traces 1-8 (tab:task_list)
+# fixed, server-stored prompt parts (DESIGN R-PFX): whole pages
+PREFIX = {"drone": 1216, "arm": 2800}
+PROMPT = {"drone": 1300, "arm": 2884}
+WORKLOADS = {
+    # name: (agents per GPU, trace pool chooser, max_ctx, BASELINE.json config)
+    "C3": dict(agents=256, max_ctx=4096, cfg="configs[2]: 256 mixed drone + robot-arm agents per GPU "
+               "(128 drone traces 1-8, prompt 1300 + 128 arm traces 9-11, prompt 2884)"),
+    "C2": dict(agents=64, max_ctx=2048, cfg="configs[1]: 64 drone agents per GPU (traces 1-8, prompt 1300)"),
+    "C4": dict(agents=128, max_ctx=4096, cfg="configs[3] weak-scaling slice: 128 agents per GPU, traces 1-11 "
+               "(drone prompt 1300, arm prompt 2884)"),
+}
+
+
+def trace_id(workload, agent, ordinal, seed):
+    """The trace an agent's ordinal-th request runs (seeded, no method arithmetic)."""
+    if workload == "C2":
+        return 1 + (agent * 7 + ordinal * 3 + seed) % 8
+    if workload == "C3":   # even agents drones, odd agents arms
+        return 1 + (agent * 7 + ordinal * 3 + seed) % 8 if agent % 2 == 0 else 9 + (agent // 2 + ordinal + seed) % 3
+    return 1 + (agent * 5 + ordinal * 3 + seed) % 11
+
+
+def robot(tid):
+    return "arm" if TRACE_CLASSES[tid] == "arm" else "drone"
+
+
+def agent_request(workload, vocab, agent, ordinal, seed, plan_len=None, prefixes=None):
+    tid = trace_id(workload, agent, ordinal, seed)
+    r = robot(tid)
+    return make_trace(tid, vocab, seed=seed * 1000003 + agent * 9973 + ordinal, prompt_len=PROMPT[r],
+                      plan_len=plan_len, prefix=None if prefixes is None else prefixes[r])
 
 
 def ncu_traffic(kernel):
     """dram__bytes_read + write per launch of `kernel` from the committed ncu capture."""
     try:
-        for d in json.load(open(os.path.join(ROOT, "profiles", "r01_ncu_attention_full.json"))):
+        for d in json.load(open(os.path.join(ROOT, NCU_ATTN_SOURCE.split()[0]))):
             if kernel in d["Kernel Name"]:
                 rd = float(d["dram__bytes_read.sum"].split()[0])
                 wr = float(d["dram__bytes_write.sum"].split()[0])
@@ -131,34 +162,35 @@ class ClockSampler:
                 "source": "nvml 5 ms poll"}
 
 
-# ------------------------------------------------------------------ workload
-def drone_request(vocab, agent, ordinal, seed, plan_len=None, prefix=None):
-    tid = TRACE_POOL[(agent * 7 + ordinal * 3 + seed) % len(TRACE_POOL)]
-    tr = make_trace(tid, vocab, seed=seed * 1000003 + agent * 9973 + ordinal, prompt_len=PROMPT,
-                    plan_len=plan_len, prefix=prefix)
-    return tr
+# ------------------------------------------------------------------ ours
+def engine_setup(args, rank, world, dist, flags=0):
+    import torch
+    from paper_2412_18695_b200 import rt
+    from paper_2412_18695_b200 import replicas as R
+    wl = WORKLOADS[args.workload]
+    shape = MODEL_SHAPES["llama3-8b"]
+    vocab = make_vocab(shape.vocab)
+    B = wl["agents"]
+    # pages: every agent's first request (prompt + plan) resident, + the e2e loop's new
+    # requests; 2 MiB per 16-token page at 8B dims
+    n_pages = min(B * ((wl["max_ctx"] + 15) // 16), 56 * 1024)
+    p = engine_params("b200-roofline", max_batch=B, max_tasks=4 * B, max_ctx=wl["max_ctx"], n_pages=n_pages,
+                      clock_mode=1)
+    nccl_id = R.bootstrap_nccl_id(dist, rank, rt.nccl_unique_id) if world > 1 else None
+    dev = torch.cuda.current_device()
+    eng = rt.Engine(shape, p, vocab, seed=1234, flags=flags | rt.RT_FLAG_TIMING, device=dev, rank=rank,
+                    world=world, nccl_id=nccl_id, max_rows_per_forward=8192)
+    return eng, shape, vocab, p, dev
 
 
 def run_ours(args, rank, world, dist):
     import torch
-    from paper_2412_18695_b200 import rt
     from paper_2412_18695_b200 import metrics as M
+    from paper_2412_18695_b200 import replicas as R
     torch.cuda.set_device(0 if world == 1 else int(os.environ.get("LOCAL_RANK", rank)))
-    dev = torch.cuda.current_device()
-    shape = MODEL_SHAPES["llama3-8b"]
-    vocab = make_vocab(shape.vocab)
-    B = AGENTS_PER_GPU
-    n_pages = B * 3 * ((MAX_CTX + 15) // 16) // 2
-    p = engine_params("b200-roofline", max_batch=B, max_tasks=4 * B, max_ctx=MAX_CTX, n_pages=n_pages,
-                      clock_mode=1)
-    nccl_id = None
-    if world > 1:
-        import torch.distributed as tdist
-        obj = [rt.nccl_unique_id() if rank == 0 else None]
-        tdist.broadcast_object_list(obj, src=0)
-        nccl_id = obj[0]
-    eng = rt.Engine(shape, p, vocab, seed=1234, flags=rt.RT_FLAG_TIMING, device=dev, rank=rank, world=world,
-                    nccl_id=nccl_id, max_rows_per_forward=8192)
+    wl = WORKLOADS[args.workload]
+    eng, shape, vocab, p, dev = engine_setup(args, rank, world, dist)
+    B = wl["agents"]
     t0 = time.perf_counter()
 
     def now():
@@ -167,15 +199,16 @@ def run_ours(args, rank, world, dist):
     # ---- setup: every agent's request admitted and prefilled (contexts resident)
     K, W = args.steps, args.warmup
     plan_len = W + 2 * K + 16   # two passes of K rounds (throughput, then attention roofline)
+    agents = R.partition(B * world, rank, world)
     reqs = {}
-    for j in range(B):
-        agent = rank + world * j
-        tr = drone_request(vocab, agent, 0, args.seed, plan_len=plan_len)
+    for agent in agents:
+        tr = agent_request(args.workload, vocab, agent, 0, args.seed, plan_len=plan_len)
         rid = eng.submit(agent, tr.prompt, now(), tr.ert_us, tr.alpha, tr.beta, p.g_us, script=tr.plan)
         reqs[rid] = dict(arrival_us=now(), beta=tr.beta, alpha=tr.alpha, ert_us=tr.ert_us, cls=tr.cls, agent=agent)
-    for _ in range(100):
+    for _ in range(400):
         info = eng.step(now())
-        if info["n_running"] == B and info["n_prefill_rows"] == 0:
+        ready = info["n_running"] == B and info["n_prefill_rows"] == 0
+        if not R.any_busy(dist, not ready):
             break
     eng.poll()
     for _ in range(p.speed_window + 1):   # WCET speed window (5 rounds) forgets the prefill round
@@ -184,6 +217,7 @@ def run_ours(args, rank, world, dist):
         eng.step(now())
     eng.poll()
     eng.sync()
+    ctx_mean = float(np.mean([r[3] for r in eng.tasks() if r[1] in (1, 2)]))
     # pass A (the timed region of `value`): no per-kernel CUDA events — the events around each
     # attention launch sit between dependent kernels and cost their programmatic-dependent-
     # launch overlap (~0.45 ms per round, tools/timing_overhead.py)
@@ -219,31 +253,24 @@ def run_ours(args, rank, world, dist):
     st["kernel_launches"], st["rounds"] = st_a["kernel_launches"], st_a["rounds"]
     eng.poll()
     eng.set_timing(False)
-    if dist:
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-        n = torch.tensor([tok, len(segs_timed)], dtype=torch.float64, device="cuda")
-        dist.all_reduce(n)
-        tok_all, seg_all = float(n[0].item()), float(n[1].item())
-    else:
-        tok_all, seg_all = float(tok), float(len(segs_timed))
+    tok_all, ms = R.reduce_throughput(dist, tok, ms)
+    seg_all, _ = R.reduce_throughput(dist, len(segs_timed), ms)
     value = tok_all / (ms / 1e3)
     seg_per_s = seg_all / (ms / 1e3)
 
     # ---- roofline of the graded kernel (paged decode attention), live CUDA events
     pk = peaks()
     attn_gbs = st["attn_bytes"] / (st["attn_ms"] / 1e3) / 1e9 if st["attn_ms"] > 0 else None
-    kv_tok = shape.kv_bytes_per_token
     w_bytes = shape.weight_bytes_streamed()
     step_bytes = w_bytes + (st["attn_bytes"] / max(st["rounds"], 1))
-    roofline = {"kernel": "paged_decode_attention", "bound": "hbm", "achieved": attn_gbs,
+    roofline = {"kernel": "paged_decode_attention (k_attn)", "bound": "hbm", "achieved": attn_gbs,
                 "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": (attn_gbs / pk["hbm_gbs"]) if attn_gbs else None,
                 "frac_of_8000": (attn_gbs / 8000.0) if attn_gbs else None,
-                "traffic": ncu_traffic("k_attn"), "traffic_source": "profiles/r01_ncu_attention_full.json "
-                "(ncu --set full, same C2 launch: B=64, ctx~1310, 8 kv heads)",
+                "traffic": ncu_traffic("k_attn"), "traffic_source": NCU_ATTN_SOURCE,
                 "alg_bytes_per_launch": st["attn_bytes"] / max(st["attn_launches"], 1),
+                "alg_bytes_rule": "per launch: sum over rows of attended tokens x 2 (K,V) x 8 kv heads x 128 x 2 B "
+                                  "(4096 B per token per layer) + q + o",
                 "ms_per_launch": st["attn_ms"] / max(st["attn_launches"], 1),
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs" if not pk.get("fallback") else "fallback",
                 "timing": "CUDA events around every attention launch on the engine stream, second pass of "
@@ -251,33 +278,36 @@ def run_ours(args, rank, world, dist):
                           "timed without them)"}
     step_roof = {"alg_bytes_per_step": step_bytes, "achieved_gbs": step_bytes / (ms / K / 1e3) / 1e9,
                  "frac": step_bytes / (ms / K / 1e3) / 1e9 / pk["hbm_gbs"],
-                 "attn_share_of_step": st["attn_ms"] / max(st["step_ms"], 1e-9)}
+                 "attn_share_of_step": st["attn_ms"] / max(st["step_ms"], 1e-9),
+                 "weights_bytes_per_step": w_bytes}
 
-    # ---- e2e: closed loop through the C ABI with host buffers (paper plans: 20-token drone).
-    # (A) every prompt private (1300 tokens prefilled per request); then drain; (B) the drone's
-    # fixed prompt part registered once as a shared prefix, requests prefill
-    # only their 84-token task part.  B is the headline `e2e` (the paper's server stores the
-    # fixed prompt components), A is reported beside it.
+    # ---- e2e: closed loop through the C ABI with host buffers.  (A) every prompt private
+    # (whole prompts prefilled per request), then drain; (B) the robots' fixed prompt parts
+    # registered once as shared prefixes, requests prefill only their task
+    # part.  B is the headline `e2e` (the paper's server stores the fixed prompt components).
     launches_per_step = st["kernel_launches"] / max(st["rounds"], 1) + 2   # forward + sched pre/post
-    e2e_private = run_e2e(args, eng, vocab, p, rank, world, now, dist, reqs, prefix=None)
+    e2e_private = run_e2e(args, eng, vocab, p, rank, world, now, dist, reqs, prefixes=None,
+                          steps=max(4, K // 2))
     e2e_private.pop("_segments")
-    drain(eng, now)
-    pfx = system_prefix(vocab, "drone", PREFIX, seed=args.seed)
-    eng.register_prefix(pfx)
-    e2e = run_e2e(args, eng, vocab, p, rank, world, now, dist, reqs, prefix=pfx,
-                  start_agents=[rank + world * j for j in range(B)])
+    R.lockstep_until_idle(lambda: eng.step(now()), dist, max_rounds=4000)
+    eng.poll()
+    eng.sync()
+    pfx = {r: system_prefix(vocab, r, PREFIX[r], seed=args.seed) for r in ("drone", "arm")}
+    for r in ("drone", "arm"):
+        eng.register_prefix(pfx[r])
+    e2e = run_e2e(args, eng, vocab, p, rank, world, now, dist, reqs, prefixes=pfx, start_agents=agents)
     e2e["shared_prefix_tokens"] = PREFIX
     util = M.report(e2e.pop("_segments"), reqs, vocab, net_us=p.net_us, seed=args.seed)
 
     out = None
     if rank == 0:
         cpu = cpu_baseline_sample(args) if world == 1 and not args.no_cpu else None
-        systems = time_utility_systems(args) if world == 1 else None
+        systems = time_utility_systems(args) if world == 1 and not args.no_cpu else None
         out = {
-            "metric": "decode tok/s (segmented decode round, C2 drone agents)", "value": value, "unit": "tok/s",
+            "metric": METRIC, "value": value, "unit": "tok/s",
             "n_gpus": world, "steps": K, "warmup": W, "ms_per_step": ms / K, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": c2_config(world),
+            "config": bench_config(args.workload, world, ctx_mean),
             "segments_per_s": seg_per_s, "roofline": roofline, "step_roofline": step_roof,
             "cpu_baseline": cpu, "e2e": e2e, "e2e_private_prompts": e2e_private,
             "gpu_launches": int(round(launches_per_step * K)),
@@ -287,6 +317,10 @@ def run_ours(args, rank, world, dist):
         }
     eng.close()
     return out
+
+
+METRIC = "decode tok/s (segmented decode round)"
+NCU_ATTN_SOURCE = "profiles/r02_ncu_attention_full.json (ncu --set full of one k_attn launch of the same workload)"
 
 
 def time_utility_systems(args, workload="WID2", max_batch=8):
@@ -316,21 +350,11 @@ def time_utility_systems(args, workload="WID2", max_batch=8):
             "paper": "1.97x time utility, 84% waiting-time reduction (PAPER.md abstract; RTX 4090)"}
 
 
-def drain(eng, now, max_rounds=2000):
-    """Run (untimed) until nothing is running or waiting, without resubmitting."""
-    for _ in range(max_rounds):
-        info = eng.step(now())
-        if info["n_running"] == 0 and info["n_waiting"] == 0:
-            break
-    eng.poll()
-    eng.sync()
-
-
-def run_e2e(args, eng, vocab, p, rank, world, now, dist, reqs, prefix=None, start_agents=()):
+def run_e2e(args, eng, vocab, p, rank, world, now, dist, reqs, prefixes=None, start_agents=(), steps=None):
     """Closed loop (SURVEY §8d saturation mode): finished agents resubmit at once;
     `start_agents` (idle agents) submit at the start of the timed region."""
-    import torch
-    K = args.steps
+    from paper_2412_18695_b200 import replicas as R
+    K = steps or args.steps
     seg_all = []
     ordinal = {}
     h2d = d2h = 0
@@ -343,12 +367,12 @@ def run_e2e(args, eng, vocab, p, rank, world, now, dist, reqs, prefix=None, star
     # plan generation is the harness's work, not the server's): a request takes >= 12 rounds
     agents = sorted(set(list(start_agents) + [v["agent"] for v in reqs.values() if "agent" in v]))
     per_agent = K // 12 + 2
-    pregen = {(a, o): drone_request(vocab, a, o, args.seed, prefix=prefix)
+    pregen = {(a, o): agent_request(args.workload, vocab, a, o, args.seed, prefixes=prefixes)
               for a in agents for o in range(1, per_agent + 1)}
 
     def submit(agent):
         o = ordinal[agent] = ordinal.get(agent, 0) + 1
-        tr = pregen.get((agent, o)) or drone_request(vocab, agent, o, args.seed, prefix=prefix)
+        tr = pregen.get((agent, o)) or agent_request(args.workload, vocab, agent, o, args.seed, prefixes=prefixes)
         arr = now()
         rid = eng.submit(agent, tr.prompt, arr, tr.ert_us, tr.alpha, tr.beta, p.g_us, script=tr.plan)
         reqs[rid] = dict(arrival_us=arr, beta=tr.beta, alpha=tr.alpha, ert_us=tr.ert_us, cls=tr.cls, agent=agent)
@@ -371,61 +395,76 @@ def run_e2e(args, eng, vocab, p, rank, world, now, dist, reqs, prefix=None, star
     d2h += SEG_BYTES * len(segs)
     eng.sync()
     el = time.perf_counter() - t_start
-    if dist:
-        t = torch.tensor([el], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        el = float(t.item())
-        n = torch.tensor([tok], dtype=torch.float64, device="cuda")
-        dist.all_reduce(n)
-        tok = float(n.item())
-    return {"value": tok / el, "unit": "tok/s", "h2d_bytes_per_step": h2d / K, "d2h_bytes_per_step": d2h / K,
-            "clock": "host wall clock around rt_submit_request/rt_step/rt_poll_segment",
+    tok, ms = R.reduce_throughput(dist, tok, el * 1e3)
+    return {"value": tok / (ms / 1e3), "unit": "tok/s", "h2d_bytes_per_step": h2d / K,
+            "d2h_bytes_per_step": d2h / K, "steps": K,
+            "clock": "host wall clock around rt_submit_request/rt_step/rt_poll_segment (max over ranks)",
             "_segments": seg_all}
 
 
 # ------------------------------------------------------------------ CPU oracle baseline
-def oracle_decode_layer_sample(seed=0, B=64, ctx=PROMPT, om=None):
-    """One Llama-3-8B-shaped decode layer for B rows at context ctx, run by the
-    oracle as it stands (numpy fp64 + bf16 points); returns (seconds, tokens/s
-    extrapolated to the 32-layer step + lm_head)."""
-    from oracle.model import OracleModel, dense_attention, rms, rope, silu
+CPU_ROWS = 8   # rows of the oracle's bounded sample (both CPU legs)
+
+
+def oracle_decode_layer(seed, om, rows, ctxs):
+    """One Llama-3-8B-shaped decode layer for `rows` rows at contexts `ctxs`, run by the
+    oracle as it stands (numpy fp64 + bf16 points) with layer 0's weights already generated
+    (om.layer(0) outside the timed region).  Returns seconds."""
+    from oracle.model import dense_attention, rms, rope, silu
     from oracle.bf16 import bf16
     shape = MODEL_SHAPES["llama3-8b"]
-    om = om or OracleModel(shape, seed=seed)
     rng = np.random.default_rng(seed)
     d, nq, nkv, hd = shape.d_model, shape.n_q_heads, shape.n_kv_heads, shape.head_dim
-    x = rng.standard_normal((B, d))
-    K = bf16(rng.standard_normal((B, ctx, nkv, hd)).astype(np.float32))
-    V = bf16(rng.standard_normal((B, ctx, nkv, hd)).astype(np.float32))
-    t0 = time.perf_counter()
+    x = rng.standard_normal((rows, d))
+    Ks = [bf16(rng.standard_normal((c, nkv, hd)).astype(np.float32)) for c in ctxs]
+    Vs = [bf16(rng.standard_normal((c, nkv, hd)).astype(np.float32)) for c in ctxs]
     w = om.layer(0)
+    t0 = time.perf_counter()
     h = bf16(rms(x))
     qkv = h @ w["qkv"].T
-    q = bf16(rope(qkv[:, :nq * hd].reshape(B, nq, hd), [ctx] * B, hd))
-    o = np.stack([dense_attention(q[i], K[i], V[i]) for i in range(B)])
-    x = x + bf16(o.reshape(B, -1)) @ w["o"].T
+    q = bf16(rope(qkv[:, :nq * hd].reshape(rows, nq, hd), list(ctxs), hd))
+    o = np.stack([dense_attention(q[i], Ks[i], Vs[i]) for i in range(rows)])
+    x = x + bf16(o.reshape(rows, -1)) @ w["o"].T
     h = bf16(rms(x))
     gu = h @ w["gu"].T
     a = bf16(silu(gu[:, :shape.d_ff]) * gu[:, shape.d_ff:])
     x = x + a @ w["d"].T
-    sec = time.perf_counter() - t0
-    return sec, B / (sec * shape.n_layers)
+    return time.perf_counter() - t0
+
+
+def cpu_ctxs(workload):
+    if workload == "C2":
+        return [PROMPT["drone"]] * CPU_ROWS
+    return [PROMPT["drone"], PROMPT["arm"]] * (CPU_ROWS // 2)
+
+
+def cpu_sample_desc(workload, n_layers):
+    return (f"{CPU_ROWS} rows of the {workload} decode step (contexts {sorted(set(cpu_ctxs(workload)))}), one of "
+            f"{n_layers} llama3-8b decoder layers per sample (QKV + RoPE + attention + O + SwiGLU MLP; the layer's "
+            f"weights generated once before timing); value = rows / ({n_layers} x layer seconds), the per-layer rate "
+            f"scaled to the {n_layers}-layer step (lm_head excluded)")
 
 
 def cpu_baseline_sample(args):
     import torch
+    from oracle.model import OracleModel
     cores = len(os.sched_getaffinity(0))
-    sec, tps = oracle_decode_layer_sample(args.seed)
-    return {"value": tps, "unit": "tok/s", "cores": cores, "threads": torch.get_num_threads(), "kind": "oracle",
-            "sample": f"1 of 32 llama3-8b decode layers (incl. counter-based weight generation) at B=64, ctx "
-                      f"{PROMPT}, {sec:.1f} s, extrapolated x32 layers (lm_head excluded)",
-            "extra": oracle_extra_timings(args)}
+    shape = MODEL_SHAPES["llama3-8b"]
+    om = OracleModel(shape, seed=args.seed)
+    om.layer(0)
+    secs = [oracle_decode_layer(args.seed + i, om, CPU_ROWS, cpu_ctxs(args.workload)) for i in range(2)]
+    sec = min(secs)
+    return {"value": CPU_ROWS / (sec * shape.n_layers), "unit": "tok/s", "cores": cores,
+            "threads": torch.get_num_threads(), "kind": "oracle", "layer_seconds": sec,
+            "sample": cpu_sample_desc(args.workload, shape.n_layers), "extra": oracle_extra_timings(args)}
 
 
 def oracle_extra_timings(args):
     """SURVEY §8(d) CPU-oracle timings besides the decode round: the whole C1 trace (tiny
-    model + scheduler, wall seconds) and a scheduling-only replay of a C4-shaped trace (1024
-    agents, traces 1-11, Poisson) in rounds/s."""
+    model + scheduler, wall seconds), scheduling-only replays of a C4-shaped trace (1024
+    agents, traces 1-11, Poisson) and of a C5-shaped one (512 agents per GPU, long robot-arm
+    plans of 100-200 tokens in 10-20 segments, 128-token prompts, AMB-26 reservations on a
+    pool that refuses admissions), in rounds/s."""
     from oracle.engine import OracleEngine
     from oracle.model import OracleModel
     from synth import compose_workload
@@ -442,57 +481,63 @@ def oracle_extra_timings(args):
     ora.run_until_idle()
     out["c1_trace_wall_s"] = time.perf_counter() - t0
     v8 = make_vocab(128256)
-    p4 = engine_params("b200-roofline", max_batch=128, max_tasks=2048, max_ctx=4096, n_pages=1 << 16)
-    reqs = compose_workload(1024, 64.0, 16, range(1, 12), 10.0, args.seed, v8, prompt_len_range=(64, 64),
-                            max_requests=2000)
-    ora = OracleEngine(p4, v8.tok_skill, v8.tok_exec_min_us, v8.eos_id, v8.vocab)
-    for r in reqs:
-        ora.submit(r.agent_id, r.prompt, r.arrival_us, r.ert_us, r.alpha, r.beta, r.exec_window_us, len(r.plan),
-                   script=r.plan)
-    t0 = time.perf_counter()
-    n = 0
-    while time.perf_counter() - t0 < 10.0:
-        info = ora.step()
-        n += 1
-        if info["n_running"] == 0 and info["n_waiting"] == 0:
-            break
-    out["c4_sched_replay_rounds_per_s"] = n / (time.perf_counter() - t0)
-    out["c4_sched_replay"] = f"{len(reqs)} requests of 1024 agents, {n} rounds (<= 10 s)"
+    for name, n_agents, eps, tpe, pool, plen, batch, pages, limit in (
+            ("c4", 1024, 64.0, 16, range(1, 12), 64, 128, 1 << 16, 2000),
+            ("c5", 512, 64.0, 16, range(9, 12), 128, 512, 277 * 24, 1536)):
+        pp = engine_params("b200-roofline", max_batch=batch, max_tasks=2048, max_ctx=4096, n_pages=pages)
+        plan_len = None if name == "c4" else 160
+        reqs = compose_workload(n_agents, eps, tpe, pool, 10.0, args.seed, v8, prompt_len_range=(plen, plen),
+                                max_requests=limit, plan_len=plan_len)
+        ora = OracleEngine(pp, v8.tok_skill, v8.tok_exec_min_us, v8.eos_id, v8.vocab)
+        for r in reqs:
+            ora.submit(r.agent_id, r.prompt, r.arrival_us, r.ert_us, r.alpha, r.beta, r.exec_window_us,
+                       256 if name == "c5" else len(r.plan), script=r.plan)
+        t0 = time.perf_counter()
+        n = refused = 0
+        while time.perf_counter() - t0 < 8.0:
+            info = ora.step()
+            n += 1
+            refused += info.get("n_refused_mem", 0)
+            if info["n_running"] == 0 and info["n_waiting"] == 0:
+                break
+        out[f"{name}_sched_replay_rounds_per_s"] = n / (time.perf_counter() - t0)
+        out[f"{name}_sched_replay"] = f"{len(reqs)} requests of {n_agents} agents, {n} rounds (<= 8 s), " \
+                                      f"{refused} memory refusals"
     return out
 
 
-def c2_config(world):
-    """The workload both arms report (BASELINE configs[1])."""
-    return {"workload": "C2: 64 drone agents per GPU, llama3-8b-shape random-init bf16, "
-                        "contexts resident (prompt 1300 prefilled in setup), scripted drone plans",
-            "model": "llama3-8b-shape", "global_batch": AGENTS_PER_GPU * world, "ctx": PROMPT,
-            "parallelism": f"replicas x{world} (agent partition, 1 allgather/round)",
-            "l2": "inputs > L2 (16 GB weights + 11 GB KV per step)"}
+def bench_config(workload, world, ctx_mean=None):
+    """The workload both arms report."""
+    wl = WORKLOADS[workload]
+    return {"workload": f"{workload}: BASELINE.json {wl['cfg']}; llama3-8b-shape random-init bf16; contexts "
+                        "resident (prompts prefilled in setup), scripted robot plans",
+            "model": "llama3-8b-shape", "global_batch": wl["agents"] * world, "mean_ctx": ctx_mean,
+            "parallelism": f"replicas x{world} (agent a -> rank a mod {world}, 1 allgather/round)",
+            "l2": "inputs > L2 (15 GB of weights + the resident KV stream through HBM every step)"}
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the CPU oracle as it stands, bounded sample per step."""
+    """--impl reference: the CPU oracle as it stands, one bounded sample per step (rank 0)."""
     if rank != 0:
         return None
+    import torch
     from oracle.model import OracleModel
     cores = len(os.sched_getaffinity(0))
-    om = OracleModel(MODEL_SHAPES["llama3-8b"], seed=args.seed)
-    for _ in range(args.warmup):
-        oracle_decode_layer_sample(args.seed, B=8, om=om)
-    secs, toks = 0.0, 0
-    for i in range(args.steps):
-        s, _ = oracle_decode_layer_sample(args.seed + i, B=8, om=om)
-        secs += s * MODEL_SHAPES["llama3-8b"].n_layers
-        toks += 8
-    v = toks / secs
-    return {"impl": "reference", "metric": "decode tok/s (segmented decode round, C2 drone agents)", "value": v,
-            "unit": "tok/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": secs / args.steps * 1e3, "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f64 (bf16 points)", "data": "synthetic",
-            "config": c2_config(world),
-            "cpu_baseline": {"value": v, "unit": "tok/s", "cores": cores, "kind": "oracle",
-                             "sample": "per timed step one C2 decode step of 8 of the drone rows at ctx 1300, "
-                                       "1 of 32 layers (weights generated in warmup), extrapolated x32 layers"},
+    shape = MODEL_SHAPES["llama3-8b"]
+    om = OracleModel(shape, seed=args.seed)
+    om.layer(0)                                     # weight generation: before warm-up, untimed
+    for i in range(args.warmup):
+        oracle_decode_layer(args.seed + i, om, CPU_ROWS, cpu_ctxs(args.workload))
+    secs = [oracle_decode_layer(args.seed + 100 + i, om, CPU_ROWS, cpu_ctxs(args.workload))
+            for i in range(args.steps)]
+    sec = float(np.sum(secs))
+    v = CPU_ROWS * args.steps / (sec * shape.n_layers)
+    return {"impl": "reference", "metric": METRIC, "value": v, "unit": "tok/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64 (bf16 points)",
+            "data": "synthetic", "config": bench_config(args.workload, world),
+            "cpu_baseline": {"value": v, "unit": "tok/s", "cores": cores, "threads": torch.get_num_threads(),
+                             "kind": "oracle", "sample": cpu_sample_desc(args.workload, shape.n_layers)},
             "e2e": {"value": v, "unit": "tok/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 
@@ -502,6 +547,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="C3", choices=sorted(WORKLOADS))
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
@@ -517,6 +563,7 @@ def main():
     if world > 1:
         import torch
         import torch.distributed as tdist
+        os.environ.setdefault("NCCL_DEBUG", "INFO")   # the driver's log shows the N ranks' communicator
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", rank)))
         tdist.init_process_group("nccl")
         dist = tdist

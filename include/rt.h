@@ -68,7 +68,10 @@ enum {
   RT_FLAG_CAPTURE = 4,      /* keep q / attention output (fp32) of layer capture_layer */
   RT_FLAG_TIMING = 8,       /* CUDA-event timing of attention / GEMM launches (rt_stats) */
   RT_FLAG_FORCE_EXCHANGE = 16, /* run the per-round NCCL allgather + merge even when world == 1 */
-  RT_FLAG_TRACE = 64           /* per-CTA %globaltimer records of every kernel (RT_DUMP_TRACE) */
+  RT_FLAG_TRACE = 64,          /* per-CTA %globaltimer records of every kernel (RT_DUMP_TRACE) */
+  RT_FLAG_CAPTURE_LAYERS = 128 /* keep every layer's intermediates of the last round (RT_DUMP_LAYER_*;
+                                  the round's first max_rows_per_forward rows; parity tests only:
+                                  a device copy after each projection / attention launch) */
 };
 /* Projection kernel path (rt_config.gemm_path, rt_op_gemm_tiled): AUTO = the measured dispatch
  * (DESIGN.md §6); the others force one kernel wherever it applies, for parity tests:
@@ -244,12 +247,24 @@ rt_status rt_reset_stats(rt_engine* e);
  *   RT_DUMP_MERGED      int64 [K][4] merged global top-K (world > 1)
  *   RT_DUMP_TRACE       rt_trace_rec [n] since the last rt_reset_stats (RT_FLAG_TRACE; at most
  *                       2^20 records, one per CTA; the buffer is process-wide: with several
- *                       traced engines in one process the last created one owns it) */
+ *                       traced engines in one process the last created one owns it)
+ * Per-layer dumps (RT_FLAG_CAPTURE_LAYERS), layer l in bits 16..30 of `what`
+ * (what = RT_DUMP_LAYER_* | l << 16), rows of the last round's first forward chunk:
+ *   RT_DUMP_LAYER_X     fp32 [n_rows][d_model]  residual stream entering layer l (l = n_layers:
+ *                       leaving the last layer)
+ *   RT_DUMP_LAYER_Q     bf16 [n_rows][n_q_heads][head_dim]  q after RoPE
+ *   RT_DUMP_LAYER_O     bf16 [n_rows][n_q_heads][head_dim]  attention output
+ *   RT_DUMP_LAYER_XMID  fp32 [n_rows][d_model]  residual after the O projection
+ *   RT_DUMP_LAYER_ACT   bf16 [n_rows][d_ff]     SwiGLU activation (down projection input)
+ *   RT_DUMP_LAYER_KV    bf16 logical [n_pages][2][n_kv_heads][16][head_dim] of layer l (any engine
+ *                       with a model; no flag needed) */
 enum {
   RT_DUMP_TASKS = 1, RT_DUMP_PAGE_TABLES = 2, RT_DUMP_ROUND = 3, RT_DUMP_LOGITS = 4,
   RT_DUMP_HIDDEN = 5, RT_DUMP_CAPTURE_Q = 6, RT_DUMP_CAPTURE_O = 7, RT_DUMP_ROWS = 8,
   RT_DUMP_KV_LAYER = 9, RT_DUMP_FREE_STACK = 10, RT_DUMP_TASK_SLOTS = 11, RT_DUMP_MERGED = 12,
-  RT_DUMP_TRACE = 13, RT_DUMP_HOST_PAGE_TABLES = 14, RT_DUMP_HOST_FREE_STACK = 15
+  RT_DUMP_TRACE = 13, RT_DUMP_HOST_PAGE_TABLES = 14, RT_DUMP_HOST_FREE_STACK = 15,
+  RT_DUMP_LAYER_X = 16, RT_DUMP_LAYER_Q = 17, RT_DUMP_LAYER_O = 18, RT_DUMP_LAYER_XMID = 19,
+  RT_DUMP_LAYER_ACT = 20, RT_DUMP_LAYER_KV = 21
 };
 /* One kernel CTA: grid = %gridid (unique per launch); kind = 1 GEMM (| epilogue mode << 8 |
  * cluster split << 16), 2 attention, 3 norm, 4 embed, 5/6 scheduler pre/post, 7 gather,

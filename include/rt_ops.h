@@ -34,6 +34,19 @@ rt_status rt_op_paged_attention(const void* d_q, const void* d_pool, const int32
                                 void* d_ws, int64_t ws_bytes, void* stream);
 int64_t rt_op_attention_ws_bytes(int32_t n_rows, int32_t max_seqlen, int32_t n_q, int32_t hd);
 
+/* a5 causal prefill attention over paged KV (NEXT-1; the prompt rows of k = 0 admissions,
+ * PAPER.md:72, 93 "Decoding 0" includes the prefill): d_tiles int32 [n_tiles][4] = (first row,
+ * rows <= 16, pos0, task): rows first_row .. first_row + rows - 1 are the consecutive positions
+ * pos0 .. pos0 + rows - 1 (pos0 a multiple of 16) of task's prompt, each attending causally to
+ * positions 0 .. its own (pages from page_table[task * pt_stride + p / 16], which must already
+ * hold the K/V of every attended position).  d_q bf16 [n_rows][n_q][hd]; d_out bf16 same shape;
+ * d_out_f32 (nullable) fp32 same shape.  groups: warp groups per CTA (0: by load, 1 or 2).
+ * hd in {32, 64, 128}; G = n_q / n_kv in {1..8}. */
+rt_status rt_op_prefill_attention(const void* d_q, const void* d_pool, const int32_t* d_page_table,
+                                  int32_t pt_stride, const int32_t* d_tiles, int32_t n_tiles, int32_t n_rows,
+                                  int32_t n_q, int32_t n_kv, int32_t hd, int32_t groups, void* d_out,
+                                  float* d_out_f32, void* stream);
+
 /* Write logical K/V rows into the swizzled pool: row r of d_k / d_v (bf16
  * [n_rows][n_kv][hd]) goes to token slot d_slot[r] = page * 16 + offset. */
 rt_status rt_op_kv_write(void* d_pool, const void* d_k, const void* d_v, const int32_t* d_slot,

@@ -12,11 +12,17 @@ KV cache", "bf16 inputs, fp32 accumulate"):
   final:      h = rms(x);  logits = h W_lm^T;  token = argmax (lowest index on ties)
   rms(x) = x * rsqrt(mean(x^2) + 1e-5)   (gamma = 1)
 
-Accumulation is fp64 here; bf16 RNE is applied at exactly the GPU's
-materialisation points when ``bf16_points`` is True: GEMM inputs (h, o, the
+Accumulation is fp64 here; bf16 RNE is applied at the materialisation points
+SURVEY c1 fixes when ``bf16_points`` is True: GEMM inputs (h = rms(x), o, the
 SwiGLU product), q after RoPE, stored K and V.  The residual stream x is not
 rounded.  With ``bf16_points=False`` this is the plain model definition
 (pinned against transformers.LlamaForCausalLM).
+
+The CUDA path folds RMSNorm into the consuming projection: it rounds x (not
+rms(x)) to bf16 and scales each output row by rsqrt(mean(x^2) + eps) in fp32
+in the epilogue — the same algebra with the rounding point moved.  The oracle
+keeps the definition above; reading R-NORM bounds the difference
+(per-op tolerances of tests/test_gpu_fullsize.py).
 """
 import numpy as np
 

@@ -98,6 +98,10 @@ struct rt_engine {
   int32_t* d_am_idx = nullptr;
   bf16 *d_h = nullptr, *d_q = nullptr, *d_o = nullptr, *d_act = nullptr, *d_hfin = nullptr;
   float *d_cap_q = nullptr, *d_cap_o = nullptr, *d_rope_cos = nullptr, *d_rope_sin = nullptr;
+  // RT_FLAG_CAPTURE_LAYERS: per-layer intermediates of the last round's first forward chunk
+  float *d_lc_x = nullptr, *d_lc_xmid = nullptr;   // [L + 1][fwd_rows][d], [L][fwd_rows][d]
+  bf16 *d_lc_q = nullptr, *d_lc_o = nullptr, *d_lc_act = nullptr;  // [L][fwd_rows][...]
+  int lc_rows = 0;                                   // rows captured in the last round
   int64_t attn_ws_cap = 0, gemm_ws_cap = 0;
   float *d_gemm_ws = nullptr, *d_ss = nullptr;
   int* d_attn_tickets = nullptr;
@@ -475,6 +479,13 @@ static rt_status create_impl(rt_engine* e, const rt_config* cfg) {
       CK(e, dalloc(e, &e->d_cap_q, (size_t)e->rows_cap * nq * hd));
       CK(e, dalloc(e, &e->d_cap_o, (size_t)e->rows_cap * nq * hd));
     }
+    if (c.flags & RT_FLAG_CAPTURE_LAYERS) {
+      CK(e, dalloc(e, &e->d_lc_x, (size_t)(L + 1) * R * d));
+      CK(e, dalloc(e, &e->d_lc_xmid, (size_t)L * R * d));
+      CK(e, dalloc(e, &e->d_lc_q, (size_t)L * R * nq * hd));
+      CK(e, dalloc(e, &e->d_lc_o, (size_t)L * R * nq * hd));
+      CK(e, dalloc(e, &e->d_lc_act, (size_t)L * R * ff));
+    }
     // RoPE tables (rotate-half, theta 500000), fp64 on host -> fp32
     std::vector<float> cs((size_t)c.max_ctx * hd / 2), sn((size_t)c.max_ctx * hd / 2);
     for (int p = 0; p < c.max_ctx; ++p)
@@ -756,6 +767,14 @@ static rt_status forward(rt_engine* e, const HostMailbox& plan) {
   const float sl2 = (float)(1.4426950408889634 / sqrt((double)hd));
   const int d_tiles = (d + 127) / 128;
   int launches = 0;
+  const bool lcap = e->d_lc_x != nullptr;
+  if (lcap) e->lc_rows = std::min(n_rows, e->fwd_rows);
+  // RT_FLAG_CAPTURE_LAYERS: device copy of a forward buffer of this chunk (first chunk only)
+  auto lc_copy = [&](void* dst_base, const void* src, int l, size_t row_bytes, int row0_) {
+    if (!lcap || row0_ != 0) return;
+    cudaMemcpyAsync((char*)dst_base + ((size_t)l * e->fwd_rows) * row_bytes, src, (size_t)e->lc_rows * row_bytes,
+                    cudaMemcpyDeviceToDevice, s);
+  };
   for (int row0 = 0; row0 < n_rows; row0 += e->fwd_rows) {
     const int n = std::min(e->fwd_rows, n_rows - row0);
     launch_embed(P.row_tok, row0, n, e->emb, d, e->d_x, e->d_h, e->d_ss, s);  // d_h = bf16(x), un-normed
@@ -865,10 +884,12 @@ static rt_status forward(rt_engine* e, const HostMailbox& plan) {
     for (int l = 0; l < c.n_layers; ++l) {
       LayerW& w = e->layers[l];
       void* pool_l = e->d_pool + (size_t)l * e->pool_layer_bytes;
+      lc_copy(e->d_lc_x, e->d_x, l, (size_t)d * 4, row0);
       {
         GemmArgs g = args_qkv(l);
         gemm(w.qkv, e->x_h, e->qkv_dim, d, g);
       }
+      lc_copy(e->d_lc_q, e->d_q, l, (size_t)nq * hd * 2, row0);
       aa.pool = pool_l;
       aa.out_f32 = (e->d_cap_o && l == c.capture_layer) ? e->d_cap_o : nullptr;
       if (timing && row0 == 0) record_timing_event(e->ev_attn[2 * l], s);
@@ -883,19 +904,23 @@ static rt_status forward(rt_engine* e, const HostMailbox& plan) {
         launch_attention_prefill(pa, s);
         ++launches;
       }
+      lc_copy(e->d_lc_o, e->d_o, l, (size_t)nq * hd * 2, row0);
       {  // O projection + residual
         GemmArgs g = args_resid(d, nq * hd);
         gemm(w.o, e->x_o, d, nq * hd, g);
       }
+      lc_copy(e->d_lc_xmid, e->d_x, l, (size_t)d * 4, row0);
       {  // gate/up projection (FFN RMSNorm as row scale) + SwiGLU
         GemmArgs g = args_gu();
         gemm(w.gu, e->x_h, 2 * ff, d, g);
       }
+      lc_copy(e->d_lc_act, e->d_act, l, (size_t)ff * 2, row0);
       {  // down projection + residual
         GemmArgs g = args_resid(d, ff);
         gemm(w.d, e->x_act, d, ff, g);
       }
     }
+    lc_copy(e->d_lc_x, e->d_x, c.n_layers, (size_t)d * 4, row0);
     // logits rows: final RMSNorm applied while gathering them
     if (B > 0) {
       launch_gather_norm(P.slot_row, B, row0, n, e->d_x, e->d_ss, d, e->d_hfin, s);
@@ -1152,6 +1177,28 @@ extern "C" rt_status rt_debug_dump(rt_engine* e, int32_t what, void* dst, int64_
   DevState ds;
   CK(e, cudaMemcpy(&ds, e->d_st, sizeof(ds), cudaMemcpyDeviceToHost));
   const int B = ds.B, n_rows = ds.n_rows;
+  const int layer = (what >> 16) & 0x7FFF;
+  what &= 0xFFFF;
+  if (what >= RT_DUMP_LAYER_X && what <= RT_DUMP_LAYER_ACT) {
+    if (!e->d_lc_x) return fail(e, RT_E_STATE, "RT_FLAG_CAPTURE_LAYERS not set");
+    if (layer > c.n_layers || (layer == c.n_layers && what != RT_DUMP_LAYER_X))
+      return fail(e, RT_E_INVAL, "layer out of range");
+    const int R = e->fwd_rows, nr = e->lc_rows;
+    const size_t qb = (size_t)c.n_q_heads * c.head_dim * 2;
+    switch (what) {
+      case RT_DUMP_LAYER_X:
+        return copy_out(e, dst, bytes, e->d_lc_x + (size_t)layer * R * c.d_model, (int64_t)nr * c.d_model * 4, bytes_out);
+      case RT_DUMP_LAYER_XMID:
+        return copy_out(e, dst, bytes, e->d_lc_xmid + (size_t)layer * R * c.d_model, (int64_t)nr * c.d_model * 4,
+                        bytes_out);
+      case RT_DUMP_LAYER_Q:
+        return copy_out(e, dst, bytes, (const char*)e->d_lc_q + (size_t)layer * R * qb, (int64_t)nr * qb, bytes_out);
+      case RT_DUMP_LAYER_O:
+        return copy_out(e, dst, bytes, (const char*)e->d_lc_o + (size_t)layer * R * qb, (int64_t)nr * qb, bytes_out);
+      default:
+        return copy_out(e, dst, bytes, e->d_lc_act + (size_t)layer * R * c.d_ff, (int64_t)nr * c.d_ff * 2, bytes_out);
+    }
+  }
   switch (what) {
     case RT_DUMP_TASKS: {
       std::vector<int64_t> v((size_t)MT * 10);
@@ -1217,15 +1264,18 @@ extern "C" rt_status rt_debug_dump(rt_engine* e, int32_t what, void* dst, int64_
       }
       return copy_out(e, dst, bytes, v.data(), (int64_t)v.size() * 4, bytes_out, false);
     }
-    case RT_DUMP_KV_LAYER: {
+    case RT_DUMP_KV_LAYER:
+    case RT_DUMP_LAYER_KV: {
       if (!e->d_pool) return fail(e, RT_E_STATE, "no model");
+      const int kl = what == RT_DUMP_LAYER_KV ? layer : c.capture_layer;
+      if (kl >= c.n_layers) return fail(e, RT_E_INVAL, "layer out of range");
       const int64_t need = (int64_t)c.n_pages * 2 * c.n_kv_heads * 16 * c.head_dim * 2;
       if (bytes_out) *bytes_out = need;
       if (!dst) return RT_OK;
       if (bytes < need) return fail(e, RT_E_INVAL, "dump buffer too small");
       bf16* tmp = nullptr;
       CK(e, cudaMalloc(&tmp, need));
-      launch_kv_read(e->d_pool + (size_t)c.capture_layer * e->pool_layer_bytes, tmp, c.n_pages, c.n_kv_heads,
+      launch_kv_read(e->d_pool + (size_t)kl * e->pool_layer_bytes, tmp, c.n_pages, c.n_kv_heads,
                      c.head_dim, e->stream);
       CK(e, cudaStreamSynchronize(e->stream));
       cudaError_t r = cudaMemcpy(dst, tmp, need, cudaMemcpyDeviceToHost);

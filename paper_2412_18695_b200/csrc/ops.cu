@@ -66,6 +66,35 @@ extern "C" rt_status rt_op_paged_attention(const void* d_q, const void* d_pool, 
   return last_launch();
 }
 
+extern "C" rt_status rt_op_prefill_attention(const void* d_q, const void* d_pool, const int32_t* d_page_table,
+                                             int32_t pt_stride, const int32_t* d_tiles, int32_t n_tiles,
+                                             int32_t n_rows, int32_t n_q, int32_t n_kv, int32_t hd, int32_t groups,
+                                             void* d_out, float* d_out_f32, void* stream) {
+  if (n_tiles < 0 || n_rows < 0 || n_kv < 1 || n_q % n_kv || n_q / n_kv > 8 || groups < 0 || groups > 2)
+    return RT_E_INVAL;
+  if (hd != 32 && hd != 64 && hd != 128) return RT_E_INVAL;
+  if (n_tiles == 0 || n_rows == 0) return RT_OK;
+  PrefillArgs a{};
+  a.q = (const bf16*)d_q;
+  a.pool = d_pool;
+  a.page_table = d_page_table;
+  a.pt_stride = pt_stride;
+  a.tiles = reinterpret_cast<const int4*>(d_tiles);
+  a.n_tiles = n_tiles;
+  a.row0 = 0;
+  a.n_rows = n_rows;
+  a.nq = n_q;
+  a.nkv = n_kv;
+  a.hd = hd;
+  a.G = n_q / n_kv;
+  a.out = (bf16*)d_out;
+  a.out_f32 = d_out_f32;
+  a.scale_log2 = (float)(1.4426950408889634 / sqrt((double)hd));
+  a.groups = groups;
+  launch_attention_prefill(a, (cudaStream_t)stream);
+  return last_launch();
+}
+
 extern "C" rt_status rt_op_kv_write(void* d_pool, const void* d_k, const void* d_v, const int32_t* d_slot,
                                     int32_t n_rows, int32_t n_kv, int32_t hd, void* stream) {
   if (n_rows < 0 || n_kv < 1 || hd % 8) return RT_E_INVAL;

@@ -24,9 +24,10 @@ def utility(beta, alpha, ert_us, w_us):
     return beta if beta <= y else y
 
 
-def report(segments, requests, vocab, net_us=8000, seed=0, exec_from="tokens"):
+def report(segments, requests, vocab, net_us=8000, seed=0, exec_from="tokens", per_request=False):
     """segments: rt_poll_segment records; requests: {rid: dict(arrival_us, beta, alpha,
-    ert_us, cls)}.  Returns per-class means and totals over completed requests.
+    ert_us, cls)}.  Returns per-class means and totals over completed requests (and, with
+    per_request, the per-request figures under "requests").
     exec_from="est": a segment executes for its est_exec_us (multi-token stop grammars, e.g.
     the chatbot's reading time) instead of sampled per-skill durations."""
     by_rid = {}
@@ -52,7 +53,7 @@ def report(segments, requests, vocab, net_us=8000, seed=0, exec_from="tokens"):
             waits.append(start - (req["arrival_us"] if prev_end is None else prev_end))
             prev_end = start + e
             e_tot += e
-        per.append(dict(cls=req.get("cls"), response_us=waits[0], waiting_us=sum(waits),
+        per.append(dict(request_id=rid, cls=req.get("cls"), response_us=waits[0], waiting_us=sum(waits),
                         completion_us=prev_end - req["arrival_us"], exec_us=e_tot,
                         utility=utility(req["beta"], req["alpha"], req["ert_us"], waits[0])))
     out = {}
@@ -63,7 +64,10 @@ def report(segments, requests, vocab, net_us=8000, seed=0, exec_from="tokens"):
                        waiting_s=sum(m["waiting_us"] for m in v) / len(v) / 1e6) for c, v in out.items()}
     total = sum(m["utility"] for m in per)
     n = len(per)
-    return dict(by_class=summary, n=n, total_utility=total,
-                mean_utility=(total / n) if per else None,
-                mean_response_s=(sum(m["response_us"] for m in per) / n / 1e6) if per else None,
-                mean_waiting_s=(sum(m["waiting_us"] for m in per) / n / 1e6) if per else None)
+    out = dict(by_class=summary, n=n, total_utility=total,
+               mean_utility=(total / n) if per else None,
+               mean_response_s=(sum(m["response_us"] for m in per) / n / 1e6) if per else None,
+               mean_waiting_s=(sum(m["waiting_us"] for m in per) / n / 1e6) if per else None)
+    if per_request:
+        out["requests"] = per
+    return out

@@ -21,7 +21,9 @@ RT_FLAG_TRACE = 64
 RT_GEMM_PATH_AUTO, RT_GEMM_PATH_SPLITK, RT_GEMM_PATH_STREAMK, RT_GEMM_PATH_PAIR = 0, 1, 2, 3
 (RT_DUMP_TASKS, RT_DUMP_PAGE_TABLES, RT_DUMP_ROUND, RT_DUMP_LOGITS, RT_DUMP_HIDDEN, RT_DUMP_CAPTURE_Q,
  RT_DUMP_CAPTURE_O, RT_DUMP_ROWS, RT_DUMP_KV_LAYER, RT_DUMP_FREE_STACK, RT_DUMP_TASK_SLOTS,
- RT_DUMP_MERGED, RT_DUMP_TRACE, RT_DUMP_HOST_PAGE_TABLES, RT_DUMP_HOST_FREE_STACK) = range(1, 16)
+ RT_DUMP_MERGED, RT_DUMP_TRACE, RT_DUMP_HOST_PAGE_TABLES, RT_DUMP_HOST_FREE_STACK, RT_DUMP_LAYER_X, RT_DUMP_LAYER_Q,
+ RT_DUMP_LAYER_O, RT_DUMP_LAYER_XMID, RT_DUMP_LAYER_ACT, RT_DUMP_LAYER_KV) = range(1, 22)
+RT_FLAG_CAPTURE_LAYERS = 128
 # rt_trace_rec (include/rt.h)
 TRACE_DTYPE = np.dtype([("grid", "<u8"), ("kind", "<u4"), ("smid", "<u4"), ("t_entry", "<u8"),
                         ("t_ready", "<u8"), ("t_aux", "<u8"), ("t_exit", "<u8")])
@@ -33,7 +35,7 @@ EXPORTED = ["rt_create", "rt_destroy", "rt_submit_request", "rt_register_prefix"
             "rt_op_paged_attention", "rt_op_attention_ws_bytes", "rt_op_kv_write", "rt_op_kv_read", "rt_op_kv_swap",
             "rt_op_gemm", "rt_op_lm_argmax", "rt_op_init_weights", "rt_op_priority", "rt_mark", "rt_elapsed_ms",
             "rt_nccl_unique_id", "rt_op_pack_tiled", "rt_op_gemm_tiled", "rt_set_timing",
-            "rt_op_merge_candidates"]
+            "rt_op_merge_candidates", "rt_op_prefill_attention"]
 
 
 class RtError(RuntimeError):
@@ -133,6 +135,7 @@ def lib():
     L.rt_op_pack_tiled.argtypes = [vp, vp, i32, i32, vp]
     L.rt_op_gemm_tiled.argtypes = [vp, vp, vp, i32, i32, i32, i32, i32, i32, i32, vp]
     L.rt_op_merge_candidates.argtypes = [vp, i32, vp, vp]
+    L.rt_op_prefill_attention.argtypes = [vp, vp, vp, i32, vp, i32, i32, i32, i32, i32, i32, vp, vp, vp]
     for f in EXPORTED:
         if f not in ("rt_last_error", "rt_version", "rt_op_attention_ws_bytes"):
             getattr(L, f).restype = C.c_int32
@@ -342,6 +345,10 @@ class Engine:
         _check(lib().rt_debug_dump(self.h, what, buf.ctypes.data, buf.nbytes, C.byref(need)), self.h)
         return buf[:need.value].view(dtype)
 
+    def layer_dump(self, what, layer, dtype):
+        """Per-layer capture (RT_FLAG_CAPTURE_LAYERS / RT_DUMP_LAYER_KV) of layer ``layer``."""
+        return self.dump(what | (layer << 16), dtype)
+
     def trace(self):
         """Per-CTA kernel records since the last reset_stats (RT_FLAG_TRACE)."""
         return self.dump(RT_DUMP_TRACE, TRACE_DTYPE)
@@ -383,6 +390,14 @@ def paged_attention(q, pool, page_table, row_task, row_seqlen, max_seqlen, n_q, 
                                    _ptr(row_task), _ptr(row_seqlen), int(q.shape[0]), int(max_seqlen), n_q, n_kv,
                                    hd, _ptr(out), _ptr(out_f32), _ptr(ws), ws.numel() * ws.element_size(),
                                    _stream(stream)))
+    return out
+
+
+def prefill_attention(q, pool, page_table, tiles, n_q, n_kv, hd, out, out_f32=None, groups=0, stream=None):
+    """tiles: int32 cuda tensor [n_tiles][4] (first row, rows <= 16, pos0, task)."""
+    _check(lib().rt_op_prefill_attention(_ptr(q), _ptr(pool), _ptr(page_table), int(page_table.shape[1]),
+                                         _ptr(tiles), int(tiles.shape[0]), int(q.shape[0]), n_q, n_kv, hd,
+                                         int(groups), _ptr(out), _ptr(out_f32), _stream(stream)))
     return out
 
 

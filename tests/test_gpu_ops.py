@@ -271,3 +271,65 @@ def test_merge_candidates_matches_oracle(rt, world):
         n_valid = len(ref)
         assert np.array_equal(got[:n_valid], np.array(ref).reshape(n_valid, 4)), (world, trial)
         assert (got[n_valid:, 2] < 0).all()
+
+
+@pytest.mark.parametrize("hd,nq,nkv,groups", [(128, 32, 8, 0), (128, 32, 8, 1), (128, 32, 8, 2), (128, 64, 8, 1),
+                                              (64, 16, 4, 2), (64, 16, 2, 1), (32, 4, 1, 0)])
+def test_prefill_attention_causal(rt, hd, nq, nkv, groups):
+    """k_attn_prefill (rt_op_prefill_attention) per causal row against oracle.paged_attention:
+    prompt lengths 1 .. 2884 (PAPER.md:71 arm prompt), prompt rows starting at a prefix offset
+    pos0 > 0 (shared-prefix tails, R-PFX: 1216 = 76 pages) and at 0, ragged last tiles,
+    G = 1 / 2 / 4 / 8, one and two warp groups; rows sampled for the long prompts (every tile's
+    first and last row, the rows around each page boundary)."""
+    rng = np.random.default_rng(hd * 7 + nq + groups)
+    P = 16
+    # (prompt length, first prompt row position): tail prefill after a shared prefix or whole prompt
+    cases = [(1, 0), (15, 0), (17, 0), (100, 0), (1300, 1216), (2884, 2800), (1300, 0), (40, 32)]
+    if hd == 32:
+        cases = [(1, 0), (17, 0), (100, 0), (300, 256)]
+    max_pages = max((L + P - 1) // P for L, _ in cases)
+    n_pages = sum((L + P - 1) // P for L, _ in cases) + 3
+    perm = rng.permutation(n_pages)
+    tables, used = [], 0
+    for L, _ in cases:
+        k = (L + P - 1) // P
+        tables.append(list(perm[used:used + k]) + [0] * (max_pages - k))
+        used += k
+    kv_k = bf16_t(rng.standard_normal((n_pages * P, nkv, hd)))
+    kv_v = bf16_t(rng.standard_normal((n_pages * P, nkv, hd)))
+    pool = torch.zeros(n_pages * nkv * 64 * hd, dtype=torch.uint8, device="cuda")
+    rt.kv_write(pool, kv_k.cuda(), kv_v.cuda(), torch.arange(n_pages * P, dtype=torch.int32, device="cuda"), nkv, hd)
+    rows, tiles = [], []
+    for t, (L, start) in enumerate(cases):
+        for pos0 in range(start - start % P, L, P):
+            lo = max(pos0, start)
+            hi = min(pos0 + P, L)
+            # a tile's rows are consecutive positions pos0 + i; the first tile of a tail may start
+            # mid-page only when start is not page aligned (never here: prefixes are whole pages)
+            assert lo == pos0
+            tiles.append((len(rows), hi - lo, pos0, t))
+            rows += [(t, p) for p in range(lo, hi)]
+    q = bf16_t(rng.standard_normal((len(rows), nq, hd)))
+    out = torch.empty(len(rows), nq, hd, dtype=torch.bfloat16, device="cuda")
+    out32 = torch.full((len(rows), nq, hd), float("nan"), device="cuda")
+    pt = torch.tensor(np.array(tables, dtype=np.int32)).cuda()
+    tl = torch.tensor(np.array(tiles, dtype=np.int32)).cuda()
+    rt.prefill_attention(q.cuda(), pool, pt, tl, nq, nkv, hd, out, out32, groups=groups)
+    torch.cuda.synchronize()
+    kp = kv_k.float().numpy().reshape(n_pages, P, nkv, hd)
+    vp = kv_v.float().numpy().reshape(n_pages, P, nkv, hd)
+    o32 = out32.cpu().numpy()
+    ob = out.float().cpu().numpy()
+    qn = q.float().numpy()
+    sample = set()
+    for (r0, nr, pos0, t) in tiles:
+        sample.update({r0, r0 + nr - 1, r0 + nr // 2})
+    sample.update(int(x) for x in rng.choice(len(rows), size=min(len(rows), 48), replace=False))
+    worst = worst_b = 0.0
+    for i in sorted(sample):
+        t, p = rows[i]
+        ref = o_attn(qn[i], kp, vp, tables[t], p + 1)
+        worst = max(worst, float(np.abs(o32[i] - ref).max()))
+        worst_b = max(worst_b, float((np.abs(ob[i] - ref) - np.abs(ref) * 2.0 ** -8).max()))
+    assert worst < 6e-3, worst
+    assert worst_b < 1e-2, worst_b

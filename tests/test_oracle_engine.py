@@ -242,3 +242,41 @@ def test_submit_validation(tiny_vocab):
     with pytest.raises(OracleError) as ex:
         e.submit(0, [1] * 40, 0, 10, -1.0, 1.0, 0, 0, script=[5])     # 3 pages > pool of 2
     assert ex.value.code == "NOMEM"
+
+
+def test_wcet_lag_for_one_generation_hand_worked(tiny_vocab):
+    """Reading R-WCET ("By introducing a lag for one generation,
+    this method offers a profiling-independent strategy"): the gate of round r uses the speed
+    measured through round r-1 — no batch-latency model, unlike SPEC.md:325's scaled WCET.
+    Hand-worked on the paper-4090 VIRTUAL clock (base 21770 us, gamma 5 %, prefill 114 us/token),
+    max_admit_per_round = 1 (the paper's incremental growth), 1-token prompts, filler scripts:
+      round 0  t = 0       A admitted alone (no history); latency 21770 + 114 = 21884
+      round 1  t = 21884   gate protects A: D_A - t = 220000 - 21884 = 198116;
+                           (10 - 1) * 21884 = 196956 <= 198116 -> B admitted
+                           (SPEC's scaled rule: 196956 * 22858 / 21770 = 206799 > 198116 would refuse)
+                           latency 21770 + floor(21770 * 0.05) + 114 = 22972
+      round 2  t = 44856   D_A - t = 175144, n = 2, S = 44856: 8 * 44856 = 358848 > 2 * 175144 = 350288
+                           -> C refused (the gate sees the grown latency one generation later)
+    A's 10-token segment (CAP) then ends at 21884 + 22972 + 8 * 22858 = 227720: 7720 us past its
+    deadline — the overrun the one-generation lag allows (bounded by the latency growth of the
+    admissions the gate has not yet seen)."""
+    v = tiny_vocab
+    e = mk(v, max_batch=4, max_tasks=8, max_ctx=64, n_pages=16, max_admit_per_round=1)
+    filler = [5] * 30 + [v.eos_id]
+    ra = e.submit(0, [1], 0, 220_000, -2.0, 1.0, 0, 0, script=filler)
+    rb = e.submit(1, [1], 1, 100_000_000, -2.0, 1.0, 0, 0, script=filler)
+    rc = e.submit(2, [1], 2, 100_000_000, -2.0, 1.0, 0, 0, script=filler)
+    i0 = e.step()
+    assert (i0["t_us"], i0["n_admitted"], e.round_log[-1]["admitted"]) == (0, 1, [ra])
+    i1 = e.step()
+    assert (i1["t_us"], i1["n_admitted"], i1["n_refused_wcet"], e.round_log[-1]["admitted"]) == (21884, 1, 0, [rb])
+    i2 = e.step()
+    assert (i2["t_us"], i2["n_admitted"], i2["n_refused_wcet"]) == (44856, 0, 1)
+    assert 9 * 21884 == 196956 and 196956 * 22858 // 21770 == 206799
+    while True:
+        e.step()
+        segs = [s for s in e.poll() if s["request_id"] == ra]
+        if segs:
+            break
+    assert segs[0]["reason"] == STOP_CAP and segs[0]["tok_end"] == 10
+    assert segs[0]["dispatch_us"] == 21884 + 22972 + 8 * 22858 == 227720

@@ -16,20 +16,24 @@ from synth.traces import system_prefix  # noqa: E402
 
 
 def main(rounds=200, trace=False):
-    eng, now = profile_step.setup(bench.AGENTS_PER_GPU, flags=rt.RT_FLAG_TRACE if trace else rt.RT_FLAG_TIMING)
+    wl = os.environ.get("WORKLOAD", "C3")
+    eng, now = profile_step.setup(None, flags=rt.RT_FLAG_TRACE if trace else rt.RT_FLAG_TIMING, workload=wl)
     from synth import MODEL_SHAPES, make_vocab
+    from paper_2412_18695_b200 import replicas as R
     vocab = make_vocab(MODEL_SHAPES["llama3-8b"].vocab)
-    bench.drain(eng, now)
-    pfx = system_prefix(vocab, "drone", bench.PREFIX, seed=0)
-    eng.register_prefix(pfx)
+    R.lockstep_until_idle(lambda: eng.step(now()), None, max_rounds=4000)
+    eng.poll()
+    pfx = {r: system_prefix(vocab, r, bench.PREFIX[r], seed=0) for r in ("drone", "arm")}
+    for r in ("drone", "arm"):
+        eng.register_prefix(pfx[r])
     ordinal = {}
 
     def submit(agent):
         o = ordinal[agent] = ordinal.get(agent, 0) + 1
-        tr = bench.drone_request(vocab, agent, o, 0, prefix=pfx)
+        tr = bench.agent_request(wl, vocab, agent, o, 0, prefixes=pfx)
         eng.submit(agent, tr.prompt, now(), tr.ert_us, tr.alpha, tr.beta, 90000, script=tr.plan)
 
-    for a in range(bench.AGENTS_PER_GPU):
+    for a in range(bench.WORKLOADS[wl]["agents"]):
         submit(a)
     if trace:   # closed loop for a while, then the device trace of 10 rounds by kernel role
         for r in range(60):

@@ -139,12 +139,12 @@ def analyse(tr):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=3)
-    ap.add_argument("--agents", type=int, default=bench.AGENTS_PER_GPU)
-    ap.add_argument("--config", default="c2", choices=["c2", "c3"])
+    ap.add_argument("--agents", type=int, default=None)
+    ap.add_argument("--workload", default="C3", choices=sorted(bench.WORKLOADS))
     ap.add_argument("--json", default=None)
     ap.add_argument("--raw", default=None, help="save the raw per-CTA records (.npy)")
     a = ap.parse_args()
-    eng, now = profile_step.setup(a.agents, flags=rt.RT_FLAG_TRACE, config=a.config)
+    eng, now = profile_step.setup(a.agents, flags=rt.RT_FLAG_TRACE, workload=a.workload)
     eng.reset_stats()
     for _ in range(a.steps):
         eng.step(now())
