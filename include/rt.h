@@ -77,8 +77,12 @@ enum {
  * (DESIGN.md §6); the others force one kernel wherever it applies, for parity tests:
  *   RT_GEMM_PATH_SPLITK   k_gemm_tc: one 128-row tile per CTA, cluster split-K
  *   RT_GEMM_PATH_STREAMK  k_gemm_sk: hybrid data-parallel + stream-K (N > 128 rows)
- *   RT_GEMM_PATH_PAIR     k_gemm_2sm: CTA pairs, tcgen05.mma.cta_group::2 (N > 128 rows) */
-enum { RT_GEMM_PATH_AUTO = 0, RT_GEMM_PATH_SPLITK = 1, RT_GEMM_PATH_STREAMK = 2, RT_GEMM_PATH_PAIR = 3 };
+ *   RT_GEMM_PATH_PAIR     k_gemm_2sm: CTA pairs, tcgen05.mma.cta_group::2 (N > 128 rows)
+ *   RT_GEMM_PATH_DECPAIR  k_gemm_dec: CTA pairs + cluster split-K over pairs (N <= 256 rows,
+ *                         weight rows a multiple of 256, few pair-tiles; the default for
+ *                         129..256-row rounds) */
+enum { RT_GEMM_PATH_AUTO = 0, RT_GEMM_PATH_SPLITK = 1, RT_GEMM_PATH_STREAMK = 2, RT_GEMM_PATH_PAIR = 3,
+       RT_GEMM_PATH_DECPAIR = 4 };
 
 typedef struct rt_engine rt_engine;
 

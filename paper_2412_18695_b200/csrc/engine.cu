@@ -201,7 +201,7 @@ static rt_status validate(const rt_config* c) {
       (!c->tok_class || (c->stop_grammar == RT_GRAMMAR_SKILL && (!c->skill_base_us || !c->skill_unit_us))))
     return RT_E_INVAL;
   if (c->vocab < 2 || !c->tok_skill || !c->tok_exec_min_us) return RT_E_INVAL;
-  if (c->gemm_path < RT_GEMM_PATH_AUTO || c->gemm_path > RT_GEMM_PATH_PAIR) return RT_E_INVAL;
+  if (c->gemm_path < RT_GEMM_PATH_AUTO || c->gemm_path > RT_GEMM_PATH_DECPAIR) return RT_E_INVAL;
   if (c->eos_id < 0 || c->eos_id >= c->vocab) return RT_E_INVAL;
   // the device merge of the per-round candidates (k_merge_cand) holds world x kTopK keys in
   // shared memory: one node of <= 8 GPUs (BASELINE.json: one 8xB200 box)

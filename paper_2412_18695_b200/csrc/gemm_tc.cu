@@ -473,7 +473,7 @@ __device__ __forceinline__ void epilogue(const GemmArgs& g, const EpiSmem& sm, c
 // runs (returns true).
 template <int MODE>
 __device__ __forceinline__ bool column_meta(const GemmArgs& g, const EpiSmem& sm, int m_tile, int n0, int cb, int ce,
-                                         int et) {
+                                         int et, bool allow_pre = true) {
   if (MODE != EPI_QKV && MODE != EPI_RESID && !g.rs_ss) return false;
   for (int cc = cb + et; cc < ce; cc += 128) {
     const int n = n0 + cc;
@@ -503,7 +503,7 @@ __device__ __forceinline__ bool column_meta(const GemmArgs& g, const EpiSmem& sm
     }
   }
   epi_bar();
-  if (ce - cb > 16) return false;
+  if (ce - cb > 16 || !allow_pre) return false;
   const int m = m_tile * 128 + et;
   if constexpr (MODE == EPI_RESID) {
 #pragma unroll 1
@@ -1372,6 +1372,261 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
 }
 
+// ============================================================ decode CTA pairs, split-K
+// Decode rounds of N <= 256 rows on the few-tile projections (QKV, O, down: 16-24 pair-tiles
+// of 256 weight rows).  One SM per 128 x 256 tile is bound by SHARED-MEMORY bandwidth, not by
+// HBM: per k-block TMA writes A (16 KB) + B (32 KB) and the MMA reads them back, ~192 B/clk
+// against ~128 B/clk per SM (measured: QKV at N = 256 ran its mainloop at 3.6 TB/s).  Here a
+// CTA pair (cluster ranks 2p, 2p + 1) issues tcgen05.mma.cta_group::2 with M = 256: each CTA
+// holds its 128 weight rows and HALF of the activation rows, so the B operand per SM halves
+// (32 KB per k-block per SM: balanced with the MMA).  The K dimension is split over the S
+// pairs of a cluster of 2S CTAs so that S x pair-tiles fill the SMs (QKV 24 x 3, O / down
+// 16 x 4).  Reduction: after one cluster barrier (every MMA done, rings free) each CTA stores
+// the column slices it does not own from TMEM straight into the owner's shared memory (the
+// owner = the CTA of pair q with the same half), a second cluster barrier publishes them, and
+// the owner sums the S partials in pair order (deterministic).  The epilogue's global inputs
+// (EPI_RESID: residual x; EPI_QKV: the RoPE cos / sin rows of each column's position) are
+// bulk-copied into shared memory while the mainloop runs, so the fused epilogue loop never
+// waits on a global load (it was latency-bound on them at N = 256: 20 us for QKV).
+namespace dec {
+template <int BN>
+struct Cfg {
+  static constexpr int HB = BN / 2;                 // activation rows per CTA
+  static constexpr int A_BYTES = 128 * kBK * 2;     // 16 KB
+  static constexpr int B_BYTES = HB * kBK * 2;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int WMAX = BN / 2;               // widest owned column slice (S >= 2, 16-col grain)
+  static constexpr int XP_BYTES = WMAX * 512;       // prefetched epilogue inputs (128 floats / column)
+  static constexpr int CTL = 256;
+  static constexpr int META = 3 * BN * 4;
+  static constexpr int RED = 2 * 4 * BN * 4;
+  static constexpr int FIXED = 1024 + XP_BYTES + CTL + META + RED;
+  static constexpr int FIT = (227 * 1024 - FIXED) / STAGE;
+  static constexpr int STAGES = FIT > 8 ? 8 : FIT;
+  static constexpr int RING = STAGES * STAGE;
+  static constexpr int SMEM = FIXED + RING;
+  static_assert(STAGES >= 3, "decode pair ring depth");
+};
+// owned columns of pair p: 16-column chunks split as evenly as possible; a receive slot holds
+// the widest slice (dec_slot columns of 128 fp32)
+__host__ __device__ inline int dec_col(int BN, int S, int p) { return 16 * ((BN / 16) * p / S); }
+__host__ __device__ inline int dec_slot(int BN, int S) { return 16 * ((BN / 16 + S - 1) / S); }
+// the reduction area (S - 1 receive slots, in the ring after the mainloop) fits
+template <int BN>
+__host__ __device__ inline bool dec_fits(int S) {
+  return S >= 2 && S <= 8 && (S - 1) * dec_slot(BN, S) * 512 <= Cfg<BN>::RING;
+}
+}  // namespace dec
+
+template <int BN, int MODE>
+__global__ void __launch_bounds__(kGemmThreads, 1)
+    k_gemm_dec(const __grid_constant__ TmaMap tmA, const __grid_constant__ TmaMap tmB, GemmArgs g, int S) {
+  using C = dec::Cfg<BN>;
+  constexpr int STAGES = C::STAGES;
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  unsigned char* sA = smem;
+  unsigned char* sB = smem + STAGES * C::A_BYTES;
+  float* xp = reinterpret_cast<float*>(smem + C::RING);
+  unsigned char* ctl = smem + C::RING + C::XP_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(ctl);
+  uint64_t* empty = full + STAGES;
+  uint64_t* done = empty + STAGES;
+  uint64_t* pf_bar = done + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pf_bar + 1);
+  EpiSmem sm;
+  sm.pos = reinterpret_cast<int*>(ctl + C::CTL);
+  sm.page = sm.pos + BN;
+  sm.inv = reinterpret_cast<float*>(sm.page + BN);
+  sm.redv = reinterpret_cast<float*>(ctl + C::CTL + C::META);
+  sm.redi = reinterpret_cast<int*>(sm.redv + 4 * BN);
+  sm.bn = BN;
+  sm.xp = xp;
+  sm.xp_sin = C::WMAX * 64;
+  __shared__ long long s_mark[9];
+  sm.mark = s_mark;
+
+  TraceScope tr(TK_GEMM | ((uint32_t)MODE << 8) | ((uint32_t)(2 * S) << 16));
+  __shared__ unsigned long long s_tdone;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const int p = (int)(rank >> 1), h = (int)(rank & 1);
+  const int t = (int)blockIdx.x / (2 * S);          // pair-tile
+  const int m_tile = 2 * t + h;
+  const int kbt = g.kb_total;
+  const int kb0 = (kbt * p) / S, kb1 = (kbt * (p + 1)) / S;
+  const int cb = dec::dec_col(BN, S, p), ce = dec::dec_col(BN, S, p + 1);
+  const uint32_t leader = (uint32_t)(2 * p);
+  const uint16_t pmask = (uint16_t)(0x3u << (2 * p));
+
+  if (warp == 0 && lane == 0) {
+    prefetch_tmap(&tmA);
+    prefetch_tmap(&tmB);
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(&full[i], 1);
+      mbar_init(&empty[i], 1);
+    }
+    mbar_init(done, 1);
+    mbar_init(pf_bar, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_arrive();  // every CTA's barriers are initialised before anyone signals them
+  cluster_wait();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (MODE != EPI_QKV && threadIdx.x == 0) pdl_trigger();
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint32_t full0 = dsmem_addr(smem_u32(full), leader);  // the pair leader's full barriers
+      const uint32_t bytes = 2u * C::STAGE;
+      const int pre_k = min(STAGES, kb1 - kb0);
+      // weights do not depend on the previous kernel: the first stages before its completion
+      for (int i = 0; i < pre_k; ++i) {
+        if (h == 0) mbar_arrive_expect_tx(&full[i], bytes);
+        tma_load_2d_pair(sA + i * C::A_BYTES, &tmA, 0, (m_tile * kbt + kb0 + i) * 128, full0 + i * 8);
+      }
+      pdl_wait();
+      if (MODE == EPI_QKV) pdl_trigger();
+      tr.ready();
+      for (int i = 0; i < pre_k; ++i)
+        tma_load_2d_pair(sB + i * C::B_BYTES, &tmB, (kb0 + i) * kBK, h * C::HB, full0 + i * 8);
+      for (int i = pre_k; i < kb1 - kb0; ++i) {
+        const int st = i % STAGES;
+        mbar_wait(&empty[st], (uint32_t)(((i / STAGES) & 1) ^ 1));
+        if (h == 0) mbar_arrive_expect_tx(&full[st], bytes);
+        tma_load_2d_pair(sA + st * C::A_BYTES, &tmA, 0, (m_tile * kbt + kb0 + i) * 128, full0 + st * 8);
+        tma_load_2d_pair(sB + st * C::B_BYTES, &tmB, (kb0 + i) * kBK, h * C::HB, full0 + st * 8);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (h == 0 && lane == 0) {
+      constexpr uint32_t idesc = umma_idesc(256, BN);
+      for (int i = 0; i < kb1 - kb0; ++i) {
+        const int st = i % STAGES;
+        mbar_wait(&full[st], (uint32_t)((i / STAGES) & 1));
+        tc_fence_after();
+        const uint32_t a0 = smem_u32(sA + st * C::A_BYTES);
+        const uint32_t b0 = smem_u32(sB + st * C::B_BYTES);
+#pragma unroll
+        for (int k = 0; k < kBK / 16; ++k)
+          umma_f16_pair(tmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
+                        (i > 0 || k > 0) ? 1u : 0u);
+        umma_commit_pair(&empty[st], pmask);
+      }
+      umma_commit_pair(done, pmask);
+    }
+    __syncwarp();
+  } else {
+    pdl_wait();
+    const int et = (warp & 3) * 32 + lane;
+    const uint32_t tb = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+    // per-column metadata of the owned columns, then their epilogue inputs -> shared memory
+    // (bulk copies on pf_bar) while the mainloop runs
+    column_meta<MODE>(g, sm, m_tile, 0, cb, ce, et, false);
+    if (et == 0) {
+      uint32_t pf = 0;
+      if constexpr (MODE == EPI_RESID) {
+        for (int c = cb; c < ce && c < g.N; ++c) pf += 512;
+        mbar_arrive_expect_tx(pf_bar, pf);
+        for (int c = cb; c < ce && c < g.N; ++c)
+          bulk_g2s(xp + (c - cb) * 128, g.x + (size_t)c * g.M + m_tile * 128, 512, pf_bar);
+      } else if constexpr (MODE == EPI_QKV) {
+        const int half = g.qkv.hd >> 1;
+        const uint32_t rb = (uint32_t)half * 4;
+        for (int c = cb; c < ce && c < g.N; ++c) pf += 2 * rb;
+        mbar_arrive_expect_tx(pf_bar, pf);
+        for (int c = cb; c < ce && c < g.N; ++c) {
+          const int pos = sm.pos[c];
+          bulk_g2s(xp + (c - cb) * 64, g.qkv.cos + (size_t)pos * half, rb, pf_bar);
+          bulk_g2s(xp + sm.xp_sin + (c - cb) * 64, g.qkv.sin + (size_t)pos * half, rb, pf_bar);
+        }
+      } else {
+        mbar_arrive(pf_bar);
+      }
+    }
+    mbar_wait(done, 0);
+    tc_fence_after();
+    if (et == 0) s_tdone = gtimer();
+  }
+  // ---- split-K reduction over the S pairs (every warp takes part in the cluster barriers):
+  // receive slot j at ring offset j * wslot columns; the summed owned slice T overwrites slot 0
+  // (each element is read, then written, by the same thread)
+  const int wslot = dec::dec_slot(BN, S);
+  float* T = reinterpret_cast<float*>(smem);
+  __syncwarp();
+  cluster_arrive();  // A: every MMA of the cluster is done -> every ring is free
+  cluster_wait();
+  if (warp >= 2) {
+    const int et = (warp & 3) * 32 + lane;
+    const uint32_t tb = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+    for (int q = 0; q < S; ++q) {  // push the slice owned by pair q (same half) into its slot p'
+      if (q == p) continue;
+      const int qb = dec::dec_col(BN, S, q), qe = dec::dec_col(BN, S, q + 1);
+      const int slot = p < q ? p : p - 1;
+      const uint32_t dst = dsmem_addr(smem_u32(smem), (uint32_t)(2 * q + h)) + (uint32_t)(slot * wslot * 512);
+#pragma unroll 1
+      for (int c0 = qb; c0 < qe; c0 += 16) {
+        float v[16];
+        tmem_ld16(tb + (uint32_t)c0, v);
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(dst + (uint32_t)(((c0 - qb + j) * 128 + et) * 4)),
+                       "f"(v[j])
+                       : "memory");
+      }
+    }
+  }
+  __syncwarp();
+  cluster_arrive();  // B (release / acquire): the slices are visible to their owners
+  cluster_wait();
+  if (warp >= 2) {
+    const int et = (warp & 3) * 32 + lane;
+    const uint32_t tb = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+    const float* R = reinterpret_cast<const float*>(smem);
+#pragma unroll 1
+    for (int c0 = cb; c0 < ce; c0 += 16) {  // sum the S partials in pair order (deterministic)
+      float own[16], acc[16];
+      tmem_ld16(tb + (uint32_t)c0, own);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) acc[j] = 0.f;
+      for (int q = 0; q < S; ++q) {
+        if (q == p) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) acc[j] += own[j];
+        } else {
+          const float* src = R + (size_t)(q < p ? q : q - 1) * wslot * 128 + (size_t)(c0 - cb) * 128 + et;
+#pragma unroll
+          for (int j = 0; j < 16; ++j) acc[j] += src[j * 128];
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 16; ++j) T[(c0 - cb + j) * 128 + et] = acc[j];
+    }
+    mbar_wait(pf_bar, 0);  // prefetched epilogue inputs
+    epi_bar();
+    const TileSrc ts{T - (size_t)cb * 128, nullptr, 0u, 1, 0, BN, 0, 0};
+    epilogue<MODE>(g, sm, ts, m_tile, 0, cb, ce, et, true);
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x == 0) tr.aux(s_tdone);
+  cluster_arrive();  // no CTA deallocates while its pair peer may still use the shared TMEM pair state
+  cluster_wait();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));
+  }
+}
+
 // ------------------------------------------------------------- host side
 static PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -1673,14 +1928,91 @@ static int pair_slots(int bn) {
   return bn == 160 ? pair_slots_bn<160>() : (bn == 192 ? pair_slots_bn<192>() : pair_slots_bn<256>());
 }
 
+
+// ---- decode CTA-pair split-K launch (k_gemm_dec)
+template <int BN, int MODE>
+static cudaError_t launch_dec_bn(const TmaMap& am, const TmaMap& bm, const GemmArgs& g, int PT, int S,
+                                 cudaStream_t s) {
+  using C = dec::Cfg<BN>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_gemm_dec<BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+    cudaFuncSetAttribute(k_gemm_dec<BN, MODE>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    attr = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * S * PT);
+  cfg.blockDim = dim3(kGemmThreads);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2 * S;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, k_gemm_dec<BN, MODE>, am, bm, g, S);
+}
+template <int MODE>
+static cudaError_t launch_dec_mode(const TmaMap& am, const GemmTmaSet& x, const GemmArgs& g, int bn, int PT, int S,
+                                   cudaStream_t s) {
+  if (bn == 64) return launch_dec_bn<64, MODE>(am, x.m32, g, PT, S, s);
+  if (bn == 128) return launch_dec_bn<128, MODE>(am, x.m64, g, PT, S, s);
+  return launch_dec_bn<256, MODE>(am, x.m128, g, PT, S, s);
+}
+// split count of the decode pair kernel: S x pair-tiles <= the SM pairs (one CTA per SM),
+// >= 4 k-blocks per pair, reduction area within the ring
+static int dec_splits(int BN, int PT, int kbt) {
+  const int pairs = sm_count() / 2;
+  int best = 0;
+  for (int S = 2; S <= 8; ++S) {
+    const bool fits = BN == 64 ? dec::dec_fits<64>(S) : (BN == 128 ? dec::dec_fits<128>(S) : dec::dec_fits<256>(S));
+    if (fits && PT * S <= pairs && kbt / S >= 4) best = S;
+  }
+  return best;
+}
+// launch the decode pair kernel if it applies (returns cudaErrorNotSupported otherwise)
+static cudaError_t try_launch_dec(const bf16* w_tiled, const GemmTmaSet& x, GemmArgs g, cudaStream_t s) {
+  const int m_tiles = (g.M + 127) / 128;
+  if (g.N > 256 || g.N < 1 || g.M % 256 || g.K % kBK || g.mode == EPI_ARGMAX) return cudaErrorNotSupported;
+  const int bn = g.N <= 64 ? 64 : (g.N <= 128 ? 128 : 256);
+  const int PT = m_tiles / 2;
+  const int kbt = g.K / kBK;
+  const int S = dec_splits(bn, PT, kbt);
+  if (S < 2) return cudaErrorNotSupported;
+  const TmaMap* am = weight_map(w_tiled, (uint64_t)m_tiles * kbt * 128);
+  if (!am) return cudaErrorNotSupported;
+  g.w = w_tiled;
+  g.kb_total = kbt;
+  g.m_tiles = m_tiles;
+  g.n_tiles = 1;
+  g.l2_evict_first = 0;
+  switch (g.mode) {
+    case EPI_STORE: return launch_dec_mode<EPI_STORE>(*am, x, g, bn, PT, S, s);
+    case EPI_QKV: return launch_dec_mode<EPI_QKV>(*am, x, g, bn, PT, S, s);
+    case EPI_RESID: return launch_dec_mode<EPI_RESID>(*am, x, g, bn, PT, S, s);
+    case EPI_SWIGLU: return launch_dec_mode<EPI_SWIGLU>(*am, x, g, bn, PT, S, s);
+    default: return cudaErrorNotSupported;
+  }
+}
+
 int64_t gemm_sk_ws_floats() { return (int64_t)sm_count() * 2 * 256 * 128; }
 
 cudaError_t launch_gemm_epi(const bf16* w_tiled, const GemmTmaSet& x, GemmArgs g, int splits, cudaStream_t s) {
+  // decode rows on the few-tile projections (<= 256 rows, 129..256 by default): CTA pairs with
+  // a cluster split-K (k_gemm_dec)
+  if (g.force_path == GEMM_PATH_DEC || (g.force_path == GEMM_PATH_AUTO && g.N > 128 && g.N <= 256)) {
+    const cudaError_t r = try_launch_dec(w_tiled, x, g, s);
+    if (r != cudaErrorNotSupported) return r;
+  }
   const GemmChoice gc = gemm_choice(g.M, g.K, g.N, g.force_bn, g.force_path);
   const int bn = gc.bn;
   // CTA-pair kernel for the tensor-bound prefill path: every pair busy (at least one
   // pair-tile per co-resident pair) and an even number of 128-row m-tiles
-  if (g.N > 128 && g.mode != EPI_ARGMAX && g.K % kBK == 0 && gc.pair) {
+  if (g.N > 128 && g.K % kBK == 0 && gc.pair) {
     const int m_tiles = (g.M + 127) / 128, n_tiles = (g.N + bn - 1) / bn;
     const int PT = (m_tiles / 2) * n_tiles;
     const int slots = pair_slots(bn);
@@ -1696,6 +2028,7 @@ cudaError_t launch_gemm_epi(const bf16* w_tiled, const GemmTmaSet& x, GemmArgs g
         a.n_tiles = n_tiles;
         switch (g.mode) {
           case EPI_STORE: return launch_2sm_mode<EPI_STORE>(*am, x, g, bn, PT, a, s);
+          case EPI_ARGMAX: return launch_2sm_mode<EPI_ARGMAX>(*am, x, g, bn, PT, a, s);
           case EPI_QKV: return launch_2sm_mode<EPI_QKV>(*am, x, g, bn, PT, a, s);
           case EPI_RESID: return launch_2sm_mode<EPI_RESID>(*am, x, g, bn, PT, a, s);
           case EPI_SWIGLU: return launch_2sm_mode<EPI_SWIGLU>(*am, x, g, bn, PT, a, s);
@@ -1720,7 +2053,9 @@ cudaError_t launch_gemm_epi(const bf16* w_tiled, const GemmTmaSet& x, GemmArgs g
     // only with a data-parallel part (T > 2 waves): measured faster there (gate/up N = 320 /
     // 384 / 512: 103 / 108 / 122 -> 89 / 95 / 116 us) and slower for all-stream-K shapes
     // (few-tile projections pay multi-contributor fixups; the cluster split-K path is better)
-    const int min_t = g.force_path == GEMM_PATH_STREAMK ? 1 : 2 * P + 1;
+    // (all-stream-K at <= 2 waves is not supported: it measured slower, RT_SK_MODE in round 1,
+    // and its fixup schedule assumes the data-parallel waves in front)
+    const int min_t = 2 * P + 1;
     a.all_sk = T <= 2 * P ? 1 : 0;
     if (T <= g.sk_cnt_cap && I_sk >= P && T >= min_t) {
       a.P = P;

@@ -95,7 +95,8 @@ enum EpiMode { EPI_STORE = 0, EPI_ARGMAX = 1, EPI_QKV = 2, EPI_RESID = 3, EPI_SW
 // projection kernel paths (GemmArgs::force_path; the values of rt.h RT_GEMM_PATH_*):
 // AUTO = measured dispatch; SPLITK = k_gemm_tc (cluster split-K / one tile per CTA);
 // STREAMK = k_gemm_sk (hybrid data-parallel + stream-K, N > 128); PAIR = k_gemm_2sm (CTA pairs, N > 128)
-enum GemmPath { GEMM_PATH_AUTO = 0, GEMM_PATH_SPLITK = 1, GEMM_PATH_STREAMK = 2, GEMM_PATH_PAIR = 3 };
+// DEC = k_gemm_dec (CTA pairs + cluster split-K, N <= 256, few pair-tiles)
+enum GemmPath { GEMM_PATH_AUTO = 0, GEMM_PATH_SPLITK = 1, GEMM_PATH_STREAMK = 2, GEMM_PATH_PAIR = 3, GEMM_PATH_DEC = 4 };
 
 struct QkvFuse {
   const int32_t *row_task, *row_pos, *page_table;

@@ -18,7 +18,7 @@ RT_POLICY_PUD, RT_POLICY_FCFS, RT_POLICY_EDF = 0, 1, 2
 RT_STOP_NONE, RT_STOP_EOS, RT_STOP_MAXNEW, RT_STOP_SKILL, RT_STOP_CAP = 0, 1, 2, 3, 4
 RT_FLAG_NO_MODEL, RT_FLAG_KEEP_LOGITS, RT_FLAG_CAPTURE, RT_FLAG_TIMING, RT_FLAG_FORCE_EXCHANGE = 1, 2, 4, 8, 16
 RT_FLAG_TRACE = 64
-RT_GEMM_PATH_AUTO, RT_GEMM_PATH_SPLITK, RT_GEMM_PATH_STREAMK, RT_GEMM_PATH_PAIR = 0, 1, 2, 3
+RT_GEMM_PATH_AUTO, RT_GEMM_PATH_SPLITK, RT_GEMM_PATH_STREAMK, RT_GEMM_PATH_PAIR, RT_GEMM_PATH_DECPAIR = 0, 1, 2, 3, 4
 (RT_DUMP_TASKS, RT_DUMP_PAGE_TABLES, RT_DUMP_ROUND, RT_DUMP_LOGITS, RT_DUMP_HIDDEN, RT_DUMP_CAPTURE_Q,
  RT_DUMP_CAPTURE_O, RT_DUMP_ROWS, RT_DUMP_KV_LAYER, RT_DUMP_FREE_STACK, RT_DUMP_TASK_SLOTS,
  RT_DUMP_MERGED, RT_DUMP_TRACE, RT_DUMP_HOST_PAGE_TABLES, RT_DUMP_HOST_FREE_STACK, RT_DUMP_LAYER_X, RT_DUMP_LAYER_Q,

@@ -119,7 +119,7 @@ class Checker:
         self.note("x_after_down", np.abs(xo[:, fd] - ref).max() / np.sqrt(ff / 512))
 
 
-def run_fullsize(rt, shape, gemm_path=0, n_dec=64, n_tail=8, seed=31):
+def run_fullsize(rt, shape, gemm_path=0, n_dec=64, n_tail=8, seed=31, mixed=True):
     """64 drone requests (1300-token private prompts, contexts >= 1300 after the first
     decode rounds) decoding, then n_tail requests whose prompts start with the registered
     1216-token drone prefix: the checked round has 64 decode rows + 8 x 84 prefill rows."""
@@ -159,6 +159,9 @@ def run_fullsize(rt, shape, gemm_path=0, n_dec=64, n_tail=8, seed=31):
         return ck.worst
 
     w_dec = check_round("decode")
+    if not mixed:
+        eng.close()
+        return w_dec, None, checked
     # the mixed round: n_tail prefix-sharing requests admitted next to the 64 running ones
     for a in range(n_tail):
         tr = make_trace(1 + a % 5, v, seed=5000 + a, prefix=pfx, plan_len=plan)
@@ -202,3 +205,16 @@ def test_llama70b_dims_every_fused_op_vs_oracle(rt):
     print(checked)
     assert_within(w_dec)
     assert_within(w_mix)
+
+
+@pytest.mark.parametrize("n_dec,gemm_path", [(256, 0), (200, 0), (64, 4), (128, 4)])
+def test_llama8b_dims_decode_pair_splitk_vs_oracle(rt, n_dec, gemm_path):
+    """The C3 decode round (256 rows; 200 = a ragged batch) runs QKV / O / down on the CTA-pair
+    cluster split-K kernel (k_gemm_dec: QKV 24 pair-tiles x 3 splits, O / down 16 x 4) and
+    gate/up on the persistent pair kernel; 64 / 128 rows force k_gemm_dec (gemm_path 4) at
+    BN = 64 / 128.  Every fused op of both layers vs the oracle on the GPU's own inputs."""
+    s8 = MODEL_SHAPES["llama3-8b"]
+    shape = ModelShape("8b-2l", 2, s8.d_model, s8.n_q_heads, s8.n_kv_heads, s8.head_dim, s8.d_ff, s8.vocab)
+    w_dec, _, checked = run_fullsize(rt, shape, gemm_path, n_dec=n_dec, n_tail=0, mixed=False)
+    print(checked)
+    assert_within(w_dec)

@@ -116,12 +116,22 @@ def test_gemm_cta_pair(rt, M, N, K):
     _gemm_tiled_case(rt, M, N, K, rt.RT_GEMM_PATH_PAIR)
 
 
-@pytest.mark.parametrize("M,N,K,bn", [(28672, 256, 512, 256), (6144, 161, 1024, 160), (4096, 384, 2048, 192),
-                                      (1024, 300, 768, 0), (384, 150, 512, 0)])
+@pytest.mark.parametrize("M,N,K,bn", [(28672, 512, 512, 256), (9728, 1024, 512, 0), (6144, 1600, 1024, 160),
+                                      (4096, 1600, 2048, 192), (28672, 330, 768, 160)])
 def test_gemm_streamk(rt, M, N, K, bn):
-    """Hybrid data-parallel + stream-K (k_gemm_sk) forced for any tile count (all-stream-K
-    at <= 2 waves: multi-contributor fixups)."""
+    """Hybrid data-parallel + stream-K (k_gemm_sk, more than two waves of tiles: the full waves
+    but one data-parallel, the rest stream-K with multi-contributor fixups), CTA pairs excluded."""
     _gemm_tiled_case(rt, M, N, K, rt.RT_GEMM_PATH_STREAMK, bn=bn)
+
+
+@pytest.mark.parametrize("M,N,K", [(6144, 256, 4096), (4096, 256, 4096), (4096, 256, 14336), (6144, 200, 4096),
+                                   (4096, 64, 4096), (6144, 33, 1024), (512, 129, 512), (4096, 128, 14336),
+                                   (8192, 256, 8192), (10240, 256, 8192)])
+def test_gemm_decode_pair_splitk(rt, M, N, K):
+    """k_gemm_dec (RT_GEMM_PATH_DECPAIR): CTA pairs (cta_group::2, M = 256) with a cluster split-K
+    over pairs and the DSMEM reduction, at the 8B / 70B decode shapes (QKV 6144 / 10240, O and
+    down 4096 / 8192 rows) and ragged batches (33, 129, 200 rows)."""
+    _gemm_tiled_case(rt, M, N, K, 4)
 
 
 @pytest.mark.parametrize("M,N,K,bn", [(28672, 256, 512, 256), (6144, 200, 1024, 0), (4096, 384, 2048, 192)])
@@ -130,7 +140,8 @@ def test_gemm_splitk_wide(rt, M, N, K, bn):
     _gemm_tiled_case(rt, M, N, K, rt.RT_GEMM_PATH_SPLITK, bn=bn)
 
 
-@pytest.mark.parametrize("M,N,K", [(512, 4, 128), (128256, 64, 1024), (1000, 33, 256)])
+@pytest.mark.parametrize("M,N,K", [(512, 4, 128), (128256, 64, 1024), (1000, 33, 256), (128256, 256, 1024),
+                                   (20480, 200, 512)])
 def test_lm_argmax(rt, M, N, K):
     g = torch.Generator().manual_seed(N)
     W = (torch.randn(M, K, generator=g) * 0.02).to(torch.bfloat16)

@@ -15,7 +15,7 @@ from synth import MODEL_SHAPES, make_vocab, engine_params  # noqa: E402
 from paper_2412_18695_b200 import rt  # noqa: E402
 
 
-def setup(B=None, flags=0, workload="C2"):
+def setup(B=None, flags=0, workload="C2", gemm_path=0):
     """The bench's steady state for a workload (bench.WORKLOADS: C2 / C3 / C4): its agents
     resident, decode-only rounds.  B overrides the agent count."""
     shape = MODEL_SHAPES["llama3-8b"]
@@ -26,7 +26,7 @@ def setup(B=None, flags=0, workload="C2"):
     n_pages = min(B * ((max_ctx + 15) // 16), 56 * 1024)
     p = engine_params("b200-roofline", max_batch=B, max_tasks=4 * B, max_ctx=max_ctx, n_pages=n_pages,
                       clock_mode=1)
-    eng = rt.Engine(shape, p, vocab, seed=1234, flags=flags, max_rows_per_forward=8192)
+    eng = rt.Engine(shape, p, vocab, seed=1234, flags=flags, max_rows_per_forward=8192, gemm_path=gemm_path)
     t0 = time.perf_counter()
     now = lambda: int((time.perf_counter() - t0) * 1e6)  # noqa: E731
     for j in range(B):

@@ -141,10 +141,11 @@ def main():
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--agents", type=int, default=None)
     ap.add_argument("--workload", default="C3", choices=sorted(bench.WORKLOADS))
+    ap.add_argument("--gemm-path", type=int, default=0)
     ap.add_argument("--json", default=None)
     ap.add_argument("--raw", default=None, help="save the raw per-CTA records (.npy)")
     a = ap.parse_args()
-    eng, now = profile_step.setup(a.agents, flags=rt.RT_FLAG_TRACE, workload=a.workload)
+    eng, now = profile_step.setup(a.agents, flags=rt.RT_FLAG_TRACE, workload=a.workload, gemm_path=a.gemm_path)
     eng.reset_stats()
     for _ in range(a.steps):
         eng.step(now())
