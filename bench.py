@@ -286,8 +286,14 @@ def run_ours(args, rank, world, dist):
     # registered once as shared prefixes, requests prefill only their task
     # part.  B is the headline `e2e` (the paper's server stores the fixed prompt components).
     launches_per_step = st["kernel_launches"] / max(st["rounds"], 1) + 2   # forward + sched pre/post
+    # both closed loops start from an idle engine with every agent submitting, and run long
+    # enough (E2E_STEPS rounds) for robot-arm plans (~100 tokens in ~10 segments) to finish
+    # and resubmit
+    R.lockstep_until_idle(lambda: eng.step(now()), dist, max_rounds=4000)
+    eng.poll()
+    eng.sync()
     e2e_private = run_e2e(args, eng, vocab, p, rank, world, now, dist, reqs, prefixes=None,
-                          steps=max(4, K // 2))
+                          start_agents=agents, steps=max(K, args.e2e_steps // 2))
     e2e_private.pop("_segments")
     R.lockstep_until_idle(lambda: eng.step(now()), dist, max_rounds=4000)
     eng.poll()
@@ -295,7 +301,8 @@ def run_ours(args, rank, world, dist):
     pfx = {r: system_prefix(vocab, r, PREFIX[r], seed=args.seed) for r in ("drone", "arm")}
     for r in ("drone", "arm"):
         eng.register_prefix(pfx[r])
-    e2e = run_e2e(args, eng, vocab, p, rank, world, now, dist, reqs, prefixes=pfx, start_agents=agents)
+    e2e = run_e2e(args, eng, vocab, p, rank, world, now, dist, reqs, prefixes=pfx, start_agents=agents,
+                  steps=max(K, args.e2e_steps))
     e2e["shared_prefix_tokens"] = PREFIX
     util = M.report(e2e.pop("_segments"), reqs, vocab, net_us=p.net_us, seed=args.seed)
 
@@ -550,6 +557,7 @@ def main():
     ap.add_argument("--workload", default="C3", choices=sorted(WORKLOADS))
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=160, help="rounds of each closed-loop e2e pass")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world = int(os.environ.get("WORLD_SIZE", "1"))

@@ -107,6 +107,10 @@ struct rt_engine {
   int* d_attn_tickets = nullptr;
   int* d_gemm_cnt = nullptr;
   GemmTmaSet x_h, x_o, x_act, x_hfin;
+  float* d_dec_ws = nullptr;     // decode-pair split-K exchange (k_gemm_dec)
+  int64_t dec_ws_floats = 0;
+  unsigned* d_dec_flags = nullptr;
+  unsigned dec_epoch = 0;
   float* d_sk_ws = nullptr;      // stream-K partial tiles (prefill projections, N > 128 rows)
   unsigned* d_sk_cnt = nullptr;  // stream-K tile tickets
   int sk_cnt_cap = 0;
@@ -505,6 +509,16 @@ static rt_status create_impl(rt_engine* e, const rt_config* cfg) {
     if (!ok) return done(fail(e, RT_E_CUDA, "cuTensorMapEncodeTiled failed (activations)"));
     e->ev_attn.resize(2 * L);
     for (auto& ev : e->ev_attn) cudaEventCreate(&ev);
+    // decode-pair split-K exchange workspace (k_gemm_dec), sized for the model's projections
+    {
+      const int shapes[4][2] = {{e->qkv_dim, d}, {d, nq * hd}, {2 * ff, d}, {d, ff}};
+      for (auto& sh : shapes)
+        e->dec_ws_floats = std::max(e->dec_ws_floats, gemm_dec_ws_floats(sh[0], 256, sh[1]));
+      if (e->dec_ws_floats > 0) {
+        CK(e, dalloc(e, &e->d_dec_ws, (size_t)e->dec_ws_floats));
+        CK(e, dalloc(e, &e->d_dec_flags, (size_t)kDecFlags));
+      }
+    }
     // hybrid DP + stream-K workspace of the prefill projections (gemm_tc.cu k_gemm_sk)
     {
       const int max_mt = (std::max(std::max(e->qkv_dim, d), 2 * ff) + 127) / 128;
@@ -830,6 +844,11 @@ static rt_status forward(rt_engine* e, const HostMailbox& plan) {
       g.sk_cnt = e->d_sk_cnt;
       g.sk_cnt_cap = e->sk_cnt_cap;
       g.force_path = c.gemm_path;
+      g.dec_ws = e->d_dec_ws;
+      g.dec_ws_floats = e->dec_ws_floats;
+      g.dec_flags = e->d_dec_flags;
+      g.dec_flags_cap = kDecFlags;
+      g.dec_epoch = ++e->dec_epoch;
       launch_gemm_epi(w, x, g, 0, s);
       ++launches;
     };

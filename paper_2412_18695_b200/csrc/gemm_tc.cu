@@ -153,6 +153,7 @@ struct EpiSmem {
   float* xp;     // [16][128] epilogue inputs prefetched during the mainloop (EPI_RESID x;
                  //  EPI_QKV cos [16][64] then sin [16][64])
   long long* mark;  // clock64 phase marks (trace), written by thread et == 0
+  bf16* stg = nullptr;  // nullable: EPI_QKV staging [2][16][128] bf16 (whole head rows, 16-byte stores)
 };
 #define EPI_MARK(i) \
   if (et == 0) sm.mark[i] = clock64()
@@ -384,7 +385,36 @@ __device__ __forceinline__ void epilogue(const GemmArgs& g, const EpiSmem& sm, c
         const float y = rope ? (odd ? v[k] * ca[k] + u[k] * cbv[k] : v[k] * ca[k] - u[k] * cbv[k]) : v[k];
         yb[k] = __float2bfloat16_rn(y);
       }
-      if (active) {
+      if (sm.stg && hd == 128 && !q.q_cap) {
+        // staged: the 128 rows of this m-tile are one head (CTA-uniform q / k / v); the chunk's
+        // 16 head rows (256 B each) go out as 16-byte stores, 2 per thread (2-byte scattered
+        // stores made this loop store-bound at 256 rows: ~8 us for 96 columns)
+        bf16* st = sm.stg + (((c0 - cb) / CH) & 1) * (CH * 128);
+#pragma unroll
+        for (int k = 0; k < CH; ++k) st[k * 128 + dim] = yb[k];
+        epi_bar();
+        if (active) {
+          const int kind = head < q.nq ? 2 : (rope ? 0 : 1);
+          const int kvh = kind == 0 ? head - q.nq : head - q.nq - q.nkv;
+#pragma unroll
+          for (int w = 0; w < 2; ++w) {
+            const int item = et + 128 * w, k = item >> 4, cc = item & 15;
+            const int c = c0 + k;
+            if (c < NL) {
+              const uint4 val = *reinterpret_cast<const uint4*>(st + k * 128 + cc * 8);
+              unsigned char* dst;
+              if (kind == 2) {
+                dst = (unsigned char*)(q.q_out + ((size_t)(n0 + c) * q.nq + head) * 128) + cc * 16;
+              } else {
+                const int pos = sm.pos[c], pg = sm.page[c], off = pos & 15;
+                dst = (unsigned char*)q.pool + (((size_t)pg * q.nkv + kvh) * 2 + kind) * (size_t)(16 * 128 * 2) +
+                      off * 256 + (kv_swz_chunk(128, off, cc) << 4);
+              }
+              *reinterpret_cast<uint4*>(dst) = val;
+            }
+          }
+        }
+      } else if (active) {
         if (head < q.nq) {  // warp-uniform (a head is 128 rows)
 #pragma unroll
           for (int k = 0; k < CH; ++k)
@@ -934,7 +964,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       Sched::Seg sg;
       for (bool ok = S.first(sg, d, q); ok; ok = S.next(sg, d, q)) {
         const int m_tile = sg.tile / a.n_tiles, n_tile = sg.tile - m_tile * a.n_tiles;
-        for (int kb = 0; kb < kbt; ++kb, ++n) {
+        for (int kb = sg.lo; kb < sg.hi; ++kb, ++n) {
           const int st = n % STAGES;
           if (n >= STAGES) mbar_wait(&empty[st], (uint32_t)(((n / STAGES) & 1) ^ 1));
           mbar_arrive_expect_tx(&full[st], A_BYTES + C::B_BYTES);
@@ -1377,14 +1407,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 // of 256 weight rows).  One SM per 128 x 256 tile is bound by SHARED-MEMORY bandwidth, not by
 // HBM: per k-block TMA writes A (16 KB) + B (32 KB) and the MMA reads them back, ~192 B/clk
 // against ~128 B/clk per SM (measured: QKV at N = 256 ran its mainloop at 3.6 TB/s).  Here a
-// CTA pair (cluster ranks 2p, 2p + 1) issues tcgen05.mma.cta_group::2 with M = 256: each CTA
-// holds its 128 weight rows and HALF of the activation rows, so the B operand per SM halves
-// (32 KB per k-block per SM: balanced with the MMA).  The K dimension is split over the S
-// pairs of a cluster of 2S CTAs so that S x pair-tiles fill the SMs (QKV 24 x 3, O / down
-// 16 x 4).  Reduction: after one cluster barrier (every MMA done, rings free) each CTA stores
-// the column slices it does not own from TMEM straight into the owner's shared memory (the
-// owner = the CTA of pair q with the same half), a second cluster barrier publishes them, and
-// the owner sums the S partials in pair order (deterministic).  The epilogue's global inputs
+// CTA pair (a cluster of 2) issues tcgen05.mma.cta_group::2 with M = 256: each CTA holds its
+// 128 weight rows and HALF of the activation rows, so the B operand per SM halves (32 KB per
+// k-block per SM: balanced with the MMA).  The K dimension is split over S pairs so that
+// S x pair-tiles fill the SMs (QKV 24 x 3, O / down 16 x 4), one CTA per SM.
+// Split-K reduction through L2, not DSMEM: clusters of 2S CTAs (6-8) did not all fit at once
+// (two waves: down 73.6 us at C3 against 48 us before), so the S pairs of a tile are separate
+// 2-CTA clusters.  Each CTA writes the column slices it does not own (fp32, st.global.cg) to
+// the owner's slots of a workspace and publishes a per-(tile, half, pair) epoch flag (release);
+// the owner (the CTA of pair q with the same half) spins on its S - 1 contributors' flags
+// (acquire) and sums the S partials in pair order (deterministic).  Deadlock-free: S x PT <=
+// 74 pairs, so every CTA is resident once the previous kernel has drained, and dependents
+// cannot launch before every CTA of this grid has started.  The epilogue's global inputs
 // (EPI_RESID: residual x; EPI_QKV: the RoPE cos / sin rows of each column's position) are
 // bulk-copied into shared memory while the mainloop runs, so the fused epilogue loop never
 // waits on a global load (it was latency-bound on them at N = 256: 20 us for QKV).
@@ -1396,44 +1430,54 @@ struct Cfg {
   static constexpr int B_BYTES = HB * kBK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int WMAX = BN / 2;               // widest owned column slice (S >= 2, 16-col grain)
-  static constexpr int XP_BYTES = WMAX * 512;       // prefetched epilogue inputs (128 floats / column)
   static constexpr int CTL = 256;
   static constexpr int META = 3 * BN * 4;
   static constexpr int RED = 2 * 4 * BN * 4;
-  static constexpr int FIXED = 1024 + XP_BYTES + CTL + META + RED;
+  static constexpr int FIXED = 1024 + CTL + META + RED;
   static constexpr int FIT = (227 * 1024 - FIXED) / STAGE;
   static constexpr int STAGES = FIT > 8 ? 8 : FIT;
   static constexpr int RING = STAGES * STAGE;
   static constexpr int SMEM = FIXED + RING;
-  static_assert(STAGES >= 3, "decode pair ring depth");
+  static_assert(STAGES >= 4, "decode pair ring depth");
 };
-// owned columns of pair p: 16-column chunks split as evenly as possible; a receive slot holds
-// the widest slice (dec_slot columns of 128 fp32)
+// after the mainloop the ring holds the S - 1 received slices (slot 0 then the summed slice)
+// and the epilogue inputs (128 floats per owned column)
+template <int BN>
+__host__ __device__ inline bool dec_fits(int S, int wslot) {
+  return (int64_t)S * wslot * 512 + 8192 <= Cfg<BN>::RING;  // + the EPI_QKV staging
+}
+// owned columns of pair p: 16-column chunks split as evenly as possible; a workspace slot
+// holds the widest slice (dec_slot columns of 128 fp32)
 __host__ __device__ inline int dec_col(int BN, int S, int p) { return 16 * ((BN / 16) * p / S); }
 __host__ __device__ inline int dec_slot(int BN, int S) { return 16 * ((BN / 16 + S - 1) / S); }
-// the reduction area (S - 1 receive slots, in the ring after the mainloop) fits
-template <int BN>
-__host__ __device__ inline bool dec_fits(int S) {
-  return S >= 2 && S <= 8 && (S - 1) * dec_slot(BN, S) * 512 <= Cfg<BN>::RING;
+constexpr int kDecPf = 8;  // weight k-blocks prefetched into L2 beyond the ring
+RT_DEV void st_release_gpu(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+RT_DEV unsigned ld_acquire_gpu(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
 }
 }  // namespace dec
 
 template <int BN, int MODE>
 __global__ void __launch_bounds__(kGemmThreads, 1)
-    k_gemm_dec(const __grid_constant__ TmaMap tmA, const __grid_constant__ TmaMap tmB, GemmArgs g, int S) {
+    k_gemm_dec(const __grid_constant__ TmaMap tmA, const __grid_constant__ TmaMap tmB, GemmArgs g, int S,
+               float* ws, unsigned* flags, unsigned epoch) {
   using C = dec::Cfg<BN>;
   constexpr int STAGES = C::STAGES;
   extern __shared__ unsigned char smem_raw[];
   unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   unsigned char* sA = smem;
   unsigned char* sB = smem + STAGES * C::A_BYTES;
-  float* xp = reinterpret_cast<float*>(smem + C::RING);
-  unsigned char* ctl = smem + C::RING + C::XP_BYTES;
+  unsigned char* ctl = smem + C::RING;
   uint64_t* full = reinterpret_cast<uint64_t*>(ctl);
   uint64_t* empty = full + STAGES;
   uint64_t* done = empty + STAGES;
   uint64_t* pf_bar = done + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pf_bar + 1);
+  uint64_t* rx_bar = pf_bar + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rx_bar + 1);
   EpiSmem sm;
   sm.pos = reinterpret_cast<int*>(ctl + C::CTL);
   sm.page = sm.pos + BN;
@@ -1441,23 +1485,28 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   sm.redv = reinterpret_cast<float*>(ctl + C::CTL + C::META);
   sm.redi = reinterpret_cast<int*>(sm.redv + 4 * BN);
   sm.bn = BN;
-  sm.xp = xp;
-  sm.xp_sin = C::WMAX * 64;
   __shared__ long long s_mark[9];
   sm.mark = s_mark;
 
   TraceScope tr(TK_GEMM | ((uint32_t)MODE << 8) | ((uint32_t)(2 * S) << 16));
   __shared__ unsigned long long s_tdone;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const uint32_t rank = cluster_rank();
-  const int p = (int)(rank >> 1), h = (int)(rank & 1);
-  const int t = (int)blockIdx.x / (2 * S);          // pair-tile
+  const int h = (int)cluster_rank();                // CTA of the pair
+  const int pr = (int)blockIdx.x >> 1;              // pair index in the grid
+  const int t = pr / S, p = pr - (pr / S) * S;      // pair-tile, split
   const int m_tile = 2 * t + h;
   const int kbt = g.kb_total;
   const int kb0 = (kbt * p) / S, kb1 = (kbt * (p + 1)) / S;
   const int cb = dec::dec_col(BN, S, p), ce = dec::dec_col(BN, S, p + 1);
-  const uint32_t leader = (uint32_t)(2 * p);
-  const uint16_t pmask = (uint16_t)(0x3u << (2 * p));
+  const int wslot = dec::dec_slot(BN, S);
+  // workspace: slot (tile, half, owner q, source p) of wslot columns x 128 rows
+  auto slot_ptr = [&](int q, int src) {
+    return ws + ((((size_t)t * 2 + h) * S + q) * S + src) * (size_t)wslot * 128;
+  };
+  float* xp = reinterpret_cast<float*>(smem) + (size_t)(S - 1) * wslot * 128;  // epilogue inputs (ring)
+  sm.xp = xp;
+  sm.xp_sin = wslot * 64;
+  sm.stg = MODE == EPI_QKV ? reinterpret_cast<bf16*>(xp + (size_t)wslot * 128) : nullptr;  // 8 KB (ring)
 
   if (warp == 0 && lane == 0) {
     prefetch_tmap(&tmA);
@@ -1468,6 +1517,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     mbar_init(done, 1);
     mbar_init(pf_bar, 1);
+    mbar_init(rx_bar, 1);
     fence_mbar_init();
   }
   if (warp == 1) {
@@ -1477,7 +1527,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   }
   tc_fence_before();
   __syncthreads();
-  cluster_arrive();  // every CTA's barriers are initialised before anyone signals them
+  cluster_arrive();  // both CTAs' barriers are initialised before anyone signals them
   cluster_wait();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
@@ -1485,7 +1535,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      const uint32_t full0 = dsmem_addr(smem_u32(full), leader);  // the pair leader's full barriers
+      const uint32_t full0 = dsmem_addr(smem_u32(full), 0);  // the pair leader's full barriers
       const uint32_t bytes = 2u * C::STAGE;
       const int pre_k = min(STAGES, kb1 - kb0);
       // weights do not depend on the previous kernel: the first stages before its completion
@@ -1498,12 +1548,25 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       tr.ready();
       for (int i = 0; i < pre_k; ++i)
         tma_load_2d_pair(sB + i * C::B_BYTES, &tmB, (kb0 + i) * kBK, h * C::HB, full0 + i * 8);
-      for (int i = pre_k; i < kb1 - kb0; ++i) {
+      // weight k-blocks beyond the ring go to L2 ahead of time (cp.async.bulk.prefetch.L2): the
+      // ring alone keeps ~64 KB of HBM reads in flight per SM (B comes from L2), ~4.3 TB/s
+      // over 128 SMs at the loaded HBM latency; the prefetch distance adds kDecPf k-blocks
+      const bf16* wt = g.w + ((size_t)m_tile * kbt + kb0) * (128 * kBK);
+      const int n_kb = kb1 - kb0;
+      for (int i = pre_k; i < min(n_kb, pre_k + dec::kDecPf); ++i)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(wt + (size_t)i * (128 * kBK)),
+                     "r"((uint32_t)C::A_BYTES)
+                     : "memory");
+      for (int i = pre_k; i < n_kb; ++i) {
         const int st = i % STAGES;
         mbar_wait(&empty[st], (uint32_t)(((i / STAGES) & 1) ^ 1));
         if (h == 0) mbar_arrive_expect_tx(&full[st], bytes);
         tma_load_2d_pair(sA + st * C::A_BYTES, &tmA, 0, (m_tile * kbt + kb0 + i) * 128, full0 + st * 8);
         tma_load_2d_pair(sB + st * C::B_BYTES, &tmB, (kb0 + i) * kBK, h * C::HB, full0 + st * 8);
+        if (i + dec::kDecPf < n_kb)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(wt + (size_t)(i + dec::kDecPf) * (128 * kBK)),
+                       "r"((uint32_t)C::A_BYTES)
+                       : "memory");
       }
     }
     __syncwarp();
@@ -1520,105 +1583,122 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         for (int k = 0; k < kBK / 16; ++k)
           umma_f16_pair(tmem, umma_desc_sw128(a0 + k * 32), umma_desc_sw128(b0 + k * 32), idesc,
                         (i > 0 || k > 0) ? 1u : 0u);
-        umma_commit_pair(&empty[st], pmask);
+        umma_commit_pair(&empty[st], 0x3);
       }
-      umma_commit_pair(done, pmask);
+      umma_commit_pair(done, 0x3);
     }
     __syncwarp();
   } else {
     pdl_wait();
     const int et = (warp & 3) * 32 + lane;
     const uint32_t tb = tmem + ((uint32_t)((warp & 3) * 32) << 16);
-    // per-column metadata of the owned columns, then their epilogue inputs -> shared memory
-    // (bulk copies on pf_bar) while the mainloop runs
+    // per-column metadata of the owned columns while the mainloop runs
     column_meta<MODE>(g, sm, m_tile, 0, cb, ce, et, false);
+    mbar_wait(done, 0);
+    tc_fence_after();
     if (et == 0) {
-      uint32_t pf = 0;
+      s_tdone = gtimer();
+      const long long c0 = clock64();
+#pragma unroll
+      for (int i = 0; i < 9; ++i) s_mark[i] = c0;
+    }
+    // the ring is free: the epilogue inputs -> shared memory (bulk copies on pf_bar, one column
+    // per thread: issued serially by one thread they took ~10 us for 96 columns), in flight
+    // while the split-K exchange runs.  (complete_tx may precede the expect_tx of the phase.)
+    {
+      const int cn = min(ce, g.N) - cb;  // owned columns that hold rows
       if constexpr (MODE == EPI_RESID) {
-        for (int c = cb; c < ce && c < g.N; ++c) pf += 512;
-        mbar_arrive_expect_tx(pf_bar, pf);
-        for (int c = cb; c < ce && c < g.N; ++c)
-          bulk_g2s(xp + (c - cb) * 128, g.x + (size_t)c * g.M + m_tile * 128, 512, pf_bar);
+        if (et == 0) mbar_arrive_expect_tx(pf_bar, (uint32_t)max(cn, 0) * 512);
+        if (et < cn) bulk_g2s(xp + et * 128, g.x + (size_t)(cb + et) * g.M + m_tile * 128, 512, pf_bar);
       } else if constexpr (MODE == EPI_QKV) {
         const int half = g.qkv.hd >> 1;
         const uint32_t rb = (uint32_t)half * 4;
-        for (int c = cb; c < ce && c < g.N; ++c) pf += 2 * rb;
-        mbar_arrive_expect_tx(pf_bar, pf);
-        for (int c = cb; c < ce && c < g.N; ++c) {
-          const int pos = sm.pos[c];
-          bulk_g2s(xp + (c - cb) * 64, g.qkv.cos + (size_t)pos * half, rb, pf_bar);
-          bulk_g2s(xp + sm.xp_sin + (c - cb) * 64, g.qkv.sin + (size_t)pos * half, rb, pf_bar);
+        if (et == 0) mbar_arrive_expect_tx(pf_bar, (uint32_t)max(cn, 0) * 2 * rb);
+        if (et < cn) {
+          const int pos = sm.pos[cb + et];
+          bulk_g2s(xp + et * 64, g.qkv.cos + (size_t)pos * half, rb, pf_bar);
+          bulk_g2s(xp + sm.xp_sin + et * 64, g.qkv.sin + (size_t)pos * half, rb, pf_bar);
         }
       } else {
-        mbar_arrive(pf_bar);
+        if (et == 0) mbar_arrive(pf_bar);
       }
     }
-    mbar_wait(done, 0);
-    tc_fence_after();
-    if (et == 0) s_tdone = gtimer();
-  }
-  // ---- split-K reduction over the S pairs (every warp takes part in the cluster barriers):
-  // receive slot j at ring offset j * wslot columns; the summed owned slice T overwrites slot 0
-  // (each element is read, then written, by the same thread)
-  const int wslot = dec::dec_slot(BN, S);
-  float* T = reinterpret_cast<float*>(smem);
-  __syncwarp();
-  cluster_arrive();  // A: every MMA of the cluster is done -> every ring is free
-  cluster_wait();
-  if (warp >= 2) {
-    const int et = (warp & 3) * 32 + lane;
-    const uint32_t tb = tmem + ((uint32_t)((warp & 3) * 32) << 16);
-    for (int q = 0; q < S; ++q) {  // push the slice owned by pair q (same half) into its slot p'
+    // ---- split-K exchange through L2: the slices other pairs own -> their workspace slots
+    for (int q = 0; q < S; ++q) {
       if (q == p) continue;
       const int qb = dec::dec_col(BN, S, q), qe = dec::dec_col(BN, S, q + 1);
-      const int slot = p < q ? p : p - 1;
-      const uint32_t dst = dsmem_addr(smem_u32(smem), (uint32_t)(2 * q + h)) + (uint32_t)(slot * wslot * 512);
+      float* dst = slot_ptr(q, p) + et;
 #pragma unroll 1
       for (int c0 = qb; c0 < qe; c0 += 16) {
         float v[16];
         tmem_ld16(tb + (uint32_t)c0, v);
 #pragma unroll
-        for (int j = 0; j < 16; ++j)
-          asm volatile("st.shared::cluster.f32 [%0], %1;" ::"r"(dst + (uint32_t)(((c0 - qb + j) * 128 + et) * 4)),
-                       "f"(v[j])
-                       : "memory");
+        for (int j = 0; j < 16; ++j) __stcg(dst + (size_t)(c0 - qb + j) * 128, v[j]);
       }
     }
-  }
-  __syncwarp();
-  cluster_arrive();  // B (release / acquire): the slices are visible to their owners
-  cluster_wait();
-  if (warp >= 2) {
-    const int et = (warp & 3) * 32 + lane;
-    const uint32_t tb = tmem + ((uint32_t)((warp & 3) * 32) << 16);
-    const float* R = reinterpret_cast<const float*>(smem);
+    EPI_MARK(1);
+    epi_bar();  // every row of this CTA's slices is written
+    unsigned* myflags = flags + ((size_t)t * 2 + h) * S;
+    if (et == 0) {
+      __threadfence();
+      dec::st_release_gpu(myflags + p, epoch);
+    }
+    EPI_MARK(2);
+    // wait for the S - 1 contributors of my slice, then bulk-copy their slices (ring slots
+    // j = 0 .. S - 2 in pair order, wslot columns each) into shared memory at once
+    float* R = reinterpret_cast<float*>(smem);
+    const uint32_t slice_bytes = (uint32_t)(ce - cb) * 512;
+    if (et == 0) {
+      for (int q = 0; q < S; ++q)
+        if (q != p)
+          while (dec::ld_acquire_gpu(myflags + q) != epoch) __nanosleep(32);
+      asm volatile("fence.proxy.async.global;" ::: "memory");  // generic writes -> bulk-copy reads
+      mbar_arrive_expect_tx(rx_bar, (uint32_t)(S - 1) * slice_bytes);
+      for (int q = 0, j = 0; q < S; ++q)
+        if (q != p) bulk_g2s(R + (size_t)(j++) * wslot * 128, slot_ptr(p, q), slice_bytes, rx_bar);
+    }
+    EPI_MARK(3);
+    mbar_wait(rx_bar, 0);
+    // ---- sum the S partials of the owned slice in pair order (deterministic) -> T (= slot 0:
+    // every element is read, then written, by the same thread)
+    float* T = R;
 #pragma unroll 1
-    for (int c0 = cb; c0 < ce; c0 += 16) {  // sum the S partials in pair order (deterministic)
+    for (int c0 = cb; c0 < ce; c0 += 16) {
       float own[16], acc[16];
       tmem_ld16(tb + (uint32_t)c0, own);
 #pragma unroll
       for (int j = 0; j < 16; ++j) acc[j] = 0.f;
-      for (int q = 0; q < S; ++q) {
+      for (int q = 0, jq = 0; q < S; ++q) {
         if (q == p) {
 #pragma unroll
           for (int j = 0; j < 16; ++j) acc[j] += own[j];
         } else {
-          const float* src = R + (size_t)(q < p ? q : q - 1) * wslot * 128 + (size_t)(c0 - cb) * 128 + et;
+          const float* src = R + (size_t)(jq++) * wslot * 128 + (size_t)(c0 - cb) * 128 + et;
 #pragma unroll
-          for (int j = 0; j < 16; ++j) acc[j] += src[j * 128];
+          for (int j = 0; j < 16; ++j) acc[j] += (c0 + j < ce) ? src[j * 128] : 0.f;
         }
       }
 #pragma unroll
-      for (int j = 0; j < 16; ++j) T[(c0 - cb + j) * 128 + et] = acc[j];
+      for (int j = 0; j < 16; ++j)
+        if (c0 + j < ce) T[(c0 - cb + j) * 128 + et] = acc[j];
     }
     mbar_wait(pf_bar, 0);  // prefetched epilogue inputs
     epi_bar();
     const TileSrc ts{T - (size_t)cb * 128, nullptr, 0u, 1, 0, BN, 0, 0};
     epilogue<MODE>(g, sm, ts, m_tile, 0, cb, ce, et, true);
+    EPI_MARK(8);
   }
   tc_fence_before();
   __syncthreads();
-  if (threadIdx.x == 0) tr.aux(s_tdone);
+  if (threadIdx.x == 0) {
+    tr.aux(s_tdone);
+    auto dd = [&](int i) {
+      const long long d = s_mark[i + 1] - s_mark[i];
+      return (unsigned long long)(uint32_t)(d > 0 ? d : 0);
+    };
+    trace_phase(TK_PHASE | TK_GEMM | ((uint32_t)MODE << 8) | ((uint32_t)(2 * S) << 16), dd(0) | (dd(1) << 32),
+                dd(2) | (dd(3) << 32), dd(4) | (dd(5) << 32), dd(6) | (dd(7) << 32));
+  }
   cluster_arrive();  // no CTA deallocates while its pair peer may still use the shared TMEM pair state
   cluster_wait();
   if (warp == 1) {
@@ -1937,7 +2017,6 @@ static cudaError_t launch_dec_bn(const TmaMap& am, const TmaMap& bm, const GemmA
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_gemm_dec<BN, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
-    cudaFuncSetAttribute(k_gemm_dec<BN, MODE>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     attr = true;
   }
   cudaLaunchConfig_t cfg{};
@@ -1947,14 +2026,14 @@ static cudaError_t launch_dec_bn(const TmaMap& am, const TmaMap& bm, const GemmA
   cfg.stream = s;
   cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = 2 * S;
+  at[0].val.clusterDim.x = 2;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
   at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = at;
   cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, k_gemm_dec<BN, MODE>, am, bm, g, S);
+  return cudaLaunchKernelEx(&cfg, k_gemm_dec<BN, MODE>, am, bm, g, S, g.dec_ws, g.dec_flags, g.dec_epoch);
 }
 template <int MODE>
 static cudaError_t launch_dec_mode(const TmaMap& am, const GemmTmaSet& x, const GemmArgs& g, int bn, int PT, int S,
@@ -1963,26 +2042,36 @@ static cudaError_t launch_dec_mode(const TmaMap& am, const GemmTmaSet& x, const 
   if (bn == 128) return launch_dec_bn<128, MODE>(am, x.m64, g, PT, S, s);
   return launch_dec_bn<256, MODE>(am, x.m128, g, PT, S, s);
 }
-// split count of the decode pair kernel: S x pair-tiles <= the SM pairs (one CTA per SM),
-// >= 4 k-blocks per pair, reduction area within the ring
-static int dec_splits(int BN, int PT, int kbt) {
+// split count of the decode pair kernel: S x pair-tiles <= the SM pairs (one CTA per SM, every
+// pair resident at once: the owners spin on their contributors), >= 4 k-blocks per pair
+static int dec_splits(int PT, int kbt, int bn) {
   const int pairs = sm_count() / 2;
   int best = 0;
   for (int S = 2; S <= 8; ++S) {
-    const bool fits = BN == 64 ? dec::dec_fits<64>(S) : (BN == 128 ? dec::dec_fits<128>(S) : dec::dec_fits<256>(S));
+    const int w = dec::dec_slot(bn, S);
+    const bool fits = bn == 64 ? dec::dec_fits<64>(S, w) : (bn == 128 ? dec::dec_fits<128>(S, w) : dec::dec_fits<256>(S, w));
     if (fits && PT * S <= pairs && kbt / S >= 4) best = S;
   }
   return best;
 }
+int64_t gemm_dec_ws_floats(int M, int N, int K) {
+  const int PT = (M + 127) / 256;
+  const int bn = N <= 64 ? 64 : (N <= 128 ? 128 : 256);
+  const int S = dec_splits(PT, K / kBK, bn);
+  return S < 2 ? 0 : (int64_t)PT * 2 * S * S * dec::dec_slot(bn, S) * 128;
+}
 // launch the decode pair kernel if it applies (returns cudaErrorNotSupported otherwise)
 static cudaError_t try_launch_dec(const bf16* w_tiled, const GemmTmaSet& x, GemmArgs g, cudaStream_t s) {
   const int m_tiles = (g.M + 127) / 128;
+  if (!g.dec_ws || !g.dec_flags) return cudaErrorNotSupported;
   if (g.N > 256 || g.N < 1 || g.M % 256 || g.K % kBK || g.mode == EPI_ARGMAX) return cudaErrorNotSupported;
   const int bn = g.N <= 64 ? 64 : (g.N <= 128 ? 128 : 256);
   const int PT = m_tiles / 2;
   const int kbt = g.K / kBK;
-  const int S = dec_splits(bn, PT, kbt);
+  const int S = dec_splits(PT, kbt, bn);
   if (S < 2) return cudaErrorNotSupported;
+  if ((int64_t)PT * 2 * S * S * dec::dec_slot(bn, S) * 128 > g.dec_ws_floats || PT * 2 * S > g.dec_flags_cap)
+    return cudaErrorNotSupported;
   const TmaMap* am = weight_map(w_tiled, (uint64_t)m_tiles * kbt * 128);
   if (!am) return cudaErrorNotSupported;
   g.w = w_tiled;

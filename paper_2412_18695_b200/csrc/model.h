@@ -136,7 +136,18 @@ struct GemmArgs {
   // kernel choice overrides (parity tests / the tuner; 0 = the measured dispatch): the N
   // tile width and the path (GEMM_PATH_*)
   int force_bn, force_path;
+  // decode-pair split-K exchange (k_gemm_dec; nullable: the kernel is not used): fp32
+  // workspace of gemm_dec_ws_floats(M, N) floats, epoch flags [pair-tiles][2][splits] (zeroed
+  // once), and an epoch that the caller increments before every launch
+  float* dec_ws;
+  int64_t dec_ws_floats;
+  unsigned* dec_flags;
+  int dec_flags_cap;
+  unsigned dec_epoch;
 };
+// floats of the k_gemm_dec workspace for an [M x K] projection at N rows (0: not used)
+int64_t gemm_dec_ws_floats(int M, int N, int K);
+constexpr int kDecFlags = 512;  // epoch flags of the k_gemm_dec exchange (pair-tiles x 2 x splits)
 int64_t gemm_sk_ws_floats();
 int gemm_bn(int M, int K, int N);
 int gemm_choose_splits(int M, int N, int K);   // cluster split-K factor (1..16)

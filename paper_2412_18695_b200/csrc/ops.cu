@@ -183,6 +183,26 @@ extern "C" rt_status rt_op_gemm_tiled(const void* d_w_tiled, const void* d_x, fl
     g.sk_cnt = sk_cnt;
     g.sk_cnt_cap = sk_cap;
   }
+  // decode-pair split-K exchange (k_gemm_dec): a process-wide workspace, grown on demand
+  static float* dec_ws = nullptr;
+  static int64_t dec_cap = 0;
+  static unsigned* dec_flags = nullptr;
+  static unsigned dec_epoch = 0;
+  const int64_t dneed = gemm_dec_ws_floats(M, N, K);
+  if (dneed > dec_cap) {
+    if (dec_ws) cudaFree(dec_ws);
+    if (cudaMalloc(&dec_ws, (size_t)dneed * 4) != cudaSuccess) return RT_E_CUDA;
+    dec_cap = dneed;
+  }
+  if (!dec_flags) {
+    if (cudaMalloc(&dec_flags, kDecFlags * 4) != cudaSuccess) return RT_E_CUDA;
+    cudaMemset(dec_flags, 0, kDecFlags * 4);
+  }
+  g.dec_ws = dec_ws;
+  g.dec_ws_floats = dec_cap;
+  g.dec_flags = dec_flags;
+  g.dec_flags_cap = kDecFlags;
+  g.dec_epoch = ++dec_epoch;
   launch_gemm_epi((const bf16*)d_w_tiled, xm, g, splits, (cudaStream_t)stream);
   return last_launch();
 }

@@ -649,3 +649,55 @@ def test_prefill_and_decode_rounds_bitwise_deterministic(rt, gemm_path):
         runs.append(logs)
     for a, b in zip(*runs):
         assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+
+
+def test_sched_parity_c5_slice_retention_stress(rt):
+    """SURVEY §8(d) C5 per-GPU slice, scheduling only (BASELINE configs[4]: 4096 agents over 8
+    GPUs = 512 per GPU, 70B dims; long robot-arm plans of 160 tokens in >10 segments, 128-token
+    prompts, AMB-26 reservations of prompt + 256 new tokens = 24 pages on a pool that holds
+    277 of them (the 35 GB left beside 141 GB of weights): admission refusals and long page
+    retention.  Device scheduler == oracle every round (admissions, refusals, slots, page
+    tables, free stack, segment records)."""
+    v = make_vocab(128256)
+    p = engine_params("b200-roofline", max_batch=512, max_tasks=2048, max_ctx=512, n_pages=277 * 24)
+    reqs = compose_workload(512, 64.0, 16, range(9, 12), 3.0, 7, v, prompt_len_range=(128, 128), plan_len=160,
+                            max_requests=900)
+    eng, ora = make_pair(rt, v, p)
+    for r in reqs:
+        a = eng.submit(r.agent_id, r.prompt, r.arrival_us, r.ert_us, r.alpha, r.beta, r.exec_window_us, 256,
+                       script=r.plan)
+        b = ora.submit(r.agent_id, r.prompt, r.arrival_us, r.ert_us, r.alpha, r.beta, r.exec_window_us, 256,
+                       script=r.plan)
+        assert a == b
+    refused = 0
+    orig_step = ora.step
+
+    def counting_step(t=None):
+        nonlocal refused
+        info = orig_step(t)
+        refused += info.get("n_refused_mem", 0)
+        return info
+    ora.step = counting_step
+    n, segs = lockstep(eng, ora, max_rounds=20000, check_every=25)
+    assert refused > 0                                  # the pool refuses admissions
+    assert len({s["request_id"] for s in segs if s["reason"] in (1, 2)}) == len(reqs)
+    assert max(s["k"] for s in segs) >= 10              # long multi-segment plans retained
+
+
+def test_sched_parity_wcet_lag_hand_worked(rt):
+    """The hand-worked R-WCET trace (tests/test_oracle_engine.py) on the device scheduler:
+    B admitted at round 1 on the pre-admission speed, C refused at round 2, A's segment
+    dispatched at 227720 us."""
+    v = make_vocab(512)
+    p = engine_params("paper-4090", max_batch=4, max_tasks=8, max_ctx=64, n_pages=16, max_admit_per_round=1)
+    eng, ora = make_pair(rt, v, p)
+    filler = [5] * 30 + [v.eos_id]
+    for agent, arr, ert in ((0, 0, 220_000), (1, 1, 100_000_000), (2, 2, 100_000_000)):
+        eng.submit(agent, [1], arr, ert, -2.0, 1.0, 0, 0, script=filler)
+        ora.submit(agent, [1], arr, ert, -2.0, 1.0, 0, 0, script=filler)
+    i = [eng.step() for _ in range(3)]
+    assert [(x["t_us"], x["n_admitted"], x["n_refused_wcet"]) for x in i] == [(0, 1, 0), (21884, 1, 0), (44856, 0, 1)]
+    for _ in range(3):
+        ora.step()
+    n, segs = lockstep(eng, ora)
+    assert [s["dispatch_us"] for s in segs if s["request_id"] == 0][0] == 227720
