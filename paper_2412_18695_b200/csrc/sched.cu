@@ -195,6 +195,10 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
   __shared__ int wbuf[32];
   __shared__ unsigned long long s_sum_ctx, s_sum_prompt, s_attn_tok;
   __shared__ int s_max_seqlen, s_ndec;
+  __shared__ long long s_pm[10];  // clock64 phase marks (RT_FLAG_TRACE)
+#define PRE_MARK(i) \
+  if (threadIdx.x == 0) s_pm[i] = clock64()
+  PRE_MARK(0);
 
   TaskTable T = p.tt;
   DevState* st = p.st;
@@ -234,6 +238,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
     if (sti == T_PENDING) atomicMin(&s_min_arr, enc_i64(T.arrival[i]));
   }
   __syncthreads();
+  PRE_MARK(1);
   const int n_run = st->n_slots;
   if (n_run == 0 && s_nwait == 0) {
     if (!wall && s_min_arr != ~0ull) {  // virtual clock jumps to the next arrival
@@ -328,6 +333,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
     if (T.holder[i]) my_out += T.R[i] - T.n_pages[i];
   if (my_out) atomicAdd(&s_outstanding, my_out);
   __syncthreads();
+  PRE_MARK(2);
   const int n = s_nc;
   int n_pad = 1;
   while (n_pad < n) n_pad <<= 1;
@@ -352,6 +358,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
     }
   }
 
+  PRE_MARK(3);
   // ---- local top-K candidates for the round allgather (a12)
   if (tid < kTopK) {
     if (tid < n) {  // record {Pri (0 for FCFS/EDF), arrival, global id, rank}
@@ -407,6 +414,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
   }
   __syncthreads();
 
+  PRE_MARK(4);
   // ---- (3b) admission in key order (reading R-MEM), with KV eviction to
   // host memory when a candidate that needs memory does not fit (R-EVICT):
   // suspended holders LATER in the key order are evicted, lowest priority first, only if
@@ -495,6 +503,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
     p.mb->n_swap_ev = min(nsw, p.swap_cap);
   }
   __syncthreads();
+  PRE_MARK(5);
   const int nadm = s_nadm;
   const int B = n_run + nadm;
 
@@ -529,6 +538,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
     s_nrest = nrest;
   }
   __syncthreads();
+  PRE_MARK(6);
   // page pops: prefill admissions (admission order) first, then decode slots in slot order
   for (int s = tid; s < B; s += nt) {
     const int task = p.slot_task[s];
@@ -604,6 +614,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
     s_nswap = nsw;
   }
   __syncthreads();
+  PRE_MARK(7);
   // forward rows: prefill slot -> n_prompt rows, decode slot -> 1 row (AMB-13)
   for (int s = tid; s < B; s += nt) {
     const int task = p.slot_task[s];
@@ -669,6 +680,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
   }
   __syncthreads();
 
+  PRE_MARK(8);
   // ---- (5) round latency (VIRTUAL cost model, AMB-24) and plan publication
   if (tid == 0) {
     const long long sum_ctx = (long long)s_sum_ctx, sum_prompt = (long long)s_sum_prompt;
@@ -719,6 +731,16 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
     mb->attn_tokens = (long long)s_attn_tok;
     __threadfence_system();
   }
+  PRE_MARK(9);
+  if (threadIdx.x == 0) {
+    auto dd = [&](int i, int j) {
+      const long long d = s_pm[j] - s_pm[i];
+      return (unsigned long long)(uint32_t)(d > 0 ? d : 0);
+    };
+    trace_phase(TK_PHASE | TK_SCHED_PRE, dd(0, 1) | (dd(1, 2) << 32), dd(2, 3) | (dd(3, 4) << 32),
+                dd(4, 5) | (dd(5, 6) << 32), dd(6, 7) | (dd(7, 9) << 32));
+  }
+#undef PRE_MARK
 }
 
 void launch_sched_pre(const SchedParams& p, int64_t now_us, cudaStream_t s) {

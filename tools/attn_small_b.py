@@ -3,4 +3,4 @@ sys.path.insert(0, os.environ["GRAFT_REPO_ROOT"] + "/tools"); sys.path.insert(0,
 import attn_bench as A
 for B, ctx in [(8, 1310), (8, 2884), (8, 8192), (16, 2884), (16, 8192), (32, 1310)]:
     us, gbs = A.bench(B, ctx)
-    print(os.environ.get("RT_ATTN_CHUNKS", "auto"), B, ctx, round(us, 1), round(gbs))
+    print(B, ctx, round(us, 1), round(gbs))

@@ -1,5 +1,5 @@
-"""Prefill projection time vs rows N for one kernel policy (environment of the process:
-RT_GEMM_PAIR, RT_GEMM_BN): `python tools/gemm_policy_sweep.py [names]` prints one line per N."""
+"""Prefill projection time vs rows N with the engine's dispatch (`python tools/gemm_policy_sweep.py
+[names]` prints one line per N; forced paths: tools/proj_bench.py)."""
 import os
 import sys
 

@@ -1,5 +1,5 @@
 """Measure the prefill projection kernels per (shape, rows N) for every candidate (forced
-tile width RT_GEMM_BN, CTA-pair kernel on / off RT_GEMM_PAIR); one JSON line per
+tile width and CTA-pair kernel on / off through rt_op_gemm_tiled(path, bn)); one JSON line per
 measurement.  `tools/gemm_policy_gen.py` turns the lines into the
 dispatch table `paper_2412_18695_b200/csrc/gemm_policy.inc`."""
 import json
@@ -36,13 +36,12 @@ def main():
             # all candidates of one N back to back in random order (clocks drift with the
             # power state over a long sweep; a per-process sweep per width biased the choice)
             for bn, pair in rnd.sample(CANDIDATES, len(CANDIDATES)):
-                os.environ["RT_GEMM_BN"] = str(bn)
-                os.environ["RT_GEMM_PAIR"] = str(pair)
+                path = rt.RT_GEMM_PATH_PAIR if pair else rt.RT_GEMM_PATH_STREAMK
                 for _ in range(2):
-                    rt.gemm_tiled(Wt, X, out, M, N, K, cap, 0)
+                    rt.gemm_tiled(Wt, X, out, M, N, K, cap, 0, path=path, bn=bn)
                 e0.record()
                 for _ in range(8):
-                    rt.gemm_tiled(Wt, X, out, M, N, K, cap, 0)
+                    rt.gemm_tiled(Wt, X, out, M, N, K, cap, 0, path=path, bn=bn)
                 e1.record()
                 torch.cuda.synchronize()
                 us = e0.elapsed_time(e1) / 8 * 1e3

@@ -21,8 +21,9 @@ def main():
     shape = MODEL_SHAPES["llama3-8b"]
     vocab = make_vocab(shape.vocab)
     B = 64
-    n_pages = B * 3 * ((bench.MAX_CTX + 15) // 16) // 2
-    p = engine_params("b200-roofline", max_batch=B, max_tasks=4 * B, max_ctx=bench.MAX_CTX, n_pages=n_pages,
+    max_ctx = bench.WORKLOADS["C2"]["max_ctx"]
+    n_pages = B * 3 * ((max_ctx + 15) // 16) // 2
+    p = engine_params("b200-roofline", max_batch=B, max_tasks=4 * B, max_ctx=max_ctx, n_pages=n_pages,
                       clock_mode=1)
     eng = rt.Engine(shape, p, vocab, seed=1234, flags=rt.RT_FLAG_TRACE | rt.RT_FLAG_TIMING,
                     max_rows_per_forward=8192)
@@ -30,7 +31,7 @@ def main():
     now = lambda: int((time.perf_counter() - t0) * 1e6)  # noqa: E731
     for rep in range(a.reps + 1):
         for j in range(a.requests):
-            tr = bench.drone_request(vocab, j + 100 * rep, 0, 0, plan_len=4)
+            tr = bench.agent_request("C2", vocab, j + 100 * rep, 0, 0, plan_len=4)
             eng.submit(j, tr.prompt, now(), tr.ert_us, tr.alpha, tr.beta, p.g_us, script=tr.plan)
         eng.sync()
         eng.reset_stats()

@@ -31,67 +31,15 @@ def role(kind, layer_pos):
         if mode == 3:   # O projection or down projection: alternate within a layer
             name = "o_proj" if layer_pos == 0 else "down"
         return f"gemm_{name}(S={kind >> 16})"
-    if base == 11:
-        return f"chain({(kind >> 8) & 0xFF} jobs)"
     return rt.TRACE_KINDS.get(base, str(base))
-
-
-chain_marks = collections.defaultdict(list)
-
-
-def chain_report(launches_by_grid):
-    """Per chain launch, per job: median / max over CTAs (us after the launch's first ready
-    CTA) of: input ready at the producer, last MMA issued, epilogues done."""
-    acc = collections.defaultdict(list)
-    for g, recs in chain_marks.items():
-        L = launches_by_grid.get(g)
-        if L is None:
-            continue
-        for role_id, vals in recs:
-            if role_id == 4:
-                continue
-            for j, t in enumerate(vals):
-                if t:
-                    acc[(role_id, j)].append((t - L["ready"]) / 1e3)
-    if not acc:
-        return
-    fx = []  # role 4: one record per tile epilogue: (start, partials summed, done, job<<32|nc)
-    for g, recs in chain_marks.items():
-        L = launches_by_grid.get(g)
-        for role_id, vals in recs:
-            if role_id == 4 and L is not None:
-                fx.append(((vals[3] >> 32), vals[3] & 0xFFFFFFFF, (vals[1] - vals[0]) / 1e3,
-                           (vals[2] - vals[1]) / 1e3, (vals[0] - L["ready"]) / 1e3))
-    if fx:
-        fx = np.array(fx)
-        print("chain tile epilogues: job nc | n | fixup sum us (med/max) | epilogue us (med/max) | start (med/max)")
-        for j in range(4):
-            for nc in sorted(set(fx[fx[:, 0] == j][:, 1].astype(int))):
-                m = fx[(fx[:, 0] == j) & (fx[:, 1] == nc)]
-                print(f"  job {j} nc {nc}: {len(m):5d} | {np.median(m[:, 2]):6.2f}/{m[:, 2].max():6.2f} | "
-                      f"{np.median(m[:, 3]):6.2f}/{m[:, 3].max():6.2f} | {np.median(m[:, 4]):6.1f}/{m[:, 4].max():6.1f}")
-    acc = {k: v for k, v in acc.items() if k[0] != 4}
-    names = {1: "input ready", 2: "last MMA", 3: "epilogue done"}
-    print("chain per-job marks (us after launch ready; median / max over CTAs and launches):")
-    for j in range(4):
-        cells = []
-        for rid in (1, 2, 3):
-            v = acc.get((rid, j))
-            cells.append(f"{names[rid]} {np.median(v):7.1f}/{np.max(v):7.1f}" if v else f"{names[rid]}   -")
-        print(f"  job {j}: " + " | ".join(cells))
 
 
 def analyse(tr):
     launches = collections.OrderedDict()
     phases = collections.defaultdict(list)
-    chain_marks.clear()
     for r in np.sort(tr, order="t_entry"):
         g = int(r["grid"])
         if int(r["kind"]) & 0x80:      # GEMM phase marks of one CTA
-            if (int(r["kind"]) & 0x7F) == 11:   # chain: per-job globaltimer marks
-                chain_marks[g].append(((int(r["kind"]) >> 8) & 0xFF,
-                                       [int(r[k]) for k in ("t_entry", "t_ready", "t_aux", "t_exit")]))
-                continue
             phases[g].append((int(r["t_entry"]), int(r["t_ready"]), int(r["t_aux"]), int(r["t_exit"])))
             continue
         if g not in launches:
@@ -132,7 +80,6 @@ def analyse(tr):
             ph_agg[name].append(np.median(cyc.astype(np.float64), axis=0) / CLOCK_GHZ / 1e3)
         prev_exit = max(prev_exit or 0, L["exit"])
     span = (max(L["exit"] for L in seq) - min(L["entry"] for L in seq)) / 1e3
-    chain_report({L["grid"]: L for L in seq})
     return agg, span, len(seq), ph_agg
 
 
@@ -171,8 +118,16 @@ def main():
     print("GEMM epilogue phases after the accumulator is complete (median us at 1.965 GHz): park | "
           "cluster barrier | slices received | partials loaded | - | epilogue loop | final reduction | bulk-copy drain")
     for name, v in ph.items():
+        if name.startswith("sched"):
+            continue
         m = np.median(np.array(v), axis=0)
         print(f"  {name:28s} " + " ".join(f"{x:7.2f}" for x in m))
+    for name, v in ph.items():
+        if name.startswith("sched"):
+            m = np.median(np.array(v), axis=0)
+            print(f"{name} phases (median us): ingest | score | sort | wcet+candidates | admit | assemble | "
+                  "page pops | rows + publish")
+            print("  " + " ".join(f"{x:7.2f}" for x in m))
     if a.json:
         json.dump(dict(steps=a.steps, span_us=span, launches=n, roles=rows), open(a.json, "w"), indent=1)
     eng.close()
