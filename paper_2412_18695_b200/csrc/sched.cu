@@ -172,6 +172,12 @@ struct PreSmem {
   int adm[kMaxTasks];
   int evn[kMaxTasks];   // candidate evicted this round (R-EVICT)
   int vic[kMaxTasks];   // victims (task slots) in eviction order
+  int evc[kMaxTasks];   // candidate's KV is on the host (T.evicted at scoring time)
+  int admx[kMaxTasks];  // candidate index of each admission
+  int sflag[kMaxTasks]; // batch slot: 1 = prefill (k = 0 admission), 2 = restore (evicted resume)
+  long long wb[32];     // WCET gate: per-warp (budget, rid, seg_tok) minima
+  long long wr[32];
+  int ws[32];
 };
 
 __device__ __forceinline__ bool key_before(const PreSmem& S, int x, int y, int n) {
@@ -326,6 +332,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
     S.ck[pos] = k;
     S.cR[pos] = T.R[i] - T.n_pfx[i];  // own pages (a shared prefix is already resident)
     S.evn[pos] = 0;
+    S.evc[pos] = T.evicted[i];
   }
   // outstanding reservations sum_active (R - held)  (AMB-26)
   int my_out = 0;
@@ -376,11 +383,12 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
     }
   }
 
-  // ---- (3a) WCET gate on the most urgent running generation
-  if (tid < 32) {
+  // ---- (3a) WCET gate on the most urgent running generation: minimum
+  // (budget, rid) over the running slots, one slot per thread, then warps, then warp 0
+  {
     long long best_bud = LLONG_MAX, best_rid = LLONG_MAX;
     int best_seg = 0;
-    for (int s = tid; s < n_run; s += 32) {
+    for (int s = tid; s < n_run; s += nt) {
       const int task = p.slot_task[s];
       const long long bud = T.D[task] - t;
       const long long rid = T.rid[task];
@@ -390,26 +398,41 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
         best_seg = T.seg_tok[task];
       }
     }
-    for (int o = 16; o > 0; o >>= 1) {
-      long long ob = __shfl_xor_sync(0xffffffffu, best_bud, o);
-      long long orid = __shfl_xor_sync(0xffffffffu, best_rid, o);
-      int os = __shfl_xor_sync(0xffffffffu, best_seg, o);
-      if (ob < best_bud || (ob == best_bud && orid < best_rid)) {
-        best_bud = ob;
-        best_rid = orid;
-        best_seg = os;
+    auto warp_min = [&](long long& b, long long& r, int& sg) {
+      for (int o = 16; o > 0; o >>= 1) {
+        const long long ob = __shfl_xor_sync(0xffffffffu, b, o);
+        const long long orid = __shfl_xor_sync(0xffffffffu, r, o);
+        const int os = __shfl_xor_sync(0xffffffffu, sg, o);
+        if (ob < b || (ob == b && orid < r)) {
+          b = ob;
+          r = orid;
+          sg = os;
+        }
       }
+    };
+    warp_min(best_bud, best_rid, best_seg);
+    if ((tid & 31) == 0) {
+      S.wb[tid >> 5] = best_bud;
+      S.wr[tid >> 5] = best_rid;
+      S.ws[tid >> 5] = best_seg;
     }
-    if (tid == 0) {
-      int gate = 1;
-      const int nh = min(p.speed_window, st->hist_n);
-      if (best_bud != LLONG_MAX && nh > 0 && !p.wcet_off) {
-        long long sum = 0;
-        for (int j = 1; j <= nh; ++j) sum += st->hist[(st->hist_pos - j + 8) & 7];
-        const long long rem = max(0, p.max_seg_tokens - best_seg);
-        gate = (rem * sum <= (long long)nh * best_bud) ? 1 : 0;
+    __syncthreads();
+    if (tid < 32) {
+      best_bud = tid < (nt >> 5) ? S.wb[tid] : LLONG_MAX;
+      best_rid = tid < (nt >> 5) ? S.wr[tid] : LLONG_MAX;
+      best_seg = tid < (nt >> 5) ? S.ws[tid] : 0;
+      warp_min(best_bud, best_rid, best_seg);
+      if (tid == 0) {
+        int gate = 1;
+        const int nh = min(p.speed_window, st->hist_n);
+        if (best_bud != LLONG_MAX && nh > 0 && !p.wcet_off) {
+          long long sum = 0;
+          for (int j = 1; j <= nh; ++j) sum += st->hist[(st->hist_pos - j + 8) & 7];
+          const long long rem = max(0, p.max_seg_tokens - best_seg);
+          gate = (rem * sum <= (long long)nh * best_bud) ? 1 : 0;
+        }
+        s_gate_ok = gate;
       }
-      s_gate_ok = gate;
     }
   }
   __syncthreads();
@@ -436,7 +459,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
         ++rmem;
         continue;
       }
-      if (S.ck[x] == 0 || T.evicted[S.cslot[x]]) {
+      if (S.ck[x] == 0 || S.evc[x]) {
         const int need = S.cR[x];
         if (!mem_blocked && avail < need && p.host_pages > 0) {
           long long gain = 0;
@@ -469,6 +492,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
         }
         avail -= need;
       }
+      S.admx[nadm] = x;
       S.adm[nadm++] = S.cslot[x];
     }
     s_nadm = nadm;
@@ -510,24 +534,29 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
   // ---- (4) batch assembly: running slots keep their order, admissions appended
   for (int j = tid; j < nadm; j += nt) {
     const int task = S.adm[j];
+    const int x = S.admx[j];
     const int s = n_run + j;
     p.slot_task[s] = task;
     p.admitted[j] = task;
     T.state[task] = T_RUNNING;
-    const int pre = (T.k[task] == 0);
+    const int pre = (S.ck[x] == 0);
     p.slot_is_prefill[s] = pre;
+    S.sflag[s] = pre ? 1 : (S.evc[x] ? 2 : 0);
     if (pre) T.holder[task] = 1;
   }
-  for (int s = tid; s < n_run; s += nt) p.slot_is_prefill[s] = 0;
+  for (int s = tid; s < n_run; s += nt) {
+    p.slot_is_prefill[s] = 0;
+    S.sflag[s] = 0;
+  }
   __syncthreads();
   // restores (evicted resumes admitted this round): re-pop their own pages with the
   // admissions (admission order), KV copied back from the host pages, host pages pushed back
   // (admission order, each in reverse order) after this round's eviction pops
   if (tid == 0) {
     int htop = st->hfree_top, nrest = 0;
-    for (int j = 0; j < nadm; ++j) {
+    for (int j = 0; j < nadm && p.host_pages > 0; ++j) {
       const int task = S.adm[j];
-      if (!T.evicted[task] || T.k[task] == 0) continue;
+      if (S.sflag[n_run + j] != 2) continue;
       ++nrest;
       const int nh = T.n_hpages[task];
       const int32_t* hpt = T.hpage_table + (size_t)task * p.pt_stride;
@@ -543,12 +572,13 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
   for (int s = tid; s < B; s += nt) {
     const int task = p.slot_task[s];
     p.round_slots[s] = task;
-    if (p.slot_is_prefill[s]) {
+    const int fl = S.sflag[s];
+    if (fl == 1) {
       S.cnt_a[s] = ceil_div_i(T.n_prompt[task], p.page_tokens) - T.n_pfx[task];
     } else {
-      S.cnt_a[s] = (s >= n_run && T.evicted[task]) ? T.n_hpages[task] : 0;  // restore pops
+      S.cnt_a[s] = fl == 2 ? T.n_hpages[task] : 0;  // restore pops
     }
-    S.cnt_b[s] = p.slot_is_prefill[s] ? 0 : ((T.ctx[task] % p.page_tokens == 0) ? 1 : 0);
+    S.cnt_b[s] = fl == 1 ? 0 : ((T.ctx[task] % p.page_tokens == 0) ? 1 : 0);
   }
   __syncthreads();
   const int tot_a = block_scan_excl(S.cnt_a, B, wbuf);
@@ -557,7 +587,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
   for (int s = tid; s < B; s += nt) {
     const int task = p.slot_task[s];
     int32_t* pt = T.page_table + (size_t)task * p.pt_stride;
-    if (p.slot_is_prefill[s]) {
+    if (S.sflag[s] == 1) {
       const int npg = ceil_div_i(T.n_prompt[task], p.page_tokens);
       const int npf = T.n_pfx[task];
       const int32_t* pp = p.pfx_pages + (size_t)max(T.pfx[task], 0) * p.pt_stride;
@@ -571,7 +601,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
       }
       T.n_pages[task] = npg;
     } else {
-      if (s >= n_run && T.evicted[task]) {  // restore: own pages re-popped, KV from host
+      if (S.sflag[s] == 2) {  // restore: own pages re-popped, KV from host
         const int npf = T.n_pfx[task], nh = T.n_hpages[task];
         for (int m = 0; m < nh; ++m) {
           const int q = S.cnt_a[s] + m;
@@ -595,11 +625,11 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
   }
   __syncthreads();
   // restore copy list (after the evictions', in admission order) and restored state
-  if (tid == 0) {
+  if (tid == 0 && p.host_pages > 0) {
     int nsw = s_nswap;
     for (int s = n_run; s < B; ++s) {
       const int task = p.slot_task[s];
-      if (p.slot_is_prefill[s] || !T.evicted[task]) continue;
+      if (S.sflag[s] != 2) continue;
       const int npf = T.n_pfx[task], nh = T.n_hpages[task];
       const int32_t* pt = T.page_table + (size_t)task * p.pt_stride;
       const int32_t* hpt = T.hpage_table + (size_t)task * p.pt_stride;
@@ -618,7 +648,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
   // forward rows: prefill slot -> n_prompt rows, decode slot -> 1 row (AMB-13)
   for (int s = tid; s < B; s += nt) {
     const int task = p.slot_task[s];
-    S.cnt_a[s] = p.slot_is_prefill[s] ? T.n_prompt[task] - p.page_tokens * T.n_pfx[task] : 1;
+    S.cnt_a[s] = S.sflag[s] == 1 ? T.n_prompt[task] - p.page_tokens * T.n_pfx[task] : 1;
   }
   __syncthreads();
   const int n_rows = block_scan_excl(S.cnt_a, B, wbuf);
@@ -626,7 +656,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
   for (int s = tid; s < B; s += nt) {
     const int task = p.slot_task[s];
     const int off = S.cnt_a[s];
-    if (p.slot_is_prefill[s]) {
+    if (S.sflag[s] == 1) {
       const int P = T.n_prompt[task];
       const int Lp = p.page_tokens * T.n_pfx[task];  // prefix positions are not recomputed
       p.slot_row[s] = off + (P - Lp) - 1;
@@ -650,7 +680,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
   // 16-position attention tiles (page-aligned: the prompt starts at position 0)
   int n_pf_tiles = 0;
   for (int s = n_run; s < B; ++s) {
-    if (!p.slot_is_prefill[s]) continue;
+    if (S.sflag[s] != 1) continue;
     const int task = p.slot_task[s];
     const int off = S.cnt_a[s];
     const int P = T.n_prompt[task];
@@ -675,7 +705,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
   if (tid == 0) {
     int k = n_run;
     for (int s = n_run; s < B; ++s)
-      if (!p.slot_is_prefill[s]) p.dec_rows[k++] = S.cnt_a[s];
+      if (S.sflag[s] != 1) p.dec_rows[k++] = S.cnt_a[s];
     s_ndec = k;
   }
   __syncthreads();
