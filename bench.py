@@ -77,10 +77,12 @@ def ncu_traffic(kernel):
     try:
         for d in json.load(open(os.path.join(ROOT, NCU_ATTN_SOURCE.split()[0]))):
             if kernel in d["Kernel Name"]:
-                rd = float(d["dram__bytes_read.sum"].split()[0])
-                wr = float(d["dram__bytes_write.sum"].split()[0])
-                scale = {"Mbyte": 1e6, "Gbyte": 1e9, "Kbyte": 1e3, "byte": 1.0}[d["dram__bytes_read.sum"].split()[1]]
-                return (rd + wr) * scale
+                unit = {"Mbyte": 1e6, "Gbyte": 1e9, "Kbyte": 1e3, "byte": 1.0}
+
+                def val(key):
+                    v, u = d[key].split()[:2]
+                    return float(v) * unit[u]
+                return val("dram__bytes_read.sum") + val("dram__bytes_write.sum")
     except Exception:
         return None
     return None

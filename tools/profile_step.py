@@ -9,6 +9,7 @@ import time
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
+import numpy as np  # noqa: E402
 import torch  # noqa: E402
 import bench  # noqa: E402
 from synth import MODEL_SHAPES, make_vocab, engine_params  # noqa: E402
@@ -60,6 +61,13 @@ def main():
     eng.sync()
     torch.cuda.profiler.stop()
     print("profiled", a.steps, "steps at B =", info["n_running"], info)
+    # algorithmic attention bytes of the last profiled round (per layer launch): decode row r
+    # attends positions 0 .. pos_r -> K + V of every kv head, plus q and o
+    rows = eng.dump(rt.RT_DUMP_ROWS, np.int32).reshape(-1, 3)
+    s = eng.shape
+    kv = int((rows[:, 1].astype(np.int64) + 1).sum()) * 2 * s.n_kv_heads * s.head_dim * 2
+    qo = 2 * len(rows) * s.n_q_heads * s.head_dim * 2
+    print(f"attention algorithmic bytes per layer launch: {kv + qo} ({len(rows)} rows, kv {kv}, q+o {qo})")
 
 
 if __name__ == "__main__":
