@@ -1352,9 +1352,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     const int et = (warp & 3) * 32 + lane;
     const uint32_t tb = tmem + ((uint32_t)((warp & 3) * 32) << 16);
     const uint32_t tempty0 = dsmem_addr(smem_u32(tempty), 0);
+    long long c_wait = 0, c_park = 0, c_epi = 0;  // epilogue-warp cycle totals (trace phases)
     int seg = 0, i = 0;
     PSeg sg;
     for (; Q.next(sg, i); ++seg) {
+      const long long c0w = clock64();
       const int buf = seg & 1;
       const int mp = sg.tile / nt_n, nt = sg.tile - mp * nt_n;
       const int m_tile = 2 * mp + (int)rank;
@@ -1363,19 +1365,46 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       mbar_wait(&tfull[buf], (uint32_t)((seg >> 1) & 1));
       tc_fence_after();
       epi_bar();  // the previous tile's epilogue is done with the staging buffer / sm
+      const long long c1w = clock64();
+      c_wait += c1w - c0w;
       const uint32_t tacc = tb + (uint32_t)(buf * BN);
       column_meta<MODE>(g, sm, m_tile, n0, 0, W, et);
       const TileSrc ts0{nullptr, nullptr, 0u, 1, 0, BN, 0, 0};
 #pragma unroll 1
       for (int cb = 0; cb < W; cb += CHUNK) {
         const int ce = min(W, cb + CHUNK);
+        const long long cp0 = clock64();
+        if constexpr (MODE == EPI_ARGMAX) {
+          // lm_head: the column maxima are taken by a column scan of the staged tile, not by
+          // cross-lane shuffle chains (one warp per SM sub-partition could not hide their
+          // latency: 175 of the 282 us of the C3 lm_head were this epilogue).  Staging layout:
+          // column c, rows 4q .. 4q + 3 at 16-byte chunk q ^ (c & 31) -> conflict-free for
+          // both the row-per-thread writes and the column-per-thread 16-byte reads.
+          const int m = m_tile * 128 + et;
 #pragma unroll 1
-        for (int c0 = cb; c0 < ce; c0 += 16) {  // TMEM -> staging
-          float v[16];
-          tmem_ld16(tacc + (uint32_t)c0, v);
+          for (int c0 = cb; c0 < ce; c0 += 16) {
+            float v[16];
+            tmem_ld16(tacc + (uint32_t)c0, v);
 #pragma unroll
-          for (int k = 0; k < 16; ++k) stg[(c0 - cb + k) * 128 + et] = v[k];
+            for (int k = 0; k < 16; ++k) {
+              const int c = c0 - cb + k;
+              stg[c * 128 + ((((et >> 2) ^ (c & 31)) << 2) | (et & 3))] = v[k];
+            }
+            if (g.out && m < g.M)  // logits (parity mode only)
+#pragma unroll
+              for (int k = 0; k < 16; ++k)
+                if (n0 + c0 + k < g.N) g.out[(size_t)(n0 + c0 + k) * g.M + m] = v[k];
+          }
+        } else {
+#pragma unroll 1
+          for (int c0 = cb; c0 < ce; c0 += 16) {  // TMEM -> staging
+            float v[16];
+            tmem_ld16(tacc + (uint32_t)c0, v);
+#pragma unroll
+            for (int k = 0; k < 16; ++k) stg[(c0 - cb + k) * 128 + et] = v[k];
+          }
         }
+        c_park += clock64() - cp0;
         if (ce == W) {  // the accumulator buffer is read out: release it to the MMA issuer
           tc_fence_before();
           epi_bar();
@@ -1385,15 +1414,67 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           }
         }
         epi_bar();
-        TileSrc ts = ts0;
-        ts.P = stg - (size_t)cb * 128;  // the epilogue indexes absolute columns
-        epilogue<MODE>(g, sm, ts, m_tile, n0, cb, ce, et, false);
+        const long long ce0 = clock64();
+        if constexpr (MODE == EPI_ARGMAX) {
+          // thread et scans half `hf` of the rows of column c (64 rows as 16 chunks of 4),
+          // ascending -> the first maximum = the lowest vocabulary index (greedy, AMB: ties)
+          const int wc = ce - cb, c = et % CHUNK, hf = et / CHUNK;
+          if (c < wc && hf < 2) {
+            float bv = -INFINITY;
+            int br = 0;
+            const float* col = stg + (size_t)c * 128;
+            const int rmax = g.M - m_tile * 128;  // rows beyond M (last m-tile) never win
+#pragma unroll 4
+            for (int q = 16 * hf; q < 16 * hf + 16; ++q) {
+              const float4 x = *reinterpret_cast<const float4*>(col + ((q ^ (c & 31)) << 2));
+              if (x.x > bv && 4 * q < rmax) { bv = x.x; br = 4 * q; }
+              if (x.y > bv && 4 * q + 1 < rmax) { bv = x.y; br = 4 * q + 1; }
+              if (x.z > bv && 4 * q + 2 < rmax) { bv = x.z; br = 4 * q + 2; }
+              if (x.w > bv && 4 * q + 3 < rmax) { bv = x.w; br = 4 * q + 3; }
+            }
+            sm.redv[hf * BN + c] = bv;
+            sm.redi[hf * BN + c] = m_tile * 128 + br;
+          }
+          epi_bar();
+          if (et < wc && n0 + cb + et < g.N) {
+            float bv = sm.redv[et];
+            int bi = sm.redi[et];
+            const float ov = sm.redv[BN + et];
+            const int oi = sm.redi[BN + et];
+            if (ov > bv) {  // the lower half wins ties (lower index)
+              bv = ov;
+              bi = oi;
+            }
+            g.part_val[(size_t)m_tile * g.N + n0 + cb + et] = bv;
+            g.part_idx[(size_t)m_tile * g.N + n0 + cb + et] = bi;
+          }
+        } else {
+          TileSrc ts = ts0;
+          ts.P = stg - (size_t)cb * 128;  // the epilogue indexes absolute columns
+          epilogue<MODE>(g, sm, ts, m_tile, n0, cb, ce, et, false);
+        }
         epi_bar();
+        c_epi += clock64() - ce0;
       }
+    }
+    if (et == 0) {  // trace: totals over this CTA's tiles (wait for the accumulator | park | epilogue)
+      s_mark[0] = 0;
+      s_mark[1] = c_wait;
+      s_mark[2] = c_wait + c_park;
+      s_mark[3] = c_wait + c_park + c_epi;
+      for (int q = 4; q < 9; ++q) s_mark[q] = s_mark[3];
     }
   }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) {
+    auto dd = [&](int i) {
+      const long long d = s_mark[i + 1] - s_mark[i];
+      return (unsigned long long)(uint32_t)(d > 0 ? d : 0);
+    };
+    trace_phase(TK_PHASE | TK_GEMM | ((uint32_t)MODE << 8) | (2u << 16), dd(0) | (dd(1) << 32),
+                dd(2) | (dd(3) << 32), dd(4) | (dd(5) << 32), dd(6) | (dd(7) << 32));
+  }
   cluster_arrive();  // no CTA leaves while its peer may still signal its barriers
   cluster_wait();
   if (warp == 1) {
