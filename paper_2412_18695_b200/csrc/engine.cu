@@ -813,7 +813,8 @@ static rt_status forward(rt_engine* e, const HostMailbox& plan) {
     aa.ws = e->d_attn_ws;
     aa.tickets = e->d_attn_tickets;
     aa.scale_log2 = sl2;
-    if (plan.n_prefill_rows > 0) {  // decode rows only (prompt rows: k_attn_prefill)
+    // decode rows in the scheduler's longest-context-first order (prompt rows: k_attn_prefill)
+    {
       aa.row_list = P.dec_rows;
       aa.chunk_rows = n;
       aa.n_rows = plan.n_dec_rows;

@@ -346,9 +346,11 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
   while (n_pad < n) n_pad <<= 1;
   for (int i = tid; i < n_pad; i += nt) S.perm[i] = i;
   __syncthreads();
-  // bitonic sort of perm by key
+  // bitonic sort of perm by key.  Compare-exchange distances j >= 32 go through shared memory
+  // with a barrier per stage; j < 32 partners sit in the same warp, so those stages run on
+  // registers with shuffles (one barrier per kk instead of five): the same network
   for (int kk = 2; kk <= n_pad; kk <<= 1) {
-    for (int j = kk >> 1; j > 0; j >>= 1) {
+    for (int j = kk >> 1; j >= 32; j >>= 1) {
       for (int i = tid; i < n_pad; i += nt) {
         const int ixj = i ^ j;
         if (ixj > i) {
@@ -363,6 +365,21 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
       }
       __syncthreads();
     }
+    for (int base = 0; base < n_pad; base += nt) {  // every lane takes part in the shuffles
+      const int i = base + tid;
+      int x = i < n_pad ? S.perm[i] : n_pad;  // index >= n: sorts last, never read
+      const bool up = ((i & kk) == 0);
+      for (int j = min(kk >> 1, 16); j > 0; j >>= 1) {
+        const int y = __shfl_xor_sync(0xffffffffu, x, j);
+        // lower position: takes the partner when it goes first; upper: the mirror
+        const bool lower = (i & j) == 0;
+        const bool sw = lower ? (up ? key_before(S, y, x, n) : key_before(S, x, y, n))
+                              : (up ? key_before(S, x, y, n) : key_before(S, y, x, n));
+        if (sw) x = y;
+      }
+      if (i < n_pad) S.perm[i] = x;
+    }
+    __syncthreads();
   }
 
   PRE_MARK(3);
@@ -653,27 +670,46 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
   __syncthreads();
   const int n_rows = block_scan_excl(S.cnt_a, B, wbuf);
   int n_prefill_rows = 0;
-  for (int s = tid; s < B; s += nt) {
-    const int task = p.slot_task[s];
-    const int off = S.cnt_a[s];
-    if (S.sflag[s] == 1) {
-      const int P = T.n_prompt[task];
-      const int Lp = p.page_tokens * T.n_pfx[task];  // prefix positions are not recomputed
-      p.slot_row[s] = off + (P - Lp) - 1;
-      T.ctx[task] = P;
-      atomicAdd(&s_sum_prompt, (unsigned long long)(P - Lp));
-      atomicAdd(&s_attn_tok, (unsigned long long)P * (P + 1) / 2 - (unsigned long long)Lp * (Lp + 1) / 2);
-      atomicMax(&s_max_seqlen, P);
-    } else {
-      const int c = T.ctx[task];
-      p.row_task[off] = task;
-      p.row_pos[off] = c;
-      p.row_tok[off] = T.pending[task];
-      p.slot_row[s] = off;
-      T.ctx[task] = c + 1;
-      atomicAdd(&s_sum_ctx, (unsigned long long)(c + 1));
-      atomicAdd(&s_attn_tok, (unsigned long long)(c + 1));
-      atomicMax(&s_max_seqlen, c + 1);
+  {
+    // the round's sums are accumulated per thread and reduced per warp: one shared atomic
+    // per warp (64-bit shared atomicAdd is a CAS spin loop, ~20 us at 256 contending slots)
+    unsigned long long l_prompt = 0, l_attn = 0, l_ctx = 0;
+    int l_max = 0;
+    for (int s = tid; s < B; s += nt) {
+      const int task = p.slot_task[s];
+      const int off = S.cnt_a[s];
+      if (S.sflag[s] == 1) {
+        const int P = T.n_prompt[task];
+        const int Lp = p.page_tokens * T.n_pfx[task];  // prefix positions are not recomputed
+        p.slot_row[s] = off + (P - Lp) - 1;
+        T.ctx[task] = P;
+        l_prompt += (unsigned long long)(P - Lp);
+        l_attn += (unsigned long long)P * (P + 1) / 2 - (unsigned long long)Lp * (Lp + 1) / 2;
+        l_max = max(l_max, P);
+      } else {
+        const int c = T.ctx[task];
+        p.row_task[off] = task;
+        p.row_pos[off] = c;
+        p.row_tok[off] = T.pending[task];
+        p.slot_row[s] = off;
+        T.ctx[task] = c + 1;
+        l_ctx += (unsigned long long)(c + 1);
+        l_attn += (unsigned long long)(c + 1);
+        l_max = max(l_max, c + 1);
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      l_prompt += __shfl_xor_sync(0xffffffffu, l_prompt, o);
+      l_attn += __shfl_xor_sync(0xffffffffu, l_attn, o);
+      l_ctx += __shfl_xor_sync(0xffffffffu, l_ctx, o);
+      l_max = max(l_max, __shfl_xor_sync(0xffffffffu, l_max, o));
+    }
+    if ((tid & 31) == 0 && (l_prompt | l_attn | l_ctx)) {
+      atomicAdd(&s_sum_prompt, l_prompt);
+      atomicAdd(&s_attn_tok, l_attn);
+      atomicAdd(&s_sum_ctx, l_ctx);
+      atomicMax(&s_max_seqlen, l_max);
     }
   }
   // prefill rows filled slot by slot, all threads in parallel; the prompt is cut into
@@ -699,14 +735,26 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
     n_pf_tiles += nt16;
     n_prefill_rows += P - Lp;
   }
-  // rows of the decode slots (running slots, then k > 0 resumes in admission order): the
-  // decode attention grid of rounds that also carry prompt rows
-  for (int s = tid; s < n_run; s += nt) p.dec_rows[s] = S.cnt_a[s];
-  if (tid == 0) {
-    int k = n_run;
-    for (int s = n_run; s < B; ++s)
-      if (S.sflag[s] != 1) p.dec_rows[k++] = S.cnt_a[s];
-    s_ndec = k;
+  // rows of the decode slots, longest context first: the decode attention's grid (one CTA per
+  // (row, KV head), issued in grid order).  Largest-processing-time order — the long rows
+  // start first and the short ones fill the tail of the last wave.  Counting sort on the
+  // page count (a bucket per page count, 1024 buckets); rows of one bucket in any order: each
+  // row's attention is independent of when its CTA runs.
+  {
+    constexpr int NB = 1024;
+    for (int i = tid; i < NB; i += nt) S.ck[i] = 0;
+    __syncthreads();
+    for (int s = tid; s < B; s += nt)  // same slot -> thread map as the rows loop (T.ctx)
+      if (S.sflag[s] != 1) {
+        const int kb = NB - 1 - min((T.ctx[p.slot_task[s]] + p.page_tokens - 1) / p.page_tokens, NB - 1);
+        S.cR[s] = kb;
+        atomicAdd(&S.ck[kb], 1);
+      }
+    __syncthreads();
+    const int ndec = block_scan_excl(S.ck, NB, wbuf);
+    for (int s = tid; s < B; s += nt)
+      if (S.sflag[s] != 1) p.dec_rows[atomicAdd(&S.ck[S.cR[s]], 1)] = S.cnt_a[s];
+    if (tid == 0) s_ndec = ndec;
   }
   __syncthreads();
 
