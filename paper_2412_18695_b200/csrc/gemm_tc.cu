@@ -124,7 +124,9 @@ __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float* v) {
 #pragma unroll
   for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
-__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+// named barrier of one 128-thread epilogue group (id 1; the decode pair kernel's second
+// group uses id 2)
+__device__ __forceinline__ void epi_bar(int id = 1) { asm volatile("bar.sync %0, 128;" ::"r"(id) : "memory"); }
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -154,9 +156,10 @@ struct EpiSmem {
                  //  EPI_QKV cos [16][64] then sin [16][64])
   long long* mark;  // clock64 phase marks (trace), written by thread et == 0
   bf16* stg = nullptr;  // nullable: EPI_QKV staging [2][16][128] bf16 (whole head rows, 16-byte stores)
+  int bar = 1;          // named barrier of this epilogue group (128 threads)
 };
 #define EPI_MARK(i) \
-  if (et == 0) sm.mark[i] = clock64()
+  if (et == 0 && sm.mark) sm.mark[i] = clock64()
 
 // Reductions of 4 columns across the 32 lanes at once (reduce-scatter: 6 shuffles instead
 // of 4 x 5): the result for column j = (lane >> 3) & 3 ends on lanes with lane & 7 == 0.
@@ -392,7 +395,7 @@ __device__ __forceinline__ void epilogue(const GemmArgs& g, const EpiSmem& sm, c
         bf16* st = sm.stg + (((c0 - cb) / CH) & 1) * (CH * 128);
 #pragma unroll
         for (int k = 0; k < CH; ++k) st[k * 128 + dim] = yb[k];
-        epi_bar();
+        epi_bar(sm.bar);
         if (active) {
           const int kind = head < q.nq ? 2 : (rope ? 0 : 1);
           const int kvh = kind == 0 ? head - q.nq : head - q.nq - q.nkv;
@@ -472,7 +475,7 @@ __device__ __forceinline__ void epilogue(const GemmArgs& g, const EpiSmem& sm, c
   }
   EPI_MARK(6);
   if constexpr (MODE == EPI_RESID || MODE == EPI_ARGMAX) {
-    epi_bar();
+    epi_bar(sm.bar);
     for (int c = cb + et; c < NL; c += 128) {  // fixed order over the 4 row quarters
       if constexpr (MODE == EPI_RESID) {
         const float t = ((sm.redv[c] + sm.redv[sm.bn + c]) + sm.redv[2 * sm.bn + c]) + sm.redv[3 * sm.bn + c];
@@ -532,24 +535,40 @@ __device__ __forceinline__ bool column_meta(const GemmArgs& g, const EpiSmem& sm
       sm.inv[cc] = rsqrtf(t / (float)g.K + 1e-5f);
     }
   }
-  epi_bar();
+  epi_bar(sm.bar);
   if (ce - cb > 16 || !allow_pre) return false;
   const int m = m_tile * 128 + et;
+  // all (<= 16 columns) loads in flight at once, then the shared stores (a serial
+  // load -> store loop paid one L2 round trip per column: the top stall of the O projection)
   if constexpr (MODE == EPI_RESID) {
-#pragma unroll 1
-    for (int c = cb; c < ce; ++c)
-      if (m < g.M && n0 + c < g.N) sm.xp[(c - cb) * 128 + et] = g.x[(size_t)(n0 + c) * g.M + m];
+    float v[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const int c = cb + k;
+      v[k] = (c < ce && m < g.M && n0 + c < g.N) ? __ldcg(g.x + (size_t)(n0 + c) * g.M + m) : 0.f;
+    }
+#pragma unroll
+    for (int k = 0; k < 16; ++k)
+      if (cb + k < ce) sm.xp[k * 128 + et] = v[k];
     return true;
   } else if constexpr (MODE == EPI_QKV) {
     const int half = g.qkv.hd >> 1;
     if (et < 64) {  // cos / sin of the rotation (position of the column, frequency i)
       const int i = et % half;
-#pragma unroll 1
-      for (int c = cb; c < ce; ++c)
-        if (n0 + c < g.N) {
-          const int pos = sm.pos[c];
-          sm.xp[(c - cb) * 64 + et] = g.qkv.cos[(size_t)pos * half + i];
-          sm.xp[1024 + (c - cb) * 64 + et] = g.qkv.sin[(size_t)pos * half + i];
+      float vc[16], vs[16];
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const int c = cb + k;
+        const bool ok = c < ce && n0 + c < g.N;
+        const int pos = ok ? sm.pos[c] : 0;
+        vc[k] = ok ? __ldg(g.qkv.cos + (size_t)pos * half + i) : 0.f;
+        vs[k] = ok ? __ldg(g.qkv.sin + (size_t)pos * half + i) : 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < 16; ++k)
+        if (cb + k < ce) {
+          sm.xp[k * 64 + et] = vc[k];
+          sm.xp[1024 + k * 64 + et] = vs[k];
         }
     }
     return true;
@@ -1525,7 +1544,7 @@ struct Cfg {
 // and the epilogue inputs (128 floats per owned column)
 template <int BN>
 __host__ __device__ inline bool dec_fits(int S, int wslot) {
-  return (int64_t)S * wslot * 512 + 8192 <= Cfg<BN>::RING;  // + the EPI_QKV staging
+  return (int64_t)S * wslot * 512 + 16384 <= Cfg<BN>::RING;  // + the EPI_QKV staging of 2 groups
 }
 // owned columns of pair p: 16-column chunks split as evenly as possible; a workspace slot
 // holds the widest slice (dec_slot columns of 128 fp32)
@@ -1542,8 +1561,10 @@ RT_DEV unsigned ld_acquire_gpu(const unsigned* p) {
 }
 }  // namespace dec
 
+constexpr int kDecThreads = 320;  // producer, MMA, 2 x 4 epilogue warps
+
 template <int BN, int MODE>
-__global__ void __launch_bounds__(kGemmThreads, 1)
+__global__ void __launch_bounds__(kDecThreads, 1)
     k_gemm_dec(const __grid_constant__ TmaMap tmA, const __grid_constant__ TmaMap tmB, GemmArgs g, int S,
                float* ws, unsigned* flags, unsigned epoch) {
   using C = dec::Cfg<BN>;
@@ -1670,14 +1691,25 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     __syncwarp();
   } else {
+    // two epilogue groups of 4 warps (warps 2-5, 6-9): both cover the 128 TMEM lanes (lane
+    // quarter = warp % 4) and split the columns, so the latency-bound exchange, sum and fused
+    // loops run on 8 warps (2 per SM sub-partition)
     pdl_wait();
+    const int grp = (warp - 2) >> 2;
     const int et = (warp & 3) * 32 + lane;
     const uint32_t tb = tmem + ((uint32_t)((warp & 3) * 32) << 16);
-    // per-column metadata of the owned columns while the mainloop runs
-    column_meta<MODE>(g, sm, m_tile, 0, cb, ce, et, false);
+    // owned columns of this group: 16-column halves of [cb, ce)
+    const int gm = cb + 16 * ((((ce - cb) >> 4) + 1) >> 1);
+    const int gcb = grp == 0 ? cb : gm, gce = grp == 0 ? gm : ce;
+    EpiSmem gs = sm;
+    gs.bar = 1 + grp;
+    gs.mark = grp == 0 ? s_mark : nullptr;
+    // per-column metadata of the owned columns while the mainloop runs (group 0; ordered
+    // before group 1's reads by the 256-thread barrier after the exchange writes)
+    if (grp == 0) column_meta<MODE>(g, sm, m_tile, 0, cb, ce, et, false);
     mbar_wait(done, 0);
     tc_fence_after();
-    if (et == 0) {
+    if (et == 0 && grp == 0) {
       s_tdone = gtimer();
       const long long c0 = clock64();
 #pragma unroll
@@ -1686,7 +1718,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     // the ring is free: the epilogue inputs -> shared memory (bulk copies on pf_bar, one column
     // per thread: issued serially by one thread they took ~10 us for 96 columns), in flight
     // while the split-K exchange runs.  (complete_tx may precede the expect_tx of the phase.)
-    {
+    if (grp == 0) {
       const int cn = min(ce, g.N) - cb;  // owned columns that hold rows
       if constexpr (MODE == EPI_RESID) {
         if (et == 0) mbar_arrive_expect_tx(pf_bar, (uint32_t)max(cn, 0) * 512);
@@ -1705,22 +1737,24 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       }
     }
     // ---- split-K exchange through L2: the slices other pairs own -> their workspace slots
-    for (int q = 0; q < S; ++q) {
+    // (16-column chunks alternate between the groups)
+    for (int q = 0, j = 0; q < S; ++q) {
       if (q == p) continue;
       const int qb = dec::dec_col(BN, S, q), qe = dec::dec_col(BN, S, q + 1);
       float* dst = slot_ptr(q, p) + et;
 #pragma unroll 1
-      for (int c0 = qb; c0 < qe; c0 += 16) {
+      for (int c0 = qb; c0 < qe; c0 += 16, ++j) {
+        if ((j & 1) != grp) continue;
         float v[16];
         tmem_ld16(tb + (uint32_t)c0, v);
 #pragma unroll
-        for (int j = 0; j < 16; ++j) __stcg(dst + (size_t)(c0 - qb + j) * 128, v[j]);
+        for (int jj = 0; jj < 16; ++jj) __stcg(dst + (size_t)(c0 - qb + jj) * 128, v[jj]);
       }
     }
     EPI_MARK(1);
-    epi_bar();  // every row of this CTA's slices is written
+    asm volatile("bar.sync 3, 256;" ::: "memory");  // every row of this CTA's slices is written
     unsigned* myflags = flags + ((size_t)t * 2 + h) * S;
-    if (et == 0) {
+    if (et == 0 && grp == 0) {
       __threadfence();
       dec::st_release_gpu(myflags + p, epoch);
     }
@@ -1729,7 +1763,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     // j = 0 .. S - 2 in pair order, wslot columns each) into shared memory at once
     float* R = reinterpret_cast<float*>(smem);
     const uint32_t slice_bytes = (uint32_t)(ce - cb) * 512;
-    if (et == 0) {
+    if (et == 0 && grp == 0) {
       for (int q = 0; q < S; ++q)
         if (q != p)
           while (dec::ld_acquire_gpu(myflags + q) != epoch) __nanosleep(32);
@@ -1740,11 +1774,11 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     EPI_MARK(3);
     mbar_wait(rx_bar, 0);
-    // ---- sum the S partials of the owned slice in pair order (deterministic) -> T (= slot 0:
-    // every element is read, then written, by the same thread)
+    // ---- sum the S partials of the group's columns in pair order (deterministic) -> T (= slot
+    // 0: every element is read, then written, by the same thread)
     float* T = R;
 #pragma unroll 1
-    for (int c0 = cb; c0 < ce; c0 += 16) {
+    for (int c0 = gcb; c0 < gce; c0 += 16) {
       float own[16], acc[16];
       tmem_ld16(tb + (uint32_t)c0, own);
 #pragma unroll
@@ -1756,17 +1790,20 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         } else {
           const float* src = R + (size_t)(jq++) * wslot * 128 + (size_t)(c0 - cb) * 128 + et;
 #pragma unroll
-          for (int j = 0; j < 16; ++j) acc[j] += (c0 + j < ce) ? src[j * 128] : 0.f;
+          for (int j = 0; j < 16; ++j) acc[j] += (c0 + j < gce) ? src[j * 128] : 0.f;
         }
       }
 #pragma unroll
       for (int j = 0; j < 16; ++j)
-        if (c0 + j < ce) T[(c0 - cb + j) * 128 + et] = acc[j];
+        if (c0 + j < gce) T[(c0 - cb + j) * 128 + et] = acc[j];
     }
     mbar_wait(pf_bar, 0);  // prefetched epilogue inputs
-    epi_bar();
+    epi_bar(gs.bar);
+    // the group's view of the prefetched inputs (indexed from its first column) and staging
+    gs.xp = xp + (size_t)(gcb - cb) * (MODE == EPI_QKV ? 64 : 128);
+    if (gs.stg) gs.stg = sm.stg + grp * (2 * kEpiCh * 128);
     const TileSrc ts{T - (size_t)cb * 128, nullptr, 0u, 1, 0, BN, 0, 0};
-    epilogue<MODE>(g, sm, ts, m_tile, 0, cb, ce, et, true);
+    if (gcb < gce) epilogue<MODE>(g, gs, ts, m_tile, 0, gcb, gce, et, true);
     EPI_MARK(8);
   }
   tc_fence_before();
@@ -2102,7 +2139,7 @@ static cudaError_t launch_dec_bn(const TmaMap& am, const TmaMap& bm, const GemmA
   }
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2 * S * PT);
-  cfg.blockDim = dim3(kGemmThreads);
+  cfg.blockDim = dim3(kDecThreads);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = s;
   cudaLaunchAttribute at[2];

@@ -9,7 +9,8 @@ import os
 
 import numpy as np
 
-_LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib", "librt_b200.so")
+_LIB_PATH = os.environ.get("RT_LIB_PATH") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "lib",
+                                                         "librt_b200.so")  # RT_LIB_PATH: A/B builds (tools)
 _lib = None
 
 RT_OK, RT_E_INVAL, RT_E_NOMEM, RT_E_CUDA, RT_E_NCCL, RT_E_STATE = 0, -1, -2, -3, -4, -5
