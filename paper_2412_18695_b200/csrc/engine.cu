@@ -16,6 +16,7 @@
 #include <string>
 #include <unordered_map>
 #include <vector>
+#include <atomic>
 
 #include "rt.h"
 #include "internal.h"
@@ -981,12 +982,25 @@ extern "C" rt_status rt_step(rt_engine* e, int64_t now_us, rt_round_info* info) 
   rt_status st = flush_staging(e);
   if (st != RT_OK) return st;
   if (timing) cudaEventRecord(e->ev_s0, s);
+  const volatile HostMailbox* mb = e->h_mb;
+  const int64_t seq0 = mb->plan_seq;
   launch_sched_pre(e->sp, now_us, s);
   if (timing) cudaEventRecord(e->ev_s1, s);
-  CK(e, cudaEventRecord(e->ev_plan, s));
-  CK(e, cudaEventSynchronize(e->ev_plan));
   CK(e, cudaGetLastError());
-  const volatile HostMailbox* mb = e->h_mb;
+  // plan handshake: spin on the sequence number k_sched_pre writes last into the mapped
+  // mailbox (an event record + synchronize cost ~5 us more per round); the stream is polled
+  // now and then so a device fault cannot hang the host
+  for (uint32_t it = 1; mb->plan_seq == seq0; ++it) {
+    if ((it & 1023) == 0) {
+      const cudaError_t q = cudaStreamQuery(s);
+      if (q != cudaSuccess && q != cudaErrorNotReady) return fail(e, RT_E_CUDA, cudaGetErrorString(q));
+      if (q == cudaSuccess && mb->plan_seq == seq0) return fail(e, RT_E_STATE, "plan handshake: no plan published");
+    }
+#if defined(__x86_64__)
+    __builtin_ia32_pause();
+#endif
+  }
+  std::atomic_thread_fence(std::memory_order_acquire);
   HostMailbox plan;
   memcpy(&plan, (const void*)mb, sizeof(plan));
   e->plan = plan;

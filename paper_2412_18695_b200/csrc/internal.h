@@ -54,6 +54,7 @@ struct DevState {
   int32_t error;
   int32_t hfree_top;     // host free-stack size (R-EVICT)
   int32_t n_swap, n_evicted, n_restored;  // this round's page copies / requests
+  int64_t plan_seq;      // rounds planned by k_sched_pre (published as HostMailbox::plan_seq)
 };
 
 // Round plan / summary published to the host (mapped pinned memory).
@@ -68,6 +69,7 @@ struct HostMailbox {
   int32_t n_dec_rows;    // decode rows of this round (SchedParams::dec_rows)
   int32_t n_swap, n_evicted, n_restored;  // KV page copies (SchedParams::swap) / requests
   int32_t n_swap_ev;     // the first n_swap_ev copies are evictions (device -> host)
+  int64_t plan_seq;      // written LAST by k_sched_pre (after a system fence): the plan is complete
 };
 
 struct SegRec {  // identical layout to rt_segment

@@ -57,6 +57,14 @@ __device__ double priority_d(int64_t t, int32_t k, int64_t ref, int64_t D, int64
 
 __device__ __forceinline__ int ceil_div_i(int a, int b) { return (a + b - 1) / b; }
 
+// The plan handshake (rt_step): the mailbox fields are written and fenced first, then the
+// sequence number the host spins on (mapped pinned memory, no event round trip)
+__device__ __forceinline__ void publish_plan(DevState* st, HostMailbox* mb) {
+  const long long q = st->plan_seq + 1;
+  st->plan_seq = q;
+  *reinterpret_cast<volatile long long*>(&mb->plan_seq) = q;
+}
+
 // Exclusive scan in place over a[0..n) (shared memory), returns the total.
 // All threads of the block must call it.
 __device__ int block_scan_excl(int* a, int n, int* wbuf) {
@@ -175,8 +183,9 @@ struct PreSmem {
   int evc[kMaxTasks];   // candidate's KV is on the host (T.evicted at scoring time)
   int admx[kMaxTasks];  // candidate index of each admission
   int sflag[kMaxTasks]; // batch slot: 1 = prefill (k = 0 admission), 2 = restore (evicted resume)
-  long long wb[32];     // WCET gate: per-warp (budget, rid, seg_tok) minima
-  long long wr[32];
+  long long wb[32];     // WCET gate: per-warp (budget, rid, seg_tok) minima; then the
+  long long wr[32];     // per-warp round sums of the rows loop (prompt, attended, ctx, max)
+  long long wc[32];
   int ws[32];
 };
 
@@ -190,6 +199,130 @@ __device__ __forceinline__ bool key_before(const PreSmem& S, int x, int y, int n
   return S.a3[x] < S.a3[y];
 }
 
+// Sort of the n <= blockDim.x scored candidates (n_pad = power of two >= 32, <= blockDim.x):
+// every key becomes a tuple of order-preserving u64 words (Pri descending via its IEEE bits
+// — the -0.0 -> +0.0 canonicalisation makes equal priorities equal bit patterns —, then
+// a1, a2, a3 ascending, then the candidate index), one element per thread, bitonic network
+// with the exchange on registers (shuffles) for distances < 32 and through double-buffered
+// shared memory otherwise (one barrier per stage).  Result: S.perm[0 .. n_pad).  The key
+// arrays S.a0..a3 are reused as the exchange buffers.
+__device__ __forceinline__ unsigned long long desc_key_f64(double d) {
+  const unsigned long long u = (unsigned long long)__double_as_longlong(d);
+  const unsigned long long asc = (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+  return ~asc;
+}
+struct SortKey {
+  unsigned long long k0, k1, k2, k3;
+  int ix;
+};
+__device__ __forceinline__ bool sk_less(const SortKey& a, const SortKey& b) {
+  if (a.k0 != b.k0) return a.k0 < b.k0;
+  if (a.k1 != b.k1) return a.k1 < b.k1;
+  if (a.k2 != b.k2) return a.k2 < b.k2;
+  if (a.k3 != b.k3) return a.k3 < b.k3;
+  return a.ix < b.ix;
+}
+__device__ __forceinline__ unsigned long long shfl_u64(unsigned long long v, int j) {
+  const unsigned lo = __shfl_xor_sync(0xffffffffu, (unsigned)v, j);
+  const unsigned hi = __shfl_xor_sync(0xffffffffu, (unsigned)(v >> 32), j);
+  return ((unsigned long long)hi << 32) | lo;
+}
+__device__ void sort_keys_small(PreSmem& S, int n, int n_pad, bool pud) {
+  const int tid = threadIdx.x;
+  const bool act = tid < n_pad;
+  SortKey me;
+  if (tid < n) {
+    me.k0 = pud ? desc_key_f64(S.a0[tid]) : 0ull;
+    me.k1 = enc_i64(S.a1[tid]);
+    me.k2 = enc_i64(S.a2[tid]);
+    me.k3 = enc_i64(S.a3[tid]);
+    me.ix = tid;
+  } else {  // padding: sorts last
+    me.k0 = me.k1 = me.k2 = me.k3 = ~0ull;
+    me.ix = tid;
+  }
+  __syncthreads();  // the key arrays become the exchange buffers
+  unsigned long long* xb = reinterpret_cast<unsigned long long*>(S.a0);  // [2][4][blockDim.x] (a0..a3)
+  int* xi = S.cnt_a;                                                     // [2][blockDim.x]
+  const int nt = blockDim.x;
+  int buf = 0;
+  for (int kk = 2; kk <= n_pad; kk <<= 1) {
+    for (int j = kk >> 1; j > 0; j >>= 1) {
+      SortKey o;
+      if (j >= 32) {
+        unsigned long long* b = xb + (size_t)buf * 4 * nt;
+        if (act) {
+          b[tid] = me.k0;
+          b[nt + tid] = me.k1;
+          b[2 * nt + tid] = me.k2;
+          b[3 * nt + tid] = me.k3;
+          xi[buf * nt + tid] = me.ix;
+        }
+        __syncthreads();
+        if (act) {
+          const int q = tid ^ j;
+          o.k0 = b[q];
+          o.k1 = b[nt + q];
+          o.k2 = b[2 * nt + q];
+          o.k3 = b[3 * nt + q];
+          o.ix = xi[buf * nt + q];
+        }
+        buf ^= 1;  // the next stage writes the other buffer: no second barrier
+      } else if (tid < ((n_pad + 31) & ~31)) {
+        o.k0 = shfl_u64(me.k0, j);
+        o.k1 = shfl_u64(me.k1, j);
+        o.k2 = shfl_u64(me.k2, j);
+        o.k3 = shfl_u64(me.k3, j);
+        o.ix = __shfl_xor_sync(0xffffffffu, me.ix, j);
+      }
+      if (act) {
+        const bool up = (tid & kk) == 0, lower = (tid & j) == 0;
+        // lower position keeps the smaller key of an ascending pair, the larger of a descending one
+        const bool take = (lower == up) ? sk_less(o, me) : sk_less(me, o);
+        if (take) me = o;
+      }
+    }
+  }
+  __syncthreads();
+  if (act) S.perm[tid] = me.ix;
+  __syncthreads();
+}
+
+// Rank sort for few candidates (n <= 128, the usual waiting queue): candidate i goes to
+// position #{j : key_j < key_i} (keys unique by index), one pass over the keys in shared
+// memory (broadcast reads), no compare-exchange network.  Same keys as sort_keys_small.
+__device__ void sort_keys_rank(PreSmem& S, int n, bool pud) {
+  const int tid = threadIdx.x;
+  unsigned long long* K = reinterpret_cast<unsigned long long*>(S.cnt_a);  // [4][n] (cnt_a, cnt_b)
+  SortKey me;
+  if (tid < n) {
+    me.k0 = pud ? desc_key_f64(S.a0[tid]) : 0ull;
+    me.k1 = enc_i64(S.a1[tid]);
+    me.k2 = enc_i64(S.a2[tid]);
+    me.k3 = enc_i64(S.a3[tid]);
+    me.ix = tid;
+    K[tid] = me.k0;
+    K[n + tid] = me.k1;
+    K[2 * n + tid] = me.k2;
+    K[3 * n + tid] = me.k3;
+  }
+  __syncthreads();
+  if (tid < n) {
+    int r = 0;
+#pragma unroll 4
+    for (int j = 0; j < n; ++j) {
+      const unsigned long long a0 = K[j], a1 = K[n + j], a2 = K[2 * n + j], a3 = K[3 * n + j];
+      // key_j < key_me, lexicographic, without branches (index j breaks ties)
+      const bool lt = a0 < me.k0 ||
+                      (a0 == me.k0 && (a1 < me.k1 || (a1 == me.k1 && (a2 < me.k2 || (a2 == me.k2 &&
+                                                                   (a3 < me.k3 || (a3 == me.k3 && j < tid)))))));
+      r += lt ? 1 : 0;
+    }
+    S.perm[r] = tid;
+  }
+  __syncthreads();
+}
+
 __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, int64_t now_us) {
   TraceScope tr(TK_SCHED_PRE);
   extern __shared__ __align__(16) unsigned char dsm[];
@@ -200,7 +333,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
   __shared__ unsigned long long s_min_arr;
   __shared__ int wbuf[32];
   __shared__ unsigned long long s_sum_ctx, s_sum_prompt, s_attn_tok;
-  __shared__ int s_max_seqlen, s_ndec;
+  __shared__ int s_max_seqlen, s_ndec, s_npf;
   __shared__ long long s_pm[10];  // clock64 phase marks (RT_FLAG_TRACE)
 #define PRE_MARK(i) \
   if (threadIdx.x == 0) s_pm[i] = clock64()
@@ -226,6 +359,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
     s_min_arr = ~0ull;
     s_outstanding = 0;
     s_sum_ctx = 0;
+    s_npf = 0;
     s_sum_prompt = 0;
     s_attn_tok = 0;
     s_max_seqlen = 0;
@@ -295,6 +429,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
           p.cand[j * 4 + 2] = -1.0;
         }
         __threadfence_system();
+        publish_plan(st, mb);
       }
       return;
     }
@@ -344,42 +479,51 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
   const int n = s_nc;
   int n_pad = 1;
   while (n_pad < n) n_pad <<= 1;
-  for (int i = tid; i < n_pad; i += nt) S.perm[i] = i;
-  __syncthreads();
-  // bitonic sort of perm by key.  Compare-exchange distances j >= 32 go through shared memory
-  // with a barrier per stage; j < 32 partners sit in the same warp, so those stages run on
-  // registers with shuffles (one barrier per kk instead of five): the same network
-  for (int kk = 2; kk <= n_pad; kk <<= 1) {
-    for (int j = kk >> 1; j >= 32; j >>= 1) {
-      for (int i = tid; i < n_pad; i += nt) {
-        const int ixj = i ^ j;
-        if (ixj > i) {
-          const int x = S.perm[i], y = S.perm[ixj];
-          const bool up = ((i & kk) == 0);
-          const bool sw = up ? key_before(S, y, x, n) : key_before(S, x, y, n);
-          if (sw) {
-            S.perm[i] = y;
-            S.perm[ixj] = x;
+  if (n <= 1) {
+    if (tid == 0) S.perm[0] = 0;
+    __syncthreads();
+  } else if (n <= 128) {
+    sort_keys_rank(S, n, p.policy == 0);
+  } else if (n_pad <= nt) {
+    sort_keys_small(S, n, n_pad, p.policy == 0);
+  } else {
+    for (int i = tid; i < n_pad; i += nt) S.perm[i] = i;
+    __syncthreads();
+    // bitonic sort of perm by key.  Compare-exchange distances j >= 32 go through shared memory
+    // with a barrier per stage; j < 32 partners sit in the same warp, so those stages run on
+    // registers with shuffles (one barrier per kk instead of five): the same network
+    for (int kk = 2; kk <= n_pad; kk <<= 1) {
+      for (int j = kk >> 1; j >= 32; j >>= 1) {
+        for (int i = tid; i < n_pad; i += nt) {
+          const int ixj = i ^ j;
+          if (ixj > i) {
+            const int x = S.perm[i], y = S.perm[ixj];
+            const bool up = ((i & kk) == 0);
+            const bool sw = up ? key_before(S, y, x, n) : key_before(S, x, y, n);
+            if (sw) {
+              S.perm[i] = y;
+              S.perm[ixj] = x;
+            }
           }
         }
+        __syncthreads();
+      }
+      for (int base = 0; base < n_pad; base += nt) {  // every lane takes part in the shuffles
+        const int i = base + tid;
+        int x = i < n_pad ? S.perm[i] : n_pad;  // index >= n: sorts last, never read
+        const bool up = ((i & kk) == 0);
+        for (int j = min(kk >> 1, 16); j > 0; j >>= 1) {
+          const int y = __shfl_xor_sync(0xffffffffu, x, j);
+          // lower position: takes the partner when it goes first; upper: the mirror
+          const bool lower = (i & j) == 0;
+          const bool sw = lower ? (up ? key_before(S, y, x, n) : key_before(S, x, y, n))
+                                : (up ? key_before(S, x, y, n) : key_before(S, y, x, n));
+          if (sw) x = y;
+        }
+        if (i < n_pad) S.perm[i] = x;
       }
       __syncthreads();
     }
-    for (int base = 0; base < n_pad; base += nt) {  // every lane takes part in the shuffles
-      const int i = base + tid;
-      int x = i < n_pad ? S.perm[i] : n_pad;  // index >= n: sorts last, never read
-      const bool up = ((i & kk) == 0);
-      for (int j = min(kk >> 1, 16); j > 0; j >>= 1) {
-        const int y = __shfl_xor_sync(0xffffffffu, x, j);
-        // lower position: takes the partner when it goes first; upper: the mirror
-        const bool lower = (i & j) == 0;
-        const bool sw = lower ? (up ? key_before(S, y, x, n) : key_before(S, x, y, n))
-                              : (up ? key_before(S, x, y, n) : key_before(S, y, x, n));
-        if (sw) x = y;
-      }
-      if (i < n_pad) S.perm[i] = x;
-    }
-    __syncthreads();
   }
 
   PRE_MARK(3);
@@ -388,7 +532,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
     if (tid < n) {  // record {Pri (0 for FCFS/EDF), arrival, global id, rank}
       const int x = S.perm[tid];
       const int task = S.cslot[x];
-      p.cand[tid * 4 + 0] = p.policy == 0 ? S.a0[x] : 0.0;
+      p.cand[tid * 4 + 0] = p.policy == 0 ? T.pri[task] : 0.0;
       p.cand[tid * 4 + 1] = (double)T.arrival[task];
       p.cand[tid * 4 + 2] = (double)T.rid[task];
       p.cand[tid * 4 + 3] = (double)p.rank;
@@ -459,7 +603,61 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
   // host memory when a candidate that needs memory does not fit (R-EVICT):
   // suspended holders LATER in the key order are evicted, lowest priority first, only if
   // evicting them (within the host pool) makes the candidate fit
-  if (tid == 0) {
+  if (p.host_pages <= 0 && n > 32) {
+    // no KV host pool (no eviction), more than a warp of candidates: the serial admission loop below in closed form, all
+    // threads.  Walking the key order, a memory-needing candidate (k = 0, or an evicted
+    // resume) is admitted iff the reservations of the memory-needing candidates up to and
+    // including it fit (R-MEM: once one does not fit, no later one does: the prefix only
+    // grows); resumes need none; the first cap = min(max_admit, max_batch - n_run) admissible
+    // candidates are admitted, and refusals count up to the last admission (the loop stops
+    // there).  Two block scans instead of a serial walk (the walk is faster for <= 32).
+    const long long avail = (long long)st->free_top - s_outstanding;
+    const int cap = max(0, min(p.max_admit, p.max_batch - n_run));
+    const bool gate = s_gate_ok != 0;
+    if (tid == 0) s_nc = (cap > 0) ? n : 0;  // c_stop (the serial loop's last iteration + 1)
+    for (int c = tid; c < n; c += nt) {
+      const int x = S.perm[c];
+      S.cnt_a[c] = (S.ck[x] == 0 || S.evc[x]) ? S.cR[x] : 0;  // reservation pages needed
+    }
+    __syncthreads();
+    block_scan_excl(S.cnt_a, n, wbuf);  // pages of the memory-needing candidates before c
+    for (int c = tid; c < n; c += nt) {
+      const int x = S.perm[c];
+      const bool memc = S.ck[x] == 0 || S.evc[x];
+      S.cnt_b[c] = (!memc || (long long)S.cnt_a[c] + S.cR[x] <= avail) ? 1 : 0;
+    }
+    __syncthreads();
+    // (cnt_b is rewritten in place by the scan: keep each candidate's admissibility first)
+    for (int c = tid; c < n; c += nt) S.sflag[c] = S.cnt_b[c];
+    __syncthreads();
+    const int tot_ok = block_scan_excl(S.cnt_b, n, wbuf);
+    int my_rmem = 0;
+    for (int c = tid; c < n; c += nt) {
+      const int x = S.perm[c];
+      const int rank = S.cnt_b[c];
+      if (S.sflag[c] && rank < cap && gate) {
+        S.admx[rank] = x;
+        S.adm[rank] = S.cslot[x];
+        if (rank == cap - 1) s_nc = c + 1;
+      }
+    }
+    __syncthreads();
+    const int c_stop = s_nc;
+    for (int c = tid; c < c_stop; c += nt) my_rmem += S.sflag[c] ? 0 : 1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) my_rmem += __shfl_xor_sync(0xffffffffu, my_rmem, o);
+    if (tid == 0) {
+      s_refused_mem = 0;
+      s_nadm = gate ? min(tot_ok, cap) : 0;
+      s_refused_wcet = (!gate && n > 0 && cap > 0) ? 1 : 0;
+      s_nvic = 0;
+      s_ftop = st->free_top;
+      s_nswap = 0;
+      p.mb->n_swap_ev = 0;
+    }
+    __syncthreads();
+    if ((tid & 31) == 0 && my_rmem && gate) atomicAdd(&s_refused_mem, my_rmem);
+  } else if (tid == 0) {
     long long avail = (long long)st->free_top - s_outstanding;
     int havail = p.host_pages > 0 ? st->hfree_top : 0;
     int nadm = 0, rmem = 0, rwcet = 0, nvic = 0;
@@ -559,7 +757,10 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
     const int pre = (S.ck[x] == 0);
     p.slot_is_prefill[s] = pre;
     S.sflag[s] = pre ? 1 : (S.evc[x] ? 2 : 0);
-    if (pre) T.holder[task] = 1;
+    if (pre) {
+      T.holder[task] = 1;
+      atomicAdd(&s_npf, 1);
+    }
   }
   for (int s = tid; s < n_run; s += nt) {
     p.slot_is_prefill[s] = 0;
@@ -663,6 +864,8 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
   __syncthreads();
   PRE_MARK(7);
   // forward rows: prefill slot -> n_prompt rows, decode slot -> 1 row (AMB-13)
+  constexpr int NB = 1024;  // decode-row buckets (page counts), filled by the rows loop
+  for (int i = tid; i < NB; i += nt) S.ck[i] = 0;
   for (int s = tid; s < B; s += nt) {
     const int task = p.slot_task[s];
     S.cnt_a[s] = S.sflag[s] == 1 ? T.n_prompt[task] - p.page_tokens * T.n_pfx[task] : 1;
@@ -693,6 +896,10 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
         p.row_tok[off] = T.pending[task];
         p.slot_row[s] = off;
         T.ctx[task] = c + 1;
+        // bucket of the decode-row order below: longest context (most pages) first
+        const int kb = NB - 1 - min((c + 1 + p.page_tokens - 1) / p.page_tokens, NB - 1);
+        S.cR[s] = kb;
+        atomicAdd(&S.ck[kb], 1);
         l_ctx += (unsigned long long)(c + 1);
         l_attn += (unsigned long long)(c + 1);
         l_max = max(l_max, c + 1);
@@ -705,17 +912,17 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
       l_ctx += __shfl_xor_sync(0xffffffffu, l_ctx, o);
       l_max = max(l_max, __shfl_xor_sync(0xffffffffu, l_max, o));
     }
-    if ((tid & 31) == 0 && (l_prompt | l_attn | l_ctx)) {
-      atomicAdd(&s_sum_prompt, l_prompt);
-      atomicAdd(&s_attn_tok, l_attn);
-      atomicAdd(&s_sum_ctx, l_ctx);
-      atomicMax(&s_max_seqlen, l_max);
+    if ((tid & 31) == 0) {  // per-warp partials, summed by warp 0 in fixed order below
+      S.wb[tid >> 5] = (long long)l_prompt;
+      S.wr[tid >> 5] = (long long)l_attn;
+      S.wc[tid >> 5] = (long long)l_ctx;
+      S.ws[tid >> 5] = l_max;
     }
   }
   // prefill rows filled slot by slot, all threads in parallel; the prompt is cut into
   // 16-position attention tiles (page-aligned: the prompt starts at position 0)
   int n_pf_tiles = 0;
-  for (int s = n_run; s < B; ++s) {
+  for (int s = n_run; s < B && s_npf > 0; ++s) {  // (resume-only rounds skip the walk)
     if (S.sflag[s] != 1) continue;
     const int task = p.slot_task[s];
     const int off = S.cnt_a[s];
@@ -741,16 +948,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
   // page count (a bucket per page count, 1024 buckets); rows of one bucket in any order: each
   // row's attention is independent of when its CTA runs.
   {
-    constexpr int NB = 1024;
-    for (int i = tid; i < NB; i += nt) S.ck[i] = 0;
-    __syncthreads();
-    for (int s = tid; s < B; s += nt)  // same slot -> thread map as the rows loop (T.ctx)
-      if (S.sflag[s] != 1) {
-        const int kb = NB - 1 - min((T.ctx[p.slot_task[s]] + p.page_tokens - 1) / p.page_tokens, NB - 1);
-        S.cR[s] = kb;
-        atomicAdd(&S.ck[kb], 1);
-      }
-    __syncthreads();
+    __syncthreads();  // buckets counted by the rows loop
     const int ndec = block_scan_excl(S.ck, NB, wbuf);
     for (int s = tid; s < B; s += nt)
       if (S.sflag[s] != 1) p.dec_rows[atomicAdd(&S.ck[S.cR[s]], 1)] = S.cnt_a[s];
@@ -759,6 +957,27 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
   __syncthreads();
 
   PRE_MARK(8);
+  if (tid < 32) {  // the round sums: per-warp partials of the rows loop
+    const int nw = nt >> 5;
+    unsigned long long a = tid < nw ? (unsigned long long)S.wb[tid] : 0ull;
+    unsigned long long b = tid < nw ? (unsigned long long)S.wr[tid] : 0ull;
+    unsigned long long c = tid < nw ? (unsigned long long)S.wc[tid] : 0ull;
+    int m = tid < nw ? S.ws[tid] : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a += __shfl_xor_sync(0xffffffffu, a, o);
+      b += __shfl_xor_sync(0xffffffffu, b, o);
+      c += __shfl_xor_sync(0xffffffffu, c, o);
+      m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+    }
+    if (tid == 0) {
+      s_sum_prompt = a;
+      s_attn_tok = b;
+      s_sum_ctx = c;
+      s_max_seqlen = m;
+    }
+  }
+  __syncwarp();
   // ---- (5) round latency (VIRTUAL cost model, AMB-24) and plan publication
   if (tid == 0) {
     const long long sum_ctx = (long long)s_sum_ctx, sum_prompt = (long long)s_sum_prompt;
@@ -808,6 +1027,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
     mb->n_refused_wcet = s_refused_wcet;
     mb->attn_tokens = (long long)s_attn_tok;
     __threadfence_system();
+    publish_plan(st, mb);
   }
   PRE_MARK(9);
   if (threadIdx.x == 0) {
@@ -1022,7 +1242,6 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_post(SchedParams p) 
     HostMailbox* mb = p.mb;
     mb->n_stopped = n_stop;
     mb->seg_written = seg_base + n_stop;
-    mb->round_seq = mb->round_seq + 1;
     __threadfence_system();
   }
 }

@@ -95,8 +95,9 @@ def main():
     eng, now = profile_step.setup(a.agents, flags=rt.RT_FLAG_TRACE, workload=a.workload, gemm_path=a.gemm_path)
     eng.reset_stats()
     for _ in range(a.steps):
-        eng.step(now())
+        info = eng.step(now())
     eng.sync()
+    print("last round:", {k: info[k] for k in ("n_running", "n_waiting", "n_admitted", "n_refused_mem", "n_refused_wcet")})
     tr = eng.trace()
     if a.raw:
         np.save(a.raw, tr)
