@@ -82,21 +82,142 @@ __global__ void __launch_bounds__(kAttnWarps * 32) k_attn(AttnArgs a) {
   __syncwarp();
   pdl_wait();
   tr.ready();
+  // QKV folded in (a.part): this CTA's chunk holding the row's last page appends this round's
+  // K / V into it, so that page is loaded only after the append (deferred below)
+  const bool fold = a.part != nullptr;
+  const int last_pg = n_pages - 1;
+  const bool appends = fold && chunk == n_chunks - 1;
   // page ids of the first 32 pages of this warp, one per lane
   int my_page = (lane < n_my) ? ptab[p_begin + warp + lane * kAttnWarps] : 0;
+  int deferred = -1;  // stage of this warp whose (last) page waits for the append
 #pragma unroll
   for (int i = 0; i < C::STAGES; ++i) {
     const int pg = __shfl_sync(0xffffffffu, my_page, i);
+    if (i < n_my && appends && p_begin + warp + i * kAttnWarps == last_pg) {
+      deferred = i;
+      continue;
+    }
     if (lane == 0 && i < n_my) {
       mbar_arrive_expect_tx(&bar[i], C::BLOCK);
       bulk_g2s_hint(ring + i * C::BLOCK, pool + (size_t)pg * page_stride + head_off, C::BLOCK, &bar[i], pol);
+    }
+  }
+  __shared__ __align__(16) bf16 s_q[8 * HD];  // folded q (G <= 8 heads) of this kv head
+  if (fold) {
+    // ---- QKV epilogue of this (row, kv head): sum the projection's split-K partials in split
+    // order, RMSNorm row scale, RoPE (rotate-half; weight rows 2i, 2i + 1 = dims i, i + hd/2),
+    // bf16 q -> shared memory (+ q_out / q_cap), bf16 k / v -> the page (swizzled rows)
+    // RMSNorm row scale: every thread sums the row's per-tile sums of squares itself, in tile
+    // order; its loads are issued together with the first group's partial loads below (one
+    // L2 round trip for both), no barrier
+    constexpr int kRsMax = 64;   // per-row tiles held in registers (d_model <= 8192)
+    const float* rs = a.rs_ss + (size_t)r * a.rs_tiles;
+    const bool rs_vec = (a.rs_tiles & 3) == 0 && a.rs_tiles <= kRsMax && ((uintptr_t)rs & 15) == 0;
+    float4 rs4[kRsMax / 4];
+#pragma unroll
+    for (int i = 0; i < kRsMax / 4; ++i)
+      rs4[i] = (rs_vec && 4 * i < a.rs_tiles) ? __ldcg(reinterpret_cast<const float4*>(rs) + i)
+                                              : make_float4(0.f, 0.f, 0.f, 0.f);
+    float inv = 0.f;
+    bool have_inv = false;
+    constexpr int HALF = HD / 2;
+    constexpr int kMaxSplits = 8;  // gemm_qkvpart_splits <= 8 (cluster / pair split-K choices)
+    constexpr int PB = 3;          // pairs per thread per round trip
+    const int pos = seqlen - 1;
+    const int pg_last = ptab[pos >> 4], off = pos & 15;
+    const int n_pairs = (G + 2) * HALF;
+    const int S = a.part_splits;
+    const size_t split_stride = (size_t)a.part_ld_n * a.part_m;
+    for (int j0 = threadIdx.x; j0 < n_pairs; j0 += PB * blockDim.x) {
+      // all the split partials (and the rotations) of PB pairs in flight at once
+      float2 w[PB][kMaxSplits];
+      float cr[PB], sr[PB];
+#pragma unroll
+      for (int u = 0; u < PB; ++u) {
+        const int j = j0 + u * (int)blockDim.x;
+        const bool ok = j < n_pairs;
+        const int hl = j / HALF, i = j - hl * HALF;  // local head: q 0..G-1, then k, v
+        const int head = hl < G ? h * G + hl : (hl == G ? a.nq + h : a.nq + a.nkv + h);
+        const float* src = a.part + (size_t)r * a.part_m + (size_t)head * HD + 2 * i;
+#pragma unroll
+        for (int sp = 0; sp < kMaxSplits; ++sp)
+          w[u][sp] = (ok && sp < S) ? __ldcg(reinterpret_cast<const float2*>(src + sp * split_stride))
+                                    : make_float2(0.f, 0.f);
+        const bool rot = ok && hl <= G;  // q and k heads are rotated
+        cr[u] = rot ? __ldg(a.cos + (size_t)pos * HALF + i) : 1.f;
+        sr[u] = rot ? __ldg(a.sin + (size_t)pos * HALF + i) : 0.f;
+      }
+      if (!have_inv) {
+        float t = 0.f;
+        if (rs_vec) {
+#pragma unroll
+          for (int i = 0; i < kRsMax / 4; ++i)
+            if (4 * i < a.rs_tiles) t = (((t + rs4[i].x) + rs4[i].y) + rs4[i].z) + rs4[i].w;
+        } else {
+          for (int i = 0; i < a.rs_tiles; ++i) t += __ldcg(rs + i);
+        }
+        inv = rsqrtf(t / (float)a.d_model + 1e-5f);
+        have_inv = true;
+      }
+#pragma unroll
+      for (int u = 0; u < PB; ++u) {
+        const int j = j0 + u * (int)blockDim.x;
+        if (j >= n_pairs) break;
+        const int hl = j / HALF, i = j - hl * HALF;
+        const int head = hl < G ? h * G + hl : (hl == G ? a.nq + h : a.nq + a.nkv + h);
+        float v0 = 0.f, v1 = 0.f;  // the sum in split order
+#pragma unroll
+        for (int sp = 0; sp < kMaxSplits; ++sp)
+          if (sp < S) {
+            v0 += w[u][sp].x;
+            v1 += w[u][sp].y;
+          }
+        v0 *= inv;
+        v1 *= inv;
+        float y0 = v0, y1 = v1;
+        if (hl <= G) {
+          y0 = v0 * cr[u] - v1 * sr[u];
+          y1 = v1 * cr[u] + v0 * sr[u];
+        }
+        const bf16 b0 = __float2bfloat16_rn(y0), b1 = __float2bfloat16_rn(y1);
+        if (hl < G) {
+          s_q[hl * HD + i] = b0;
+          s_q[hl * HD + i + HALF] = b1;
+          if (chunk == 0) {
+            bf16* qo = a.q_out + ((size_t)r * a.nq + head) * HD;
+            qo[i] = b0;
+            qo[i + HALF] = b1;
+            if (a.q_cap) {
+              float* qc = a.q_cap + ((size_t)row * a.nq + head) * HD;
+              qc[i] = __bfloat162float(b0);
+              qc[i + HALF] = __bfloat162float(b1);
+            }
+          }
+        } else if (appends) {
+          const int kind = hl - G;  // 0: K, 1: V
+          unsigned char* pb = (unsigned char*)a.pool +
+                              (((size_t)pg_last * a.nkv + h) * 2 + kind) * (size_t)(16 * HD * 2) + off * HD * 2;
+          *(bf16*)(pb + (kv_swz_chunk(HD, off, i >> 3) << 4) + ((i & 7) << 1)) = b0;
+          *(bf16*)(pb + (kv_swz_chunk(HD, off, (i + HALF) >> 3) << 4) + (((i + HALF) & 7) << 1)) = b1;
+        }
+      }
+    }
+    fence_proxy_async_global();  // the appended K / V rows are read by the bulk copies below
+    __syncthreads();
+    if (deferred >= 0) {  // (warp-uniform)
+      const int pg = __shfl_sync(0xffffffffu, my_page, deferred);
+      if (lane == 0) {
+        mbar_arrive_expect_tx(&bar[deferred], C::BLOCK);
+        bulk_g2s_hint(ring + deferred * C::BLOCK, pool + (size_t)pg * page_stride + head_off, C::BLOCK,
+                      &bar[deferred], pol);
+      }
     }
   }
 
   // q fragments (A operand of S^T = Q K^T), rows g >= G are zero
   uint32_t qa[HD / 16][2];
   {
-    const bf16* qrow = a.q + ((size_t)r * a.nq + (size_t)h * G) * HD;
+    const bf16* qrow = fold ? s_q : a.q + ((size_t)r * a.nq + (size_t)h * G) * HD;
 #pragma unroll
     for (int ks = 0; ks < HD / 16; ++ks) {
       if (gq < G) {

@@ -99,6 +99,8 @@ struct rt_engine {
   int32_t* d_am_idx = nullptr;
   bf16 *d_h = nullptr, *d_q = nullptr, *d_o = nullptr, *d_act = nullptr, *d_hfin = nullptr;
   float *d_cap_q = nullptr, *d_cap_o = nullptr, *d_rope_cos = nullptr, *d_rope_sin = nullptr;
+  float* d_qkv_part = nullptr;   // decode QKV split-K partials folded into the attention
+  int qkv_part_rows = 0;         // decode rows the fold serves (its partials are sized for)
   // RT_FLAG_CAPTURE_LAYERS: per-layer intermediates of the last round's first forward chunk
   float *d_lc_x = nullptr, *d_lc_xmid = nullptr;   // [L + 1][fwd_rows][d], [L][fwd_rows][d]
   bf16 *d_lc_q = nullptr, *d_lc_o = nullptr, *d_lc_act = nullptr;  // [L][fwd_rows][...]
@@ -510,6 +512,15 @@ static rt_status create_impl(rt_engine* e, const rt_config* cfg) {
     if (!ok) return done(fail(e, RT_E_CUDA, "cuTensorMapEncodeTiled failed (activations)"));
     e->ev_attn.resize(2 * L);
     for (auto& ev : e->ev_attn) cudaEventCreate(&ev);
+    // decode QKV folded into the attention (EPI_QKVPART): raw split-K partials of up to
+    // min(max_batch, 256, fwd_rows) decode rows
+    {
+      e->qkv_part_rows = std::min(std::min(c.max_batch, 256), R);
+      int smax = 0;
+      for (int n = 1; n <= e->qkv_part_rows; ++n) smax = std::max(smax, gemm_qkvpart_splits(e->qkv_dim, d, n));
+      if (smax > 0 && hd % 16 == 0 && nq / nkv <= 8)
+        CK(e, dalloc(e, &e->d_qkv_part, (size_t)smax * e->qkv_part_rows * e->qkv_dim));
+    }
     // decode-pair split-K exchange workspace (k_gemm_dec), sized for the model's projections
     {
       const int shapes[4][2] = {{e->qkv_dim, d}, {d, nq * hd}, {2 * ff, d}, {d, ff}};
@@ -772,6 +783,9 @@ static void harvest_timing(rt_engine* e) {
 // ------------------------------------------------------------------ forward
 static void record_timing_event(cudaEvent_t ev, cudaStream_t s) { cudaEventRecord(ev, s); }
 
+#ifndef RT_QKV_FOLD
+#define RT_QKV_FOLD 1
+#endif
 static rt_status forward(rt_engine* e, const HostMailbox& plan) {
   const rt_config& c = e->cfg;
   const int d = c.d_model, hd = c.head_dim, nq = c.n_q_heads, nkv = c.n_kv_heads, ff = c.d_ff, V = c.vocab;
@@ -838,6 +852,26 @@ static rt_status forward(rt_engine* e, const HostMailbox& plan) {
     pa.out = e->d_o;
     pa.scale_log2 = sl2;
     const bool any_decode = plan.n_rows > plan.n_prefill_rows;
+    // decode-only rounds: the QKV projection writes its raw split-K partials and the decode
+    // attention runs the QKV epilogue (sum, RMSNorm scale, RoPE, KV append) for its own (row,
+    // kv head) — no split-K exchange or fused epilogue on the projection's critical path
+    int fold_S = (RT_QKV_FOLD && e->d_qkv_part && c.gemm_path == GEMM_PATH_AUTO &&
+                  plan.n_prefill_rows == 0 && n_rows <= e->fwd_rows && n <= e->qkv_part_rows)
+                     ? gemm_qkvpart_splits(e->qkv_dim, d, n)
+                     : 0;
+    if (fold_S > 8 || d / 128 > 64) fold_S = 0;  // the attention's fold holds <= 8 partials, <= 64 tiles
+    if (fold_S > 0) {
+      aa.part = e->d_qkv_part;
+      aa.part_splits = fold_S;
+      aa.part_ld_n = n;
+      aa.part_m = e->qkv_dim;
+      aa.rs_ss = e->d_ss;
+      aa.rs_tiles = d_tiles;
+      aa.d_model = d;
+      aa.cos = e->d_rope_cos;
+      aa.sin = e->d_rope_sin;
+      aa.q_out = e->d_q;
+    }
     auto gemm = [&](const bf16* w, const GemmTmaSet& x, int M, int K, GemmArgs g) {
       g.M = M;
       g.N = n;
@@ -908,10 +942,16 @@ static rt_status forward(rt_engine* e, const HostMailbox& plan) {
       lc_copy(e->d_lc_x, e->d_x, l, (size_t)d * 4, row0);
       {
         GemmArgs g = args_qkv(l);
+        if (fold_S > 0) {
+          g.mode = EPI_QKVPART;
+          g.part = e->d_qkv_part;
+          g.part_ld_n = n;
+          g.rs_ss = nullptr;  // the row scale is applied by the attention
+        }
         gemm(w.qkv, e->x_h, e->qkv_dim, d, g);
       }
-      lc_copy(e->d_lc_q, e->d_q, l, (size_t)nq * hd * 2, row0);
       aa.pool = pool_l;
+      aa.q_cap = (fold_S > 0 && e->d_cap_q && l == c.capture_layer) ? e->d_cap_q : nullptr;
       aa.out_f32 = (e->d_cap_o && l == c.capture_layer) ? e->d_cap_o : nullptr;
       if (timing && row0 == 0) record_timing_event(e->ev_attn[2 * l], s);
       if (any_decode) {
@@ -925,6 +965,7 @@ static rt_status forward(rt_engine* e, const HostMailbox& plan) {
         launch_attention_prefill(pa, s);
         ++launches;
       }
+      lc_copy(e->d_lc_q, e->d_q, l, (size_t)nq * hd * 2, row0);  // (after the attention: q of a fold)
       lc_copy(e->d_lc_o, e->d_o, l, (size_t)nq * hd * 2, row0);
       {  // O projection + residual
         GemmArgs g = args_resid(d, nq * hd);

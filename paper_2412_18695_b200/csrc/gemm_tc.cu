@@ -658,7 +658,10 @@ __global__ void __launch_bounds__(kGemmThreads, GemmCfg<BN>::CTAS_PER_SM)
   // EPI_QKV: dependents (the decode attention) may launch only once this kernel has passed
   // its own dependency wait — the attention reads the round's row metadata before its wait,
   // which is safe only if every kernel before it has completed (PDL)
-  if (MODE != EPI_QKV && threadIdx.x == 0) pdl_trigger();
+  constexpr bool QKV_LIKE = MODE == EPI_QKV || MODE == EPI_QKVPART;
+  // EPI_QKVPART: no split-K exchange at all — every split writes its raw partial
+  constexpr bool PART = MODE == EPI_QKVPART;
+  if (!QKV_LIKE && threadIdx.x == 0) pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -673,7 +676,7 @@ __global__ void __launch_bounds__(kGemmThreads, GemmCfg<BN>::CTAS_PER_SM)
         bulk_g2s_hint(sA + i * C::A_BYTES, wt + (size_t)i * (128 * kBK), C::A_BYTES, &full[i], pol);
       }
       pdl_wait();
-      if (MODE == EPI_QKV) pdl_trigger();
+      if (QKV_LIKE) pdl_trigger();
       tr.ready();
       for (int i = 0; i < pre_k; ++i)
         tma_load_2d(sB + i * C::B_BYTES, &tmB, (kb0 + i) * kBK, n0, &full[i]);
@@ -721,33 +724,45 @@ __global__ void __launch_bounds__(kGemmThreads, GemmCfg<BN>::CTAS_PER_SM)
 #pragma unroll
       for (int i = 0; i < 9; ++i) s_mark[i] = t;
     }
+    if constexpr (PART) {  // raw partial of split `rank` -> part[rank][n][m] (coalesced over m)
+      const int m = m_tile * 128 + et;
+      float* dst = g.part + ((size_t)rank * g.part_ld_n + n0) * g.M + m;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN && n0 + c0 < g.N; c0 += 16) {
+        float v[16];
+        tmem_ld16(tb + c0, v);
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (m < g.M && n0 + c0 + j < g.N) __stcg(dst + (size_t)(c0 + j) * g.M, v[j]);
+      }
+    }
     // split-K push: arrive on the cluster barrier as soon as this CTA's MMAs are done (its
     // ring may then receive the peers' slices) and park the accumulator while the slower
     // CTAs finish; the park writes P, the peers write the receive slots R (disjoint).  Pull
     // (the peers READ P over DSMEM after the barrier): arrive only once P is parked — an
     // early arrive there let a peer read a half-written P (intermittent wrong sums, found by
     // a run-to-run determinism check, tools/determinism_check.py)
-    if (S > 1 && push) cluster_arrive();
+    if (!PART && S > 1 && push) cluster_arrive();
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 16) {  // park the accumulator in shared memory
+    for (int c0 = 0; c0 < (PART ? 0 : BN); c0 += 16) {  // park the accumulator in shared memory
       float v[16];
       tmem_ld16(tb + c0, v);
 #pragma unroll
       for (int j = 0; j < 16; ++j) P[(c0 + j) * 128 + et] = v[j];
     }
     if (push) fence_proxy_async();  // P is read by the bulk-copy (async) proxy
-    if (S > 1 && !push) cluster_arrive();
+    if (!PART && S > 1 && !push) cluster_arrive();
     EPI_MARK(1);
-    if (S > 1) cluster_wait();
+    if (!PART && S > 1) cluster_wait();
   }
   // ---- cluster split-K: CTA `rank` finishes columns [cb, ce) of the tile.  The barrier
   // also certifies that every CTA's mainloop is over (its ring is free for the slices).
-  if (S > 1 && warp < 2) {  // (the epilogue warps arrived / waited above)
+  if (!PART && S > 1 && warp < 2) {  // (the epilogue warps arrived / waited above)
     __syncwarp();
     cluster_arrive();
     cluster_wait();
   }
-  if (warp >= 2) {
+  if (!PART && warp >= 2) {
     const int et = (warp & 3) * 32 + lane;
     EPI_MARK(2);
     if (S > 1 && push) {
@@ -773,7 +788,7 @@ __global__ void __launch_bounds__(kGemmThreads, GemmCfg<BN>::CTAS_PER_SM)
     if (push && et == 0) asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
     EPI_MARK(8);
   }
-  if (S > 1 && !push) {  // keep shared memory alive until every CTA has read it
+  if (!PART && S > 1 && !push) {  // keep shared memory alive until every CTA has read it
     __syncwarp();
     cluster_arrive();
     cluster_wait();
@@ -1633,7 +1648,9 @@ __global__ void __launch_bounds__(kDecThreads, 1)
   cluster_wait();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  if (MODE != EPI_QKV && threadIdx.x == 0) pdl_trigger();
+  constexpr bool QKV_LIKE = MODE == EPI_QKV || MODE == EPI_QKVPART;
+  constexpr bool PART = MODE == EPI_QKVPART;  // raw partials, no split-K exchange
+  if (!QKV_LIKE && threadIdx.x == 0) pdl_trigger();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -1646,7 +1663,7 @@ __global__ void __launch_bounds__(kDecThreads, 1)
         tma_load_2d_pair(sA + i * C::A_BYTES, &tmA, 0, (m_tile * kbt + kb0 + i) * 128, full0 + i * 8);
       }
       pdl_wait();
-      if (MODE == EPI_QKV) pdl_trigger();
+      if (QKV_LIKE) pdl_trigger();
       tr.ready();
       for (int i = 0; i < pre_k; ++i)
         tma_load_2d_pair(sB + i * C::B_BYTES, &tmB, (kb0 + i) * kBK, h * C::HB, full0 + i * 8);
@@ -1715,6 +1732,19 @@ __global__ void __launch_bounds__(kDecThreads, 1)
 #pragma unroll
       for (int i = 0; i < 9; ++i) s_mark[i] = c0;
     }
+    if constexpr (PART) {  // raw partial of split p -> part[p][n][m]; group g: columns [g BN/2, ..)
+      const int m = m_tile * 128 + et;
+      float* dst = g.part + (size_t)p * g.part_ld_n * g.M + m;
+      const int c_hi = min((grp + 1) * (BN / 2), g.N);
+#pragma unroll 1
+      for (int c0 = grp * (BN / 2); c0 < c_hi; c0 += 16) {
+        float v[16];
+        tmem_ld16(tb + (uint32_t)c0, v);
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (c0 + j < c_hi) __stcg(dst + (size_t)(c0 + j) * g.M, v[j]);
+      }
+    } else {
     // the ring is free: the epilogue inputs -> shared memory (bulk copies on pf_bar, one column
     // per thread: issued serially by one thread they took ~10 us for 96 columns), in flight
     // while the split-K exchange runs.  (complete_tx may precede the expect_tx of the phase.)
@@ -1804,6 +1834,7 @@ __global__ void __launch_bounds__(kDecThreads, 1)
     if (gs.stg) gs.stg = sm.stg + grp * (2 * kEpiCh * 128);
     const TileSrc ts{T - (size_t)cb * 128, nullptr, 0u, 1, 0, BN, 0, 0};
     if (gcb < gce) epilogue<MODE>(g, gs, ts, m_tile, 0, gcb, gce, et, true);
+    }  // !PART
     EPI_MARK(8);
   }
   tc_fence_before();
@@ -2090,6 +2121,7 @@ static cudaError_t launch_2sm_bn(const TmaMap& am, const TmaMap& bm, const TmaMa
 template <int MODE>
 static cudaError_t launch_2sm_mode(const TmaMap& am, const GemmTmaSet& x, const GemmArgs& g, int bn, int PT,
                                    const SkArgs& a, cudaStream_t s) {
+  if (bn == 128) return launch_2sm_bn<128, MODE>(am, x.m64, x.m32, g, PT, a, s);
   if (bn == 160) return launch_2sm_bn<160, MODE>(am, x.m80, x.m32, g, PT, a, s);
   if (bn == 192) return launch_2sm_bn<192, MODE>(am, x.m96, x.m32, g, PT, a, s);
   return launch_2sm_bn<256, MODE>(am, x.m128, x.m32, g, PT, a, s);
@@ -2179,16 +2211,19 @@ int64_t gemm_dec_ws_floats(int M, int N, int K) {
   return S < 2 ? 0 : (int64_t)PT * 2 * S * S * dec::dec_slot(bn, S) * 128;
 }
 // launch the decode pair kernel if it applies (returns cudaErrorNotSupported otherwise)
-static cudaError_t try_launch_dec(const bf16* w_tiled, const GemmTmaSet& x, GemmArgs g, cudaStream_t s) {
+static cudaError_t try_launch_dec(const bf16* w_tiled, const GemmTmaSet& x, GemmArgs g, int force_s,
+                                  cudaStream_t s) {
   const int m_tiles = (g.M + 127) / 128;
-  if (!g.dec_ws || !g.dec_flags) return cudaErrorNotSupported;
+  const bool part = g.mode == EPI_QKVPART;  // no exchange: no workspace / flags needed
+  if (!part && (!g.dec_ws || !g.dec_flags)) return cudaErrorNotSupported;
   if (g.N > 256 || g.N < 1 || g.M % 256 || g.K % kBK || g.mode == EPI_ARGMAX) return cudaErrorNotSupported;
   const int bn = g.N <= 64 ? 64 : (g.N <= 128 ? 128 : 256);
   const int PT = m_tiles / 2;
   const int kbt = g.K / kBK;
-  const int S = dec_splits(PT, kbt, bn);
+  int S = dec_splits(PT, kbt, bn);
+  if (force_s >= 2 && force_s <= S) S = force_s;  // op-level override (tools / tests): fewer splits
   if (S < 2) return cudaErrorNotSupported;
-  if ((int64_t)PT * 2 * S * S * dec::dec_slot(bn, S) * 128 > g.dec_ws_floats || PT * 2 * S > g.dec_flags_cap)
+  if (!part && ((int64_t)PT * 2 * S * S * dec::dec_slot(bn, S) * 128 > g.dec_ws_floats || PT * 2 * S > g.dec_flags_cap))
     return cudaErrorNotSupported;
   const TmaMap* am = weight_map(w_tiled, (uint64_t)m_tiles * kbt * 128);
   if (!am) return cudaErrorNotSupported;
@@ -2202,17 +2237,40 @@ static cudaError_t try_launch_dec(const bf16* w_tiled, const GemmTmaSet& x, Gemm
     case EPI_QKV: return launch_dec_mode<EPI_QKV>(*am, x, g, bn, PT, S, s);
     case EPI_RESID: return launch_dec_mode<EPI_RESID>(*am, x, g, bn, PT, S, s);
     case EPI_SWIGLU: return launch_dec_mode<EPI_SWIGLU>(*am, x, g, bn, PT, S, s);
+    case EPI_QKVPART: return launch_dec_mode<EPI_QKVPART>(*am, x, g, bn, PT, S, s);
     default: return cudaErrorNotSupported;
   }
 }
 
 int64_t gemm_sk_ws_floats() { return (int64_t)sm_count() * 2 * 256 * 128; }
 
+// Split count of the decode QKV projection in EPI_QKVPART (QKV folded into the attention):
+// the decode pair kernel's at 129..256 rows, the cluster split-K kernel's at <= 128 rows;
+// 0 = not supported at this shape (the caller keeps EPI_QKV).  launch_gemm_epi runs exactly
+// this choice, so the attention knows how many partials to sum.
+int gemm_qkvpart_splits(int M, int K, int N) {
+  if (N < 1 || N > 256 || K % kBK) return 0;
+  if (N > 128) {
+    if (M % 256) return 0;
+    const int S = dec_splits(M / 256, K / kBK, 256);
+    return S >= 2 ? S : 0;
+  }
+  return std::max(1, std::min(gemm_choose_splits(M, N, K), std::min(16, K / kBK)));
+}
+
 cudaError_t launch_gemm_epi(const bf16* w_tiled, const GemmTmaSet& x, GemmArgs g, int splits, cudaStream_t s) {
+  if (g.mode == EPI_QKVPART) {  // only the two decode kernels write raw partials
+    const int S = gemm_qkvpart_splits(g.M, g.K, g.N);
+    if (S == 0 || !g.part) return cudaErrorInvalidValue;
+    if (g.N > 128) return try_launch_dec(w_tiled, x, g, 0, s);
+    g.force_path = GEMM_PATH_SPLITK;
+    g.force_bn = 0;
+    splits = S;
+  }
   // decode rows on the few-tile projections (<= 256 rows, 129..256 by default): CTA pairs with
   // a cluster split-K (k_gemm_dec)
   if (g.force_path == GEMM_PATH_DEC || (g.force_path == GEMM_PATH_AUTO && g.N > 128 && g.N <= 256)) {
-    const cudaError_t r = try_launch_dec(w_tiled, x, g, s);
+    const cudaError_t r = try_launch_dec(w_tiled, x, g, g.force_path == GEMM_PATH_DEC ? splits : 0, s);
     if (r != cudaErrorNotSupported) return r;
   }
   const GemmChoice gc = gemm_choice(g.M, g.K, g.N, g.force_bn, g.force_path);
@@ -2297,6 +2355,7 @@ cudaError_t launch_gemm_epi(const bf16* w_tiled, const GemmTmaSet& x, GemmArgs g
       case EPI_QKV: return launch_mode<EPI_QKV>(x, g, bn, S, s);
       case EPI_RESID: return launch_mode<EPI_RESID>(x, g, bn, S, s);
       case EPI_SWIGLU: return launch_mode<EPI_SWIGLU>(x, g, bn, S, s);
+      case EPI_QKVPART: return launch_mode<EPI_QKVPART>(x, g, bn, S, s);
       default: return cudaErrorInvalidValue;
     }
   };

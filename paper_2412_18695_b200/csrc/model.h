@@ -55,6 +55,19 @@ struct AttnArgs {
                              // outside [row0, row0 + chunk_rows) are skipped); n_rows = list size
   int chunk_rows;
   int l2_evict_first;        // set by launch_attention: K/V pages are read once per step
+  // QKV folded into the decode attention (nullable part): the projection's split-K partials
+  // part[s][r][m] (s < part_splits, r < part_ld_n rows, m < part_m = (nq + 2 nkv) hd in the
+  // weights' physical row order: within a head rows 2i, 2i + 1 = dims i, i + hd/2), summed in
+  // split order, scaled by the row's RMSNorm rsqrt(sum_t rs_ss[r][t] / d_model + 1e-5), RoPE
+  // on q and k (cos / sin [pos][hd/2]); bf16 q -> q_out (and fp32 -> q_cap[row0 + r], nullable),
+  // bf16 k / v appended into the row's page at its position (the pool above, writable)
+  const float* part;
+  int part_splits, part_ld_n, part_m;
+  const float* rs_ss;
+  int rs_tiles, d_model;
+  const float *cos, *sin;
+  bf16* q_out;
+  float* q_cap;
 };
 int64_t attn_ws_floats(int n_rows, int nq, int hd, int max_chunks);
 void attn_plan(int n_rows, int nkv, int max_seqlen, int* chunk_pages, int* max_chunks);
@@ -91,7 +104,7 @@ struct GemmTmaSet {       // activation operand: one map per supported N tile
 };
 bool make_gemm_act_maps(GemmTmaSet* out, const void* base, int K, int rows_cap);
 
-enum EpiMode { EPI_STORE = 0, EPI_ARGMAX = 1, EPI_QKV = 2, EPI_RESID = 3, EPI_SWIGLU = 4 };
+enum EpiMode { EPI_STORE = 0, EPI_ARGMAX = 1, EPI_QKV = 2, EPI_RESID = 3, EPI_SWIGLU = 4, EPI_QKVPART = 5 };
 // projection kernel paths (GemmArgs::force_path; the values of rt.h RT_GEMM_PATH_*):
 // AUTO = measured dispatch; SPLITK = k_gemm_tc (cluster split-K / one tile per CTA);
 // STREAMK = k_gemm_sk (hybrid data-parallel + stream-K, N > 128); PAIR = k_gemm_2sm (CTA pairs, N > 128)
@@ -124,6 +137,11 @@ struct GemmArgs {
   int ff;
   QkvFuse qkv;        // EPI_QKV
   int l2_evict_first;  // set by launch_gemm_epi: weight tiles are read once per step
+  // EPI_QKVPART (decode QKV folded into the attention): split s of the cluster / pair
+  // split-K writes its raw fp32 partial to part[s][n][m] (rows n < N, ld_n rows per split);
+  // the attention kernel sums the splits, applies the RMSNorm scale and RoPE, appends K/V
+  float* part;
+  int part_ld_n;
   // set by launch_gemm_epi: CTA (x, y) runs linear tile tile0 + y of the GEMM's m_tiles x
   // n_tiles tiles (n fastest: the n-tiles of one m-tile are adjacent and the later ones read
   // the weight tile from L2); tile_count tiles in this launch
@@ -151,6 +169,7 @@ constexpr int kDecFlags = 512;  // epoch flags of the k_gemm_dec exchange (pair-
 int64_t gemm_sk_ws_floats();
 int gemm_bn(int M, int K, int N);
 int gemm_choose_splits(int M, int N, int K);   // cluster split-K factor (1..16)
+int gemm_qkvpart_splits(int M, int K, int N);  // EPI_QKVPART partial count (0: unsupported)
 // splits <= 0: gemm_choose_splits
 cudaError_t launch_gemm_epi(const bf16* w_tiled, const GemmTmaSet& xmaps, GemmArgs g, int splits, cudaStream_t s);
 

@@ -153,7 +153,7 @@ extern "C" rt_status rt_op_gemm_tiled(const void* d_w_tiled, const void* d_x, fl
   if (M < 1 || N < 1 || K < 64 || K % 64 || n_cap < N || splits < 0 || splits > K / 64) return RT_E_INVAL;
   if (path < RT_GEMM_PATH_AUTO || path > RT_GEMM_PATH_DECPAIR) return RT_E_INVAL;
   if (bn != 0 && bn != 32 && bn != 64 && bn != 128 && bn != 160 && bn != 192 && bn != 256) return RT_E_INVAL;
-  if (bn != 0 && bn <= 128 && N > 128) return RT_E_INVAL;
+  if (bn != 0 && bn <= 128 && N > 128 && !(bn == 128 && path == RT_GEMM_PATH_PAIR)) return RT_E_INVAL;
   GemmTmaSet xm;
   if (!make_gemm_act_maps(&xm, d_x, K, n_cap)) return RT_E_CUDA;
   GemmArgs g{};
