@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32) k_attn(AttnArgs a) {
     float inv = 0.f;
     bool have_inv = false;
     constexpr int HALF = HD / 2;
-    constexpr int kMaxSplits = 8;  // gemm_qkvpart_splits <= 8 (cluster / pair split-K choices)
+    constexpr int kMaxSplits = 8;  // gemm_part_splits <= 8 (cluster / pair split-K choices)
     constexpr int PB = 3;          // pairs per thread per round trip
     const int pos = seqlen - 1;
     const int pg_last = ptab[pos >> 4], off = pos & 15;

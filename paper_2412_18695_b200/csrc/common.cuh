@@ -88,7 +88,7 @@ static __device__ TraceBuf g_trace;  // per translation unit, bound by trace_bin
 
 enum TraceKind : uint32_t {
   TK_GEMM = 1, TK_ATTN = 2, TK_NORM = 3, TK_EMBED = 4, TK_SCHED_PRE = 5, TK_SCHED_POST = 6,
-  TK_GATHER = 7, TK_ARGMAX = 8, TK_MERGE = 9, TK_ATTN_PREFILL = 10, TK_PHASE = 0x80
+  TK_GATHER = 7, TK_ARGMAX = 8, TK_MERGE = 9, TK_ATTN_PREFILL = 10, TK_RESID = 11, TK_PHASE = 0x80
 };
 
 RT_DEV unsigned long long gtimer() {

@@ -512,14 +512,16 @@ static rt_status create_impl(rt_engine* e, const rt_config* cfg) {
     if (!ok) return done(fail(e, RT_E_CUDA, "cuTensorMapEncodeTiled failed (activations)"));
     e->ev_attn.resize(2 * L);
     for (auto& ev : e->ev_attn) cudaEventCreate(&ev);
-    // decode QKV folded into the attention (EPI_QKVPART): raw split-K partials of up to
+    // decode QKV folded into the attention (EPI_PART): raw split-K partials of up to
     // min(max_batch, 256, fwd_rows) decode rows
     {
       e->qkv_part_rows = std::min(std::min(c.max_batch, 256), R);
-      int smax = 0;
-      for (int n = 1; n <= e->qkv_part_rows; ++n) smax = std::max(smax, gemm_qkvpart_splits(e->qkv_dim, d, n));
-      if (smax > 0 && hd % 16 == 0 && nq / nkv <= 8)
-        CK(e, dalloc(e, &e->d_qkv_part, (size_t)smax * e->qkv_part_rows * e->qkv_dim));
+      int64_t need = 0;  // the QKV, O and down projections' partials share one buffer
+      const int shapes[3][2] = {{e->qkv_dim, d}, {d, nq * hd}, {d, ff}};
+      for (int n = 1; n <= e->qkv_part_rows; ++n)
+        for (auto& sh : shapes) need = std::max(need, (int64_t)gemm_part_splits(sh[0], sh[1], n) * sh[0]);
+      if (need > 0 && hd % 16 == 0 && nq / nkv <= 8)
+        CK(e, dalloc(e, &e->d_qkv_part, (size_t)need * e->qkv_part_rows));
     }
     // decode-pair split-K exchange workspace (k_gemm_dec), sized for the model's projections
     {
@@ -786,6 +788,9 @@ static void record_timing_event(cudaEvent_t ev, cudaStream_t s) { cudaEventRecor
 #ifndef RT_QKV_FOLD
 #define RT_QKV_FOLD 1
 #endif
+#ifndef RT_RESID_PART
+#define RT_RESID_PART 1
+#endif
 static rt_status forward(rt_engine* e, const HostMailbox& plan) {
   const rt_config& c = e->cfg;
   const int d = c.d_model, hd = c.head_dim, nq = c.n_q_heads, nkv = c.n_kv_heads, ff = c.d_ff, V = c.vocab;
@@ -857,9 +862,18 @@ static rt_status forward(rt_engine* e, const HostMailbox& plan) {
     // kv head) — no split-K exchange or fused epilogue on the projection's critical path
     int fold_S = (RT_QKV_FOLD && e->d_qkv_part && c.gemm_path == GEMM_PATH_AUTO &&
                   plan.n_prefill_rows == 0 && n_rows <= e->fwd_rows && n <= e->qkv_part_rows)
-                     ? gemm_qkvpart_splits(e->qkv_dim, d, n)
+                     ? gemm_part_splits(e->qkv_dim, d, n)
                      : 0;
     if (fold_S > 8 || d / 128 > 64) fold_S = 0;  // the attention's fold holds <= 8 partials, <= 64 tiles
+    // ... and the O / down projections write theirs too, finished by k_resid_reduce (residual
+    // add, bf16 copy, RMSNorm sums) instead of a split-K exchange inside the GEMM
+    auto part_s = [&](int M, int K) {
+      // (at <= 128 rows the single-SM kernel's in-cluster DSMEM exchange is cheaper than the
+      // extra reduce launch: measured equal or slower at C2)
+      const int S = (RT_RESID_PART && fold_S > 0 && n > 128) ? gemm_part_splits(M, K, n) : 0;
+      return (S > 0 && S <= 8 && M % 128 == 0) ? S : 0;
+    };
+    const int o_S = part_s(d, nq * hd), dn_S = part_s(d, ff);
     if (fold_S > 0) {
       aa.part = e->d_qkv_part;
       aa.part_splits = fold_S;
@@ -943,7 +957,7 @@ static rt_status forward(rt_engine* e, const HostMailbox& plan) {
       {
         GemmArgs g = args_qkv(l);
         if (fold_S > 0) {
-          g.mode = EPI_QKVPART;
+          g.mode = EPI_PART;
           g.part = e->d_qkv_part;
           g.part_ld_n = n;
           g.rs_ss = nullptr;  // the row scale is applied by the attention
@@ -969,7 +983,16 @@ static rt_status forward(rt_engine* e, const HostMailbox& plan) {
       lc_copy(e->d_lc_o, e->d_o, l, (size_t)nq * hd * 2, row0);
       {  // O projection + residual
         GemmArgs g = args_resid(d, nq * hd);
+        if (o_S > 0) {
+          g.mode = EPI_PART;
+          g.part = e->d_qkv_part;
+          g.part_ld_n = n;
+        }
         gemm(w.o, e->x_o, d, nq * hd, g);
+        if (o_S > 0) {
+          launch_resid_reduce(e->d_qkv_part, o_S, n, n, d, e->d_x, e->d_h, e->d_ss, s);
+          ++launches;
+        }
       }
       lc_copy(e->d_lc_xmid, e->d_x, l, (size_t)d * 4, row0);
       {  // gate/up projection (FFN RMSNorm as row scale) + SwiGLU
@@ -979,7 +1002,16 @@ static rt_status forward(rt_engine* e, const HostMailbox& plan) {
       lc_copy(e->d_lc_act, e->d_act, l, (size_t)ff * 2, row0);
       {  // down projection + residual
         GemmArgs g = args_resid(d, ff);
+        if (dn_S > 0) {
+          g.mode = EPI_PART;
+          g.part = e->d_qkv_part;
+          g.part_ld_n = n;
+        }
         gemm(w.d, e->x_act, d, ff, g);
+        if (dn_S > 0) {
+          launch_resid_reduce(e->d_qkv_part, dn_S, n, n, d, e->d_x, e->d_h, e->d_ss, s);
+          ++launches;
+        }
       }
     }
     lc_copy(e->d_lc_x, e->d_x, c.n_layers, (size_t)d * 4, row0);

@@ -658,9 +658,9 @@ __global__ void __launch_bounds__(kGemmThreads, GemmCfg<BN>::CTAS_PER_SM)
   // EPI_QKV: dependents (the decode attention) may launch only once this kernel has passed
   // its own dependency wait — the attention reads the round's row metadata before its wait,
   // which is safe only if every kernel before it has completed (PDL)
-  constexpr bool QKV_LIKE = MODE == EPI_QKV || MODE == EPI_QKVPART;
-  // EPI_QKVPART: no split-K exchange at all — every split writes its raw partial
-  constexpr bool PART = MODE == EPI_QKVPART;
+  constexpr bool QKV_LIKE = MODE == EPI_QKV || MODE == EPI_PART;
+  // EPI_PART: no split-K exchange at all — every split writes its raw partial
+  constexpr bool PART = MODE == EPI_PART;
   if (!QKV_LIKE && threadIdx.x == 0) pdl_trigger();
 
   if (warp == 0) {
@@ -1648,8 +1648,8 @@ __global__ void __launch_bounds__(kDecThreads, 1)
   cluster_wait();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  constexpr bool QKV_LIKE = MODE == EPI_QKV || MODE == EPI_QKVPART;
-  constexpr bool PART = MODE == EPI_QKVPART;  // raw partials, no split-K exchange
+  constexpr bool QKV_LIKE = MODE == EPI_QKV || MODE == EPI_PART;
+  constexpr bool PART = MODE == EPI_PART;  // raw partials, no split-K exchange
   if (!QKV_LIKE && threadIdx.x == 0) pdl_trigger();
 
   if (warp == 0) {
@@ -2214,7 +2214,7 @@ int64_t gemm_dec_ws_floats(int M, int N, int K) {
 static cudaError_t try_launch_dec(const bf16* w_tiled, const GemmTmaSet& x, GemmArgs g, int force_s,
                                   cudaStream_t s) {
   const int m_tiles = (g.M + 127) / 128;
-  const bool part = g.mode == EPI_QKVPART;  // no exchange: no workspace / flags needed
+  const bool part = g.mode == EPI_PART;  // no exchange: no workspace / flags needed
   if (!part && (!g.dec_ws || !g.dec_flags)) return cudaErrorNotSupported;
   if (g.N > 256 || g.N < 1 || g.M % 256 || g.K % kBK || g.mode == EPI_ARGMAX) return cudaErrorNotSupported;
   const int bn = g.N <= 64 ? 64 : (g.N <= 128 ? 128 : 256);
@@ -2237,18 +2237,18 @@ static cudaError_t try_launch_dec(const bf16* w_tiled, const GemmTmaSet& x, Gemm
     case EPI_QKV: return launch_dec_mode<EPI_QKV>(*am, x, g, bn, PT, S, s);
     case EPI_RESID: return launch_dec_mode<EPI_RESID>(*am, x, g, bn, PT, S, s);
     case EPI_SWIGLU: return launch_dec_mode<EPI_SWIGLU>(*am, x, g, bn, PT, S, s);
-    case EPI_QKVPART: return launch_dec_mode<EPI_QKVPART>(*am, x, g, bn, PT, S, s);
+    case EPI_PART: return launch_dec_mode<EPI_PART>(*am, x, g, bn, PT, S, s);
     default: return cudaErrorNotSupported;
   }
 }
 
 int64_t gemm_sk_ws_floats() { return (int64_t)sm_count() * 2 * 256 * 128; }
 
-// Split count of the decode QKV projection in EPI_QKVPART (QKV folded into the attention):
+// Split count of the decode QKV projection in EPI_PART (QKV folded into the attention):
 // the decode pair kernel's at 129..256 rows, the cluster split-K kernel's at <= 128 rows;
 // 0 = not supported at this shape (the caller keeps EPI_QKV).  launch_gemm_epi runs exactly
 // this choice, so the attention knows how many partials to sum.
-int gemm_qkvpart_splits(int M, int K, int N) {
+int gemm_part_splits(int M, int K, int N) {
   if (N < 1 || N > 256 || K % kBK) return 0;
   if (N > 128) {
     if (M % 256) return 0;
@@ -2259,8 +2259,8 @@ int gemm_qkvpart_splits(int M, int K, int N) {
 }
 
 cudaError_t launch_gemm_epi(const bf16* w_tiled, const GemmTmaSet& x, GemmArgs g, int splits, cudaStream_t s) {
-  if (g.mode == EPI_QKVPART) {  // only the two decode kernels write raw partials
-    const int S = gemm_qkvpart_splits(g.M, g.K, g.N);
+  if (g.mode == EPI_PART) {  // only the two decode kernels write raw partials
+    const int S = gemm_part_splits(g.M, g.K, g.N);
     if (S == 0 || !g.part) return cudaErrorInvalidValue;
     if (g.N > 128) return try_launch_dec(w_tiled, x, g, 0, s);
     g.force_path = GEMM_PATH_SPLITK;
@@ -2355,7 +2355,7 @@ cudaError_t launch_gemm_epi(const bf16* w_tiled, const GemmTmaSet& x, GemmArgs g
       case EPI_QKV: return launch_mode<EPI_QKV>(x, g, bn, S, s);
       case EPI_RESID: return launch_mode<EPI_RESID>(x, g, bn, S, s);
       case EPI_SWIGLU: return launch_mode<EPI_SWIGLU>(x, g, bn, S, s);
-      case EPI_QKVPART: return launch_mode<EPI_QKVPART>(x, g, bn, S, s);
+      case EPI_PART: return launch_mode<EPI_PART>(x, g, bn, S, s);
       default: return cudaErrorInvalidValue;
     }
   };

@@ -104,7 +104,7 @@ struct GemmTmaSet {       // activation operand: one map per supported N tile
 };
 bool make_gemm_act_maps(GemmTmaSet* out, const void* base, int K, int rows_cap);
 
-enum EpiMode { EPI_STORE = 0, EPI_ARGMAX = 1, EPI_QKV = 2, EPI_RESID = 3, EPI_SWIGLU = 4, EPI_QKVPART = 5 };
+enum EpiMode { EPI_STORE = 0, EPI_ARGMAX = 1, EPI_QKV = 2, EPI_RESID = 3, EPI_SWIGLU = 4, EPI_PART = 5 };
 // projection kernel paths (GemmArgs::force_path; the values of rt.h RT_GEMM_PATH_*):
 // AUTO = measured dispatch; SPLITK = k_gemm_tc (cluster split-K / one tile per CTA);
 // STREAMK = k_gemm_sk (hybrid data-parallel + stream-K, N > 128); PAIR = k_gemm_2sm (CTA pairs, N > 128)
@@ -137,7 +137,7 @@ struct GemmArgs {
   int ff;
   QkvFuse qkv;        // EPI_QKV
   int l2_evict_first;  // set by launch_gemm_epi: weight tiles are read once per step
-  // EPI_QKVPART (decode QKV folded into the attention): split s of the cluster / pair
+  // EPI_PART (decode QKV folded into the attention): split s of the cluster / pair
   // split-K writes its raw fp32 partial to part[s][n][m] (rows n < N, ld_n rows per split);
   // the attention kernel sums the splits, applies the RMSNorm scale and RoPE, appends K/V
   float* part;
@@ -169,7 +169,10 @@ constexpr int kDecFlags = 512;  // epoch flags of the k_gemm_dec exchange (pair-
 int64_t gemm_sk_ws_floats();
 int gemm_bn(int M, int K, int N);
 int gemm_choose_splits(int M, int N, int K);   // cluster split-K factor (1..16)
-int gemm_qkvpart_splits(int M, int K, int N);  // EPI_QKVPART partial count (0: unsupported)
+int gemm_part_splits(int M, int K, int N);  // EPI_PART partial count (0: unsupported)
+// x[n][:] += sum_s part[s][n][:] (split order), xb = bf16(x), ss[n][M/128] sums of squares
+void launch_resid_reduce(const float* part, int S, int ld_n, int N, int M, float* x, bf16* xb, float* ss,
+                         cudaStream_t s);
 // splits <= 0: gemm_choose_splits
 cudaError_t launch_gemm_epi(const bf16* w_tiled, const GemmTmaSet& xmaps, GemmArgs g, int splits, cudaStream_t s);
 

@@ -29,7 +29,7 @@ RT_FLAG_CAPTURE_LAYERS = 128
 TRACE_DTYPE = np.dtype([("grid", "<u8"), ("kind", "<u4"), ("smid", "<u4"), ("t_entry", "<u8"),
                         ("t_ready", "<u8"), ("t_aux", "<u8"), ("t_exit", "<u8")])
 TRACE_KINDS = {1: "gemm", 2: "attn", 3: "norm", 4: "embed", 5: "sched_pre", 6: "sched_post", 7: "gather",
-               8: "argmax", 9: "merge", 10: "attn_prefill"}
+               8: "argmax", 9: "merge", 10: "attn_prefill", 11: "resid_reduce"}
 
 EXPORTED = ["rt_create", "rt_destroy", "rt_submit_request", "rt_register_prefix", "rt_step", "rt_poll_segment", "rt_last_round",
             "rt_sync", "rt_get_stats", "rt_reset_stats", "rt_debug_dump", "rt_last_error", "rt_version",

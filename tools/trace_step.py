@@ -20,7 +20,7 @@ import profile_step  # noqa: E402
 from paper_2412_18695_b200 import rt  # noqa: E402
 
 CLOCK_GHZ = 1.965   # SM clock under load (bench clocks line) for the clock64 phase marks
-EPI = {0: "store", 1: "lm_head", 2: "qkv", 3: "resid", 4: "swiglu"}
+EPI = {0: "store", 1: "lm_head", 2: "qkv", 3: "resid", 4: "swiglu", 5: "part"}
 
 
 def role(kind, layer_pos):
@@ -30,6 +30,8 @@ def role(kind, layer_pos):
         name = EPI.get(mode, str(mode))
         if mode == 3:   # O projection or down projection: alternate within a layer
             name = "o_proj" if layer_pos == 0 else "down"
+        if mode == 5:   # raw split-K partials: QKV, O, down in layer order
+            name = ("qkv", "o_proj", "down")[layer_pos] + "(part)"
         return f"gemm_{name}(S={kind >> 16})"
     return rt.TRACE_KINDS.get(base, str(base))
 
@@ -56,12 +58,16 @@ def analyse(tr):
     agg = collections.defaultdict(lambda: [0, 0.0, 0.0, 0.0, 0, [], []])
     ph_agg = collections.defaultdict(list)
     resid_seen = 0
+    part_seen = 0
     prev_exit = None
     for L in seq:
         pos = 0
         if (L["kind"] & 0xFF) == 1 and ((L["kind"] >> 8) & 0xFF) == 3:
             pos = resid_seen % 2
             resid_seen += 1
+        if (L["kind"] & 0xFF) == 1 and ((L["kind"] >> 8) & 0xFF) == 5:
+            pos = part_seen % 3
+            part_seen += 1
         name = role(L["kind"], pos)
         gap = (L["ready"] - prev_exit) / 1e3 if prev_exit is not None else 0.0
         a = agg[name]
