@@ -199,52 +199,49 @@ __global__ void k_gather_norm(const int32_t* slot_row, int B, int row0, int n_ro
 // order), the bf16 copy of x (the next projection's operand) and the per-128-feature sums of
 // squares of the new x (the next RMSNorm, folded into its consumer).  CTA = (row n, 1024
 // features), 256 threads x 4 features (float4); one warp = one 128-feature tile.
-__global__ void __launch_bounds__(256) k_resid_reduce(const float* part, int S, int ld_n, int M, float* x, bf16* xb,
+template <int S>
+__global__ void __launch_bounds__(256) k_resid_reduce(const float* part, int ld_n, int M, float* x, bf16* xb,
                                                       float* ss) {
   TraceScope tr(TK_RESID);
   if (threadIdx.x == 0) pdl_trigger();
   pdl_wait();
   tr.ready();
-  // CTA = (row n, 2048 features): thread t takes float4 groups t and t + 256 (two 128-feature
-  // tiles per warp), every load of the thread in flight at once
+  // CTA = (row n, 1024 features), thread = one float4 group; the split count is a template
+  // parameter so the registers (and the one-wave occupancy of all CTAs) fit
   const int n = blockIdx.x;
-  constexpr int kMax = 8, V = 2;
-  float4 w[V][kMax], xo[V];
-  int f[V];
+  const int f = blockIdx.y * 1024 + threadIdx.x * 4;
+  if (f >= M) return;  // (M % 128 == 0: whole warps)
+  float4 w[S];
 #pragma unroll
-  for (int u = 0; u < V; ++u) {
-    f[u] = blockIdx.y * 2048 + (threadIdx.x + 256 * u) * 4;
-    const bool ok = f[u] < M;
+  for (int sp = 0; sp < S; ++sp) w[sp] = __ldcg(reinterpret_cast<const float4*>(part + ((size_t)sp * ld_n + n) * M + f));
+  float4* xp = reinterpret_cast<float4*>(x + (size_t)n * M + f);
+  const float4 xo = __ldcg(xp);
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-    for (int sp = 0; sp < kMax; ++sp)
-      w[u][sp] = (ok && sp < S) ? __ldcg(reinterpret_cast<const float4*>(part + ((size_t)sp * ld_n + n) * M + f[u]))
-                                : make_float4(0.f, 0.f, 0.f, 0.f);
-    xo[u] = ok ? __ldcg(reinterpret_cast<const float4*>(x + (size_t)n * M + f[u])) : make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int sp = 0; sp < S; ++sp) {
+    acc.x += w[sp].x;
+    acc.y += w[sp].y;
+    acc.z += w[sp].z;
+    acc.w += w[sp].w;
   }
+  const float4 xn = make_float4(xo.x + acc.x, xo.y + acc.y, xo.z + acc.z, xo.w + acc.w);
+  *xp = xn;
+  *reinterpret_cast<uint2*>(xb + (size_t)n * M + f) = make_uint2(pack_bf16x2(xn.x, xn.y), pack_bf16x2(xn.z, xn.w));
+  float q = ((xn.x * xn.x + xn.y * xn.y) + xn.z * xn.z) + xn.w * xn.w;
 #pragma unroll
-  for (int u = 0; u < V; ++u) {
-    if (f[u] >= M) break;  // (M % 128 == 0: whole warps)
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-    for (int sp = 0; sp < kMax; ++sp)
-      if (sp < S) {
-        acc.x += w[u][sp].x;
-        acc.y += w[u][sp].y;
-        acc.z += w[u][sp].z;
-        acc.w += w[u][sp].w;
-      }
-    const float4 xn = make_float4(xo[u].x + acc.x, xo[u].y + acc.y, xo[u].z + acc.z, xo[u].w + acc.w);
-    *reinterpret_cast<float4*>(x + (size_t)n * M + f[u]) = xn;
-    *reinterpret_cast<uint2*>(xb + (size_t)n * M + f[u]) = make_uint2(pack_bf16x2(xn.x, xn.y), pack_bf16x2(xn.z, xn.w));
-    float q = ((xn.x * xn.x + xn.y * xn.y) + xn.z * xn.z) + xn.w * xn.w;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
-    if ((threadIdx.x & 31) == 0) ss[(size_t)n * (M / 128) + f[u] / 128] = q;
-  }
+  for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+  if ((threadIdx.x & 31) == 0) ss[(size_t)n * (M / 128) + f / 128] = q;
 }
 void launch_resid_reduce(const float* part, int S, int ld_n, int N, int M, float* x, bf16* xb, float* ss,
                          cudaStream_t s) {
-  launch_pdl(k_resid_reduce, dim3(N, (M + 2047) / 2048), dim3(256), 0, s, part, S, ld_n, M, x, xb, ss);
+  const dim3 grid(N, (M + 1023) / 1024), block(256);
+  switch (S) {
+#define RT_RR(k) \
+  case k: launch_pdl(k_resid_reduce<k>, grid, block, 0, s, part, ld_n, M, x, xb, ss); break;
+    RT_RR(1) RT_RR(2) RT_RR(3) RT_RR(4) RT_RR(5) RT_RR(6) RT_RR(7) RT_RR(8)
+#undef RT_RR
+    default: break;
+  }
 }
 
 // ------------------------------------------------------ argmax final reduce
