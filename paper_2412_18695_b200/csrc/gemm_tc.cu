@@ -50,6 +50,7 @@
 namespace rt {
 
 constexpr int kGemmThreads = 192;
+constexpr int kDecThreads = 320;  // CTA-pair kernels: producer, MMA, 2 x 4 epilogue warps
 constexpr int kBK = 64;  // one 128-byte swizzle atom of bf16 along K
 
 template <int BN>
@@ -1182,8 +1183,8 @@ struct Cfg {
   static constexpr int A_BYTES = 128 * kBK * 2;
   static constexpr int B_BYTES = HB * kBK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int CHUNK = 64;
-  static constexpr int STG_BYTES = CHUNK * 128 * 4;
+  static constexpr int CHUNK = 32;                     // epilogue columns per staging pass (per group)
+  static constexpr int STG_BYTES = 2 * CHUNK * 128 * 4;  // one staging buffer per epilogue group
   static constexpr int TMEM_COLS = 2 * BN <= 256 ? 256 : 512;
   static constexpr int CTL = 256;
   static constexpr int META = 3 * BN * 4;
@@ -1257,7 +1258,7 @@ struct PairSeq {
 };
 
 template <int BN, int MODE>
-__global__ void __launch_bounds__(kGemmThreads, 1)
+__global__ void __launch_bounds__(kDecThreads, 1)
     k_gemm_2sm(const __grid_constant__ TmaMap tmA, const __grid_constant__ TmaMap tmB,
                const __grid_constant__ TmaMap tmBs, GemmArgs g, SkArgs a) {
   using C = sm2::Cfg<BN>;
@@ -1305,7 +1306,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 2);
+      mbar_init(&tempty[i], 4);  // one arrival per epilogue group of each CTA
     }
     fence_mbar_init();
   }
@@ -1382,10 +1383,18 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     }
     __syncwarp();
   } else {
+    // two epilogue groups of 4 warps (2-5, 6-9), both over the 128 TMEM lanes, taking
+    // alternate CHUNK-column chunks of each tile with their own staging buffer: the last
+    // tile's epilogue (not overlapped by a next mainloop) runs on 8 warps
     pdl_wait();
+    const int grp = (warp - 2) >> 2;
     const int et = (warp & 3) * 32 + lane;
     const uint32_t tb = tmem + ((uint32_t)((warp & 3) * 32) << 16);
     const uint32_t tempty0 = dsmem_addr(smem_u32(tempty), 0);
+    float* gstg = stg + (size_t)grp * CHUNK * 128;
+    EpiSmem gsm = sm;
+    gsm.bar = 1 + grp;
+    gsm.mark = nullptr;
     long long c_wait = 0, c_park = 0, c_epi = 0;  // epilogue-warp cycle totals (trace phases)
     int seg = 0, i = 0;
     PSeg sg;
@@ -1398,14 +1407,19 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
       const int W = sg.sub >= 0 ? kPairSubW : BN;  // accumulator columns of this segment
       mbar_wait(&tfull[buf], (uint32_t)((seg >> 1) & 1));
       tc_fence_after();
-      epi_bar();  // the previous tile's epilogue is done with the staging buffer / sm
+      // both groups are done with the previous tile (staging, per-column metadata)
+      asm volatile("bar.sync 3, 256;" ::: "memory");
       const long long c1w = clock64();
       c_wait += c1w - c0w;
       const uint32_t tacc = tb + (uint32_t)(buf * BN);
-      column_meta<MODE>(g, sm, m_tile, n0, 0, W, et);
+      if (grp == 0) column_meta<MODE>(g, sm, m_tile, n0, 0, W, et);  // (group barrier inside)
+      asm volatile("bar.sync 3, 256;" ::: "memory");                // ... seen by group 1 too
       const TileSrc ts0{nullptr, nullptr, 0u, 1, 0, BN, 0, 0};
+      const int n_ch = (W + CHUNK - 1) / CHUNK;
+      const int my_last = ((n_ch - 1 - grp) >= 0) ? grp + 2 * ((n_ch - 1 - grp) / 2) : -1;  // last chunk of this group
 #pragma unroll 1
-      for (int cb = 0; cb < W; cb += CHUNK) {
+      for (int ch = grp; ch < n_ch; ch += 2) {
+        const int cb = ch * CHUNK;
         const int ce = min(W, cb + CHUNK);
         const long long cp0 = clock64();
         if constexpr (MODE == EPI_ARGMAX) {
@@ -1422,7 +1436,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
 #pragma unroll
             for (int k = 0; k < 16; ++k) {
               const int c = c0 - cb + k;
-              stg[c * 128 + ((((et >> 2) ^ (c & 31)) << 2) | (et & 3))] = v[k];
+              gstg[c * 128 + ((((et >> 2) ^ (c & 31)) << 2) | (et & 3))] = v[k];
             }
             if (g.out && m < g.M)  // logits (parity mode only)
 #pragma unroll
@@ -1435,63 +1449,75 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
             float v[16];
             tmem_ld16(tacc + (uint32_t)c0, v);
 #pragma unroll
-            for (int k = 0; k < 16; ++k) stg[(c0 - cb + k) * 128 + et] = v[k];
+            for (int k = 0; k < 16; ++k) gstg[(c0 - cb + k) * 128 + et] = v[k];
           }
         }
         c_park += clock64() - cp0;
-        if (ce == W) {  // the accumulator buffer is read out: release it to the MMA issuer
+        if (ch == my_last) {  // this group is done reading the accumulator: release its part
           tc_fence_before();
-          epi_bar();
+          epi_bar(gsm.bar);
           if (et == 0) {
             if (rank == 0) mbar_arrive(&tempty[buf]);
             else mbar_arrive_cluster(tempty0 + (uint32_t)buf * 8u);
           }
         }
-        epi_bar();
+        epi_bar(gsm.bar);
         const long long ce0 = clock64();
         if constexpr (MODE == EPI_ARGMAX) {
-          // thread et scans half `hf` of the rows of column c (64 rows as 16 chunks of 4),
+          // thread et scans quarter `hf` of the rows of column c (32 rows as 8 chunks of 4),
           // ascending -> the first maximum = the lowest vocabulary index (greedy, AMB: ties)
+          constexpr int NHF = 128 / CHUNK;  // row parts (4 at 32-column chunks)
           const int wc = ce - cb, c = et % CHUNK, hf = et / CHUNK;
-          if (c < wc && hf < 2) {
+          if (c < wc && hf < NHF) {
             float bv = -INFINITY;
             int br = 0;
-            const float* col = stg + (size_t)c * 128;
+            const float* col = gstg + (size_t)c * 128;
             const int rmax = g.M - m_tile * 128;  // rows beyond M (last m-tile) never win
+            constexpr int QP = 32 / NHF;          // 16-byte chunks per part
 #pragma unroll 4
-            for (int q = 16 * hf; q < 16 * hf + 16; ++q) {
+            for (int q = QP * hf; q < QP * hf + QP; ++q) {
               const float4 x = *reinterpret_cast<const float4*>(col + ((q ^ (c & 31)) << 2));
               if (x.x > bv && 4 * q < rmax) { bv = x.x; br = 4 * q; }
               if (x.y > bv && 4 * q + 1 < rmax) { bv = x.y; br = 4 * q + 1; }
               if (x.z > bv && 4 * q + 2 < rmax) { bv = x.z; br = 4 * q + 2; }
               if (x.w > bv && 4 * q + 3 < rmax) { bv = x.w; br = 4 * q + 3; }
             }
-            sm.redv[hf * BN + c] = bv;
-            sm.redi[hf * BN + c] = m_tile * 128 + br;
+            sm.redv[hf * BN + cb + c] = bv;
+            sm.redi[hf * BN + cb + c] = m_tile * 128 + br;
           }
-          epi_bar();
+          epi_bar(gsm.bar);
           if (et < wc && n0 + cb + et < g.N) {
-            float bv = sm.redv[et];
-            int bi = sm.redi[et];
-            const float ov = sm.redv[BN + et];
-            const int oi = sm.redi[BN + et];
-            if (ov > bv) {  // the lower half wins ties (lower index)
-              bv = ov;
-              bi = oi;
+            float bv = sm.redv[cb + et];
+            int bi = sm.redi[cb + et];
+#pragma unroll
+            for (int p = 1; p < NHF; ++p) {  // lower row parts win ties (lower index)
+              const float ov = sm.redv[p * BN + cb + et];
+              const int oi = sm.redi[p * BN + cb + et];
+              if (ov > bv) {
+                bv = ov;
+                bi = oi;
+              }
             }
             g.part_val[(size_t)m_tile * g.N + n0 + cb + et] = bv;
             g.part_idx[(size_t)m_tile * g.N + n0 + cb + et] = bi;
           }
         } else {
           TileSrc ts = ts0;
-          ts.P = stg - (size_t)cb * 128;  // the epilogue indexes absolute columns
-          epilogue<MODE>(g, sm, ts, m_tile, n0, cb, ce, et, false);
+          ts.P = gstg - (size_t)cb * 128;  // the epilogue indexes absolute columns
+          epilogue<MODE>(g, gsm, ts, m_tile, n0, cb, ce, et, false);
         }
-        epi_bar();
+        epi_bar(gsm.bar);
         c_epi += clock64() - ce0;
       }
+      if (my_last < 0) {  // (a group without chunks in this tile still releases its part)
+        tc_fence_before();
+        if (et == 0) {
+          if (rank == 0) mbar_arrive(&tempty[buf]);
+          else mbar_arrive_cluster(tempty0 + (uint32_t)buf * 8u);
+        }
+      }
     }
-    if (et == 0) {  // trace: totals over this CTA's tiles (wait for the accumulator | park | epilogue)
+    if (et == 0 && grp == 0) {  // trace: totals over this CTA's tiles (wait for the accumulator | park | epilogue)
       s_mark[0] = 0;
       s_mark[1] = c_wait;
       s_mark[2] = c_wait + c_park;
@@ -1575,8 +1601,6 @@ RT_DEV unsigned ld_acquire_gpu(const unsigned* p) {
   return v;
 }
 }  // namespace dec
-
-constexpr int kDecThreads = 320;  // producer, MMA, 2 x 4 epilogue warps
 
 template <int BN, int MODE>
 __global__ void __launch_bounds__(kDecThreads, 1)
@@ -2080,7 +2104,7 @@ static cudaError_t launch_2sm_bn(const TmaMap& am, const TmaMap& bm, const TmaMa
     if (slots) return cudaSuccess;
   }
   cudaLaunchConfig_t cfg{};
-  cfg.blockDim = dim3(kGemmThreads);
+  cfg.blockDim = dim3(kDecThreads);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = s;
   cudaLaunchAttribute at[2];
@@ -2137,7 +2161,7 @@ static int pair_slots_bn() {
     TmaMap t{};
     launch_2sm_bn<BN, EPI_STORE>(t, t, t, g, 0, SkArgs{}, nullptr);
     cudaLaunchConfig_t cfg{};
-    cfg.blockDim = dim3(kGemmThreads);
+    cfg.blockDim = dim3(kDecThreads);
     cfg.dynamicSmemBytes = sm2::Cfg<BN>::SMEM;
     cfg.gridDim = dim3(sm_count() & ~1);
     cudaLaunchAttribute at[1];
