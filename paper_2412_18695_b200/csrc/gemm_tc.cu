@@ -1183,7 +1183,10 @@ struct Cfg {
   static constexpr int A_BYTES = 128 * kBK * 2;
   static constexpr int B_BYTES = HB * kBK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int CHUNK = 32;                     // epilogue columns per staging pass (per group)
+#ifndef RT_PAIR_CHUNK
+#define RT_PAIR_CHUNK 16
+#endif
+  static constexpr int CHUNK = RT_PAIR_CHUNK;          // epilogue columns per staging pass (per group)
   static constexpr int STG_BYTES = 2 * CHUNK * 128 * 4;  // one staging buffer per epilogue group
   static constexpr int TMEM_COLS = 2 * BN <= 256 ? 256 : 512;
   static constexpr int CTL = 256;
@@ -1466,7 +1469,7 @@ __global__ void __launch_bounds__(kDecThreads, 1)
         if constexpr (MODE == EPI_ARGMAX) {
           // thread et scans quarter `hf` of the rows of column c (32 rows as 8 chunks of 4),
           // ascending -> the first maximum = the lowest vocabulary index (greedy, AMB: ties)
-          constexpr int NHF = 128 / CHUNK;  // row parts (4 at 32-column chunks)
+          constexpr int NHF = 128 / CHUNK < 4 ? 128 / CHUNK : 4;  // row parts (redv / redi hold 4)
           const int wc = ce - cb, c = et % CHUNK, hf = et / CHUNK;
           if (c < wc && hf < NHF) {
             float bv = -INFINITY;
