@@ -102,7 +102,8 @@ __global__ void __launch_bounds__(kAttnWarps * 32) k_attn(AttnArgs a) {
       bulk_g2s_hint(ring + i * C::BLOCK, pool + (size_t)pg * page_stride + head_off, C::BLOCK, &bar[i], pol);
     }
   }
-  __shared__ __align__(16) bf16 s_q[8 * HD];  // folded q (G <= 8 heads) of this kv head
+  constexpr int QLD = HD + 8;  // folded-q row stride: the 8 rows of a fragment load hit distinct banks
+  __shared__ __align__(16) bf16 s_q[8 * QLD];  // folded q (G <= 8 heads) of this kv head
   if (fold) {
     // ---- QKV epilogue of this (row, kv head): sum the projection's split-K partials in split
     // order, RMSNorm row scale, RoPE (rotate-half; weight rows 2i, 2i + 1 = dims i, i + hd/2),
@@ -181,8 +182,8 @@ __global__ void __launch_bounds__(kAttnWarps * 32) k_attn(AttnArgs a) {
         }
         const bf16 b0 = __float2bfloat16_rn(y0), b1 = __float2bfloat16_rn(y1);
         if (hl < G) {
-          s_q[hl * HD + i] = b0;
-          s_q[hl * HD + i + HALF] = b1;
+          s_q[hl * QLD + i] = b0;
+          s_q[hl * QLD + i + HALF] = b1;
           if (chunk == 0) {
             bf16* qo = a.q_out + ((size_t)r * a.nq + head) * HD;
             qo[i] = b0;
@@ -218,10 +219,11 @@ __global__ void __launch_bounds__(kAttnWarps * 32) k_attn(AttnArgs a) {
   uint32_t qa[HD / 16][2];
   {
     const bf16* qrow = fold ? s_q : a.q + ((size_t)r * a.nq + (size_t)h * G) * HD;
+    const int qld = fold ? QLD : HD;
 #pragma unroll
     for (int ks = 0; ks < HD / 16; ++ks) {
       if (gq < G) {
-        const uint32_t* q32 = reinterpret_cast<const uint32_t*>(qrow + (size_t)gq * HD + ks * 16);
+        const uint32_t* q32 = reinterpret_cast<const uint32_t*>(qrow + (size_t)gq * qld + ks * 16);
         qa[ks][0] = q32[qq];
         qa[ks][1] = q32[4 + qq];
       } else {

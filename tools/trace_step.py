@@ -58,7 +58,7 @@ def analyse(tr):
     agg = collections.defaultdict(lambda: [0, 0.0, 0.0, 0.0, 0, [], []])
     ph_agg = collections.defaultdict(list)
     resid_seen = 0
-    part_seen = 0
+    prev_role = None
     prev_exit = None
     for L in seq:
         pos = 0
@@ -66,9 +66,10 @@ def analyse(tr):
             pos = resid_seen % 2
             resid_seen += 1
         if (L["kind"] & 0xFF) == 1 and ((L["kind"] >> 8) & 0xFF) == 5:
-            pos = part_seen % 3
-            part_seen += 1
+            # raw partials: O follows the attention, down follows gate/up, QKV otherwise
+            pos = 1 if prev_role == "attn" else (2 if (prev_role or "").startswith("gemm_swiglu") else 0)
         name = role(L["kind"], pos)
+        prev_role = name
         gap = (L["ready"] - prev_exit) / 1e3 if prev_exit is not None else 0.0
         a = agg[name]
         a[0] += 1
