@@ -123,6 +123,42 @@ def test_sched_parity_comparison_systems(rt, policy, seg_mode):
     assert len(admits) == len(set(admits)) == len(reqs)   # never suspended / re-queued
 
 
+@pytest.mark.parametrize("name", ["c5", "c4"])
+def test_sched_parity_at_c4_c5_task_counts(rt, name):
+    """Scheduling-only parity at the task counts of BASELINE configs[3-4] (the bench's CPU
+    replays): C5 = 512 agents of long robot-arm plans (160 tokens, max_new 256), 128-token
+    prompts, AMB-26 reservations on a pool that refuses admissions, batch 512; C4 = 1024 agents
+    of traces 1-11, batch 128.  Hundreds of waiting candidates per round exercise the device
+    sorts (rank sort <= 128, register bitonic <= 1024, shared-memory bitonic beyond) and the
+    closed-form admission; rounds, admissions, segments, page tables and the free stack are
+    bit-exact against the oracle."""
+    v = make_vocab(128256)
+    if name == "c5":
+        p = engine_params("b200-roofline", max_batch=512, max_tasks=2048, max_ctx=4096, n_pages=277 * 24)
+        reqs = compose_workload(512, 64.0, 16, range(9, 12), 10.0, 0, v, prompt_len_range=(128, 128),
+                                max_requests=1536, plan_len=160)
+    else:
+        p = engine_params("b200-roofline", max_batch=128, max_tasks=2048, max_ctx=4096, n_pages=1 << 16)
+        reqs = compose_workload(1024, 640.0, 16, range(1, 12), 10.0, 0, v, prompt_len_range=(64, 64),
+                                max_requests=2000)
+    eng, ora = make_pair(rt, v, p)
+    for r in reqs:
+        mx = 256 if name == "c5" else len(r.plan)
+        a = eng.submit(r.agent_id, r.prompt, r.arrival_us, r.ert_us, r.alpha, r.beta, r.exec_window_us, mx,
+                       script=r.plan)
+        b = ora.submit(r.agent_id, r.prompt, r.arrival_us, r.ert_us, r.alpha, r.beta, r.exec_window_us, mx,
+                       script=r.plan)
+        assert a == b
+    n, segs = lockstep(eng, ora, max_rounds=400, check_every=20)
+    waiting = max(r["n_waiting"] for r in ora.round_log)
+    assert waiting > 128                      # beyond the rank sort
+    if name == "c5":
+        assert any(r["n_refused_mem"] > 0 for r in ora.round_log)
+    else:
+        assert waiting > 1024                 # the shared-memory bitonic path
+    eng.close()
+
+
 def _evict_workload(v, **kw):
     p = engine_params("paper-4090", max_batch=8, max_tasks=512, max_ctx=256, n_pages=40, host_pages=64,
                       swap_us_per_page=116, **kw)
