@@ -1808,14 +1808,14 @@ __global__ void __launch_bounds__(kDecThreads, 1)
         for (int jj = 0; jj < 16; ++jj) __stcg(dst + (size_t)(c0 - qb + jj) * 128, v[jj]);
       }
     }
-    EPI_MARK(1);
+    if (et == 0 && grp == 0) s_mark[1] = clock64();  // (trace marks: group 0 only)
     asm volatile("bar.sync 3, 256;" ::: "memory");  // every row of this CTA's slices is written
     unsigned* myflags = flags + ((size_t)t * 2 + h) * S;
     if (et == 0 && grp == 0) {
       __threadfence();
       dec::st_release_gpu(myflags + p, epoch);
     }
-    EPI_MARK(2);
+    if (et == 0 && grp == 0) s_mark[2] = clock64();
     // wait for the S - 1 contributors of my slice, then bulk-copy their slices (ring slots
     // j = 0 .. S - 2 in pair order, wslot columns each) into shared memory at once
     float* R = reinterpret_cast<float*>(smem);
@@ -1829,7 +1829,7 @@ __global__ void __launch_bounds__(kDecThreads, 1)
       for (int q = 0, j = 0; q < S; ++q)
         if (q != p) bulk_g2s(R + (size_t)(j++) * wslot * 128, slot_ptr(p, q), slice_bytes, rx_bar);
     }
-    EPI_MARK(3);
+    if (et == 0 && grp == 0) s_mark[3] = clock64();
     mbar_wait(rx_bar, 0);
     // ---- sum the S partials of the group's columns in pair order (deterministic) -> T (= slot
     // 0: every element is read, then written, by the same thread)
@@ -1862,7 +1862,7 @@ __global__ void __launch_bounds__(kDecThreads, 1)
     const TileSrc ts{T - (size_t)cb * 128, nullptr, 0u, 1, 0, BN, 0, 0};
     if (gcb < gce) epilogue<MODE>(g, gs, ts, m_tile, 0, gcb, gce, et, true);
     }  // !PART
-    EPI_MARK(8);
+    if (et == 0 && grp == 0) s_mark[8] = clock64();
   }
   tc_fence_before();
   __syncthreads();
