@@ -64,8 +64,9 @@ __global__ void __launch_bounds__(kAttnWarps * 32) k_attn(AttnArgs a) {
   // those trigger their dependents only AFTER their own griddepcontrol.wait — so when this
   // code runs, every kernel before the QKV projection, the scheduler included, has completed.
   // (With the trigger at the QKV kernel's start, a chain of early launches could reach here
-  // while the scheduler was still writing: found as an intermittent stale read.)  q and the
-  // new KV entries come from the QKV projection itself: page ids, q and pages after the wait.
+  // while the scheduler was still writing: found as an intermittent stale read.)  The page
+  // table is the scheduler's too; only q and the new KV entries (the row's last page) come from
+  // the QKV projection itself and are read after the wait.
   const int row = a.row_list ? a.row_list[blockIdx.z] : a.row0 + (int)blockIdx.z;
   const int r = row - a.row0;  // row within this forward chunk
   if (a.row_list && (r < 0 || r >= a.chunk_rows)) return;
@@ -80,20 +81,20 @@ __global__ void __launch_bounds__(kAttnWarps * 32) k_attn(AttnArgs a) {
   // pages of this warp: p_begin + warp + i * NW
   const int n_my = p_end - (p_begin + warp) > 0 ? (p_end - (p_begin + warp) + kAttnWarps - 1) / kAttnWarps : 0;
   __syncwarp();
-  pdl_wait();
-  tr.ready();
-  // QKV folded in (a.part): this CTA's chunk holding the row's last page appends this round's
-  // K / V into it, so that page is loaded only after the append (deferred below)
+  // The K / V of every position before this round's token were written in earlier rounds
+  // (pages and page-table entries are stable: see the metadata note above), so the first
+  // stages' page loads are issued BEFORE the dependency wait — only the row's last page, which
+  // receives this round's K / V (from the QKV projection, or appended by the fold below), waits.
   const bool fold = a.part != nullptr;
   const int last_pg = n_pages - 1;
   const bool appends = fold && chunk == n_chunks - 1;
   // page ids of the first 32 pages of this warp, one per lane
   int my_page = (lane < n_my) ? ptab[p_begin + warp + lane * kAttnWarps] : 0;
-  int deferred = -1;  // stage of this warp whose (last) page waits for the append
+  int deferred = -1;  // stage of this warp whose (last) page waits for the dependency / append
 #pragma unroll
   for (int i = 0; i < C::STAGES; ++i) {
     const int pg = __shfl_sync(0xffffffffu, my_page, i);
-    if (i < n_my && appends && p_begin + warp + i * kAttnWarps == last_pg) {
+    if (i < n_my && p_begin + warp + i * kAttnWarps == last_pg) {
       deferred = i;
       continue;
     }
@@ -102,6 +103,8 @@ __global__ void __launch_bounds__(kAttnWarps * 32) k_attn(AttnArgs a) {
       bulk_g2s_hint(ring + i * C::BLOCK, pool + (size_t)pg * page_stride + head_off, C::BLOCK, &bar[i], pol);
     }
   }
+  pdl_wait();
+  tr.ready();
   constexpr int QLD = HD + 8;  // folded-q row stride: the 8 rows of a fragment load hit distinct banks
   __shared__ __align__(16) bf16 s_q[8 * QLD];  // folded q (G <= 8 heads) of this kv head
   if (fold) {
@@ -205,13 +208,14 @@ __global__ void __launch_bounds__(kAttnWarps * 32) k_attn(AttnArgs a) {
     }
     fence_proxy_async_global();  // the appended K / V rows are read by the bulk copies below
     __syncthreads();
-    if (deferred >= 0) {  // (warp-uniform)
-      const int pg = __shfl_sync(0xffffffffu, my_page, deferred);
-      if (lane == 0) {
-        mbar_arrive_expect_tx(&bar[deferred], C::BLOCK);
-        bulk_g2s_hint(ring + deferred * C::BLOCK, pool + (size_t)pg * page_stride + head_off, C::BLOCK,
-                      &bar[deferred], pol);
-      }
+  }
+  if (deferred >= 0) {  // the last page, after the dependency (and the fold's append); warp-uniform
+    const int pg = __shfl_sync(0xffffffffu, my_page, deferred);
+    if (lane == 0) {
+      if (!fold) fence_proxy_async_global();
+      mbar_arrive_expect_tx(&bar[deferred], C::BLOCK);
+      bulk_g2s_hint(ring + deferred * C::BLOCK, pool + (size_t)pg * page_stride + head_off, C::BLOCK,
+                    &bar[deferred], pol);
     }
   }
 
