@@ -75,6 +75,9 @@ def main(rounds=200, trace=False):
     print(f"rounds {len(a)}: mean rows {a[:, 0].mean():.0f} (prompt {a[:, 1].mean():.0f}), tokens/round "
           f"{a[:, 2].mean():.1f}, wall {a[:, 3].mean():.2f} ms, device {a[:, 4].mean():.2f} ms "
           f"(forward {a[:, 5].mean():.2f}, attention {a[:, 6].mean():.2f}) -> {a[:, 2].sum() / a[:, 3].sum() * 1e3:.0f} tok/s")
+    big = a[a[:, 0] >= 513, 0]
+    if len(big):
+        print("  rows of the > 512-row rounds: percentiles 10/50/90 =", np.percentile(big, [10, 50, 90]).round())
     for lo, hi in ((0, 65), (65, 129), (129, 257), (257, 513), (513, 100000)):
         m = (a[:, 0] >= lo) & (a[:, 0] < hi)
         if m.any():
