@@ -300,8 +300,10 @@ def run_ours(args, rank, world, dist):
     R.lockstep_until_idle(lambda: eng.step(now()), dist, max_rounds=4000)
     eng.poll()
     eng.sync()
-    pfx = {r: system_prefix(vocab, r, PREFIX[r], seed=args.seed) for r in ("drone", "arm")}
-    for r in ("drone", "arm"):
+    # the robots this workload serves (C2: drones only, whose contexts fit max_ctx = 2048)
+    robots = ("drone",) if args.workload == "C2" else ("drone", "arm")
+    pfx = {r: system_prefix(vocab, r, PREFIX[r], seed=args.seed) for r in robots}
+    for r in robots:
         eng.register_prefix(pfx[r])
     e2e = run_e2e(args, eng, vocab, p, rank, world, now, dist, reqs, prefixes=pfx, start_agents=agents,
                   steps=max(K, args.e2e_steps))
