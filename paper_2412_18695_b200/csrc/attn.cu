@@ -34,6 +34,112 @@ struct AttnCfg {
   static constexpr int SMEM = (RING > MERGE ? RING : MERGE) + kAttnWarps * STAGES * 8 + 64;
 };
 
+// The QKV projection's epilogue for one (row, kv head) when the projection wrote raw split-K
+// partials (EPI_PART): sum the splits in order, RMSNorm row scale, RoPE on the G
+// q heads and the k head (weight rows 2i, 2i + 1 = dims i, i + hd/2), bf16 q -> s_q (shared,
+// row stride qld, nullable) and / or a.q_out (+ a.q_cap), bf16 k / v appended at position pos of
+// page pg_last.  All 128 threads of the CTA; no barrier inside.
+template <int HD>
+__device__ __forceinline__ void fold_qkv(const AttnArgs& a, int r, int row, int h, int pos, int pg_last, int G,
+                                         bf16* s_q, int qld, bool write_q, bool append) {
+  // RMSNorm row scale: every thread sums the row's per-tile sums of squares itself, in tile
+  // order; its loads are issued together with the first group's partial loads below (one
+  // L2 round trip for both), no barrier
+  constexpr int kRsMax = 64;   // per-row tiles held in registers (d_model <= 8192)
+  const float* rs = a.rs_ss + (size_t)r * a.rs_tiles;
+  const bool rs_vec = (a.rs_tiles & 3) == 0 && a.rs_tiles <= kRsMax && ((uintptr_t)rs & 15) == 0;
+  float4 rs4[kRsMax / 4];
+#pragma unroll
+  for (int i = 0; i < kRsMax / 4; ++i)
+    rs4[i] = (rs_vec && 4 * i < a.rs_tiles) ? __ldcg(reinterpret_cast<const float4*>(rs) + i)
+                                            : make_float4(0.f, 0.f, 0.f, 0.f);
+  float inv = 0.f;
+  bool have_inv = false;
+  constexpr int HALF = HD / 2;
+  constexpr int kMaxSplits = 8;  // gemm_part_splits <= 8 (cluster / pair split-K choices)
+  constexpr int PB = 3;          // pairs per thread per round trip
+  const int off = pos & 15;
+  const int n_pairs = (G + 2) * HALF;
+  const int S = a.part_splits;
+  const size_t split_stride = (size_t)a.part_ld_n * a.part_m;
+  for (int j0 = threadIdx.x; j0 < n_pairs; j0 += PB * blockDim.x) {
+    // all the split partials (and the rotations) of PB pairs in flight at once
+    float2 w[PB][kMaxSplits];
+    float cr[PB], sr[PB];
+#pragma unroll
+    for (int u = 0; u < PB; ++u) {
+      const int j = j0 + u * (int)blockDim.x;
+      const bool ok = j < n_pairs;
+      const int hl = j / HALF, i = j - hl * HALF;  // local head: q 0..G-1, then k, v
+      const int head = hl < G ? h * G + hl : (hl == G ? a.nq + h : a.nq + a.nkv + h);
+      const float* src = a.part + (size_t)r * a.part_m + (size_t)head * HD + 2 * i;
+#pragma unroll
+      for (int sp = 0; sp < kMaxSplits; ++sp)
+        w[u][sp] = (ok && sp < S) ? __ldcg(reinterpret_cast<const float2*>(src + sp * split_stride))
+                                  : make_float2(0.f, 0.f);
+      const bool rot = ok && hl <= G;  // q and k heads are rotated
+      cr[u] = rot ? __ldg(a.cos + (size_t)pos * HALF + i) : 1.f;
+      sr[u] = rot ? __ldg(a.sin + (size_t)pos * HALF + i) : 0.f;
+    }
+    if (!have_inv) {
+      float t = 0.f;
+      if (rs_vec) {
+#pragma unroll
+        for (int i = 0; i < kRsMax / 4; ++i)
+          if (4 * i < a.rs_tiles) t = (((t + rs4[i].x) + rs4[i].y) + rs4[i].z) + rs4[i].w;
+      } else {
+        for (int i = 0; i < a.rs_tiles; ++i) t += __ldcg(rs + i);
+      }
+      inv = rsqrtf(t / (float)a.d_model + 1e-5f);
+      have_inv = true;
+    }
+#pragma unroll
+    for (int u = 0; u < PB; ++u) {
+      const int j = j0 + u * (int)blockDim.x;
+      if (j >= n_pairs) break;
+      const int hl = j / HALF, i = j - hl * HALF;
+      const int head = hl < G ? h * G + hl : (hl == G ? a.nq + h : a.nq + a.nkv + h);
+      float v0 = 0.f, v1 = 0.f;  // the sum in split order
+#pragma unroll
+      for (int sp = 0; sp < kMaxSplits; ++sp)
+        if (sp < S) {
+          v0 += w[u][sp].x;
+          v1 += w[u][sp].y;
+        }
+      v0 *= inv;
+      v1 *= inv;
+      float y0 = v0, y1 = v1;
+      if (hl <= G) {
+        y0 = v0 * cr[u] - v1 * sr[u];
+        y1 = v1 * cr[u] + v0 * sr[u];
+      }
+      const bf16 b0 = __float2bfloat16_rn(y0), b1 = __float2bfloat16_rn(y1);
+      if (hl < G) {
+        if (s_q) {
+          s_q[hl * qld + i] = b0;
+          s_q[hl * qld + i + HALF] = b1;
+        }
+        if (write_q) {
+          bf16* qo = a.q_out + ((size_t)r * a.nq + head) * HD;
+          qo[i] = b0;
+          qo[i + HALF] = b1;
+          if (a.q_cap) {
+            float* qc = a.q_cap + ((size_t)row * a.nq + head) * HD;
+            qc[i] = __bfloat162float(b0);
+            qc[i + HALF] = __bfloat162float(b1);
+          }
+        }
+      } else if (append) {
+        const int kind = hl - G;  // 0: K, 1: V
+        unsigned char* pb = (unsigned char*)a.pool +
+                            (((size_t)pg_last * a.nkv + h) * 2 + kind) * (size_t)(16 * HD * 2) + off * HD * 2;
+        *(bf16*)(pb + (kv_swz_chunk(HD, off, i >> 3) << 4) + ((i & 7) << 1)) = b0;
+        *(bf16*)(pb + (kv_swz_chunk(HD, off, (i + HALF) >> 3) << 4) + (((i + HALF) & 7) << 1)) = b1;
+      }
+    }
+  }
+}
+
 template <int HD>
 __global__ void __launch_bounds__(kAttnWarps * 32) k_attn(AttnArgs a) {
   using C = AttnCfg<HD>;
@@ -111,101 +217,7 @@ __global__ void __launch_bounds__(kAttnWarps * 32) k_attn(AttnArgs a) {
     // ---- QKV epilogue of this (row, kv head): sum the projection's split-K partials in split
     // order, RMSNorm row scale, RoPE (rotate-half; weight rows 2i, 2i + 1 = dims i, i + hd/2),
     // bf16 q -> shared memory (+ q_out / q_cap), bf16 k / v -> the page (swizzled rows)
-    // RMSNorm row scale: every thread sums the row's per-tile sums of squares itself, in tile
-    // order; its loads are issued together with the first group's partial loads below (one
-    // L2 round trip for both), no barrier
-    constexpr int kRsMax = 64;   // per-row tiles held in registers (d_model <= 8192)
-    const float* rs = a.rs_ss + (size_t)r * a.rs_tiles;
-    const bool rs_vec = (a.rs_tiles & 3) == 0 && a.rs_tiles <= kRsMax && ((uintptr_t)rs & 15) == 0;
-    float4 rs4[kRsMax / 4];
-#pragma unroll
-    for (int i = 0; i < kRsMax / 4; ++i)
-      rs4[i] = (rs_vec && 4 * i < a.rs_tiles) ? __ldcg(reinterpret_cast<const float4*>(rs) + i)
-                                              : make_float4(0.f, 0.f, 0.f, 0.f);
-    float inv = 0.f;
-    bool have_inv = false;
-    constexpr int HALF = HD / 2;
-    constexpr int kMaxSplits = 8;  // gemm_part_splits <= 8 (cluster / pair split-K choices)
-    constexpr int PB = 3;          // pairs per thread per round trip
-    const int pos = seqlen - 1;
-    const int pg_last = ptab[pos >> 4], off = pos & 15;
-    const int n_pairs = (G + 2) * HALF;
-    const int S = a.part_splits;
-    const size_t split_stride = (size_t)a.part_ld_n * a.part_m;
-    for (int j0 = threadIdx.x; j0 < n_pairs; j0 += PB * blockDim.x) {
-      // all the split partials (and the rotations) of PB pairs in flight at once
-      float2 w[PB][kMaxSplits];
-      float cr[PB], sr[PB];
-#pragma unroll
-      for (int u = 0; u < PB; ++u) {
-        const int j = j0 + u * (int)blockDim.x;
-        const bool ok = j < n_pairs;
-        const int hl = j / HALF, i = j - hl * HALF;  // local head: q 0..G-1, then k, v
-        const int head = hl < G ? h * G + hl : (hl == G ? a.nq + h : a.nq + a.nkv + h);
-        const float* src = a.part + (size_t)r * a.part_m + (size_t)head * HD + 2 * i;
-#pragma unroll
-        for (int sp = 0; sp < kMaxSplits; ++sp)
-          w[u][sp] = (ok && sp < S) ? __ldcg(reinterpret_cast<const float2*>(src + sp * split_stride))
-                                    : make_float2(0.f, 0.f);
-        const bool rot = ok && hl <= G;  // q and k heads are rotated
-        cr[u] = rot ? __ldg(a.cos + (size_t)pos * HALF + i) : 1.f;
-        sr[u] = rot ? __ldg(a.sin + (size_t)pos * HALF + i) : 0.f;
-      }
-      if (!have_inv) {
-        float t = 0.f;
-        if (rs_vec) {
-#pragma unroll
-          for (int i = 0; i < kRsMax / 4; ++i)
-            if (4 * i < a.rs_tiles) t = (((t + rs4[i].x) + rs4[i].y) + rs4[i].z) + rs4[i].w;
-        } else {
-          for (int i = 0; i < a.rs_tiles; ++i) t += __ldcg(rs + i);
-        }
-        inv = rsqrtf(t / (float)a.d_model + 1e-5f);
-        have_inv = true;
-      }
-#pragma unroll
-      for (int u = 0; u < PB; ++u) {
-        const int j = j0 + u * (int)blockDim.x;
-        if (j >= n_pairs) break;
-        const int hl = j / HALF, i = j - hl * HALF;
-        const int head = hl < G ? h * G + hl : (hl == G ? a.nq + h : a.nq + a.nkv + h);
-        float v0 = 0.f, v1 = 0.f;  // the sum in split order
-#pragma unroll
-        for (int sp = 0; sp < kMaxSplits; ++sp)
-          if (sp < S) {
-            v0 += w[u][sp].x;
-            v1 += w[u][sp].y;
-          }
-        v0 *= inv;
-        v1 *= inv;
-        float y0 = v0, y1 = v1;
-        if (hl <= G) {
-          y0 = v0 * cr[u] - v1 * sr[u];
-          y1 = v1 * cr[u] + v0 * sr[u];
-        }
-        const bf16 b0 = __float2bfloat16_rn(y0), b1 = __float2bfloat16_rn(y1);
-        if (hl < G) {
-          s_q[hl * QLD + i] = b0;
-          s_q[hl * QLD + i + HALF] = b1;
-          if (chunk == 0) {
-            bf16* qo = a.q_out + ((size_t)r * a.nq + head) * HD;
-            qo[i] = b0;
-            qo[i + HALF] = b1;
-            if (a.q_cap) {
-              float* qc = a.q_cap + ((size_t)row * a.nq + head) * HD;
-              qc[i] = __bfloat162float(b0);
-              qc[i + HALF] = __bfloat162float(b1);
-            }
-          }
-        } else if (appends) {
-          const int kind = hl - G;  // 0: K, 1: V
-          unsigned char* pb = (unsigned char*)a.pool +
-                              (((size_t)pg_last * a.nkv + h) * 2 + kind) * (size_t)(16 * HD * 2) + off * HD * 2;
-          *(bf16*)(pb + (kv_swz_chunk(HD, off, i >> 3) << 4) + ((i & 7) << 1)) = b0;
-          *(bf16*)(pb + (kv_swz_chunk(HD, off, (i + HALF) >> 3) << 4) + (((i + HALF) & 7) << 1)) = b1;
-        }
-      }
-    }
+    fold_qkv<HD>(a, r, row, h, seqlen - 1, ptab[(seqlen - 1) >> 4], G, s_q, QLD, chunk == 0, appends);
     fence_proxy_async_global();  // the appended K / V rows are read by the bulk copies below
     __syncthreads();
   }
@@ -641,6 +653,35 @@ int64_t attn_ws_floats(int n_rows, int nq, int hd, int max_chunks) {
 // and the merge, and were never faster for >= 32 (row, head) pairs.  Below that the
 // step is latency-bound and c = ceil(64 / pairs) <= 8 chunks help (1 row x 4096:
 // 32 -> 14.5 us).  RT_ATTN_CHUNKS overrides c (tuning).
+// Prompt rows of a round whose QKV projection wrote raw partials (mixed decode + prefill
+// rounds of <= 256 rows): the same folded epilogue for every (prompt row, kv head) — q to
+// a.q_out for the prefill attention, k / v appended into the rows' pages.  CTA = (16-position
+// tile, position in the tile) x kv head over SchedParams::pf_tiles (first row, rows, first
+// position, task).  Launched after the decode attention and before the prefill attention.
+template <int HD>
+__global__ void __launch_bounds__(kAttnWarps * 32) k_qkv_finish(AttnArgs a, const int4* tiles) {
+  TraceScope tr(TK_ATTN_PREFILL | (1u << 8));
+  if (threadIdx.x == 0) pdl_trigger();
+  pdl_wait();
+  tr.ready();
+  const int4 t = tiles[blockIdx.x >> 4];
+  const int i = blockIdx.x & 15;
+  if (i >= t.y) return;
+  const int row = t.x + i, pos = t.z + i, h = blockIdx.y;
+  const int32_t* ptab = a.page_table + (size_t)t.w * a.pt_stride;
+  fold_qkv<HD>(a, row - a.row0, row, h, pos, ptab[pos >> 4], a.G, nullptr, 0, true, true);
+}
+void launch_qkv_finish(const AttnArgs& a, const int4* tiles, int n_tiles, cudaStream_t s) {
+  if (n_tiles <= 0) return;
+  const dim3 grid(16 * n_tiles, a.nkv), block(kAttnWarps * 32);
+  switch (a.hd) {
+    case 128: launch_pdl(k_qkv_finish<128>, grid, block, 0, s, a, tiles); break;
+    case 64: launch_pdl(k_qkv_finish<64>, grid, block, 0, s, a, tiles); break;
+    case 32: launch_pdl(k_qkv_finish<32>, grid, block, 0, s, a, tiles); break;
+    default: break;
+  }
+}
+
 void attn_plan(int n_rows, int nkv, int max_seqlen, int* chunk_pages, int* max_chunks) {
   const int max_pages = (max_seqlen + 15) / 16;
   const long long base = (long long)n_rows * nkv;

@@ -861,7 +861,7 @@ static rt_status forward(rt_engine* e, const HostMailbox& plan) {
     // attention runs the QKV epilogue (sum, RMSNorm scale, RoPE, KV append) for its own (row,
     // kv head) — no split-K exchange or fused epilogue on the projection's critical path
     int fold_S = (RT_QKV_FOLD && e->d_qkv_part && c.gemm_path == GEMM_PATH_AUTO &&
-                  plan.n_prefill_rows == 0 && n_rows <= e->fwd_rows && n <= e->qkv_part_rows)
+                  n_rows <= e->fwd_rows && n <= e->qkv_part_rows && plan.n_pf_tiles <= e->sp.pf_tiles_cap)
                      ? gemm_part_splits(e->qkv_dim, d, n)
                      : 0;
     if (fold_S > 8 || d / 128 > 64) fold_S = 0;  // the attention's fold holds <= 8 partials, <= 64 tiles
@@ -973,6 +973,10 @@ static rt_status forward(rt_engine* e, const HostMailbox& plan) {
         ++launches;
       }
       if (timing && row0 == 0) record_timing_event(e->ev_attn[2 * l + 1], s);
+      if (fold_S > 0 && pa.n_tiles > 0) {  // the folded QKV epilogue of the prompt rows
+        launch_qkv_finish(aa, P.pf_tiles, pa.n_tiles, s);
+        ++launches;
+      }
       if (pa.n_tiles > 0) {  // prompt rows of k = 0 admissions
         pa.pool = pool_l;
         pa.out_f32 = aa.out_f32;

@@ -72,6 +72,8 @@ struct AttnArgs {
 int64_t attn_ws_floats(int n_rows, int nq, int hd, int max_chunks);
 void attn_plan(int n_rows, int nkv, int max_seqlen, int* chunk_pages, int* max_chunks);
 void launch_attention(const AttnArgs& a, cudaStream_t s);
+// the folded QKV epilogue (a.part, ...) for the prompt rows of SchedParams::pf_tiles
+void launch_qkv_finish(const AttnArgs& a, const int4* tiles, int n_tiles, cudaStream_t s);
 
 // ---- causal prefill attention over paged KV (attn.cu): prompt rows of k = 0 admissions,
 // tiles of <= 16 consecutive positions; CTA = (tile, kv head), one warp per q head of the

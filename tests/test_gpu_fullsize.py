@@ -238,3 +238,18 @@ def test_llama8b_dims_decode_pair_splitk_vs_oracle(rt, n_dec, gemm_path):
     w_dec, _, checked = run_fullsize(rt, shape, gemm_path, n_dec=n_dec, n_tail=0, mixed=False)
     print(checked)
     assert_within(w_dec)
+
+
+@pytest.mark.parametrize("n_dec,n_tail", [(64, 2), (32, 1)])
+def test_llama8b_dims_mixed_fold_vs_oracle(rt, n_dec, n_tail):
+    """Mixed rounds of <= 256 rows (decode rows + shared-prefix prompt tails, 232 / 116 rows):
+    the QKV projection writes raw split-K partials, the decode attention runs the folded QKV
+    epilogue of the decode rows and k_qkv_finish that of the prompt rows (q for the prefill
+    attention, K/V appended); at > 128 rows O / down also write partials finished by the
+    residual reduce.  Every fused op of both layers vs the oracle on the GPU's own inputs."""
+    s8 = MODEL_SHAPES["llama3-8b"]
+    shape = ModelShape("8b-2l", 2, s8.d_model, s8.n_q_heads, s8.n_kv_heads, s8.head_dim, s8.d_ff, s8.vocab)
+    w_dec, w_mix, checked = run_fullsize(rt, shape, 0, n_dec=n_dec, n_tail=n_tail)
+    print(checked)
+    assert_within(w_dec)
+    assert_within(w_mix)
