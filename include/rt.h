@@ -222,6 +222,15 @@ rt_status rt_step(rt_engine* e, int64_t now_us, rt_round_info* info);
  * slot order within a round. */
 rt_status rt_poll_segment(rt_engine* e, rt_segment* out, int32_t cap, int32_t* n_out);
 
+/* Non-blocking rt_poll_segment: drains only the records of rounds the device has
+ * already retired (k_sched_post published them to the mapped ring), without waiting
+ * for the round in flight.  A serving loop that calls it right after rt_step overlaps
+ * its own host work (polling, submitting the next requests) with the round running on
+ * the GPU; a round's records appear here at the latest once the next rt_step has
+ * returned (that call's plan handshake follows the round's k_sched_post on the stream).
+ * Same arguments, ownership and errors as rt_poll_segment (§8(b)). */
+rt_status rt_poll_segment_ready(rt_engine* e, rt_segment* out, int32_t cap, int32_t* n_out);
+
 /* Completed summary of the last executed round (synchronises). */
 rt_status rt_last_round(rt_engine* e, rt_round_info* info);
 

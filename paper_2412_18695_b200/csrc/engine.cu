@@ -1163,14 +1163,22 @@ extern "C" rt_status rt_sync(rt_engine* e) {
   return RT_OK;
 }
 
-extern "C" rt_status rt_poll_segment(rt_engine* e, rt_segment* out, int32_t cap, int32_t* n_out) {
+// Drains the mapped segment ring up to the count k_sched_post published last.  `wait`:
+// first block until the last launched round is complete (rt_poll_segment); without it
+// (rt_poll_segment_ready) only the rounds the device has already retired are visible —
+// k_sched_post writes every record, then (after a barrier and a system-scope fence) the
+// count, so a count read here covers only complete records.
+static rt_status poll_ring(rt_engine* e, rt_segment* out, int32_t cap, int32_t* n_out, bool wait) {
   if (!e || !n_out || (cap > 0 && !out)) return RT_E_INVAL;
   if (e->sticky) return RT_E_CUDA;
   *n_out = 0;
-  rt_status st = wait_post(e);
-  if (st != RT_OK) return st;
+  if (wait) {
+    rt_status st = wait_post(e);
+    if (st != RT_OK) return st;
+  }
   const volatile HostMailbox* mb = e->h_mb;
   const int64_t published = mb->seg_written;
+  std::atomic_thread_fence(std::memory_order_acquire);
   if (published - e->seg_read > e->ring_cap) return fail(e, RT_E_STATE, "segment ring overflow (poll more often)");
   int32_t n = 0;
   while (n < cap && e->seg_read < published) {
@@ -1192,6 +1200,14 @@ extern "C" rt_status rt_poll_segment(rt_engine* e, rt_segment* out, int32_t cap,
   e->stats.segments += n;
   *n_out = n;
   return RT_OK;
+}
+
+extern "C" rt_status rt_poll_segment(rt_engine* e, rt_segment* out, int32_t cap, int32_t* n_out) {
+  return poll_ring(e, out, cap, n_out, true);
+}
+
+extern "C" rt_status rt_poll_segment_ready(rt_engine* e, rt_segment* out, int32_t cap, int32_t* n_out) {
+  return poll_ring(e, out, cap, n_out, false);
 }
 
 extern "C" rt_status rt_last_round(rt_engine* e, rt_round_info* info) {

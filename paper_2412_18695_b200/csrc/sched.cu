@@ -1241,6 +1241,10 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_post(SchedParams p) 
     }
     HostMailbox* mb = p.mb;
     mb->n_stopped = n_stop;
+    // every thread's ring records (ordered before this thread by the barrier above) become
+    // visible to the host before the count that publishes them (rt_poll_segment_ready reads
+    // the count without waiting for the round)
+    __threadfence_system();
     mb->seg_written = seg_base + n_stop;
     __threadfence_system();
   }

@@ -31,7 +31,8 @@ TRACE_DTYPE = np.dtype([("grid", "<u8"), ("kind", "<u4"), ("smid", "<u4"), ("t_e
 TRACE_KINDS = {1: "gemm", 2: "attn", 3: "norm", 4: "embed", 5: "sched_pre", 6: "sched_post", 7: "gather",
                8: "argmax", 9: "merge", 10: "attn_prefill", 11: "resid_reduce"}
 
-EXPORTED = ["rt_create", "rt_destroy", "rt_submit_request", "rt_register_prefix", "rt_step", "rt_poll_segment", "rt_last_round",
+EXPORTED = ["rt_create", "rt_destroy", "rt_submit_request", "rt_register_prefix", "rt_step", "rt_poll_segment", "rt_poll_segment_ready",
+            "rt_last_round",
             "rt_sync", "rt_get_stats", "rt_reset_stats", "rt_debug_dump", "rt_last_error", "rt_version",
             "rt_op_paged_attention", "rt_op_attention_ws_bytes", "rt_op_kv_write", "rt_op_kv_read", "rt_op_kv_swap",
             "rt_op_gemm", "rt_op_lm_argmax", "rt_op_init_weights", "rt_op_priority", "rt_mark", "rt_elapsed_ms",
@@ -110,6 +111,7 @@ def lib():
     L.rt_step.argtypes = [C.c_void_p, C.c_int64, C.POINTER(rt_round_info)]
     L.rt_register_prefix.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.POINTER(C.c_int32)]
     L.rt_poll_segment.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.POINTER(C.c_int32)]
+    L.rt_poll_segment_ready.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.POINTER(C.c_int32)]
     L.rt_last_round.argtypes = [C.c_void_p, C.POINTER(rt_round_info)]
     L.rt_sync.argtypes = [C.c_void_p]
     L.rt_get_stats.argtypes = [C.c_void_p, C.POINTER(rt_stats)]
@@ -245,7 +247,9 @@ class Engine:
         _check(lib().rt_last_round(self.h, C.byref(info)), self.h)
         return _info_dict(info)
 
-    def poll(self, cap=512):
+    def poll(self, cap=512, wait=True):
+        """rt_poll_segment (wait=True: the last launched round included) or
+        rt_poll_segment_ready (wait=False: only rounds the device has retired)."""
         # one reusable record buffer per engine (a fresh 4096-record ctypes array was 2.3 MB
         # of zeroing per call, visible in the e2e loop's host time)
         buf = getattr(self, "_pbuf", None)
@@ -254,8 +258,9 @@ class Engine:
         cap = len(buf)
         n = C.c_int32()
         out = []
+        fn = lib().rt_poll_segment if wait else lib().rt_poll_segment_ready
         while True:
-            _check(lib().rt_poll_segment(self.h, buf, cap, C.byref(n)), self.h)
+            _check(fn(self.h, buf, cap, C.byref(n)), self.h)
             for i in range(n.value):
                 s = buf[i]
                 nt = s.tok_end - s.tok_begin

@@ -89,6 +89,32 @@ def test_sched_parity_c1(rt, seed):
     assert len({s["request_id"] for s in segs if s["reason"] in (1, 2)}) == 12
 
 
+def test_poll_ready_pipelined(rt):
+    """rt_poll_segment_ready (the non-blocking drain of the pipelined serving loop, bench.py
+    e2e): after rt_step of round r returns, every record of rounds <= r - 1 is visible; what it
+    returns is always a prefix of the oracle's record sequence (round order, slot order), never
+    a partial record; the final blocking poll completes the sequence bit-exact."""
+    v = make_vocab(512)
+    p = engine_params("paper-4090", max_batch=16, max_tasks=1024, max_ctx=256, n_pages=96,
+                      max_admit_per_round=1 << 30)
+    reqs = compose_workload(64, 8.0, 16, range(1, 12), 6.0, 3, v, prompt_len_range=(20, 120), max_requests=300)
+    eng, ora = make_pair(rt, v, p)
+    submit_both(eng, ora, reqs)
+    got, want, through = [], [], [0]
+    for n in range(20000):
+        eng.step()
+        io = ora.step()
+        want += ora.poll()
+        through.append(len(want))              # records of rounds <= n
+        got += eng.poll(wait=False)
+        assert len(got) >= through[n], (n, len(got), through[n])   # rounds <= n - 1 all visible
+        assert got == want[:len(got)], n
+        if io["n_running"] == 0 and all(r.state == FINISHED for r in ora.reqs.values()):
+            break
+    got += eng.poll()
+    assert got == want and len(want) > 100
+
+
 @pytest.mark.parametrize("policy,max_admit", [(0, 1), (0, 4), (0, 1 << 30), (POLICY_FCFS, 1 << 30),
                                               (POLICY_EDF, 2)])
 def test_sched_parity_contention(rt, policy, max_admit):
