@@ -7,15 +7,19 @@
 // UMMA M slot (128 rows per tile) and the batch in N (32..256), so the weights
 // stream through HBM once per step (HBM-bound for N <~ 210).
 //
-// Split-K across a THREAD-BLOCK CLUSTER: the S CTAs of a cluster (grid.x = S, up to
-// 16 with the non-portable opt-in) stream disjoint K ranges of the same 128 x BN tile
-// into their own TMEM accumulators; each then parks its fp32 partial in its own
-// shared memory, and after one cluster barrier CTA r reduces columns
-// [r BN / S, (r+1) BN / S) across the S partials through distributed shared memory
-// (ld.shared::cluster, fixed rank order -> deterministic) and applies the fused
-// epilogue to them.  No global workspace, no atomics, and the reduction runs on all
-// S SMs in parallel.  S is chosen per shape so that S x tiles fills the 148 SMs
-// (QKV 48 tiles x 6, O / down 32 x 9, gate-up 224 x 5, lm_head 1002 x 2).
+// Split-K across a THREAD-BLOCK CLUSTER (k_gemm_tc, <= 128 rows): the S CTAs of a
+// cluster (grid.x = S, up to 16 with the non-portable opt-in) stream disjoint K ranges
+// of the same 128 x BN tile into their own TMEM accumulators; each then parks its fp32
+// partial in its own shared memory and, after one cluster barrier, PUSHES the column
+// slice every peer owns into that peer's receive slot (cp.async.bulk.shared::cluster,
+// mbarrier complete_tx); CTA r sums the S slices of its columns [r BN / S, (r+1) BN / S)
+// in fixed rank order (deterministic) and applies the fused epilogue to them.  No
+// global workspace, no atomics, the reduction runs on all S SMs in parallel.  S comes
+// from gemm_choose_splits: the largest S <= 8 with S x tiles <= 256 co-resident CTAs
+// (128 for 192/256-wide tiles) and >= 4 k-blocks per split — at the 8B decode shapes
+// QKV 48 tiles x 5, O / down 32 x 8, gate-up / lm_head (>= 148 tiles) unsplit.  EPI_PART
+// (decode QKV / O / down) skips the exchange: every split writes its
+// raw fp32 partial and the consumer (k_attn's QKV fold, k_resid_reduce) sums them.
 // CTA roles (192 threads):
 //   warp 0 lane 0 : TMA producer — weights are stored in HBM as UMMA-ready 16 KiB
 //                   SW128 tiles, so each k-block of W is ONE

@@ -67,11 +67,12 @@ __device__ __forceinline__ void publish_plan(DevState* st, HostMailbox* mb) {
 
 // Exclusive scan in place over a[0..n) (shared memory), returns the total.
 // All threads of the block must call it.
-__device__ int block_scan_excl(int* a, int n, int* wbuf) {
+__device__ __noinline__ int block_scan_excl(int* a, int n, int* wbuf) {
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, w = tid >> 5, nw = nt >> 5;
   const int per = (n + nt - 1) / nt;
   const int beg = min(tid * per, n), end = min(beg + per, n);
   int local = 0;
+  #pragma unroll 1
   for (int i = beg; i < end; ++i) local += a[i];
   int v = local;
 #pragma unroll
@@ -93,6 +94,7 @@ __device__ int block_scan_excl(int* a, int n, int* wbuf) {
   __syncthreads();
   int run = (w > 0 ? wbuf[w - 1] : 0) + v - local;
   const int total = wbuf[nw - 1];
+  #pragma unroll 1
   for (int i = beg; i < end; ++i) {
     int x = a[i];
     a[i] = run;
@@ -113,9 +115,11 @@ __global__ void k_apply_submits(SchedParams p, const SubmitRec* recs, const int3
   const SubmitRec r = recs[blockIdx.x];
   TaskTable T = p.tt;
   const int i = r.slot;
+  #pragma unroll 1
   for (int j = threadIdx.x; j < r.n_prompt; j += blockDim.x)
     T.prompt[(size_t)i * p.max_ctx + j] = toks[r.tok_off + j];
   if (r.scripted)
+    #pragma unroll 1
     for (int j = threadIdx.x; j < r.max_new; j += blockDim.x)
       T.script[(size_t)i * p.max_ctx + j] = toks[r.tok_off + r.n_prompt + j];
   if (threadIdx.x == 0) {
@@ -163,6 +167,7 @@ void launch_apply_submits(const SchedParams& p, const SubmitRec* d_recs, const i
 
 __global__ void k_init_free_stack(int32_t* stack, int n) {
   // stack[0] is the bottom; top = stack[n-1] = 0 -> pops yield 0, 1, 2, ... (AMB-14)
+  #pragma unroll 1
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
     stack[i] = n - 1 - i;
 }
@@ -246,7 +251,9 @@ __device__ void sort_keys_small(PreSmem& S, int n, int n_pad, bool pud) {
   int* xi = S.cnt_a;                                                     // [2][blockDim.x]
   const int nt = blockDim.x;
   int buf = 0;
+  #pragma unroll 1
   for (int kk = 2; kk <= n_pad; kk <<= 1) {
+    #pragma unroll 1
     for (int j = kk >> 1; j > 0; j >>= 1) {
       SortKey o;
       if (j >= 32) {
@@ -291,34 +298,48 @@ __device__ void sort_keys_small(PreSmem& S, int n, int n_pad, bool pud) {
 // Rank sort for few candidates (n <= 128, the usual waiting queue): candidate i goes to
 // position #{j : key_j < key_i} (keys unique by index), one pass over the keys in shared
 // memory (broadcast reads), no compare-exchange network.  Same keys as sort_keys_small.
+// g = min(32, blockDim / n) (a power of two) threads share a candidate: lane `sub` of the
+// group counts the keys j = sub, sub + g, ... and the group sums by shuffles, so the serial
+// pass is n / g keys long (C3: 90 candidates, 8 lanes each: 12 keys instead of 90).
 __device__ void sort_keys_rank(PreSmem& S, int n, bool pud) {
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, nt = blockDim.x;
   unsigned long long* K = reinterpret_cast<unsigned long long*>(S.cnt_a);  // [4][n] (cnt_a, cnt_b)
-  SortKey me;
-  if (tid < n) {
-    me.k0 = pud ? desc_key_f64(S.a0[tid]) : 0ull;
-    me.k1 = enc_i64(S.a1[tid]);
-    me.k2 = enc_i64(S.a2[tid]);
-    me.k3 = enc_i64(S.a3[tid]);
-    me.ix = tid;
-    K[tid] = me.k0;
-    K[n + tid] = me.k1;
-    K[2 * n + tid] = me.k2;
-    K[3 * n + tid] = me.k3;
+#pragma unroll 1
+  for (int i = tid; i < n; i += nt) {
+    K[i] = pud ? desc_key_f64(S.a0[i]) : 0ull;
+    K[n + i] = enc_i64(S.a1[i]);
+    K[2 * n + i] = enc_i64(S.a2[i]);
+    K[3 * n + i] = enc_i64(S.a3[i]);
   }
   __syncthreads();
-  if (tid < n) {
-    int r = 0;
-#pragma unroll 4
-    for (int j = 0; j < n; ++j) {
-      const unsigned long long a0 = K[j], a1 = K[n + j], a2 = K[2 * n + j], a3 = K[3 * n + j];
-      // key_j < key_me, lexicographic, without branches (index j breaks ties)
-      const bool lt = a0 < me.k0 ||
-                      (a0 == me.k0 && (a1 < me.k1 || (a1 == me.k1 && (a2 < me.k2 || (a2 == me.k2 &&
-                                                                   (a3 < me.k3 || (a3 == me.k3 && j < tid)))))));
-      r += lt ? 1 : 0;
+  int g = 1;
+  while (g < 32 && 2 * g * n <= nt) g <<= 1;
+  const int e = tid / g, sub = tid & (g - 1);
+  if (e * g < nt && (tid >> 5) * 32 < min(n * g, nt)) {  // warps that hold a candidate (whole warps: shuffles)
+    const bool act = e < n;
+    unsigned long long m0 = 0, m1 = 0, m2 = 0, m3 = 0;
+    if (act) {
+      m0 = K[e];
+      m1 = K[n + e];
+      m2 = K[2 * n + e];
+      m3 = K[3 * n + e];
     }
-    S.perm[r] = tid;
+    int r = 0;
+    if (act) {
+#pragma unroll 2
+      for (int j = sub; j < n; j += g) {
+        const unsigned long long a0 = K[j], a1 = K[n + j], a2 = K[2 * n + j], a3 = K[3 * n + j];
+        // key_j < key_e, lexicographic, without branches (index j breaks ties)
+        const bool lt = a0 < m0 ||
+                        (a0 == m0 && (a1 < m1 || (a1 == m1 && (a2 < m2 || (a2 == m2 &&
+                                                                (a3 < m3 || (a3 == m3 && j < e)))))));
+        r += lt ? 1 : 0;
+      }
+    }
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1)
+      if (o < g) r += __shfl_xor_sync(0xffffffffu, r, o);
+    if (act && sub == 0) S.perm[r] = e;
   }
   __syncthreads();
 }
@@ -368,6 +389,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
   int64_t t = s_t;
 
   // ---- (1) ingest arrivals <= t
+  #pragma unroll 1
   for (int i = tid; i < p.max_tasks; i += nt) {
     int sti = T.state[i];
     if (sti == T_PENDING && T.arrival[i] <= t) {
@@ -388,6 +410,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
         s_t = t;
         st->t = t;
       }
+      #pragma unroll 1
       for (int i = tid; i < p.max_tasks; i += nt) {
         if (T.state[i] == T_PENDING && T.arrival[i] <= t) {
           T.state[i] = T_WAITING;
@@ -424,6 +447,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
         mb->n_swap_ev = 0;
         mb->n_evicted = 0;
         mb->n_restored = 0;
+        #pragma unroll 1
         for (int j = 0; j < kTopK; ++j) {
           p.cand[j * 4 + 0] = -INFINITY;
           p.cand[j * 4 + 2] = -1.0;
@@ -435,19 +459,26 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
     }
   }
 
-  // ---- (2) score every waiting task (Eq. 4 recomputed before fetching)
+  // ---- (2) score every waiting task (Eq. 4 recomputed before fetching), and
+  // the outstanding reservations sum_active (R - held) (AMB-26) in the same pass.  Every
+  // field is loaded before the state test, so a task's loads are one round trip in flight
+  // together instead of a state load followed by dependent field loads.
   if (tid == 0) s_nc = 0;
   __syncthreads();
+  int my_out = 0;
+#pragma unroll 1
   for (int i = tid; i < p.max_tasks; i += nt) {
-    if (T.state[i] != T_WAITING) continue;
+    const int sti = T.state[i], hold = T.holder[i], Ri = T.R[i], npg = T.n_pages[i], npf = T.n_pfx[i];
+    const int evi = T.evicted[i], k = T.k[i];
+    const int64_t arr = T.arrival[i], rid = T.rid[i], ref = T.ref[i], Di = T.D[i], ert = T.ert[i];
+    const double al = T.alpha[i], be = T.beta[i];
+    if (hold) my_out += Ri - npg;
+    if (sti != T_WAITING) continue;
     const int pos = atomicAdd(&s_nc, 1);
-    const int64_t arr = T.arrival[i], rid = T.rid[i];
-    const int k = T.k[i];
     double a0 = 0.0;
     long long a1, a2, a3 = 0;
     if (p.policy == 0) {  // PUD (the paper's)
-      a0 = priority_d(t, k, T.ref[i], T.D[i], T.ert[i], T.alpha[i], T.beta[i], p.g_us, p.net_us,
-                      p.eps_l_us);
+      a0 = priority_d(t, k, ref, Di, ert, al, be, p.g_us, p.net_us, p.eps_l_us);
       T.pri[i] = a0;
       a1 = arr;
       a2 = rid;
@@ -455,7 +486,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
       a1 = arr;
       a2 = rid;
     } else {  // EDF on the initial deadline
-      a1 = arr + T.ert[i];
+      a1 = arr + ert;
       a2 = arr;
       a3 = rid;
     }
@@ -465,14 +496,10 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
     S.a3[pos] = a3;
     S.cslot[pos] = i;
     S.ck[pos] = k;
-    S.cR[pos] = T.R[i] - T.n_pfx[i];  // own pages (a shared prefix is already resident)
+    S.cR[pos] = Ri - npf;  // own pages (a shared prefix is already resident)
     S.evn[pos] = 0;
-    S.evc[pos] = T.evicted[i];
+    S.evc[pos] = evi;
   }
-  // outstanding reservations sum_active (R - held)  (AMB-26)
-  int my_out = 0;
-  for (int i = tid; i < p.max_tasks; i += nt)
-    if (T.holder[i]) my_out += T.R[i] - T.n_pages[i];
   if (my_out) atomicAdd(&s_outstanding, my_out);
   __syncthreads();
   PRE_MARK(2);
@@ -487,13 +514,17 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
   } else if (n_pad <= nt) {
     sort_keys_small(S, n, n_pad, p.policy == 0);
   } else {
+    #pragma unroll 1
     for (int i = tid; i < n_pad; i += nt) S.perm[i] = i;
     __syncthreads();
     // bitonic sort of perm by key.  Compare-exchange distances j >= 32 go through shared memory
     // with a barrier per stage; j < 32 partners sit in the same warp, so those stages run on
     // registers with shuffles (one barrier per kk instead of five): the same network
+    #pragma unroll 1
     for (int kk = 2; kk <= n_pad; kk <<= 1) {
+      #pragma unroll 1
       for (int j = kk >> 1; j >= 32; j >>= 1) {
+        #pragma unroll 1
         for (int i = tid; i < n_pad; i += nt) {
           const int ixj = i ^ j;
           if (ixj > i) {
@@ -508,10 +539,12 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
         }
         __syncthreads();
       }
+      #pragma unroll 1
       for (int base = 0; base < n_pad; base += nt) {  // every lane takes part in the shuffles
         const int i = base + tid;
         int x = i < n_pad ? S.perm[i] : n_pad;  // index >= n: sorts last, never read
         const bool up = ((i & kk) == 0);
+        #pragma unroll 1
         for (int j = min(kk >> 1, 16); j > 0; j >>= 1) {
           const int y = __shfl_xor_sync(0xffffffffu, x, j);
           // lower position: takes the partner when it goes first; upper: the mirror
@@ -549,6 +582,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
   {
     long long best_bud = LLONG_MAX, best_rid = LLONG_MAX;
     int best_seg = 0;
+    #pragma unroll 1
     for (int s = tid; s < n_run; s += nt) {
       const int task = p.slot_task[s];
       const long long bud = T.D[task] - t;
@@ -560,6 +594,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
       }
     }
     auto warp_min = [&](long long& b, long long& r, int& sg) {
+      #pragma unroll 1
       for (int o = 16; o > 0; o >>= 1) {
         const long long ob = __shfl_xor_sync(0xffffffffu, b, o);
         const long long orid = __shfl_xor_sync(0xffffffffu, r, o);
@@ -588,6 +623,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
         const int nh = min(p.speed_window, st->hist_n);
         if (best_bud != LLONG_MAX && nh > 0 && !p.wcet_off) {
           long long sum = 0;
+          #pragma unroll 1
           for (int j = 1; j <= nh; ++j) sum += st->hist[(st->hist_pos - j + 8) & 7];
           const long long rem = max(0, p.max_seg_tokens - best_seg);
           gate = (rem * sum <= (long long)nh * best_bud) ? 1 : 0;
@@ -615,12 +651,14 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
     const int cap = max(0, min(p.max_admit, p.max_batch - n_run));
     const bool gate = s_gate_ok != 0;
     if (tid == 0) s_nc = (cap > 0) ? n : 0;  // c_stop (the serial loop's last iteration + 1)
+    #pragma unroll 1
     for (int c = tid; c < n; c += nt) {
       const int x = S.perm[c];
       S.cnt_a[c] = (S.ck[x] == 0 || S.evc[x]) ? S.cR[x] : 0;  // reservation pages needed
     }
     __syncthreads();
     block_scan_excl(S.cnt_a, n, wbuf);  // pages of the memory-needing candidates before c
+    #pragma unroll 1
     for (int c = tid; c < n; c += nt) {
       const int x = S.perm[c];
       const bool memc = S.ck[x] == 0 || S.evc[x];
@@ -628,10 +666,12 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
     }
     __syncthreads();
     // (cnt_b is rewritten in place by the scan: keep each candidate's admissibility first)
+    #pragma unroll 1
     for (int c = tid; c < n; c += nt) S.sflag[c] = S.cnt_b[c];
     __syncthreads();
     const int tot_ok = block_scan_excl(S.cnt_b, n, wbuf);
     int my_rmem = 0;
+    #pragma unroll 1
     for (int c = tid; c < n; c += nt) {
       const int x = S.perm[c];
       const int rank = S.cnt_b[c];
@@ -643,6 +683,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
     }
     __syncthreads();
     const int c_stop = s_nc;
+    #pragma unroll 1
     for (int c = tid; c < c_stop; c += nt) my_rmem += S.sflag[c] ? 0 : 1;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) my_rmem += __shfl_xor_sync(0xffffffffu, my_rmem, o);
@@ -662,6 +703,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
     int havail = p.host_pages > 0 ? st->hfree_top : 0;
     int nadm = 0, rmem = 0, rwcet = 0, nvic = 0;
     bool mem_blocked = false;
+    #pragma unroll 1
     for (int c = 0; c < n; ++c) {
       if (nadm >= p.max_admit) break;
       if (n_run + nadm >= p.max_batch) break;
@@ -679,6 +721,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
         if (!mem_blocked && avail < need && p.host_pages > 0) {
           long long gain = 0;
           int hneed = 0, nv = 0;
+          #pragma unroll 1
           for (int cj = n - 1; cj > c && avail + gain < need; --cj) {
             const int y = S.perm[cj];
             const int vt = S.cslot[y];
@@ -691,6 +734,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
             }
           }
           if (avail + gain >= need) {
+            #pragma unroll 1
             for (int v = 0; v < nv; ++v) {
               const int y = S.cnt_b[v];
               S.evn[y] = 1;
@@ -717,11 +761,13 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
     // evictions: own pages -> host pages (host pops in page-table order), device pages
     // pushed back in reverse page-table order, victims in eviction order
     int ftop = st->free_top, htop = st->hfree_top, nsw = 0;
+    #pragma unroll 1
     for (int v = 0; v < nvic; ++v) {
       const int vt = S.vic[v];
       const int npf = T.n_pfx[vt], own = T.n_pages[vt] - npf;
       int32_t* pt = T.page_table + (size_t)vt * p.pt_stride;
       int32_t* hpt = T.hpage_table + (size_t)vt * p.pt_stride;
+      #pragma unroll 1
       for (int m = 0; m < own; ++m) {
         const int hp = p.hfree_stack[htop - 1 - m];
         hpt[m] = hp;
@@ -729,6 +775,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
         ++nsw;
       }
       htop -= own;
+      #pragma unroll 1
       for (int m = 0; m < own; ++m) p.free_stack[ftop + m] = pt[npf + own - 1 - m];
       ftop += own;
       T.n_hpages[vt] = own;
@@ -747,6 +794,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
   const int B = n_run + nadm;
 
   // ---- (4) batch assembly: running slots keep their order, admissions appended
+  #pragma unroll 1
   for (int j = tid; j < nadm; j += nt) {
     const int task = S.adm[j];
     const int x = S.admx[j];
@@ -762,6 +810,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
       atomicAdd(&s_npf, 1);
     }
   }
+  #pragma unroll 1
   for (int s = tid; s < n_run; s += nt) {
     p.slot_is_prefill[s] = 0;
     S.sflag[s] = 0;
@@ -772,12 +821,14 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
   // (admission order, each in reverse order) after this round's eviction pops
   if (tid == 0) {
     int htop = st->hfree_top, nrest = 0;
+    #pragma unroll 1
     for (int j = 0; j < nadm && p.host_pages > 0; ++j) {
       const int task = S.adm[j];
       if (S.sflag[n_run + j] != 2) continue;
       ++nrest;
       const int nh = T.n_hpages[task];
       const int32_t* hpt = T.hpage_table + (size_t)task * p.pt_stride;
+      #pragma unroll 1
       for (int m = 0; m < nh; ++m) p.hfree_stack[htop + m] = hpt[nh - 1 - m];
       htop += nh;
     }
@@ -787,6 +838,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
   __syncthreads();
   PRE_MARK(6);
   // page pops: prefill admissions (admission order) first, then decode slots in slot order
+  #pragma unroll 1
   for (int s = tid; s < B; s += nt) {
     const int task = p.slot_task[s];
     p.round_slots[s] = task;
@@ -802,6 +854,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
   const int tot_a = block_scan_excl(S.cnt_a, B, wbuf);
   const int tot_b = block_scan_excl(S.cnt_b, B, wbuf);
   const int top = s_ftop;
+  #pragma unroll 1
   for (int s = tid; s < B; s += nt) {
     const int task = p.slot_task[s];
     int32_t* pt = T.page_table + (size_t)task * p.pt_stride;
@@ -809,7 +862,9 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
       const int npg = ceil_div_i(T.n_prompt[task], p.page_tokens);
       const int npf = T.n_pfx[task];
       const int32_t* pp = p.pfx_pages + (size_t)max(T.pfx[task], 0) * p.pt_stride;
+      #pragma unroll 1
       for (int m = 0; m < npf; ++m) pt[m] = pp[m];  // shared prefix pages, read-only
+      #pragma unroll 1
       for (int m = 0; m < npg - npf; ++m) {
         const int q = S.cnt_a[s] + m;
         const int pg = p.free_stack[top - 1 - q];
@@ -821,6 +876,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
     } else {
       if (S.sflag[s] == 2) {  // restore: own pages re-popped, KV from host
         const int npf = T.n_pfx[task], nh = T.n_hpages[task];
+        #pragma unroll 1
         for (int m = 0; m < nh; ++m) {
           const int q = S.cnt_a[s] + m;
           const int pg = p.free_stack[top - 1 - q];
@@ -845,12 +901,14 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
   // restore copy list (after the evictions', in admission order) and restored state
   if (tid == 0 && p.host_pages > 0) {
     int nsw = s_nswap;
+    #pragma unroll 1
     for (int s = n_run; s < B; ++s) {
       const int task = p.slot_task[s];
       if (S.sflag[s] != 2) continue;
       const int npf = T.n_pfx[task], nh = T.n_hpages[task];
       const int32_t* pt = T.page_table + (size_t)task * p.pt_stride;
       const int32_t* hpt = T.hpage_table + (size_t)task * p.pt_stride;
+      #pragma unroll 1
       for (int m = 0; m < nh; ++m) {
         if (nsw < p.swap_cap) p.swap[nsw] = make_int4(1, task, pt[npf + m], hpt[m]);
         ++nsw;
@@ -865,7 +923,9 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
   PRE_MARK(7);
   // forward rows: prefill slot -> n_prompt rows, decode slot -> 1 row (AMB-13)
   constexpr int NB = 1024;  // decode-row buckets (page counts), filled by the rows loop
+  #pragma unroll 1
   for (int i = tid; i < NB; i += nt) S.ck[i] = 0;
+  #pragma unroll 1
   for (int s = tid; s < B; s += nt) {
     const int task = p.slot_task[s];
     S.cnt_a[s] = S.sflag[s] == 1 ? T.n_prompt[task] - p.page_tokens * T.n_pfx[task] : 1;
@@ -878,6 +938,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
     // per warp (64-bit shared atomicAdd is a CAS spin loop, ~20 us at 256 contending slots)
     unsigned long long l_prompt = 0, l_attn = 0, l_ctx = 0;
     int l_max = 0;
+    #pragma unroll 1
     for (int s = tid; s < B; s += nt) {
       const int task = p.slot_task[s];
       const int off = S.cnt_a[s];
@@ -922,6 +983,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
   // prefill rows filled slot by slot, all threads in parallel; the prompt is cut into
   // 16-position attention tiles (page-aligned: the prompt starts at position 0)
   int n_pf_tiles = 0;
+  #pragma unroll 1
   for (int s = n_run; s < B && s_npf > 0; ++s) {  // (resume-only rounds skip the walk)
     if (S.sflag[s] != 1) continue;
     const int task = p.slot_task[s];
@@ -929,12 +991,14 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
     const int P = T.n_prompt[task];
     const int Lp = p.page_tokens * T.n_pfx[task];  // rows start after the shared prefix
     const int32_t* pr = T.prompt + (size_t)task * p.max_ctx;
+    #pragma unroll 1
     for (int j = tid; j < P - Lp; j += nt) {
       p.row_task[off + j] = task;
       p.row_pos[off + j] = Lp + j;
       p.row_tok[off + j] = pr[Lp + j];
     }
     const int nt16 = (P - Lp + 15) >> 4;
+    #pragma unroll 1
     for (int t16 = tid; t16 < nt16; t16 += nt)
       if (n_pf_tiles + t16 < p.pf_tiles_cap)
         p.pf_tiles[n_pf_tiles + t16] =
@@ -950,6 +1014,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
   {
     __syncthreads();  // buckets counted by the rows loop
     const int ndec = block_scan_excl(S.ck, NB, wbuf);
+    #pragma unroll 1
     for (int s = tid; s < B; s += nt)
       if (S.sflag[s] != 1) p.dec_rows[atomicAdd(&S.ck[S.cR[s]], 1)] = S.cnt_a[s];
     if (tid == 0) s_ndec = ndec;
