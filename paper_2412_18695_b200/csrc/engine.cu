@@ -686,7 +686,7 @@ extern "C" rt_status rt_submit_request(rt_engine* e, int32_t agent_id, const int
   return RT_OK;
 }
 
-static rt_status forward(rt_engine* e, const HostMailbox& plan);
+static rt_status forward(rt_engine* e, const HostMailbox& plan, bool embed0_done = false);
 
 // ------------------------------------------------------------ shared prefixes
 // NEXT-1 (fixed prompt components pre-stored on the server): the prefix's pages are
@@ -791,7 +791,7 @@ static void record_timing_event(cudaEvent_t ev, cudaStream_t s) { cudaEventRecor
 #ifndef RT_RESID_PART
 #define RT_RESID_PART 1
 #endif
-static rt_status forward(rt_engine* e, const HostMailbox& plan) {
+static rt_status forward(rt_engine* e, const HostMailbox& plan, bool embed0_done) {
   const rt_config& c = e->cfg;
   const int d = c.d_model, hd = c.head_dim, nq = c.n_q_heads, nkv = c.n_kv_heads, ff = c.d_ff, V = c.vocab;
   const int B = plan.B, n_rows = plan.n_rows;
@@ -811,8 +811,10 @@ static rt_status forward(rt_engine* e, const HostMailbox& plan) {
   };
   for (int row0 = 0; row0 < n_rows; row0 += e->fwd_rows) {
     const int n = std::min(e->fwd_rows, n_rows - row0);
-    launch_embed(P.row_tok, row0, n, e->emb, d, e->d_x, e->d_h, e->d_ss, s);  // d_h = bf16(x), un-normed
-    ++launches;
+    if (!(row0 == 0 && embed0_done)) {  // chunk 0 of a scheduler round: k_embed_plan (rt_step)
+      launch_embed(P.row_tok, row0, n, e->emb, d, e->d_x, e->d_h, e->d_ss, s);  // d_h = bf16(x), un-normed
+      ++launches;
+    }
     AttnArgs aa{};
     aa.q = e->d_q;
     aa.page_table = e->tt.page_table;
@@ -1063,6 +1065,14 @@ extern "C" rt_status rt_step(rt_engine* e, int64_t now_us, rt_round_info* info) 
   const int64_t seq0 = mb->plan_seq;
   launch_sched_pre(e->sp, now_us, s);
   if (timing) cudaEventRecord(e->ev_s1, s);
+  // the first chunk's embedding goes in right behind the scheduler, before the handshake: it
+  // reads the row count from the device state, so it runs while the host spins on the plan
+  // and launches the layers (hides the plan handshake behind the embedding)
+  const bool embed0 = !(c.flags & RT_FLAG_NO_MODEL);
+  if (embed0) {
+    launch_embed_plan(e->sp.row_tok, &e->d_st->n_rows, e->fwd_rows, e->emb, c.d_model, e->d_x, e->d_h, e->d_ss, s);
+    e->stats.kernel_launches++;
+  }
   CK(e, cudaGetLastError());
   // plan handshake: spin on the sequence number k_sched_pre writes last into the mapped
   // mailbox (an event record + synchronize cost ~5 us more per round); the stream is polled
@@ -1120,7 +1130,7 @@ extern "C" rt_status rt_step(rt_engine* e, int64_t now_us, rt_round_info* info) 
   }
   if (timing) cudaEventRecord(e->ev_f0, s);
   if (!(c.flags & RT_FLAG_NO_MODEL)) {
-    st = forward(e, plan);
+    st = forward(e, plan, embed0);
     if (st != RT_OK) return st;
   }
   if (timing) {

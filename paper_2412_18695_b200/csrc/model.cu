@@ -8,6 +8,7 @@
 // fp32.
 #include "common.cuh"
 #include "model.h"
+#include <algorithm>
 
 namespace rt {
 
@@ -158,6 +159,39 @@ __global__ void k_embed(const int32_t* row_tok, int32_t row0, const bf16* emb, i
     }
     sq = warp_sum(sq);
     if (lane == 0) ss[(size_t)r * n_tiles + t] = sq;
+  }
+}
+
+// The same embedding for the first forward chunk of a scheduler round, launched right behind
+// k_sched_pre BEFORE the host has read the plan: the row count comes from the device state
+// the scheduler writes (min(*n_rows, fwd_rows)), rows in a grid-stride loop, so the launch
+// does not depend on the plan and the embedding runs while the host completes the plan
+// handshake and launches the layers (rt_step).
+__global__ void k_embed_plan(const int32_t* row_tok, const int32_t* n_rows_dev, int fwd_rows, const bf16* emb,
+                             int d, int n_tiles, float* x, bf16* xb, float* ss) {
+  TraceScope tr(TK_EMBED);
+  if (threadIdx.x == 0) pdl_trigger();
+  pdl_wait();  // row_tok and the row count come from the scheduler kernel
+  tr.ready();
+  const int n = min(*n_rows_dev, fwd_rows);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int r = blockIdx.x; r < n; r += gridDim.x) {
+    const int tok = row_tok[r];
+    const bf16* e = emb + (size_t)tok * d;
+    float* xr = x + (size_t)r * d;
+    bf16* hr = xb + (size_t)r * d;
+    for (int t = warp; t < n_tiles; t += nw) {
+      float sq = 0.f;
+      for (int i = t * 128 + lane; i < min(d, t * 128 + 128); i += 32) {
+        const bf16 b = e[i];
+        const float v = __bfloat162float(b);
+        xr[i] = v;
+        hr[i] = b;
+        sq += v * v;
+      }
+      sq = warp_sum(sq);
+      if (lane == 0) ss[(size_t)r * n_tiles + t] = sq;
+    }
   }
 }
 
@@ -326,6 +360,11 @@ __global__ void k_kv_read(const unsigned char* pool, bf16* out, int nkv, int hd)
 void launch_embed(const int32_t* row_tok, int row0, int n, const bf16* emb, int d, float* x, bf16* xb, float* ss,
                   cudaStream_t s) {
   launch_pdl(k_embed, dim3(n), dim3(256), 0, s, row_tok, row0, emb, d, (d + 127) / 128, x, xb, ss);
+}
+void launch_embed_plan(const int32_t* row_tok, const int32_t* n_rows_dev, int fwd_rows, const bf16* emb, int d,
+                       float* x, bf16* xb, float* ss, cudaStream_t s) {
+  launch_pdl(k_embed_plan, dim3(std::min(fwd_rows, 296)), dim3(256), 0, s, row_tok, n_rows_dev, fwd_rows, emb, d,
+             (d + 127) / 128, x, xb, ss);
 }
 void launch_gather_norm(const int32_t* slot_row, int B, int row0, int n, const float* x, const float* ss, int d,
                         bf16* hfin, cudaStream_t s) {

@@ -22,6 +22,9 @@ inline int64_t tiled_elems(int M, int K) { return (int64_t)((M + 127) / 128) * 1
 // x = emb[tok] (fp32), xb = bf16(x), ss [n][ceil(d/128)] per-tile sums of squares of x
 void launch_embed(const int32_t* row_tok, int row0, int n, const bf16* emb, int d, float* x, bf16* xb, float* ss,
                   cudaStream_t s);
+// first-chunk embedding launched before the plan handshake (row count read on the device)
+void launch_embed_plan(const int32_t* row_tok, const int32_t* n_rows_dev, int fwd_rows, const bf16* emb, int d,
+                       float* x, bf16* xb, float* ss, cudaStream_t s);
 // hfin[s] = bf16(RMSNorm(x[slot_row[s] - row0])) from x fp32 and its ss partials
 void launch_gather_norm(const int32_t* slot_row, int B, int row0, int n, const float* x, const float* ss, int d,
                         bf16* hfin, cudaStream_t s);
