@@ -67,7 +67,7 @@ __device__ __forceinline__ void publish_plan(DevState* st, HostMailbox* mb) {
 
 // Exclusive scan in place over a[0..n) (shared memory), returns the total.
 // All threads of the block must call it.
-__device__ __noinline__ int block_scan_excl(int* a, int n, int* wbuf) {
+__device__ __forceinline__ int block_scan_excl_inl(int* a, int n, int* wbuf) {
   const int tid = threadIdx.x, nt = blockDim.x, lane = tid & 31, w = tid >> 5, nw = nt >> 5;
   const int per = (n + nt - 1) / nt;
   const int beg = min(tid * per, n), end = min(beg + per, n);
@@ -103,6 +103,9 @@ __device__ __noinline__ int block_scan_excl(int* a, int n, int* wbuf) {
   __syncthreads();
   return total;
 }
+// k_sched_pre calls the scan at ten sites: one out-of-line copy keeps its (cold, once per
+// round) code small; k_sched_post keeps the inlined form (measured faster there)
+__device__ __noinline__ int block_scan_excl(int* a, int n, int* wbuf) { return block_scan_excl_inl(a, n, wbuf); }
 
 __device__ void hist_push(DevState* st, int64_t v) {
   st->hist[st->hist_pos] = v;
@@ -358,6 +361,9 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_pre(SchedParams p, i
   __shared__ long long s_pm[10];  // clock64 phase marks (RT_FLAG_TRACE)
 #define PRE_MARK(i) \
   if (threadIdx.x == 0) s_pm[i] = clock64()
+  pdl_wait();  // launched with PDL: every read of the task table / state follows the wait
+  tr.ready();
+  if (threadIdx.x == 0) pdl_trigger();
   PRE_MARK(0);
 
   TaskTable T = p.tt;
@@ -1112,7 +1118,8 @@ void launch_sched_pre(const SchedParams& p, int64_t now_us, cudaStream_t s) {
     cudaFuncSetAttribute(k_sched_pre, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PreSmem));
     attr = true;
   }
-  k_sched_pre<<<1, kSchedThreads, sizeof(PreSmem), s>>>(p, now_us);
+  // programmatic dependent launch: resident while k_sched_post finishes, waits in pdl_wait()
+  launch_pdl(k_sched_pre, dim3(1), dim3(kSchedThreads), sizeof(PreSmem), s, p, now_us);
 }
 
 // -------------------------------------------------------------- sched_post
@@ -1127,6 +1134,11 @@ struct PostSmem {
 
 __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_post(SchedParams p) {
   TraceScope tr(TK_SCHED_POST);
+  // launched with PDL behind k_argmax_reduce: nothing is read before the wait; the trigger
+  // lets the next round's k_sched_pre become resident (it waits for this kernel's completion)
+  pdl_wait();
+  tr.ready();
+  if (threadIdx.x == 0) pdl_trigger();
   extern __shared__ __align__(16) unsigned char dsm[];
   PostSmem& S = *reinterpret_cast<PostSmem*>(dsm);
   __shared__ int wbuf[32];
@@ -1214,8 +1226,8 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_post(SchedParams p) 
     S.keep_task[s] = task;
   }
   __syncthreads();
-  const int n_stop = block_scan_excl(S.stop_off, B, wbuf);
-  const int n_keep = block_scan_excl(S.keep_off, B, wbuf);
+  const int n_stop = block_scan_excl_inl(S.stop_off, B, wbuf);
+  const int n_keep = block_scan_excl_inl(S.keep_off, B, wbuf);
   const int64_t seg_base = st->seg_written;
 
   // ---- (7) segment records + retire (a10)
@@ -1283,7 +1295,7 @@ __global__ void __launch_bounds__(kSchedThreads, 1) k_sched_post(SchedParams p) 
   __syncthreads();
   for (int f = tid; f < nfin; f += nt) S.fin_off[f] = T.n_pages[S.fin[f]] - T.n_pfx[S.fin[f]];  // own pages
   __syncthreads();
-  const int n_push = block_scan_excl(S.fin_off, nfin, wbuf);
+  const int n_push = block_scan_excl_inl(S.fin_off, nfin, wbuf);
   const int top = st->free_top;
   for (int f = tid; f < nfin; f += nt) {
     const int task = S.fin[f];
@@ -1321,7 +1333,7 @@ void launch_sched_post(const SchedParams& p, cudaStream_t s) {
     cudaFuncSetAttribute(k_sched_post, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(PostSmem));
     attr = true;
   }
-  k_sched_post<<<1, kSchedThreads, sizeof(PostSmem), s>>>(p);
+  launch_pdl(k_sched_post, dim3(1), dim3(kSchedThreads), sizeof(PostSmem), s, p);
 }
 
 // ------------------------------------------------ multi-GPU candidate merge (a12)

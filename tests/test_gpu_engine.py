@@ -319,6 +319,35 @@ def test_submit_errors(rt):
 
 
 # ------------------------------------------------------------- model parity
+def test_tiny_model_chunked_forward(rt):
+    """Prefill rounds larger than one forward chunk (max_rows_per_forward = 48: the 4 x 40-64
+    prompt rows of the first rounds run as 3-6 chunks): chunk 0's embedding is the one launched
+    before the plan handshake (k_embed_plan, row count read on the device), the others the
+    per-chunk k_embed; logits end to end vs the oracle and bit-exact segments."""
+    shape = MODEL_SHAPES["tiny"]
+    v = make_vocab(shape.vocab)
+    p = engine_params("paper-4090", max_batch=4, max_tasks=64, max_ctx=256, n_pages=64)
+    reqs = compose_workload(4, 1.0, 2, range(1, 9), 30.0, 4, v, prompt_len_range=(40, 64), max_requests=12)
+    eng, ora = make_pair(rt, v, p, shape=shape, seed=5, flags=rt.RT_FLAG_KEEP_LOGITS, model=True,
+                         max_rows_per_forward=48)
+    submit_both(eng, ora, reqs)
+    worst, chunked = 0.0, 0
+    for n in range(400):
+        ig, io = eng.step(), ora.step()
+        assert ig["n_running"] == io["n_running"] and ig["n_rows"] == io.get("n_rows", ig["n_rows"])
+        chunked += ig["n_rows"] > 48
+        if io["n_running"] == 0:
+            if all(r.state == FINISHED for r in ora.reqs.values()):
+                break
+            continue
+        lg = eng.dump(rt.RT_DUMP_LOGITS, np.float32).reshape(io["n_running"], -1)
+        lo = np.stack([ora.round_log[-1]["logits"][rid] for rid in ora.round_log[-1]["slots"]])
+        worst = max(worst, float(np.abs(lg - lo).max()))
+    assert chunked > 0
+    assert eng.poll() == ora.poll()
+    assert worst <= 1e-2, worst
+
+
 @pytest.mark.parametrize("gemm_path", [0, 1, 2, 3])
 def test_tiny_model_e2e_and_per_op(rt, gemm_path):
     """C1 end to end against the oracle, through every projection kernel path (rt_config.gemm_path:
