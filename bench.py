@@ -73,7 +73,10 @@ def agent_request(workload, vocab, agent, ordinal, seed, plan_len=None, prefixes
 
 
 def ncu_traffic(kernel):
-    """dram__bytes_read + write per launch of `kernel` from the committed ncu capture."""
+    """(dram__bytes_read + write, algorithmic bytes) of the launch of `kernel` in the committed
+    ncu capture; the capture's own algorithmic bytes (its round's attended tokens, printed by
+    tools/profile_step.py) make traffic / algorithmic comparable even though that round's
+    context mix is not the timed rounds' one."""
     try:
         for d in json.load(open(os.path.join(ROOT, NCU_ATTN_SOURCE.split()[0]))):
             if kernel in d["Kernel Name"]:
@@ -82,10 +85,11 @@ def ncu_traffic(kernel):
                 def val(key):
                     v, u = d[key].split()[:2]
                     return float(v) * unit[u]
-                return val("dram__bytes_read.sum") + val("dram__bytes_write.sum")
+                return (val("dram__bytes_read.sum") + val("dram__bytes_write.sum"),
+                        d.get("alg_bytes_per_launch"))
     except Exception:
-        return None
-    return None
+        return None, None
+    return None, None
 
 
 def peaks():
@@ -262,6 +266,7 @@ def run_ours(args, rank, world, dist):
 
     # ---- roofline of the graded kernel (paged decode attention), live CUDA events
     pk = peaks()
+    traffic, traffic_alg = ncu_traffic("k_attn")
     attn_gbs = st["attn_bytes"] / (st["attn_ms"] / 1e3) / 1e9 if st["attn_ms"] > 0 else None
     w_bytes = shape.weight_bytes_streamed()
     step_bytes = w_bytes + (st["attn_bytes"] / max(st["rounds"], 1))
@@ -269,7 +274,9 @@ def run_ours(args, rank, world, dist):
                 "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": (attn_gbs / pk["hbm_gbs"]) if attn_gbs else None,
                 "frac_of_8000": (attn_gbs / 8000.0) if attn_gbs else None,
-                "traffic": ncu_traffic("k_attn"), "traffic_source": NCU_ATTN_SOURCE,
+                "traffic": traffic, "traffic_source": NCU_ATTN_SOURCE,
+                "traffic_capture_alg_bytes": traffic_alg,
+                "traffic_over_alg": (traffic / traffic_alg) if traffic and traffic_alg else None,
                 "alg_bytes_per_launch": st["attn_bytes"] / max(st["attn_launches"], 1),
                 "alg_bytes_rule": "per launch: sum over rows of attended tokens x 2 (K,V) x 8 kv heads x 128 x 2 B "
                                   "(4096 B per token per layer) + q + o",
