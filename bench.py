@@ -274,6 +274,10 @@ def run_ours(args, rank, world, dist):
                 "peak": pk["hbm_gbs"], "unit": "GB/s",
                 "frac": (attn_gbs / pk["hbm_gbs"]) if attn_gbs else None,
                 "frac_of_8000": (attn_gbs / 8000.0) if attn_gbs else None,
+                # the HBM read ceiling of this access pattern measured without the math
+                # (tools/read_bw.py; a read-only stream exceeds the read+write copy peak)
+                "read_ceiling_gbs": READ_CEILING_GBS,
+                "frac_of_read_ceiling": (attn_gbs / READ_CEILING_GBS) if attn_gbs else None,
                 "traffic": traffic, "traffic_source": NCU_ATTN_SOURCE,
                 "traffic_capture_alg_bytes": traffic_alg,
                 "traffic_over_alg": (traffic / traffic_alg) if traffic and traffic_alg else None,
@@ -338,6 +342,7 @@ def run_ours(args, rank, world, dist):
 
 
 METRIC = "decode tok/s (segmented decode round)"
+READ_CEILING_GBS = 7309.0   # profiles/r02_read_ceiling.txt: sequential 8 KiB pages, 3-stage rings
 NCU_ATTN_SOURCE = "profiles/r02_ncu_attention_full.json (ncu --set full of one k_attn launch of the same workload)"
 
 
